@@ -1,0 +1,239 @@
+/*
+ * geoshoot_b200.h -- C ABI of the B200-native geodesic-shooting hot path.
+ *
+ * This is the drop-in boundary. Every entry point takes plain
+ * host pointers in the reference layout -- `const double* xyz` of 3*n doubles,
+ * i.e. reinterpret_cast<const double*>(std::vector<Vec3>::data()), Vec3 being
+ * three doubles (reference core.hpp:16-20) -- plus sizes, and returns a
+ * gs_status. No C++ types, no torch types, no exceptions cross it. The C++
+ * reference API (paper_1907_04834_b200/include/geoshoot/*.hpp) is a thin shim
+ * over these calls that maps gs_status back to the reference's exception
+ * types; INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Each function names the reference interface it replaces
+ * (file:line under the reference's proj/).
+ *
+ * Calls are synchronous at the boundary: results are in host memory when the
+ * call returns. One gs_ctx per host thread (a context owns a CUDA stream and
+ * its workspaces). The device work is done by hand-written sm_100a kernels;
+ * there is no CPU fallback: without a usable B200 gs_create fails with
+ * GS_NO_DEVICE.
+ */
+#ifndef GEOSHOOT_B200_H
+#define GEOSHOOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+/* Mirrors the reference's exception types (core.hpp:69-116). */
+typedef enum gs_status {
+  GS_OK = 0,
+  GS_DIMENSION_MISMATCH = 1, /* DimensionMismatch, core.hpp:69 / require_aligned :172-178 */
+  GS_CONFIG_ERROR = 2,       /* ConfigError{violations}, core.hpp:233-247 (mask: gs_last_config_violations) */
+  GS_NONFINITE = 3,          /* NonFiniteState{timestep}, core.hpp:83-89 (step: gs_last_nonfinite_step) */
+  GS_CONFIG_MISMATCH = 4,    /* ConfigMismatch, core.hpp:91 */
+  GS_EMPTY_TREE = 5,         /* EmptyTree, core.hpp:77 */
+  GS_OUT_OF_BOUNDS = 6,      /* OutOfBounds, core.hpp:73 */
+  GS_INVALID_ARGUMENT = 7,   /* std::invalid_argument (empty / non-finite PointSet, core.hpp:124-170) */
+  GS_CUDA_ERROR = 8,
+  GS_NO_DEVICE = 9,
+  GS_INTERNAL = 99
+} gs_status;
+
+/* ConfigViolation bits (core.hpp:215-220), in declaration order. */
+enum {
+  GS_VIOLATION_NON_POSITIVE_SIGMA = 1u << 0,
+  GS_VIOLATION_NON_POSITIVE_LAMBDA = 1u << 1,
+  GS_VIOLATION_ZERO_TIMESTEPS = 1u << 2,
+  GS_VIOLATION_NON_POSITIVE_THRESHOLD = 1u << 3
+};
+
+typedef enum gs_precision { GS_F64 = 0, GS_F32 = 1 } gs_precision;
+typedef enum gs_backend { GS_EXACT = 0, GS_BARNES_HUT = 1 } gs_backend;
+/* The reference integrates with explicit Euler only (shooting.hpp:16-18).
+ * GS_RK4 is the classical four-stage scheme over the same RHS (BASELINE
+ * config 4), the Barnes-Hut tree rebuilt at every stage. */
+typedef enum gs_integrator { GS_EULER = 0, GS_RK4 = 1 } gs_integrator;
+
+/* ShootingConfig (core.hpp:204-213) plus the B200 knobs. */
+typedef struct gs_config {
+  double sigma;                /* kernel width */
+  double lambda;               /* data-attachment weight */
+  int32_t timesteps;           /* uniform steps over [0, 1] */
+  int32_t backend;             /* gs_backend */
+  double threshold_multiplier; /* BH opening threshold = multiplier * sigma (3 by default) */
+  int32_t integrator;          /* gs_integrator */
+  int32_t precision;           /* gs_precision of the device arithmetic */
+} gs_config;
+
+/* Reference defaults (core.hpp:204-213): sigma 2, lambda 1, 40 steps, exact,
+ * 3 sigma; Euler; F64. */
+gs_config gs_default_config(void);
+
+/* TraversalStats (bh_kernel.hpp:28-38) + EvalStats (shooting.hpp:41-55). */
+typedef struct gs_stats {
+  uint64_t direct_interactions;
+  uint64_t approximated_interactions;
+  uint64_t nodes_visited;
+  uint64_t traversal_queries;
+  double tree_build_ms;
+  double forward_ms;
+  double backward_ms;
+} gs_stats;
+
+/* ObjectiveReport (shooting.hpp:33-38). */
+typedef struct gs_report {
+  double energy;
+  double attachment;
+  double total;
+  double residual_sse;
+} gs_report;
+
+typedef struct gs_ctx gs_ctx;
+
+/* ---- context --------------------------------------------------------------- */
+gs_ctx* gs_create(int device, gs_status* status);
+void gs_destroy(gs_ctx* ctx);
+const char* gs_last_error(const gs_ctx* ctx);
+int gs_last_nonfinite_step(const gs_ctx* ctx);
+uint32_t gs_last_config_violations(const gs_ctx* ctx);
+int gs_abi_version(void);
+/* validate_config, core.cpp:5-17: every violated bound in *mask. */
+gs_status gs_validate_config(const gs_config* cfg, uint32_t* mask);
+
+/* ---- kernel_exact (kernel_exact.hpp:37-80) ---------------------------------- */
+/* hamiltonian, kernel_exact.cpp:13-27. */
+gs_status gs_hamiltonian(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
+                         const double* p, double sigma, double* h_out);
+/* hamiltonian_with_gradients, kernel_exact.cpp:29-61 (h_out may be NULL). */
+gs_status gs_exact_rhs(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
+                       const double* p, double sigma, double* dH_dp, double* dH_dq,
+                       double* h_out);
+/* exact_velocity, kernel_exact.cpp:70-82. */
+gs_status gs_exact_velocity(gs_ctx* ctx, int32_t precision, int64_t m, const double* x,
+                            int64_t n, const double* q, const double* p, double sigma,
+                            double* v_out);
+/* hessian_products, kernel_exact.cpp:84-135. */
+gs_status gs_hessian_products(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
+                              const double* p, const double* alpha, const double* beta,
+                              double sigma, double* pq_alpha, double* pp_alpha,
+                              double* qq_beta, double* qp_beta);
+
+/* ---- octree (octree.hpp:17-87) ---------------------------------------------- */
+/* A device-resident octree with the reference's node semantics (octree.cpp:
+ * 25-117: anisotropic padded root box, midpoint subdivision, single-point
+ * leaves, depth-32 buckets), built from midpoint-replay Morton keys. Nodes are
+ * stored in depth-first pre-order (children 0..7); points in leaf order. */
+typedef struct gs_tree gs_tree;
+
+/* Octree::build, octree.cpp:25-40. */
+gs_status gs_tree_build(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
+                        const double* p, gs_tree** out);
+void gs_tree_free(gs_tree* tree);
+int64_t gs_tree_node_count(const gs_tree* tree);
+int64_t gs_tree_point_count(const gs_tree* tree);
+/* Octree::accumulate_adjoints, octree.cpp:119-139. */
+gs_status gs_tree_accumulate_adjoints(gs_tree* tree, const double* alpha, const double* beta);
+/* Host copy of the tree for inspection (any pointer may be NULL):
+ *   order[n]          point index at each leaf-order position (DFS, children 0..7)
+ *   key_hi/key_lo[n]  midpoint-replay Morton keys per point index (levels 1..21 / 22..32)
+ *   level[m]          node depth (root 0)
+ *   parent[m]         pre-order index of the parent (-1 for the root)
+ *   skip[m]           pre-order index just past the node's subtree
+ *   range[2m]         [first, last] leaf-order positions of the node's points
+ *   boxes[12m]        cell_min, cell_max, actual_min, actual_max (octree.hpp:23-24)
+ *   sums[12m]         position_sum, momentum_sum, alpha_sum, beta_sum (:25-28)
+ *   count[m]          point count (:29)                                       */
+gs_status gs_tree_download(const gs_tree* tree, int32_t* order, uint64_t* key_hi,
+                           uint64_t* key_lo, int32_t* level, int32_t* parent,
+                           int32_t* skip, int32_t* range, double* boxes, double* sums,
+                           uint32_t* count);
+
+/* ---- bh_kernel (bh_kernel.hpp:48-99) ----------------------------------------- */
+/* bh_velocity, bh_kernel.cpp:62-79, for m eval points. stats may be NULL. */
+gs_status gs_bh_velocity(gs_tree* tree, int64_t m, const double* x, double sigma,
+                         double threshold, double* v_out, gs_stats* stats);
+/* bh_hamiltonian_gradients, bh_kernel.cpp:193-210 (queries = the tree's own points). */
+gs_status gs_bh_rhs(gs_tree* tree, double sigma, double threshold, double* dH_dp,
+                    double* dH_dq, gs_stats* stats);
+/* Per-query (direct, approximated, visited) counts of the last gs_bh_rhs /
+ * gs_bh_velocity call on this tree (3*m uint64, query order). */
+gs_status gs_bh_query_stats(const gs_tree* tree, uint64_t* per_query);
+/* bh_hamiltonian, bh_kernel.cpp:162-191. */
+gs_status gs_bh_hamiltonian(gs_tree* tree, double sigma, double threshold, double* h_out,
+                            gs_stats* stats);
+/* bh_hessian_products, bh_kernel.cpp:212-236; the tree must carry the same
+ * alpha/beta via gs_tree_accumulate_adjoints. */
+gs_status gs_bh_hessian_products(gs_tree* tree, const double* alpha, const double* beta,
+                                 double sigma, double threshold, double* pq_alpha,
+                                 double* pp_alpha, double* qq_beta, double* qp_beta,
+                                 gs_stats* stats);
+
+/* ---- shooting (shooting.hpp:57-86) ------------------------------------------- */
+/* shoot_forward, shooting.cpp:244-249. traj_q/traj_p: (T+1) x n x 3, or NULL
+ * to return only the final state in final_q/final_p (either may be NULL).
+ * energy_out: H(q0, p0) = 1/2 <p0, dH/dp> (shooting.cpp:104-108), may be NULL. */
+gs_status gs_shoot_forward(gs_ctx* ctx, const gs_config* cfg, int64_t n, const double* q0,
+                           const double* p0, double* traj_q, double* traj_p,
+                           double* final_q, double* final_p, double* energy_out,
+                           gs_stats* stats);
+/* objective, shooting.cpp:251-257. */
+gs_status gs_objective(gs_ctx* ctx, const gs_config* cfg, int64_t n, const double* q0,
+                       const double* p0, const double* target, gs_report* report);
+/* backward_gradient, shooting.cpp:259-264; `states` snapshots (must be T+1). */
+gs_status gs_backward_gradient(gs_ctx* ctx, const gs_config* cfg, int64_t n, int32_t states,
+                               const double* traj_q, const double* traj_p,
+                               const double* target, double* grad_out);
+/* warp_points, shooting.cpp:266-300. */
+gs_status gs_warp_points(gs_ctx* ctx, const gs_config* cfg, int64_t n, int32_t states,
+                         const double* traj_q, const double* traj_p, int64_t m,
+                         const double* x, double* y_out);
+/* evaluate, shooting.cpp:302-314: fused forward (trees kept on device) +
+ * report + adjoint backward. */
+gs_status gs_evaluate(gs_ctx* ctx, const gs_config* cfg, int64_t n, const double* q0,
+                      const double* p0, const double* target, gs_report* report,
+                      double* grad_out, gs_stats* stats);
+
+/* ---- device-resident flow (bench / batched callers) --------------------------
+ * A flow keeps (q, p) resident in HBM between calls so a caller can advance it
+ * without host round trips; gs_shoot_forward is upload + gs_flow_advance +
+ * download. Target sharding for multi-GPU: a flow owns targets
+ * [shard_begin, shard_begin + shard_count) of n and exposes its packed source
+ * buffer (all n points) so the caller can all-gather shards after every
+ * integrator stage (see paper_1907_04834_b200/shard.py). */
+typedef struct gs_flow gs_flow;
+gs_status gs_flow_create(gs_ctx* ctx, const gs_config* cfg, int64_t n, gs_flow** out);
+void gs_flow_destroy(gs_flow* flow);
+gs_status gs_flow_upload(gs_flow* flow, const double* q0, const double* p0);
+/* Advance `steps` integrator steps (each Euler step = 1 RHS, RK4 = 4) with no
+ * host synchronisation; errors surface at gs_flow_sync. */
+gs_status gs_flow_advance(gs_flow* flow, int32_t steps);
+gs_status gs_flow_sync(gs_flow* flow);
+gs_status gs_flow_download(gs_flow* flow, double* q, double* p);
+/* Number of kernels the last gs_flow_advance launched (bench evidence). */
+int64_t gs_flow_last_launches(const gs_flow* flow);
+/* cudaStream_t of the flow (as void*), for event timing on the launch stream. */
+void* gs_flow_stream(const gs_flow* flow);
+
+/* Sharded stage API (one rank = one flow): */
+gs_status gs_flow_set_shard(gs_flow* flow, int64_t shard_begin, int64_t shard_count);
+/* Device pointer and byte size of the packed per-point source records
+ * (n records, record bytes = gs_flow_record_bytes); the shard's records are
+ * contiguous at shard_begin. */
+void* gs_flow_source_buffer(gs_flow* flow);
+int64_t gs_flow_record_bytes(const gs_flow* flow);
+/* One integrator stage on the shard (RHS over all n sources + fused stage
+ * epilogue that rewrites the shard's records); stage = 0..stages-1 of the
+ * current step (Euler 1, RK4 4). */
+gs_status gs_flow_stage(gs_flow* flow, int32_t stage);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEOSHOOT_B200_H */

@@ -1,0 +1,576 @@
+// allpairs.cu -- exact O(N^2) kernel sums on sm_100a (FP32 + FP64).
+//
+// Replaces kernel_exact.cpp:29-61 (hamiltonian_with_gradients), :70-82
+// (exact_velocity) and :84-135 (hessian_products). The reference sweeps the
+// upper triangle and scatters every pair to both ends; on the GPU each thread
+// OWNS `TPT` targets and gathers over all sources (self included: its terms
+// are exactly the reference's explicit diagonal, kernel_exact.cpp:41-44 and
+// :94-97), so no atomics and a fixed, launch-independent summation order per
+// target -> bitwise-deterministic results (test_shooting.cpp:305-318).
+//
+// Work decomposition: grid.x = target blocks of NT*TPT targets, grid.y = S
+// source chunks; each CTA streams its chunk through shared memory in tiles of
+// TILE records (coalesced 16-B loads, broadcast LDS.128 reads) and writes one
+// partial per (chunk, target). The stage epilogue (epilogue.cu) folds the S
+// partials in fixed order, applies the constants and the integrator update.
+// S is picked so that the grid fills an integral number of waves of resident
+// CTAs (148 SMs x occupancy).
+//
+// FP32 inner loop per (target, source) pair, pre-scaled coordinates
+// (gs_common.cuh): 3 FADD (d) + FMUL+2 FFMA (-r^2) + MUFU.EX2 (g) + FMUL+2 FFMA
+// (p_i.p_j) + FMUL (c) + 3 FFMA (sum g p_j) + 3 FFMA (sum c d) = 16 FP32 + 1 SFU.
+// No tensor cores: the contraction dimension is 3.
+#include "engine.h"
+
+namespace gsb {
+
+constexpr int kTile = 256;
+
+// ----------------------------------------------------------------------------
+// forward RHS partials: A = sum_j g p_j, B = sum_j (p_i.p_j) g d'_ij
+// ----------------------------------------------------------------------------
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_rhs_f32(const float4* __restrict__ rec, int n,
+                                                int tgt_begin, int n_tgt, int chunk,
+                                                float kap, float kc0x, float kc0y, float kc0z,
+                                                float4* __restrict__ part) {
+  __shared__ float4 sq[kTile];
+  __shared__ float4 sp[kTile];
+  float qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
+  float ax[TPT], ay[TPT], az[TPT], bx[TPT], by[TPT], bz[TPT];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+    if (t < n_tgt) {
+      q = rec[2 * (tgt_begin + t)];
+      p = rec[2 * (tgt_begin + t) + 1];
+    }
+    qx[k] = fmaf(kap, q.x, -kc0x); qy[k] = fmaf(kap, q.y, -kc0y); qz[k] = fmaf(kap, q.z, -kc0z);
+    px[k] = p.x; py[k] = p.y; pz[k] = p.z;
+    ax[k] = ay[k] = az[k] = bx[k] = by[k] = bz[k] = 0.f;
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < j1) {
+        q = rec[2 * j];
+        p = rec[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q;  // zero records contribute exactly 0 (p = 0)
+      sp[u] = p;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u];
+      const float4 b = sp[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const float dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
+        float nr2 = -dx * dx;
+        nr2 = fmaf(-dy, dy, nr2);
+        nr2 = fmaf(-dz, dz, nr2);
+        const float g = ex2(nr2);
+        float pp = px[k] * b.x;
+        pp = fmaf(py[k], b.y, pp);
+        pp = fmaf(pz[k], b.z, pp);
+        const float c = pp * g;
+        ax[k] = fmaf(g, b.x, ax[k]);
+        ay[k] = fmaf(g, b.y, ay[k]);
+        az[k] = fmaf(g, b.z, az[k]);
+        bx[k] = fmaf(c, dx, bx[k]);
+        by[k] = fmaf(c, dy, by[k]);
+        bz[k] = fmaf(c, dz, bz[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < n_tgt) {
+      float4* o = part + 2 * ((size_t)blockIdx.y * n_tgt + t);
+      o[0] = make_float4(ax[k], ay[k], az[k], 0.f);
+      o[1] = make_float4(bx[k], by[k], bz[k], 0.f);
+    }
+  }
+}
+
+// FP64: the reference's own expression exp(-|d|^2 * inv_two_s) in unscaled
+// coordinates; libdevice exp (no SFU path exists for FP64).
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_rhs_f64(const double4* __restrict__ rec, int n,
+                                                int tgt_begin, int n_tgt, int chunk,
+                                                double inv_two_s, double4* __restrict__ part) {
+  __shared__ double4 sq[kTile / 2];
+  __shared__ double4 sp[kTile / 2];
+  constexpr int tile = kTile / 2;
+  double qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
+  double ax[TPT], ay[TPT], az[TPT], bx[TPT], by[TPT], bz[TPT];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    double4 q = make_double4(0, 0, 0, 0), p = q;
+    if (t < n_tgt) {
+      q = ld4(rec + 2 * (tgt_begin + t));
+      p = ld4(rec + 2 * (tgt_begin + t) + 1);
+    }
+    qx[k] = q.x; qy[k] = q.y; qz[k] = q.z;
+    px[k] = p.x; py[k] = p.y; pz[k] = p.z;
+    ax[k] = ay[k] = az[k] = bx[k] = by[k] = bz[k] = 0.0;
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += tile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < tile; u += NT) {
+      const int j = jt + u;
+      double4 q = make_double4(0, 0, 0, 0), p = q;
+      if (j < j1) {
+        q = ld4(rec + 2 * j);
+        p = ld4(rec + 2 * j + 1);
+      }
+      sq[u] = q;  // zero records (p = 0) contribute exactly 0
+      sp[u] = p;
+    }
+    __syncthreads();
+    for (int u = 0; u < tile; ++u) {
+      const double4 a = sq[u];
+      const double4 b = sp[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const double dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
+        const double r2 = dx * dx + dy * dy + dz * dz;
+        const double g = exp(-r2 * inv_two_s);
+        const double pp = px[k] * b.x + py[k] * b.y + pz[k] * b.z;
+        const double c = pp * g;
+        ax[k] += g * b.x; ay[k] += g * b.y; az[k] += g * b.z;
+        bx[k] += c * dx; by[k] += c * dy; bz[k] += c * dz;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < n_tgt) {
+      double4* o = part + 2 * ((size_t)blockIdx.y * n_tgt + t);
+      st4(o, make_double4(ax[k], ay[k], az[k], 0.0));
+      st4(o + 1, make_double4(bx[k], by[k], bz[k], 0.0));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Hessian-vector products (kernel_exact.hpp:53-69), gather form over all j:
+//   Apq = sum g (p_j.a_i + p_i.a_j) d'     Aqq = sum g (p_i.p_j) ((d'.db) C1 d' - db)
+//   App = sum g a_j                         Aqp = sum g (d'.db) p_j
+// with db = b_i - b_j; constants applied by the backward epilogue.
+// Sources: state records (q, p) of step k + adjoint records (alpha, beta).
+// 40 FP32 + 1 SFU per pair.
+// ----------------------------------------------------------------------------
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_hess_f32(const float4* __restrict__ rec,
+                                                 const float4* __restrict__ adj, int n,
+                                                 int tgt_begin, int n_tgt, int chunk, float kap,
+                                                 float kc0x, float kc0y, float kc0z, float c1,
+                                                 float4* __restrict__ part) {
+  __shared__ float4 sq[kTile / 2], sp[kTile / 2], sa[kTile / 2], sb[kTile / 2];
+  constexpr int tile = kTile / 2;
+  float qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
+  float ix[TPT], iy[TPT], iz[TPT], jx[TPT], jy[TPT], jz[TPT];  // alpha_i, beta_i
+  float4 A0[TPT], A1[TPT], A2[TPT], A3[TPT];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q, a = q, b = q;
+    if (t < n_tgt) {
+      const int i = tgt_begin + t;
+      q = rec[2 * i]; p = rec[2 * i + 1]; a = adj[2 * i]; b = adj[2 * i + 1];
+    }
+    qx[k] = fmaf(kap, q.x, -kc0x); qy[k] = fmaf(kap, q.y, -kc0y); qz[k] = fmaf(kap, q.z, -kc0z);
+    px[k] = p.x; py[k] = p.y; pz[k] = p.z;
+    ix[k] = a.x; iy[k] = a.y; iz[k] = a.z;
+    jx[k] = b.x; jy[k] = b.y; jz[k] = b.z;
+    A0[k] = A1[k] = A2[k] = A3[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += tile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < tile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q, a = q, b = q;
+      if (j < j1) {
+        q = rec[2 * j]; p = rec[2 * j + 1]; a = adj[2 * j]; b = adj[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q; sp[u] = p; sa[u] = a; sb[u] = b;  // zero records contribute exactly 0
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < tile; ++u) {
+      const float4 Q = sq[u], P = sp[u], Al = sa[u], Be = sb[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const float dx = qx[k] - Q.x, dy = qy[k] - Q.y, dz = qz[k] - Q.z;
+        float nr2 = -dx * dx;
+        nr2 = fmaf(-dy, dy, nr2);
+        nr2 = fmaf(-dz, dz, nr2);
+        const float g = ex2(nr2);
+        const float dbx = jx[k] - Be.x, dby = jy[k] - Be.y, dbz = jz[k] - Be.z;
+        float ddb = dx * dbx;
+        ddb = fmaf(dy, dby, ddb);
+        ddb = fmaf(dz, dbz, ddb);
+        float s1 = P.x * ix[k];
+        s1 = fmaf(P.y, iy[k], s1);
+        s1 = fmaf(P.z, iz[k], s1);
+        s1 = fmaf(px[k], Al.x, s1);
+        s1 = fmaf(py[k], Al.y, s1);
+        s1 = fmaf(pz[k], Al.z, s1);
+        float pp = px[k] * P.x;
+        pp = fmaf(py[k], P.y, pp);
+        pp = fmaf(pz[k], P.z, pp);
+        const float t1 = g * s1;
+        A0[k].x = fmaf(t1, dx, A0[k].x); A0[k].y = fmaf(t1, dy, A0[k].y); A0[k].z = fmaf(t1, dz, A0[k].z);
+        A1[k].x = fmaf(g, Al.x, A1[k].x); A1[k].y = fmaf(g, Al.y, A1[k].y); A1[k].z = fmaf(g, Al.z, A1[k].z);
+        const float w = g * pp;
+        const float uu = ddb * c1;
+        const float zx = fmaf(uu, dx, -dbx), zy = fmaf(uu, dy, -dby), zz = fmaf(uu, dz, -dbz);
+        A2[k].x = fmaf(w, zx, A2[k].x); A2[k].y = fmaf(w, zy, A2[k].y); A2[k].z = fmaf(w, zz, A2[k].z);
+        const float m = g * ddb;
+        A3[k].x = fmaf(m, P.x, A3[k].x); A3[k].y = fmaf(m, P.y, A3[k].y); A3[k].z = fmaf(m, P.z, A3[k].z);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < n_tgt) {
+      float4* o = part + 4 * ((size_t)blockIdx.y * n_tgt + t);
+      o[0] = A0[k]; o[1] = A1[k]; o[2] = A2[k]; o[3] = A3[k];
+    }
+  }
+}
+
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_hess_f64(const double4* __restrict__ rec,
+                                                 const double4* __restrict__ adj, int n,
+                                                 int tgt_begin, int n_tgt, int chunk,
+                                                 double inv_two_s, double inv_s,
+                                                 double4* __restrict__ part) {
+  constexpr int tile = kTile / 4;
+  __shared__ double4 sq[tile], sp[tile], sa[tile], sb[tile];
+  double qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
+  double ix[TPT], iy[TPT], iz[TPT], jx[TPT], jy[TPT], jz[TPT];
+  double A[TPT][12];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    double4 q = make_double4(0, 0, 0, 0), p = q, a = q, b = q;
+    if (t < n_tgt) {
+      const int i = tgt_begin + t;
+      q = ld4(rec + 2 * i); p = ld4(rec + 2 * i + 1); a = ld4(adj + 2 * i); b = ld4(adj + 2 * i + 1);
+    }
+    qx[k] = q.x; qy[k] = q.y; qz[k] = q.z; px[k] = p.x; py[k] = p.y; pz[k] = p.z;
+    ix[k] = a.x; iy[k] = a.y; iz[k] = a.z; jx[k] = b.x; jy[k] = b.y; jz[k] = b.z;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) A[k][c] = 0.0;
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += tile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < tile; u += NT) {
+      const int j = jt + u;
+      double4 q = make_double4(0, 0, 0, 0), p = q, a = q, b = q;
+      if (j < j1) {
+        q = ld4(rec + 2 * j); p = ld4(rec + 2 * j + 1); a = ld4(adj + 2 * j); b = ld4(adj + 2 * j + 1);
+      }
+      sq[u] = q; sp[u] = p; sa[u] = a; sb[u] = b;
+    }
+    __syncthreads();
+    for (int u = 0; u < tile; ++u) {
+      const double4 Q = sq[u], P = sp[u], Al = sa[u], Be = sb[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const double dx = qx[k] - Q.x, dy = qy[k] - Q.y, dz = qz[k] - Q.z;
+        const double g = exp(-(dx * dx + dy * dy + dz * dz) * inv_two_s);
+        const double dbx = jx[k] - Be.x, dby = jy[k] - Be.y, dbz = jz[k] - Be.z;
+        const double ddb = dx * dbx + dy * dby + dz * dbz;
+        const double s1 = (P.x * ix[k] + P.y * iy[k] + P.z * iz[k]) +
+                          (px[k] * Al.x + py[k] * Al.y + pz[k] * Al.z);
+        const double pp = px[k] * P.x + py[k] * P.y + pz[k] * P.z;
+        const double t1 = g * s1;
+        A[k][0] += t1 * dx; A[k][1] += t1 * dy; A[k][2] += t1 * dz;
+        A[k][3] += g * Al.x; A[k][4] += g * Al.y; A[k][5] += g * Al.z;
+        const double w = g * pp, uu = ddb * inv_s;
+        A[k][6] += w * (uu * dx - dbx); A[k][7] += w * (uu * dy - dby); A[k][8] += w * (uu * dz - dbz);
+        const double m = g * ddb;
+        A[k][9] += m * P.x; A[k][10] += m * P.y; A[k][11] += m * P.z;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < n_tgt) {
+      double4* o = part + 4 * ((size_t)blockIdx.y * n_tgt + t);
+      st4(o + 0, make_double4(A[k][0], A[k][1], A[k][2], 0.0));
+      st4(o + 1, make_double4(A[k][3], A[k][4], A[k][5], 0.0));
+      st4(o + 2, make_double4(A[k][6], A[k][7], A[k][8], 0.0));
+      st4(o + 3, make_double4(A[k][9], A[k][10], A[k][11], 0.0));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Velocity field v(x) = sum_j G(|x - q_j|) p_j at separate eval points
+// (exact_velocity, kernel_exact.cpp:70-82; warp, shooting.cpp:288-294).
+// 9 FP32 + 1 SFU per pair. Eval points: records of (x, unused).
+// ----------------------------------------------------------------------------
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_vel_f32(const float4* __restrict__ rec, int n,
+                                                const float4* __restrict__ ev, int m, int chunk,
+                                                float kap, float kc0x, float kc0y, float kc0z,
+                                                float4* __restrict__ part) {
+  __shared__ float4 sq[kTile], sp[kTile];
+  float qx[TPT], qy[TPT], qz[TPT], ax[TPT], ay[TPT], az[TPT];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < m) x = ev[2 * t];
+    qx[k] = fmaf(kap, x.x, -kc0x); qy[k] = fmaf(kap, x.y, -kc0y); qz[k] = fmaf(kap, x.z, -kc0z);
+    ax[k] = ay[k] = az[k] = 0.f;
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < j1) {
+        q = rec[2 * j]; p = rec[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q; sp[u] = p;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u], b = sp[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const float dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
+        float nr2 = -dx * dx;
+        nr2 = fmaf(-dy, dy, nr2);
+        nr2 = fmaf(-dz, dz, nr2);
+        const float g = ex2(nr2);
+        ax[k] = fmaf(g, b.x, ax[k]); ay[k] = fmaf(g, b.y, ay[k]); az[k] = fmaf(g, b.z, az[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < m) part[(size_t)blockIdx.y * m + t] = make_float4(ax[k], ay[k], az[k], 0.f);
+  }
+}
+
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_vel_f64(const double4* __restrict__ rec, int n,
+                                                const double4* __restrict__ ev, int m, int chunk,
+                                                double inv_two_s, double4* __restrict__ part) {
+  constexpr int tile = kTile / 2;
+  __shared__ double4 sq[tile], sp[tile];
+  double qx[TPT], qy[TPT], qz[TPT], ax[TPT], ay[TPT], az[TPT];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    double4 x = make_double4(0, 0, 0, 0);
+    if (t < m) x = ld4(ev + 2 * t);
+    qx[k] = x.x; qy[k] = x.y; qz[k] = x.z;
+    ax[k] = ay[k] = az[k] = 0.0;
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += tile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < tile; u += NT) {
+      const int j = jt + u;
+      double4 q = make_double4(0, 0, 0, 0), p = q;
+      if (j < j1) { q = ld4(rec + 2 * j); p = ld4(rec + 2 * j + 1); }
+      sq[u] = q; sp[u] = p;
+    }
+    __syncthreads();
+    for (int u = 0; u < tile; ++u) {
+      const double4 a = sq[u], b = sp[u];
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        const double dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
+        const double g = exp(-(dx * dx + dy * dy + dz * dz) * inv_two_s);
+        ax[k] += g * b.x; ay[k] += g * b.y; az[k] += g * b.z;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TPT; ++k) {
+    const int t = tb + k * NT;
+    if (t < m) st4(part + (size_t)blockIdx.y * m + t, make_double4(ax[k], ay[k], az[k], 0.0));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// launch planning
+// ----------------------------------------------------------------------------
+namespace {
+
+struct Plan {
+  int tpt, S, chunk;
+  dim3 grid;
+};
+
+// Choose targets-per-thread and the number of source chunks S so that the
+// grid covers an integral number of waves of resident CTAs.
+Plan plan(int n_src, int n_tgt, int nt, const int* tpts, int ntpt, int tile, int occ,
+          int sms) {
+  const long slots = (long)occ * sms;
+  Plan pl{};
+  int tpt = tpts[ntpt - 1];
+  for (int i = 0; i < ntpt; ++i) {
+    const long b = (n_tgt + (long)nt * tpts[i] - 1) / ((long)nt * tpts[i]);
+    if (b * 16 >= 2 * slots) { tpt = tpts[i]; break; }
+  }
+  const long B = (n_tgt + (long)nt * tpt - 1) / ((long)nt * tpt);
+  const int smax = (int)std::max(1L, std::min((long)kMaxChunks, ((long)n_src + tile - 1) / tile));
+  int bestS = 1;
+  double best = -1.0;
+  for (int s = 1; s <= smax; ++s) {
+    const double w = (double)(B * s) / slots;
+    const double eff = w / std::ceil(w);
+    // prefer fewer chunks unless clearly better balanced
+    if (eff > best + 0.01) { best = eff; bestS = s; }
+    if (w > 8.0 && eff > 0.97) break;
+  }
+  pl.tpt = tpt;
+  pl.S = bestS;
+  pl.chunk = (int)(((long)n_src + bestS - 1) / bestS);
+  pl.chunk = (pl.chunk + tile - 1) / tile * tile;
+  pl.S = (int)(((long)n_src + pl.chunk - 1) / pl.chunk);
+  if (pl.S < 1) pl.S = 1;
+  pl.grid = dim3((unsigned)B, (unsigned)pl.S, 1);
+  return pl;
+}
+
+template <typename K>
+int occupancy(K kernel, int nt) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, 0);
+  return occ > 0 ? occ : 1;
+}
+
+}  // namespace
+
+constexpr int kNT = 128;
+
+// Dispatch helpers: one instantiation per TPT.
+#define GS_TPT_SWITCH(tpt, KERNEL, ...)                                   \
+  switch (tpt) {                                                          \
+    case 8: KERNEL<8, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break;  \
+    case 4: KERNEL<4, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break;  \
+    case 2: KERNEL<2, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break;  \
+    default: KERNEL<1, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break; \
+  }
+
+int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
+  if (prec == kF32) {
+    static const int tpts[] = {8, 4, 2, 1};
+    static int occ = occupancy(k_rhs_f32<8, kNT>, kNT);
+    Plan pl = plan(n, n_tgt, kNT, tpts, 4, kTile, occ, dev.sms);
+    if (pl.S > part_cap_chunks) return -1;
+    const float kap = (float)kc.kappa;
+    GS_TPT_SWITCH(pl.tpt, k_rhs_f32, (const float4*)rec, n, tgt_begin, n_tgt, pl.chunk, kap,
+                  (float)(kc.kappa * kc.c0[0]), (float)(kc.kappa * kc.c0[1]),
+                  (float)(kc.kappa * kc.c0[2]), (float4*)part);
+    return pl.S;
+  }
+  static const int tpts[] = {4, 2, 1};
+  static int occ = occupancy(k_rhs_f64<4, kNT>, kNT);
+  Plan pl = plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms);
+  if (pl.S > part_cap_chunks) return -1;
+  switch (pl.tpt) {
+    case 4: k_rhs_f64<4, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
+    case 2: k_rhs_f64<2, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
+    default: k_rhs_f64<1, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
+  }
+  return pl.S;
+}
+
+int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
+                  int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
+                  int part_cap_chunks, cudaStream_t st) {
+  if (prec == kF32) {
+    static const int tpts[] = {4, 2, 1};
+    static int occ = occupancy(k_hess_f32<4, kNT>, kNT);
+    Plan pl = plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms);
+    if (pl.S > part_cap_chunks) return -1;
+    const float kap = (float)kc.kappa;
+    const float c1 = (float)(1.0 / (kc.kappa * kc.kappa * kc.s));
+    const float a = (float)(kc.kappa * kc.c0[0]), b = (float)(kc.kappa * kc.c0[1]),
+                c = (float)(kc.kappa * kc.c0[2]);
+    switch (pl.tpt) {
+      case 4: k_hess_f32<4, kNT><<<pl.grid, kNT, 0, st>>>((const float4*)rec, (const float4*)adj, n, tgt_begin, n_tgt, pl.chunk, kap, a, b, c, c1, (float4*)part); break;
+      case 2: k_hess_f32<2, kNT><<<pl.grid, kNT, 0, st>>>((const float4*)rec, (const float4*)adj, n, tgt_begin, n_tgt, pl.chunk, kap, a, b, c, c1, (float4*)part); break;
+      default: k_hess_f32<1, kNT><<<pl.grid, kNT, 0, st>>>((const float4*)rec, (const float4*)adj, n, tgt_begin, n_tgt, pl.chunk, kap, a, b, c, c1, (float4*)part); break;
+    }
+    return pl.S;
+  }
+  static const int tpts[] = {2, 1};
+  static int occ = occupancy(k_hess_f64<2, kNT>, kNT);
+  Plan pl = plan(n, n_tgt, kNT, tpts, 2, kTile / 4, occ, dev.sms);
+  if (pl.S > part_cap_chunks) return -1;
+  switch (pl.tpt) {
+    case 2: k_hess_f64<2, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, (const double4*)adj, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, kc.inv_s, (double4*)part); break;
+    default: k_hess_f64<1, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, (const double4*)adj, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, kc.inv_s, (double4*)part); break;
+  }
+  return pl.S;
+}
+
+int vel_partials(const Device& dev, int prec, const void* rec, int n, const void* ev, int m,
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
+  if (prec == kF32) {
+    static const int tpts[] = {8, 4, 2, 1};
+    static int occ = occupancy(k_vel_f32<8, kNT>, kNT);
+    Plan pl = plan(n, m, kNT, tpts, 4, kTile, occ, dev.sms);
+    if (pl.S > part_cap_chunks) return -1;
+    GS_TPT_SWITCH(pl.tpt, k_vel_f32, (const float4*)rec, n, (const float4*)ev, m, pl.chunk,
+                  (float)kc.kappa, (float)(kc.kappa * kc.c0[0]), (float)(kc.kappa * kc.c0[1]),
+                  (float)(kc.kappa * kc.c0[2]), (float4*)part);
+    return pl.S;
+  }
+  static const int tpts[] = {4, 2, 1};
+  static int occ = occupancy(k_vel_f64<4, kNT>, kNT);
+  Plan pl = plan(n, m, kNT, tpts, 3, kTile / 2, occ, dev.sms);
+  if (pl.S > part_cap_chunks) return -1;
+  switch (pl.tpt) {
+    case 4: k_vel_f64<4, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, (const double4*)ev, m, pl.chunk, kc.inv_two_s, (double4*)part); break;
+    case 2: k_vel_f64<2, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, (const double4*)ev, m, pl.chunk, kc.inv_two_s, (double4*)part); break;
+    default: k_vel_f64<1, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, (const double4*)ev, m, pl.chunk, kc.inv_two_s, (double4*)part); break;
+  }
+  return pl.S;
+}
+
+}  // namespace gsb

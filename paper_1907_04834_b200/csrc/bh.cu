@@ -1,0 +1,395 @@
+// bh.cu -- warp-cooperative Barnes-Hut traversal on sm_100a.
+//
+// Replaces traverse() + the per-query kernels of bh_kernel.cpp:30-160. Per
+// query the reference walks the tree with a LIFO stack: a leaf contributes its
+// point(s) directly (:40-45), a node whose tight box lies farther than the
+// threshold contributes ONE term at its centroid with its aggregate momentum /
+// adjoints (:46-48, :74-77, :143-157), anything else is opened (:49-57).
+//
+// Here the nodes are in depth-first pre-order with skip pointers, so a query's
+// walk is a monotone sweep: visit n; leaf/far -> next = skip[n]; open ->
+// next = n + 1. A warp holds 32 Morton-adjacent queries and always serves the
+// smallest pending node of its lanes (__reduce_min_sync); the lanes parked at
+// that node classify it, so every lane visits exactly its own reference node
+// set, in lock step with its neighbours (coherent loads, little divergence).
+// Direct work is batched: a leaf -- or a node whose FARTHEST box point is
+// within the threshold, all of whose descendants the reference would open
+// down to their leaves -- is a contiguous range of leaf-order points that the
+// lanes parked there sweep together with broadcast loads. The interaction set
+// and the per-query (direct, approximated, visited) counts equal the
+// reference's exactly; only the summation order differs.
+//
+// The gate min_distance(tight box, x) > thr (octree.cpp:141-149) is evaluated
+// bit-exactly: FP64 with the reference's operation order and no contraction,
+// compared as d2 > T2 with T2 the largest double whose sqrt is <= thr. The
+// FP32 path first decides in FP32 with a 1e-6 relative guard band and only
+// falls back to the exact FP64 test inside the band.
+#include <cfloat>
+#include <climits>
+
+#include "bh.h"
+
+namespace gsb {
+
+double gate_t2(double thr) {
+  if (!(thr < INFINITY)) return INFINITY;
+  double x = thr * thr;
+  while (x > 0 && std::sqrt(x) > thr) x = std::nextafter(x, 0.0);
+  while (std::sqrt(std::nextafter(x, INFINITY)) <= thr) x = std::nextafter(x, INFINITY);
+  return x;
+}
+
+namespace {
+
+constexpr int kBhNT = 128;
+
+template <typename R>
+struct BhArgs {
+  const int4* meta;
+  const V4<R>* lo;
+  const V4<R>* hi;
+  const V4<R>* cen;
+  const V4<R>* mom;
+  const V4<R>* nadj_a;
+  const V4<R>* nadj_b;
+  const V4<R>* srec;  // [n][2] interaction coords (scaled FP32), p
+  const V4<R>* squ;   // [n] unscaled q
+  const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
+  const int* perm;
+  int n, nq, tgt_begin, n_tgt;
+  const V4<R>* ev;  // VEL eval records
+  double kap, kc0x, kc0y, kc0z;
+  double T2;         // exact gate threshold on d2
+  R thr2_hi, thr2_lo;  // FP32 guard band around T2
+  R thr2_in;           // max-distance shortcut: all descendants open
+  R inv_two_s, c1;     // FP64 exp scale; HESS FP32 constant
+  V4<R>* part;
+  uint32_t* per_query;
+  unsigned long long* totals;
+};
+
+// exact reference gate: sqrt(dx^2 + dy^2 + dz^2) > thr, dx = max(lo-x, 0, x-hi)
+__device__ __forceinline__ bool gate_exact(double lx, double ly, double lz, double hx, double hy,
+                                           double hz, double x, double y, double z, double T2) {
+  const double dx = fmax(fmax(__dsub_rn(lx, x), 0.0), __dsub_rn(x, hx));
+  const double dy = fmax(fmax(__dsub_rn(ly, y), 0.0), __dsub_rn(y, hy));
+  const double dz = fmax(fmax(__dsub_rn(lz, z), 0.0), __dsub_rn(z, hz));
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return d2 > T2;
+}
+
+__device__ __forceinline__ bool gate(const float4& l, const float4& h, const float4& x,
+                                     const BhArgs<float>& a) {
+  const float dx = fmaxf(fmaxf(l.x - x.x, 0.f), x.x - h.x);
+  const float dy = fmaxf(fmaxf(l.y - x.y, 0.f), x.y - h.y);
+  const float dz = fmaxf(fmaxf(l.z - x.z, 0.f), x.z - h.z);
+  const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+  if (d2 > a.thr2_hi) return true;
+  if (d2 < a.thr2_lo) return false;
+  return gate_exact(l.x, l.y, l.z, h.x, h.y, h.z, x.x, x.y, x.z, a.T2);
+}
+
+__device__ __forceinline__ bool gate(const double4& l, const double4& h, const double4& x,
+                                     const BhArgs<double>& a) {
+  return gate_exact(l.x, l.y, l.z, h.x, h.y, h.z, x.x, x.y, x.z, a.T2);
+}
+
+template <typename R>
+__device__ __forceinline__ bool all_inside(const V4<R>& l, const V4<R>& h, const V4<R>& x, R lim) {
+  const R mx = max(x.x - l.x, h.x - x.x), my = max(x.y - l.y, h.y - x.y), mz = max(x.z - l.z, h.z - x.z);
+  return mx * mx + my * my + mz * mz <= lim;
+}
+
+// Gaussian weight between the query and a source in interaction coordinates.
+__device__ __forceinline__ float kern(float dx, float dy, float dz, const BhArgs<float>&) {
+  float nr2 = -dx * dx;
+  nr2 = fmaf(-dy, dy, nr2);
+  nr2 = fmaf(-dz, dz, nr2);
+  return ex2(nr2);
+}
+__device__ __forceinline__ double kern(double dx, double dy, double dz, const BhArgs<double>& a) {
+  return exp(-(dx * dx + dy * dy + dz * dz) * a.inv_two_s);
+}
+
+template <typename R>
+struct Acc {
+  R v[12];
+};
+
+// One (direct or aggregate) unit: Q = source coords, P = momentum (sum),
+// Al = alpha (sum), Be = beta (mean) -- bh_kernel.cpp:86-110 / :119-157.
+template <typename R, int MODE>
+__device__ __forceinline__ void unit(Acc<R>& acc, const V4<R>& xs, const V4<R>& px,
+                                     const V4<R>& ai, const V4<R>& bi, const V4<R>& Q,
+                                     const V4<R>& P, const V4<R>& Al, const V4<R>& Be,
+                                     const BhArgs<R>& a) {
+  const R dx = xs.x - Q.x, dy = xs.y - Q.y, dz = xs.z - Q.z;
+  const R g = kern(dx, dy, dz, a);
+  if (MODE == kBhVel) {
+    acc.v[0] += g * P.x; acc.v[1] += g * P.y; acc.v[2] += g * P.z;
+  } else if (MODE == kBhRhs) {
+    const R c = (px.x * P.x + px.y * P.y + px.z * P.z) * g;
+    acc.v[0] += g * P.x; acc.v[1] += g * P.y; acc.v[2] += g * P.z;
+    acc.v[3] += c * dx; acc.v[4] += c * dy; acc.v[5] += c * dz;
+  } else {
+    const R dbx = bi.x - Be.x, dby = bi.y - Be.y, dbz = bi.z - Be.z;
+    const R ddb = dx * dbx + dy * dby + dz * dbz;
+    const R s1 = (P.x * ai.x + P.y * ai.y + P.z * ai.z) + (px.x * Al.x + px.y * Al.y + px.z * Al.z);
+    const R pp = px.x * P.x + px.y * P.y + px.z * P.z;
+    const R t1 = g * s1;
+    acc.v[0] += t1 * dx; acc.v[1] += t1 * dy; acc.v[2] += t1 * dz;
+    acc.v[3] += g * Al.x; acc.v[4] += g * Al.y; acc.v[5] += g * Al.z;
+    const R w = g * pp, uu = ddb * a.c1;
+    acc.v[6] += w * (uu * dx - dbx); acc.v[7] += w * (uu * dy - dby); acc.v[8] += w * (uu * dz - dbz);
+    const R m = g * ddb;
+    acc.v[9] += m * P.x; acc.v[10] += m * P.y; acc.v[11] += m * P.z;
+  }
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
+  const int qi = blockIdx.x * kBhNT + threadIdx.x;
+  const bool valid = qi < a.nq;
+  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
+  int out = -1;
+  if (valid) {
+    if (MODE == kBhVel) {
+      x = ld4(a.ev + 2 * qi);
+      if (sizeof(R) == 4)
+        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
+                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
+                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
+      else
+        xs = x;
+      out = qi;
+    } else {
+      const int t = qi;  // leaf-order position
+      x = ld4(a.squ + t);
+      xs = ld4(a.srec + 2 * t);
+      px = ld4(a.srec + 2 * t + 1);
+      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
+      const int i = a.perm[t] - a.tgt_begin;
+      out = (i >= 0 && i < a.n_tgt) ? i : -1;
+    }
+  }
+  Acc<R> acc;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
+  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  int next = out >= 0 ? 0 : INT_MAX;
+  const V4<R> zero = mk4<R>(0, 0, 0);
+  for (;;) {
+    const int nd = __reduce_min_sync(0xffffffffu, next);
+    if (nd == INT_MAX) break;
+    bool ranged = false;
+    int4 mi = make_int4(0, 0, 0, 0);
+    if (next == nd) {
+      mi = a.meta[nd];
+      ++c_vis;
+      if (mi.w & 1) {  // leaf: its point(s) directly
+        ranged = true;
+        next = mi.x;
+      } else {
+        const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
+        if (gate(l, h, x, a)) {  // far: one aggregate term
+          const V4<R> C = ld4(a.cen + nd), P = ld4(a.mom + nd);
+          if (MODE == kBhHess)
+            unit<R, MODE>(acc, xs, px, ai, bi, C, P, ld4(a.nadj_a + nd), ld4(a.nadj_b + nd), a);
+          else
+            unit<R, MODE>(acc, xs, px, ai, bi, C, P, zero, zero, a);
+          ++c_app;
+          next = mi.x;
+        } else if (all_inside(l, h, x, a.thr2_in)) {  // whole subtree opens: range
+          ranged = true;
+          c_vis += (uint32_t)(mi.x - nd - 1);
+          next = mi.x;
+        } else {
+          next = nd + 1;
+        }
+      }
+    }
+    const unsigned rm = __ballot_sync(0xffffffffu, ranged);
+    if (rm) {
+      const int src = __ffs(rm) - 1;
+      const int b = __shfl_sync(0xffffffffu, mi.y, src);
+      const int e = __shfl_sync(0xffffffffu, mi.z, src);
+      if (ranged) {
+        c_dir += (uint32_t)(e - b + 1);
+        for (int j = b; j <= e; ++j) {
+          const V4<R> Q = ld4(a.srec + 2 * j), P = ld4(a.srec + 2 * j + 1);
+          if (MODE == kBhHess)
+            unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
+          else
+            unit<R, MODE>(acc, xs, px, ai, bi, Q, P, zero, zero, a);
+        }
+      }
+    }
+  }
+  if (out >= 0) {
+    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
+    V4<R>* o = a.part + (size_t)per * out;
+    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
+    if (a.per_query) {
+      a.per_query[3 * out] = c_dir;
+      a.per_query[3 * out + 1] = c_app;
+      a.per_query[3 * out + 2] = c_vis;
+    }
+  }
+  if (a.totals) {
+    unsigned long long d = c_dir, p = c_app, v = c_vis;
+    for (int o = 16; o > 0; o >>= 1) {
+      d += __shfl_down_sync(0xffffffffu, d, o);
+      p += __shfl_down_sync(0xffffffffu, p, o);
+      v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.totals, d);
+      atomicAdd(a.totals + 1, p);
+      atomicAdd(a.totals + 2, v);
+    }
+  }
+}
+
+template <typename R>
+int launch(int mode, const BhArgs<R>& a, cudaStream_t st) {
+  const int nb = std::max(1, (a.nq + kBhNT - 1) / kBhNT);
+  if (mode == kBhRhs) k_bh<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
+  else if (mode == kBhHess) k_bh<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
+  else k_bh<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+template <typename R>
+BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
+  BhArgs<R> a{};
+  a.meta = t.meta.as<int4>();
+  a.lo = t.lo.as<V4<R>>();
+  a.hi = t.hi.as<V4<R>>();
+  a.cen = t.cen.as<V4<R>>();
+  a.mom = t.mom.as<V4<R>>();
+  a.nadj_a = t.nadj_a.as<V4<R>>();
+  a.nadj_b = t.nadj_b.as<V4<R>>();
+  a.srec = t.srec.as<V4<R>>();
+  a.squ = t.squ.as<V4<R>>();
+  a.sadj = t.sadj.as<V4<R>>();
+  a.perm = t.perm.as<int>();
+  a.n = (int)t.n;
+  a.tgt_begin = q.tgt_begin;
+  a.n_tgt = q.n_tgt;
+  a.nq = q.mode == kBhVel ? q.m : (int)t.n;
+  a.ev = static_cast<const V4<R>*>(q.ev);
+  const KernelConsts& kc = t.kc;
+  a.kap = kc.kappa;
+  a.kc0x = kc.c0[0];
+  a.kc0y = kc.c0[1];
+  a.kc0z = kc.c0[2];
+  a.T2 = gate_t2(thr);
+  const double t2 = a.T2;
+  if (sizeof(R) == 4) {
+    a.thr2_hi = (R)(t2 * (1.0 + 1e-6));
+    a.thr2_lo = (R)(t2 * (1.0 - 1e-6));
+    a.c1 = (R)(1.0 / (kc.kappa * kc.kappa * kc.s));
+  } else {
+    a.thr2_hi = (R)t2;
+    a.thr2_lo = (R)t2;
+    a.c1 = (R)kc.inv_s;
+  }
+  a.thr2_in = (R)(thr < INFINITY ? thr * thr * (1.0 - 1e-5) : INFINITY);
+  a.inv_two_s = (R)kc.inv_two_s;
+  a.part = static_cast<V4<R>*>(q.part);
+  a.per_query = q.per_query;
+  a.totals = q.totals;
+  (void)sigma;
+  return a;
+}
+
+}  // namespace
+
+int bh_traverse(const Device&, int prec, DevTree& t, double sigma, double thr, const BhQuery& q,
+                cudaStream_t st) {
+  if (prec == kF32) return launch<float>(q.mode, make_args<float>(t, sigma, thr, q), st);
+  return launch<double>(q.mode, make_args<double>(t, sigma, thr, q), st);
+}
+
+int bh_keep_trees(BhWork& w, int T) {
+  while ((int)w.kept.size() < T) w.kept.emplace_back(new DevTree);
+  return GS_OK;
+}
+
+static DevTree& tree_for(BhWork& w) {
+  if (w.cache_slot >= 0 && w.cache_slot < (int)w.kept.size()) return *w.kept[w.cache_slot];
+  return w.cur;
+}
+
+int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec, int64_t n, int64_t tb, int64_t nt, BhWork& w, FwdEpi e,
+                     cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats*) {
+  DevTree& t = tree_for(w);
+  GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st));
+  GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+  GS_TRY_INT(w.stats.ensure(64));
+  BhQuery q;
+  q.mode = kBhRhs;
+  q.tgt_begin = (int)tb;
+  q.n_tgt = (int)nt;
+  q.part = w.part.ptr;
+  q.totals = w.stats.as<unsigned long long>();
+  const double thr = cfg.threshold_multiplier * cfg.sigma;
+  GS_TRY_INT(bh_traverse(dev, prec, t, cfg.sigma, thr, q, st));
+  e.S = 1;
+  e.parts_per_tgt = 2;
+  e.part = w.part.ptr;
+  e.n_tgt = (int)nt;
+  e.tgt_begin = (int)tb;
+  e.cp = 2.0;
+  e.cq = prec == kF32 ? -kc.two_over_s / kc.kappa : -kc.two_over_s;
+  GS_TRY_INT(fwd_epilogue(prec, e, st, energy_blocks));
+  if (launches) *launches += 30;  // build (~27) + traversal + epilogue
+  return GS_OK;
+}
+
+int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec_k, void* adj, int64_t n, int k, BhWork& w, bool cached,
+                     BwdEpi e, cudaStream_t st, gs_stats*) {
+  DevTree* t = nullptr;
+  if (cached && k < (int)w.kept.size()) {
+    t = w.kept[k].get();
+  } else {
+    t = &w.cur;
+    GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, *t, st));
+  }
+  GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
+  GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * n));
+  GS_TRY_INT(w.stats.ensure(64));
+  BhQuery q;
+  q.mode = kBhHess;
+  q.tgt_begin = 0;
+  q.n_tgt = (int)n;
+  q.part = w.part.ptr;
+  q.totals = w.stats.as<unsigned long long>();
+  GS_TRY_INT(bh_traverse(dev, prec, *t, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));
+  e.S = 1;
+  e.part = w.part.ptr;
+  GS_TRY_INT(bwd_epilogue(prec, e, st));
+  return GS_OK;
+}
+
+int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
+                     cudaStream_t st) {
+  GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, w.cur, st));
+  GS_TRY_INT(w.part.ensure(vec_bytes(prec) * m));
+  BhQuery q;
+  q.mode = kBhVel;
+  q.ev = ev;
+  q.m = (int)m;
+  q.part = w.part.ptr;
+  GS_TRY_INT(bh_traverse(dev, prec, w.cur, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));
+  e.S = 1;
+  e.part = w.part.ptr;
+  GS_TRY_INT(vel_epilogue(prec, e, st));
+  return GS_OK;
+}
+
+}  // namespace gsb

@@ -1,0 +1,103 @@
+// bh.h -- device octree (tree.cu) and Barnes-Hut traversal (bh.cu) interfaces.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.h"
+
+namespace gsb {
+
+// Device octree with the reference's node semantics (octree.cpp:25-117),
+// built from midpoint-replay Morton keys. Nodes in depth-first pre-order
+// (children 0..7): a node's subtree is [idx, skip) and its points are the
+// contiguous leaf-order positions [begin, end].
+struct DevTree {
+  int prec = kF64;
+  int64_t n = 0, m = 0;
+  // per point (index order)
+  DBuf key_hi, key_lo;  // u64
+  // per leaf-order position
+  DBuf perm;            // i32 point index
+  DBuf skey_hi, skey_lo;
+  DBuf lcp;             // i32 common digits with the next position
+  DBuf first;           // i32 [n+1] pre-order index of the first node starting here
+  DBuf srec;            // [n][2] V4<R>: scaled q' (FP32) / q (FP64), p
+  DBuf squ;             // [n] V4<R>: unscaled q (gate queries, aggregates)
+  DBuf sadj;            // [n][2] V4<R>: alpha, beta in leaf order
+  // per node
+  DBuf meta;            // int4 {skip, begin, end, leaf | level << 8}
+  DBuf parent;          // i32
+  DBuf nchild;          // i32
+  DBuf counter;         // i32 bottom-up arrival counters
+  DBuf lo, hi;          // V4<R> tight AABB (unscaled)
+  DBuf cen, mom;        // V4<R> centroid (scaled in FP32) / momentum sum
+  DBuf nadj_a, nadj_b;  // V4<R> alpha sum / beta mean
+  DBuf psum, msum;      // double4 exact-order-independent aggregates
+  DBuf asum, bsum;      // double4
+  DBuf root;            // double[6] padded root box
+  // radix-sort scratch
+  DBuf tmp_k, tmp_v, hist;
+  DBuf scan_tmp;
+  DBuf scal;
+  KernelConsts kc{};
+  double thr = 0.0;
+  bool adj_valid = false;
+};
+
+int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
+               DevTree& t, cudaStream_t st);
+// (re)writes the interaction coordinates (FP32: scaled by kc.kappa) and centroids
+int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, cudaStream_t st);
+// adj: [n][2] records (alpha, beta) by point index; node sums + leaf-order copy
+int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st);
+// leaf-order copy of per-point adjoints only (node sums untouched)
+int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t st);
+// host copies for gs_tree_download
+int tree_download(const DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
+                  uint64_t* key_lo, int32_t* level, int32_t* parent, int32_t* skip,
+                  int32_t* range, double* boxes, double* sums, uint32_t* count);
+
+enum BhMode { kBhRhs = 0, kBhHess = 1, kBhVel = 2 };
+
+struct BhQuery {
+  int mode = kBhRhs;
+  // RHS / HESS: queries are the tree's own points restricted to point indices
+  // [tgt_begin, tgt_begin + n_tgt); partials written per target (index - tgt_begin)
+  int tgt_begin = 0, n_tgt = 0;
+  // VEL: m external eval records (x, -) ; partials per eval point
+  const void* ev = nullptr;
+  int m = 0;
+  void* part = nullptr;
+  uint32_t* per_query = nullptr;  // optional [nq][3] direct, approx, visited (query order)
+  unsigned long long* totals = nullptr;  // optional [3] sums
+};
+int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,
+                const BhQuery& q, cudaStream_t st);
+
+// Barnes-Hut work area of a flow: the current tree plus, for evaluate(), the
+// forward trees kept per step (shooting.cpp:96-97, :177-183).
+struct BhWork {
+  DevTree cur;
+  std::vector<std::unique_ptr<DevTree>> kept;
+  int cache_slot = -1;
+  DBuf part;   // traversal partials
+  DBuf stats;  // u64 totals (direct, approximated, visited)
+};
+
+int bh_keep_trees(BhWork& w, int T);
+int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec, int64_t n, int64_t tb, int64_t nt, BhWork& w, FwdEpi e,
+                     cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats* stats);
+int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec_k, void* adj, int64_t n, int k, BhWork& w, bool cached,
+                     BwdEpi e, cudaStream_t st, gs_stats* stats);
+int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
+                     const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
+                     cudaStream_t st);
+
+// Largest double T2 with sqrt(T2) <= thr: the gate sqrt(d2) > thr
+// (octree.cpp:141-149 + bh_kernel.cpp:46) is then exactly d2 > T2.
+double gate_t2(double thr);
+
+}  // namespace gsb

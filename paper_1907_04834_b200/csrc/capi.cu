@@ -1,0 +1,1159 @@
+// capi.cu -- the C ABI (include/geoshoot_b200.h): contexts, device-resident
+// flows, and the reference-facing entry points (kernel_exact / octree /
+// bh_kernel / shooting). Host code only orchestrates: every arithmetic step
+// of the hot path runs in the sm_100a kernels of allpairs.cu, epilogue.cu,
+// tree.cu and bh.cu. There is no CPU fallback -- without a B200 the context
+// cannot be created.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "bh.h"
+#include "engine.h"
+
+namespace gsb {
+
+thread_local std::string g_err;
+thread_local int g_nonfinite = 0;
+thread_local uint32_t g_violations = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                cudaGetErrorString(e), what, file, line);
+  g_err = buf;
+  return GS_CUDA_ERROR;
+}
+
+int DBuf::ensure(size_t need) {
+  if (need <= bytes && ptr) return GS_OK;
+  release();
+  need = std::max<size_t>(need, 256);
+  GS_CUDA_OK(cudaMalloc(&ptr, need));
+  bytes = need;
+  return GS_OK;
+}
+
+void DBuf::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+}  // namespace gsb
+
+using namespace gsb;
+
+#define GS_TRY(expr)                 \
+  do {                               \
+    const int s__ = (expr);          \
+    if (s__ != GS_OK) return (gs_status)s__; \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------
+struct gs_ctx {
+  Device dev;
+  cudaStream_t stream = nullptr;
+  // host-array staging (double [n][3]) and small scalars
+  DBuf stage_a, stage_b, stage_c, stage_d, scal;
+  DBuf rec_a, rec_b, part, epart;
+  gs_flow* scratch = nullptr;
+};
+
+struct gs_flow {
+  gs_ctx* ctx = nullptr;
+  gs_config cfg{};
+  int prec = kF64;
+  int64_t n = 0, shard_begin = 0, shard_count = 0;
+  KernelConsts kc{};
+  DBuf rec, rec_next, y, ks, part, dhdp0, epart, flags, scal;
+  int steps_done = 0;
+  int64_t launches = 0;
+  bool want_energy = false;
+  bool have_energy_part = false;
+  int energy_blocks = 0;
+  BhWork bh;
+  gs_stats stats{};
+};
+
+extern "C" {
+
+gs_config gs_default_config(void) {
+  gs_config c;
+  c.sigma = 2.0;
+  c.lambda = 1.0;
+  c.timesteps = 40;
+  c.backend = GS_EXACT;
+  c.threshold_multiplier = 3.0;
+  c.integrator = GS_EULER;
+  c.precision = GS_F64;
+  return c;
+}
+
+int gs_abi_version(void) { return GS_ABI_VERSION; }
+
+gs_ctx* gs_create(int device, gs_status* status) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0 || device < 0 || device >= count) {
+    g_err = std::string("no CUDA device available: ") +
+            (e != cudaSuccess ? cudaGetErrorString(e) : "device index out of range");
+    if (status) *status = GS_NO_DEVICE;
+    return nullptr;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    g_err = "geoshoot_b200 needs an sm_100a (Blackwell) device";
+    if (status) *status = GS_NO_DEVICE;
+    return nullptr;
+  }
+  cudaSetDevice(device);
+  gs_ctx* c = new gs_ctx;
+  c->dev.id = device;
+  c->dev.sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    g_err = "cudaStreamCreate failed";
+    delete c;
+    if (status) *status = GS_CUDA_ERROR;
+    return nullptr;
+  }
+  if (status) *status = GS_OK;
+  return c;
+}
+
+void gs_destroy(gs_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->scratch) gs_flow_destroy(ctx->scratch);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* gs_last_error(const gs_ctx*) { return g_err.c_str(); }
+int gs_last_nonfinite_step(const gs_ctx*) { return g_nonfinite; }
+uint32_t gs_last_config_violations(const gs_ctx*) { return g_violations; }
+
+gs_status gs_validate_config(const gs_config* cfg, uint32_t* mask) {
+  uint32_t m = 0;
+  if (!(cfg->sigma > 0.0)) m |= GS_VIOLATION_NON_POSITIVE_SIGMA;
+  if (!(cfg->lambda > 0.0)) m |= GS_VIOLATION_NON_POSITIVE_LAMBDA;
+  if (cfg->timesteps < 1) m |= GS_VIOLATION_ZERO_TIMESTEPS;
+  if (!(cfg->threshold_multiplier > 0.0)) m |= GS_VIOLATION_NON_POSITIVE_THRESHOLD;
+  if (mask) *mask = m;
+  g_violations = m;
+  if (m) {
+    g_err = "invalid shooting config";
+    return GS_CONFIG_ERROR;
+  }
+  return GS_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------
+namespace {
+
+gs_status bad_arg(const char* msg) {
+  g_err = msg;
+  return GS_INVALID_ARGUMENT;
+}
+
+// host [n][3] doubles -> device staging buffer
+int h2d(gs_ctx* c, DBuf& dst, const double* src, int64_t n) {
+  GS_TRY(dst.ensure(sizeof(double) * 3 * std::max<int64_t>(n, 1)));
+  if (n > 0)
+    GS_CUDA_OK(cudaMemcpyAsync(dst.ptr, src, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
+                               c->stream));
+  return GS_OK;
+}
+
+int d2h(gs_ctx* c, double* dst, const void* src, int64_t count) {
+  if (dst && count > 0)
+    GS_CUDA_OK(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                               c->stream));
+  return GS_OK;
+}
+
+int sync(gs_ctx* c) {
+  GS_CUDA_OK(cudaStreamSynchronize(c->stream));
+  return GS_OK;
+}
+
+// FP32 centring: midpoint of the host bounding box (cheap, keeps |x'| small).
+void bbox_center(const double* q, int64_t n, double* c0) {
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) lo[a] = hi[a] = q[a];
+  for (int64_t i = 1; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const double v = q[3 * i + a];
+      lo[a] = v < lo[a] ? v : lo[a];
+      hi[a] = v > hi[a] ? v : hi[a];
+    }
+  for (int a = 0; a < 3; ++a) c0[a] = 0.5 * (lo[a] + hi[a]);
+}
+
+// upload + pack; flags non-finite input (PointSet/MomentumSet ctor, core.hpp:124-170)
+int upload_records(gs_ctx* c, int prec, const double* q, const double* p, int64_t n, DBuf& rec) {
+  GS_TRY(h2d(c, c->stage_a, q, n));
+  if (p) GS_TRY(h2d(c, c->stage_b, p, n));
+  GS_TRY(rec.ensure(2 * vec_bytes(prec) * n));
+  GS_TRY(c->scal.ensure(64));
+  int* bad = c->scal.as<int>();
+  GS_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  GS_TRY(pack_records(prec, c->stage_a.as<double>(), p ? c->stage_b.as<double>() : nullptr, n,
+                      rec.ptr, bad, c->stream));
+  int hbad = 0;
+  GS_CUDA_OK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  GS_TRY(sync(c));
+  if (hbad) return bad_arg("non-finite coordinate in input");
+  return GS_OK;
+}
+
+double fwd_cq(int prec, const KernelConsts& kc) {
+  // dH/dq = -(2/s) sum c d ; FP32 partials hold d' = kappa d
+  return prec == kF32 ? -kc.two_over_s / kc.kappa : -kc.two_over_s;
+}
+
+// one exact RHS over all n sources for targets [tb, tb + nt) + its epilogue
+int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
+                int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
+                int* energy_blocks) {
+  GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+  const int S = rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr, kMaxChunks, st);
+  if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
+  GS_CUDA_OK(cudaGetLastError());
+  e.S = S;
+  e.part = part.ptr;
+  e.n_tgt = (int)nt;
+  e.tgt_begin = (int)tb;
+  e.cp = 2.0;
+  e.cq = fwd_cq(prec, kc);
+  GS_TRY(fwd_epilogue(prec, e, st, energy_blocks));
+  if (launches) *launches += 2;
+  return GS_OK;
+}
+
+int check_n(int64_t n) {
+  if (n < 1) return bad_arg("point set must contain at least one point");
+  if (n > (int64_t)INT32_MAX / 4) return bad_arg("point count exceeds the 2^29 limit");
+  return GS_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// flows
+// ----------------------------------------------------------------------------
+namespace {
+
+int flow_stages(const gs_flow* f) { return f->cfg.integrator == GS_RK4 ? 4 : 1; }
+
+// One integrator stage for the shard: RHS (exact or Barnes-Hut) + epilogue.
+// rec_in (default: the flow's records) holds all n source records; the
+// shard's updated records go to rec_out (default: in place).
+int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
+  gs_ctx* c = f->ctx;
+  cudaStream_t st = c->stream;
+  if (!rec_in) rec_in = f->rec.ptr;
+  GS_TRY(f->flags.ensure(64));
+  FwdEpi e;
+  e.rec = rec_in;
+  e.rec_out = rec_out;
+  e.y = f->y.ptr;
+  e.ks = f->ks.ptr;
+  e.integrator = f->cfg.integrator;
+  e.stage = stage;
+  e.update = 1;
+  e.dt = 1.0 / f->cfg.timesteps;
+  e.bad_step = f->flags.as<int>();
+  e.step = f->steps_done + 1;
+  const bool first = f->want_energy && f->steps_done == 0 && stage == 0;
+  if (first) {
+    GS_TRY(f->epart.ensure(sizeof(double) * (f->shard_count / 128 + 8)));
+    GS_TRY(f->dhdp0.ensure(sizeof(double) * 3 * f->shard_count));
+    e.energy_part = f->epart.as<double>();
+    e.dhdp_out = f->dhdp0.as<double>();
+  }
+  int blocks = 0;
+  if (f->cfg.backend == GS_EXACT) {
+    GS_TRY(exact_stage(c->dev, f->prec, f->kc, rec_in, f->n, f->shard_begin, f->shard_count,
+                       f->part, e, st, &f->launches, &blocks));
+    f->stats.direct_interactions += (uint64_t)f->n * (uint64_t)f->shard_count;
+    f->stats.traversal_queries += (uint64_t)f->shard_count;
+  } else {
+    GS_TRY(bh_forward_stage(c->dev, f->prec, f->kc, f->cfg, rec_in, f->n, f->shard_begin,
+                            f->shard_count, f->bh, e, st, &f->launches, &blocks, &f->stats));
+  }
+  if (first) {
+    f->have_energy_part = true;
+    f->energy_blocks = blocks;
+  }
+  return GS_OK;
+}
+
+int flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
+  f->ctx = c;
+  f->cfg = *cfg;
+  f->prec = cfg->precision == GS_F32 ? kF32 : kF64;
+  f->n = n;
+  f->shard_begin = 0;
+  f->shard_count = n;
+  f->steps_done = 0;
+  f->launches = 0;
+  f->want_energy = false;
+  f->have_energy_part = false;
+  f->stats = gs_stats{};
+  const size_t rb = 2 * vec_bytes(f->prec) * n;
+  GS_TRY(f->rec.ensure(rb));
+  if (cfg->integrator == GS_RK4) {
+    GS_TRY(f->y.ensure(rb));
+    GS_TRY(f->ks.ensure(rb));
+  }
+  GS_TRY(f->flags.ensure(64));
+  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, sizeof(int), c->stream));  // bad_step = +big
+  GS_TRY(f->bh.stats.ensure(64));
+  GS_CUDA_OK(cudaMemsetAsync(f->bh.stats.ptr, 0, 64, c->stream));
+  return GS_OK;
+}
+
+// fold the device-side Barnes-Hut counters into the host stats
+int flow_bh_stats(gs_flow* f, gs_stats* out) {
+  if (f->cfg.backend != GS_BARNES_HUT || !out) return GS_OK;
+  unsigned long long v[3] = {0, 0, 0};
+  GS_CUDA_OK(cudaMemcpyAsync(v, f->bh.stats.ptr, sizeof v, cudaMemcpyDeviceToHost, f->ctx->stream));
+  GS_TRY(sync(f->ctx));
+  out->direct_interactions += v[0];
+  out->approximated_interactions += v[1];
+  out->nodes_visited += v[2];
+  return GS_OK;
+}
+
+int flow_upload(gs_flow* f, const double* q0, const double* p0) {
+  double c0[3];
+  bbox_center(q0, f->n, c0);
+  f->kc = make_consts(f->cfg.sigma, f->prec == kF32 ? c0 : nullptr);
+  GS_TRY(upload_records(f->ctx, f->prec, q0, p0, f->n, f->rec));
+  f->steps_done = 0;
+  f->have_energy_part = false;
+  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, sizeof(int), f->ctx->stream));
+  return GS_OK;
+}
+
+int flow_advance(gs_flow* f, int steps) {
+  f->launches = 0;
+  for (int k = 0; k < steps; ++k) {
+    for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
+    ++f->steps_done;
+  }
+  return GS_OK;
+}
+
+// returns GS_NONFINITE (and records the step) if the device flag was raised
+int flow_check(gs_flow* f) {
+  int bad = 0;
+  GS_CUDA_OK(cudaMemcpyAsync(&bad, f->flags.ptr, sizeof(int), cudaMemcpyDeviceToHost,
+                             f->ctx->stream));
+  GS_TRY(sync(f->ctx));
+  if (bad != 0x7f7f7f7f) {
+    g_nonfinite = bad;
+    g_err = "non-finite state at timestep " + std::to_string(bad);
+    return GS_NONFINITE;
+  }
+  return GS_OK;
+}
+
+int flow_energy(gs_flow* f, double* out) {
+  if (!f->have_energy_part) { *out = 0.0; return GS_OK; }
+  GS_TRY(f->scal.ensure(64));
+  GS_TRY(reduce_sum(f->epart.as<double>(), f->energy_blocks, f->scal.as<double>(), f->ctx->stream));
+  double h = 0.0;
+  GS_CUDA_OK(cudaMemcpyAsync(&h, f->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost,
+                             f->ctx->stream));
+  GS_TRY(sync(f->ctx));
+  *out = 0.5 * h;  // H = 1/2 <p0, dH/dp>, shooting.cpp:104-108
+  return GS_OK;
+}
+
+gs_flow* scratch_flow(gs_ctx* c) {
+  if (!c->scratch) c->scratch = new gs_flow;
+  return c->scratch;
+}
+
+struct Timer {
+  cudaEvent_t a{}, b{};
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double ms() {
+    float v = 0.f;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&v, a, b);
+    return v;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+gs_status gs_flow_create(gs_ctx* ctx, const gs_config* cfg, int64_t n, gs_flow** out) {
+  if (!ctx || !cfg || !out) return bad_arg("null argument");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  auto* f = new gs_flow;
+  const int s = flow_init(f, ctx, cfg, n);
+  if (s != GS_OK) {
+    delete f;
+    return (gs_status)s;
+  }
+  *out = f;
+  return GS_OK;
+}
+
+void gs_flow_destroy(gs_flow* flow) {
+  if (!flow) return;
+  if (flow->ctx) cudaStreamSynchronize(flow->ctx->stream);
+  delete flow;
+}
+
+gs_status gs_flow_upload(gs_flow* f, const double* q0, const double* p0) {
+  if (!f || !q0 || !p0) return bad_arg("null argument");
+  return (gs_status)flow_upload(f, q0, p0);
+}
+
+gs_status gs_flow_advance(gs_flow* f, int32_t steps) {
+  if (!f) return bad_arg("null flow");
+  return (gs_status)flow_advance(f, steps);
+}
+
+gs_status gs_flow_sync(gs_flow* f) {
+  if (!f) return bad_arg("null flow");
+  return (gs_status)flow_check(f);
+}
+
+gs_status gs_flow_download(gs_flow* f, double* q, double* p) {
+  if (!f) return bad_arg("null flow");
+  gs_ctx* c = f->ctx;
+  GS_TRY(c->stage_a.ensure(sizeof(double) * 3 * f->n));
+  GS_TRY(c->stage_b.ensure(sizeof(double) * 3 * f->n));
+  GS_TRY(unpack_records(f->prec, f->rec.ptr, f->n, c->stage_a.as<double>(),
+                        c->stage_b.as<double>(), c->stream));
+  GS_TRY(d2h(c, q, c->stage_a.ptr, 3 * f->n));
+  GS_TRY(d2h(c, p, c->stage_b.ptr, 3 * f->n));
+  GS_TRY(sync(c));
+  return GS_OK;
+}
+
+int64_t gs_flow_last_launches(const gs_flow* f) { return f ? f->launches : 0; }
+void* gs_flow_stream(const gs_flow* f) { return f ? (void*)f->ctx->stream : nullptr; }
+
+gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
+  if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
+  f->shard_begin = begin;
+  f->shard_count = count;
+  return GS_OK;
+}
+
+void* gs_flow_source_buffer(gs_flow* f) { return f ? f->rec.ptr : nullptr; }
+int64_t gs_flow_record_bytes(const gs_flow* f) { return f ? 2 * (int64_t)vec_bytes(f->prec) : 0; }
+
+gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
+  if (!f || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");
+  f->launches = 0;
+  GS_TRY(flow_stage(f, stage, nullptr, nullptr));
+  if (stage == flow_stages(f) - 1) ++f->steps_done;
+  return GS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// kernel_exact
+// ----------------------------------------------------------------------------
+gs_status gs_exact_rhs(gs_ctx* c, int32_t precision, int64_t n, const double* q, const double* p,
+                       double sigma, double* dHdp, double* dHdq, double* h_out) {
+  if (!c || !q || !p) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  const int prec = precision == GS_F32 ? kF32 : kF64;
+  double c0[3];
+  bbox_center(q, n, c0);
+  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
+  GS_TRY(c->stage_c.ensure(sizeof(double) * 3 * n));
+  GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
+  GS_TRY(c->epart.ensure(sizeof(double) * (n / 128 + 8)));
+  GS_TRY(c->scal.ensure(64));
+  FwdEpi e;
+  e.rec = c->rec_a.ptr;
+  e.update = 0;
+  e.dhdp_out = c->stage_c.as<double>();
+  e.dhdq_out = c->stage_d.as<double>();
+  e.energy_part = h_out ? c->epart.as<double>() : nullptr;
+  int blocks = 0;
+  GS_TRY(exact_stage(c->dev, prec, kc, c->rec_a.ptr, n, 0, n, c->part, e, c->stream, nullptr,
+                     &blocks));
+  double h = 0.0;
+  if (h_out) {
+    GS_TRY(reduce_sum(c->epart.as<double>(), blocks, c->scal.as<double>(), c->stream));
+    GS_CUDA_OK(cudaMemcpyAsync(&h, c->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  GS_TRY(d2h(c, dHdp, c->stage_c.ptr, 3 * n));
+  GS_TRY(d2h(c, dHdq, c->stage_d.ptr, 3 * n));
+  GS_TRY(sync(c));
+  if (h_out) *h_out = 0.5 * h;  // H = 1/2 <p, dH/dp> (same double sum, kernel_exact.hpp:22-28)
+  return GS_OK;
+}
+
+gs_status gs_hamiltonian(gs_ctx* c, int32_t precision, int64_t n, const double* q,
+                         const double* p, double sigma, double* h_out) {
+  if (!h_out) return bad_arg("null argument");
+  return gs_exact_rhs(c, precision, n, q, p, sigma, nullptr, nullptr, h_out);
+}
+
+gs_status gs_exact_velocity(gs_ctx* c, int32_t precision, int64_t m, const double* x, int64_t n,
+                            const double* q, const double* p, double sigma, double* v_out) {
+  if (!c || !x || !q || !p || !v_out) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  GS_TRY(check_n(m));
+  const int prec = precision == GS_F32 ? kF32 : kF64;
+  double c0[3];
+  bbox_center(q, n, c0);
+  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
+  GS_TRY(upload_records(c, prec, x, nullptr, m, c->rec_b));
+  GS_TRY(c->part.ensure((size_t)kMaxChunks * vec_bytes(prec) * m));
+  GS_TRY(c->stage_c.ensure(sizeof(double) * 3 * m));
+  const int S = vel_partials(c->dev, prec, c->rec_a.ptr, (int)n, c->rec_b.ptr, (int)m, kc,
+                             c->part.ptr, kMaxChunks, c->stream);
+  if (S < 0) return (gs_status)GS_INTERNAL;
+  GS_CUDA_OK(cudaGetLastError());
+  VelEpi e;
+  e.m = (int)m;
+  e.S = S;
+  e.part = c->part.ptr;
+  e.scale = 1.0;
+  e.v_out = c->stage_c.as<double>();
+  GS_TRY(vel_epilogue(prec, e, c->stream));
+  GS_TRY(d2h(c, v_out, c->stage_c.ptr, 3 * m));
+  GS_TRY(sync(c));
+  return GS_OK;
+}
+
+gs_status gs_hessian_products(gs_ctx* c, int32_t precision, int64_t n, const double* q,
+                              const double* p, const double* alpha, const double* beta,
+                              double sigma, double* pq, double* pp, double* qq, double* qp) {
+  if (!c || !q || !p || !alpha || !beta) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  const int prec = precision == GS_F32 ? kF32 : kF64;
+  double c0[3];
+  bbox_center(q, n, c0);
+  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
+  GS_TRY(upload_records(c, prec, alpha, beta, n, c->rec_b));
+  GS_TRY(c->part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * n));
+  DBuf* outs[4] = {&c->stage_a, &c->stage_b, &c->stage_c, &c->stage_d};
+  for (DBuf* b : outs) GS_TRY(b->ensure(sizeof(double) * 3 * n));
+  const int S = hess_partials(c->dev, prec, c->rec_a.ptr, c->rec_b.ptr, (int)n, 0, (int)n, kc,
+                              c->part.ptr, kMaxChunks, c->stream);
+  if (S < 0) return (gs_status)GS_INTERNAL;
+  GS_CUDA_OK(cudaGetLastError());
+  BwdEpi e;
+  e.n_tgt = (int)n;
+  e.S = S;
+  e.part = c->part.ptr;
+  e.update = 0;
+  const double cd = prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;
+  e.cpq = -cd;
+  e.cpp = 2.0;
+  e.cqq = kc.two_over_s;
+  e.cqp = -cd;
+  for (int k = 0; k < 4; ++k) e.out[k] = outs[k]->as<double>();
+  GS_TRY(bwd_epilogue(prec, e, c->stream));
+  double* hs[4] = {pq, pp, qq, qp};
+  for (int k = 0; k < 4; ++k) GS_TRY(d2h(c, hs[k], outs[k]->ptr, 3 * n));
+  GS_TRY(sync(c));
+  return GS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// shooting
+// ----------------------------------------------------------------------------
+gs_status gs_shoot_forward(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
+                           const double* p0, double* traj_q, double* traj_p, double* final_q,
+                           double* final_p, double* energy_out, gs_stats* stats) {
+  if (!c || !cfg || !q0 || !p0) return bad_arg("null argument");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  gs_flow* f = scratch_flow(c);
+  GS_TRY(flow_init(f, c, cfg, n));
+  GS_TRY(flow_upload(f, q0, p0));
+  f->want_energy = energy_out != nullptr;
+  const int T = cfg->timesteps;
+  const bool traj = traj_q || traj_p;
+  if (traj) {
+    GS_TRY(c->stage_c.ensure(sizeof(double) * 3 * n * (T + 1)));
+    GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n * (T + 1)));
+  }
+  Timer tm(c->stream);
+  for (int k = 0; k <= T; ++k) {
+    if (traj)
+      GS_TRY(unpack_records(f->prec, f->rec.ptr, n, c->stage_c.as<double>() + (size_t)3 * n * k,
+                            c->stage_d.as<double>() + (size_t)3 * n * k, c->stream));
+    if (k < T) {
+      for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
+      ++f->steps_done;
+    }
+  }
+  const double fwd_ms = tm.ms();
+  GS_TRY(flow_check(f));
+  if (traj) {
+    GS_TRY(d2h(c, traj_q, c->stage_c.ptr, 3 * n * (T + 1)));
+    GS_TRY(d2h(c, traj_p, c->stage_d.ptr, 3 * n * (T + 1)));
+  }
+  if (final_q || final_p) {
+    GS_TRY(c->stage_a.ensure(sizeof(double) * 3 * n));
+    GS_TRY(c->stage_b.ensure(sizeof(double) * 3 * n));
+    GS_TRY(unpack_records(f->prec, f->rec.ptr, n, c->stage_a.as<double>(), c->stage_b.as<double>(),
+                          c->stream));
+    GS_TRY(d2h(c, final_q, c->stage_a.ptr, 3 * n));
+    GS_TRY(d2h(c, final_p, c->stage_b.ptr, 3 * n));
+  }
+  GS_TRY(sync(c));
+  if (energy_out) GS_TRY(flow_energy(f, energy_out));
+  if (stats) {
+    *stats = f->stats;
+    GS_TRY(flow_bh_stats(f, stats));
+    stats->forward_ms = fwd_ms - f->stats.tree_build_ms;
+  }
+  return GS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Adjoint recursion over device-resident trajectory records traj[0..T]
+// (run_backward, shooting.cpp:143-240). dhdp0 must hold dH/dp(q0, p0).
+int backward_pass(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts& kc, int64_t n,
+                  const char* traj, size_t rec_bytes, const double* target_dev,
+                  const double* dhdp0, BhWork* bh, bool trees_cached, DBuf& adj, DBuf& part,
+                  double* grad_dev, double* sse_dev, gs_stats* stats) {
+  cudaStream_t st = c->stream;
+  const int T = cfg->timesteps;
+  const double dt = 1.0 / T;
+  GS_TRY(adj.ensure(rec_bytes));
+  GS_TRY(c->epart.ensure(sizeof(double) * (n / 128 + 8)));
+  int blocks = 0;
+  GS_TRY(adjoint_init(prec, traj + (size_t)T * rec_bytes, target_dev, cfg->lambda, n, adj.ptr,
+                      c->epart.as<double>(), &blocks, st));
+  if (sse_dev) GS_TRY(reduce_sum(c->epart.as<double>(), blocks, sse_dev, st));
+  const double cd = prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;
+  BwdEpi e;
+  e.n_tgt = (int)n;
+  e.adj = adj.ptr;
+  e.update = 1;
+  e.dt = dt;
+  e.cpq = -cd;
+  e.cpp = 2.0;
+  e.cqq = kc.two_over_s;
+  e.cqp = -cd;
+  for (int k = T - 1; k >= 0; --k) {
+    const void* rk = traj + (size_t)k * rec_bytes;
+    if (cfg->backend == GS_EXACT) {
+      GS_TRY(part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * n));
+      const int S = hess_partials(c->dev, prec, rk, adj.ptr, (int)n, 0, (int)n, kc, part.ptr,
+                                  kMaxChunks, st);
+      if (S < 0) return GS_INTERNAL;
+      GS_CUDA_OK(cudaGetLastError());
+      e.S = S;
+      e.part = part.ptr;
+      GS_TRY(bwd_epilogue(prec, e, st));
+      if (stats) {
+        stats->direct_interactions += (uint64_t)n * n;
+        stats->traversal_queries += n;
+      }
+    } else {
+      GS_TRY(bh_backward_step(c->dev, prec, kc, *cfg, rk, adj.ptr, n, k, *bh, trees_cached, e, st,
+                              stats));
+    }
+  }
+  GS_TRY(gradient_finalize(prec, adj.ptr, dhdp0, n, grad_dev, st));
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
+                      const double* p0, const double* target, gs_report* report,
+                      double* grad_out, gs_stats* stats) {
+  if (!c || !cfg || !q0 || !p0 || !target) return bad_arg("null argument");
+  if (cfg->integrator != GS_EULER) return bad_arg("evaluate: the adjoint is the transpose of Euler");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  const int T = cfg->timesteps;
+  gs_flow* f = scratch_flow(c);
+  GS_TRY(flow_init(f, c, cfg, n));
+  GS_TRY(flow_upload(f, q0, p0));
+  f->want_energy = true;
+  GS_TRY(h2d(c, c->stage_c, target, n));
+  const size_t rb = 2 * vec_bytes(f->prec) * n;
+  // trajectory records traj[0..T] resident in HBM
+  GS_TRY(c->rec_b.ensure(rb * (T + 1)));
+  char* traj = c->rec_b.as<char>();
+  GS_CUDA_OK(cudaMemcpyAsync(traj, f->rec.ptr, rb, cudaMemcpyDeviceToDevice, c->stream));
+  if (cfg->backend == GS_BARNES_HUT) GS_TRY(bh_keep_trees(f->bh, T));
+  Timer tf(c->stream);
+  for (int k = 0; k < T; ++k) {
+    // RHS reads traj[k]; the epilogue writes traj[k+1]
+    f->bh.cache_slot = cfg->backend == GS_BARNES_HUT ? k : -1;
+    const int s = flow_stage(f, 0, traj + (size_t)k * rb, traj + (size_t)(k + 1) * rb);
+    f->bh.cache_slot = -1;
+    GS_TRY(s);
+    ++f->steps_done;
+  }
+  const double fwd_ms = tf.ms();
+  GS_TRY(flow_check(f));
+  double energy = 0.0;
+  GS_TRY(flow_energy(f, &energy));
+  GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
+  GS_TRY(c->scal.ensure(64));
+  gs_stats bst{};
+  Timer tb(c->stream);
+  GS_TRY(backward_pass(c, cfg, f->prec, f->kc, n, traj, rb, c->stage_c.as<double>(),
+                       f->dhdp0.as<double>(), &f->bh, true, c->rec_a, c->part,
+                       c->stage_d.as<double>(), c->scal.as<double>() + 1, &bst));
+  const double bwd_ms = tb.ms();
+  double sse = 0.0;
+  GS_CUDA_OK(cudaMemcpyAsync(&sse, c->scal.as<double>() + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+  GS_TRY(d2h(c, grad_out, c->stage_d.ptr, 3 * n));
+  GS_TRY(sync(c));
+  if (report) {
+    report->energy = energy;
+    report->residual_sse = sse;
+    report->attachment = cfg->lambda * sse;
+    report->total = report->energy + report->attachment;
+  }
+  if (stats) {
+    *stats = f->stats;
+    GS_TRY(flow_bh_stats(f, stats));
+    stats->direct_interactions += bst.direct_interactions;
+    stats->approximated_interactions += bst.approximated_interactions;
+    stats->nodes_visited += bst.nodes_visited;
+    stats->traversal_queries += bst.traversal_queries;
+    // the energy-gradient term reuses the step-0 forward RHS (one more RHS in the reference)
+    stats->forward_ms = fwd_ms - f->stats.tree_build_ms;
+    stats->backward_ms = bwd_ms;
+  }
+  return GS_OK;
+}
+
+gs_status gs_objective(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
+                       const double* p0, const double* target, gs_report* report) {
+  if (!c || !cfg || !q0 || !p0 || !target || !report) return bad_arg("null argument");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  std::vector<double> fq((size_t)3 * n);
+  double energy = 0.0;
+  GS_TRY(gs_shoot_forward(c, cfg, n, q0, p0, nullptr, nullptr, fq.data(), nullptr, &energy,
+                          nullptr));
+  double sse = 0.0;  // make_report, shooting.cpp:126-138 (O(N) on the host copy)
+  for (int64_t i = 0; i < n; ++i) {
+    const double dx = fq[3 * i] - target[3 * i], dy = fq[3 * i + 1] - target[3 * i + 1],
+                 dz = fq[3 * i + 2] - target[3 * i + 2];
+    sse += dx * dx + dy * dy + dz * dz;
+  }
+  report->energy = energy;
+  report->residual_sse = sse;
+  report->attachment = cfg->lambda * sse;
+  report->total = report->energy + report->attachment;
+  return GS_OK;
+}
+
+gs_status gs_backward_gradient(gs_ctx* c, const gs_config* cfg, int64_t n, int32_t states,
+                               const double* traj_q, const double* traj_p, const double* target,
+                               double* grad_out) {
+  if (!c || !cfg || !traj_q || !traj_p || !target || !grad_out) return bad_arg("null argument");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  const int T = cfg->timesteps;
+  if (states != T + 1) {
+    g_err = "backward_gradient: trajectory length != timesteps + 1";
+    return GS_CONFIG_MISMATCH;
+  }
+  const int prec = cfg->precision == GS_F32 ? kF32 : kF64;
+  double c0[3];
+  bbox_center(traj_q, n, c0);
+  const KernelConsts kc = make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr);
+  const size_t rb = 2 * vec_bytes(prec) * n;
+  gs_flow* f = scratch_flow(c);
+  GS_TRY(flow_init(f, c, cfg, n));
+  DBuf& traj = c->rec_b;
+  GS_TRY(traj.ensure(rb * (T + 1)));
+  for (int k = 0; k <= T; ++k) {
+    DBuf tmp;
+    GS_TRY(upload_records(c, prec, traj_q + (size_t)3 * n * k, traj_p + (size_t)3 * n * k, n,
+                          c->rec_a));
+    GS_CUDA_OK(cudaMemcpyAsync(traj.as<char>() + (size_t)k * rb, c->rec_a.ptr, rb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+  }
+  GS_TRY(h2d(c, c->stage_c, target, n));
+  // dH/dp(q0, p0) for the energy term (shooting.cpp:217-234)
+  GS_TRY(f->dhdp0.ensure(sizeof(double) * 3 * n));
+  {
+    FwdEpi e;
+    e.rec = traj.ptr;
+    e.update = 0;
+    e.dhdp_out = f->dhdp0.as<double>();
+    if (cfg->backend == GS_EXACT) {
+      GS_TRY(exact_stage(c->dev, prec, kc, traj.ptr, n, 0, n, f->part, e, c->stream, nullptr,
+                         nullptr));
+    } else {
+      int blocks = 0;
+      int64_t l = 0;
+      GS_TRY(bh_forward_stage(c->dev, prec, kc, *cfg, traj.ptr, n, 0, n, f->bh, e, c->stream, &l,
+                              &blocks, nullptr));
+    }
+  }
+  GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
+  GS_TRY(backward_pass(c, cfg, prec, kc, n, traj.as<char>(), rb, c->stage_c.as<double>(),
+                       f->dhdp0.as<double>(), &f->bh, false, c->rec_a, c->part,
+                       c->stage_d.as<double>(), nullptr, nullptr));
+  GS_TRY(d2h(c, grad_out, c->stage_d.ptr, 3 * n));
+  GS_TRY(sync(c));
+  return GS_OK;
+}
+
+gs_status gs_warp_points(gs_ctx* c, const gs_config* cfg, int64_t n, int32_t states,
+                         const double* traj_q, const double* traj_p, int64_t m, const double* x,
+                         double* y_out) {
+  if (!c || !cfg || !traj_q || !traj_p || !x || !y_out) return bad_arg("null argument");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  GS_TRY(check_n(m));
+  const int T = cfg->timesteps;
+  if (states != T + 1) {
+    g_err = "warp_points: trajectory length != timesteps + 1";
+    return GS_CONFIG_MISMATCH;
+  }
+  const int prec = cfg->precision == GS_F32 ? kF32 : kF64;
+  double c0[3];
+  bbox_center(traj_q, n, c0);
+  const KernelConsts kc = make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr);
+  const size_t rb = 2 * vec_bytes(prec) * n;
+  DBuf& traj = c->rec_b;
+  GS_TRY(traj.ensure(rb * T));
+  for (int k = 0; k < T; ++k) {
+    GS_TRY(upload_records(c, prec, traj_q + (size_t)3 * n * k, traj_p + (size_t)3 * n * k, n,
+                          c->rec_a));
+    GS_CUDA_OK(cudaMemcpyAsync(traj.as<char>() + (size_t)k * rb, c->rec_a.ptr, rb,
+                               cudaMemcpyDeviceToDevice, c->stream));
+  }
+  DBuf ev;
+  GS_TRY(upload_records(c, prec, x, nullptr, m, ev));
+  GS_TRY(c->scal.ensure(64));
+  int* bad = c->scal.as<int>() + 4;
+  GS_CUDA_OK(cudaMemsetAsync(bad, 0x7f, sizeof(int), c->stream));
+  gs_flow* f = scratch_flow(c);
+  for (int k = 0; k < T; ++k) {
+    const void* rk = traj.as<char>() + (size_t)k * rb;
+    VelEpi e;
+    e.m = (int)m;
+    e.ev = ev.ptr;
+    e.scale = 2.0;  // flow_velocity_factor, kernel_exact.hpp:28
+    e.dt = 1.0 / T;
+    e.update = 1;
+    e.bad_step = bad;
+    e.step = k + 1;
+    if (cfg->backend == GS_EXACT) {
+      GS_TRY(c->part.ensure((size_t)kMaxChunks * vec_bytes(prec) * m));
+      const int S = vel_partials(c->dev, prec, rk, (int)n, ev.ptr, (int)m, kc, c->part.ptr,
+                                 kMaxChunks, c->stream);
+      if (S < 0) return (gs_status)GS_INTERNAL;
+      GS_CUDA_OK(cudaGetLastError());
+      e.S = S;
+      e.part = c->part.ptr;
+      GS_TRY(vel_epilogue(prec, e, c->stream));
+    } else {
+      GS_TRY(bh_velocity_step(c->dev, prec, kc, *cfg, rk, n, ev.ptr, m, f->bh, e, c->stream));
+    }
+  }
+  int hbad = 0;
+  GS_CUDA_OK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  GS_TRY(c->stage_a.ensure(sizeof(double) * 3 * m));
+  GS_TRY(unpack_records(prec, ev.ptr, m, c->stage_a.as<double>(), nullptr, c->stream));
+  GS_TRY(d2h(c, y_out, c->stage_a.ptr, 3 * m));
+  GS_TRY(sync(c));
+  if (hbad != 0x7f7f7f7f) {
+    g_nonfinite = hbad;
+    g_err = "non-finite state at timestep " + std::to_string(hbad);
+    return GS_NONFINITE;
+  }
+  return GS_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------
+// octree + bh_kernel entry points
+// ----------------------------------------------------------------------------
+struct gs_tree {
+  gs_ctx* ctx = nullptr;
+  int prec = kF64;
+  DevTree t;
+  DBuf rec;        // the build's records (index order)
+  DBuf adj;        // last annotation (index order)
+  DBuf part, outs, pq, stats;
+  double c0[3] = {0, 0, 0};
+  double sigma = -1.0;  // sigma the interaction coordinates are scaled for
+  int64_t last_queries = 0;
+};
+
+namespace {
+
+int tree_for_sigma(gs_tree* tr, double sigma) {
+  if (tr->prec == kF32 && sigma != tr->sigma) {
+    const KernelConsts kc = make_consts(sigma, tr->c0);
+    GS_TRY(tree_rescale(tr->prec, tr->t, tr->rec.ptr, kc, tr->ctx->stream));
+  }
+  tr->sigma = sigma;
+  tr->t.kc = make_consts(sigma, tr->prec == kF32 ? tr->c0 : nullptr);
+  return GS_OK;
+}
+
+int fill_stats(gs_tree* tr, gs_stats* stats, int64_t queries) {
+  if (!stats) return GS_OK;
+  unsigned long long v[3] = {0, 0, 0};
+  GS_CUDA_OK(cudaMemcpyAsync(v, tr->stats.ptr, sizeof v, cudaMemcpyDeviceToHost, tr->ctx->stream));
+  GS_TRY(sync(tr->ctx));
+  *stats = gs_stats{};
+  stats->direct_interactions = v[0];
+  stats->approximated_interactions = v[1];
+  stats->nodes_visited = v[2];
+  stats->traversal_queries = (uint64_t)queries;
+  return GS_OK;
+}
+
+// RHS traversal over all tree points -> dH/dp, dH/dq (device doubles) and optionally H
+int tree_rhs(gs_tree* tr, double sigma, double thr, double* dhdp_dev, double* dhdq_dev,
+             double* energy_part, int* blocks) {
+  gs_ctx* c = tr->ctx;
+  const int64_t n = tr->t.n;
+  GS_TRY(tree_for_sigma(tr, sigma));
+  GS_TRY(tr->part.ensure(2 * vec_bytes(tr->prec) * n));
+  GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * n));
+  GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
+  BhQuery q;
+  q.mode = kBhRhs;
+  q.tgt_begin = 0;
+  q.n_tgt = (int)n;
+  q.part = tr->part.ptr;
+  q.per_query = tr->pq.as<uint32_t>();
+  q.totals = tr->stats.as<unsigned long long>();
+  GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
+  FwdEpi e;
+  e.rec = tr->rec.ptr;
+  e.update = 0;
+  e.S = 1;
+  e.part = tr->part.ptr;
+  e.n_tgt = (int)n;
+  e.cp = 2.0;
+  e.cq = fwd_cq(tr->prec, tr->t.kc);
+  e.dhdp_out = dhdp_dev;
+  e.dhdq_out = dhdq_dev;
+  e.energy_part = energy_part;
+  GS_TRY(fwd_epilogue(tr->prec, e, c->stream, blocks));
+  tr->last_queries = n;
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+gs_status gs_tree_build(gs_ctx* c, int32_t precision, int64_t n, const double* q, const double* p,
+                        gs_tree** out) {
+  if (!c || !q || !p || !out) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  auto* tr = new gs_tree;
+  tr->ctx = c;
+  tr->prec = precision == GS_F32 ? kF32 : kF64;
+  bbox_center(q, n, tr->c0);
+  int s = upload_records(c, tr->prec, q, p, n, tr->rec);
+  if (s == GS_OK) {
+    const KernelConsts kc = make_consts(1.0, tr->prec == kF32 ? tr->c0 : nullptr);
+    tr->sigma = 1.0;
+    s = tree_build(c->dev, tr->prec, kc, tr->rec.ptr, n, tr->t, c->stream);
+  }
+  if (s == GS_OK) s = sync(c);
+  if (s != GS_OK) {
+    delete tr;
+    return (gs_status)s;
+  }
+  *out = tr;
+  return GS_OK;
+}
+
+void gs_tree_free(gs_tree* tr) {
+  if (!tr) return;
+  cudaStreamSynchronize(tr->ctx->stream);
+  delete tr;
+}
+
+int64_t gs_tree_node_count(const gs_tree* tr) { return tr ? tr->t.m : 0; }
+int64_t gs_tree_point_count(const gs_tree* tr) { return tr ? tr->t.n : 0; }
+
+gs_status gs_tree_accumulate_adjoints(gs_tree* tr, const double* alpha, const double* beta) {
+  if (!tr || !alpha || !beta) return bad_arg("null argument");
+  GS_TRY(upload_records(tr->ctx, tr->prec, alpha, beta, tr->t.n, tr->adj));
+  GS_TRY(tree_accumulate(tr->prec, tr->t, tr->adj.ptr, tr->ctx->stream));
+  return (gs_status)sync(tr->ctx);
+}
+
+gs_status gs_tree_download(const gs_tree* tr, int32_t* order, uint64_t* key_hi, uint64_t* key_lo,
+                           int32_t* level, int32_t* parent, int32_t* skip, int32_t* range,
+                           double* boxes, double* sums, uint32_t* count) {
+  if (!tr) return bad_arg("null tree");
+  return (gs_status)tree_download(tr->t, tr->ctx->stream, order, key_hi, key_lo, level, parent,
+                                  skip, range, boxes, sums, count);
+}
+
+gs_status gs_bh_rhs(gs_tree* tr, double sigma, double thr, double* dHdp, double* dHdq,
+                    gs_stats* stats) {
+  if (!tr) return bad_arg("null tree");
+  gs_ctx* c = tr->ctx;
+  const int64_t n = tr->t.n;
+  GS_TRY(tr->outs.ensure(sizeof(double) * 6 * n));
+  double* dp = tr->outs.as<double>();
+  GS_TRY(tree_rhs(tr, sigma, thr, dp, dp + 3 * n, nullptr, nullptr));
+  GS_TRY(d2h(c, dHdp, dp, 3 * n));
+  GS_TRY(d2h(c, dHdq, dp + 3 * n, 3 * n));
+  GS_TRY(sync(c));
+  return (gs_status)fill_stats(tr, stats, n);
+}
+
+gs_status gs_bh_hamiltonian(gs_tree* tr, double sigma, double thr, double* h_out, gs_stats* stats) {
+  if (!tr || !h_out) return bad_arg("null argument");
+  gs_ctx* c = tr->ctx;
+  const int64_t n = tr->t.n;
+  GS_TRY(c->epart.ensure(sizeof(double) * (n / 128 + 8)));
+  GS_TRY(c->scal.ensure(64));
+  int blocks = 0;
+  GS_TRY(tree_rhs(tr, sigma, thr, nullptr, nullptr, c->epart.as<double>(), &blocks));
+  GS_TRY(reduce_sum(c->epart.as<double>(), blocks, c->scal.as<double>(), c->stream));
+  double h = 0.0;
+  GS_CUDA_OK(cudaMemcpyAsync(&h, c->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  GS_TRY(sync(c));
+  // bh_hamiltonian = sum_j p_j . sum_units G P = 1/2 <p, dH/dp> (bh_kernel.cpp:162-191)
+  *h_out = 0.5 * h;
+  return (gs_status)fill_stats(tr, stats, n);
+}
+
+gs_status gs_bh_velocity(gs_tree* tr, int64_t m, const double* x, double sigma, double thr,
+                         double* v_out, gs_stats* stats) {
+  if (!tr || !x || !v_out) return bad_arg("null argument");
+  GS_TRY(check_n(m));
+  gs_ctx* c = tr->ctx;
+  GS_TRY(tree_for_sigma(tr, sigma));
+  DBuf ev;
+  GS_TRY(upload_records(c, tr->prec, x, nullptr, m, ev));
+  GS_TRY(tr->part.ensure(vec_bytes(tr->prec) * m));
+  GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * m));
+  GS_TRY(tr->outs.ensure(sizeof(double) * 3 * m));
+  GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
+  BhQuery q;
+  q.mode = kBhVel;
+  q.ev = ev.ptr;
+  q.m = (int)m;
+  q.part = tr->part.ptr;
+  q.per_query = tr->pq.as<uint32_t>();
+  q.totals = tr->stats.as<unsigned long long>();
+  GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
+  VelEpi e;
+  e.m = (int)m;
+  e.S = 1;
+  e.part = tr->part.ptr;
+  e.scale = 1.0;
+  e.v_out = tr->outs.as<double>();
+  GS_TRY(vel_epilogue(tr->prec, e, c->stream));
+  GS_TRY(d2h(c, v_out, tr->outs.ptr, 3 * m));
+  GS_TRY(sync(c));
+  tr->last_queries = m;
+  return (gs_status)fill_stats(tr, stats, m);
+}
+
+gs_status gs_bh_query_stats(const gs_tree* tr, uint64_t* per_query) {
+  if (!tr || !per_query) return bad_arg("null argument");
+  std::vector<uint32_t> v((size_t)3 * tr->last_queries);
+  if (!v.empty()) {
+    GS_CUDA_OK(cudaMemcpyAsync(v.data(), tr->pq.ptr, sizeof(uint32_t) * v.size(),
+                               cudaMemcpyDeviceToHost, tr->ctx->stream));
+    GS_TRY(sync(tr->ctx));
+  }
+  for (size_t i = 0; i < v.size(); ++i) per_query[i] = v[i];
+  return GS_OK;
+}
+
+gs_status gs_bh_hessian_products(gs_tree* tr, const double* alpha, const double* beta,
+                                 double sigma, double thr, double* pq, double* pp, double* qq,
+                                 double* qp, gs_stats* stats) {
+  if (!tr || !alpha || !beta) return bad_arg("null argument");
+  gs_ctx* c = tr->ctx;
+  const int64_t n = tr->t.n;
+  GS_TRY(tree_for_sigma(tr, sigma));
+  DBuf adj;
+  GS_TRY(upload_records(c, tr->prec, alpha, beta, n, adj));
+  if (!tr->t.adj_valid) GS_TRY(tree_accumulate(tr->prec, tr->t, adj.ptr, c->stream));
+  else GS_TRY(tree_set_point_adjoints(tr->prec, tr->t, adj.ptr, c->stream));
+  GS_TRY(tr->part.ensure(4 * vec_bytes(tr->prec) * n));
+  GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->outs.ensure(sizeof(double) * 12 * n));
+  GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
+  BhQuery q;
+  q.mode = kBhHess;
+  q.tgt_begin = 0;
+  q.n_tgt = (int)n;
+  q.part = tr->part.ptr;
+  q.totals = tr->stats.as<unsigned long long>();
+  GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
+  const KernelConsts& kc = tr->t.kc;
+  const double cd = tr->prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;
+  BwdEpi e;
+  e.n_tgt = (int)n;
+  e.S = 1;
+  e.part = tr->part.ptr;
+  e.update = 0;
+  e.cpq = -cd;
+  e.cpp = 2.0;
+  e.cqq = kc.two_over_s;
+  e.cqp = -cd;
+  double* o = tr->outs.as<double>();
+  for (int k = 0; k < 4; ++k) e.out[k] = o + (size_t)3 * n * k;
+  GS_TRY(bwd_epilogue(tr->prec, e, c->stream));
+  double* hs[4] = {pq, pp, qq, qp};
+  for (int k = 0; k < 4; ++k) GS_TRY(d2h(c, hs[k], o + (size_t)3 * n * k, 3 * n));
+  GS_TRY(sync(c));
+  tr->last_queries = n;
+  return (gs_status)fill_stats(tr, stats, n);
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// engine.h -- internal interfaces between the C-ABI (capi.cu) and the kernels.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "gs_common.cuh"
+#include "geoshoot_b200.h"
+
+namespace gsb {
+
+enum { kF64 = GS_F64, kF32 = GS_F32 };
+
+struct Device {
+  int id = 0;
+  int sms = 148;
+};
+
+#define GS_TRY_INT(expr)        \
+  do {                          \
+    const int s__ = (expr);     \
+    if (s__ != GS_OK) return s__; \
+  } while (0)
+
+// Records the failing call in the thread's error slot; returns GS_CUDA_ERROR.
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+void set_error(const std::string& msg);
+
+// Growable device buffer (cudaMalloc, never shrinks).
+struct DBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need);
+  void release();
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+  ~DBuf() { release(); }
+};
+
+inline size_t vec_bytes(int prec) { return prec == kF32 ? sizeof(float4) : sizeof(double4); }
+
+// ---- all-pairs (allpairs.cu); return the number of source chunks S used,
+// ---- or -1 if S would exceed part_cap_chunks.
+int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st);
+int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
+                  int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
+                  int part_cap_chunks, cudaStream_t st);
+int vel_partials(const Device& dev, int prec, const void* rec, int n, const void* ev, int m,
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st);
+constexpr int kMaxChunks = 16;
+
+// ---- epilogues (epilogue.cu) -----------------------------------------------
+// Forward stage epilogue: folds partials A = sum g p, B = sum c d (per target),
+// forms dH/dp = cp * A, dH/dq = cq * B and applies the integrator.
+struct FwdEpi {
+  int n_tgt = 0, tgt_begin = 0, S = 1, parts_per_tgt = 2;
+  const void* part = nullptr;
+  void* rec = nullptr;      // [n][2] records read for the targets
+  void* rec_out = nullptr;  // where updated target records go (nullptr = rec, in place)
+  void* y = nullptr;    // RK4: step-start records
+  void* ks = nullptr;   // RK4: k1 + 2 k2 + 2 k3 (+ k4)
+  int integrator = GS_EULER, stage = 0, update = 1;
+  double dt = 0.0, cp = 2.0, cq = 0.0;
+  double* dhdp_out = nullptr;  // optional double[3 n_tgt]
+  double* dhdq_out = nullptr;
+  double* energy_part = nullptr;  // optional per-block partial of <p, dH/dp>
+  int* bad_step = nullptr;        // atomicMin on non-finite output
+  int step = 0;                   // step index (1-based) reported on non-finite
+};
+int fwd_epilogue(int prec, const FwdEpi& e, cudaStream_t st, int* blocks_out);
+
+struct BwdEpi {
+  int n_tgt = 0, tgt_begin = 0, S = 1;
+  const void* part = nullptr;
+  void* adj = nullptr;  // [n][2] (alpha, beta) updated in place when update != 0
+  int update = 1;
+  double dt = 0.0, cpq = 0.0, cpp = 2.0, cqq = 0.0, cqp = 0.0;
+  double* out[4] = {nullptr, nullptr, nullptr, nullptr};  // pq, pp, qq, qp (optional)
+};
+int bwd_epilogue(int prec, const BwdEpi& e, cudaStream_t st);
+
+// Velocity epilogue: v = scale * sum partials; either written out (double) or
+// used to advect eval records y += dt * v in place.
+struct VelEpi {
+  int m = 0, S = 1;
+  const void* part = nullptr;
+  void* ev = nullptr;
+  double scale = 1.0, dt = 0.0;
+  int update = 0;
+  double* v_out = nullptr;
+  int* bad_step = nullptr;
+  int step = 0;
+};
+int vel_epilogue(int prec, const VelEpi& e, cudaStream_t st);
+
+// pack host-layout doubles [n][3] (device copy) into records; flags non-finite
+int pack_records(int prec, const double* q, const double* p, int64_t n, void* rec, int* bad,
+                 cudaStream_t st);
+int unpack_records(int prec, const void* rec, int64_t n, double* q, double* p, cudaStream_t st);
+// grad[i] = beta_i + dhdp0[i]
+int gradient_finalize(int prec, const void* adj, const double* dhdp0, int64_t n, double* grad,
+                      cudaStream_t st);
+// alpha = 2 lambda (q_T - target), beta = 0
+int adjoint_init(int prec, const void* rec_T, const double* target, double lambda, int64_t n,
+                 void* adj, double* sse_part, int* blocks, cudaStream_t st);
+int reduce_sum(const double* part, int count, double* out, cudaStream_t st);
+
+}  // namespace gsb

@@ -1,0 +1,90 @@
+// gs_common.cuh -- shared device types and helpers for the sm_100a kernels.
+//
+// Layout in HBM: every point is a record of two 4-vectors
+// {q.x, q.y, q.z, 0 | p.x, p.y, p.z, 0} in the working precision (32 B in
+// FP32, 64 B in FP64). Records are the integrator state, the all-pairs source
+// tiles and the unit of the multi-GPU all-gather. The pad lane keeps every
+// load a single 16-B (FP32) or two 16-B (FP64) vector transaction.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+namespace gsb {
+
+constexpr double kLog2e = 1.4426950408889634073599246810019;
+
+template <typename R> struct V4T;
+template <> struct V4T<float> { using type = float4; };
+template <> struct V4T<double> { using type = double4; };
+template <typename R> using V4 = typename V4T<R>::type;
+
+template <typename R>
+__host__ __device__ inline V4<R> mk4(R x, R y, R z, R w = R(0)) {
+  V4<R> v; v.x = x; v.y = y; v.z = z; v.w = w; return v;
+}
+
+// Loads a 4-vector as 16-B vector transactions (double4 = 2 x 16 B).
+__device__ __forceinline__ float4 ld4(const float4* p) { return *p; }
+__device__ __forceinline__ double4 ld4(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1];
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void st4(double4* p, double4 v) {
+  double2* q = reinterpret_cast<double2*>(p);
+  q[0] = make_double2(v.x, v.y);
+  q[1] = make_double2(v.z, v.w);
+}
+
+// exp2 on the SFU: one MUFU.EX2, flush-to-zero (underflow -> 0 is exactly the
+// behaviour wanted for far pairs).
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Per-call constants of the Gaussian kernel G(r) = exp(-r^2 / (2 sigma^2)).
+// FP32 kernels work in pre-scaled coordinates x' = kappa (x - c0) with
+// kappa^2 = log2(e) / (2 s), so that G = 2^(-|x'_i - x'_j|^2): one MUFU.EX2 per
+// pair and no per-pair multiply. c0 (the centre of the
+// initial bounding box) keeps |x'| small so the FP32 differences stay sharp.
+// FP64 kernels use unscaled coordinates and the reference's own expression
+// exp(-|d|^2 * inv_two_s) (kernel_exact.cpp:7-9).
+struct KernelConsts {
+  double sigma, s, inv_s, inv_two_s, two_over_s;
+  double kappa;        // sqrt(log2e / (2 s))
+  double c0[3];        // FP32 centring
+};
+
+inline KernelConsts make_consts(double sigma, const double* c0) {
+  KernelConsts k;
+  k.sigma = sigma;
+  k.s = sigma * sigma;
+  k.inv_s = 1.0 / k.s;
+  k.inv_two_s = 1.0 / (2.0 * k.s);
+  k.two_over_s = 2.0 / k.s;
+  k.kappa = __builtin_sqrt(kLog2e / (2.0 * k.s));
+  for (int a = 0; a < 3; ++a) k.c0[a] = c0 ? c0[a] : 0.0;
+  return k;
+}
+
+// Converts to int or to gs_status so the macro works in both kinds of function.
+struct StatusCode {
+  int v;
+  operator int() const { return v; }
+  template <typename E, typename = typename std::enable_if<std::is_enum<E>::value>::type>
+  operator E() const { return static_cast<E>(v); }
+};
+
+#define GS_CUDA_OK(expr)                                               \
+  do {                                                                 \
+    cudaError_t e__ = (expr);                                          \
+    if (e__ != cudaSuccess)                                            \
+      return ::gsb::StatusCode{::gsb::cuda_fail(e__, #expr, __FILE__, __LINE__)}; \
+  } while (0)
+
+}  // namespace gsb

@@ -1,0 +1,773 @@
+// tree.cu -- octree build on sm_100a: bbox -> midpoint-replay Morton keys ->
+// LSD radix sort -> radix-tree topology collapsed to the reference octree ->
+// bottom-up aggregates.
+//
+// The reference builds its octree by sequential pointer insertion
+// (octree.cpp:74-117). Its node set is fully determined by the points:
+//   * the root cell is the bounding box padded by 1e-9 * extent (octree.cpp:9,25-40);
+//   * a child cell is an octant of its parent's cell split at the FP64
+//     midpoint c = 0.5 * (lo + hi), points on the plane going high
+//     (octant_of :42-45, make_child :59-72);
+//   * a cell exists iff it is the root, or its parent holds >= 2 points and it
+//     holds >= 1; it is a leaf iff it holds 1 point or sits at depth 32
+//     (bucket, :93-97).
+// So with key = the 3-bit octant digits of every level (replayed per axis in
+// FP64 exactly as the reference computes them), the cells are the distinct
+// key prefixes shared by >= 2 points plus one leaf per point (or bucket), and
+// a depth-first walk of the reference tree with children 0..7 visits the
+// points in sorted-key order. With L[t] = common digits of sorted keys t and
+// t+1, position a starts the internal nodes of levels L[a-1]+1 .. min(L[a],31)
+// and one leaf; ordering nodes by (start, level) is the depth-first pre-order.
+// Everything below is that construction, one thread per position/node.
+#include "bh.h"
+
+namespace gsb {
+
+namespace {
+
+constexpr int kNT = 256;
+
+inline int nblocks(int64_t n, int nt) { return (int)std::max<int64_t>(1, (n + nt - 1) / nt); }
+
+// ------------------------------------------------------------------ bbox ---
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, double* part) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const V4<R> q = ld4(rec + 2 * i);
+    const double v[3] = {(double)q.x, (double)q.y, (double)q.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fmin(lo[a], v[a]);
+      hi[a] = fmax(hi[a], v[a]);
+    }
+  }
+  __shared__ double s[6][kNT / 32];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s[a][threadIdx.x >> 5] = lo[a];
+      s[3 + a][threadIdx.x >> 5] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double r = s[threadIdx.x][0];
+    for (int w = 1; w < kNT / 32; ++w)
+      r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][w]) : fmax(r, s[threadIdx.x][w]);
+    part[6 * blockIdx.x + threadIdx.x] = r;
+  }
+}
+
+// root = [lo - pad, hi + pad], pad = 1e-9 * (hi - lo)   (octree.cpp:9,27-35)
+__global__ void k_bbox_final(const double* part, int nb, double* root) {
+  if (threadIdx.x >= 3) return;
+  const int a = threadIdx.x;
+  double lo = part[a], hi = part[3 + a];
+  for (int b = 1; b < nb; ++b) {
+    lo = fmin(lo, part[6 * b + a]);
+    hi = fmax(hi, part[6 * b + 3 + a]);
+  }
+  const double pad = __dmul_rn(__dsub_rn(hi, lo), 1e-9);
+  root[a] = __dsub_rn(lo, pad);
+  root[3 + a] = __dadd_rn(hi, pad);
+}
+
+// ------------------------------------------------------------------ keys ---
+// Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo.
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
+                                              uint64_t* kh, uint64_t* kl, int* idx) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= n) return;
+  const V4<R> q = ld4(rec + 2 * i);
+  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
+  double lo[3] = {root[0], root[1], root[2]}, hi[3] = {root[3], root[4], root[5]};
+  uint64_t h = 0, l = 0;
+#pragma unroll
+  for (int lev = 1; lev <= 32; ++lev) {
+    unsigned dig = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[a], hi[a]));
+      const bool up = x[a] >= c;
+      lo[a] = up ? c : lo[a];
+      hi[a] = up ? hi[a] : c;
+      dig |= (unsigned)up << a;
+    }
+    if (lev <= 21) h = (h << 3) | dig;
+    else l = (l << 3) | dig;
+  }
+  kh[i] = h;
+  kl[i] = l;
+  idx[i] = (int)i;
+}
+
+// ------------------------------------------------------------ radix sort ---
+// Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, 3 kernels per
+// pass: per-tile digit histograms, one exclusive scan (digit-major), and a
+// stable scatter that ranks keys inside a tile with warp match/popc.
+constexpr int kRsNT = 256, kRsIPT = 16, kRsTile = kRsNT * kRsIPT;
+
+__global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t* keys, int64_t n, int shift,
+                                                  unsigned* ghist, int ntiles) {
+  __shared__ unsigned h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRsTile;
+#pragma unroll 4
+  for (int r = 0; r < kRsIPT; ++r) {
+    const int64_t i = base + r * kRsNT + threadIdx.x;
+    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  ghist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
+__global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
+  __shared__ unsigned sums[1024];
+  const int64_t per = (count + 1023) / 1024;
+  const int64_t b = threadIdx.x * per, e = min(count, b + per);
+  unsigned s = 0;
+  for (int64_t i = b; i < e; ++i) s += a[i];
+  sums[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned v = threadIdx.x >= o ? sums[threadIdx.x - o] : 0u;
+    __syncthreads();
+    sums[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned run = sums[threadIdx.x] - s;
+  for (int64_t i = b; i < e; ++i) {
+    const unsigned v = a[i];
+    a[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const int* vin,
+                                                     uint64_t* kout, int* vout, int64_t n,
+                                                     int shift, const unsigned* ghist,
+                                                     int ntiles) {
+  __shared__ unsigned wh[kRsNT / 32][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t seg = (int64_t)blockIdx.x * kRsTile + (int64_t)warp * (32 * kRsIPT);
+  uint64_t key[kRsIPT];
+  int val[kRsIPT];
+  unsigned loc[kRsIPT];
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    const int64_t i = seg + r * 32 + lane;
+    const bool ok = i < n;
+    key[r] = ok ? kin[i] : 0ull;
+    val[r] = ok ? vin[i] : 0;
+    const unsigned d = (unsigned)(key[r] >> shift) & 255u;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    loc[r] = 0;
+    if (ok) {
+      const unsigned peers = __match_any_sync(act, d);
+      const int leader = __ffs(peers) - 1;
+      const unsigned cnt = __popc(peers);
+      const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+      if (lane == leader) wh[warp][d] += cnt;
+      __syncwarp(act);
+      loc[r] = wh[warp][d] - cnt + rank;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const unsigned d = threadIdx.x;
+    unsigned run = ghist[(int64_t)d * ntiles + blockIdx.x];
+    for (int w = 0; w < kRsNT / 32; ++w) {
+      const unsigned t = wh[w][d];
+      wh[w][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    const int64_t i = seg + r * 32 + lane;
+    if (i < n) {
+      const unsigned d = (unsigned)(key[r] >> shift) & 255u;
+      const unsigned pos = wh[warp][d] + loc[r];
+      kout[pos] = key[r];
+      vout[pos] = val[r];
+    }
+  }
+}
+
+// Points whose 63-bit keys tie: order the (rare, short) run by the deeper
+// digits, then by index (bucket members are equivalent; ascending index).
+__global__ void k_fix_ties(const uint64_t* skh, int* perm, const uint64_t* kl, int64_t n) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t >= n) return;
+  if (t > 0 && skh[t] == skh[t - 1]) return;
+  int64_t e = t;
+  while (e + 1 < n && skh[e + 1] == skh[t]) ++e;
+  if (e == t) return;
+  for (int64_t a = t + 1; a <= e; ++a) {
+    const int v = perm[a];
+    const uint64_t kv = kl[v];
+    int64_t b = a - 1;
+    while (b >= t && (kl[perm[b]] > kv || (kl[perm[b]] == kv && perm[b] > v))) {
+      perm[b + 1] = perm[b];
+      --b;
+    }
+    perm[b + 1] = v;
+  }
+}
+
+// ------------------------------------------------------------- topology ---
+__device__ __forceinline__ int lcp_digits(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
+  const uint64_t x = ah ^ bh;
+  if (x) return (__clzll((long long)x) - 1) / 3;
+  const uint64_t y = al ^ bl;
+  if (y) return 21 + (__clzll((long long)y) - 31) / 3;
+  return 32;
+}
+
+__global__ void k_gather_lo_lcp(const int* perm, const uint64_t* kl, const uint64_t* skh,
+                                uint64_t* skl, int64_t n) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t < n) skl[t] = kl[perm[t]];
+}
+
+__device__ __forceinline__ int lm_of(const int* L, int64_t a) { return a > 0 ? L[a - 1] : -1; }
+
+__global__ void k_lcp(const uint64_t* skh, const uint64_t* skl, int64_t n, int* L) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t + 1 < n) L[t] = lcp_digits(skh[t], skl[t], skh[t + 1], skl[t + 1]);
+}
+
+// nodes starting at position a: internal levels (Lm, min(Lp,31)] + one leaf
+// unless a continues a depth-32 bucket.
+__device__ __forceinline__ void starts(const int* L, int64_t n, int64_t a, int& Lm, int& Lp,
+                                       int& cint, int& leaf) {
+  Lm = lm_of(L, a);
+  Lp = a + 1 < n ? L[a] : -1;
+  cint = max(0, min(Lp, 31) - Lm);
+  leaf = Lm < 32 ? 1 : 0;
+}
+
+__global__ void k_count(const int* L, int64_t n, int* cnt) {
+  const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (a >= n) return;
+  int Lm, Lp, ci, lf;
+  starts(L, n, a, Lm, Lp, ci, lf);
+  cnt[a] = ci + lf;
+}
+
+// largest b >= a with lcp(a, b) >= l
+__device__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t n, int64_t a,
+                                int l) {
+  const uint64_t ah = kh[a], al = kl[a];
+  int64_t step = 1, good = a;
+  while (a + step < n && lcp_digits(ah, al, kh[a + step], kl[a + step]) >= l) {
+    good = a + step;
+    step <<= 1;
+  }
+  int64_t lo = good, hi = min(n - 1, a + step);  // lo good, (hi bad or end)
+  while (hi > lo) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (lcp_digits(ah, al, kh[mid], kl[mid]) >= l) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// smallest s <= a with lcp(s, a) >= l
+__device__ int64_t search_left(const uint64_t* kh, const uint64_t* kl, int64_t a, int l) {
+  const uint64_t ah = kh[a], al = kl[a];
+  int64_t step = 1, good = a;
+  while (a - step >= 0 && lcp_digits(ah, al, kh[a - step], kl[a - step]) >= l) {
+    good = a - step;
+    step <<= 1;
+  }
+  int64_t hi = good, lo = max((int64_t)0, a - step);
+  while (hi > lo) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (lcp_digits(ah, al, kh[mid], kl[mid]) >= l) hi = mid;
+    else lo = mid + 1;
+  }
+  return hi;
+}
+
+__device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
+                         int64_t a, int plevel) {
+  const int64_t s = search_left(kh, kl, a, plevel);
+  return first[s] + (plevel - (lm_of(L, s) + 1));
+}
+
+__global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
+                        int64_t n, int4* meta, int* parent) {
+  const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (a >= n) return;
+  int Lm, Lp, ci, lf;
+  starts(L, n, a, Lm, Lp, ci, lf);
+  const int base = first[a];
+  const int l0 = Lm + 1;
+  for (int k = 0; k < ci; ++k) {
+    const int l = l0 + k;
+    const int idx = base + k;
+    const int64_t b = search_right(kh, kl, n, a, l);
+    meta[idx] = make_int4(first[b + 1], (int)a, (int)b, l << 8);
+    parent[idx] = l == 0 ? -1 : (k > 0 ? idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
+  }
+  if (lf) {
+    const int idx = base + ci;
+    int level;
+    int64_t b = a;
+    if (Lp == 32) {
+      level = 32;
+      b = search_right(kh, kl, n, a, 32);
+    } else {
+      level = max(Lm, Lp) + 1;
+    }
+    meta[idx] = make_int4(first[b + 1], (int)a, (int)b, (level << 8) | 1);
+    parent[idx] = level == 0 ? -1 : (level - 1 >= l0 ? idx - 1 : parent_of(kh, kl, L, first, a, level - 1));
+  }
+}
+
+__global__ void k_nchild(const int4* meta, int64_t m, int* nchild) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= m) return;
+  const int4 mi = meta[i];
+  int c = 0;
+  if (!(mi.w & 1))
+    for (int ch = (int)i + 1; ch < mi.x; ch = meta[ch].x) ++c;
+  nchild[i] = c;
+}
+
+// ------------------------------------------------------------ aggregates ---
+// Forward: tight AABB + sums of q and p; backward: sums of alpha and beta.
+// Leaves sum their points in leaf order; an internal node is completed by the
+// last child to arrive (atomic counter) as the sum of its children in child
+// order -- deterministic whatever the arrival order.
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_gather(const V4<R>* rec, const int* perm, int64_t n,
+                                                double kap, double c0x, double c0y, double c0z,
+                                                int scaled, V4<R>* srec, V4<R>* squ) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t >= n) return;
+  const int i = perm[t];
+  const V4<R> q = ld4(rec + 2 * i), p = ld4(rec + 2 * i + 1);
+  st4(squ + t, q);
+  V4<R> qs = q;
+  if (scaled) {  // FP32 interaction coordinates, same rounding as the all-pairs path
+    const float kf = (float)kap;
+    qs = mk4<R>((R)fmaf(kf, (float)q.x, -(float)(kap * c0x)), (R)fmaf(kf, (float)q.y, -(float)(kap * c0y)),
+                (R)fmaf(kf, (float)q.z, -(float)(kap * c0z)));
+  }
+  st4(srec + 2 * t, qs);
+  st4(srec + 2 * t + 1, p);
+}
+
+template <typename R>
+__global__ void k_gather_adj(const V4<R>* adj, const int* perm, int64_t n, V4<R>* sadj) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t >= n) return;
+  const int i = perm[t];
+  st4(sadj + 2 * t, ld4(adj + 2 * i));
+  st4(sadj + 2 * t + 1, ld4(adj + 2 * i + 1));
+}
+
+__device__ __forceinline__ double4 ldcg4(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldcg(q), b = __ldcg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 ldcg4(const float4* p) { return __ldcg(p); }
+
+// mode 0: forward (lo, hi, psum, msum from squ/srec p); mode 1: adjoint sums
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64_t n,
+                                                   const int* first, const int4* meta,
+                                                   const int* parent, const int* nchild,
+                                                   int* counter, const V4<R>* squ,
+                                                   const V4<R>* srec, const V4<R>* sadj,
+                                                   V4<R>* lo, V4<R>* hi, double4* s0, double4* s1) {
+  const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (a >= n) return;
+  int Lm, Lp, ci, lf;
+  starts(L, n, a, Lm, Lp, ci, lf);
+  if (!lf) return;
+  int node = first[a] + ci;
+  {
+    const int4 mi = meta[node];
+    double4 A = make_double4(0, 0, 0, 0), B = A;
+    V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
+    for (int t = mi.y; t <= mi.z; ++t) {
+      if (mode == 0) {
+        const V4<R> q = ld4(squ + t), p = ld4(srec + 2 * t + 1);
+        l.x = min(l.x, q.x); l.y = min(l.y, q.y); l.z = min(l.z, q.z);
+        h.x = max(h.x, q.x); h.y = max(h.y, q.y); h.z = max(h.z, q.z);
+        A.x += q.x; A.y += q.y; A.z += q.z;
+        B.x += p.x; B.y += p.y; B.z += p.z;
+      } else {
+        const V4<R> al = ld4(sadj + 2 * t), be = ld4(sadj + 2 * t + 1);
+        A.x += al.x; A.y += al.y; A.z += al.z;
+        B.x += be.x; B.y += be.y; B.z += be.z;
+      }
+    }
+    if (mode == 0) { st4(lo + node, l); st4(hi + node, h); }
+    s0[node] = A;
+    s1[node] = B;
+  }
+  for (;;) {
+    const int par = parent[node];
+    if (par < 0) return;
+    __threadfence();
+    const int old = atomicAdd(counter + par, 1);
+    if (old != nchild[par] - 1) return;
+    __threadfence();
+    const int end = meta[par].x;
+    double4 A = make_double4(0, 0, 0, 0), B = A;
+    V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
+    for (int ch = par + 1; ch < end; ch = meta[ch].x) {
+      const double4 a0 = ldcg4(s0 + ch), a1 = ldcg4(s1 + ch);
+      A.x += a0.x; A.y += a0.y; A.z += a0.z;
+      B.x += a1.x; B.y += a1.y; B.z += a1.z;
+      if (mode == 0) {
+        const V4<R> cl = ldcg4(lo + ch), chh = ldcg4(hi + ch);
+        l.x = min(l.x, cl.x); l.y = min(l.y, cl.y); l.z = min(l.z, cl.z);
+        h.x = max(h.x, chh.x); h.y = max(h.y, chh.y); h.z = max(h.z, chh.z);
+      }
+    }
+    if (mode == 0) { st4(lo + par, l); st4(hi + par, h); }
+    s0[par] = A;
+    s1[par] = B;
+    node = par;
+  }
+}
+
+// traversal-format node fields: centroid = position_sum * (1 / count)
+// (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
+template <typename R>
+__global__ void k_finalize(int mode, const int4* meta, int64_t m, const double4* s0,
+                           const double4* s1, double kap, double c0x, double c0y, double c0z,
+                           int scaled, V4<R>* o0, V4<R>* o1) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= m) return;
+  const int4 mi = meta[i];
+  const int cnt = mi.z - mi.y + 1;
+  const double inv = 1.0 / cnt;
+  const double4 a = s0[i], b = s1[i];
+  if (mode == 0) {
+    double cx = __dmul_rn(a.x, inv), cy = __dmul_rn(a.y, inv), cz = __dmul_rn(a.z, inv);
+    if (scaled) {
+      const float kf = (float)kap;
+      st4(o0 + i, mk4<R>((R)fmaf(kf, (float)cx, -(float)(kap * c0x)),
+                         (R)fmaf(kf, (float)cy, -(float)(kap * c0y)),
+                         (R)fmaf(kf, (float)cz, -(float)(kap * c0z)), R(cnt)));
+    } else {
+      st4(o0 + i, mk4<R>(R(cx), R(cy), R(cz), R(cnt)));
+    }
+    st4(o1 + i, mk4<R>(R(b.x), R(b.y), R(b.z)));
+  } else {
+    st4(o0 + i, mk4<R>(R(a.x), R(a.y), R(a.z)));
+    // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
+    st4(o1 + i, mk4<R>(R(__dmul_rn(inv, b.x)), R(__dmul_rn(inv, b.y)), R(__dmul_rn(inv, b.z))));
+  }
+}
+
+// cell box of a node: replay its key prefix from the root box
+__global__ void k_cells(const int4* meta, int64_t m, const uint64_t* skh, const uint64_t* skl,
+                        const double* root, double* boxes) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= m) return;
+  const int4 mi = meta[i];
+  const int level = mi.w >> 8;
+  const uint64_t h = skh[mi.y], l = skl[mi.y];
+  double lo[3] = {root[0], root[1], root[2]}, hi[3] = {root[3], root[4], root[5]};
+  for (int lev = 1; lev <= level; ++lev) {
+    const unsigned dig = lev <= 21 ? (unsigned)(h >> (3 * (21 - lev))) & 7u
+                                   : (unsigned)(l >> (3 * (32 - lev))) & 7u;
+    for (int a = 0; a < 3; ++a) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[a], hi[a]));
+      if ((dig >> a) & 1u) lo[a] = c;
+      else hi[a] = c;
+    }
+  }
+  for (int a = 0; a < 3; ++a) {
+    boxes[12 * i + a] = lo[a];
+    boxes[12 * i + 3 + a] = hi[a];
+  }
+}
+
+// int exclusive scan (n + 1 outputs: out[n] = total), 3 phases
+__global__ void __launch_bounds__(1024) k_scan_blocks(const int* in, int64_t n, int* out, int* bsum) {
+  __shared__ int s[1024];
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  const int v = i < n ? in[i] : 0;
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (i < n) out[i] = s[threadIdx.x] - v;
+  if (threadIdx.x == 1023) bsum[blockIdx.x] = s[1023];
+}
+
+__global__ void k_scan_add(int* out, int64_t n, const int* bsum_scanned, int nb) {
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  if (i < n && blockIdx.x > 0) out[i] += bsum_scanned[blockIdx.x];
+  if (i == 0) out[n] = bsum_scanned[nb];
+}
+
+}  // namespace
+
+int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st);
+
+// exclusive scan of n ints into out[0..n] (out[n] = total); bsum scratch
+static int scan_ints(const int* in, int64_t n, int* out, DBuf& scratch, cudaStream_t st) {
+  const int nb = nblocks(n, 1024);
+  GS_TRY_INT(scratch.ensure(sizeof(unsigned) * (nb + 2)));
+  unsigned* bs = scratch.as<unsigned>();
+  k_scan_blocks<<<nb, 1024, 0, st>>>(in, n, out, (int*)bs);
+  // scan the block sums (nb + 1 entries, last = 0 -> becomes the total)
+  GS_CUDA_OK(cudaMemsetAsync(bs + nb, 0, sizeof(unsigned), st));
+  k_rs_scan<<<1, 1024, 0, st>>>(bs, nb + 1);
+  k_scan_add<<<nb, 1024, 0, st>>>(out, n, (const int*)bs, nb);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
+               DevTree& t, cudaStream_t st) {
+  t.prec = prec;
+  t.n = n;
+  t.kc = kc;
+  t.adj_valid = false;
+  const size_t vb = vec_bytes(prec);
+  GS_TRY_INT(t.key_hi.ensure(8 * n));
+  GS_TRY_INT(t.key_lo.ensure(8 * n));
+  GS_TRY_INT(t.perm.ensure(4 * n));
+  GS_TRY_INT(t.skey_hi.ensure(8 * n));
+  GS_TRY_INT(t.skey_lo.ensure(8 * n));
+  GS_TRY_INT(t.lcp.ensure(4 * (n + 1)));
+  GS_TRY_INT(t.first.ensure(4 * (n + 2)));
+  GS_TRY_INT(t.srec.ensure(2 * vb * n));
+  GS_TRY_INT(t.tmp_k.ensure(8 * n));
+  GS_TRY_INT(t.tmp_v.ensure(4 * n));
+  GS_TRY_INT(t.root.ensure(8 * 8));
+  GS_TRY_INT(t.scal.ensure(64));
+  const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
+  GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
+  // 1. padded root box
+  if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
+  else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
+  k_bbox_final<<<1, 32, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+  // 2. keys
+  const int nb = nblocks(n, kNT);
+  if (prec == kF32)
+    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), t.tmp_v.as<int>());
+  else
+    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), t.tmp_v.as<int>());
+  GS_CUDA_OK(cudaGetLastError());
+  // 3. stable radix sort of key_hi (values: point index), 8 passes of 8 bits
+  GS_CUDA_OK(cudaMemcpyAsync(t.skey_hi.ptr, t.key_hi.ptr, 8 * n, cudaMemcpyDeviceToDevice, st));
+  GS_CUDA_OK(cudaMemcpyAsync(t.perm.ptr, t.tmp_v.ptr, 4 * n, cudaMemcpyDeviceToDevice, st));
+  const int ntiles = nblocks(n, kRsTile);
+  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * ntiles));
+  uint64_t* ka = t.skey_hi.as<uint64_t>();
+  uint64_t* kb = t.tmp_k.as<uint64_t>();
+  int* va = t.perm.as<int>();
+  int* vb2 = t.tmp_v.as<int>();
+  for (int shift = 0; shift < 64; shift += 8) {
+    k_rs_hist<<<ntiles, kRsNT, 0, st>>>(ka, n, shift, t.hist.as<unsigned>(), ntiles);
+    k_rs_scan<<<1, 1024, 0, st>>>(t.hist.as<unsigned>(), (int64_t)256 * ntiles);
+    k_rs_scatter<<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, shift, t.hist.as<unsigned>(), ntiles);
+    std::swap(ka, kb);
+    std::swap(va, vb2);
+  }
+  // 8 passes: result back in skey_hi / perm
+  GS_CUDA_OK(cudaGetLastError());
+  k_fix_ties<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.perm.as<int>(), t.key_lo.as<uint64_t>(), n);
+  k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
+  // 4. topology
+  k_lcp<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>());
+  k_count<<<nb, kNT, 0, st>>>(t.lcp.as<int>(), n, t.tmp_v.as<int>());
+  GS_TRY_INT(scan_ints(t.tmp_v.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
+  int m = 0;
+  GS_CUDA_OK(cudaMemcpyAsync(&m, t.first.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GS_CUDA_OK(cudaStreamSynchronize(st));
+  t.m = m;
+  GS_TRY_INT(t.meta.ensure(sizeof(int4) * m));
+  GS_TRY_INT(t.parent.ensure(4 * m));
+  GS_TRY_INT(t.nchild.ensure(4 * m));
+  GS_TRY_INT(t.counter.ensure(4 * m));
+  GS_TRY_INT(t.lo.ensure(vb * m));
+  GS_TRY_INT(t.hi.ensure(vb * m));
+  GS_TRY_INT(t.cen.ensure(vb * m));
+  GS_TRY_INT(t.mom.ensure(vb * m));
+  GS_TRY_INT(t.psum.ensure(sizeof(double4) * m));
+  GS_TRY_INT(t.msum.ensure(sizeof(double4) * m));
+  GS_TRY_INT(t.squ.ensure(vb * n));
+  k_nodes<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
+                              t.first.as<int>(), n, t.meta.as<int4>(), t.parent.as<int>());
+  const int mb = nblocks(m, kNT);
+  k_nchild<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.nchild.as<int>());
+  // 5. leaf-order records + aggregates
+  const int scaled = prec == kF32;
+  void* squ = t.squ.ptr;  // unscaled q in leaf order
+  if (prec == kF32)
+    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<float4>(), (float4*)squ);
+  else
+    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<double4>(), (double4*)squ);
+  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * m, st));
+  if (prec == kF32)
+    k_aggregate<float><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>());
+  else
+    k_aggregate<double><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>());
+  GS_CUDA_OK(cudaGetLastError());
+  (void)mb;
+  return tree_finalize_fwd(prec, t, kc, st);
+}
+
+int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st) {
+  const int64_t m = t.m;
+  const int mb = nblocks(m, kNT);
+  const int scaled = prec == kF32;
+  t.kc = kc;
+  if (prec == kF32)
+    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), m, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>());
+  else
+    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), m, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>());
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, cudaStream_t st) {
+  const int64_t n = t.n;
+  const int nb = nblocks(n, kNT);
+  if (prec == kF32)
+    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>());
+  else
+    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>());
+  GS_CUDA_OK(cudaGetLastError());
+  return tree_finalize_fwd(prec, t, kc, st);
+}
+
+int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t st) {
+  const int64_t n = t.n;
+  GS_TRY_INT(t.sadj.ensure(2 * vec_bytes(prec) * n));
+  const int nb = nblocks(n, kNT);
+  if (prec == kF32) k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
+  else k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
+  const int64_t n = t.n, m = t.m;
+  const size_t vb = vec_bytes(prec);
+  GS_TRY_INT(t.sadj.ensure(2 * vb * n));
+  GS_TRY_INT(t.asum.ensure(sizeof(double4) * m));
+  GS_TRY_INT(t.bsum.ensure(sizeof(double4) * m));
+  GS_TRY_INT(t.nadj_a.ensure(vb * m));
+  GS_TRY_INT(t.nadj_b.ensure(vb * m));
+  const int nb = nblocks(n, kNT), mb = nblocks(m, kNT);
+  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * m, st));
+  if (prec == kF32) {
+    k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
+    k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), m, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<float4>(), t.nadj_b.as<float4>());
+  } else {
+    k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
+    k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), m, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<double4>(), t.nadj_b.as<double4>());
+  }
+  GS_CUDA_OK(cudaGetLastError());
+  t.adj_valid = true;
+  return GS_OK;
+}
+
+namespace {
+
+template <typename R>
+__global__ void k_dl_nodes(const int4* meta, const int* parent, int64_t m, const V4<R>* lo,
+                           const V4<R>* hi, const double4* psum, const double4* msum,
+                           const double4* asum, const double4* bsum, int32_t* level,
+                           int32_t* par, int32_t* skip, int32_t* range, double* boxes,
+                           double* sums, uint32_t* count) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= m) return;
+  const int4 mi = meta[i];
+  if (level) level[i] = mi.w >> 8;
+  if (par) par[i] = parent[i];
+  if (skip) skip[i] = mi.x;
+  if (range) { range[2 * i] = mi.y; range[2 * i + 1] = mi.z; }
+  if (count) count[i] = (uint32_t)(mi.z - mi.y + 1);
+  if (boxes) {
+    const V4<R> l = ld4(lo + i), h = ld4(hi + i);
+    boxes[12 * i + 6] = l.x; boxes[12 * i + 7] = l.y; boxes[12 * i + 8] = l.z;
+    boxes[12 * i + 9] = h.x; boxes[12 * i + 10] = h.y; boxes[12 * i + 11] = h.z;
+  }
+  if (sums) {
+    const double4 z = make_double4(0, 0, 0, 0);
+    const double4 v[4] = {psum[i], msum[i], asum ? asum[i] : z, bsum ? bsum[i] : z};
+    for (int k = 0; k < 4; ++k) {
+      sums[12 * i + 3 * k] = v[k].x; sums[12 * i + 3 * k + 1] = v[k].y; sums[12 * i + 3 * k + 2] = v[k].z;
+    }
+  }
+}
+
+template <typename T>
+int dl(T* host, const DBuf& d, int64_t count, cudaStream_t st) {
+  if (host && count > 0)
+    GS_CUDA_OK(cudaMemcpyAsync(host, d.ptr, sizeof(T) * count, cudaMemcpyDeviceToHost, st));
+  return GS_OK;
+}
+
+}  // namespace
+
+int tree_download(const DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
+                  uint64_t* key_lo, int32_t* level, int32_t* parent, int32_t* skip,
+                  int32_t* range, double* boxes, double* sums, uint32_t* count) {
+  const int64_t n = t.n, m = t.m;
+  DBuf b_level, b_par, b_skip, b_range, b_boxes, b_sums, b_count;
+  if (level) GS_TRY_INT(b_level.ensure(4 * m));
+  if (parent) GS_TRY_INT(b_par.ensure(4 * m));
+  if (skip) GS_TRY_INT(b_skip.ensure(4 * m));
+  if (range) GS_TRY_INT(b_range.ensure(8 * m));
+  if (boxes) GS_TRY_INT(b_boxes.ensure(96 * m));
+  if (sums) GS_TRY_INT(b_sums.ensure(96 * m));
+  if (count) GS_TRY_INT(b_count.ensure(4 * m));
+  const int mb = nblocks(m, kNT);
+  const double4* as = t.adj_valid ? t.asum.as<double4>() : nullptr;
+  const double4* bs = t.adj_valid ? t.bsum.as<double4>() : nullptr;
+  if (t.prec == kF32)
+    k_dl_nodes<float><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.parent.as<int>(), m, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), as, bs, b_level.as<int32_t>(), b_par.as<int32_t>(), b_skip.as<int32_t>(), b_range.as<int32_t>(), b_boxes.as<double>(), b_sums.as<double>(), b_count.as<uint32_t>());
+  else
+    k_dl_nodes<double><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.parent.as<int>(), m, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), as, bs, b_level.as<int32_t>(), b_par.as<int32_t>(), b_skip.as<int32_t>(), b_range.as<int32_t>(), b_boxes.as<double>(), b_sums.as<double>(), b_count.as<uint32_t>());
+  if (boxes)
+    k_cells<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.root.as<double>(), b_boxes.as<double>());
+  GS_CUDA_OK(cudaGetLastError());
+  GS_TRY_INT(dl(order, t.perm, n, st));
+  GS_TRY_INT(dl(key_hi, t.key_hi, n, st));
+  GS_TRY_INT(dl(key_lo, t.key_lo, n, st));
+  GS_TRY_INT(dl(level, b_level, m, st));
+  GS_TRY_INT(dl(parent, b_par, m, st));
+  GS_TRY_INT(dl(skip, b_skip, m, st));
+  GS_TRY_INT(dl(range, b_range, 2 * m, st));
+  GS_TRY_INT(dl(boxes, b_boxes, 12 * m, st));
+  GS_TRY_INT(dl(sums, b_sums, 12 * m, st));
+  GS_TRY_INT(dl(count, b_count, m, st));
+  GS_CUDA_OK(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+}  // namespace gsb

@@ -1,0 +1,242 @@
+"""Parity of the exact (all-pairs) CUDA path against the reference oracle.
+
+Tolerances (BASELINE.json north_star): FP64 relative L2 <= 1e-10 on final q
+and p; FP32 <= 1e-4 (per RHS we hold FP32 to 1e-5, the FP32-input floor being
+~1e-6). FP32 runs compare against the oracle given the same
+FP32-rounded inputs.
+"""
+import numpy as np
+import pytest
+
+from paper_1907_04834_b200 import (EXACT, F32, F64, RK4, ConfigError, ConfigMismatch,
+                                   DimensionMismatch, NonFiniteState, ShootingConfig)
+from tests.util import f32, rel_l2, sphere, sym_uniform, uniform
+
+pytestmark = pytest.mark.gpu
+
+F64_TOL = 1e-10
+F32_RHS_TOL = 1e-5
+F32_TRAJ_TOL = 1e-4
+
+
+# ---------------------------------------------------------------- kernel_exact
+@pytest.mark.parametrize("n", [1, 3, 127, 1000, 4099])
+def test_exact_rhs_f64_matches_reference(gs, ref, n):
+    q, p = uniform(n, 8.0, seed=n), sym_uniform(n, 1.0, seed=n + 1)
+    h, dp, dq = gs.hamiltonian_with_gradients(q, p, 1.1)
+    wp, wq, wh = ref.exact_rhs(q, p, 1.1)
+    assert rel_l2(dp, wp) < 1e-13
+    assert rel_l2(dq, wq) < 1e-12 or np.abs(dq - wq).max() < 1e-14
+    assert abs(h - wh) <= 1e-12 * abs(wh)
+
+
+@pytest.mark.parametrize("n", [5, 1000, 4099])
+def test_exact_rhs_f32_matches_reference(gs, ref, n):
+    q, p = f32(uniform(n, 8.0, seed=n)), f32(sym_uniform(n, 1.0, seed=n + 1))
+    h, dp, dq = gs.hamiltonian_with_gradients(q, p, 1.1, precision=F32)
+    wp, wq, wh = ref.exact_rhs(q, p, 1.1)
+    assert rel_l2(dp, wp) < F32_RHS_TOL
+    assert rel_l2(dq, wq) < F32_RHS_TOL
+    assert abs(h - wh) <= F32_RHS_TOL * abs(wh)
+
+
+def test_known_answers(gs):
+    # single point: H = |p|^2, dH/dp = 2p exactly, dH/dq = 0 (test_kernel_exact.cpp:65-69,136-142)
+    q = np.array([[1.0, 2.0, 3.0]])
+    p = np.array([[0.5, -1.0, 0.25]])
+    h, dp, dq = gs.hamiltonian_with_gradients(q, p, 3.0)
+    assert np.array_equal(dp, 2 * p) and np.array_equal(dq, np.zeros((1, 3)))
+    assert h == pytest.approx(1.3125, rel=1e-15)
+    # zero momentum -> zero field and zero gradients
+    q = uniform(6, 5.0, 11)
+    h, dp, dq = gs.hamiltonian_with_gradients(q, np.zeros((6, 3)), 1.5)
+    assert h == 0.0 and not dp.any() and not dq.any()
+
+
+def test_flow_factor_two(gs, ref):
+    # dH/dp == 2 * exact_velocity (kernel_exact.hpp:22-28, test_kernel_exact.cpp:190-200)
+    q, p = uniform(8, 3.0, 81), sym_uniform(8, 1.0, 82)
+    dp, _ = gs.hamiltonian_gradients(q, p, 1.4)
+    v = gs.exact_velocity(q, q, p, 1.4)
+    assert np.allclose(dp, 2.0 * v, rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-13), (F32, F32_RHS_TOL)])
+def test_exact_velocity_matches_reference(gs, ref, prec, tol):
+    q, p = uniform(700, 3.0, 71), sym_uniform(700, 1.5, 72)
+    x = uniform(333, 3.0, 73)
+    if prec == F32:
+        q, p, x = f32(q), f32(p), f32(x)
+    v = gs.exact_velocity(x, q, p, 0.4, precision=prec)
+    assert rel_l2(v, ref.exact_velocity(x, q, p, 0.4)) < tol
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-12), (F32, 2e-5)])
+@pytest.mark.parametrize("n", [4, 600])
+def test_hessian_products_match_reference(gs, ref, prec, tol, n):
+    q, p = uniform(n, 2.0 + n / 100, 91), sym_uniform(n, 1.0, 92)
+    a, b = sym_uniform(n, 1.0, 93), sym_uniform(n, 1.0, 94)
+    if prec == F32:
+        q, p, a, b = f32(q), f32(p), f32(a), f32(b)
+    got = gs.hessian_products(q, p, a, b, 1.2, precision=prec)
+    want = ref.hessian_products(q, p, a, b, 1.2)
+    for g, w in zip(got, want):
+        assert rel_l2(g, w) < tol
+
+
+def test_dimension_mismatch(gs):
+    with pytest.raises(DimensionMismatch):
+        gs.hamiltonian(uniform(3, 1.0, 1), np.zeros((4, 3)), 1.0)
+
+
+# ---------------------------------------------------------------- shooting
+def c1_inputs(n=1024, seed=7):
+    q = sphere(n, seed)
+    p = np.random.default_rng(seed + 1).normal(0, 0.01, (n, 3))
+    return q, p
+
+
+def test_config1_exact_f64(gs, ref):
+    """BASELINE config 1: N=1024 unit sphere, sigma 0.2, 10 Euler steps, FP64."""
+    q, p = c1_inputs()
+    cfg = ShootingConfig(sigma=0.2, timesteps=10, backend=EXACT, precision=F64)
+    tr = gs.shoot_forward(q, p, cfg)
+    wq, wp = ref.shoot_forward(q, p, 0.2, 10)
+    assert rel_l2(tr.q[-1], wq[-1]) <= F64_TOL
+    assert rel_l2(tr.p[-1], wp[-1]) <= F64_TOL
+    assert rel_l2(tr.q, wq) <= F64_TOL
+    fq, fp, energy, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    assert np.array_equal(fq, tr.q[-1]) and np.array_equal(fp, tr.p[-1])
+    assert energy == pytest.approx(ref.hamiltonian(q, p, 0.2), rel=1e-12)
+
+
+def test_config1_exact_f32(gs, ref):
+    q, p = c1_inputs()
+    q, p = f32(q), f32(p)
+    cfg = ShootingConfig(sigma=0.2, timesteps=10, backend=EXACT, precision=F32)
+    fq, fp, _, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    wq, wp = ref.shoot_forward(q, p, 0.2, 10)
+    assert rel_l2(fq, wq[-1]) <= F32_TRAJ_TOL
+    assert rel_l2(fp, wp[-1]) <= F32_TRAJ_TOL
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, F64_TOL), (F32, F32_TRAJ_TOL)])
+def test_rk4_matches_composed_oracle(gs, port, prec, tol):
+    """RK4 (BASELINE config 4) against the CPU RK4 composed over the reference RHS."""
+    n = 800
+    q = uniform(n, 1.0, 31)
+    p = np.random.default_rng(32).normal(0, 1e-2, (n, 3))
+    if prec == F32:
+        q, p = f32(q), f32(p)
+    cfg = ShootingConfig(sigma=0.05, timesteps=10, backend=EXACT, integrator=RK4, precision=prec)
+    fq, fp, e, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    w = port.shoot_forward(q, p, 0.05, 10, integrator=1, keep_traj=False)
+    assert rel_l2(fq, w["q"]) <= tol
+    assert rel_l2(fp, w["p"]) <= tol
+    assert e == pytest.approx(w["energy"], rel=1e-12 if prec == F64 else 1e-5)
+
+
+def test_two_body_rk4_reference(gs):
+    """test_shooting.cpp:98-108: head-on pair under Euler T=1e4 vs an RK4 oracle."""
+    q = np.array([[-1.0, 0, 0], [1.0, 0, 0]])
+    p = np.array([[0.3, 0, 0], [-0.3, 0, 0]])
+    cfg = ShootingConfig(sigma=1.0, timesteps=10000)
+    fq, fp, _, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    cfg4 = ShootingConfig(sigma=1.0, timesteps=2000, integrator=RK4)
+    rq, rp, _, _ = gs.shoot_forward(q, p, cfg4, keep_trajectory=False)
+    assert np.abs(fq - rq).max() < 1e-3 and np.abs(fp - rp).max() < 1e-3
+
+
+def test_free_particle(gs):
+    q = np.array([[0.5, -0.25, 2.0]])
+    p = np.array([[1.0, 0.0, 0.0]])
+    for t in (1, 7, 40):
+        tr = gs.shoot_forward(q, p, ShootingConfig(sigma=3.0, timesteps=t))
+        assert np.linalg.norm(tr.q[-1][0] - (q[0] + 2.0 * p[0])) < 1e-12
+        assert np.array_equal(tr.p[-1], p)
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, F64_TOL), (F32, 1e-4)])
+def test_evaluate_exact_matches_reference(gs, ref, prec, tol):
+    n = 300
+    q, p, t = uniform(n, 5.0, 461), sym_uniform(n, 0.3, 462), uniform(n, 5.0, 463)
+    if prec == F32:
+        q, p, t = f32(q), f32(p), f32(t)
+    cfg = ShootingConfig(sigma=1.2, lambda_=0.7, timesteps=8, precision=prec)
+    ev = gs.evaluate(q, p, t, cfg)
+    rep, g, _, _ = ref.evaluate(q, p, t, 1.2, 0.7, 8, 0)
+    assert ev.report["total"] == pytest.approx(rep[2], rel=tol)
+    assert ev.report["energy"] == pytest.approx(rep[0], rel=tol)
+    assert ev.report["residual_sse"] == pytest.approx(rep[3], rel=tol)
+    assert rel_l2(ev.gradient, g) <= tol * 10
+
+
+def test_backward_gradient_and_objective(gs, ref):
+    n = 50
+    q, p, t = uniform(n, 2.0, 441), sym_uniform(n, 0.3, 442), uniform(n, 2.0, 443)
+    cfg = ShootingConfig(sigma=1.1, lambda_=0.8, timesteps=10)
+    tr = gs.shoot_forward(q, p, cfg)
+    g = gs.backward_gradient(tr, t, cfg)
+    wq, wp = ref.shoot_forward(q, p, 1.1, 10)
+    wg = ref.backward_gradient(wq, wp, t, 1.1, 0.8, 10)
+    assert rel_l2(g, wg) <= F64_TOL
+    obj = gs.objective(q, p, t, cfg)
+    want = ref.objective(q, p, t, 1.1, 0.8, 10)
+    assert obj["total"] == pytest.approx(want[2], rel=1e-12)
+
+
+def test_gradient_zero_at_minimum(gs):
+    q = uniform(4, 2.0, 431)
+    cfg = ShootingConfig(sigma=1.0, timesteps=6)
+    tr = gs.shoot_forward(q, np.zeros((4, 3)), cfg)
+    assert not gs.backward_gradient(tr, q, cfg).any()
+
+
+def test_warp_points_matches_reference(gs, ref):
+    n = 200
+    q, p = uniform(n, 1.5, 471), sym_uniform(n, 0.25, 472)
+    cfg = ShootingConfig(sigma=0.8, timesteps=20)
+    tr = gs.shoot_forward(q, p, cfg)
+    x = uniform(97, 3.0, 473)
+    y = gs.warp_points(tr, x, cfg)
+    assert rel_l2(y, ref.warp_points(tr.q, tr.p, x, 0.8, 20)) <= 1e-12
+    carried = gs.warp_points(tr, q, cfg)  # carrier points reproduce the endpoint
+    assert np.abs(carried - tr.q[-1]).max() < 1e-10
+    other = ShootingConfig(sigma=0.8, timesteps=21)
+    with pytest.raises(ConfigMismatch):
+        gs.warp_points(tr, q, other)
+    with pytest.raises(ConfigMismatch):
+        gs.backward_gradient(tr, q, other)
+
+
+def test_nonfinite_reports_step(gs):
+    q = np.array([[0.0, 0, 0], [0.1, 0, 0]])
+    p = np.array([[1e200, 0, 0], [1e200, 0, 0]])
+    with pytest.raises(NonFiniteState) as e:
+        gs.shoot_forward(q, p, ShootingConfig(sigma=0.05, timesteps=4))
+    assert 1 <= e.value.timestep <= 4
+
+
+def test_config_errors(gs):
+    with pytest.raises(ConfigError) as e:
+        gs.shoot_forward(uniform(3, 1, 1), np.zeros((3, 3)),
+                         ShootingConfig(sigma=-1, lambda_=0, timesteps=0, threshold_multiplier=0))
+    assert e.value.violations == ["NonPositiveSigma", "NonPositiveLambda", "ZeroTimesteps",
+                                  "NonPositiveThreshold"]
+
+
+def test_empty_and_nonfinite_inputs(gs):
+    with pytest.raises(ValueError):
+        gs.hamiltonian(np.zeros((0, 3)), np.zeros((0, 3)), 1.0)
+    with pytest.raises(ValueError):
+        gs.hamiltonian(np.array([[np.nan, 0, 0]]), np.zeros((1, 3)), 1.0)
+
+
+def test_bitwise_determinism(gs):
+    q, p, t = uniform(400, 4.0, 481), sym_uniform(400, 0.3, 482), uniform(400, 4.0, 483)
+    for prec in (F64, F32):
+        cfg = ShootingConfig(sigma=1.0, timesteps=6, precision=prec)
+        a = gs.evaluate(q, p, t, cfg)
+        b = gs.evaluate(q, p, t, cfg)
+        assert a.report["total"] == b.report["total"]
+        assert np.array_equal(a.gradient, b.gradient)
