@@ -135,6 +135,12 @@ typedef struct gs_tree gs_tree;
 /* Octree::build, octree.cpp:25-40. */
 gs_status gs_tree_build(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
                         const double* p, gs_tree** out);
+/* Octree(cell_min, cell_max) + insert of every point in index order
+ * (octree.hpp:38-51): same tree over an explicit root cell; GS_OUT_OF_BOUNDS
+ * if a point lies outside it (octree.cpp:76-78). */
+gs_status gs_tree_build_in_cell(gs_ctx* ctx, int32_t precision, int64_t n, const double* q,
+                                const double* p, const double* cell_min, const double* cell_max,
+                                gs_tree** out);
 void gs_tree_free(gs_tree* tree);
 int64_t gs_tree_node_count(const gs_tree* tree);
 int64_t gs_tree_point_count(const gs_tree* tree);
@@ -221,6 +227,14 @@ int64_t gs_flow_last_launches(const gs_flow* flow);
 /* cudaStream_t of the flow (as void*), for event timing on the launch stream. */
 void* gs_flow_stream(const gs_flow* flow);
 
+/* Event timing of the dominant kernels of subsequent advances / stages
+ * (the all-pairs RHS kernel or the Barnes-Hut traversal; and the tree build),
+ * on the flow's stream: summed milliseconds and launch counts since the last
+ * read. */
+gs_status gs_flow_profile(gs_flow* flow, int32_t enable);
+gs_status gs_flow_profile_read(gs_flow* flow, double* kernel_ms, int64_t* kernel_launches,
+                               double* build_ms, int64_t* builds);
+
 /* Sharded stage API (one rank = one flow): */
 gs_status gs_flow_set_shard(gs_flow* flow, int64_t shard_begin, int64_t shard_count);
 /* Device pointer and byte size of the packed per-point source records
@@ -232,6 +246,10 @@ int64_t gs_flow_record_bytes(const gs_flow* flow);
  * epilogue that rewrites the shard's records); stage = 0..stages-1 of the
  * current step (Euler 1, RK4 4). */
 gs_status gs_flow_stage(gs_flow* flow, int32_t stage);
+
+/* ---- measured device peaks (roofline denominators) ----------------------------
+ * kind 0: FP32 FFMA lane-ops/s, 1: MUFU.EX2 lane-ops/s, 2: FP64 DFMA lane-ops/s. */
+gs_status gs_microbench(int device, int32_t kind, double* ops_per_s);
 
 #ifdef __cplusplus
 }

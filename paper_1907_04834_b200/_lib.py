@@ -88,6 +88,7 @@ SIGNATURES = [
     ("gs_exact_velocity", _st, [_vp, C.c_int32, _i64, _d, _i64, _d, _d, C.c_double, _d]),
     ("gs_hessian_products", _st, [_vp, C.c_int32, _i64, _d, _d, _d, _d, C.c_double, _d, _d, _d, _d]),
     ("gs_tree_build", _st, [_vp, C.c_int32, _i64, _d, _d, C.POINTER(_vp)]),
+    ("gs_tree_build_in_cell", _st, [_vp, C.c_int32, _i64, _d, _d, _d, _d, C.POINTER(_vp)]),
     ("gs_tree_free", None, [_vp]),
     ("gs_tree_node_count", _i64, [_vp]),
     ("gs_tree_point_count", _i64, [_vp]),
@@ -114,10 +115,13 @@ SIGNATURES = [
     ("gs_flow_download", _st, [_vp, _d, _d]),
     ("gs_flow_last_launches", _i64, [_vp]),
     ("gs_flow_stream", _vp, [_vp]),
+    ("gs_flow_profile", _st, [_vp, C.c_int32]),
+    ("gs_flow_profile_read", _st, [_vp, _d, C.POINTER(_i64), _d, C.POINTER(_i64)]),
     ("gs_flow_set_shard", _st, [_vp, _i64, _i64]),
     ("gs_flow_source_buffer", _vp, [_vp]),
     ("gs_flow_record_bytes", _i64, [_vp]),
     ("gs_flow_stage", _st, [_vp, C.c_int32]),
+    ("gs_microbench", _st, [C.c_int, C.c_int32, _d]),
 ]
 
 _lib = None

@@ -56,7 +56,7 @@ struct BhArgs {
   const V4<R>* squ;   // [n] unscaled q
   const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
   const int* perm;
-  int n, nq, tgt_begin, n_tgt;
+  int n, m, nq, tgt_begin, n_tgt;
   const V4<R>* ev;  // VEL eval records
   double kap, kc0x, kc0y, kc0z;
   double T2;         // exact gate threshold on d2
@@ -207,6 +207,9 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
           next = nd + 1;
         }
       }
+      // past the last node (skip == m): this query is done; a non-advancing skip
+      // (cannot happen on a valid tree) must never loop
+      if (next >= a.m || next <= nd) next = INT_MAX;
     }
     const unsigned rm = __ballot_sync(0xffffffffu, ranged);
     if (rm) {
@@ -275,6 +278,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.sadj = t.sadj.as<V4<R>>();
   a.perm = t.perm.as<int>();
   a.n = (int)t.n;
+  a.m = (int)t.m;
   a.tgt_begin = q.tgt_begin;
   a.n_tgt = q.n_tgt;
   a.nq = q.mode == kBhVel ? q.m : (int)t.n;
@@ -326,7 +330,9 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
                      const void* rec, int64_t n, int64_t tb, int64_t nt, BhWork& w, FwdEpi e,
                      cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats*) {
   DevTree& t = tree_for(w);
+  kt_mark(1, st);
   GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st));
+  kt_mark(1, st);
   GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
@@ -336,7 +342,9 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   q.part = w.part.ptr;
   q.totals = w.stats.as<unsigned long long>();
   const double thr = cfg.threshold_multiplier * cfg.sigma;
+  kt_mark(0, st);
   GS_TRY_INT(bh_traverse(dev, prec, t, cfg.sigma, thr, q, st));
+  kt_mark(0, st);
   e.S = 1;
   e.parts_per_tgt = 2;
   e.part = w.part.ptr;

@@ -45,8 +45,10 @@ struct DevTree {
   bool adj_valid = false;
 };
 
+// root_box (host, {lo xyz, hi xyz}) overrides the padded bounding box
+// (Octree(cell_min, cell_max) + insert, octree.hpp:38-51).
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
-               DevTree& t, cudaStream_t st);
+               DevTree& t, cudaStream_t st, const double* root_box = nullptr);
 // (re)writes the interaction coordinates (FP32: scaled by kc.kappa) and centroids
 int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, cudaStream_t st);
 // adj: [n][2] records (alpha, beta) by point index; node sums + leaf-order copy

@@ -16,6 +16,7 @@
 namespace gsb {
 
 thread_local std::string g_err;
+thread_local KTimer* g_ktimer = nullptr;
 thread_local int g_nonfinite = 0;
 thread_local uint32_t g_violations = 0;
 
@@ -80,6 +81,8 @@ struct gs_flow {
   int energy_blocks = 0;
   BhWork bh;
   gs_stats stats{};
+  KTimer* timer = nullptr;  // gs_flow_profile
+  ~gs_flow() { delete timer; }
 };
 
 extern "C" {
@@ -228,7 +231,9 @@ int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void*
                 int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
                 int* energy_blocks) {
   GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+  kt_mark(0, st);
   const int S = rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr, kMaxChunks, st);
+  kt_mark(0, st);
   if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
   GS_CUDA_OK(cudaGetLastError());
   e.S = S;
@@ -284,6 +289,11 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
     e.dhdp_out = f->dhdp0.as<double>();
   }
   int blocks = 0;
+  struct Install {
+    KTimer* prev;
+    explicit Install(KTimer* t) : prev(g_ktimer) { g_ktimer = t; }
+    ~Install() { g_ktimer = prev; }
+  } install(f->timer);
   if (f->cfg.backend == GS_EXACT) {
     GS_TRY(exact_stage(c->dev, f->prec, f->kc, rec_in, f->n, f->shard_begin, f->shard_count,
                        f->part, e, st, &f->launches, &blocks));
@@ -463,6 +473,27 @@ gs_status gs_flow_download(gs_flow* f, double* q, double* p) {
 
 int64_t gs_flow_last_launches(const gs_flow* f) { return f ? f->launches : 0; }
 void* gs_flow_stream(const gs_flow* f) { return f ? (void*)f->ctx->stream : nullptr; }
+
+gs_status gs_flow_profile(gs_flow* f, int32_t enable) {
+  if (!f) return bad_arg("null flow");
+  if (enable && !f->timer) f->timer = new KTimer;
+  if (!enable) {
+    delete f->timer;
+    f->timer = nullptr;
+  }
+  return GS_OK;
+}
+
+gs_status gs_flow_profile_read(gs_flow* f, double* kernel_ms, int64_t* kernel_launches,
+                               double* build_ms, int64_t* builds) {
+  if (!f || !f->timer) return bad_arg("profiling not enabled");
+  GS_CUDA_OK(cudaStreamSynchronize(f->ctx->stream));
+  const double k = f->timer->drain(0, kernel_launches);
+  const double b = f->timer->drain(1, builds);
+  if (kernel_ms) *kernel_ms = k;
+  if (build_ms) *build_ms = b;
+  return GS_OK;
+}
 
 gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
   if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
@@ -1002,6 +1033,37 @@ gs_status gs_tree_build(gs_ctx* c, int32_t precision, int64_t n, const double* q
     const KernelConsts kc = make_consts(1.0, tr->prec == kF32 ? tr->c0 : nullptr);
     tr->sigma = 1.0;
     s = tree_build(c->dev, tr->prec, kc, tr->rec.ptr, n, tr->t, c->stream);
+  }
+  if (s == GS_OK) s = sync(c);
+  if (s != GS_OK) {
+    delete tr;
+    return (gs_status)s;
+  }
+  *out = tr;
+  return GS_OK;
+}
+
+gs_status gs_tree_build_in_cell(gs_ctx* c, int32_t precision, int64_t n, const double* q,
+                                const double* p, const double* cell_min, const double* cell_max,
+                                gs_tree** out) {
+  if (!c || !q || !p || !cell_min || !cell_max || !out) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  for (int64_t i = 0; i < n; ++i)  // Octree::insert, octree.cpp:76-78
+    for (int a = 0; a < 3; ++a)
+      if (!(q[3 * i + a] >= cell_min[a] && q[3 * i + a] <= cell_max[a])) {
+        g_err = "Octree::insert: point outside the root cell";
+        return GS_OUT_OF_BOUNDS;
+      }
+  auto* tr = new gs_tree;
+  tr->ctx = c;
+  tr->prec = precision == GS_F32 ? kF32 : kF64;
+  bbox_center(q, n, tr->c0);
+  const double box[6] = {cell_min[0], cell_min[1], cell_min[2], cell_max[0], cell_max[1], cell_max[2]};
+  int s = upload_records(c, tr->prec, q, p, n, tr->rec);
+  if (s == GS_OK) {
+    const KernelConsts kc = make_consts(1.0, tr->prec == kF32 ? tr->c0 : nullptr);
+    tr->sigma = 1.0;
+    s = tree_build(c->dev, tr->prec, kc, tr->rec.ptr, n, tr->t, c->stream, box);
   }
   if (s == GS_OK) s = sync(c);
   if (s != GS_OK) {

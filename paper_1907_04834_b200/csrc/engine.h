@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "gs_common.cuh"
 #include "geoshoot_b200.h"
@@ -38,6 +39,42 @@ struct DBuf {
   template <typename T> T* as() const { return static_cast<T*>(ptr); }
   ~DBuf() { release(); }
 };
+
+// Optional event timing of the dominant kernels inside a flow (bench roofline):
+// channel 0 = the O(N^2) / traversal kernel, channel 1 = the tree build.
+struct KTimer {
+  std::vector<cudaEvent_t> ev[2];
+  size_t used[2] = {0, 0};
+  void mark(int ch, cudaStream_t st) {
+    if (used[ch] == ev[ch].size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev[ch].push_back(e);
+    }
+    cudaEventRecord(ev[ch][used[ch]++], st);
+  }
+  // sum of (end - start) over the recorded pairs; resets
+  double drain(int ch, int64_t* pairs) {
+    double ms = 0.0;
+    for (size_t k = 0; k + 1 < used[ch]; k += 2) {
+      float v = 0.f;
+      cudaEventSynchronize(ev[ch][k + 1]);
+      cudaEventElapsedTime(&v, ev[ch][k], ev[ch][k + 1]);
+      ms += v;
+    }
+    if (pairs) *pairs = (int64_t)(used[ch] / 2);
+    used[ch] = 0;
+    return ms;
+  }
+  ~KTimer() {
+    for (auto& v : ev)
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+  }
+};
+extern thread_local KTimer* g_ktimer;
+inline void kt_mark(int ch, cudaStream_t st) {
+  if (g_ktimer) g_ktimer->mark(ch, st);
+}
 
 inline size_t vec_bytes(int prec) { return prec == kF32 ? sizeof(float4) : sizeof(double4); }
 

@@ -344,7 +344,7 @@ __global__ void k_nchild(const int4* meta, int64_t m, int* nchild) {
   const int4 mi = meta[i];
   int c = 0;
   if (!(mi.w & 1))
-    for (int ch = (int)i + 1; ch < mi.x; ch = meta[ch].x) ++c;
+    for (int ch = (int)i + 1; ch < mi.x && c < 8; ch = max(ch + 1, meta[ch].x)) ++c;
   nchild[i] = c;
 }
 
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
-    for (int ch = par + 1; ch < end; ch = meta[ch].x) {
+    for (int ch = par + 1; ch < end; ch = max(ch + 1, meta[ch].x)) {
       const double4 a0 = ldcg4(s0 + ch), a1 = ldcg4(s1 + ch);
       A.x += a0.x; A.y += a0.y; A.z += a0.z;
       B.x += a1.x; B.y += a1.y; B.z += a1.z;
@@ -546,7 +546,7 @@ static int scan_ints(const int* in, int64_t n, int* out, DBuf& scratch, cudaStre
 }
 
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
-               DevTree& t, cudaStream_t st) {
+               DevTree& t, cudaStream_t st, const double* root_box) {
   t.prec = prec;
   t.n = n;
   t.kc = kc;
@@ -566,10 +566,14 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.scal.ensure(64));
   const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
   GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
-  // 1. padded root box
-  if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
-  else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
-  k_bbox_final<<<1, 32, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+  // 1. padded root box (or the caller's explicit root cell)
+  if (root_box) {
+    GS_CUDA_OK(cudaMemcpyAsync(t.root.ptr, root_box, 6 * sizeof(double), cudaMemcpyHostToDevice, st));
+  } else {
+    if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
+    else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
+    k_bbox_final<<<1, 32, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+  }
   // 2. keys
   const int nb = nblocks(n, kNT);
   if (prec == kF32)

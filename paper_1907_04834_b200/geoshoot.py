@@ -408,6 +408,17 @@ class Flow:
     def stream(self) -> int:
         return self.gs.lib.gs_flow_stream(self.h) or 0
 
+    def profile(self, enable: bool = True):
+        self.gs.check(self.gs.lib.gs_flow_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        k, b = C.c_double(), C.c_double()
+        kl, bl = C.c_int64(), C.c_int64()
+        self.gs.check(self.gs.lib.gs_flow_profile_read(self.h, C.byref(k), C.byref(kl), C.byref(b),
+                                                       C.byref(bl)))
+        return {"kernel_ms": k.value, "kernel_launches": kl.value, "build_ms": b.value,
+                "builds": bl.value}
+
     # sharded stage API (see shard.py)
     def set_shard(self, begin: int, count: int):
         self.gs.check(self.gs.lib.gs_flow_set_shard(self.h, begin, count))

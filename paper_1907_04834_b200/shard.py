@@ -1,0 +1,77 @@
+"""Multi-GPU driver: target sharding with one all-gather per integrator stage.
+
+SURVEY.md §8e: within a stage every target's RHS is independent, so rank r
+owns targets [r*N/G, (r+1)*N/G), computes their RHS against all N sources and
+updates its own records in the fused stage epilogue; then the ranks all-gather
+the updated shards (torch.distributed, NCCL over NVLink/NVSwitch on B200s,
+gloo in the CPU tests). The all-gather is in place: every rank's record buffer
+is the gather output and its own shard is the input slice. Per-target
+arithmetic does not depend on G, so results are bitwise identical to 1 GPU.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Equal contiguous shards (n must be divisible by world)."""
+    if n % world:
+        raise ValueError(f"point count {n} not divisible by world size {world}")
+    s = n // world
+    return rank * s, s
+
+
+class _CudaBuf:
+    """Exposes a raw device allocation to torch via __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes // 4,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+            "strides": None}
+
+
+def records_view(flow) -> torch.Tensor:
+    """The flow's packed (q, p) records as a flat float32 CUDA tensor (no copy)."""
+    nbytes = flow.n * flow.record_bytes()
+    return torch.as_tensor(_CudaBuf(flow.source_buffer(), nbytes), device="cuda")
+
+
+class ShardedFlow:
+    """Drives a flow-like object over a torch.distributed process group.
+
+    ``flow`` needs: n, stage(s), set_shard(begin, count), stages (int), and
+    either a ``records()`` method returning its record tensor or the gs_flow
+    accessors used by records_view(). ``stream`` (optional) is the CUDA stream
+    the flow launches on; the all-gather is ordered after it.
+    """
+
+    def __init__(self, flow, stages: int, group=None, stream=None):
+        self.flow = flow
+        self.stages = stages
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.begin, self.count = shard_range(flow.n, self.rank, self.world)
+        flow.set_shard(self.begin, self.count)
+        self.stream = stream
+        self._rec = flow.records() if hasattr(flow, "records") else records_view(flow)
+        per = self._rec.numel() // flow.n
+        self._mine = self._rec[self.begin * per:(self.begin + self.count) * per]
+        self.collectives = 0
+
+    def _gather(self):
+        if self.world == 1:
+            return
+        if self.stream is not None:
+            with torch.cuda.stream(self.stream):
+                dist.all_gather_into_tensor(self._rec, self._mine, group=self.group)
+        else:
+            dist.all_gather_into_tensor(self._rec, self._mine, group=self.group)
+        self.collectives += 1
+
+    def step(self, steps: int = 1):
+        for _ in range(steps):
+            for s in range(self.stages):
+                self.flow.stage(s)
+                self._gather()
