@@ -248,7 +248,8 @@ int64_t gs_flow_record_bytes(const gs_flow* flow);
 gs_status gs_flow_stage(gs_flow* flow, int32_t stage);
 
 /* ---- measured device peaks (roofline denominators) ----------------------------
- * kind 0: FP32 FFMA lane-ops/s, 1: MUFU.EX2 lane-ops/s, 2: FP64 DFMA lane-ops/s. */
+ * kind 0: FP32 FFMA lane-ops/s (constant operands), 1: MUFU.EX2 lane-ops/s,
+ * 2: FP64 DFMA lane-ops/s, 3: FP32 FFMA lane-ops/s with all-register operands. */
 gs_status gs_microbench(int device, int32_t kind, double* ops_per_s);
 
 #ifdef __cplusplus

@@ -25,6 +25,27 @@ __global__ void __launch_bounds__(256) k_ffma(float* out, int iters, float a, fl
   if (s == 1234.5f) out[threadIdx.x] = s;
 }
 
+// all-register operands (FFMA R, R, R, R), the form the pair kernel issues
+__global__ void __launch_bounds__(256) k_ffma_reg(float* out, int iters, const float* ab) {
+  float x[kChains], a[kChains], b[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    x[c] = threadIdx.x * 1e-3f + c;
+    a[c] = ab[c] + threadIdx.x * 1e-9f;
+    b[c] = ab[8 + c];
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < kChains; ++c) x[c] = fmaf(x[c], a[(c + u) & 7], b[(c + 3 * u) & 7]);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += x[c];
+  if (s == 1234.5f) out[threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) k_ex2(float* out, int iters) {
   float x[kChains];
 #pragma unroll
@@ -71,6 +92,12 @@ extern "C" gs_status gs_microbench(int device, int32_t kind, double* ops_per_s) 
   const int iters = kind == 2 ? 256 : 2048;
   void* out = nullptr;
   GS_CUDA_OK(cudaMalloc(&out, 4096));
+  GS_CUDA_OK(cudaMemset(out, 0, 4096));
+  if (kind == 3) {
+    float ab[16];
+    for (int c = 0; c < 16; ++c) ab[c] = c < 8 ? 0.9999f + 1e-6f * c : 1e-7f * c;
+    GS_CUDA_OK(cudaMemcpy(out, ab, sizeof ab, cudaMemcpyHostToDevice));
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -79,6 +106,7 @@ extern "C" gs_status gs_microbench(int device, int32_t kind, double* ops_per_s) 
     cudaEventRecord(a);
     if (kind == 0) k_ffma<<<blocks, threads>>>((float*)out, iters, 0.999999f, 1e-7f);
     else if (kind == 1) k_ex2<<<blocks, threads>>>((float*)out, iters);
+    else if (kind == 3) k_ffma_reg<<<blocks, threads>>>((float*)out + 64, iters, (const float*)out);
     else k_dfma<<<blocks, threads>>>((double*)out, iters, 0.999999, 1e-7);
     cudaEventRecord(b);
     cudaEventSynchronize(b);

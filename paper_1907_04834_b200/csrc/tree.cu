@@ -609,16 +609,19 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_CUDA_OK(cudaMemcpyAsync(&m, t.first.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
   GS_CUDA_OK(cudaStreamSynchronize(st));
   t.m = m;
-  GS_TRY_INT(t.meta.ensure(sizeof(int4) * m));
-  GS_TRY_INT(t.parent.ensure(4 * m));
-  GS_TRY_INT(t.nchild.ensure(4 * m));
-  GS_TRY_INT(t.counter.ensure(4 * m));
-  GS_TRY_INT(t.lo.ensure(vb * m));
-  GS_TRY_INT(t.hi.ensure(vb * m));
-  GS_TRY_INT(t.cen.ensure(vb * m));
-  GS_TRY_INT(t.mom.ensure(vb * m));
-  GS_TRY_INT(t.psum.ensure(sizeof(double4) * m));
-  GS_TRY_INT(t.msum.ensure(sizeof(double4) * m));
+  // node arrays with 25% headroom: the node count drifts from stage to stage
+  // and a re-allocation (cudaFree/cudaMalloc) would stall the stream
+  const int64_t mc = m + m / 4 + 64;
+  GS_TRY_INT(t.meta.ensure(sizeof(int4) * mc));
+  GS_TRY_INT(t.parent.ensure(4 * mc));
+  GS_TRY_INT(t.nchild.ensure(4 * mc));
+  GS_TRY_INT(t.counter.ensure(4 * mc));
+  GS_TRY_INT(t.lo.ensure(vb * mc));
+  GS_TRY_INT(t.hi.ensure(vb * mc));
+  GS_TRY_INT(t.cen.ensure(vb * mc));
+  GS_TRY_INT(t.mom.ensure(vb * mc));
+  GS_TRY_INT(t.psum.ensure(sizeof(double4) * mc));
+  GS_TRY_INT(t.msum.ensure(sizeof(double4) * mc));
   GS_TRY_INT(t.squ.ensure(vb * n));
   k_nodes<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
                               t.first.as<int>(), n, t.meta.as<int4>(), t.parent.as<int>());
@@ -679,10 +682,11 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   const int64_t n = t.n, m = t.m;
   const size_t vb = vec_bytes(prec);
   GS_TRY_INT(t.sadj.ensure(2 * vb * n));
-  GS_TRY_INT(t.asum.ensure(sizeof(double4) * m));
-  GS_TRY_INT(t.bsum.ensure(sizeof(double4) * m));
-  GS_TRY_INT(t.nadj_a.ensure(vb * m));
-  GS_TRY_INT(t.nadj_b.ensure(vb * m));
+  const int64_t mc = m + m / 4 + 64;
+  GS_TRY_INT(t.asum.ensure(sizeof(double4) * mc));
+  GS_TRY_INT(t.bsum.ensure(sizeof(double4) * mc));
+  GS_TRY_INT(t.nadj_a.ensure(vb * mc));
+  GS_TRY_INT(t.nadj_b.ensure(vb * mc));
   const int nb = nblocks(n, kNT), mb = nblocks(m, kNT);
   GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * m, st));
   if (prec == kF32) {
