@@ -214,6 +214,8 @@ def run_ours(args):
     lib.gs_microbench(local, 0, C.byref(ffma))
     ex2 = C.c_double()
     lib.gs_microbench(local, 1, C.byref(ex2))
+    ffma_reg = C.c_double()
+    lib.gs_microbench(local, 3, C.byref(ffma_reg))
     k_ms = prof["kernel_ms"] / max(1, prof["kernel_launches"])
     pairs_per_launch = float(N) * shard
     achieved = pairs_per_launch / (k_ms * 1e-3) / 1e9  # Gpair/s
@@ -227,6 +229,7 @@ def run_ours(args):
                        f"{ffma.value / 1e12:.2f} T lane-FFMA/s / 16 FP32 instructions per pair; "
                        "MEASURED_PEAKS.json has no FP32 figure",
         "nominal_peak": nominal, "frac_of_nominal": achieved / nominal,
+        "peak_register_operand_ffma": ffma_reg.value / 16.0 / 1e9,
         "sfu_frac": achieved * 1e9 / ex2.value if ex2.value else None,
         "kernel": "k_rhs_f32<8,128>", "kernel_ms_avg": k_ms,
         "kernel_share_of_step": prof["kernel_ms"] / ms if ms else None,
