@@ -20,6 +20,8 @@
 // (gs_common.cuh): 3 FADD (d) + FMUL+2 FFMA (-r^2) + MUFU.EX2 (g) + FMUL+2 FFMA
 // (p_i.p_j) + FMUL (c) + 3 FFMA (sum g p_j) + 3 FFMA (sum c d) = 16 FP32 + 1 SFU.
 // No tensor cores: the contraction dimension is 3.
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace gsb {
@@ -29,11 +31,11 @@ constexpr int kTile = 256;
 // ----------------------------------------------------------------------------
 // forward RHS partials: A = sum_j g p_j, B = sum_j (p_i.p_j) g d'_ij
 // ----------------------------------------------------------------------------
-template <int TPT, int NT>
-__global__ void __launch_bounds__(NT) k_rhs_f32(const float4* __restrict__ rec, int n,
-                                                int tgt_begin, int n_tgt, int chunk,
-                                                float kap, float kc0x, float kc0y, float kc0z,
-                                                float4* __restrict__ part) {
+template <int TPT, int NT, int MINB, bool PHASED>
+__global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__ rec, int n,
+                                                      int tgt_begin, int n_tgt, int chunk,
+                                                      float kap, float kc0x, float kc0y, float kc0z,
+                                                      float4* __restrict__ part) {
   __shared__ float4 sq[kTile];
   __shared__ float4 sp[kTile];
   float qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
@@ -67,27 +69,59 @@ __global__ void __launch_bounds__(NT) k_rhs_f32(const float4* __restrict__ rec, 
       sp[u] = p;
     }
     __syncthreads();
+    if (PHASED) {
+      // all TPT exponentials are issued before the first one is consumed, so
+      // the MUFU latency hides behind independent work of the same warp
 #pragma unroll 2
-    for (int u = 0; u < kTile; ++u) {
-      const float4 a = sq[u];
-      const float4 b = sp[u];
+      for (int u = 0; u < kTile; ++u) {
+        const float4 a = sq[u];
+        const float4 b = sp[u];
+        float dx[TPT], dy[TPT], dz[TPT], g[TPT];
 #pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        const float dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
-        float nr2 = -dx * dx;
-        nr2 = fmaf(-dy, dy, nr2);
-        nr2 = fmaf(-dz, dz, nr2);
-        const float g = ex2(nr2);
-        float pp = px[k] * b.x;
-        pp = fmaf(py[k], b.y, pp);
-        pp = fmaf(pz[k], b.z, pp);
-        const float c = pp * g;
-        ax[k] = fmaf(g, b.x, ax[k]);
-        ay[k] = fmaf(g, b.y, ay[k]);
-        az[k] = fmaf(g, b.z, az[k]);
-        bx[k] = fmaf(c, dx, bx[k]);
-        by[k] = fmaf(c, dy, by[k]);
-        bz[k] = fmaf(c, dz, bz[k]);
+        for (int k = 0; k < TPT; ++k) {
+          dx[k] = qx[k] - a.x; dy[k] = qy[k] - a.y; dz[k] = qz[k] - a.z;
+          float nr2 = -dx[k] * dx[k];
+          nr2 = fmaf(-dy[k], dy[k], nr2);
+          nr2 = fmaf(-dz[k], dz[k], nr2);
+          g[k] = ex2(nr2);
+        }
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          float pp = px[k] * b.x;
+          pp = fmaf(py[k], b.y, pp);
+          pp = fmaf(pz[k], b.z, pp);
+          const float c = pp * g[k];
+          ax[k] = fmaf(g[k], b.x, ax[k]);
+          ay[k] = fmaf(g[k], b.y, ay[k]);
+          az[k] = fmaf(g[k], b.z, az[k]);
+          bx[k] = fmaf(c, dx[k], bx[k]);
+          by[k] = fmaf(c, dy[k], by[k]);
+          bz[k] = fmaf(c, dz[k], bz[k]);
+        }
+      }
+    } else {
+#pragma unroll 2
+      for (int u = 0; u < kTile; ++u) {
+        const float4 a = sq[u];
+        const float4 b = sp[u];
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          const float dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
+          float nr2 = -dx * dx;
+          nr2 = fmaf(-dy, dy, nr2);
+          nr2 = fmaf(-dz, dz, nr2);
+          const float g = ex2(nr2);
+          float pp = px[k] * b.x;
+          pp = fmaf(py[k], b.y, pp);
+          pp = fmaf(pz[k], b.z, pp);
+          const float c = pp * g;
+          ax[k] = fmaf(g, b.x, ax[k]);
+          ay[k] = fmaf(g, b.y, ay[k]);
+          az[k] = fmaf(g, b.z, az[k]);
+          bx[k] = fmaf(c, dx, bx[k]);
+          by[k] = fmaf(c, dy, by[k]);
+          bz[k] = fmaf(c, dz, bz[k]);
+        }
       }
     }
   }
@@ -494,17 +528,68 @@ constexpr int kNT = 128;
     default: KERNEL<1, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break; \
   }
 
+// FP32 RHS variants: {TPT, min CTAs/SM, phased}. Variant 0 is the default;
+// GS_RHS_VARIANT selects another one for tuning sweeps (tools/sweep_rhs.py).
+struct RhsVariant {
+  int tpt, minb;
+  bool phased;
+};
+static const RhsVariant kRhsVariants[] = {
+    {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true}};
+constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
+
+static int rhs_variant() {
+  static int v = [] {
+    const char* e = std::getenv("GS_RHS_VARIANT");
+    const int x = e ? std::atoi(e) : 0;
+    return (x >= 0 && x < kNumRhsVariants) ? x : 0;
+  }();
+  return v;
+}
+
+template <int TPT, int MINB, bool PH>
+static void launch_rhs_f32(const Plan& pl, cudaStream_t st, const float4* rec, int n, int tb,
+                           int nt, const KernelConsts& kc, float4* part) {
+  k_rhs_f32<TPT, kNT, MINB, PH><<<pl.grid, kNT, 0, st>>>(
+      rec, n, tb, nt, pl.chunk, (float)kc.kappa, (float)(kc.kappa * kc.c0[0]),
+      (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), part);
+}
+
+template <int TPT, int MINB, bool PH>
+static int occ_rhs_f32() {
+  return occupancy(k_rhs_f32<TPT, kNT, MINB, PH>, kNT);
+}
+
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
                  const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
   if (prec == kF32) {
-    static const int tpts[] = {8, 4, 2, 1};
-    static int occ = occupancy(k_rhs_f32<8, kNT>, kNT);
-    Plan pl = plan(n, n_tgt, kNT, tpts, 4, kTile, occ, dev.sms);
+    const int vi = rhs_variant();
+    const RhsVariant v = kRhsVariants[vi];
+    // small problems: fall back to narrower target blocks so the grid fills the GPU
+    const long slots = 3L * dev.sms;
+    int use = vi;
+    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = 6;  // TPT 2
+    if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;           // TPT 1
+    const RhsVariant u = kRhsVariants[use];
+    static int occs[kNumRhsVariants] = {
+        occ_rhs_f32<8, 3, true>(), occ_rhs_f32<8, 3, false>(), occ_rhs_f32<8, 4, true>(),
+        occ_rhs_f32<4, 6, true>(), occ_rhs_f32<4, 4, false>(), occ_rhs_f32<6, 4, true>(),
+        occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>()};
+    const int tp[] = {u.tpt};
+    Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
     if (pl.S > part_cap_chunks) return -1;
-    const float kap = (float)kc.kappa;
-    GS_TPT_SWITCH(pl.tpt, k_rhs_f32, (const float4*)rec, n, tgt_begin, n_tgt, pl.chunk, kap,
-                  (float)(kc.kappa * kc.c0[0]), (float)(kc.kappa * kc.c0[1]),
-                  (float)(kc.kappa * kc.c0[2]), (float4*)part);
+    const float4* r = (const float4*)rec;
+    float4* o = (float4*)part;
+    switch (use) {
+      case 0: launch_rhs_f32<8, 3, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 1: launch_rhs_f32<8, 3, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 2: launch_rhs_f32<8, 4, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 3: launch_rhs_f32<4, 6, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 4: launch_rhs_f32<4, 4, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 5: launch_rhs_f32<6, 4, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 6: launch_rhs_f32<2, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+    }
     return pl.S;
   }
   static const int tpts[] = {4, 2, 1};

@@ -184,13 +184,14 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
     bool ranged = false;
     int4 mi = make_int4(0, 0, 0, 0);
     if (next == nd) {
+      // the three node loads are independent: issue them together
       mi = a.meta[nd];
+      const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
       ++c_vis;
       if (mi.w & 1) {  // leaf: its point(s) directly
         ranged = true;
         next = mi.x;
       } else {
-        const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
         if (gate(l, h, x, a)) {  // far: one aggregate term
           const V4<R> C = ld4(a.cen + nd), P = ld4(a.mom + nd);
           if (MODE == kBhHess)
