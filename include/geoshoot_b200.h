@@ -235,6 +235,11 @@ gs_status gs_flow_profile(gs_flow* flow, int32_t enable);
 gs_status gs_flow_profile_read(gs_flow* flow, double* kernel_ms, int64_t* kernel_launches,
                                double* build_ms, int64_t* builds);
 
+/* Per-channel form of gs_flow_profile_read: channel 0 dominant kernel,
+ * 1 tree build, 2..5 tree-build phases (bbox+keys, radix sort, topology,
+ * aggregates); ms[c] summed, counts[c] pairs recorded. */
+gs_status gs_flow_profile_phases(gs_flow* flow, double* ms, int64_t* counts, int32_t channels);
+
 /* Sharded stage API (one rank = one flow): */
 gs_status gs_flow_set_shard(gs_flow* flow, int64_t shard_begin, int64_t shard_count);
 /* Device pointer and byte size of the packed per-point source records

@@ -117,6 +117,7 @@ SIGNATURES = [
     ("gs_flow_stream", _vp, [_vp]),
     ("gs_flow_profile", _st, [_vp, C.c_int32]),
     ("gs_flow_profile_read", _st, [_vp, _d, C.POINTER(_i64), _d, C.POINTER(_i64)]),
+    ("gs_flow_profile_phases", _st, [_vp, _d, C.POINTER(_i64), C.c_int32]),
     ("gs_flow_set_shard", _st, [_vp, _i64, _i64]),
     ("gs_flow_source_buffer", _vp, [_vp]),
     ("gs_flow_record_bytes", _i64, [_vp]),

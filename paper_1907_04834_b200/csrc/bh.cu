@@ -26,6 +26,7 @@
 // falls back to the exact FP64 test inside the band.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "bh.h"
 
@@ -254,12 +255,137 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
   }
 }
 
+// Work-stream variant: every lane walks its own query independently; each
+// iteration a lane either continues its pending direct range (one point) or
+// visits its next node (and, for a leaf / far / fully-inside node, evaluates
+// the first unit in the same iteration). All lanes holding a unit then run
+// the interaction together, so the warp does one unit of work per lane per
+// iteration whatever node each lane is at. Same per-query node set, decisions
+// and counts as the reference; only the summation order differs.
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
+  const int qi = blockIdx.x * kBhNT + threadIdx.x;
+  const bool valid = qi < a.nq;
+  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
+  int out = -1;
+  if (valid) {
+    if (MODE == kBhVel) {
+      x = ld4(a.ev + 2 * qi);
+      if (sizeof(R) == 4)
+        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
+                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
+                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
+      else
+        xs = x;
+      out = qi;
+    } else {
+      const int t = qi;
+      x = ld4(a.squ + t);
+      xs = ld4(a.srec + 2 * t);
+      px = ld4(a.srec + 2 * t + 1);
+      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
+      const int i = a.perm[t] - a.tgt_begin;
+      out = (i >= 0 && i < a.n_tgt) ? i : -1;
+    }
+  }
+  Acc<R> acc;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
+  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  int next = out >= 0 ? 0 : INT_MAX;
+  int j = 0, je = -1;  // pending direct range
+  const V4<R> zero = mk4<R>(0, 0, 0);
+  while (__any_sync(0xffffffffu, next < a.m || j <= je)) {
+    bool have = false;
+    bool approx = false;
+    int src = 0;
+    if (j > je && next < a.m) {
+      const int nd = next;
+      const int4 mi = a.meta[nd];
+      const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
+      ++c_vis;
+      next = mi.x;
+      if (mi.w & 1) {  // leaf: its point(s) directly
+        j = mi.y;
+        je = mi.z;
+      } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
+        approx = true;
+        have = true;
+        src = nd;
+        ++c_app;
+      } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
+        j = mi.y;
+        je = mi.z;
+        c_vis += (uint32_t)(mi.x - nd - 1);
+      } else {
+        next = nd + 1;
+      }
+      if (next <= nd) next = INT_MAX;  // never loop on a corrupt skip
+    }
+    if (!have && j <= je) {
+      have = true;
+      src = j++;
+      ++c_dir;
+    }
+    if (have) {
+      V4<R> Q, P, Al = zero, Be = zero;
+      if (approx) {
+        Q = ld4(a.cen + src);
+        P = ld4(a.mom + src);
+        if (MODE == kBhHess) { Al = ld4(a.nadj_a + src); Be = ld4(a.nadj_b + src); }
+      } else {
+        Q = ld4(a.srec + 2 * src);
+        P = ld4(a.srec + 2 * src + 1);
+        if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * src); Be = ld4(a.sadj + 2 * src + 1); }
+      }
+      unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
+    }
+  }
+  if (out >= 0) {
+    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
+    V4<R>* o = a.part + (size_t)per * out;
+    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
+    if (a.per_query) {
+      a.per_query[3 * out] = c_dir;
+      a.per_query[3 * out + 1] = c_app;
+      a.per_query[3 * out + 2] = c_vis;
+    }
+  }
+  if (a.totals) {
+    unsigned long long d = c_dir, p = c_app, v = c_vis;
+    for (int o = 16; o > 0; o >>= 1) {
+      d += __shfl_down_sync(0xffffffffu, d, o);
+      p += __shfl_down_sync(0xffffffffu, p, o);
+      v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.totals, d);
+      atomicAdd(a.totals + 1, p);
+      atomicAdd(a.totals + 2, v);
+    }
+  }
+}
+
+static int bh_kernel_choice() {
+  static int v = [] {
+    const char* e = std::getenv("GS_BH_KERNEL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <typename R>
 int launch(int mode, const BhArgs<R>& a, cudaStream_t st) {
   const int nb = std::max(1, (a.nq + kBhNT - 1) / kBhNT);
-  if (mode == kBhRhs) k_bh<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
-  else if (mode == kBhHess) k_bh<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
-  else k_bh<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+  if (bh_kernel_choice() == 1) {
+    if (mode == kBhRhs) k_bh_ws<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
+    else if (mode == kBhHess) k_bh_ws<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
+    else k_bh_ws<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+  } else {
+    if (mode == kBhRhs) k_bh<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
+    else if (mode == kBhHess) k_bh<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
+    else k_bh<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+  }
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }

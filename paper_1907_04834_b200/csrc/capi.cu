@@ -495,6 +495,13 @@ gs_status gs_flow_profile_read(gs_flow* f, double* kernel_ms, int64_t* kernel_la
   return GS_OK;
 }
 
+gs_status gs_flow_profile_phases(gs_flow* f, double* ms, int64_t* counts, int32_t channels) {
+  if (!f || !f->timer) return bad_arg("profiling not enabled");
+  GS_CUDA_OK(cudaStreamSynchronize(f->ctx->stream));
+  for (int c = 0; c < channels && c < KTimer::kChannels; ++c) ms[c] = f->timer->drain(c, counts + c);
+  return GS_OK;
+}
+
 gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
   if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
   f->shard_begin = begin;

@@ -41,10 +41,12 @@ struct DBuf {
 };
 
 // Optional event timing of the dominant kernels inside a flow (bench roofline):
-// channel 0 = the O(N^2) / traversal kernel, channel 1 = the tree build.
+// channel 0 = the O(N^2) / traversal kernel, channel 1 = the tree build,
+// 2..5 = tree-build phases (bbox+keys, sort, topology, aggregates).
 struct KTimer {
-  std::vector<cudaEvent_t> ev[2];
-  size_t used[2] = {0, 0};
+  static constexpr int kChannels = 8;
+  std::vector<cudaEvent_t> ev[kChannels];
+  size_t used[kChannels] = {0, 0, 0, 0, 0, 0, 0, 0};
   void mark(int ch, cudaStream_t st) {
     if (used[ch] == ev[ch].size()) {
       cudaEvent_t e;

@@ -64,17 +64,32 @@ __global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, doubl
 }
 
 // root = [lo - pad, hi + pad], pad = 1e-9 * (hi - lo)   (octree.cpp:9,27-35)
-__global__ void k_bbox_final(const double* part, int nb, double* root) {
-  if (threadIdx.x >= 3) return;
-  const int a = threadIdx.x;
-  double lo = part[a], hi = part[3 + a];
-  for (int b = 1; b < nb; ++b) {
-    lo = fmin(lo, part[6 * b + a]);
-    hi = fmax(hi, part[6 * b + 3 + a]);
+__global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, double* root) {
+  __shared__ double s[6][kNT / 32];
+  double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int b = threadIdx.x; b < nb; b += kNT)
+#pragma unroll
+    for (int a = 0; a < 6; ++a) v[a] = a < 3 ? fmin(v[a], part[6 * b + a]) : fmax(v[a], part[6 * b + a]);
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_down_sync(0xffffffffu, v[a], o);
+      v[a] = a < 3 ? fmin(v[a], w) : fmax(v[a], w);
+    }
+    if ((threadIdx.x & 31) == 0) s[a][threadIdx.x >> 5] = v[a];
   }
-  const double pad = __dmul_rn(__dsub_rn(hi, lo), 1e-9);
-  root[a] = __dsub_rn(lo, pad);
-  root[3 + a] = __dadd_rn(hi, pad);
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int a = threadIdx.x;
+    double lo = s[a][0], hi = s[3 + a][0];
+    for (int w = 1; w < kNT / 32; ++w) {
+      lo = fmin(lo, s[a][w]);
+      hi = fmax(hi, s[3 + a][w]);
+    }
+    const double pad = __dmul_rn(__dsub_rn(hi, lo), 1e-9);
+    root[a] = __dsub_rn(lo, pad);
+    root[3 + a] = __dadd_rn(hi, pad);
+  }
 }
 
 // ------------------------------------------------------------------ keys ---
@@ -125,7 +140,39 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t* keys, int64_t
     if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  ghist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  ghist[(int64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];  // tile-major
+}
+
+// ghist[tile][digit] -> exclusive prefix over tiles per digit; row ntiles holds
+// the exclusive prefix over digit totals (the digit's base offset).
+__global__ void __launch_bounds__(256) k_rs_digit_scan(unsigned* ghist, int ntiles) {
+  __shared__ unsigned tot[256];
+  const int d = threadIdx.x;
+  unsigned run = 0;
+  int t = 0;
+  for (; t + 4 <= ntiles; t += 4) {
+    const unsigned a = ghist[(int64_t)t * 256 + d], b = ghist[(int64_t)(t + 1) * 256 + d],
+                   c = ghist[(int64_t)(t + 2) * 256 + d], e = ghist[(int64_t)(t + 3) * 256 + d];
+    ghist[(int64_t)t * 256 + d] = run;
+    ghist[(int64_t)(t + 1) * 256 + d] = run + a;
+    ghist[(int64_t)(t + 2) * 256 + d] = run + a + b;
+    ghist[(int64_t)(t + 3) * 256 + d] = run + a + b + c;
+    run += a + b + c + e;
+  }
+  for (; t < ntiles; ++t) {
+    const unsigned a = ghist[(int64_t)t * 256 + d];
+    ghist[(int64_t)t * 256 + d] = run;
+    run += a;
+  }
+  tot[d] = run;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const unsigned v = d >= o ? tot[d - o] : 0u;
+    __syncthreads();
+    tot[d] += v;
+    __syncthreads();
+  }
+  ghist[(int64_t)ntiles * 256 + d] = tot[d] - run;
 }
 
 // exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
@@ -186,7 +233,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
   __syncthreads();
   {
     const unsigned d = threadIdx.x;
-    unsigned run = ghist[(int64_t)d * ntiles + blockIdx.x];
+    unsigned run = ghist[(int64_t)blockIdx.x * 256 + d] + ghist[(int64_t)ntiles * 256 + d];
     for (int w = 0; w < kRsNT / 32; ++w) {
       const unsigned t = wh[w][d];
       wh[w][d] = run;
@@ -566,13 +613,14 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.scal.ensure(64));
   const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
   GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
+  kt_mark(2, st);
   // 1. padded root box (or the caller's explicit root cell)
   if (root_box) {
     GS_CUDA_OK(cudaMemcpyAsync(t.root.ptr, root_box, 6 * sizeof(double), cudaMemcpyHostToDevice, st));
   } else {
     if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
     else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
-    k_bbox_final<<<1, 32, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+    k_bbox_final<<<1, kNT, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
   }
   // 2. keys
   const int nb = nblocks(n, kNT);
@@ -581,18 +629,20 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   else
     k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), t.tmp_v.as<int>());
   GS_CUDA_OK(cudaGetLastError());
+  kt_mark(2, st);
+  kt_mark(3, st);
   // 3. stable radix sort of key_hi (values: point index), 8 passes of 8 bits
   GS_CUDA_OK(cudaMemcpyAsync(t.skey_hi.ptr, t.key_hi.ptr, 8 * n, cudaMemcpyDeviceToDevice, st));
   GS_CUDA_OK(cudaMemcpyAsync(t.perm.ptr, t.tmp_v.ptr, 4 * n, cudaMemcpyDeviceToDevice, st));
   const int ntiles = nblocks(n, kRsTile);
-  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * ntiles));
+  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
   uint64_t* ka = t.skey_hi.as<uint64_t>();
   uint64_t* kb = t.tmp_k.as<uint64_t>();
   int* va = t.perm.as<int>();
   int* vb2 = t.tmp_v.as<int>();
   for (int shift = 0; shift < 64; shift += 8) {
     k_rs_hist<<<ntiles, kRsNT, 0, st>>>(ka, n, shift, t.hist.as<unsigned>(), ntiles);
-    k_rs_scan<<<1, 1024, 0, st>>>(t.hist.as<unsigned>(), (int64_t)256 * ntiles);
+    k_rs_digit_scan<<<1, 256, 0, st>>>(t.hist.as<unsigned>(), ntiles);
     k_rs_scatter<<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, shift, t.hist.as<unsigned>(), ntiles);
     std::swap(ka, kb);
     std::swap(va, vb2);
@@ -601,6 +651,8 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_CUDA_OK(cudaGetLastError());
   k_fix_ties<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.perm.as<int>(), t.key_lo.as<uint64_t>(), n);
   k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
+  kt_mark(3, st);
+  kt_mark(4, st);
   // 4. topology
   k_lcp<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>());
   k_count<<<nb, kNT, 0, st>>>(t.lcp.as<int>(), n, t.tmp_v.as<int>());
@@ -627,6 +679,8 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
                               t.first.as<int>(), n, t.meta.as<int4>(), t.parent.as<int>());
   const int mb = nblocks(m, kNT);
   k_nchild<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.nchild.as<int>());
+  kt_mark(4, st);
+  kt_mark(5, st);
   // 5. leaf-order records + aggregates
   const int scaled = prec == kF32;
   void* squ = t.squ.ptr;  // unscaled q in leaf order
@@ -641,7 +695,9 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     k_aggregate<double><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>());
   GS_CUDA_OK(cudaGetLastError());
   (void)mb;
-  return tree_finalize_fwd(prec, t, kc, st);
+  const int fs = tree_finalize_fwd(prec, t, kc, st);
+  kt_mark(5, st);
+  return fs;
 }
 
 int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st) {

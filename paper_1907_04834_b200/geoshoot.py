@@ -419,6 +419,15 @@ class Flow:
         return {"kernel_ms": k.value, "kernel_launches": kl.value, "build_ms": b.value,
                 "builds": bl.value}
 
+    def profile_phases(self, channels: int = 6):
+        import numpy as _np
+        ms = _np.zeros(channels)
+        cnt = _np.zeros(channels, _np.int64)
+        self.gs.check(self.gs.lib.gs_flow_profile_phases(
+            self.h, _p(ms), cnt.ctypes.data_as(C.POINTER(C.c_int64)), channels))
+        names = ["kernel", "build", "bbox_keys", "sort", "topology", "aggregate", "c6", "c7"]
+        return {names[c]: {"ms": float(ms[c]), "count": int(cnt[c])} for c in range(channels)}
+
     # sharded stage API (see shard.py)
     def set_shard(self, begin: int, count: int):
         self.gs.check(self.gs.lib.gs_flow_set_shard(self.h, begin, count))

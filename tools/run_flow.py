@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--prec", default="f32", choices=["f32", "f64"])
     ap.add_argument("--euler", action="store_true")
     ap.add_argument("--sigma", type=float, default=0.0131)
+    ap.add_argument("--phases", action="store_true")
     a = ap.parse_args()
     import numpy as np
     from paper_1907_04834_b200 import BARNES_HUT, EULER, EXACT, F32, F64, RK4, Geoshoot, ShootingConfig
@@ -38,9 +39,9 @@ def main():
     f.advance(a.steps)
     f.sync()
     dt = time.perf_counter() - t0
-    pr = f.profile_read()
+    pr = f.profile_phases() if a.phases else f.profile_read()
     print(json.dumps({"backend": a.backend, "n": a.n, "steps": a.steps, "wall_s": dt,
-                      "steps_per_s": a.steps / dt, **pr}))
+                      "steps_per_s": a.steps / dt, "profile": pr}))
 
 
 if __name__ == "__main__":
