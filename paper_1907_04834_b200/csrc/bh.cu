@@ -57,7 +57,8 @@ struct BhArgs {
   const V4<R>* squ;   // [n] unscaled q
   const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
   const int* perm;
-  int n, m, nq, tgt_begin, n_tgt;
+  int n, nq, tgt_begin, n_tgt;
+  const int* mp;  // node count on the device (first[n])
   const V4<R>* ev;  // VEL eval records
   double kap, kc0x, kc0y, kc0z;
   double T2;         // exact gate threshold on d2
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
 #pragma unroll
   for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
   uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  const int m = *a.mp;
   int next = out >= 0 ? 0 : INT_MAX;
   const V4<R> zero = mk4<R>(0, 0, 0);
   for (;;) {
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
       }
       // past the last node (skip == m): this query is done; a non-advancing skip
       // (cannot happen on a valid tree) must never loop
-      if (next >= a.m || next <= nd) next = INT_MAX;
+      if (next >= m || next <= nd) next = INT_MAX;
     }
     const unsigned rm = __ballot_sync(0xffffffffu, ranged);
     if (rm) {
@@ -292,14 +294,15 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
 #pragma unroll
   for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
   uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  const int m = *a.mp;
   int next = out >= 0 ? 0 : INT_MAX;
   int j = 0, je = -1;  // pending direct range
   const V4<R> zero = mk4<R>(0, 0, 0);
-  while (__any_sync(0xffffffffu, next < a.m || j <= je)) {
+  while (__any_sync(0xffffffffu, next < m || j <= je)) {
     bool have = false;
     bool approx = false;
     int src = 0;
-    if (j > je && next < a.m) {
+    if (j > je && next < m) {
       const int nd = next;
       const int4 mi = a.meta[nd];
       const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
@@ -405,7 +408,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.sadj = t.sadj.as<V4<R>>();
   a.perm = t.perm.as<int>();
   a.n = (int)t.n;
-  a.m = (int)t.m;
+  a.mp = t.first.as<int>() + t.n;
   a.tgt_begin = q.tgt_begin;
   a.n_tgt = q.n_tgt;
   a.nq = q.mode == kBhVel ? q.m : (int)t.n;
@@ -458,7 +461,7 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
                      cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats*) {
   DevTree& t = tree_for(w);
   kt_mark(1, st);
-  GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st));
+  GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st, nullptr, e.bad_step ? e.bad_step + 1 : nullptr));
   kt_mark(1, st);
   GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));

@@ -14,7 +14,8 @@ namespace gsb {
 // contiguous leaf-order positions [begin, end].
 struct DevTree {
   int prec = kF64;
-  int64_t n = 0, m = 0;
+  int64_t n = 0, m = -1;  // m: node count (-1 = only known on the device, first[n])
+  int64_t cap = 0;        // node slots allocated
   // per point (index order)
   DBuf key_hi, key_lo;  // u64
   // per leaf-order position
@@ -47,8 +48,13 @@ struct DevTree {
 
 // root_box (host, {lo xyz, hi xyz}) overrides the padded bounding box
 // (Octree(cell_min, cell_max) + insert, octree.hpp:38-51).
+// overflow (device int, optional) is set when the tree needs more than the
+// 4n + 64 node slots; the node count itself stays on the device.
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
-               DevTree& t, cudaStream_t st, const double* root_box = nullptr);
+               DevTree& t, cudaStream_t st, const double* root_box = nullptr,
+               int* overflow = nullptr);
+// exact node count (host round trip on first call after a build)
+int64_t tree_node_count(DevTree& t, cudaStream_t st);
 // (re)writes the interaction coordinates (FP32: scaled by kc.kappa) and centroids
 int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, cudaStream_t st);
 // adj: [n][2] records (alpha, beta) by point index; node sums + leaf-order copy
@@ -56,7 +62,7 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st);
 // leaf-order copy of per-point adjoints only (node sums untouched)
 int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t st);
 // host copies for gs_tree_download
-int tree_download(const DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
+int tree_download(DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
                   uint64_t* key_lo, int32_t* level, int32_t* parent, int32_t* skip,
                   int32_t* range, double* boxes, double* sums, uint32_t* count);
 

@@ -329,7 +329,7 @@ int flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
     GS_TRY(f->ks.ensure(rb));
   }
   GS_TRY(f->flags.ensure(64));
-  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, sizeof(int), c->stream));  // bad_step = +big
+  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), c->stream));  // bad_step = +big, no overflow
   GS_TRY(f->bh.stats.ensure(64));
   GS_CUDA_OK(cudaMemsetAsync(f->bh.stats.ptr, 0, 64, c->stream));
   return GS_OK;
@@ -354,7 +354,7 @@ int flow_upload(gs_flow* f, const double* q0, const double* p0) {
   GS_TRY(upload_records(f->ctx, f->prec, q0, p0, f->n, f->rec));
   f->steps_done = 0;
   f->have_energy_part = false;
-  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, sizeof(int), f->ctx->stream));
+  GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), f->ctx->stream));
   return GS_OK;
 }
 
@@ -369,10 +369,15 @@ int flow_advance(gs_flow* f, int steps) {
 
 // returns GS_NONFINITE (and records the step) if the device flag was raised
 int flow_check(gs_flow* f) {
-  int bad = 0;
-  GS_CUDA_OK(cudaMemcpyAsync(&bad, f->flags.ptr, sizeof(int), cudaMemcpyDeviceToHost,
+  int fl[2] = {0, 0};
+  GS_CUDA_OK(cudaMemcpyAsync(fl, f->flags.ptr, sizeof fl, cudaMemcpyDeviceToHost,
                              f->ctx->stream));
   GS_TRY(sync(f->ctx));
+  const int bad = fl[0];
+  if (fl[1] == 1) {
+    g_err = "octree node capacity (4n + 64) exceeded: degenerate point clustering";
+    return GS_INTERNAL;
+  }
   if (bad != 0x7f7f7f7f) {
     g_nonfinite = bad;
     g_err = "non-finite state at timestep " + std::to_string(bad);
@@ -1087,7 +1092,9 @@ void gs_tree_free(gs_tree* tr) {
   delete tr;
 }
 
-int64_t gs_tree_node_count(const gs_tree* tr) { return tr ? tr->t.m : 0; }
+int64_t gs_tree_node_count(const gs_tree* tr) {
+  return tr ? tree_node_count(const_cast<gs_tree*>(tr)->t, tr->ctx->stream) : 0;
+}
 int64_t gs_tree_point_count(const gs_tree* tr) { return tr ? tr->t.n : 0; }
 
 gs_status gs_tree_accumulate_adjoints(gs_tree* tr, const double* alpha, const double* beta) {
@@ -1101,7 +1108,7 @@ gs_status gs_tree_download(const gs_tree* tr, int32_t* order, uint64_t* key_hi, 
                            int32_t* level, int32_t* parent, int32_t* skip, int32_t* range,
                            double* boxes, double* sums, uint32_t* count) {
   if (!tr) return bad_arg("null tree");
-  return (gs_status)tree_download(tr->t, tr->ctx->stream, order, key_hi, key_lo, level, parent,
+  return (gs_status)tree_download(const_cast<gs_tree*>(tr)->t, tr->ctx->stream, order, key_hi, key_lo, level, parent,
                                   skip, range, boxes, sums, count);
 }
 

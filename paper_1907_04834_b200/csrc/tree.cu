@@ -19,6 +19,9 @@
 // t+1, position a starts the internal nodes of levels L[a-1]+1 .. min(L[a],31)
 // and one leaf; ordering nodes by (start, level) is the depth-first pre-order.
 // Everything below is that construction, one thread per position/node.
+#include <chrono>
+#include <cstdlib>
+
 #include "bh.h"
 
 namespace gsb {
@@ -356,9 +359,13 @@ __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, c
 }
 
 __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
-                        int64_t n, int4* meta, int* parent) {
+                        int64_t n, int64_t cap, int4* meta, int* parent, int* overflow) {
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (a >= n) return;
+  if (first[n] > cap) {  // more nodes than the arrays hold (degenerate clustering)
+    if (a == 0 && overflow) atomicExch(overflow, 1);
+    return;
+  }
   int Lm, Lp, ci, lf;
   starts(L, n, a, Lm, Lp, ci, lf);
   const int base = first[a];
@@ -385,9 +392,9 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
   }
 }
 
-__global__ void k_nchild(const int4* meta, int64_t m, int* nchild) {
+__global__ void k_nchild(const int4* meta, const int* mp, int* nchild) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= m) return;
+  if (i >= *mp) return;
   const int4 mi = meta[i];
   int c = 0;
   if (!(mi.w & 1))
@@ -442,9 +449,10 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
                                                    const int* parent, const int* nchild,
                                                    int* counter, const V4<R>* squ,
                                                    const V4<R>* srec, const V4<R>* sadj,
-                                                   V4<R>* lo, V4<R>* hi, double4* s0, double4* s1) {
+                                                   V4<R>* lo, V4<R>* hi, double4* s0, double4* s1,
+                                                   int64_t cap) {
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (a >= n) return;
+  if (a >= n || first[n] > cap) return;
   int Lm, Lp, ci, lf;
   starts(L, n, a, Lm, Lp, ci, lf);
   if (!lf) return;
@@ -500,11 +508,11 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 // traversal-format node fields: centroid = position_sum * (1 / count)
 // (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
 template <typename R>
-__global__ void k_finalize(int mode, const int4* meta, int64_t m, const double4* s0,
+__global__ void k_finalize(int mode, const int4* meta, const int* mp, const double4* s0,
                            const double4* s1, double kap, double c0x, double c0y, double c0z,
                            int scaled, V4<R>* o0, V4<R>* o1) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= m) return;
+  if (i >= *mp) return;
   const int4 mi = meta[i];
   const int cnt = mi.z - mi.y + 1;
   const double inv = 1.0 / cnt;
@@ -593,7 +601,7 @@ static int scan_ints(const int* in, int64_t n, int* out, DBuf& scratch, cudaStre
 }
 
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
-               DevTree& t, cudaStream_t st, const double* root_box) {
+               DevTree& t, cudaStream_t st, const double* root_box, int* overflow) {
   t.prec = prec;
   t.n = n;
   t.kc = kc;
@@ -657,28 +665,29 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   k_lcp<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>());
   k_count<<<nb, kNT, 0, st>>>(t.lcp.as<int>(), n, t.tmp_v.as<int>());
   GS_TRY_INT(scan_ints(t.tmp_v.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
-  int m = 0;
-  GS_CUDA_OK(cudaMemcpyAsync(&m, t.first.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
-  GS_CUDA_OK(cudaStreamSynchronize(st));
-  t.m = m;
-  // node arrays with 25% headroom: the node count drifts from stage to stage
-  // and a re-allocation (cudaFree/cudaMalloc) would stall the stream
-  const int64_t mc = m + m / 4 + 64;
-  GS_TRY_INT(t.meta.ensure(sizeof(int4) * mc));
-  GS_TRY_INT(t.parent.ensure(4 * mc));
-  GS_TRY_INT(t.nchild.ensure(4 * mc));
-  GS_TRY_INT(t.counter.ensure(4 * mc));
-  GS_TRY_INT(t.lo.ensure(vb * mc));
-  GS_TRY_INT(t.hi.ensure(vb * mc));
-  GS_TRY_INT(t.cen.ensure(vb * mc));
-  GS_TRY_INT(t.mom.ensure(vb * mc));
-  GS_TRY_INT(t.psum.ensure(sizeof(double4) * mc));
-  GS_TRY_INT(t.msum.ensure(sizeof(double4) * mc));
+  // The node count m = first[n] stays on the device: node arrays are sized
+  // for 4n + 64 nodes (m ~ 1.5n for volumes and surfaces) and every kernel
+  // reads m from first[n]; more nodes than that (degenerate clustering) raise
+  // *overflow instead of writing out of bounds. No host round trip per build.
+  t.m = -1;
+  const int64_t cap = 4 * n + 64;
+  t.cap = cap;
+  GS_TRY_INT(t.meta.ensure(sizeof(int4) * cap));
+  GS_TRY_INT(t.parent.ensure(4 * cap));
+  GS_TRY_INT(t.nchild.ensure(4 * cap));
+  GS_TRY_INT(t.counter.ensure(4 * cap));
+  GS_TRY_INT(t.lo.ensure(vb * cap));
+  GS_TRY_INT(t.hi.ensure(vb * cap));
+  GS_TRY_INT(t.cen.ensure(vb * cap));
+  GS_TRY_INT(t.mom.ensure(vb * cap));
+  GS_TRY_INT(t.psum.ensure(sizeof(double4) * cap));
+  GS_TRY_INT(t.msum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.squ.ensure(vb * n));
   k_nodes<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
-                              t.first.as<int>(), n, t.meta.as<int4>(), t.parent.as<int>());
-  const int mb = nblocks(m, kNT);
-  k_nchild<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.nchild.as<int>());
+                              t.first.as<int>(), n, cap, t.meta.as<int4>(), t.parent.as<int>(),
+                              overflow);
+  const int mb = nblocks(cap, kNT);
+  k_nchild<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>());
   kt_mark(4, st);
   kt_mark(5, st);
   // 5. leaf-order records + aggregates
@@ -688,11 +697,11 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<float4>(), (float4*)squ);
   else
     k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<double4>(), (double4*)squ);
-  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * m, st));
+  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
   if (prec == kF32)
-    k_aggregate<float><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>());
+    k_aggregate<float><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
   else
-    k_aggregate<double><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>());
+    k_aggregate<double><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
   GS_CUDA_OK(cudaGetLastError());
   (void)mb;
   const int fs = tree_finalize_fwd(prec, t, kc, st);
@@ -701,14 +710,14 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
 }
 
 int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st) {
-  const int64_t m = t.m;
-  const int mb = nblocks(m, kNT);
+  const int* mp = t.first.as<int>() + t.n;
+  const int mb = nblocks(t.cap, kNT);
   const int scaled = prec == kF32;
   t.kc = kc;
   if (prec == kF32)
-    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), m, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>());
   else
-    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), m, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>());
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
@@ -735,24 +744,24 @@ int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t 
 }
 
 int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
-  const int64_t n = t.n, m = t.m;
+  const int64_t n = t.n, cap = t.cap;
+  const int* mp = t.first.as<int>() + n;
   const size_t vb = vec_bytes(prec);
   GS_TRY_INT(t.sadj.ensure(2 * vb * n));
-  const int64_t mc = m + m / 4 + 64;
-  GS_TRY_INT(t.asum.ensure(sizeof(double4) * mc));
-  GS_TRY_INT(t.bsum.ensure(sizeof(double4) * mc));
-  GS_TRY_INT(t.nadj_a.ensure(vb * mc));
-  GS_TRY_INT(t.nadj_b.ensure(vb * mc));
-  const int nb = nblocks(n, kNT), mb = nblocks(m, kNT);
-  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * m, st));
+  GS_TRY_INT(t.asum.ensure(sizeof(double4) * cap));
+  GS_TRY_INT(t.bsum.ensure(sizeof(double4) * cap));
+  GS_TRY_INT(t.nadj_a.ensure(vb * cap));
+  GS_TRY_INT(t.nadj_b.ensure(vb * cap));
+  const int nb = nblocks(n, kNT), mb = nblocks(cap, kNT);
+  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
   if (prec == kF32) {
     k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
-    k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>());
-    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), m, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<float4>(), t.nadj_b.as<float4>());
+    k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
+    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<float4>(), t.nadj_b.as<float4>());
   } else {
     k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
-    k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>());
-    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), m, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<double4>(), t.nadj_b.as<double4>());
+    k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
+    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<double4>(), t.nadj_b.as<double4>());
   }
   GS_CUDA_OK(cudaGetLastError());
   t.adj_valid = true;
@@ -798,10 +807,26 @@ int dl(T* host, const DBuf& d, int64_t count, cudaStream_t st) {
 
 }  // namespace
 
-int tree_download(const DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
+int64_t tree_node_count(DevTree& t, cudaStream_t st) {
+  if (t.m < 0) {
+    int m = 0;
+    if (cudaMemcpyAsync(&m, t.first.as<int>() + t.n, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return -1;
+    t.m = m;
+  }
+  return t.m;
+}
+
+int tree_download(DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
                   uint64_t* key_lo, int32_t* level, int32_t* parent, int32_t* skip,
                   int32_t* range, double* boxes, double* sums, uint32_t* count) {
-  const int64_t n = t.n, m = t.m;
+  const int64_t n = t.n, m = tree_node_count(t, st);
+  if (m < 0) return cuda_fail(cudaGetLastError(), "tree_node_count", __FILE__, __LINE__);
+  if (m > t.cap) {
+    set_error("octree node capacity exceeded (degenerate clustering)");
+    return GS_INTERNAL;
+  }
   DBuf b_level, b_par, b_skip, b_range, b_boxes, b_sums, b_count;
   if (level) GS_TRY_INT(b_level.ensure(4 * m));
   if (parent) GS_TRY_INT(b_par.ensure(4 * m));
