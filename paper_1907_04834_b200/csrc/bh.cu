@@ -53,6 +53,7 @@ struct BhArgs {
   const V4<R>* mom;
   const V4<R>* nadj_a;
   const V4<R>* nadj_b;
+  const V4<R>* nrec;  // [m][2] compact node records {lo, code} {hi, begin}
   const V4<R>* srec;  // [n][2] interaction coords (scaled FP32), p
   const V4<R>* squ;   // [n] unscaled q
   const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
@@ -112,6 +113,9 @@ __device__ __forceinline__ float kern(float dx, float dy, float dz, const BhArgs
 __device__ __forceinline__ double kern(double dx, double dy, double dz, const BhArgs<double>& a) {
   return exp(-(dx * dx + dy * dy + dz * dz) * a.inv_two_s);
 }
+
+__device__ __forceinline__ int code_of(float v) { return __float_as_int(v); }
+__device__ __forceinline__ int code_of(double v) { return (int)v; }
 
 template <typename R>
 struct Acc {
@@ -304,22 +308,26 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
     int src = 0;
     if (j > je && next < m) {
       const int nd = next;
-      const int4 mi = a.meta[nd];
-      const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
+      V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);  // one 32-B sector (FP32)
+      const int code = code_of(l.w);
+      const int begin = code_of(h.w);
       ++c_vis;
-      next = mi.x;
-      if (mi.w & 1) {  // leaf: its point(s) directly
-        j = mi.y;
-        je = mi.z;
+      next = code & 0x3fffffff;
+      if (code < 0) {  // single-point leaf
+        j = begin;
+        je = begin;
+      } else if (code & 0x40000000) {  // depth-32 bucket: all its points
+        j = begin;
+        je = begin + code_of(ld4(a.mom + nd).w) - 1;
       } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
         approx = true;
         have = true;
         src = nd;
         ++c_app;
       } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
-        j = mi.y;
-        je = mi.z;
-        c_vis += (uint32_t)(mi.x - nd - 1);
+        j = begin;
+        je = begin + code_of(ld4(a.mom + nd).w) - 1;
+        c_vis += (uint32_t)(next - nd - 1);
       } else {
         next = nd + 1;
       }
@@ -369,6 +377,123 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
   }
 }
 
+// Software-pipelined work-stream variant: the loads of iteration i+1 (the
+// next node's compact record + its centroid/momentum, or the next range
+// point) are issued before the interaction of iteration i is computed, so one
+// iteration of arithmetic covers the next iteration's memory latency.
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
+  const int qi = blockIdx.x * kBhNT + threadIdx.x;
+  const bool valid = qi < a.nq;
+  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
+  int out = -1;
+  if (valid) {
+    if (MODE == kBhVel) {
+      x = ld4(a.ev + 2 * qi);
+      if (sizeof(R) == 4)
+        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
+                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
+                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
+      else
+        xs = x;
+      out = qi;
+    } else {
+      const int t = qi;
+      x = ld4(a.squ + t);
+      xs = ld4(a.srec + 2 * t);
+      px = ld4(a.srec + 2 * t + 1);
+      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
+      const int i = a.perm[t] - a.tgt_begin;
+      out = (i >= 0 && i < a.n_tgt) ? i : -1;
+    }
+  }
+  Acc<R> acc;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
+  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  const int m = *a.mp;
+  int next = out >= 0 ? 0 : INT_MAX;
+  int j = 0, je = -1;
+  const V4<R> zero = mk4<R>(0, 0, 0);
+  // prefetched node (record, centroid, momentum[, adjoint aggregates]) and source
+  V4<R> NL = zero, NH = zero, NC = zero, NM = zero, NA = zero, NB = zero;
+  V4<R> SQ = zero, SP = zero, SA = zero, SB = zero;
+  if (next < m) {
+    NL = ld4(a.nrec); NH = ld4(a.nrec + 1); NC = ld4(a.cen); NM = ld4(a.mom);
+    if (MODE == kBhHess) { NA = ld4(a.nadj_a); NB = ld4(a.nadj_b); }
+  }
+  while (__any_sync(0xffffffffu, next < m || j <= je)) {
+    bool have = false;
+    V4<R> Q = zero, P = zero, Al = zero, Be = zero;
+    if (j <= je) {  // continue the pending direct range (point j prefetched)
+      Q = SQ; P = SP; Al = SA; Be = SB;
+      have = true;
+      ++j;
+      ++c_dir;
+    } else if (next < m) {  // visit node `next` (prefetched)
+      const int nd = next;
+      const int code = code_of(NL.w);
+      const int begin = code_of(NH.w);
+      ++c_vis;
+      next = code & 0x3fffffff;
+      if (code < 0) {  // single-point leaf
+        j = begin;
+        je = begin;
+      } else if (code & 0x40000000) {  // depth-32 bucket
+        j = begin;
+        je = begin + code_of(NM.w) - 1;
+      } else if (gate(NL, NH, x, a)) {  // far: one aggregate term
+        Q = NC; P = NM; Al = NA; Be = NB;
+        have = true;
+        ++c_app;
+      } else if (all_inside(NL, NH, x, a.thr2_in)) {  // whole subtree direct
+        j = begin;
+        je = begin + code_of(NM.w) - 1;
+        c_vis += (uint32_t)(next - nd - 1);
+      } else {
+        next = nd + 1;
+      }
+      if (next <= nd) next = INT_MAX;  // never loop on a corrupt skip
+    }
+    // issue the next iteration's loads before this iteration's arithmetic
+    if (j <= je) {
+      SQ = ld4(a.srec + 2 * j);
+      SP = ld4(a.srec + 2 * j + 1);
+      if (MODE == kBhHess) { SA = ld4(a.sadj + 2 * j); SB = ld4(a.sadj + 2 * j + 1); }
+    } else if (next < m) {
+      NL = ld4(a.nrec + 2 * next);
+      NH = ld4(a.nrec + 2 * next + 1);
+      NC = ld4(a.cen + next);
+      NM = ld4(a.mom + next);
+      if (MODE == kBhHess) { NA = ld4(a.nadj_a + next); NB = ld4(a.nadj_b + next); }
+    }
+    if (have) unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
+  }
+  if (out >= 0) {
+    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
+    V4<R>* o = a.part + (size_t)per * out;
+    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
+    if (a.per_query) {
+      a.per_query[3 * out] = c_dir;
+      a.per_query[3 * out + 1] = c_app;
+      a.per_query[3 * out + 2] = c_vis;
+    }
+  }
+  if (a.totals) {
+    unsigned long long d = c_dir, p = c_app, v = c_vis;
+    for (int o = 16; o > 0; o >>= 1) {
+      d += __shfl_down_sync(0xffffffffu, d, o);
+      p += __shfl_down_sync(0xffffffffu, p, o);
+      v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.totals, d);
+      atomicAdd(a.totals + 1, p);
+      atomicAdd(a.totals + 2, v);
+    }
+  }
+}
+
 static int bh_kernel_choice() {
   static int v = [] {
     const char* e = std::getenv("GS_BH_KERNEL");
@@ -380,7 +505,11 @@ static int bh_kernel_choice() {
 template <typename R>
 int launch(int mode, const BhArgs<R>& a, cudaStream_t st) {
   const int nb = std::max(1, (a.nq + kBhNT - 1) / kBhNT);
-  if (bh_kernel_choice() == 1) {
+  if (bh_kernel_choice() == 2) {
+    if (mode == kBhRhs) k_bh_pipe<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
+    else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
+    else k_bh_pipe<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+  } else if (bh_kernel_choice() == 1) {
     if (mode == kBhRhs) k_bh_ws<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
     else if (mode == kBhHess) k_bh_ws<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
     else k_bh_ws<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
@@ -404,6 +533,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.nadj_a = t.nadj_a.as<V4<R>>();
   a.nadj_b = t.nadj_b.as<V4<R>>();
   a.srec = t.srec.as<V4<R>>();
+  a.nrec = t.nrec.as<V4<R>>();
   a.squ = t.squ.as<V4<R>>();
   a.sadj = t.sadj.as<V4<R>>();
   a.perm = t.perm.as<int>();

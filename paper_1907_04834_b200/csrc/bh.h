@@ -32,7 +32,8 @@ struct DevTree {
   DBuf nchild;          // i32
   DBuf counter;         // i32 bottom-up arrival counters
   DBuf lo, hi;          // V4<R> tight AABB (unscaled)
-  DBuf cen, mom;        // V4<R> centroid (scaled in FP32) / momentum sum
+  DBuf cen, mom;        // V4<R> centroid (scaled in FP32) + count / momentum sum + count bits
+  DBuf nrec;            // [cap][2] V4<R> compact traversal record {lo, code} {hi, begin}
   DBuf nadj_a, nadj_b;  // V4<R> alpha sum / beta mean
   DBuf psum, msum;      // double4 exact-order-independent aggregates
   DBuf asum, bsum;      // double4

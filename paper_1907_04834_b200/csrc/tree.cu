@@ -507,16 +507,32 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 
 // traversal-format node fields: centroid = position_sum * (1 / count)
 // (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
+// Compact traversal record (2 vec4 per node, one 32-B sector in FP32):
+//   {lo.xyz, code} {hi.xyz, begin}, code = skip | single-point leaf << 31 |
+//   bucket leaf << 30; the point count rides in mom.w.
+__device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
+__device__ __forceinline__ double ival(double, int v) { return (double)v; }
+
 template <typename R>
 __global__ void k_finalize(int mode, const int4* meta, const int* mp, const double4* s0,
                            const double4* s1, double kap, double c0x, double c0y, double c0z,
-                           int scaled, V4<R>* o0, V4<R>* o1) {
+                           int scaled, V4<R>* o0, V4<R>* o1, const V4<R>* lo = nullptr,
+                           const V4<R>* hi = nullptr, V4<R>* nrec = nullptr) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= *mp) return;
   const int4 mi = meta[i];
   const int cnt = mi.z - mi.y + 1;
   const double inv = 1.0 / cnt;
   const double4 a = s0[i], b = s1[i];
+  if (mode == 0 && nrec) {
+    const bool leaf = mi.w & 1;
+    const int code = mi.x | ((leaf && cnt == 1) ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0);
+    V4<R> l = ld4(lo + i), h = ld4(hi + i);
+    l.w = ival(R(0), code);
+    h.w = ival(R(0), mi.y);
+    st4(nrec + 2 * i, l);
+    st4(nrec + 2 * i + 1, h);
+  }
   if (mode == 0) {
     double cx = __dmul_rn(a.x, inv), cy = __dmul_rn(a.y, inv), cz = __dmul_rn(a.z, inv);
     if (scaled) {
@@ -527,7 +543,7 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
     } else {
       st4(o0 + i, mk4<R>(R(cx), R(cy), R(cz), R(cnt)));
     }
-    st4(o1 + i, mk4<R>(R(b.x), R(b.y), R(b.z)));
+    st4(o1 + i, mk4<R>(R(b.x), R(b.y), R(b.z), ival(R(0), cnt)));
   } else {
     st4(o0 + i, mk4<R>(R(a.x), R(a.y), R(a.z)));
     // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
@@ -680,6 +696,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.hi.ensure(vb * cap));
   GS_TRY_INT(t.cen.ensure(vb * cap));
   GS_TRY_INT(t.mom.ensure(vb * cap));
+  GS_TRY_INT(t.nrec.ensure(2 * vb * cap));
   GS_TRY_INT(t.psum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.msum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.squ.ensure(vb * n));
@@ -715,9 +732,9 @@ int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t
   const int scaled = prec == kF32;
   t.kc = kc;
   if (prec == kF32)
-    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.nrec.as<float4>());
   else
-    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.nrec.as<double4>());
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
