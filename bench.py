@@ -222,9 +222,17 @@ def run_ours(args):
     peak = ffma.value / 16.0 / 1e9
     mp = peaks_json()
     nominal = 148 * 128 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 16.0 / 1e9
+    traffic = None
+    try:  # dram bytes per launch of the same kernel from the committed ncu capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_rhs_traffic.json")))
+        if tj.get("n") == N and world == 1:
+            traffic = tj["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {
         "bound": "fp32-issue", "achieved": achieved, "peak": peak, "unit": "Gpair/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch (ncu, profiles/r01_rhs_traffic.json)",
         "peak_source": "live FFMA microbenchmark (gs_microbench kind 0): "
                        f"{ffma.value / 1e12:.2f} T lane-FFMA/s / 16 FP32 instructions per pair; "
                        "MEASURED_PEAKS.json has no FP32 figure",

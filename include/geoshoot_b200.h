@@ -252,6 +252,46 @@ int64_t gs_flow_record_bytes(const gs_flow* flow);
  * current step (Euler 1, RK4 4). */
 gs_status gs_flow_stage(gs_flow* flow, int32_t stage);
 
+/* ---- registration optimizer ------------------------------
+ * optimize(), optimizer.cpp:301-351: L-BFGS + strong-Wolfe line search over p0
+ * from p0 = 0, every objective/gradient one gs_evaluate on the device.
+ * OptimizerConfig + LineSearchConfig (core.hpp:190-202). */
+typedef struct gs_opt_config {
+  int32_t max_iterations;             /* 200 */
+  int32_t memory;                     /* 10 history pairs */
+  double gradient_tolerance;          /* 1e-6 (inf-norm) */
+  double relative_objective_tolerance;/* 1e-9 */
+  double sufficient_decrease;         /* Wolfe c1 = 1e-4 */
+  double curvature;                   /* Wolfe c2 = 0.9 (strong) */
+  int32_t max_trials;                 /* 20 evaluations per line search */
+} gs_opt_config;
+/* TerminationReason (optimizer.hpp:18-24), in declaration order. */
+enum {
+  GS_TERM_GRADIENT_TOLERANCE = 0,
+  GS_TERM_OBJECTIVE_TOLERANCE = 1,
+  GS_TERM_MAX_ITERATIONS = 2,
+  GS_TERM_LINE_SEARCH_FAILURE = 3,
+  GS_TERM_NON_FINITE = 4
+};
+gs_opt_config gs_default_opt_config(void);
+/* p_out: n x 3 optimal momenta. trace (optional): up to max_iterations + 1
+ * rows of {iter, total, energy, attachment, grad_inf, wall_ms} (the
+ * reference's trace CSV columns, optimizer.cpp:204-213); GS_NONFINITE if the
+ * objective is non-finite at p0 = 0 (NonFiniteObjectiveAtStart). */
+gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* opt, int64_t n,
+                      const double* q0, const double* target, double* p_out, int32_t* reason,
+                      int32_t* iterations, int32_t* evaluations, double* trace,
+                      int32_t* trace_len, gs_stats* stats);
+
+/* Batched independent registrations (BASELINE config 5, "replicas only"):
+ * subject b has n[b] points; each runs gs_optimize on its own context/stream
+ * and host thread so the device overlaps them. final_total[b] = objective at
+ * the returned p0. */
+gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_config* opt,
+                            int32_t batch, const int64_t* n, const double* const* q0,
+                            const double* const* target, double* const* p_out, int32_t* reasons,
+                            int32_t* iterations, int32_t* evaluations, double* final_total);
+
 /* ---- measured device peaks (roofline denominators) ----------------------------
  * kind 0: FP32 FFMA lane-ops/s (constant operands), 1: MUFU.EX2 lane-ops/s,
  * 2: FP64 DFMA lane-ops/s, 3: FP32 FFMA lane-ops/s with all-register operands. */

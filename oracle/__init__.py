@@ -274,6 +274,9 @@ class Ref:
             "ref_warp_points": [_i64, C.c_int, _d, _d, _i64, _d, C.c_double, C.c_int, C.c_int,
                                 C.c_double, _d],
             "ref_generate": [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64, _d],
+            "ref_optimize": [_i64, _d, _d, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
+                             C.c_int, _d, C.POINTER(C.c_int), C.POINTER(C.c_int), _d,
+                             C.POINTER(C.c_int)],
         }.items():
             getattr(L, name).argtypes = args
             getattr(L, name).restype = C.c_int
@@ -368,6 +371,20 @@ class Ref:
         self._chk(self.lib.ref_warp_points(tq.shape[1], tq.shape[0], _p(tq), _p(tp), len(x), _p(x),
                                            sigma, timesteps, backend, thr_mult, _p(y)))
         return y
+
+    def optimize(self, q0, target, sigma, lam, timesteps, backend=0, thr_mult=3.0,
+                 max_iterations=200):
+        q0, t = _c(q0), _c(target)
+        p = _vec(len(q0))
+        reason, iters, tl = C.c_int(), C.c_int(), C.c_int()
+        trace = np.zeros((max_iterations + 1, 6))
+        self._chk(self.lib.ref_optimize(len(q0), _p(q0), _p(t), sigma, lam, timesteps, backend,
+                                        thr_mult, max_iterations, _p(p), C.byref(reason),
+                                        C.byref(iters), _p(trace), C.byref(tl)))
+        names = ["gradient_tolerance", "objective_tolerance", "max_iterations",
+                 "line_search_failure", "non_finite"]
+        return {"p0": p, "reason": names[reason.value], "iterations": iters.value,
+                "trace": trace[:tl.value]}
 
     def validate_config(self, sigma, lam, timesteps, thr_mult):
         return self.lib.ref_validate_config(sigma, lam, timesteps, thr_mult)

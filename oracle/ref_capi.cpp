@@ -23,6 +23,7 @@
 #include "geoshoot/core.hpp"
 #include "geoshoot/kernel_exact.hpp"
 #include "geoshoot/octree.hpp"
+#include "geoshoot/optimizer.hpp"
 #include "geoshoot/parallel.hpp"
 #include "geoshoot/shooting.hpp"
 #include "geoshoot/synthetic.hpp"
@@ -382,6 +383,27 @@ int ref_warp_points(std::int64_t n, int states, const double* traj_q, const doub
                                    PointSet(vecs(x, m)),
                                    make_cfg(sigma, 1.0, timesteps, backend, thr_mult));
     store(y_out, y.data());
+  });
+}
+
+// optimize, optimizer.cpp:301-351 (threads = 0: process default)
+int ref_optimize(std::int64_t n, const double* q0, const double* target, double sigma,
+                 double lambda, int timesteps, int backend, double thr_mult, int max_iterations,
+                 double* p_out, int* reason, int* iterations, double* trace, int* trace_len) {
+  return guarded([&] {
+    ShootingConfig c = make_cfg(sigma, lambda, timesteps, backend, thr_mult);
+    c.optimizer.max_iterations = max_iterations;
+    auto [p, tr] = optimize(PointSet(vecs(q0, n)), PointSet(vecs(target, n)), c, nullptr, 0);
+    store(p_out, p.data());
+    *reason = static_cast<int>(tr.reason);
+    *iterations = tr.records.empty() ? 0 : tr.records.back().iteration;
+    for (std::size_t k = 0; k < tr.records.size(); ++k) {
+      const auto& r = tr.records[k];
+      double* o = trace + 6 * k;
+      o[0] = r.iteration; o[1] = r.total; o[2] = r.energy; o[3] = r.attachment;
+      o[4] = r.grad_inf; o[5] = r.wall_ms;
+    }
+    *trace_len = static_cast<int>(tr.records.size());
   });
 }
 

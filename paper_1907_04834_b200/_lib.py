@@ -56,6 +56,18 @@ class gs_stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class gs_opt_config(C.Structure):
+    _fields_ = [
+        ("max_iterations", C.c_int32),
+        ("memory", C.c_int32),
+        ("gradient_tolerance", C.c_double),
+        ("relative_objective_tolerance", C.c_double),
+        ("sufficient_decrease", C.c_double),
+        ("curvature", C.c_double),
+        ("max_trials", C.c_int32),
+    ]
+
+
 class gs_report(C.Structure):
     _fields_ = [
         ("energy", C.c_double),
@@ -123,6 +135,14 @@ SIGNATURES = [
     ("gs_flow_record_bytes", _i64, [_vp]),
     ("gs_flow_stage", _st, [_vp, C.c_int32]),
     ("gs_microbench", _st, [C.c_int, C.c_int32, _d]),
+    ("gs_default_opt_config", gs_opt_config, []),
+    ("gs_optimize_batch", _st, [C.c_int, C.POINTER(gs_config), C.POINTER(gs_opt_config), C.c_int32,
+                                C.POINTER(C.c_int64), C.POINTER(_d), C.POINTER(_d), C.POINTER(_d),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                _d]),
+    ("gs_optimize", _st, [_vp, C.POINTER(gs_config), C.POINTER(gs_opt_config), _i64, _d, _d, _d,
+                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), _d,
+                          C.POINTER(C.c_int32), C.POINTER(gs_stats)]),
 ]
 
 _lib = None

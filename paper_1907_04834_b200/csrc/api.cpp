@@ -4,6 +4,8 @@
 // mapped back to the reference's exception types. No arithmetic of the hot
 // path happens here.
 #include <algorithm>
+#include <cstdio>
+#include <ostream>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -12,6 +14,7 @@
 #include "geoshoot/core.hpp"
 #include "geoshoot/kernel_exact.hpp"
 #include "geoshoot/octree.hpp"
+#include "geoshoot/optimizer.hpp"
 #include "geoshoot/shooting.hpp"
 #include "geoshoot_b200.h"
 
@@ -474,6 +477,64 @@ Evaluation evaluate(const PointSet& q0, const MomentumSet& p0, const PointSet& t
   ev.stats.traversal = to_traversal(st);
   ev.stats.traversal_queries = st.traversal_queries;
   return ev;
+}
+
+// ---- optimizer ------------------------------------------------------------------
+const char* to_string(TerminationReason r) {
+  static const char* names[] = {"gradient_tolerance", "objective_tolerance", "max_iterations",
+                                "line_search_failure", "non_finite"};
+  return names[static_cast<int>(r)];
+}
+
+void OptimizationTrace::write_csv(std::ostream& os) const {
+  os << "iter,total,energy,attachment,grad_inf,wall_ms\n";
+  char line[256];
+  for (const TraceRecord& r : records) {
+    std::snprintf(line, sizeof line, "%d,%.17g,%.17g,%.17g,%.17g,%.3f\n", r.iteration, r.total,
+                  r.energy, r.attachment, r.grad_inf, r.wall_ms);
+    os << line;
+  }
+}
+
+std::pair<MomentumSet, OptimizationTrace> optimize(const PointSet& q0, const PointSet& target,
+                                                   const ShootingConfig& config,
+                                                   EvalStats* eval_stats, int) {
+  validate_config(config);
+  require_aligned(q0.size(), target.size(), "optimize");
+  const gs_config c = to_c(config);
+  gs_opt_config oc = gs_default_opt_config();
+  oc.max_iterations = config.optimizer.max_iterations;
+  oc.memory = config.optimizer.memory;
+  oc.gradient_tolerance = config.optimizer.gradient_tolerance;
+  oc.relative_objective_tolerance = config.optimizer.relative_objective_tolerance;
+  oc.sufficient_decrease = config.optimizer.line_search.sufficient_decrease;
+  oc.curvature = config.optimizer.line_search.curvature;
+  oc.max_trials = config.optimizer.line_search.max_trials;
+  const std::size_t n = q0.size();
+  std::vector<Vec3> p(n);
+  std::vector<double> trace(6 * (std::size_t)(oc.max_iterations + 1));
+  int32_t reason = 0, iters = 0, evals = 0, tl = 0;
+  gs_stats st{};
+  const gs_status s = gs_optimize(ctx(), &c, &oc, (int64_t)n, raw(q0.data()), raw(target.data()),
+                                  raw(p), &reason, &iters, &evals, trace.data(), &tl, &st);
+  if (s == GS_NONFINITE) throw NonFiniteObjectiveAtStart("objective is non-finite at the start point");
+  check(s);
+  OptimizationTrace tr;
+  tr.reason = static_cast<TerminationReason>(reason);
+  for (int32_t k = 0; k < tl; ++k) {
+    const double* r = &trace[6 * (std::size_t)k];
+    tr.records.push_back({(int)r[0], r[1], r[2], r[3], r[4], r[5]});
+  }
+  if (eval_stats) {
+    EvalStats es;
+    es.tree_build_ms = st.tree_build_ms;
+    es.forward_ms = st.forward_ms;
+    es.backward_ms = st.backward_ms;
+    es.traversal = to_traversal(st);
+    es.traversal_queries = st.traversal_queries;
+    eval_stats->merge(es);
+  }
+  return {MomentumSet(std::move(p)), std::move(tr)};
 }
 
 }  // namespace geoshoot

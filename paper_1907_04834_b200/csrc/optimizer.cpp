@@ -1,0 +1,335 @@
+// optimizer.cpp -- the registration optimizer as a
+// caller of the device evaluate(): limited-memory BFGS with a strong-Wolfe
+// line search over the initial momenta, starting from p0 = 0.
+//
+// Restates the reference's algorithm (proj/src/optimizer.cpp): two-loop
+// recursion with gamma = s.y / y.y scaling (:37-58), steepest-descent restart
+// on a non-descent direction (:243-247), initial step 1/max(1, |g|_inf) on an
+// empty history (:248-249), bracketing by doubling then bisection zoom within
+// a shared trial budget, falling back to the best sufficient-decrease point
+// (:82-189), curvature-gated history updates (:271-277) and the same
+// termination order (:235-298). Non-finite flows map to +inf (:328-332).
+//
+// Every objective/gradient is one gs_evaluate call: the forward flow, trees,
+// adjoint and gradient run on the B200; the O(N m) L-BFGS vector algebra
+// stays on the host in FP64 (as in the reference), which keeps the control
+// flow of the search identical to the reference given the same evaluations.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <deque>
+#include <limits>
+#include <thread>
+#include <vector>
+
+#include "geoshoot_b200.h"
+
+namespace {
+
+using Vec = std::vector<double>;
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+double vdot(const Vec& a, const Vec& b) {
+  double s = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+double vmax_abs(const Vec& a) {
+  double m = 0.0;
+  for (double v : a) m = std::max(m, std::abs(v));
+  return m;
+}
+
+struct Pair {
+  Vec s, y;
+  double rho;
+};
+
+// H_k g through the two-loop recursion, negated: the search direction.
+Vec direction(const Vec& g, const std::deque<Pair>& hist) {
+  Vec d = g;
+  if (!hist.empty()) {
+    std::vector<double> alpha(hist.size());
+    for (std::size_t i = hist.size(); i-- > 0;) {
+      alpha[i] = hist[i].rho * vdot(hist[i].s, d);
+      for (std::size_t k = 0; k < d.size(); ++k) d[k] -= alpha[i] * hist[i].y[k];
+    }
+    const Pair& last = hist.back();
+    const double gamma = vdot(last.s, last.y) / vdot(last.y, last.y);
+    for (double& v : d) v *= gamma;
+    for (std::size_t i = 0; i < hist.size(); ++i) {
+      const double beta = hist[i].rho * vdot(hist[i].y, d);
+      for (std::size_t k = 0; k < d.size(); ++k) d[k] += (alpha[i] - beta) * hist[i].s[k];
+    }
+  }
+  for (double& v : d) v = -v;
+  return d;
+}
+
+struct Objective {
+  gs_ctx* ctx;
+  const gs_config* cfg;
+  int64_t n;
+  const double* q0;
+  const double* target;
+  int evaluations = 0;
+  gs_report last{};
+  gs_stats stats{};
+  gs_status hard_error = GS_OK;  // a device failure aborts the optimization
+
+  double operator()(const Vec& x, Vec& g) {
+    ++evaluations;
+    g.assign(x.size(), 0.0);
+    for (double v : x)
+      if (!std::isfinite(v)) return kInf;  // MomentumSet rejects it (invalid_argument)
+    gs_report r{};
+    gs_stats s{};
+    const gs_status st = gs_evaluate(ctx, cfg, n, q0, x.data(), target, &r, g.data(), &s);
+    if (st == GS_NONFINITE || st == GS_INVALID_ARGUMENT) return kInf;
+    if (st != GS_OK) {
+      hard_error = st;
+      return kInf;
+    }
+    last = r;
+    stats.direct_interactions += s.direct_interactions;
+    stats.approximated_interactions += s.approximated_interactions;
+    stats.nodes_visited += s.nodes_visited;
+    stats.traversal_queries += s.traversal_queries;
+    stats.tree_build_ms += s.tree_build_ms;
+    stats.forward_ms += s.forward_ms;
+    stats.backward_ms += s.backward_ms;
+    return r.total;
+  }
+};
+
+struct Step {
+  bool ok = false;
+  double f = kInf;
+  Vec x, g;
+};
+
+Step wolfe(Objective& F, const Vec& x0, double f0, const Vec& g0, const Vec& d, double a0,
+           const gs_opt_config& c) {
+  Step out;
+  const double slope0 = vdot(g0, d);
+  if (slope0 >= 0.0) return out;
+  auto point = [&](double a) {
+    Vec x(x0.size());
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] = x0[i] + a * d[i];
+    return x;
+  };
+  auto decreases = [&](double a, double fa) { return fa <= f0 + c.sufficient_decrease * a * slope0; };
+  auto curvature_ok = [&](double slope) { return std::abs(slope) <= -c.curvature * slope0; };
+
+  int trials = 0;
+  double best_a = 0.0, best_f = f0;
+  double a_prev = 0.0, f_prev = f0, a = a0;
+  double lo = -1.0, hi = -1.0, f_lo = 0.0;
+  bool bracketed = false;
+  Vec g;
+  while (trials < c.max_trials) {
+    const double at = bracketed ? 0.5 * (lo + hi) : a;
+    Vec x = point(at);
+    const double fa = F(x, g);
+    ++trials;
+    if (F.hard_error != GS_OK) return out;
+    const double slope = std::isfinite(fa) ? vdot(g, d) : 0.0;
+    if (!bracketed) {
+      if (!std::isfinite(fa) || !decreases(at, fa) || (trials > 1 && fa >= f_prev)) {
+        lo = a_prev;
+        f_lo = f_prev;
+        hi = at;
+        bracketed = true;
+        continue;
+      }
+    } else if (!std::isfinite(fa) || !decreases(at, fa) || fa >= f_lo) {
+      hi = at;
+      continue;
+    }
+    if (fa < best_f) {
+      best_a = at;
+      best_f = fa;
+    }
+    if (curvature_ok(slope)) {
+      out.ok = true;
+      out.f = fa;
+      out.x = std::move(x);
+      out.g = std::move(g);
+      return out;
+    }
+    if (!bracketed) {
+      if (slope >= 0.0) {
+        lo = at;
+        f_lo = fa;
+        hi = a_prev;
+        bracketed = true;
+        continue;
+      }
+      a_prev = at;
+      f_prev = fa;
+      a = 2.0 * at;
+    } else {
+      if (slope * (hi - lo) >= 0.0) hi = lo;
+      lo = at;
+      f_lo = fa;
+    }
+  }
+  if (best_a > 0.0 && best_f < f0) {  // budget spent: re-evaluate the best decrease point
+    Vec x = point(best_a);
+    const double fb = F(x, g);
+    if (std::isfinite(fb) && fb < f0) {
+      out.ok = true;
+      out.f = fb;
+      out.x = std::move(x);
+      out.g = std::move(g);
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+gs_opt_config gs_default_opt_config(void) {
+  gs_opt_config c;
+  c.max_iterations = 200;
+  c.memory = 10;
+  c.gradient_tolerance = 1e-6;
+  c.relative_objective_tolerance = 1e-9;
+  c.sufficient_decrease = 1e-4;
+  c.curvature = 0.9;
+  c.max_trials = 20;
+  return c;
+}
+
+gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc, int64_t n,
+                      const double* q0, const double* target, double* p_out, int32_t* reason,
+                      int32_t* iterations, int32_t* evaluations, double* trace,
+                      int32_t* trace_len, gs_stats* stats) {
+  if (!ctx || !cfg || !oc || !q0 || !target || !p_out) return GS_INVALID_ARGUMENT;
+  gs_status st = gs_validate_config(cfg, nullptr);
+  if (st != GS_OK) return st;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  Objective F{ctx, cfg, n, q0, target};
+  int32_t tl = 0;
+  auto record = [&](int it, double ginf) {  // trace row: iter,total,energy,attachment,grad_inf,wall_ms
+    if (!trace) return;
+    double* r = trace + 6 * (size_t)tl;
+    r[0] = it;
+    r[1] = F.last.total;
+    r[2] = F.last.energy;
+    r[3] = F.last.attachment;
+    r[4] = ginf;
+    r[5] = ms();
+    ++tl;
+  };
+
+  Vec x((size_t)3 * n, 0.0), g;
+  double f = F(x, g);
+  if (F.hard_error != GS_OK) return F.hard_error;
+  if (!std::isfinite(f)) return GS_NONFINITE;  // NonFiniteObjectiveAtStart
+  double ginf = vmax_abs(g);
+  record(0, ginf);
+  int32_t why = GS_TERM_MAX_ITERATIONS, iters = 0;
+  std::deque<Pair> hist;
+  bool done = false;
+  for (int it = 1; it <= oc->max_iterations && !done; ++it) {
+    if (ginf <= oc->gradient_tolerance) {
+      why = GS_TERM_GRADIENT_TOLERANCE;
+      done = true;
+      break;
+    }
+    Vec d = direction(g, hist);
+    if (vdot(g, d) >= 0.0) {
+      hist.clear();
+      d = g;
+      for (double& v : d) v = -v;
+    }
+    const double a0 = hist.empty() ? 1.0 / std::max(1.0, ginf) : 1.0;
+    Step s = wolfe(F, x, f, g, d, a0, *oc);
+    if (F.hard_error != GS_OK) return F.hard_error;
+    if (!s.ok) {
+      why = GS_TERM_LINE_SEARCH_FAILURE;
+      done = true;
+      break;
+    }
+    if (!std::isfinite(vmax_abs(s.g))) {
+      why = GS_TERM_NON_FINITE;
+      done = true;
+      break;
+    }
+    Pair pr;
+    pr.s.resize(x.size());
+    pr.y.resize(x.size());
+    for (std::size_t k = 0; k < x.size(); ++k) {
+      pr.s[k] = s.x[k] - x[k];
+      pr.y[k] = s.g[k] - g[k];
+    }
+    const double sy = vdot(pr.s, pr.y);
+    if (sy > 1e-10 * std::sqrt(vdot(pr.s, pr.s)) * std::sqrt(vdot(pr.y, pr.y))) {
+      pr.rho = 1.0 / sy;
+      hist.push_back(std::move(pr));
+      if ((int)hist.size() > oc->memory) hist.pop_front();
+    }
+    const double f_prev = f;
+    x = std::move(s.x);
+    f = s.f;
+    g = std::move(s.g);
+    ginf = vmax_abs(g);
+    iters = it;
+    record(it, ginf);
+    if (std::abs(f_prev - f) <= oc->relative_objective_tolerance * std::max(1.0, std::abs(f))) {
+      why = GS_TERM_OBJECTIVE_TOLERANCE;
+      done = true;
+    }
+  }
+  if (!done) why = ginf <= oc->gradient_tolerance ? GS_TERM_GRADIENT_TOLERANCE : GS_TERM_MAX_ITERATIONS;
+  std::copy(x.begin(), x.end(), p_out);
+  if (reason) *reason = why;
+  if (iterations) *iterations = iters;
+  if (evaluations) *evaluations = F.evaluations;
+  if (trace_len) *trace_len = tl;
+  if (stats) *stats = F.stats;
+  return GS_OK;
+}
+
+// Batched subjects (BASELINE config 5): B independent registrations, each on
+// its own context (CUDA stream) and host thread so the device overlaps the
+// subjects' kernels; no communication between subjects.
+gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_config* opt,
+                            int32_t batch, const int64_t* n, const double* const* q0,
+                            const double* const* target, double* const* p_out, int32_t* reasons,
+                            int32_t* iterations, int32_t* evaluations, double* final_total) {
+  if (!cfg || !opt || batch < 0 || !n || !q0 || !target || !p_out) return GS_INVALID_ARGUMENT;
+  std::vector<gs_status> st((size_t)batch, GS_OK);
+  std::vector<std::thread> pool;
+  for (int32_t b = 0; b < batch; ++b)
+    pool.emplace_back([&, b] {
+      gs_status cs = GS_OK;
+      gs_ctx* c = gs_create(device, &cs);
+      if (!c) {
+        st[b] = cs;
+        return;
+      }
+      std::vector<double> trace(6 * (size_t)(opt->max_iterations + 1));
+      int32_t r = 0, it = 0, ev = 0, tl = 0;
+      st[b] = gs_optimize(c, cfg, opt, n[b], q0[b], target[b], p_out[b], &r, &it, &ev,
+                          trace.data(), &tl, nullptr);
+      if (reasons) reasons[b] = r;
+      if (iterations) iterations[b] = it;
+      if (evaluations) evaluations[b] = ev;
+      if (final_total) final_total[b] = tl > 0 ? trace[6 * (size_t)(tl - 1) + 1] : 0.0;
+      gs_destroy(c);
+    });
+  for (auto& t : pool) t.join();
+  for (gs_status s : st)
+    if (s != GS_OK) return s;
+  return GS_OK;
+}
+
+}  // extern "C"

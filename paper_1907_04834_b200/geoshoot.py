@@ -285,6 +285,49 @@ class Geoshoot:
                "residual_sse": r.residual_sse}
         return Evaluation(rep, g, st.as_dict())
 
+    def optimize(self, q0, target, cfg: ShootingConfig, max_iterations=200, memory=10,
+                 gradient_tolerance=1e-6, relative_objective_tolerance=1e-9,
+                 sufficient_decrease=1e-4, curvature=0.9, max_trials=20):
+        """optimize() (optimizer.cpp:301-351): L-BFGS over p0 from 0."""
+        q0, t = _arr(q0, "q0"), _arr(target, "target")
+        _require_aligned(len(q0), len(t), "optimize")
+        c = cfg.c()
+        oc = L.gs_opt_config(max_iterations, memory, gradient_tolerance,
+                             relative_objective_tolerance, sufficient_decrease, curvature,
+                             max_trials)
+        p = np.empty_like(q0)
+        reason, iters, evals, tl = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        trace = np.zeros((max_iterations + 1, 6))
+        st = L.gs_stats()
+        self.check(self.lib.gs_optimize(self.ctx, C.byref(c), C.byref(oc), len(q0), _p(q0), _p(t),
+                                        _p(p), C.byref(reason), C.byref(iters), C.byref(evals),
+                                        _p(trace), C.byref(tl), C.byref(st)))
+        names = ["gradient_tolerance", "objective_tolerance", "max_iterations",
+                 "line_search_failure", "non_finite"]
+        return {"p0": p, "reason": names[reason.value], "iterations": iters.value,
+                "evaluations": evals.value, "trace": trace[:tl.value], "stats": st.as_dict()}
+
+    def optimize_batch(self, q0s, targets, cfg: ShootingConfig, device: int = 0,
+                       max_iterations=200, memory=10, gradient_tolerance=1e-6,
+                       relative_objective_tolerance=1e-9):
+        """Independent registrations (config 5), one stream + host thread each."""
+        B = len(q0s)
+        q0s = [_arr(q) for q in q0s]
+        targets = [_arr(t) for t in targets]
+        outs = [np.empty_like(q) for q in q0s]
+        c = cfg.c()
+        oc = L.gs_opt_config(max_iterations, memory, gradient_tolerance,
+                             relative_objective_tolerance, 1e-4, 0.9, 20)
+        ns = (C.c_int64 * B)(*[len(q) for q in q0s])
+        P = L._d * B
+        qa, ta, pa = P(*map(_p, q0s)), P(*map(_p, targets)), P(*map(_p, outs))
+        reasons, iters, evals = (C.c_int32 * B)(), (C.c_int32 * B)(), (C.c_int32 * B)()
+        tot = np.zeros(B)
+        self.check(self.lib.gs_optimize_batch(device, C.byref(c), C.byref(oc), B, ns, qa, ta, pa,
+                                              reasons, iters, evals, _p(tot)))
+        return {"p0": outs, "reasons": list(reasons), "iterations": list(iters),
+                "evaluations": list(evals), "final_total": tot}
+
     def flow(self, cfg: ShootingConfig, n: int) -> "Flow":
         return Flow(self, cfg, n)
 
