@@ -216,6 +216,8 @@ def run_ours(args):
     lib.gs_microbench(local, 1, C.byref(ex2))
     ffma_reg = C.c_double()
     lib.gs_microbench(local, 3, C.byref(ffma_reg))
+    ffma2 = C.c_double()
+    lib.gs_microbench(local, 4, C.byref(ffma2))
     k_ms = prof["kernel_ms"] / max(1, prof["kernel_launches"])
     pairs_per_launch = float(N) * shard
     achieved = pairs_per_launch / (k_ms * 1e-3) / 1e9  # Gpair/s
@@ -238,8 +240,9 @@ def run_ours(args):
                        "MEASURED_PEAKS.json has no FP32 figure",
         "nominal_peak": nominal, "frac_of_nominal": achieved / nominal,
         "peak_register_operand_ffma": ffma_reg.value / 16.0 / 1e9,
+        "peak_packed_ffma2": ffma2.value / 16.0 / 1e9,
         "sfu_frac": achieved * 1e9 / ex2.value if ex2.value else None,
-        "kernel": "k_rhs_f32<8,128>", "kernel_ms_avg": k_ms,
+        "kernel": "k_rhs_f32x2<8,128,3> (packed FFMA2)", "kernel_ms_avg": k_ms,
         "kernel_share_of_step": prof["kernel_ms"] / ms if ms else None,
         "algorithmic_per_launch": f"{pairs_per_launch:.3e} ordered pairs x 16 FP32 + 1 MUFU",
     }

@@ -294,7 +294,8 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
 
 /* ---- measured device peaks (roofline denominators) ----------------------------
  * kind 0: FP32 FFMA lane-ops/s (constant operands), 1: MUFU.EX2 lane-ops/s,
- * 2: FP64 DFMA lane-ops/s, 3: FP32 FFMA lane-ops/s with all-register operands. */
+ * 2: FP64 DFMA lane-ops/s, 3: FP32 FFMA lane-ops/s with all-register operands,
+ * 4: FP32 lane-FMAs/s issued as packed FFMA2 (2 per lane per instruction). */
 gs_status gs_microbench(int device, int32_t kind, double* ops_per_s);
 
 #ifdef __cplusplus

@@ -136,6 +136,253 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__
   }
 }
 
+// ---- packed FP32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2) -----------------
+// Two targets share one 64-bit register pair; a source coordinate enters as a
+// scalar operand broadcast to both halves, so one issue slot does the work of
+// two scalar FP32 instructions.
+struct f2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(f2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ f2 bc2(float x) { return pk2(x, x); }
+// 2^-x on the SFU for both halves (the negation folds into MUFU's operand)
+__device__ __forceinline__ f2 nex2x2(f2 r2) {
+  float lo, hi;
+  up2(r2, lo, hi);
+  return pk2(ex2(-lo), ex2(-hi));
+}
+
+// Packed variant of k_rhs_f32: TPT targets per thread as TPT/2 register
+// pairs. Per two (target, source) pairs: 3 FADD2 + FMUL2 + 2 FFMA2 (r^2) +
+// 2 MUFU + FMUL2 + 2 FFMA2 (p_i.p_j) + FMUL2 (c) + 3 FFMA2 (sum g p_j) +
+// 3 FFMA2 (sum c d') = 16 packed FP32 + 2 SFU issue slots (9 per pair instead
+// of 17); identical arithmetic per target to the scalar kernel.
+template <int TPT, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict__ rec, int n,
+                                                        int tgt_begin, int n_tgt, int chunk,
+                                                        float kap, float kc0x, float kc0y,
+                                                        float kc0z, float4* __restrict__ part) {
+  constexpr int TP = TPT / 2;
+  __shared__ float4 sq[kTile];
+  __shared__ float4 sp[kTile];
+  f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
+  f2 ax[TP], ay[TP], az[TP], bx[TP], by[TP], bz[TP];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float4 q[2], p[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      q[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      p[h] = q[h];
+      if (t < n_tgt) {
+        q[h] = rec[2 * (tgt_begin + t)];
+        p[h] = rec[2 * (tgt_begin + t) + 1];
+      }
+      q[h] = make_float4(fmaf(kap, q[h].x, -kc0x), fmaf(kap, q[h].y, -kc0y), fmaf(kap, q[h].z, -kc0z), 0.f);
+    }
+    qx[k] = pk2(q[0].x, q[1].x); qy[k] = pk2(q[0].y, q[1].y); qz[k] = pk2(q[0].z, q[1].z);
+    px[k] = pk2(p[0].x, p[1].x); py[k] = pk2(p[0].y, p[1].y); pz[k] = pk2(p[0].z, p[1].z);
+    ax[k] = ay[k] = az[k] = bx[k] = by[k] = bz[k] = pk2(0.f, 0.f);
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < j1) {
+        q = rec[2 * j];
+        p = rec[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q;  // zero records contribute exactly 0 (p = 0)
+      sp[u] = p;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u];
+      const float4 b = sp[u];
+      const f2 axx = bc2(a.x), ayy = bc2(a.y), azz = bc2(a.z);
+      const f2 bxx = bc2(b.x), byy = bc2(b.y), bzz = bc2(b.z);
+      f2 dx[TP], dy[TP], dz[TP], g[TP];
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        dx[k] = sub2(qx[k], axx);
+        dy[k] = sub2(qy[k], ayy);
+        dz[k] = sub2(qz[k], azz);
+        f2 r2 = mul2(dx[k], dx[k]);
+        r2 = fma2(dy[k], dy[k], r2);
+        r2 = fma2(dz[k], dz[k], r2);
+        g[k] = nex2x2(r2);
+      }
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        f2 pp = mul2(px[k], bxx);
+        pp = fma2(py[k], byy, pp);
+        pp = fma2(pz[k], bzz, pp);
+        const f2 c = mul2(pp, g[k]);
+        ax[k] = fma2(g[k], bxx, ax[k]);
+        ay[k] = fma2(g[k], byy, ay[k]);
+        az[k] = fma2(g[k], bzz, az[k]);
+        bx[k] = fma2(c, dx[k], bx[k]);
+        by[k] = fma2(c, dy[k], by[k]);
+        bz[k] = fma2(c, dz[k], bz[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float a0[2][3], b0[2][3];
+    up2(ax[k], a0[0][0], a0[1][0]); up2(ay[k], a0[0][1], a0[1][1]); up2(az[k], a0[0][2], a0[1][2]);
+    up2(bx[k], b0[0][0], b0[1][0]); up2(by[k], b0[0][1], b0[1][1]); up2(bz[k], b0[0][2], b0[1][2]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      if (t < n_tgt) {
+        float4* o = part + 2 * ((size_t)blockIdx.y * n_tgt + t);
+        o[0] = make_float4(a0[h][0], a0[h][1], a0[h][2], 0.f);
+        o[1] = make_float4(b0[h][0], b0[h][1], b0[h][2], 0.f);
+      }
+    }
+  }
+}
+
+// Packed (FFMA2) Hessian-product kernel: TPT targets as TPT/2 pairs; 40
+// packed FP32 + 2 MUFU issue slots per two (target, source) pairs.
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_hess_f32x2(const float4* __restrict__ rec,
+                                                   const float4* __restrict__ adj, int n,
+                                                   int tgt_begin, int n_tgt, int chunk, float kap,
+                                                   float kc0x, float kc0y, float kc0z, float c1,
+                                                   float4* __restrict__ part) {
+  constexpr int TP = TPT / 2;
+  constexpr int tile = kTile / 2;
+  __shared__ float4 sq[tile], sp[tile], sa[tile], sb[tile];
+  f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
+  f2 ix[TP], iy[TP], iz[TP], jx[TP], jy[TP], jz[TP];  // alpha_i, beta_i
+  f2 A[TP][12];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float4 q[2], p[2], al[2], be[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      q[h] = p[h] = al[h] = be[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < n_tgt) {
+        const int i = tgt_begin + t;
+        q[h] = rec[2 * i]; p[h] = rec[2 * i + 1]; al[h] = adj[2 * i]; be[h] = adj[2 * i + 1];
+      }
+      q[h] = make_float4(fmaf(kap, q[h].x, -kc0x), fmaf(kap, q[h].y, -kc0y), fmaf(kap, q[h].z, -kc0z), 0.f);
+    }
+    qx[k] = pk2(q[0].x, q[1].x); qy[k] = pk2(q[0].y, q[1].y); qz[k] = pk2(q[0].z, q[1].z);
+    px[k] = pk2(p[0].x, p[1].x); py[k] = pk2(p[0].y, p[1].y); pz[k] = pk2(p[0].z, p[1].z);
+    ix[k] = pk2(al[0].x, al[1].x); iy[k] = pk2(al[0].y, al[1].y); iz[k] = pk2(al[0].z, al[1].z);
+    jx[k] = pk2(be[0].x, be[1].x); jy[k] = pk2(be[0].y, be[1].y); jz[k] = pk2(be[0].z, be[1].z);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) A[k][c] = pk2(0.f, 0.f);
+  }
+  const f2 cc1 = bc2(-c1);
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += tile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < tile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q, a = q, b = q;
+      if (j < j1) {
+        q = rec[2 * j]; p = rec[2 * j + 1]; a = adj[2 * j]; b = adj[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q; sp[u] = p; sa[u] = a; sb[u] = b;  // zero records contribute exactly 0
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < tile; ++u) {
+      const float4 Q = sq[u], P = sp[u], Al = sa[u], Be = sb[u];
+      const f2 Qx = bc2(Q.x), Qy = bc2(Q.y), Qz = bc2(Q.z);
+      const f2 Px = bc2(P.x), Py = bc2(P.y), Pz = bc2(P.z);
+      const f2 Ax = bc2(Al.x), Ay = bc2(Al.y), Az = bc2(Al.z);
+      const f2 Bx = bc2(Be.x), By = bc2(Be.y), Bz = bc2(Be.z);
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        const f2 dx = sub2(qx[k], Qx), dy = sub2(qy[k], Qy), dz = sub2(qz[k], Qz);
+        f2 r2 = mul2(dx, dx);
+        r2 = fma2(dy, dy, r2);
+        r2 = fma2(dz, dz, r2);
+        const f2 g = nex2x2(r2);
+        // negated db = beta_j - beta_i, so z = uu d - db is one FFMA2 per axis;
+        // the sign comes back through -c1 and the final negation of A[9..11]
+        const f2 dbx = sub2(Bx, jx[k]), dby = sub2(By, jy[k]), dbz = sub2(Bz, jz[k]);
+        f2 ddb = mul2(dx, dbx);
+        ddb = fma2(dy, dby, ddb);
+        ddb = fma2(dz, dbz, ddb);
+        f2 s1 = mul2(ix[k], Px);
+        s1 = fma2(iy[k], Py, s1);
+        s1 = fma2(iz[k], Pz, s1);
+        s1 = fma2(px[k], Ax, s1);
+        s1 = fma2(py[k], Ay, s1);
+        s1 = fma2(pz[k], Az, s1);
+        f2 pp = mul2(px[k], Px);
+        pp = fma2(py[k], Py, pp);
+        pp = fma2(pz[k], Pz, pp);
+        const f2 t1 = mul2(g, s1);
+        A[k][0] = fma2(t1, dx, A[k][0]); A[k][1] = fma2(t1, dy, A[k][1]); A[k][2] = fma2(t1, dz, A[k][2]);
+        A[k][3] = fma2(g, Ax, A[k][3]); A[k][4] = fma2(g, Ay, A[k][4]); A[k][5] = fma2(g, Az, A[k][5]);
+        const f2 w = mul2(g, pp);
+        const f2 uu = mul2(ddb, cc1);  // cc1 = -c1
+        const f2 zx = fma2(uu, dx, dbx), zy = fma2(uu, dy, dby), zz = fma2(uu, dz, dbz);
+        A[k][6] = fma2(w, zx, A[k][6]); A[k][7] = fma2(w, zy, A[k][7]); A[k][8] = fma2(w, zz, A[k][8]);
+        const f2 m = mul2(g, ddb);
+        A[k][9] = fma2(m, Px, A[k][9]); A[k][10] = fma2(m, Py, A[k][10]); A[k][11] = fma2(m, Pz, A[k][11]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float v[2][12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) up2(A[k][c], v[0][c], v[1][c]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      if (t < n_tgt) {
+        float4* o = part + 4 * ((size_t)blockIdx.y * n_tgt + t);
+        o[0] = make_float4(v[h][0], v[h][1], v[h][2], 0.f);
+        o[1] = make_float4(v[h][3], v[h][4], v[h][5], 0.f);
+        o[2] = make_float4(v[h][6], v[h][7], v[h][8], 0.f);
+        o[3] = make_float4(-v[h][9], -v[h][10], -v[h][11], 0.f);
+      }
+    }
+  }
+}
+
 // FP64: the reference's own expression exp(-|d|^2 * inv_two_s) in unscaled
 // coordinates; libdevice exp (no SFU path exists for FP64).
 template <int TPT, int NT>
@@ -535,13 +782,15 @@ struct RhsVariant {
   bool phased;
 };
 static const RhsVariant kRhsVariants[] = {
-    {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true}};
+    {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true},
+    // packed FP32x2 (FFMA2) variants
+    {8, 3, true}, {8, 4, true}, {4, 6, true}};
 constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
 
 static int rhs_variant() {
   static int v = [] {
     const char* e = std::getenv("GS_RHS_VARIANT");
-    const int x = e ? std::atoi(e) : 0;
+    const int x = e ? std::atoi(e) : 8;
     return (x >= 0 && x < kNumRhsVariants) ? x : 0;
   }();
   return v;
@@ -560,6 +809,19 @@ static int occ_rhs_f32() {
   return occupancy(k_rhs_f32<TPT, kNT, MINB, PH>, kNT);
 }
 
+template <int TPT, int MINB>
+static void launch_rhs_f32x2(const Plan& pl, cudaStream_t st, const float4* rec, int n, int tb,
+                             int nt, const KernelConsts& kc, float4* part) {
+  k_rhs_f32x2<TPT, kNT, MINB><<<pl.grid, kNT, 0, st>>>(
+      rec, n, tb, nt, pl.chunk, (float)kc.kappa, (float)(kc.kappa * kc.c0[0]),
+      (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), part);
+}
+
+template <int TPT, int MINB>
+static int occ_rhs_f32x2() {
+  return occupancy(k_rhs_f32x2<TPT, kNT, MINB>, kNT);
+}
+
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
                  const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
   if (prec == kF32) {
@@ -574,7 +836,8 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     static int occs[kNumRhsVariants] = {
         occ_rhs_f32<8, 3, true>(), occ_rhs_f32<8, 3, false>(), occ_rhs_f32<8, 4, true>(),
         occ_rhs_f32<4, 6, true>(), occ_rhs_f32<4, 4, false>(), occ_rhs_f32<6, 4, true>(),
-        occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>()};
+        occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>(),
+        occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>()};
     const int tp[] = {u.tpt};
     Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
     if (pl.S > part_cap_chunks) return -1;
@@ -588,6 +851,9 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
       case 4: launch_rhs_f32<4, 4, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 5: launch_rhs_f32<6, 4, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 6: launch_rhs_f32<2, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 8: launch_rhs_f32x2<8, 3>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 9: launch_rhs_f32x2<8, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 10: launch_rhs_f32x2<4, 6>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
     }
     return pl.S;
@@ -609,9 +875,24 @@ int hess_partials(const Device& dev, int prec, const void* rec, const void* adj,
                   int part_cap_chunks, cudaStream_t st) {
   if (prec == kF32) {
     static const int tpts[] = {4, 2, 1};
-    static int occ = occupancy(k_hess_f32<4, kNT>, kNT);
+    static int occ = occupancy(k_hess_f32x2<4, kNT>, kNT);
     Plan pl = plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms);
     if (pl.S > part_cap_chunks) return -1;
+    static const bool packed = [] {
+      const char* e = std::getenv("GS_HESS_PACKED");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    if (packed && pl.tpt >= 2) {
+      const float kap = (float)kc.kappa;
+      const float c1 = (float)(1.0 / (kc.kappa * kc.kappa * kc.s));
+      const float a = (float)(kc.kappa * kc.c0[0]), b = (float)(kc.kappa * kc.c0[1]),
+                  c = (float)(kc.kappa * kc.c0[2]);
+      if (pl.tpt == 4)
+        k_hess_f32x2<4, kNT><<<pl.grid, kNT, 0, st>>>((const float4*)rec, (const float4*)adj, n, tgt_begin, n_tgt, pl.chunk, kap, a, b, c, c1, (float4*)part);
+      else
+        k_hess_f32x2<2, kNT><<<pl.grid, kNT, 0, st>>>((const float4*)rec, (const float4*)adj, n, tgt_begin, n_tgt, pl.chunk, kap, a, b, c, c1, (float4*)part);
+      return pl.S;
+    }
     const float kap = (float)kc.kappa;
     const float c1 = (float)(1.0 / (kc.kappa * kc.kappa * kc.s));
     const float a = (float)(kc.kappa * kc.c0[0]), b = (float)(kc.kappa * kc.c0[1]),

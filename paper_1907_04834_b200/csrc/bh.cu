@@ -261,6 +261,57 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
   }
 }
 
+// Cooperative sweep of one lane's long direct range: the 32 lanes split the
+// range's points (lane-strided, coalesced loads), each accumulates the owner's
+// terms, then a fixed butterfly reduction hands the sum to the owner. Fixed
+// assignment + fixed reduction tree keep the result deterministic.
+constexpr int kBigRange = 48;
+
+template <typename R>
+__device__ __forceinline__ V4<R> shfl4(const V4<R>& v, int src) {
+  return mk4<R>(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                __shfl_sync(0xffffffffu, v.z, src), R(0));
+}
+
+template <typename R, int MODE>
+__device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc<R>& acc,
+                                            uint32_t& c_dir, const V4<R>& xs, const V4<R>& px,
+                                            const V4<R>& ai, const V4<R>& bi,
+                                            const BhArgs<R>& a) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kAcc = MODE == kBhHess ? 12 : (MODE == kBhRhs ? 6 : 3);
+  while (owners) {
+    const int o = __ffs(owners) - 1;
+    owners &= owners - 1;
+    const int rb = __shfl_sync(0xffffffffu, j, o), re = __shfl_sync(0xffffffffu, je, o);
+    const V4<R> oxs = shfl4<R>(xs, o), opx = shfl4<R>(px, o);
+    V4<R> oai = ai, obi = bi;
+    if (MODE == kBhHess) { oai = shfl4<R>(ai, o); obi = shfl4<R>(bi, o); }
+    Acc<R> part;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) part.v[c] = R(0);
+    const V4<R> zero = mk4<R>(0, 0, 0);
+    for (int s = rb + lane; s <= re; s += 32) {
+      const V4<R> Q = ld4(a.srec + 2 * s), P = ld4(a.srec + 2 * s + 1);
+      if (MODE == kBhHess)
+        unit<R, MODE>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
+      else
+        unit<R, MODE>(part, oxs, opx, oai, obi, Q, P, zero, zero, a);
+    }
+#pragma unroll
+    for (int c = 0; c < kAcc; ++c) {
+      R v = part.v[c];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == o) acc.v[c] += v;
+    }
+    if (lane == o) {
+      c_dir += (uint32_t)(re - rb + 1);
+      j = re + 1;
+    }
+  }
+}
+
 // Work-stream variant: every lane walks its own query independently; each
 // iteration a lane either continues its pending direct range (one point) or
 // visits its next node (and, for a leaf / far / fully-inside node, evaluates
@@ -333,6 +384,9 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
       }
       if (next <= nd) next = INT_MAX;  // never loop on a corrupt skip
     }
+    // long direct ranges (dense near field) are swept by the whole warp
+    const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
+    if (big) coop_ranges<R, MODE>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
     if (!have && j <= je) {
       have = true;
       src = j++;

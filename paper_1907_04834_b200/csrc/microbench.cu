@@ -46,6 +46,33 @@ __global__ void __launch_bounds__(256) k_ffma_reg(float* out, int iters, const f
   if (s == 1234.5f) out[threadIdx.x] = s;
 }
 
+// packed FP32x2 FMA (FFMA2): counts 2 lane-FMAs per lane per instruction
+__global__ void __launch_bounds__(256) k_ffma2(float* out, int iters, float a, float b) {
+  unsigned long long x[kChains], av, bv;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(av) : "f"(a));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bv) : "f"(b));
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    const float lo = threadIdx.x * 1e-3f + c, hi = lo + 0.5f;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x[c]) : "f"(lo), "f"(hi));
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < kChains; ++c)
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(av), "l"(bv));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x[c]));
+    s += lo + hi;
+  }
+  if (s == 1234.5f) out[threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(256) k_ex2(float* out, int iters) {
   float x[kChains];
 #pragma unroll
@@ -107,6 +134,7 @@ extern "C" gs_status gs_microbench(int device, int32_t kind, double* ops_per_s) 
     if (kind == 0) k_ffma<<<blocks, threads>>>((float*)out, iters, 0.999999f, 1e-7f);
     else if (kind == 1) k_ex2<<<blocks, threads>>>((float*)out, iters);
     else if (kind == 3) k_ffma_reg<<<blocks, threads>>>((float*)out + 64, iters, (const float*)out);
+    else if (kind == 4) k_ffma2<<<blocks, threads>>>((float*)out, iters, 0.999999f, 1e-7f);
     else k_dfma<<<blocks, threads>>>((double*)out, iters, 0.999999, 1e-7);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
@@ -119,7 +147,7 @@ extern "C" gs_status gs_microbench(int device, int32_t kind, double* ops_per_s) 
   cudaFree(out);
   GS_CUDA_OK(cudaGetLastError());
   // lane-operations per second (one FFMA / MUFU / DFMA per lane per op)
-  const double ops = (double)blocks * threads * iters * 16.0 * kChains;
+  const double ops = (double)blocks * threads * iters * 16.0 * kChains * (kind == 4 ? 2.0 : 1.0);
   *ops_per_s = ops / (best * 1e-3);
   return GS_OK;
 }

@@ -22,11 +22,18 @@ def main():
     ap.add_argument("--euler", action="store_true")
     ap.add_argument("--sigma", type=float, default=0.0131)
     ap.add_argument("--phases", action="store_true")
+    ap.add_argument("--shape", default="cube", choices=["cube", "tube", "ellipsoid"])
+    ap.add_argument("--amp", type=float, default=0.01)
     a = ap.parse_args()
     import numpy as np
     from paper_1907_04834_b200 import BARNES_HUT, EULER, EXACT, F32, F64, RK4, Geoshoot, ShootingConfig
     rng = np.random.default_rng(2024)
-    q, p = rng.uniform(0, 1, (a.n, 3)), rng.normal(0, 1e-2, (a.n, 3))
+    if a.shape == "cube":
+        q, p = rng.uniform(0, 1, (a.n, 3)), rng.normal(0, 1e-2, (a.n, 3))
+    else:
+        from tests.util import ellipsoid, smooth_momenta, tube
+        q = tube(a.n, seed=3) if a.shape == "tube" else ellipsoid(a.n, seed=44)
+        p = smooth_momenta(q, a.amp, 4)
     gs = Geoshoot(0)
     cfg = ShootingConfig(sigma=a.sigma, timesteps=10, backend=BARNES_HUT if a.backend == "bh" else EXACT,
                          integrator=EULER if a.euler else RK4, precision=F32 if a.prec == "f32" else F64)
