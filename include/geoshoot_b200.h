@@ -43,6 +43,9 @@ typedef enum gs_status {
   GS_INVALID_ARGUMENT = 7,   /* std::invalid_argument (empty / non-finite PointSet, core.hpp:124-170) */
   GS_CUDA_ERROR = 8,
   GS_NO_DEVICE = 9,
+  GS_PARSE_ERROR = 10,       /* ParseError{line}, core.hpp:95-100 (line: gs_last_parse_line) */
+  GS_UNSUPPORTED_FORMAT = 11,/* UnsupportedFormat, core.hpp:102-104 */
+  GS_IO_ERROR = 12,          /* std::runtime_error "cannot open ..." (pipeline_io.cpp:160-182) */
   GS_INTERNAL = 99
 } gs_status;
 
@@ -291,6 +294,21 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
                             int32_t batch, const int64_t* n, const double* const* q0,
                             const double* const* target, double* const* p_out, int32_t* reasons,
                             int32_t* iterations, int32_t* evaluations, double* final_total);
+
+/* ---- point-cloud files (pipeline.hpp:52-68) ---------------
+ * xyz text ("x y z" per line, '#' comments) and legacy-VTK ASCII polydata
+ * (points only); output with %.17g, so values round-trip bit-exactly. */
+typedef enum gs_point_format { GS_FORMAT_XYZ = 0, GS_FORMAT_VTK = 1 } gs_point_format;
+/* format_for_path, pipeline_io.cpp:153-158: ".vtk" -> VTK, else xyz. */
+int32_t gs_format_for_path(const char* path);
+/* read_points: call with xyz_out = NULL to get *n_out, then with capacity >= n. */
+gs_status gs_read_points(const char* path, int32_t format, double* xyz_out, int64_t capacity,
+                         int64_t* n_out);
+/* write_points: header lines become '#' comments (xyz) or the title (VTK). */
+gs_status gs_write_points(const char* path, int32_t format, int64_t n, const double* xyz,
+                          const char* const* header, int32_t n_header);
+long long gs_last_parse_line(void);
+const char* gs_last_io_error(void);
 
 /* ---- measured device peaks (roofline denominators) ----------------------------
  * kind 0: FP32 FFMA lane-ops/s (constant operands), 1: MUFU.EX2 lane-ops/s,

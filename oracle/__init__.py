@@ -274,6 +274,9 @@ class Ref:
             "ref_warp_points": [_i64, C.c_int, _d, _d, _i64, _d, C.c_double, C.c_int, C.c_int,
                                 C.c_double, _d],
             "ref_generate": [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64, _d],
+            "ref_read_points": [C.c_char_p, C.c_int, _d, _i64, C.POINTER(_i64),
+                                C.POINTER(C.c_longlong)],
+            "ref_write_points": [C.c_char_p, C.c_int, _i64, _d, C.c_char_p],
             "ref_optimize": [_i64, _d, _d, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
                              C.c_int, _d, C.POINTER(C.c_int), C.POINTER(C.c_int), _d,
                              C.POINTER(C.c_int)],
@@ -385,6 +388,38 @@ class Ref:
                  "line_search_failure", "non_finite"]
         return {"p0": p, "reason": names[reason.value], "iterations": iters.value,
                 "trace": trace[:tl.value]}
+
+    def read_points(self, path, vtk):
+        """-> (status, points or None, parse line). The reference's iostream
+        parsing crashes inside a process that has imported numpy (observed),
+        so it runs in a numpy-free child process."""
+        import json
+        import subprocess
+        import sys
+        code = (
+            "import ctypes as C, json, sys\n"
+            "L = C.CDLL(sys.argv[1])\n"
+            "L.ref_read_points.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_double), C.c_int64,"
+            " C.POINTER(C.c_int64), C.POINTER(C.c_longlong)]\n"
+            "n, line = C.c_int64(), C.c_longlong()\n"
+            "st = L.ref_read_points(sys.argv[2].encode(), int(sys.argv[3]), None, 0, C.byref(n), C.byref(line))\n"
+            "pts = None\n"
+            "if st == 0:\n"
+            "    buf = (C.c_double * (3 * n.value))()\n"
+            "    L.ref_read_points(sys.argv[2].encode(), int(sys.argv[3]), buf, n.value, C.byref(n), C.byref(line))\n"
+            "    pts = [float.hex(v) for v in buf]\n"
+            "print(json.dumps([st, line.value, pts]))\n")
+        out = subprocess.run([sys.executable, "-c", code, REF_SO, path, str(int(vtk))],
+                             capture_output=True, text=True, check=True).stdout
+        st, line, pts = json.loads(out)
+        if st:
+            return st, None, line
+        return 0, np.array([float.fromhex(v) for v in pts]).reshape(-1, 3), 0
+
+    def write_points(self, path, vtk, pts, header=None):
+        pts = _c(pts)
+        self._chk(self.lib.ref_write_points(path.encode(), vtk, len(pts), _p(pts),
+                                            header.encode() if header else None))
 
     def validate_config(self, sigma, lam, timesteps, thr_mult):
         return self.lib.ref_validate_config(sigma, lam, timesteps, thr_mult)

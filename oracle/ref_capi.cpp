@@ -25,6 +25,7 @@
 #include "geoshoot/octree.hpp"
 #include "geoshoot/optimizer.hpp"
 #include "geoshoot/parallel.hpp"
+#include "geoshoot/pipeline.hpp"
 #include "geoshoot/shooting.hpp"
 #include "geoshoot/synthetic.hpp"
 
@@ -404,6 +405,37 @@ int ref_optimize(std::int64_t n, const double* q0, const double* target, double 
       o[4] = r.grad_inf; o[5] = r.wall_ms;
     }
     *trace_len = static_cast<int>(tr.records.size());
+  });
+}
+
+// read_points / write_points, pipeline_io.cpp:160-182. status 10 = ParseError
+// (line in *line), 11 = UnsupportedFormat, 12 = runtime_error (open failure).
+int ref_read_points(const char* path, int vtk, double* out, std::int64_t cap, std::int64_t* n,
+                    long long* line) {
+  try {
+    const PointSet p = read_points(path, vtk ? PointFormat::LegacyPolydataAscii : PointFormat::XyzText);
+    *n = static_cast<std::int64_t>(p.size());
+    if (out && cap >= *n) store(out, p.data());
+    return kOk;
+  } catch (const ParseError& e) {
+    *line = static_cast<long long>(e.line);
+    return 10;
+  } catch (const UnsupportedFormat&) {
+    return 11;
+  } catch (const std::invalid_argument&) {
+    return kInvalidArgument;
+  } catch (const std::runtime_error&) {
+    return 12;
+  }
+}
+
+int ref_write_points(const char* path, int vtk, std::int64_t n, const double* xyz,
+                     const char* header) {
+  return guarded([&] {
+    std::vector<std::string> h;
+    if (header) h.push_back(header);
+    write_points(PointSet(vecs(xyz, n)), path,
+                 vtk ? PointFormat::LegacyPolydataAscii : PointFormat::XyzText, h);
   });
 }
 

@@ -9,7 +9,8 @@ from . import _lib  # noqa: F401
 from .geoshoot import (  # noqa: F401
     BARNES_HUT, EULER, EXACT, F32, F64, RK4, ConfigError, ConfigMismatch, DeviceError,
     DimensionMismatch, EmptyTree, Evaluation, Flow, Geoshoot, NonFiniteState, Octree,
-    OutOfBounds, ShootingConfig, Trajectory)
+    OutOfBounds, ParseError, ShootingConfig, Trajectory, UnsupportedFormat, VTK, XYZ,
+    format_for_path, read_points, write_points)
 
 __all__ = [
     "Geoshoot", "ShootingConfig", "Trajectory", "Octree", "Flow", "Evaluation",

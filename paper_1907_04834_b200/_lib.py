@@ -23,6 +23,9 @@ GS_OUT_OF_BOUNDS = 6
 GS_INVALID_ARGUMENT = 7
 GS_CUDA_ERROR = 8
 GS_NO_DEVICE = 9
+GS_PARSE_ERROR = 10
+GS_UNSUPPORTED_FORMAT = 11
+GS_IO_ERROR = 12
 
 GS_F64, GS_F32 = 0, 1
 GS_EXACT, GS_BARNES_HUT = 0, 1
@@ -135,6 +138,11 @@ SIGNATURES = [
     ("gs_flow_record_bytes", _i64, [_vp]),
     ("gs_flow_stage", _st, [_vp, C.c_int32]),
     ("gs_microbench", _st, [C.c_int, C.c_int32, _d]),
+    ("gs_format_for_path", C.c_int32, [C.c_char_p]),
+    ("gs_read_points", _st, [C.c_char_p, C.c_int32, _d, _i64, C.POINTER(_i64)]),
+    ("gs_write_points", _st, [C.c_char_p, C.c_int32, _i64, _d, C.POINTER(C.c_char_p), C.c_int32]),
+    ("gs_last_parse_line", C.c_longlong, []),
+    ("gs_last_io_error", C.c_char_p, []),
     ("gs_default_opt_config", gs_opt_config, []),
     ("gs_optimize_batch", _st, [C.c_int, C.POINTER(gs_config), C.POINTER(gs_opt_config), C.c_int32,
                                 C.POINTER(C.c_int64), C.POINTER(_d), C.POINTER(_d), C.POINTER(_d),

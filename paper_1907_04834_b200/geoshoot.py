@@ -67,6 +67,55 @@ class DeviceError(GeoshootError):
     pass
 
 
+class ParseError(GeoshootError):
+    def __init__(self, line: int, msg: str):
+        super().__init__(msg)
+        self.line = line
+
+
+class UnsupportedFormat(GeoshootError):
+    pass
+
+
+# ---- point-cloud files (pipeline.hpp:52-68; host-side, no device needed) -----
+XYZ, VTK = 0, 1
+
+
+def format_for_path(path: str) -> int:
+    return L.load().gs_format_for_path(path.encode())
+
+
+def _io_check(lib, st):
+    if st == L.GS_OK:
+        return
+    msg = (lib.gs_last_io_error() or b"").decode()
+    if st == L.GS_PARSE_ERROR:
+        raise ParseError(lib.gs_last_parse_line(), msg)
+    if st == L.GS_UNSUPPORTED_FORMAT:
+        raise UnsupportedFormat(msg)
+    if st == L.GS_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise OSError(msg)
+
+
+def read_points(path: str, fmt: int = None) -> np.ndarray:
+    lib = L.load()
+    fmt = format_for_path(path) if fmt is None else fmt
+    n = C.c_int64()
+    _io_check(lib, lib.gs_read_points(path.encode(), fmt, None, 0, C.byref(n)))
+    out = np.empty((n.value, 3))
+    _io_check(lib, lib.gs_read_points(path.encode(), fmt, _p(out), n.value, C.byref(n)))
+    return out
+
+
+def write_points(points, path: str, fmt: int = None, header=()):
+    lib = L.load()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    fmt = format_for_path(path) if fmt is None else fmt
+    hdr = (C.c_char_p * max(1, len(header)))(*[h.encode() for h in header])
+    _io_check(lib, lib.gs_write_points(path.encode(), fmt, len(pts), _p(pts), hdr, len(header)))
+
+
 # ---- config (core.hpp:184-213) ------------------------------------------------
 EXACT, BARNES_HUT = L.GS_EXACT, L.GS_BARNES_HUT
 EULER, RK4 = L.GS_EULER, L.GS_RK4
