@@ -46,6 +46,7 @@ typedef enum gs_status {
   GS_PARSE_ERROR = 10,       /* ParseError{line}, core.hpp:95-100 (line: gs_last_parse_line) */
   GS_UNSUPPORTED_FORMAT = 11,/* UnsupportedFormat, core.hpp:102-104 */
   GS_IO_ERROR = 12,          /* std::runtime_error "cannot open ..." (pipeline_io.cpp:160-182) */
+  GS_DEGENERATE = 13,        /* DegenerateConfiguration, core.hpp:106-108 */
   GS_INTERNAL = 99
 } gs_status;
 
@@ -309,6 +310,15 @@ gs_status gs_write_points(const char* path, int32_t format, int64_t n, const dou
                           const char* const* header, int32_t n_header);
 long long gs_last_parse_line(void);
 const char* gs_last_io_error(void);
+
+/* ---- rigid pre-alignment (procrustes.cpp:7-58) -----------
+ * Least-squares rotation + translation taking source onto target (index
+ * correspondence, reflection-corrected). Centroids, cross-covariance and the
+ * transform of every point on the device (FP64); the 3x3 SVD on the host.
+ * rotation_rows[9] row-major, translation[3], aligned_out n x 3 (any may be
+ * NULL). GS_DEGENERATE for n < 3 or collinear sources. */
+gs_status gs_procrustes_align(gs_ctx* ctx, int64_t n, const double* source, const double* target,
+                              double* rotation_rows, double* translation, double* aligned_out);
 
 /* ---- measured device peaks (roofline denominators) ----------------------------
  * kind 0: FP32 FFMA lane-ops/s (constant operands), 1: MUFU.EX2 lane-ops/s,

@@ -7,7 +7,8 @@ reference's API in Python; ``include/geoshoot/*.hpp`` does so in C++.
 """
 from . import _lib  # noqa: F401
 from .geoshoot import (  # noqa: F401
-    BARNES_HUT, EULER, EXACT, F32, F64, RK4, ConfigError, ConfigMismatch, DeviceError,
+    BARNES_HUT, EULER, EXACT, F32, F64, RK4, ConfigError, ConfigMismatch, DegenerateConfiguration,
+    DeviceError,
     DimensionMismatch, EmptyTree, Evaluation, Flow, Geoshoot, NonFiniteState, Octree,
     OutOfBounds, ParseError, ShootingConfig, Trajectory, UnsupportedFormat, VTK, XYZ,
     format_for_path, read_points, write_points)

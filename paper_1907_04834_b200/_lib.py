@@ -26,6 +26,7 @@ GS_NO_DEVICE = 9
 GS_PARSE_ERROR = 10
 GS_UNSUPPORTED_FORMAT = 11
 GS_IO_ERROR = 12
+GS_DEGENERATE = 13
 
 GS_F64, GS_F32 = 0, 1
 GS_EXACT, GS_BARNES_HUT = 0, 1
@@ -139,6 +140,7 @@ SIGNATURES = [
     ("gs_flow_stage", _st, [_vp, C.c_int32]),
     ("gs_microbench", _st, [C.c_int, C.c_int32, _d]),
     ("gs_format_for_path", C.c_int32, [C.c_char_p]),
+    ("gs_procrustes_align", _st, [_vp, _i64, _d, _d, _d, _d, _d]),
     ("gs_read_points", _st, [C.c_char_p, C.c_int32, _d, _i64, C.POINTER(_i64)]),
     ("gs_write_points", _st, [C.c_char_p, C.c_int32, _i64, _d, C.POINTER(C.c_char_p), C.c_int32]),
     ("gs_last_parse_line", C.c_longlong, []),

@@ -784,7 +784,7 @@ struct RhsVariant {
 static const RhsVariant kRhsVariants[] = {
     {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true},
     // packed FP32x2 (FFMA2) variants
-    {8, 3, true}, {8, 4, true}, {4, 6, true}};
+    {8, 3, true}, {8, 4, true}, {4, 6, true}, {2, 8, true}};
 constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
 
 static int rhs_variant() {
@@ -830,14 +830,16 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     // small problems: fall back to narrower target blocks so the grid fills the GPU
     const long slots = 3L * dev.sms;
     int use = vi;
-    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = 6;  // TPT 2
-    if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;           // TPT 1
+    // (packed TPT 2 when the chosen variant is packed, scalar TPT 1 for tiny N)
+    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = vi >= 8 ? 11 : 6;
+    if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;
     const RhsVariant u = kRhsVariants[use];
     static int occs[kNumRhsVariants] = {
         occ_rhs_f32<8, 3, true>(), occ_rhs_f32<8, 3, false>(), occ_rhs_f32<8, 4, true>(),
         occ_rhs_f32<4, 6, true>(), occ_rhs_f32<4, 4, false>(), occ_rhs_f32<6, 4, true>(),
         occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>(),
-        occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>()};
+        occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>(),
+        occ_rhs_f32x2<2, 8>()};
     const int tp[] = {u.tpt};
     Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
     if (pl.S > part_cap_chunks) return -1;
@@ -854,6 +856,7 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
       case 8: launch_rhs_f32x2<8, 3>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 9: launch_rhs_f32x2<8, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 10: launch_rhs_f32x2<4, 6>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 11: launch_rhs_f32x2<2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
     }
     return pl.S;

@@ -15,6 +15,7 @@
 #include "geoshoot/kernel_exact.hpp"
 #include "geoshoot/octree.hpp"
 #include "geoshoot/optimizer.hpp"
+#include "geoshoot/pipeline.hpp"
 #include "geoshoot/shooting.hpp"
 #include "geoshoot_b200.h"
 
@@ -62,6 +63,7 @@ void check(gs_status st) {
     case GS_EMPTY_TREE: throw EmptyTree(msg);
     case GS_OUT_OF_BOUNDS: throw OutOfBounds(msg);
     case GS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case GS_DEGENERATE: throw DegenerateConfiguration(msg);
     default: throw DeviceError("geoshoot device error " + std::to_string(st) + ": " + msg);
   }
 }
@@ -477,6 +479,57 @@ Evaluation evaluate(const PointSet& q0, const MomentumSet& p0, const PointSet& t
   ev.stats.traversal = to_traversal(st);
   ev.stats.traversal_queries = st.traversal_queries;
   return ev;
+}
+
+// ---- point-cloud files ----------------------------------------------------------
+namespace {
+void io_check(gs_status st) {
+  if (st == GS_OK) return;
+  const std::string msg = gs_last_io_error();
+  if (st == GS_PARSE_ERROR) {
+    const std::string prefix = "line " + std::to_string(gs_last_parse_line()) + ": ";
+    throw ParseError((std::size_t)gs_last_parse_line(),
+                     msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
+  }
+  if (st == GS_UNSUPPORTED_FORMAT) throw UnsupportedFormat(msg);
+  if (st == GS_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+int32_t fmt_of(PointFormat f) { return f == PointFormat::LegacyPolydataAscii ? GS_FORMAT_VTK : GS_FORMAT_XYZ; }
+}  // namespace
+
+PointFormat format_for_path(const std::string& path) {
+  return gs_format_for_path(path.c_str()) == GS_FORMAT_VTK ? PointFormat::LegacyPolydataAscii
+                                                            : PointFormat::XyzText;
+}
+
+PointSet read_points(const std::string& path, PointFormat format) {
+  int64_t n = 0;
+  io_check(gs_read_points(path.c_str(), fmt_of(format), nullptr, 0, &n));
+  std::vector<Vec3> v((std::size_t)n);
+  io_check(gs_read_points(path.c_str(), fmt_of(format), raw(v), n, &n));
+  return PointSet(std::move(v));
+}
+
+void write_points(const PointSet& points, const std::string& path, PointFormat format,
+                  const std::vector<std::string>& header_comments) {
+  std::vector<const char*> h;
+  for (const auto& s : header_comments) h.push_back(s.c_str());
+  io_check(gs_write_points(path.c_str(), fmt_of(format), (int64_t)points.size(), raw(points.data()),
+                           h.data(), (int32_t)h.size()));
+}
+
+// ---- rigid pre-alignment ---------------------------------------------------------
+ProcrustesResult procrustes_align(const PointSet& source, const PointSet& target) {
+  require_aligned(source.size(), target.size(), "procrustes_align");
+  double R[9], t[3];
+  std::vector<Vec3> y(source.size());
+  check(gs_procrustes_align(ctx(), (int64_t)source.size(), raw(source.data()), raw(target.data()),
+                            R, t, raw(y)));
+  RigidTransform tf;
+  for (int r = 0; r < 3; ++r) tf.rotation_rows[r] = {R[3 * r], R[3 * r + 1], R[3 * r + 2]};
+  tf.translation = {t[0], t[1], t[2]};
+  return {tf, PointSet(std::move(y))};
 }
 
 // ---- optimizer ------------------------------------------------------------------

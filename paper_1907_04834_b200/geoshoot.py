@@ -77,6 +77,10 @@ class UnsupportedFormat(GeoshootError):
     pass
 
 
+class DegenerateConfiguration(GeoshootError):
+    pass
+
+
 # ---- point-cloud files (pipeline.hpp:52-68; host-side, no device needed) -----
 XYZ, VTK = 0, 1
 
@@ -219,6 +223,8 @@ class Geoshoot:
             raise OutOfBounds(msg)
         if st == L.GS_INVALID_ARGUMENT:
             raise ValueError(msg)
+        if st == L.GS_DEGENERATE:
+            raise DegenerateConfiguration(msg)
         raise DeviceError(f"status {st}: {msg}")
 
     # ---- kernel_exact -----------------------------------------------------
@@ -376,6 +382,14 @@ class Geoshoot:
                                               reasons, iters, evals, _p(tot)))
         return {"p0": outs, "reasons": list(reasons), "iterations": list(iters),
                 "evaluations": list(evals), "final_total": tot}
+
+    def procrustes_align(self, source, target):
+        """procrustes_align (procrustes.cpp:7-58) -> (rotation 3x3, translation, aligned)."""
+        s, t = _arr(source, "source"), _arr(target, "target")
+        _require_aligned(len(s), len(t), "procrustes_align")
+        R, tr, y = np.empty((3, 3)), np.empty(3), np.empty_like(s)
+        self.check(self.lib.gs_procrustes_align(self.ctx, len(s), _p(s), _p(t), _p(R), _p(tr), _p(y)))
+        return R, tr, y
 
     def flow(self, cfg: ShootingConfig, n: int) -> "Flow":
         return Flow(self, cfg, n)

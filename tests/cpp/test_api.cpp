@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "geoshoot/bh_kernel.hpp"
+#include "geoshoot/optimizer.hpp"
+#include "geoshoot/pipeline.hpp"
 #include "geoshoot/shooting.hpp"
 
 using namespace geoshoot;
@@ -201,11 +203,37 @@ static void shooting() {
   for (std::size_t i = 0; i < 60; ++i) CHECK(norm(w[i] - tr.final_state().q[i]) < 1e-10);
 }
 
+static void adjacent() {
+  // optimize (optimizer.cpp:301-351): objective decreases from p0 = 0
+  const PointSet q(vecs(40, 0, 6, 501));
+  std::vector<Vec3> moved = q.data();
+  for (Vec3& v : moved) v += Vec3{0.3, -0.2, 0.1};
+  ShootingConfig c = cfg(2.0, 1.0, 6);
+  c.optimizer.max_iterations = 10;
+  auto [p, trace] = optimize(q, PointSet(moved), c);
+  CHECK(trace.records.size() >= 2 && trace.records.back().total < trace.records.front().total);
+  CHECK(p.size() == q.size());
+  // files: %.17g round trip (pipeline_io.cpp:117-149)
+  const std::string f = "/tmp/geoshoot_b200_test_api.vtk";
+  write_points(q, f, format_for_path(f), {"title"});
+  const PointSet back = read_points(f, PointFormat::LegacyPolydataAscii);
+  bool same = back.size() == q.size();
+  for (std::size_t i = 0; same && i < q.size(); ++i) same = back[i] == q[i];
+  CHECK(same);
+  // procrustes: exact recovery of a translation
+  const ProcrustesResult pr = procrustes_align(q, PointSet(moved));
+  CHECK(norm(pr.transform.translation - Vec3{0.3, -0.2, 0.1}) < 1e-12);
+  CHECK(throws<DegenerateConfiguration>([] {
+    procrustes_align(PointSet({{0, 0, 0}, {1, 1, 1}}), PointSet({{0, 0, 0}, {1, 1, 1}}));
+  }));
+}
+
 int main() {
   kernel_exact();
   octree();
   bh();
   shooting();
+  adjacent();
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
