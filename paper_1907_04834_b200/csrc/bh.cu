@@ -43,6 +43,10 @@ double gate_t2(double thr) {
 namespace {
 
 constexpr int kBhNT = 128;
+#ifndef GS_BH_MINB
+#define GS_BH_MINB 1
+#endif
+constexpr int kBhMinBlocks = GS_BH_MINB;  // caps registers (occupancy hides the node-load latency)
 
 template <typename R>
 struct BhArgs {
@@ -320,7 +324,7 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
 // iteration whatever node each lane is at. Same per-query node set, decisions
 // and counts as the reference; only the summation order differs.
 template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
+__global__ void __launch_bounds__(kBhNT, kBhMinBlocks) k_bh_ws(const BhArgs<R> a) {
   const int qi = blockIdx.x * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
@@ -355,25 +359,28 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
   const V4<R> zero = mk4<R>(0, 0, 0);
   while (__any_sync(0xffffffffu, next < m || j <= je)) {
     bool have = false;
-    bool approx = false;
-    int src = 0;
+    V4<R> Q = zero, P = zero, Al = zero, Be = zero;  // this iteration's unit
     if (j > je && next < m) {
       const int nd = next;
-      V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);  // one 32-B sector (FP32)
+      const V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);  // one 32-B sector (FP32)
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
       ++c_vis;
       next = code & 0x3fffffff;
-      if (code < 0) {  // single-point leaf
-        j = begin;
-        je = begin;
+      if (code < 0) {  // single-point leaf: the record holds the point itself
+        Q = l;
+        P = h;
+        if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
+        have = true;
+        ++c_dir;
       } else if (code & 0x40000000) {  // depth-32 bucket: all its points
         j = begin;
         je = begin + code_of(ld4(a.mom + nd).w) - 1;
       } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
-        approx = true;
+        Q = ld4(a.cen + nd);
+        P = ld4(a.mom + nd);
+        if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
         have = true;
-        src = nd;
         ++c_app;
       } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
         j = begin;
@@ -388,23 +395,14 @@ __global__ void __launch_bounds__(kBhNT) k_bh_ws(const BhArgs<R> a) {
     const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
     if (big) coop_ranges<R, MODE>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
     if (!have && j <= je) {
+      Q = ld4(a.srec + 2 * j);
+      P = ld4(a.srec + 2 * j + 1);
+      if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * j); Be = ld4(a.sadj + 2 * j + 1); }
       have = true;
-      src = j++;
+      ++j;
       ++c_dir;
     }
-    if (have) {
-      V4<R> Q, P, Al = zero, Be = zero;
-      if (approx) {
-        Q = ld4(a.cen + src);
-        P = ld4(a.mom + src);
-        if (MODE == kBhHess) { Al = ld4(a.nadj_a + src); Be = ld4(a.nadj_b + src); }
-      } else {
-        Q = ld4(a.srec + 2 * src);
-        P = ld4(a.srec + 2 * src + 1);
-        if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * src); Be = ld4(a.sadj + 2 * src + 1); }
-      }
-      unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
-    }
+    if (have) unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);

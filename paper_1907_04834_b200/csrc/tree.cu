@@ -517,7 +517,8 @@ template <typename R>
 __global__ void k_finalize(int mode, const int4* meta, const int* mp, const double4* s0,
                            const double4* s1, double kap, double c0x, double c0y, double c0z,
                            int scaled, V4<R>* o0, V4<R>* o1, const V4<R>* lo = nullptr,
-                           const V4<R>* hi = nullptr, V4<R>* nrec = nullptr) {
+                           const V4<R>* hi = nullptr, V4<R>* nrec = nullptr,
+                           const V4<R>* srec = nullptr) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= *mp) return;
   const int4 mi = meta[i];
@@ -527,7 +528,11 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
   if (mode == 0 && nrec) {
     const bool leaf = mi.w & 1;
     const int code = mi.x | ((leaf && cnt == 1) ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0);
-    V4<R> l = ld4(lo + i), h = ld4(hi + i);
+    // a single-point leaf is always direct (leaf-first, bh_kernel.cpp:40-45), so
+    // its record carries the point itself -- interaction coords and momentum --
+    // and the traversal needs no second, dependent load for it
+    V4<R> l = (leaf && cnt == 1) ? ld4(srec + 2 * mi.y) : ld4(lo + i);
+    V4<R> h = (leaf && cnt == 1) ? ld4(srec + 2 * mi.y + 1) : ld4(hi + i);
     l.w = ival(R(0), code);
     h.w = ival(R(0), mi.y);
     st4(nrec + 2 * i, l);
@@ -732,9 +737,9 @@ int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t
   const int scaled = prec == kF32;
   t.kc = kc;
   if (prec == kF32)
-    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.nrec.as<float4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.nrec.as<float4>(), t.srec.as<float4>());
   else
-    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.nrec.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.nrec.as<double4>(), t.srec.as<double4>());
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
