@@ -119,7 +119,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "flow steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config4 exact RK4 N={args.n} (extrapolated by N^2 from a sample)",
                    "n": args.n, "sigma": SIGMA, "integrator": "rk4", "timesteps": T_STEPS},
@@ -250,7 +250,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "flow steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak" if False else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform cube, BASELINE config 4)",
         "config": {"workload": f"config4: exact all-pairs RHS, RK4 x {T_STEPS} steps, N={N}, "
                                f"sigma={SIGMA}, unit cube, fp32; 1 step = 4 RHS",

@@ -82,7 +82,21 @@ struct gs_flow {
   BhWork bh;
   gs_stats stats{};
   KTimer* timer = nullptr;  // gs_flow_profile
-  ~gs_flow() { delete timer; }
+  // CUDA graph of one integrator step (all stages + the step-counter bump),
+  // captured after the first eager step and replayed for the following ones
+  DBuf stepctr;
+  cudaGraphExec_t gexec = nullptr;
+  KernelConsts gkc{};
+  gs_config gcfg{};
+  int64_t gn = -1, glaunches = 0;
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+  ~gs_flow() {
+    drop_graph();
+    delete timer;
+  }
 };
 
 extern "C" {
@@ -281,6 +295,7 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
   e.dt = 1.0 / f->cfg.timesteps;
   e.bad_step = f->flags.as<int>();
   e.step = f->steps_done + 1;
+  e.step_dev = f->stepctr.as<int>();
   const bool first = f->want_energy && f->steps_done == 0 && stage == 0;
   if (first) {
     GS_TRY(f->epart.ensure(sizeof(double) * (f->shard_count / 128 + 8)));
@@ -332,6 +347,8 @@ int flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
   GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), c->stream));  // bad_step = +big, no overflow
   GS_TRY(f->bh.stats.ensure(64));
   GS_CUDA_OK(cudaMemsetAsync(f->bh.stats.ptr, 0, 64, c->stream));
+  GS_TRY(f->stepctr.ensure(64));
+  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), c->stream));
   return GS_OK;
 }
 
@@ -355,14 +372,73 @@ int flow_upload(gs_flow* f, const double* q0, const double* p0) {
   f->steps_done = 0;
   f->have_energy_part = false;
   GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), f->ctx->stream));
+  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), f->ctx->stream));
+  return GS_OK;
+}
+
+int flow_step_eager(gs_flow* f) {
+  for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
+  GS_TRY(step_counter_inc(f->stepctr.as<int>(), f->ctx->stream));
+  ++f->launches;
+  ++f->steps_done;
+  return GS_OK;
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_GRAPHS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Capture one step (the kernel parameters -- buffers, constants -- are fixed
+// for a given flow configuration and input scaling), instantiate, keep.
+int flow_capture_step(gs_flow* f) {
+  f->drop_graph();
+  cudaStream_t st = f->ctx->stream;
+  const gs_stats saved = f->stats;
+  const int64_t l0 = f->launches;
+  const int steps_saved = f->steps_done;
+  cudaGraph_t g = nullptr;
+  GS_CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int s = GS_OK;
+  for (int k = 0; k < flow_stages(f) && s == GS_OK; ++k) s = flow_stage(f, k, nullptr, nullptr);
+  if (s == GS_OK) s = step_counter_inc(f->stepctr.as<int>(), st);
+  const cudaError_t ce = cudaStreamEndCapture(st, &g);
+  f->stats = saved;  // nothing ran during capture
+  f->steps_done = steps_saved;
+  GS_TRY(s);
+  GS_CUDA_OK(ce);
+  const cudaError_t ie = cudaGraphInstantiate(&f->gexec, g, 0);
+  cudaGraphDestroy(g);
+  GS_CUDA_OK(ie);
+  f->glaunches = f->launches - l0 + 1;
+  f->launches = l0;
+  std::memcpy(&f->gkc, &f->kc, sizeof f->kc);  // byte copies: compared with memcmp
+  std::memcpy(&f->gcfg, &f->cfg, sizeof f->cfg);
+  f->gn = f->n;
   return GS_OK;
 }
 
 int flow_advance(gs_flow* f, int steps) {
   f->launches = 0;
+  const bool graphs = graphs_enabled() && !f->timer && f->shard_begin == 0 && f->shard_count == f->n;
   for (int k = 0; k < steps; ++k) {
-    for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
+    if (!graphs || f->steps_done == 0) {  // the first step runs eagerly (energy, allocations)
+      GS_TRY(flow_step_eager(f));
+      continue;
+    }
+    if (!f->gexec || f->gn != f->n || std::memcmp(&f->gkc, &f->kc, sizeof f->kc) != 0 ||
+        std::memcmp(&f->gcfg, &f->cfg, sizeof f->cfg) != 0)
+      GS_TRY(flow_capture_step(f));
+    GS_CUDA_OK(cudaGraphLaunch(f->gexec, f->ctx->stream));
+    f->launches += f->glaunches;
     ++f->steps_done;
+    if (f->cfg.backend == GS_EXACT) {  // the host-side counters an eager step keeps
+      f->stats.direct_interactions += (uint64_t)flow_stages(f) * f->n * (uint64_t)f->shard_count;
+      f->stats.traversal_queries += (uint64_t)flow_stages(f) * f->shard_count;
+    }
   }
   return GS_OK;
 }
@@ -521,7 +597,10 @@ gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
   if (!f || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");
   f->launches = 0;
   GS_TRY(flow_stage(f, stage, nullptr, nullptr));
-  if (stage == flow_stages(f) - 1) ++f->steps_done;
+  if (stage == flow_stages(f) - 1) {
+    GS_TRY(step_counter_inc(f->stepctr.as<int>(), f->ctx->stream));
+    ++f->steps_done;
+  }
   return GS_OK;
 }
 
@@ -653,13 +732,13 @@ gs_status gs_shoot_forward(gs_ctx* c, const gs_config* cfg, int64_t n, const dou
     GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n * (T + 1)));
   }
   Timer tm(c->stream);
-  for (int k = 0; k <= T; ++k) {
-    if (traj)
+  if (!traj) {
+    GS_TRY(flow_advance(f, T));  // graph-replayed after the first step
+  } else {
+    for (int k = 0; k <= T; ++k) {
       GS_TRY(unpack_records(f->prec, f->rec.ptr, n, c->stage_c.as<double>() + (size_t)3 * n * k,
                             c->stage_d.as<double>() + (size_t)3 * n * k, c->stream));
-    if (k < T) {
-      for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
-      ++f->steps_done;
+      if (k < T) GS_TRY(flow_step_eager(f));
     }
   }
   const double fwd_ms = tm.ms();

@@ -108,6 +108,7 @@ struct FwdEpi {
   double* energy_part = nullptr;  // optional per-block partial of <p, dH/dp>
   int* bad_step = nullptr;        // atomicMin on non-finite output
   int step = 0;                   // step index (1-based) reported on non-finite
+  const int* step_dev = nullptr;  // if set: step = *step_dev + 1 (graph-replayable)
 };
 int fwd_epilogue(int prec, const FwdEpi& e, cudaStream_t st, int* blocks_out);
 
@@ -146,5 +147,7 @@ int gradient_finalize(int prec, const void* adj, const double* dhdp0, int64_t n,
 int adjoint_init(int prec, const void* rec_T, const double* target, double lambda, int64_t n,
                  void* adj, double* sse_part, int* blocks, cudaStream_t st);
 int reduce_sum(const double* part, int count, double* out, cudaStream_t st);
+// ++*counter on the device (the step counter of graph-replayed flows)
+int step_counter_inc(int* counter, cudaStream_t st);
 
 }  // namespace gsb

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kEpiNT) k_fwd_epi(FwdEpi e) {
       st4(out + 2 * i + 1, p);
       if (check && e.bad_step &&
           !(fin(q.x) && fin(q.y) && fin(q.z) && fin(p.x) && fin(p.y) && fin(p.z)))
-        atomicMin(e.bad_step, e.step);
+        atomicMin(e.bad_step, e.step_dev ? *e.step_dev + 1 : e.step);
     }
   }
   if (e.energy_part) {
@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(kEpiNT) k_adj_init(const V4<R>* recT, const do
   if (threadIdx.x == 0 && sse_part) sse_part[blockIdx.x] = s;
 }
 
+__global__ void k_step_inc(int* c) { *c += 1; }
+
 __global__ void k_reduce(const double* part, int count, double* out) {
   // one warp, fixed order per lane then fixed tree: deterministic
   double s = 0.0;
@@ -300,6 +302,12 @@ int adjoint_init(int prec, const void* rec_T, const double* target, double lambd
     k_adj_init<float><<<nb, kEpiNT, 0, st>>>((const float4*)rec_T, target, lambda, n, (float4*)adj, sse_part);
   else
     k_adj_init<double><<<nb, kEpiNT, 0, st>>>((const double4*)rec_T, target, lambda, n, (double4*)adj, sse_part);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int step_counter_inc(int* counter, cudaStream_t st) {
+  k_step_inc<<<1, 1, 0, st>>>(counter);
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }

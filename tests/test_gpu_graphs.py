@@ -1,0 +1,53 @@
+"""CUDA-graph replay of integrator steps (capi.cu flow_advance) is bit-identical
+to eager stepping: the same launches with the same arguments, only replayed.
+Eager mode is forced with GS_GRAPHS=0 in a child process (the switch is read
+once per process)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, numpy as np
+from paper_1907_04834_b200 import Geoshoot, ShootingConfig, EXACT, BARNES_HUT, F32, F64, EULER, RK4
+from tests.util import uniform, sym_uniform
+out = {}
+gs = Geoshoot()
+q, p, t = uniform(700, 3.0, 11), sym_uniform(700, 0.2, 12), uniform(700, 3.0, 13)
+for be in (EXACT, BARNES_HUT):
+    for prec in (F64, F32):
+        for integ in (EULER, RK4):
+            cfg = ShootingConfig(sigma=0.4, timesteps=7, backend=be, precision=prec, integrator=integ)
+            fq, fp, e, st = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+            key = f"{be}_{prec}_{integ}"
+            out[key + "_q"], out[key + "_p"] = fq, fp
+            out[key + "_e"] = np.array([e])
+            out[key + "_direct"] = np.array([st["direct_interactions"]])
+            f = gs.flow(cfg, len(q))
+            f.upload(q, p)
+            f.advance(3)
+            f.advance(2)
+            out[key + "_fq"], out[key + "_fp"] = f.download()
+np.savez(sys.argv[1], **out)
+"""
+
+
+def _run(tmp_path, graphs):
+    path = str(tmp_path / f"g{graphs}.npz")
+    env = dict(os.environ, GS_GRAPHS=str(graphs))
+    subprocess.run([sys.executable, "-c", CHILD, path], check=True, cwd=ROOT, env=env, timeout=600)
+    return np.load(path)
+
+
+def test_graph_replay_bitwise_equals_eager(tmp_path):
+    g, e = _run(tmp_path, 1), _run(tmp_path, 0)
+    assert sorted(g.files) == sorted(e.files)
+    for k in g.files:
+        assert np.array_equal(g[k], e[k]), k
+
