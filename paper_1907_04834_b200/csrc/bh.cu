@@ -26,6 +26,7 @@
 // falls back to the exact FP64 test inside the band.
 #include <cfloat>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "bh.h"
@@ -43,10 +44,6 @@ double gate_t2(double thr) {
 namespace {
 
 constexpr int kBhNT = 128;
-#ifndef GS_BH_MINB
-#define GS_BH_MINB 1
-#endif
-constexpr int kBhMinBlocks = GS_BH_MINB;  // caps registers (occupancy hides the node-load latency)
 
 template <typename R>
 struct BhArgs {
@@ -70,6 +67,10 @@ struct BhArgs {
   R thr2_hi, thr2_lo;  // FP32 guard band around T2
   R thr2_in;           // max-distance shortcut: all descendants open
   R inv_two_s, c1;     // FP64 exp scale; HESS FP32 constant
+  R grp_lim2;          // warps whose query box has diagonal^2 <= this walk as a group
+  int split;           // 1: k_bh_grp takes the group warps, k_bh_ws the others
+  int ntask;           // pre-order node windows per query (blockIdx.y); partials [task][query]
+  unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
   uint32_t* per_query;
   unsigned long long* totals;
@@ -242,7 +243,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    V4<R>* o = a.part + (size_t)per * out;
+    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
+    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
     for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
     if (a.per_query) {
       a.per_query[3 * out] = c_dir;
@@ -263,6 +265,26 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
       atomicAdd(a.totals + 2, v);
     }
   }
+}
+
+// Squared diagonal of the warp's query box (valid lanes only): decides, per
+// warp and identically in both kernels of a split launch, whether the warp's
+// queries walk the tree as a group (k_bh_grp) or independently (k_bh_ws).
+template <typename R>
+__device__ __forceinline__ R warp_box_diag2(const V4<R>& x, bool valid) {
+  R lx = valid ? x.x : R(INFINITY), ly = valid ? x.y : R(INFINITY), lz = valid ? x.z : R(INFINITY);
+  R hx = valid ? x.x : R(-INFINITY), hy = valid ? x.y : R(-INFINITY), hz = valid ? x.z : R(-INFINITY);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lx = min(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+    ly = min(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+    lz = min(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+    hx = max(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+    hy = max(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+    hz = max(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+  }
+  if (!(hx >= lx)) return R(0);  // no valid lane
+  return (hx - lx) * (hx - lx) + (hy - ly) * (hy - ly) + (hz - lz) * (hz - lz);
 }
 
 // Cooperative sweep of one lane's long direct range: the 32 lanes split the
@@ -323,8 +345,14 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
 // the interaction together, so the warp does one unit of work per lane per
 // iteration whatever node each lane is at. Same per-query node set, decisions
 // and counts as the reference; only the summation order differs.
+// FP32: cap registers for occupancy (RHS 80 regs -> 6 CTAs/SM, no spills)
 template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT, kBhMinBlocks) k_bh_ws(const BhArgs<R> a) {
+constexpr int ws_min_blocks() {
+  return sizeof(R) != 4 ? 1 : (MODE == kBhRhs ? 6 : (MODE == kBhHess ? 4 : 5));
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT, ws_min_blocks<R, MODE>()) k_bh_ws(const BhArgs<R> a) {
   const int qi = blockIdx.x * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
@@ -349,11 +377,21 @@ __global__ void __launch_bounds__(kBhNT, kBhMinBlocks) k_bh_ws(const BhArgs<R> a
       out = (i >= 0 && i < a.n_tgt) ? i : -1;
     }
   }
+  if (a.split && warp_box_diag2<R>(x, out >= 0) <= a.grp_lim2) return;  // k_bh_grp's warp
   Acc<R> acc;
 #pragma unroll
   for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
   uint32_t c_dir = 0, c_app = 0, c_vis = 0;
   const int m = *a.mp;
+  // this block's window [A, B) of the pre-order node array and the leaf-order
+  // interval [bA, bB) of the leaves inside it (see bh_tasks)
+  int A = 0, B = m, bA = 0, bB = a.n;
+  if (a.ntask > 1) {
+    A = (int)((long long)m * blockIdx.y / a.ntask);
+    B = (int)((long long)m * (blockIdx.y + 1) / a.ntask);
+    bA = A < m ? code_of(ld4(a.nrec + 2 * A + 1).w) : a.n;
+    bB = B < m ? code_of(ld4(a.nrec + 2 * B + 1).w) : a.n;
+  }
   int next = out >= 0 ? 0 : INT_MAX;
   int j = 0, je = -1;  // pending direct range
   const V4<R> zero = mk4<R>(0, 0, 0);
@@ -365,31 +403,37 @@ __global__ void __launch_bounds__(kBhNT, kBhMinBlocks) k_bh_ws(const BhArgs<R> a
       const V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);  // one 32-B sector (FP32)
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
-      ++c_vis;
-      next = code & 0x3fffffff;
-      if (code < 0) {  // single-point leaf: the record holds the point itself
-        Q = l;
-        P = h;
-        if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
-        have = true;
-        ++c_dir;
-      } else if (code & 0x40000000) {  // depth-32 bucket: all its points
-        j = begin;
-        je = begin + code_of(ld4(a.mom + nd).w) - 1;
-      } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
-        Q = ld4(a.cen + nd);
-        P = ld4(a.mom + nd);
-        if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
-        have = true;
-        ++c_app;
-      } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
-        j = begin;
-        je = begin + code_of(ld4(a.mom + nd).w) - 1;
-        c_vis += (uint32_t)(next - nd - 1);
-      } else {
-        next = nd + 1;
+      const int skip = code & 0x3fffffff;
+      const bool own = nd >= A;  // the node itself is in this block's window
+      next = skip;
+      if (skip > A) {  // the subtree reaches into the window (else: pass it by)
+        c_vis += own;
+        if (code < 0) {  // single-point leaf (always own): the record holds the point itself
+          Q = l;
+          P = h;
+          if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
+          have = true;
+          ++c_dir;
+        } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
+          j = begin;
+          je = begin + code_of(ld4(a.mom + nd).w) - 1;
+        } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
+          if (own) {
+            Q = ld4(a.cen + nd);
+            P = ld4(a.mom + nd);
+            if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+            have = true;
+            ++c_app;
+          }
+        } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
+          j = max(begin, bA);
+          je = min(begin + code_of(ld4(a.mom + nd).w), bB) - 1;
+          c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+        } else {
+          next = nd + 1;
+        }
       }
-      if (next <= nd) next = INT_MAX;  // never loop on a corrupt skip
+      if (next >= B || next <= nd) next = INT_MAX;  // window done; never loop on a corrupt skip
     }
     // long direct ranges (dense near field) are swept by the whole warp
     const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
@@ -406,7 +450,185 @@ __global__ void __launch_bounds__(kBhNT, kBhMinBlocks) k_bh_ws(const BhArgs<R> a
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    V4<R>* o = a.part + (size_t)per * out;
+    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
+    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
+    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
+    if (a.per_query) {
+      a.per_query[3 * out] = c_dir;
+      a.per_query[3 * out + 1] = c_app;
+      a.per_query[3 * out + 2] = c_vis;
+    }
+  }
+  if (a.totals) {
+    unsigned long long d = c_dir, p = c_app, v = c_vis;
+    for (int o = 16; o > 0; o >>= 1) {
+      d += __shfl_down_sync(0xffffffffu, d, o);
+      p += __shfl_down_sync(0xffffffffu, p, o);
+      v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.totals, d);
+      atomicAdd(a.totals + 1, p);
+      atomicAdd(a.totals + 2, v);
+    }
+  }
+}
+
+// Group walk for warps whose 32 queries sit close together relative to the
+// threshold (the dense regime of configs 2, 3 and 5, where each query's direct
+// near field is thousands of points and neighbouring queries' fields nearly
+// coincide). The warp walks the union of its lanes' node sets in pre-order,
+// always serving the smallest pending node (lanes parked there classify it
+// with their own exact gate, exactly as the reference would for that query).
+// Direct work is NOT done per lane: each lane only records its pending direct
+// interval of leaf-order points (a leaf, bucket, or fully-inside subtree), and
+// the warp sweeps the union of the lanes' intervals in leaf order, one point
+// per step with a broadcast load, every lane whose interval covers the point
+// accumulating it. Sweeping [cursor, F) is safe once F = begin(current node):
+// every lane has decided all its nodes before the current one. Each query's
+// (direct, approximated, visited) sets and counts equal the reference's; only
+// the summation order differs (and is fixed, so results are deterministic).
+template <typename R, int MODE>
+__device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Acc<R>& acc,
+                                          uint32_t& c_dir, const V4<R>& xs, const V4<R>& px,
+                                          const V4<R>& ai, const V4<R>& bi, const BhArgs<R>& a,
+                                          unsigned& n_seg, unsigned& n_step) {
+  for (;;) {
+    const int from = max(ds, cursor);
+    const int start = __reduce_min_sync(0xffffffffu, (de >= from) ? from : INT_MAX);
+    if (start >= F) return;
+    cursor = start;
+    const bool cover = ds <= cursor && cursor <= de;
+    const int lim = cover ? de + 1 : ((ds > cursor && de >= ds) ? ds : INT_MAX);
+    const int seg_end = min(F, __reduce_min_sync(0xffffffffu, lim));
+    ++n_seg;
+    n_step += (unsigned)(seg_end - cursor);
+    if (cover) {
+      c_dir += (uint32_t)(seg_end - cursor);
+#pragma unroll 4
+      for (int j = cursor; j < seg_end; ++j) {
+        const V4<R> Q = ld4(a.srec + 2 * j), P = ld4(a.srec + 2 * j + 1);
+        if (MODE == kBhHess)
+          unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
+        else
+          unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Q, Q, a);
+      }
+    }
+    cursor = seg_end;
+  }
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
+  const int qi = blockIdx.x * kBhNT + threadIdx.x;
+  const bool valid = qi < a.nq;
+  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
+  int out = -1;
+  if (valid) {
+    if (MODE == kBhVel) {
+      x = ld4(a.ev + 2 * qi);
+      if (sizeof(R) == 4)
+        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
+                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
+                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
+      else
+        xs = x;
+      out = qi;
+    } else {
+      const int t = qi;
+      x = ld4(a.squ + t);
+      xs = ld4(a.srec + 2 * t);
+      px = ld4(a.srec + 2 * t + 1);
+      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
+      const int i = a.perm[t] - a.tgt_begin;
+      out = (i >= 0 && i < a.n_tgt) ? i : -1;
+    }
+  }
+  if (a.split && !(warp_box_diag2<R>(x, out >= 0) <= a.grp_lim2)) return;  // k_bh_ws's warp
+  Acc<R> acc;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
+  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
+  const int m = *a.mp;
+  // this block's window [A, B) of the pre-order node array and the leaf-order
+  // interval [bA, bB) of the leaves inside it (see bh_tasks)
+  int A = 0, B = m, bA = 0, bB = a.n;
+  if (a.ntask > 1) {
+    A = (int)((long long)m * blockIdx.y / a.ntask);
+    B = (int)((long long)m * (blockIdx.y + 1) / a.ntask);
+    bA = A < m ? code_of(ld4(a.nrec + 2 * A + 1).w) : a.n;
+    bB = B < m ? code_of(ld4(a.nrec + 2 * B + 1).w) : a.n;
+  }
+  int next = out >= 0 ? 0 : INT_MAX;
+  int ds = 0, de = -1;  // this lane's pending direct interval (leaf order, inclusive)
+  int cursor = 0;       // warp-uniform sweep position
+  unsigned n_iter = 0, n_seg = 0, n_step = 0;
+  const V4<R> zero = mk4<R>(0, 0, 0);
+  for (;;) {
+    const int nd = __reduce_min_sync(0xffffffffu, next);
+    if (nd == INT_MAX) break;
+    ++n_iter;
+    // the node's compact record, loaded by every lane (one broadcast sector)
+    const V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);
+    const int code = code_of(l.w);
+    const int begin = code_of(h.w);
+    const int skip = code & 0x3fffffff;
+    const bool here = next == nd;
+    bool have = false, ranged = false;
+    V4<R> Q = zero, P = zero, Al = zero, Be = zero;
+    int rb = 0, re = -1;
+    if (here) {
+      const bool own = nd >= A;  // the node itself is in this block's window
+      next = skip;
+      if (skip > A) {  // the subtree reaches into the window (else: pass it by)
+        c_vis += own;
+        if (code < 0) {  // single-point leaf (always own): the record holds the point itself
+          Q = l;
+          P = h;
+          if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
+          have = true;
+          ++c_dir;
+        } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
+          ranged = true;
+          rb = begin;
+          re = begin + code_of(ld4(a.mom + nd).w) - 1;
+        } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
+          if (own) {
+            Q = ld4(a.cen + nd);
+            P = ld4(a.mom + nd);
+            if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+            have = true;
+            ++c_app;
+          }
+        } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
+          ranged = true;
+          rb = max(begin, bA);
+          re = min(begin + code_of(ld4(a.mom + nd).w), bB) - 1;
+          c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+        } else {
+          next = nd + 1;
+        }
+      }
+      if (next >= B || next <= nd) next = INT_MAX;
+    }
+    if (__any_sync(0xffffffffu, ranged)) {
+      // every earlier pending interval ends before begin(nd): settle them first
+      grp_sweep<R, MODE>(begin, cursor, ds, de, acc, c_dir, xs, px, ai, bi, a, n_seg, n_step);
+      if (ranged) { ds = rb; de = re; }
+    }
+    if (have) unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
+  }
+  grp_sweep<R, MODE>(INT_MAX, cursor, ds, de, acc, c_dir, xs, px, ai, bi, a, n_seg, n_step);
+  if (a.dbg && (threadIdx.x & 31) == 0) {
+    atomicAdd(a.dbg, 1ull);
+    atomicAdd(a.dbg + 1, (unsigned long long)n_iter);
+    atomicAdd(a.dbg + 2, (unsigned long long)n_seg);
+    atomicAdd(a.dbg + 3, (unsigned long long)n_step);
+  }
+  if (out >= 0) {
+    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
+    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
+    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
     for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
     if (a.per_query) {
       a.per_query[3 * out] = c_dir;
@@ -523,7 +745,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    V4<R>* o = a.part + (size_t)per * out;
+    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
+    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
     for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
     if (a.per_query) {
       a.per_query[3 * out] = c_dir;
@@ -546,6 +769,12 @@ __global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
   }
 }
 
+// GS_BH_KERNEL: 1 (default) = independent walks (k_bh_ws), 3 = group walk
+// (k_bh_grp), 4 = split launch (group walk for warps whose query box is small
+// against the threshold, independent walks for the rest), 0 = warp-synchronous
+// min-node walk, 2 = pipelined independent walks. Measured (B200, FP32): the
+// group walk wins on config 3 (tube, sigma 5: 3.8 vs 4.6 ms per RHS) and loses
+// on configs 2, 4 and 5, so independent walks are the default.
 static int bh_kernel_choice() {
   static int v = [] {
     const char* e = std::getenv("GS_BH_KERNEL");
@@ -554,14 +783,47 @@ static int bh_kernel_choice() {
   return v;
 }
 
+// A warp walks as a group when its query box diagonal is <= ratio * thr.
+static double bh_group_ratio() {
+  static double v = [] {
+    const char* e = std::getenv("GS_BH_GRP_RATIO");
+    return e ? std::atof(e) : 0.25;
+  }();
+  return v;
+}
+
 template <typename R>
-int launch(int mode, const BhArgs<R>& a, cudaStream_t st) {
-  const int nb = std::max(1, (a.nq + kBhNT - 1) / kBhNT);
-  if (bh_kernel_choice() == 2) {
+int launch(int mode, BhArgs<R> a, cudaStream_t st) {
+  const int kind = bh_kernel_choice();
+  if (kind == 0 || kind == 2) a.ntask = 1;  // single-window kernels
+  const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
+  static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
+  static unsigned long long* dbuf = nullptr;
+  if (dbg && !dbuf) cudaMalloc(&dbuf, 64);
+  if (dbg) {
+    cudaMemsetAsync(dbuf, 0, 64, st);
+    a.dbg = dbuf;
+  }
+  if (kind == 3 || kind == 4) {
+    a.split = kind == 4;
+    if (mode == kBhRhs) k_bh_grp<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
+    else if (mode == kBhHess) k_bh_grp<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
+    else k_bh_grp<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+    GS_CUDA_OK(cudaGetLastError());
+    if (dbg) {
+      unsigned long long h[4];
+      cudaMemcpyAsync(h, dbuf, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "[bh grp mode %d nq %d] warps %llu iters %llu segs %llu steps %llu\n", mode,
+                   a.nq, h[0], h[1], h[2], h[3]);
+    }
+    if (kind == 3) return GS_OK;
+  }
+  if (kind == 2) {
     if (mode == kBhRhs) k_bh_pipe<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
     else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
     else k_bh_pipe<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
-  } else if (bh_kernel_choice() == 1) {
+  } else if (kind == 1 || kind == 4) {
     if (mode == kBhRhs) k_bh_ws<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
     else if (mode == kBhHess) k_bh_ws<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
     else k_bh_ws<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
@@ -612,10 +874,16 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
     a.c1 = (R)kc.inv_s;
   }
   a.thr2_in = (R)(thr < INFINITY ? thr * thr * (1.0 - 1e-5) : INFINITY);
+  {
+    const double g = bh_group_ratio() * thr;
+    a.grp_lim2 = (R)(g < 1e150 ? g * g : INFINITY);
+  }
+  a.split = 0;
   a.inv_two_s = (R)kc.inv_two_s;
   a.part = static_cast<V4<R>*>(q.part);
   a.per_query = q.per_query;
   a.totals = q.totals;
+  a.ntask = q.per_query ? 1 : std::max(1, q.ntask);  // per-query counts: one window
   (void)sigma;
   return a;
 }
@@ -626,6 +894,22 @@ int bh_traverse(const Device&, int prec, DevTree& t, double sigma, double thr, c
                 cudaStream_t st) {
   if (prec == kF32) return launch<float>(q.mode, make_args<float>(t, sigma, thr, q), st);
   return launch<double>(q.mode, make_args<double>(t, sigma, thr, q), st);
+}
+
+// Node windows per query: a latency-bound walk needs many resident warps, and
+// with few queries (configs 2, 3, 5: 20k-50k points = 600-1600 warps) one warp
+// per 32 queries leaves the SMs mostly idle. Splitting the pre-order node
+// array into K windows (each block walks its queries through one window;
+// the epilogue folds the K partials in fixed order) multiplies the warps by K.
+int bh_tasks(int64_t nq) {
+  static const int forced = [] {
+    const char* e = std::getenv("GS_BH_TASKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return std::min(forced, kMaxChunks);
+  const int64_t warps = (nq + 31) / 32;
+  const int64_t want = 148 * 64;  // ~2 waves of 32 resident warps per SM
+  return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, (want + warps - 1) / warps));
 }
 
 int bh_keep_trees(BhWork& w, int T) {
@@ -645,10 +929,12 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   kt_mark(1, st);
   GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st, nullptr, e.bad_step ? e.bad_step + 1 : nullptr));
   kt_mark(1, st);
-  GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+  const int K = bh_tasks(nt);
+  GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * K * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
   q.mode = kBhRhs;
+  q.ntask = K;
   q.tgt_begin = (int)tb;
   q.n_tgt = (int)nt;
   q.part = w.part.ptr;
@@ -657,7 +943,7 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   kt_mark(0, st);
   GS_TRY_INT(bh_traverse(dev, prec, t, cfg.sigma, thr, q, st));
   kt_mark(0, st);
-  e.S = 1;
+  e.S = K;
   e.parts_per_tgt = 2;
   e.part = w.part.ptr;
   e.n_tgt = (int)nt;
@@ -680,16 +966,18 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
     GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, *t, st));
   }
   GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
-  GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * n));
+  const int K = bh_tasks(n);
+  GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * K * n));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
   q.mode = kBhHess;
+  q.ntask = K;
   q.tgt_begin = 0;
   q.n_tgt = (int)n;
   q.part = w.part.ptr;
   q.totals = w.stats.as<unsigned long long>();
   GS_TRY_INT(bh_traverse(dev, prec, *t, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));
-  e.S = 1;
+  e.S = K;
   e.part = w.part.ptr;
   GS_TRY_INT(bwd_epilogue(prec, e, st));
   return GS_OK;
@@ -699,14 +987,16 @@ int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const 
                      const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
                      cudaStream_t st) {
   GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, w.cur, st));
-  GS_TRY_INT(w.part.ensure(vec_bytes(prec) * m));
+  const int K = bh_tasks(m);
+  GS_TRY_INT(w.part.ensure(vec_bytes(prec) * K * m));
   BhQuery q;
   q.mode = kBhVel;
+  q.ntask = K;
   q.ev = ev;
   q.m = (int)m;
   q.part = w.part.ptr;
   GS_TRY_INT(bh_traverse(dev, prec, w.cur, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));
-  e.S = 1;
+  e.S = K;
   e.part = w.part.ptr;
   GS_TRY_INT(vel_epilogue(prec, e, st));
   return GS_OK;

@@ -57,12 +57,14 @@ struct KTimer {
   }
   // sum of (end - start) over the recorded pairs; resets
   double drain(int ch, int64_t* pairs) {
+    static const bool verbose = std::getenv("GS_KT_VERBOSE") != nullptr;
     double ms = 0.0;
     for (size_t k = 0; k + 1 < used[ch]; k += 2) {
       float v = 0.f;
       cudaEventSynchronize(ev[ch][k + 1]);
       cudaEventElapsedTime(&v, ev[ch][k], ev[ch][k + 1]);
       ms += v;
+      if (verbose) std::fprintf(stderr, "[kt] ch %d pair %zu: %.3f ms\n", ch, k / 2, v);
     }
     if (pairs) *pairs = (int64_t)(used[ch] / 2);
     used[ch] = 0;
