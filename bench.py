@@ -34,6 +34,8 @@ sys.path.insert(0, ROOT)
 SIGMA = 0.0131
 T_STEPS = 10
 METRIC = "flow steps/s (RK4, 4 RHS/step) & G pair-interactions/s, config 4"
+# Algorithmic DRAM bytes per point of one FP32 tree build (DESIGN.md §4 table)
+BUILD_BYTES_PER_POINT = 1014
 
 
 def workload(n: int, seed: int = 2024):
@@ -270,26 +272,96 @@ def run_ours(args):
         fb = gs.flow(cfg_bh, N)
         fb.upload(q0, p0)
         sb = torch.cuda.ExternalStream(fb.stream())
-        fb.advance(1)
+        fb.advance(max(1, args.warmup))
         fb.sync()
+        # time the first kb steps of the config-4 flow itself (the point
+        # distribution, hence the traversal work, evolves along the flow)
+        fb.upload(q0, p0)
+        fb.sync()
+        st0 = fb.stats()
         fb.profile(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kb = max(1, args.steps)
+        with torch.cuda.stream(sb):
+            flush.zero_()
         e0.record(sb)
         fb.advance(kb)
         e1.record(sb)
         torch.cuda.synchronize()
         fb.sync()
         bms = e0.elapsed_time(e1)
-        bp = fb.profile_read()
-        _, _, _, st = gs.shoot_forward(q0[:2], p0[:2], cfg_bh, keep_trajectory=False)  # warm API
+        ph = fb.profile_phases(6)
+        st1 = fb.stats()
+        fb.profile(False)
+        rhs = 4 * kb
+        d = st1["direct_interactions"] - st0["direct_interactions"]
+        a_ = st1["approximated_interactions"] - st0["approximated_interactions"]
+        v = st1["nodes_visited"] - st0["nodes_visited"]
+        trav_s = ph["kernel"]["ms"] / 1e3
+        build_ms = ph["build"]["ms"] / max(1, ph["build"]["count"])
+        lane_peak = ffma.value  # lane FFMA/s (live microbenchmark)
         line["bh"] = {
             "value": kb / (bms / 1e3), "unit": "flow steps/s", "ms_per_step": bms / kb,
             "n2_equivalent_pairs_per_s": 4.0 * N * float(N) * kb / (bms / 1e3),
-            "traversal_ms_per_rhs": bp["kernel_ms"] / max(1, bp["kernel_launches"]),
-            "tree_build_ms_per_rhs": bp["build_ms"] / max(1, bp["builds"]),
+            "interactions_per_s": (d + a_) / (bms / 1e3),
+            "per_query_per_rhs": {"direct": d / (rhs * N), "approximated": a_ / (rhs * N),
+                                  "visited": v / (rhs * N)},
+            "traversal_ms_per_rhs": ph["kernel"]["ms"] / max(1, ph["kernel"]["count"]),
+            "tree_build_ms_per_rhs": build_ms,
+            "build_phases_ms_per_rhs": {k: ph[k]["ms"] / max(1, ph[k]["count"])
+                                        for k in ("bbox_keys", "sort", "topology", "aggregate")},
+            # 16 FP32 per interaction + 12 per visited node
+            "traversal_fp32_issue_frac": ((16.0 * (d + a_) + 12.0 * v) / trav_s) / lane_peak
+            if trav_s > 0 else None,
+            # algorithmic bytes of the build kernels, FP32 (per point)
+            "build_gbs_algorithmic": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9,
+            "build_hbm_frac": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9
+            / float(mp.get("hbm_gbs", 6550.0)),
+            "kernel": "k_bh_ws<float> (independent walks); tree: radix sort + LCP topology",
         }
         del fb
+
+    # ---- exact FP64 and N = 100k FP32 lines (same workload family) -------------
+    if not args.no_extra and world == 1:
+        def timed_flow(n, prec, integ, steps):
+            qq, pp = workload(n)
+            c = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=EXACT, integrator=integ,
+                               precision=prec)
+            fl = gs.flow(c, n)
+            fl.upload(qq, pp)
+            s_ = torch.cuda.ExternalStream(fl.stream())
+            fl.advance(1)
+            fl.sync()
+            fl.profile(True)
+            t0_, t1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0_.record(s_)
+            fl.advance(steps)
+            t1_.record(s_)
+            torch.cuda.synchronize()
+            fl.sync()
+            pr = fl.profile_read()
+            return t0_.elapsed_time(t1_), pr
+        from paper_1907_04834_b200 import EULER, F64
+        n64 = 200_000
+        ms64, pr64 = timed_flow(n64, F64, EULER, 2)
+        dfma = C.c_double()
+        lib.gs_microbench(local, 2, C.byref(dfma))
+        k64 = pr64["kernel_ms"] / max(1, pr64["kernel_launches"])
+        pps64 = float(n64) * n64 / (k64 * 1e-3)
+        line["fp64"] = {
+            "workload": f"exact FP64 RHS, N={n64}, Euler (config-4 distribution)",
+            "pair_interactions_per_s": pps64, "kernel_ms": k64,
+            "steps_per_s": 2 / (ms64 / 1e3),
+            "peak_dfma_lane_per_s": dfma.value,
+            "frac_16dp_basis": pps64 * 16.0 / dfma.value if dfma.value else None,
+            "frac_34dp_basis_incl_exp": pps64 * 34.0 / dfma.value if dfma.value else None,
+        }
+        ms1, pr1 = timed_flow(100_000, F32, RK4, 3)
+        line["n100k"] = {
+            "value": 3 / (ms1 / 1e3), "unit": "flow steps/s (RK4)",
+            "pair_interactions_per_s": 4.0 * 1e10 * 3 / (ms1 / 1e3),
+            "frac_of_ffma_peak": (4.0 * 1e10 * 3 / (ms1 / 1e3)) / peak / 1e9,
+        }
 
     # ---- end to end through the public C-ABI call, host buffers ----------------
     if world == 1:
@@ -328,6 +400,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--cpu-sample", type=int, default=8192)
+    ap.add_argument("--no-extra", action="store_true", help="skip the FP64 / N=100k lines")
     ap.add_argument("--no-bh", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -230,6 +230,10 @@ gs_status gs_flow_download(gs_flow* flow, double* q, double* p);
 int64_t gs_flow_last_launches(const gs_flow* flow);
 /* cudaStream_t of the flow (as void*), for event timing on the launch stream. */
 void* gs_flow_stream(const gs_flow* flow);
+/* Work counters accumulated since the last upload (TraversalStats,
+ * bh_kernel.hpp:28-38): direct / approximated interactions and visited nodes
+ * (Barnes-Hut, counted on the device) or ordered pairs (exact). Synchronises. */
+gs_status gs_flow_stats(gs_flow* flow, gs_stats* out);
 
 /* Event timing of the dominant kernels of subsequent advances / stages
  * (the all-pairs RHS kernel or the Barnes-Hut traversal; and the tree build),

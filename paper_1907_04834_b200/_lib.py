@@ -130,6 +130,7 @@ SIGNATURES = [
     ("gs_flow_sync", _st, [_vp]),
     ("gs_flow_download", _st, [_vp, _d, _d]),
     ("gs_flow_last_launches", _i64, [_vp]),
+    ("gs_flow_stats", _st, [_vp, C.POINTER(gs_stats)]),
     ("gs_flow_stream", _vp, [_vp]),
     ("gs_flow_profile", _st, [_vp, C.c_int32]),
     ("gs_flow_profile_read", _st, [_vp, _d, C.POINTER(_i64), _d, C.POINTER(_i64)]),

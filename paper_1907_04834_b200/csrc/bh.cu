@@ -352,7 +352,7 @@ constexpr int ws_min_blocks() {
 }
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT, ws_min_blocks<R, MODE>()) k_bh_ws(const BhArgs<R> a) {
+__global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE>())) k_bh_ws(const BhArgs<R> a) {
   const int qi = blockIdx.x * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;

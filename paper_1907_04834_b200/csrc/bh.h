@@ -39,7 +39,7 @@ struct DevTree {
   DBuf asum, bsum;      // double4
   DBuf root;            // double[6] padded root box
   // radix-sort scratch
-  DBuf tmp_k, tmp_v, hist;
+  DBuf tmp_k, tmp_v, tmp_v2, hist;
   DBuf scan_tmp;
   DBuf scal;
   KernelConsts kc{};

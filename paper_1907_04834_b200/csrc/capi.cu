@@ -583,6 +583,13 @@ gs_status gs_flow_profile_phases(gs_flow* f, double* ms, int64_t* counts, int32_
   return GS_OK;
 }
 
+gs_status gs_flow_stats(gs_flow* f, gs_stats* out) {
+  if (!f || !out) return bad_arg("null argument");
+  *out = f->stats;
+  GS_TRY(flow_bh_stats(f, out));
+  return GS_OK;
+}
+
 gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
   if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
   f->shard_begin = begin;

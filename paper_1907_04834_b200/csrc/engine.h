@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -46,13 +47,17 @@ struct DBuf {
 struct KTimer {
   static constexpr int kChannels = 8;
   std::vector<cudaEvent_t> ev[kChannels];
+  std::vector<double> host_us[kChannels];  // GS_KT_VERBOSE: host clock at each mark
   size_t used[kChannels] = {0, 0, 0, 0, 0, 0, 0, 0};
   void mark(int ch, cudaStream_t st) {
     if (used[ch] == ev[ch].size()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
       ev[ch].push_back(e);
+      host_us[ch].push_back(0.0);
     }
+    host_us[ch][used[ch]] = (double)std::chrono::duration_cast<std::chrono::microseconds>(
+        std::chrono::steady_clock::now().time_since_epoch()).count();
     cudaEventRecord(ev[ch][used[ch]++], st);
   }
   // sum of (end - start) over the recorded pairs; resets
@@ -64,7 +69,10 @@ struct KTimer {
       cudaEventSynchronize(ev[ch][k + 1]);
       cudaEventElapsedTime(&v, ev[ch][k], ev[ch][k + 1]);
       ms += v;
-      if (verbose) std::fprintf(stderr, "[kt] ch %d pair %zu: %.3f ms\n", ch, k / 2, v);
+      if (verbose)
+        std::fprintf(stderr, "[kt] ch %d pair %zu: %.3f ms (host %.3f ms, host t %.3f ms)\n", ch,
+                     k / 2, v, (host_us[ch][k + 1] - host_us[ch][k]) / 1e3,
+                     std::fmod(host_us[ch][k] / 1e3, 1e5));
     }
     if (pairs) *pairs = (int64_t)(used[ch] / 2);
     used[ch] = 0;

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
 // Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo.
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
-                                              uint64_t* kh, uint64_t* kl, int* idx) {
+                                              uint64_t* kh, uint64_t* kl) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= n) return;
   const V4<R> q = ld4(rec + 2 * i);
@@ -122,7 +122,6 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
   }
   kh[i] = h;
   kl[i] = l;
-  idx[i] = (int)i;
 }
 
 // ------------------------------------------------------------ radix sort ---
@@ -146,36 +145,25 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t* keys, int64_t
   ghist[(int64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];  // tile-major
 }
 
-// ghist[tile][digit] -> exclusive prefix over tiles per digit; row ntiles holds
-// the exclusive prefix over digit totals (the digit's base offset).
+// ghist[tile][digit] -> exclusive prefix over tiles per digit, one warp per
+// digit (256 warps); row ntiles receives the digit totals (the scatter forms
+// the digit base offsets from them).
 __global__ void __launch_bounds__(256) k_rs_digit_scan(unsigned* ghist, int ntiles) {
-  __shared__ unsigned tot[256];
-  const int d = threadIdx.x;
+  const int d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   unsigned run = 0;
-  int t = 0;
-  for (; t + 4 <= ntiles; t += 4) {
-    const unsigned a = ghist[(int64_t)t * 256 + d], b = ghist[(int64_t)(t + 1) * 256 + d],
-                   c = ghist[(int64_t)(t + 2) * 256 + d], e = ghist[(int64_t)(t + 3) * 256 + d];
-    ghist[(int64_t)t * 256 + d] = run;
-    ghist[(int64_t)(t + 1) * 256 + d] = run + a;
-    ghist[(int64_t)(t + 2) * 256 + d] = run + a + b;
-    ghist[(int64_t)(t + 3) * 256 + d] = run + a + b + c;
-    run += a + b + c + e;
+  for (int t0 = 0; t0 < ntiles; t0 += 32) {
+    const int t = t0 + lane;
+    const unsigned v = t < ntiles ? ghist[(int64_t)t * 256 + d] : 0u;
+    unsigned x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (t < ntiles) ghist[(int64_t)t * 256 + d] = run + x - v;
+    run += __shfl_sync(0xffffffffu, x, 31);
   }
-  for (; t < ntiles; ++t) {
-    const unsigned a = ghist[(int64_t)t * 256 + d];
-    ghist[(int64_t)t * 256 + d] = run;
-    run += a;
-  }
-  tot[d] = run;
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const unsigned v = d >= o ? tot[d - o] : 0u;
-    __syncthreads();
-    tot[d] += v;
-    __syncthreads();
-  }
-  ghist[(int64_t)ntiles * 256 + d] = tot[d] - run;
+  if (lane == 0) ghist[(int64_t)ntiles * 256 + d] = run;
 }
 
 // exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
@@ -218,7 +206,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
     const int64_t i = seg + r * 32 + lane;
     const bool ok = i < n;
     key[r] = ok ? kin[i] : 0ull;
-    val[r] = ok ? vin[i] : 0;
+    val[r] = ok ? (vin ? vin[i] : (int)i) : 0;  // first pass: values are the indices
     const unsigned d = (unsigned)(key[r] >> shift) & 255u;
     const unsigned act = __ballot_sync(0xffffffffu, ok);
     loc[r] = 0;
@@ -233,10 +221,19 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
     }
     __syncwarp();
   }
+  // digit base offsets: exclusive prefix of the digit totals (row ntiles)
+  __shared__ unsigned base[256];
+  base[threadIdx.x] = ghist[(int64_t)ntiles * 256 + threadIdx.x];
   __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const unsigned v = threadIdx.x >= o ? base[threadIdx.x - o] : 0u;
+    __syncthreads();
+    base[threadIdx.x] += v;
+    __syncthreads();
+  }
   {
     const unsigned d = threadIdx.x;
-    unsigned run = ghist[(int64_t)blockIdx.x * 256 + d] + ghist[(int64_t)ntiles * 256 + d];
+    unsigned run = ghist[(int64_t)blockIdx.x * 256 + d] + base[d] - ghist[(int64_t)ntiles * 256 + d];
     for (int w = 0; w < kRsNT / 32; ++w) {
       const unsigned t = wh[w][d];
       wh[w][d] = run;
@@ -256,25 +253,10 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
   }
 }
 
-// Points whose 63-bit keys tie: order the (rare, short) run by the deeper
-// digits, then by index (bucket members are equivalent; ascending index).
-__global__ void k_fix_ties(const uint64_t* skh, int* perm, const uint64_t* kl, int64_t n) {
+// out[t] = key[perm[t]]
+__global__ void k_gather_u64(const int* perm, const uint64_t* key, uint64_t* out, int64_t n) {
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (t >= n) return;
-  if (t > 0 && skh[t] == skh[t - 1]) return;
-  int64_t e = t;
-  while (e + 1 < n && skh[e + 1] == skh[t]) ++e;
-  if (e == t) return;
-  for (int64_t a = t + 1; a <= e; ++a) {
-    const int v = perm[a];
-    const uint64_t kv = kl[v];
-    int64_t b = a - 1;
-    while (b >= t && (kl[perm[b]] > kv || (kl[perm[b]] == kv && perm[b] > v))) {
-      perm[b + 1] = perm[b];
-      --b;
-    }
-    perm[b + 1] = v;
-  }
+  if (t < n) out[t] = key[perm[t]];
 }
 
 // ------------------------------------------------------------- topology ---
@@ -654,31 +636,50 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // 2. keys
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), t.tmp_v.as<int>());
+    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
   else
-    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), t.tmp_v.as<int>());
+    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
-  // 3. stable radix sort of key_hi (values: point index), 8 passes of 8 bits
-  GS_CUDA_OK(cudaMemcpyAsync(t.skey_hi.ptr, t.key_hi.ptr, 8 * n, cudaMemcpyDeviceToDevice, st));
-  GS_CUDA_OK(cudaMemcpyAsync(t.perm.ptr, t.tmp_v.ptr, 4 * n, cudaMemcpyDeviceToDevice, st));
+  // 3. stable LSD radix sort by (key_hi, key_lo, index): 5 passes over the 33
+  // significant bits of key_lo, then the keys' key_hi in that order, then 8
+  // passes over key_hi; 8-bit digits, no copies (buffers ping-pong):
+  //   lo: (key_lo, index) -> (tmp_k, tmp_v) -> (skey_lo, tmp_v2) -> ... -> (tmp_k, tmp_v)
+  //   hi: (skey_lo := key_hi[tmp_v], tmp_v) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
+  // Ties in all 32 levels (depth-32 buckets) keep ascending index.
   const int ntiles = nblocks(n, kRsTile);
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
-  uint64_t* ka = t.skey_hi.as<uint64_t>();
-  uint64_t* kb = t.tmp_k.as<uint64_t>();
-  int* va = t.perm.as<int>();
-  int* vb2 = t.tmp_v.as<int>();
-  for (int shift = 0; shift < 64; shift += 8) {
-    k_rs_hist<<<ntiles, kRsNT, 0, st>>>(ka, n, shift, t.hist.as<unsigned>(), ntiles);
-    k_rs_digit_scan<<<1, 256, 0, st>>>(t.hist.as<unsigned>(), ntiles);
-    k_rs_scatter<<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, shift, t.hist.as<unsigned>(), ntiles);
-    std::swap(ka, kb);
-    std::swap(va, vb2);
+  GS_TRY_INT(t.tmp_v2.ensure(4 * n));
+  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift) {
+    k_rs_hist<<<ntiles, kRsNT, 0, st>>>(ki, n, shift, t.hist.as<unsigned>(), ntiles);
+    k_rs_digit_scan<<<32, 256, 0, st>>>(t.hist.as<unsigned>(), ntiles);
+    k_rs_scatter<<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, t.hist.as<unsigned>(), ntiles);
+  };
+  {
+    const uint64_t* ka = t.key_lo.as<uint64_t>();
+    const int* va = nullptr;  // implicit: the index
+    for (int p = 0; p < 5; ++p) {
+      uint64_t* kb = (p & 1) ? t.skey_lo.as<uint64_t>() : t.tmp_k.as<uint64_t>();
+      int* vb = (p & 1) ? t.tmp_v2.as<int>() : t.tmp_v.as<int>();
+      pass(ka, va, kb, vb, 8 * p);
+      ka = kb;
+      va = vb;
+    }
   }
-  // 8 passes: result back in skey_hi / perm
+  k_gather_u64<<<nb, kNT, 0, st>>>(t.tmp_v.as<int>(), t.key_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
+  {
+    const uint64_t* ka = t.skey_lo.as<uint64_t>();
+    const int* va = t.tmp_v.as<int>();
+    for (int p = 0; p < 8; ++p) {
+      uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
+      int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
+      pass(ka, va, kb, vb, 8 * p);
+      ka = kb;
+      va = vb;
+    }
+  }
   GS_CUDA_OK(cudaGetLastError());
-  k_fix_ties<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.perm.as<int>(), t.key_lo.as<uint64_t>(), n);
   k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
   kt_mark(3, st);
   kt_mark(4, st);

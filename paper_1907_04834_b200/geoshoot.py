@@ -511,6 +511,11 @@ class Flow:
     def last_launches(self) -> int:
         return self.gs.lib.gs_flow_last_launches(self.h)
 
+    def stats(self) -> dict:
+        st = L.gs_stats()
+        self.gs.check(self.gs.lib.gs_flow_stats(self.h, C.byref(st)))
+        return st.as_dict()
+
     def stream(self) -> int:
         return self.gs.lib.gs_flow_stream(self.h) or 0
 
