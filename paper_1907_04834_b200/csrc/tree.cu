@@ -128,14 +128,15 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
 // Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, 3 kernels per
 // pass: per-tile digit histograms, one exclusive scan (digit-major), and a
 // stable scatter that ranks keys inside a tile with warp match/popc.
-constexpr int kRsNT = 256, kRsIPT = 16, kRsTile = kRsNT * kRsIPT;
+constexpr int kRsNT = 256;  // items per thread (tile = 256 * IPT keys): template parameter
 
+template <int kRsIPT>
 __global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t* keys, int64_t n, int shift,
                                                   unsigned* ghist, int ntiles) {
   __shared__ unsigned h[256];
   h[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kRsTile;
+  const int64_t base = (int64_t)blockIdx.x * (kRsNT * kRsIPT);
 #pragma unroll 4
   for (int r = 0; r < kRsIPT; ++r) {
     const int64_t i = base + r * kRsNT + threadIdx.x;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
   }
 }
 
+template <int kRsIPT>
 __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const int* vin,
                                                      uint64_t* kout, int* vout, int64_t n,
                                                      int shift, const unsigned* ghist,
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
   __syncthreads();
-  const int64_t seg = (int64_t)blockIdx.x * kRsTile + (int64_t)warp * (32 * kRsIPT);
+  const int64_t seg = (int64_t)blockIdx.x * (kRsNT * kRsIPT) + (int64_t)warp * (32 * kRsIPT);
   uint64_t key[kRsIPT];
   int val[kRsIPT];
   unsigned loc[kRsIPT];
@@ -648,13 +650,26 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   //   lo: (key_lo, index) -> (tmp_k, tmp_v) -> (skey_lo, tmp_v2) -> ... -> (tmp_k, tmp_v)
   //   hi: (skey_lo := key_hi[tmp_v], tmp_v) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
   // Ties in all 32 levels (depth-32 buckets) keep ascending index.
-  const int ntiles = nblocks(n, kRsTile);
+  // keys per thread: small tiles (more CTAs) for small n, 8 from ~0.5M points
+  // (measured sort per build: 50k 0.22 ms at 4 vs 0.28 at 8; 1M 0.48 at 8 vs 0.52 at 4)
+  static const int ipt_env = [] {
+    const char* e = std::getenv("GS_RS_IPT");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 4 || v == 8 || v == 16) ? v : 0;
+  }();
+  const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
+  const int ntiles = nblocks(n, kRsNT * ipt);
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
   auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift) {
-    k_rs_hist<<<ntiles, kRsNT, 0, st>>>(ki, n, shift, t.hist.as<unsigned>(), ntiles);
-    k_rs_digit_scan<<<32, 256, 0, st>>>(t.hist.as<unsigned>(), ntiles);
-    k_rs_scatter<<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, t.hist.as<unsigned>(), ntiles);
+    unsigned* gh = t.hist.as<unsigned>();
+    if (ipt == 16) k_rs_hist<16><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
+    else if (ipt == 8) k_rs_hist<8><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
+    else k_rs_hist<4><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
+    k_rs_digit_scan<<<32, 256, 0, st>>>(gh, ntiles);
+    if (ipt == 16) k_rs_scatter<16><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
+    else if (ipt == 8) k_rs_scatter<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
+    else k_rs_scatter<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
   };
   {
     const uint64_t* ka = t.key_lo.as<uint64_t>();

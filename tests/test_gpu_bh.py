@@ -51,6 +51,11 @@ SETS = {
                        sym_uniform(400, 1.0, 5)),
     "duplicates": lambda: (np.concatenate([np.full((10, 3), 0.5), uniform(990, 2.0, 6)]),
                            sym_uniform(1000, 1.0, 7)),
+    # a dense cluster far below the root cell's resolution: long runs of equal
+    # 63-bit keys resolved by the deeper digits, plus depth-32 buckets
+    "cluster": lambda: (np.concatenate([uniform(3000, 1e-7, 8), np.array([[-1e3, -1e3, -1e3],
+                                                                          [1e3, 1e3, 1e3]])]),
+                        sym_uniform(3002, 1.0, 9)),
     "corners": lambda: (np.array([[1.0 if i & 1 else -1.0, 1.0 if i & 2 else -1.0,
                                    1.0 if i & 4 else -1.0] for i in range(8)]), np.zeros((8, 3))),
 }
