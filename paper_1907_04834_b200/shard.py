@@ -14,6 +14,46 @@ import torch
 import torch.distributed as dist
 
 
+def subject_range(count: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of independent subjects for a rank (any count: the
+    first count % world ranks take one extra)."""
+    base, extra = divmod(count, world)
+    begin = rank * base + min(rank, extra)
+    return begin, base + (1 if rank < extra else 0)
+
+
+def register_subjects(gs, templates, targets, cfg, group=None, runner=None, **opt):
+    """Config 5 across GPUs (SURVEY.md §8e "batched subjects"): independent
+    registrations, no data-path collective. Rank r optimises its contiguous
+    block of subjects concurrently on its own GPU (``Geoshoot.optimize_batch``:
+    one stream + host thread per subject) and the per-subject results are
+    gathered to every rank once at the end (``all_gather_object``: O(subjects)
+    small host objects plus the p0 arrays). Results are bitwise the ones a
+    single GPU computes for the same subjects.
+
+    ``runner(templates, targets, cfg, **opt)`` defaults to ``gs.optimize_batch``
+    (tests substitute a CPU stand-in). Returns the list of per-subject dicts
+    {"subject", "p0", "reason", "iterations", "evaluations", "final_total"} in
+    subject order.
+    """
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    b, c = subject_range(len(templates), rank, world)
+    run = runner if runner is not None else gs.optimize_batch
+    mine = []
+    if c:
+        r = run(templates[b:b + c], targets[b:b + c], cfg, **opt)
+        for k in range(c):
+            mine.append({"subject": b + k, "p0": r["p0"][k], "reason": r["reasons"][k],
+                         "iterations": r["iterations"][k], "evaluations": r["evaluations"][k],
+                         "final_total": float(r["final_total"][k])})
+    if world == 1:
+        return mine
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    return [x for part in parts for x in part]
+
+
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Equal contiguous shards (n must be divisible by world)."""
     if n % world:

@@ -61,3 +61,18 @@ def test_optimize_batch_equals_single(gs, ref):
         one = gs.optimize(q, t, cfg, max_iterations=8)
         assert np.array_equal(out["p0"][k], one["p0"])  # bitwise: deterministic kernels
         assert out["iterations"][k] == one["iterations"]
+
+
+def test_register_subjects_single_rank(gs, ref):
+    """shard.register_subjects (config 5 across GPUs) on one rank: the rank's
+    block is every subject, results equal optimize_batch's."""
+    from paper_1907_04834_b200.shard import register_subjects
+    qs = [ref.generate(3, 60 + 5 * k, 60.0, 4.0) for k in range(3)]
+    ts = [ref.generate(4, 60 + 5 * k, 60.0, 4.0, 0.2) for k in range(3)]
+    cfg = ShootingConfig(sigma=4.0, lambda_=1.0, timesteps=4, backend=BARNES_HUT, precision=F32)
+    res = register_subjects(gs, qs, ts, cfg, max_iterations=4)
+    out = gs.optimize_batch(qs, ts, cfg, max_iterations=4)
+    assert [r["subject"] for r in res] == [0, 1, 2]
+    for k, r in enumerate(res):
+        assert np.array_equal(r["p0"], out["p0"][k])
+        assert r["iterations"] == out["iterations"][k]

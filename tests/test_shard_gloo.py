@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1907_04834_b200.shard import ShardedFlow, shard_range
+from paper_1907_04834_b200.shard import ShardedFlow, register_subjects, shard_range, subject_range
 
 
 class CpuFlow:
@@ -86,3 +86,57 @@ def test_two_rank_gloo_matches_single_rank(tmp_path):
     for r in range(2):
         assert np.array_equal(np.load(tmp_path / f"q{r}.npy"), wq)
         assert np.array_equal(np.load(tmp_path / f"p{r}.npy"), wp)
+
+
+def fake_batch(templates, targets, cfg, **opt):
+    """CPU stand-in for Geoshoot.optimize_batch: a deterministic per-subject result."""
+    return {"p0": [0.5 * (t - q) for q, t in zip(templates, targets)],
+            "reasons": [1] * len(templates), "iterations": [len(q) for q in templates],
+            "evaluations": [len(q) + 1 for q in templates],
+            "final_total": np.array([float(np.abs(t - q).sum()) for q, t in zip(templates, targets)])}
+
+
+def subjects():
+    rng = np.random.default_rng(11)
+    qs = [rng.uniform(0, 1, (5 + k, 3)) for k in range(7)]
+    ts = [q + 0.1 * (k + 1) for k, q in enumerate(qs)]
+    return qs, ts
+
+
+def subject_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    qs, ts = subjects()
+    seen = []
+
+    def runner(a, b, cfg, **opt):
+        seen.append(len(a))
+        return fake_batch(a, b, cfg, **opt)
+
+    res = register_subjects(None, qs, ts, cfg=None, runner=runner, max_iterations=3)
+    assert seen == [subject_range(7, rank, world)[1]]
+    np.save(os.path.join(out, f"s{rank}.npy"),
+            np.concatenate([np.concatenate([[r["subject"], r["iterations"], r["final_total"]],
+                                            r["p0"].ravel()]) for r in res]))
+    dist.destroy_process_group()
+
+
+def test_subject_ranges_cover_all():
+    for count in (0, 1, 7, 64):
+        for world in (1, 2, 3, 8):
+            spans = [subject_range(count, r, world) for r in range(world)]
+            assert sum(c for _, c in spans) == count
+            assert all(spans[r][0] + spans[r][1] == spans[r + 1][0] for r in range(world - 1))
+
+
+def test_two_rank_subjects_match_single_rank(tmp_path):
+    port = 29600 + os.getpid() % 1000
+    mp.spawn(subject_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    qs, ts = subjects()
+    want = register_subjects(None, qs, ts, cfg=None, runner=fake_batch)
+    flat = np.concatenate([np.concatenate([[r["subject"], r["iterations"], r["final_total"]],
+                                           r["p0"].ravel()]) for r in want])
+    assert [r["subject"] for r in want] == list(range(7))
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"s{r}.npy"), flat)
