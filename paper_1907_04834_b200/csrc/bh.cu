@@ -44,6 +44,16 @@ double gate_t2(double thr) {
 namespace {
 
 constexpr int kBhNT = 128;
+#ifndef GS_BH_WS_NOWIN_MINB
+#define GS_BH_WS_NOWIN_MINB 7
+#endif
+#ifndef GS_BH_WS_WIN_MINB
+#define GS_BH_WS_WIN_MINB 8
+#endif
+#ifndef GS_BH_WS_HESS_MINB
+#define GS_BH_WS_HESS_MINB 5
+#endif
+
 
 template <typename R>
 struct BhArgs {
@@ -54,7 +64,7 @@ struct BhArgs {
   const V4<R>* mom;
   const V4<R>* nadj_a;
   const V4<R>* nadj_b;
-  const V4<R>* nrec;  // [m][2] compact node records {lo, code} {hi, begin}
+  const V4<R>* nrec;  // [m][4] node records {lo, code} {hi, begin} {centroid} {momentum}
   const V4<R>* srec;  // [n][2] interaction coords (scaled FP32), p
   const V4<R>* squ;   // [n] unscaled q
   const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
@@ -70,6 +80,7 @@ struct BhArgs {
   R grp_lim2;          // warps whose query box has diagonal^2 <= this walk as a group
   int split;           // 1: k_bh_grp takes the group warps, k_bh_ws the others
   int ntask;           // pre-order node windows per query (blockIdx.y); partials [task][query]
+  int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
   uint32_t* per_query;
@@ -100,6 +111,17 @@ __device__ __forceinline__ bool gate(const float4& l, const float4& h, const flo
 __device__ __forceinline__ bool gate(const double4& l, const double4& h, const double4& x,
                                      const BhArgs<double>& a) {
   return gate_exact(l.x, l.y, l.z, h.x, h.y, h.z, x.x, x.y, x.z, a.T2);
+}
+
+// Non-binding L1 prefetch (no register): the skip target's record is needed
+// next whenever the node is not opened, and is usually not in L1 yet.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ bool lane_is_first_parked(bool here) {
+  const unsigned b = __ballot_sync(0xffffffffu, here);
+  return here && (threadIdx.x & 31) == __ffs(b) - 1;
 }
 
 template <typename R>
@@ -346,13 +368,17 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
 // iteration whatever node each lane is at. Same per-query node set, decisions
 // and counts as the reference; only the summation order differs.
 // FP32: cap registers for occupancy (RHS 80 regs -> 6 CTAs/SM, no spills)
-template <typename R, int MODE>
+template <typename R, int MODE, bool WIN>
 constexpr int ws_min_blocks() {
-  return sizeof(R) != 4 ? 1 : (MODE == kBhRhs ? 6 : (MODE == kBhHess ? 4 : 5));
+  return sizeof(R) != 4 ? 1
+                        : (MODE == kBhRhs ? (WIN ? GS_BH_WS_WIN_MINB : GS_BH_WS_NOWIN_MINB)
+                                          : (MODE == kBhHess ? GS_BH_WS_HESS_MINB : 5));
 }
 
-template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE>())) k_bh_ws(const BhArgs<R> a) {
+// WIN: node windows (ntask > 1); the single-window instantiation drops the
+// window bookkeeping (registers and instructions) for large N.
+template <typename R, int MODE, bool WIN>
+__global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_ws(const BhArgs<R> a) {
   const int qi = blockIdx.x * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
@@ -386,11 +412,11 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE>())) k_bh_ws(con
   // this block's window [A, B) of the pre-order node array and the leaf-order
   // interval [bA, bB) of the leaves inside it (see bh_tasks)
   int A = 0, B = m, bA = 0, bB = a.n;
-  if (a.ntask > 1) {
+  if (WIN) {
     A = (int)((long long)m * blockIdx.y / a.ntask);
     B = (int)((long long)m * (blockIdx.y + 1) / a.ntask);
-    bA = A < m ? code_of(ld4(a.nrec + 2 * A + 1).w) : a.n;
-    bB = B < m ? code_of(ld4(a.nrec + 2 * B + 1).w) : a.n;
+    bA = A < m ? code_of(ld4(a.nrec + 4 * A + 1).w) : a.n;
+    bB = B < m ? code_of(ld4(a.nrec + 4 * B + 1).w) : a.n;
   }
   int next = out >= 0 ? 0 : INT_MAX;
   int j = 0, je = -1;  // pending direct range
@@ -400,11 +426,12 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE>())) k_bh_ws(con
     V4<R> Q = zero, P = zero, Al = zero, Be = zero;  // this iteration's unit
     if (j > je && next < m) {
       const int nd = next;
-      const V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);  // one 32-B sector (FP32)
+      const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);  // one 32-B sector (FP32)
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
       const int skip = code & 0x3fffffff;
       const bool own = nd >= A;  // the node itself is in this block's window
+      if (a.prefetch && skip < B) prefetch_l1(a.nrec + 4 * skip);
       next = skip;
       if (skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
@@ -416,18 +443,18 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE>())) k_bh_ws(con
           ++c_dir;
         } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
           j = begin;
-          je = begin + code_of(ld4(a.mom + nd).w) - 1;
+          je = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
         } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
           if (own) {
-            Q = ld4(a.cen + nd);
-            P = ld4(a.mom + nd);
+            Q = ld4(a.nrec + 4 * nd + 2);
+            P = ld4(a.nrec + 4 * nd + 3);
             if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
             have = true;
             ++c_app;
           }
         } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
           j = max(begin, bA);
-          je = min(begin + code_of(ld4(a.mom + nd).w), bB) - 1;
+          je = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
           c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
         } else {
           next = nd + 1;
@@ -556,8 +583,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
   if (a.ntask > 1) {
     A = (int)((long long)m * blockIdx.y / a.ntask);
     B = (int)((long long)m * (blockIdx.y + 1) / a.ntask);
-    bA = A < m ? code_of(ld4(a.nrec + 2 * A + 1).w) : a.n;
-    bB = B < m ? code_of(ld4(a.nrec + 2 * B + 1).w) : a.n;
+    bA = A < m ? code_of(ld4(a.nrec + 4 * A + 1).w) : a.n;
+    bB = B < m ? code_of(ld4(a.nrec + 4 * B + 1).w) : a.n;
   }
   int next = out >= 0 ? 0 : INT_MAX;
   int ds = 0, de = -1;  // this lane's pending direct interval (leaf order, inclusive)
@@ -569,11 +596,12 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
     if (nd == INT_MAX) break;
     ++n_iter;
     // the node's compact record, loaded by every lane (one broadcast sector)
-    const V4<R> l = ld4(a.nrec + 2 * nd), h = ld4(a.nrec + 2 * nd + 1);
+    const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);
     const int code = code_of(l.w);
     const int begin = code_of(h.w);
     const int skip = code & 0x3fffffff;
     const bool here = next == nd;
+    if (a.prefetch && skip < B && lane_is_first_parked(here)) prefetch_l1(a.nrec + 4 * skip);
     bool have = false, ranged = false;
     V4<R> Q = zero, P = zero, Al = zero, Be = zero;
     int rb = 0, re = -1;
@@ -591,11 +619,11 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
         } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
           ranged = true;
           rb = begin;
-          re = begin + code_of(ld4(a.mom + nd).w) - 1;
+          re = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
         } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
           if (own) {
-            Q = ld4(a.cen + nd);
-            P = ld4(a.mom + nd);
+            Q = ld4(a.nrec + 4 * nd + 2);
+            P = ld4(a.nrec + 4 * nd + 3);
             if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
             have = true;
             ++c_app;
@@ -603,7 +631,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
         } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
           ranged = true;
           rb = max(begin, bA);
-          re = min(begin + code_of(ld4(a.mom + nd).w), bB) - 1;
+          re = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
           c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
         } else {
           next = nd + 1;
@@ -735,8 +763,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
       SP = ld4(a.srec + 2 * j + 1);
       if (MODE == kBhHess) { SA = ld4(a.sadj + 2 * j); SB = ld4(a.sadj + 2 * j + 1); }
     } else if (next < m) {
-      NL = ld4(a.nrec + 2 * next);
-      NH = ld4(a.nrec + 2 * next + 1);
+      NL = ld4(a.nrec + 4 * next);
+      NH = ld4(a.nrec + 4 * next + 1);
       NC = ld4(a.cen + next);
       NM = ld4(a.mom + next);
       if (MODE == kBhHess) { NA = ld4(a.nadj_a + next); NB = ld4(a.nadj_b + next); }
@@ -824,9 +852,15 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
     else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
     else k_bh_pipe<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
   } else if (kind == 1 || kind == 4) {
-    if (mode == kBhRhs) k_bh_ws<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
-    else if (mode == kBhHess) k_bh_ws<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
-    else k_bh_ws<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
+    if (a.ntask > 1) {
+      if (mode == kBhRhs) k_bh_ws<R, kBhRhs, true><<<nb, kBhNT, 0, st>>>(a);
+      else if (mode == kBhHess) k_bh_ws<R, kBhHess, true><<<nb, kBhNT, 0, st>>>(a);
+      else k_bh_ws<R, kBhVel, true><<<nb, kBhNT, 0, st>>>(a);
+    } else {
+      if (mode == kBhRhs) k_bh_ws<R, kBhRhs, false><<<nb, kBhNT, 0, st>>>(a);
+      else if (mode == kBhHess) k_bh_ws<R, kBhHess, false><<<nb, kBhNT, 0, st>>>(a);
+      else k_bh_ws<R, kBhVel, false><<<nb, kBhNT, 0, st>>>(a);
+    }
   } else {
     if (mode == kBhRhs) k_bh<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
     else if (mode == kBhHess) k_bh<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
@@ -879,6 +913,13 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
     a.grp_lim2 = (R)(g < 1e150 ? g * g : INFINITY);
   }
   a.split = 0;
+  {
+    static const int pf = [] {
+      const char* e = std::getenv("GS_BH_PREFETCH");
+      return e ? std::atoi(e) : 0;  // measured: no gain (records hit L1/L2 already)
+    }();
+    a.prefetch = pf;
+  }
   a.inv_two_s = (R)kc.inv_two_s;
   a.part = static_cast<V4<R>*>(q.part);
   a.per_query = q.per_query;

@@ -492,8 +492,10 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 // traversal-format node fields: centroid = position_sum * (1 / count)
 // (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
 // Compact traversal record (2 vec4 per node, one 32-B sector in FP32):
-//   {lo.xyz, code} {hi.xyz, begin}, code = skip | single-point leaf << 31 |
-//   bucket leaf << 30; the point count rides in mom.w.
+//   {lo.xyz, code} {hi.xyz, begin} {centroid, count} {momentum sum, count},
+//   code = skip | single-point leaf << 31 | bucket leaf << 30: 64 B (FP32),
+//   one cache-line half, so a far node's centroid/momentum loads after the
+//   gate hit L1; the point count rides in mom.w.
 __device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
 __device__ __forceinline__ double ival(double, int v) { return (double)v; }
 
@@ -519,20 +521,22 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
     V4<R> h = (leaf && cnt == 1) ? ld4(srec + 2 * mi.y + 1) : ld4(hi + i);
     l.w = ival(R(0), code);
     h.w = ival(R(0), mi.y);
-    st4(nrec + 2 * i, l);
-    st4(nrec + 2 * i + 1, h);
+    st4(nrec + 4 * i, l);
+    st4(nrec + 4 * i + 1, h);
   }
   if (mode == 0) {
     double cx = __dmul_rn(a.x, inv), cy = __dmul_rn(a.y, inv), cz = __dmul_rn(a.z, inv);
-    if (scaled) {
-      const float kf = (float)kap;
-      st4(o0 + i, mk4<R>((R)fmaf(kf, (float)cx, -(float)(kap * c0x)),
-                         (R)fmaf(kf, (float)cy, -(float)(kap * c0y)),
-                         (R)fmaf(kf, (float)cz, -(float)(kap * c0z)), R(cnt)));
-    } else {
-      st4(o0 + i, mk4<R>(R(cx), R(cy), R(cz), R(cnt)));
+    const V4<R> cen = scaled ? mk4<R>((R)fmaf((float)kap, (float)cx, -(float)(kap * c0x)),
+                                      (R)fmaf((float)kap, (float)cy, -(float)(kap * c0y)),
+                                      (R)fmaf((float)kap, (float)cz, -(float)(kap * c0z)), R(cnt))
+                             : mk4<R>(R(cx), R(cy), R(cz), R(cnt));
+    const V4<R> mom = mk4<R>(R(b.x), R(b.y), R(b.z), ival(R(0), cnt));
+    st4(o0 + i, cen);
+    st4(o1 + i, mom);
+    if (nrec && !((mi.w & 1) && cnt == 1)) {  // the record's far-field half
+      st4(nrec + 4 * i + 2, cen);
+      st4(nrec + 4 * i + 3, mom);
     }
-    st4(o1 + i, mk4<R>(R(b.x), R(b.y), R(b.z), ival(R(0), cnt)));
   } else {
     st4(o0 + i, mk4<R>(R(a.x), R(a.y), R(a.z)));
     // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
@@ -717,7 +721,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.hi.ensure(vb * cap));
   GS_TRY_INT(t.cen.ensure(vb * cap));
   GS_TRY_INT(t.mom.ensure(vb * cap));
-  GS_TRY_INT(t.nrec.ensure(2 * vb * cap));
+  GS_TRY_INT(t.nrec.ensure(4 * vb * cap));
   GS_TRY_INT(t.psum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.msum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.squ.ensure(vb * n));
