@@ -74,6 +74,10 @@ typedef struct gs_config {
   double threshold_multiplier; /* BH opening threshold = multiplier * sigma (3 by default) */
   int32_t integrator;          /* gs_integrator */
   int32_t precision;           /* gs_precision of the device arithmetic */
+  /* Barnes-Hut aggregate dot scale: 0 = 1 (reference default), 1 = 1/count
+   * (the reference built with GEOSHOOT_BH_LITERAL_MEAN_DOT, bh_kernel.cpp:19-26). */
+  int32_t literal_mean_dot;
+  int32_t reserved0;           /* must be 0 */
 } gs_config;
 
 /* Reference defaults (core.hpp:204-213): sigma 2, lambda 1, 40 steps, exact,
@@ -105,6 +109,11 @@ typedef struct gs_ctx gs_ctx;
 gs_ctx* gs_create(int device, gs_status* status);
 void gs_destroy(gs_ctx* ctx);
 const char* gs_last_error(const gs_ctx* ctx);
+/* Literal-mean-dot mode of the context's tree-level Barnes-Hut calls
+ * (gs_bh_rhs / gs_bh_hessian_products / gs_bh_hamiltonian): the reference's
+ * compile-time GEOSHOOT_BH_LITERAL_MEAN_DOT switch (bh_kernel.cpp:19-26) as a
+ * runtime setting. Shooting calls take it from gs_config.literal_mean_dot. */
+gs_status gs_set_literal_mean_dot(gs_ctx* ctx, int32_t enable);
 int gs_last_nonfinite_step(const gs_ctx* ctx);
 uint32_t gs_last_config_violations(const gs_ctx* ctx);
 int gs_abi_version(void);
@@ -299,6 +308,15 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
                             int32_t batch, const int64_t* n, const double* const* q0,
                             const double* const* target, double* const* p_out, int32_t* reasons,
                             int32_t* iterations, int32_t* evaluations, double* final_total);
+
+/* Batched independent evaluations (SURVEY.md §8b gs_evaluate_batch): subject b
+ * (n[b] points, its own q0 / p0 / target) runs gs_evaluate on its own
+ * context/stream and host thread; reports[b], grad_out[b] (n[b] x 3) and
+ * stats[b] (optional) as gs_evaluate. Results equal one-at-a-time calls. */
+gs_status gs_evaluate_batch(int device, const gs_config* cfg, int32_t batch, const int64_t* n,
+                            const double* const* q0, const double* const* p0,
+                            const double* const* target, gs_report* reports,
+                            double* const* grad_out, gs_stats* stats);
 
 /* ---- point-cloud files (pipeline.hpp:52-68) ---------------
  * xyz text ("x y z" per line, '#' comments) and legacy-VTK ASCII polydata

@@ -20,6 +20,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle_port.so")
 REF_SO = os.path.join(HERE, "_ref", "libgeoshoot_ref.so")
+# built with -DGEOSHOOT_BH_LITERAL_MEAN_DOT (oracle/Makefile): literal_mean_dot parity
+REF_LMD_SO = os.path.join(HERE, "_ref", "libgeoshoot_ref_lmd.so")
 
 _d = C.POINTER(C.c_double)
 _u64 = C.POINTER(C.c_uint64)
@@ -468,6 +470,12 @@ class RefTree(_TreeDump):
                                                    _p(b), sigma, thr, threads, *map(_p, out)))
         return tuple(out)
 
+    def bh_hamiltonian(self, sigma, thr):
+        h = C.c_double()
+        self.ref._chk(self.ref.lib.ref_bh_hamiltonian(self.h, self.n, _p(self.q), _p(self.p), sigma,
+                                                      thr, C.byref(h)))
+        return h.value
+
     def bh_velocity(self, x, sigma, thr):
         x = _c(x)
         v = _vec(len(x))
@@ -497,3 +505,14 @@ def ref() -> Ref:
 
 def have_ref() -> bool:
     return os.path.exists(REF_SO)
+
+
+_ref_lmd = None
+
+
+def ref_lmd() -> Ref:
+    """The reference built with GEOSHOOT_BH_LITERAL_MEAN_DOT (aggregate dot scale 1/count)."""
+    global _ref_lmd
+    if _ref_lmd is None:
+        _ref_lmd = Ref(REF_LMD_SO)
+    return _ref_lmd

@@ -29,7 +29,7 @@
 #include "geoshoot/shooting.hpp"
 #include "geoshoot/synthetic.hpp"
 
-using namespace geoshoot_ref;
+using namespace geoshoot;  // renamed by -Dgeoshoot=geoshoot_ref[_lmd] (oracle/Makefile)
 
 namespace {
 

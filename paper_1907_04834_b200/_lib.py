@@ -42,6 +42,8 @@ class gs_config(C.Structure):
         ("threshold_multiplier", C.c_double),
         ("integrator", C.c_int32),
         ("precision", C.c_int32),
+        ("literal_mean_dot", C.c_int32),
+        ("reserved0", C.c_int32),
     ]
 
 
@@ -96,6 +98,7 @@ SIGNATURES = [
     ("gs_create", _vp, [C.c_int, C.POINTER(C.c_int)]),
     ("gs_destroy", None, [_vp]),
     ("gs_last_error", C.c_char_p, [_vp]),
+    ("gs_set_literal_mean_dot", _st, [_vp, C.c_int32]),
     ("gs_last_nonfinite_step", C.c_int, [_vp]),
     ("gs_last_config_violations", C.c_uint32, [_vp]),
     ("gs_validate_config", _st, [C.POINTER(gs_config), C.POINTER(C.c_uint32)]),
@@ -147,6 +150,9 @@ SIGNATURES = [
     ("gs_last_parse_line", C.c_longlong, []),
     ("gs_last_io_error", C.c_char_p, []),
     ("gs_default_opt_config", gs_opt_config, []),
+    ("gs_evaluate_batch", _st, [C.c_int, C.POINTER(gs_config), C.c_int32, C.POINTER(_i64),
+                                C.POINTER(_d), C.POINTER(_d), C.POINTER(_d), C.POINTER(gs_report),
+                                C.POINTER(_d), C.POINTER(gs_stats)]),
     ("gs_optimize_batch", _st, [C.c_int, C.POINTER(gs_config), C.POINTER(gs_opt_config), C.c_int32,
                                 C.POINTER(C.c_int64), C.POINTER(_d), C.POINTER(_d), C.POINTER(_d),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -79,6 +79,8 @@ gs_config to_c(const ShootingConfig& c) {
   g.threshold_multiplier = c.threshold_multiplier;
   g.integrator = c.integrator == Integrator::RK4 ? GS_RK4 : GS_EULER;
   g.precision = prec_of(c.precision);
+  g.literal_mean_dot = c.literal_mean_dot ? 1 : 0;
+  g.reserved0 = 0;
   return g;
 }
 
@@ -304,6 +306,8 @@ void require_tree(const Octree& t) {
   if (t.point_count() == 0 || !t.device()) throw EmptyTree("Barnes-Hut query on an empty tree");
 }
 }  // namespace
+
+void set_bh_literal_mean_dot(bool enable) { check(gs_set_literal_mean_dot(ctx(), enable ? 1 : 0)); }
 
 BhVelocity bh_velocity(const Octree& tree, const Vec3& x, double sigma, double threshold) {
   require_tree(tree);

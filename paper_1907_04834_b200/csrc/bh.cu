@@ -81,6 +81,7 @@ struct BhArgs {
   int split;           // 1: k_bh_grp takes the group warps, k_bh_ws the others
   int ntask;           // pre-order node windows per query (blockIdx.y); partials [task][query]
   int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
+  int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
   uint32_t* per_query;
@@ -151,19 +152,25 @@ struct Acc {
 
 // One (direct or aggregate) unit: Q = source coords, P = momentum (sum),
 // Al = alpha (sum), Be = beta (mean) -- bh_kernel.cpp:86-110 / :119-157.
-template <typename R, int MODE>
+// dsc: aggregate_dot_scale (bh_kernel.cpp:19-26) -- 1 for direct units and by
+// default; 1/count for an approximated node under literal-mean-dot (LMD).
+// LMD also accumulates sum c into acc.v[6] (the RHS partial's B.w) for
+// bh_hamiltonian, whose dot is scaled too (bh_kernel.cpp:184).
+template <typename R, int MODE, bool LMD = false>
 __device__ __forceinline__ void unit(Acc<R>& acc, const V4<R>& xs, const V4<R>& px,
                                      const V4<R>& ai, const V4<R>& bi, const V4<R>& Q,
                                      const V4<R>& P, const V4<R>& Al, const V4<R>& Be,
-                                     const BhArgs<R>& a) {
+                                     const BhArgs<R>& a, R dsc = R(1)) {
   const R dx = xs.x - Q.x, dy = xs.y - Q.y, dz = xs.z - Q.z;
   const R g = kern(dx, dy, dz, a);
   if (MODE == kBhVel) {
     acc.v[0] += g * P.x; acc.v[1] += g * P.y; acc.v[2] += g * P.z;
   } else if (MODE == kBhRhs) {
-    const R c = (px.x * P.x + px.y * P.y + px.z * P.z) * g;
+    const R c = LMD ? (px.x * P.x + px.y * P.y + px.z * P.z) * dsc * g
+                    : (px.x * P.x + px.y * P.y + px.z * P.z) * g;
     acc.v[0] += g * P.x; acc.v[1] += g * P.y; acc.v[2] += g * P.z;
     acc.v[3] += c * dx; acc.v[4] += c * dy; acc.v[5] += c * dz;
+    if (LMD) acc.v[6] += c;
   } else {
     const R dbx = bi.x - Be.x, dby = bi.y - Be.y, dbz = bi.z - Be.z;
     const R ddb = dx * dbx + dy * dby + dz * dbz;
@@ -172,7 +179,7 @@ __device__ __forceinline__ void unit(Acc<R>& acc, const V4<R>& xs, const V4<R>& 
     const R t1 = g * s1;
     acc.v[0] += t1 * dx; acc.v[1] += t1 * dy; acc.v[2] += t1 * dz;
     acc.v[3] += g * Al.x; acc.v[4] += g * Al.y; acc.v[5] += g * Al.z;
-    const R w = g * pp, uu = ddb * a.c1;
+    const R w = LMD ? g * (pp * dsc) : g * pp, uu = ddb * a.c1;
     acc.v[6] += w * (uu * dx - dbx); acc.v[7] += w * (uu * dy - dby); acc.v[8] += w * (uu * dz - dbz);
     const R m = g * ddb;
     acc.v[9] += m * P.x; acc.v[10] += m * P.y; acc.v[11] += m * P.z;
@@ -321,13 +328,13 @@ __device__ __forceinline__ V4<R> shfl4(const V4<R>& v, int src) {
                 __shfl_sync(0xffffffffu, v.z, src), R(0));
 }
 
-template <typename R, int MODE>
+template <typename R, int MODE, bool LMD = false>
 __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc<R>& acc,
                                             uint32_t& c_dir, const V4<R>& xs, const V4<R>& px,
                                             const V4<R>& ai, const V4<R>& bi,
                                             const BhArgs<R>& a) {
   const int lane = threadIdx.x & 31;
-  constexpr int kAcc = MODE == kBhHess ? 12 : (MODE == kBhRhs ? 6 : 3);
+  constexpr int kAcc = MODE == kBhHess ? 12 : (MODE == kBhRhs ? (LMD ? 7 : 6) : 3);
   while (owners) {
     const int o = __ffs(owners) - 1;
     owners &= owners - 1;
@@ -342,9 +349,9 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
     for (int s = rb + lane; s <= re; s += 32) {
       const V4<R> Q = ld4(a.srec + 2 * s), P = ld4(a.srec + 2 * s + 1);
       if (MODE == kBhHess)
-        unit<R, MODE>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
+        unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
       else
-        unit<R, MODE>(part, oxs, opx, oai, obi, Q, P, zero, zero, a);
+        unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, zero, zero, a);
     }
 #pragma unroll
     for (int c = 0; c < kAcc; ++c) {
@@ -377,7 +384,7 @@ constexpr int ws_min_blocks() {
 
 // WIN: node windows (ntask > 1); the single-window instantiation drops the
 // window bookkeeping (registers and instructions) for large N.
-template <typename R, int MODE, bool WIN>
+template <typename R, int MODE, bool WIN, bool LMD = false>
 __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_ws(const BhArgs<R> a) {
   const int qi = blockIdx.x * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
@@ -424,6 +431,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
   while (__any_sync(0xffffffffu, next < m || j <= je)) {
     bool have = false;
     V4<R> Q = zero, P = zero, Al = zero, Be = zero;  // this iteration's unit
+    R dsc = R(1);
     if (j > je && next < m) {
       const int nd = next;
       const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);  // one 32-B sector (FP32)
@@ -449,6 +457,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
             Q = ld4(a.nrec + 4 * nd + 2);
             P = ld4(a.nrec + 4 * nd + 3);
             if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+            if (LMD) dsc = R(1) / Q.w;  // Q.w = count
             have = true;
             ++c_app;
           }
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     }
     // long direct ranges (dense near field) are swept by the whole warp
     const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
-    if (big) coop_ranges<R, MODE>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
+    if (big) coop_ranges<R, MODE, LMD>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
     if (!have && j <= je) {
       Q = ld4(a.srec + 2 * j);
       P = ld4(a.srec + 2 * j + 1);
@@ -473,13 +482,15 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       ++j;
       ++c_dir;
     }
-    if (have) unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
+    if (have) unit<R, MODE, LMD>(acc, xs, px, ai, bi, Q, P, Al, Be, a, dsc);
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
     const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
     V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
-    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
+    for (int k = 0; k < per; ++k)
+      st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2],
+                        (LMD && MODE == kBhRhs && k == 1) ? acc.v[6] : R(0)));
     if (a.per_query) {
       a.per_query[3 * out] = c_dir;
       a.per_query[3 * out + 1] = c_app;
@@ -822,7 +833,7 @@ static double bh_group_ratio() {
 
 template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
-  const int kind = bh_kernel_choice();
+  const int kind = a.lmd ? 1 : bh_kernel_choice();  // literal-mean-dot: independent walks only
   if (kind == 0 || kind == 2) a.ntask = 1;  // single-window kernels
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
@@ -852,7 +863,15 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
     else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
     else k_bh_pipe<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
   } else if (kind == 1 || kind == 4) {
-    if (a.ntask > 1) {
+    if (a.lmd && mode != kBhVel) {  // the dot scale has no effect on velocities
+      if (a.ntask > 1) {
+        if (mode == kBhRhs) k_bh_ws<R, kBhRhs, true, true><<<nb, kBhNT, 0, st>>>(a);
+        else k_bh_ws<R, kBhHess, true, true><<<nb, kBhNT, 0, st>>>(a);
+      } else {
+        if (mode == kBhRhs) k_bh_ws<R, kBhRhs, false, true><<<nb, kBhNT, 0, st>>>(a);
+        else k_bh_ws<R, kBhHess, false, true><<<nb, kBhNT, 0, st>>>(a);
+      }
+    } else if (a.ntask > 1) {
       if (mode == kBhRhs) k_bh_ws<R, kBhRhs, true><<<nb, kBhNT, 0, st>>>(a);
       else if (mode == kBhHess) k_bh_ws<R, kBhHess, true><<<nb, kBhNT, 0, st>>>(a);
       else k_bh_ws<R, kBhVel, true><<<nb, kBhNT, 0, st>>>(a);
@@ -925,6 +944,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.per_query = q.per_query;
   a.totals = q.totals;
   a.ntask = q.per_query ? 1 : std::max(1, q.ntask);  // per-query counts: one window
+  a.lmd = q.lmd;
   (void)sigma;
   return a;
 }
@@ -976,6 +996,7 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   BhQuery q;
   q.mode = kBhRhs;
   q.ntask = K;
+  q.lmd = cfg.literal_mean_dot;
   q.tgt_begin = (int)tb;
   q.n_tgt = (int)nt;
   q.part = w.part.ptr;
@@ -1013,6 +1034,7 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
   BhQuery q;
   q.mode = kBhHess;
   q.ntask = K;
+  q.lmd = cfg.literal_mean_dot;
   q.tgt_begin = 0;
   q.n_tgt = (int)n;
   q.part = w.part.ptr;

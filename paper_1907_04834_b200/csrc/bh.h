@@ -81,6 +81,7 @@ struct BhQuery {
   uint32_t* per_query = nullptr;  // optional [nq][3] direct, approx, visited (query order)
   unsigned long long* totals = nullptr;  // optional [3] sums
   int ntask = 1;  // node windows (bh_tasks); part holds [ntask][queries] partials
+  int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
 };
 int bh_tasks(int64_t nq);
 int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,

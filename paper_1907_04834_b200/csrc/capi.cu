@@ -61,6 +61,7 @@ using namespace gsb;
 struct gs_ctx {
   Device dev;
   cudaStream_t stream = nullptr;
+  int lmd = 0;  // gs_set_literal_mean_dot (tree-level Barnes-Hut calls)
   // host-array staging (double [n][3]) and small scalars
   DBuf stage_a, stage_b, stage_c, stage_d, scal;
   DBuf rec_a, rec_b, part, epart;
@@ -101,6 +102,12 @@ struct gs_flow {
 
 extern "C" {
 
+gs_status gs_set_literal_mean_dot(gs_ctx* c, int32_t enable) {
+  if (!c) return GS_INVALID_ARGUMENT;
+  c->lmd = enable ? 1 : 0;
+  return GS_OK;
+}
+
 gs_config gs_default_config(void) {
   gs_config c;
   c.sigma = 2.0;
@@ -110,6 +117,8 @@ gs_config gs_default_config(void) {
   c.threshold_multiplier = 3.0;
   c.integrator = GS_EULER;
   c.precision = GS_F64;
+  c.literal_mean_dot = 0;
+  c.reserved0 = 0;
   return c;
 }
 
@@ -1097,6 +1106,7 @@ int tree_rhs(gs_tree* tr, double sigma, double thr, double* dhdp_dev, double* dh
   q.part = tr->part.ptr;
   q.per_query = tr->pq.as<uint32_t>();
   q.totals = tr->stats.as<unsigned long long>();
+  q.lmd = c->lmd;
   GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
   FwdEpi e;
   e.rec = tr->rec.ptr;
@@ -1220,12 +1230,15 @@ gs_status gs_bh_hamiltonian(gs_tree* tr, double sigma, double thr, double* h_out
   GS_TRY(c->scal.ensure(64));
   int blocks = 0;
   GS_TRY(tree_rhs(tr, sigma, thr, nullptr, nullptr, c->epart.as<double>(), &blocks));
+  if (c->lmd)  // the dot is scaled too (bh_kernel.cpp:184): the kernel's per-target sum of c
+    GS_TRY(sum_part_w(tr->prec, tr->part.ptr, (int)n, 2, 1, c->epart.as<double>(), &blocks, c->stream));
   GS_TRY(reduce_sum(c->epart.as<double>(), blocks, c->scal.as<double>(), c->stream));
   double h = 0.0;
   GS_CUDA_OK(cudaMemcpyAsync(&h, c->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   GS_TRY(sync(c));
-  // bh_hamiltonian = sum_j p_j . sum_units G P = 1/2 <p, dH/dp> (bh_kernel.cpp:162-191)
-  *h_out = 0.5 * h;
+  // bh_hamiltonian = sum_j p_j . sum_units G P = 1/2 <p, dH/dp> (bh_kernel.cpp:162-191);
+  // under literal-mean-dot, sum_j sum_units (p_j . P) scale G directly
+  *h_out = c->lmd ? h : 0.5 * h;
   return (gs_status)fill_stats(tr, stats, n);
 }
 
@@ -1296,6 +1309,7 @@ gs_status gs_bh_hessian_products(gs_tree* tr, const double* alpha, const double*
   q.n_tgt = (int)n;
   q.part = tr->part.ptr;
   q.totals = tr->stats.as<unsigned long long>();
+  q.lmd = c->lmd;
   GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
   const KernelConsts& kc = tr->t.kc;
   const double cd = tr->prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;

@@ -157,6 +157,9 @@ int gradient_finalize(int prec, const void* adj, const double* dhdp0, int64_t n,
 int adjoint_init(int prec, const void* rec_T, const double* target, double lambda, int64_t n,
                  void* adj, double* sse_part, int* blocks, cudaStream_t st);
 int reduce_sum(const double* part, int count, double* out, cudaStream_t st);
+// per-block FP64 sums of the .w lane of partial vec4 `which` of n targets ([n][per] layout)
+int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
+               int* blocks, cudaStream_t st);
 // ++*counter on the device (the step counter of graph-replayed flows)
 int step_counter_inc(int* counter, cudaStream_t st);
 

@@ -241,7 +241,29 @@ __global__ void k_reduce(const double* part, int count, double* out) {
 
 inline int blocks_for(int64_t n, int nt) { return (int)std::max<int64_t>(1, (n + nt - 1) / nt); }
 
+// per-block sums of the .w lane of partial vec4 `which` ([S][n][per] layout, S = 1)
+template <typename R>
+__global__ void __launch_bounds__(kEpiNT) k_sum_w(const V4<R>* part, int n, int per, int which,
+                                                  double* out) {
+  const int t = blockIdx.x * kEpiNT + threadIdx.x;
+  const double v = t < n ? (double)ld4(part + (size_t)per * t + which).w : 0.0;
+  const double s = block_sum<kEpiNT>(v);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 }  // namespace
+
+int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
+               int* blocks, cudaStream_t st) {
+  const int nb = blocks_for(n, kEpiNT);
+  if (prec == kF32)
+    k_sum_w<float><<<nb, kEpiNT, 0, st>>>(static_cast<const float4*>(part), n, per, which, block_out);
+  else
+    k_sum_w<double><<<nb, kEpiNT, 0, st>>>(static_cast<const double4*>(part), n, per, which, block_out);
+  GS_CUDA_OK(cudaGetLastError());
+  *blocks = nb;
+  return GS_OK;
+}
 
 int fwd_epilogue(int prec, const FwdEpi& e, cudaStream_t st, int* blocks_out) {
   const int nb = blocks_for(e.n_tgt, kEpiNT);

@@ -332,4 +332,30 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
   return GS_OK;
 }
 
+gs_status gs_evaluate_batch(int device, const gs_config* cfg, int32_t batch, const int64_t* n,
+                            const double* const* q0, const double* const* p0,
+                            const double* const* target, gs_report* reports,
+                            double* const* grad_out, gs_stats* stats) {
+  if (!cfg || batch < 0 || !n || !q0 || !p0 || !target || !reports || !grad_out)
+    return GS_INVALID_ARGUMENT;
+  std::vector<gs_status> st((size_t)batch, GS_OK);
+  std::vector<std::thread> pool;
+  for (int32_t b = 0; b < batch; ++b)
+    pool.emplace_back([&, b] {
+      gs_status cs = GS_OK;
+      gs_ctx* c = gs_create(device, &cs);
+      if (!c) {
+        st[b] = cs;
+        return;
+      }
+      st[b] = gs_evaluate(c, cfg, n[b], q0[b], p0[b], target[b], reports + b, grad_out[b],
+                          stats ? stats + b : nullptr);
+      gs_destroy(c);
+    });
+  for (auto& t : pool) t.join();
+  for (gs_status s : st)
+    if (s != GS_OK) return s;
+  return GS_OK;
+}
+
 }  // extern "C"

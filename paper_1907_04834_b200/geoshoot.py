@@ -135,13 +135,15 @@ class ShootingConfig:
     threshold_multiplier: float = 3.0
     integrator: int = EULER
     precision: int = F64
+    literal_mean_dot: bool = False  # GEOSHOOT_BH_LITERAL_MEAN_DOT (bh_kernel.cpp:19-26)
 
     def opening_threshold(self) -> float:
         return self.threshold_multiplier * self.sigma
 
     def c(self) -> L.gs_config:
         return L.gs_config(self.sigma, self.lambda_, self.timesteps, self.backend,
-                           self.threshold_multiplier, self.integrator, self.precision)
+                           self.threshold_multiplier, self.integrator, self.precision,
+                           1 if self.literal_mean_dot else 0, 0)
 
 
 def _arr(a, name="array") -> np.ndarray:
@@ -268,6 +270,11 @@ class Geoshoot:
         return tuple(out)  # pq_alpha, pp_alpha, qq_beta, qp_beta
 
     # ---- octree -------------------------------------------------------------
+    def set_literal_mean_dot(self, enable: bool):
+        """Tree-level BH calls on this context use the reference's
+        GEOSHOOT_BH_LITERAL_MEAN_DOT aggregate dot scale 1/count (bh_kernel.cpp:19-26)."""
+        self.check(self.lib.gs_set_literal_mean_dot(self.ctx, 1 if enable else 0))
+
     def build_tree(self, q, p, precision=F64) -> "Octree":
         q, p = _arr(q, "q"), _arr(p, "p")
         _require_aligned(len(q), len(p), "Octree::build")
@@ -382,6 +389,26 @@ class Geoshoot:
                                               reasons, iters, evals, _p(tot)))
         return {"p0": outs, "reasons": list(reasons), "iterations": list(iters),
                 "evaluations": list(evals), "final_total": tot}
+
+    def evaluate_batch(self, q0s, p0s, targets, cfg: ShootingConfig, device: int = 0):
+        """Independent evaluations (one stream + host thread each) -> [Evaluation]."""
+        B = len(q0s)
+        q0s, p0s, targets = ([_arr(a) for a in q0s], [_arr(a) for a in p0s],
+                             [_arr(a) for a in targets])
+        for q, p, t in zip(q0s, p0s, targets):
+            _require_aligned(len(q), len(p), "evaluate_batch")
+            _require_aligned(len(q), len(t), "evaluate_batch(target)")
+        grads = [np.empty_like(q) for q in q0s]
+        c = cfg.c()
+        ns = (C.c_int64 * B)(*[len(q) for q in q0s])
+        P = L._d * B
+        reps, sts = (L.gs_report * B)(), (L.gs_stats * B)()
+        self.check(self.lib.gs_evaluate_batch(device, C.byref(c), B, ns, P(*map(_p, q0s)),
+                                              P(*map(_p, p0s)), P(*map(_p, targets)), reps,
+                                              P(*map(_p, grads)), sts))
+        return [Evaluation({"energy": r.energy, "attachment": r.attachment, "total": r.total,
+                            "residual_sse": r.residual_sse}, g, s.as_dict())
+                for r, g, s in zip(reps, grads, sts)]
 
     def procrustes_align(self, source, target):
         """procrustes_align (procrustes.cpp:7-58) -> (rotation 3x3, translation, aligned)."""

@@ -22,6 +22,12 @@ struct TraversalStats {
   }
 };
 
+/// The reference's compile-time GEOSHOOT_BH_LITERAL_MEAN_DOT switch
+/// (bh_kernel.cpp:19-26: aggregate dot scale 1/count) as a runtime setting of
+/// this thread's tree-level Barnes-Hut calls. Shooting uses
+/// ShootingConfig::literal_mean_dot.
+void set_bh_literal_mean_dot(bool enable);
+
 struct BhVelocity {
   Vec3 velocity;
   TraversalStats stats;

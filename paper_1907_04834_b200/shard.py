@@ -54,6 +54,28 @@ def register_subjects(gs, templates, targets, cfg, group=None, runner=None, **op
     return [x for part in parts for x in part]
 
 
+def evaluate_subjects(gs, templates, momenta, targets, cfg, group=None, runner=None):
+    """Batched evaluations across ranks (SURVEY.md §8b ``gs_evaluate_batch``
+    "distributed across ranks"): rank r evaluates its contiguous block of
+    subjects concurrently on its GPU (``Geoshoot.evaluate_batch``) and the
+    per-subject (report, gradient, stats) are gathered to every rank.
+    Returns [{"subject", "report", "gradient", "stats"}] in subject order."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    b, c = subject_range(len(templates), rank, world)
+    run = runner if runner is not None else gs.evaluate_batch
+    mine = []
+    if c:
+        evs = run(templates[b:b + c], momenta[b:b + c], targets[b:b + c], cfg)
+        mine = [{"subject": b + k, "report": e.report, "gradient": e.gradient, "stats": e.stats}
+                for k, e in enumerate(evs)]
+    if world == 1:
+        return mine
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    return [x for part in parts for x in part]
+
+
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Equal contiguous shards (n must be divisible by world)."""
     if n % world:

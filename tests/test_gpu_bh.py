@@ -9,6 +9,8 @@
 * Traversal: per-query (direct, approximated, visited) counts EXACTLY equal to
   the reference's; FP64 values to 1e-12, FP32 (FP32-rounded inputs) to 1e-5.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -261,3 +263,67 @@ def test_bh_warp_carrier_points(gs):
     tr = gs.shoot_forward(q, p, cfg)
     warped = gs.warp_points(tr, q, cfg)
     assert np.abs(warped - tr.q[-1]).max() < 1e-10
+
+
+# ---- literal-mean-dot mode: pinned to the reference built with
+# GEOSHOOT_BH_LITERAL_MEAN_DOT (oracle/_ref/libgeoshoot_ref_lmd.so) ----------
+@pytest.fixture
+def ref_lmd():
+    import oracle
+    if not os.path.exists(oracle.REF_LMD_SO):
+        pytest.skip("oracle/_ref/libgeoshoot_ref_lmd.so not built")
+    return oracle.ref_lmd()
+
+
+@pytest.fixture
+def gs_lmd(gs):
+    gs.set_literal_mean_dot(True)
+    yield gs
+    gs.set_literal_mean_dot(False)
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-12), (F32, 1e-5)])
+def test_lmd_tree_calls_match_reference(gs_lmd, ref, ref_lmd, prec, tol):
+    gs = gs_lmd
+    q, p, sigma = CASES["cube_small_sigma"]()
+    a, b = sym_uniform(len(q), 1.0, 991), sym_uniform(len(q), 1.0, 992)
+    if prec == F32:
+        q, p, a, b = f32(q), f32(p), f32(a), f32(b)
+    thr = 3.0 * sigma
+    t = gs.build_tree(q, p, precision=prec)
+    dp, dq, st = t.bh_hamiltonian_gradients(sigma, thr)
+    rt = ref_lmd.tree(q, p)
+    wp, wq, wper = rt.bh_rhs(sigma, thr, threads=8)
+    assert np.array_equal(t.query_stats(), wper)
+    assert rel_l2(dp, wp) <= tol and rel_l2(dq, wq) <= tol
+    # the scale changes dH/dq (and only it) against the default build
+    _, dq0, _ = ref.tree(q, p).bh_rhs(sigma, thr, threads=8)
+    assert rel_l2(dq, dq0) > 100 * tol
+    h, _ = t.bh_hamiltonian(sigma, thr)
+    assert h == pytest.approx(rt.bh_hamiltonian(sigma, thr), rel=tol)
+    t.accumulate_adjoints(a, b)
+    *got, _ = t.bh_hessian_products(a, b, sigma, thr)
+    rt.accumulate(a, b)
+    want = rt.bh_hessprod(a, b, sigma, thr, threads=8)
+    for g, w in zip(got, want):
+        assert rel_l2(g, w) <= 2 * tol
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-10), (F32, 1e-4)])
+def test_lmd_shooting_matches_reference(gs, ref_lmd, prec, tol):
+    n, sigma = 1500, 2.0
+    q = np.stack([np.linspace(0, 100, n), np.random.default_rng(83).uniform(-2, 2, n),
+                  np.zeros(n)], 1)
+    p = sym_uniform(n, 0.05, 84)
+    t = q + np.array([0.0, 0.5, 0.1])
+    if prec == F32:
+        q, p, t = f32(q), f32(p), f32(t)
+    cfg = ShootingConfig(sigma=sigma, lambda_=1.0, timesteps=10, backend=BARNES_HUT, precision=prec,
+                         literal_mean_dot=True)
+    fq, fp, _, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    wq, wp = ref_lmd.shoot_forward(q, p, sigma, 10, backend=1)
+    assert rel_l2(fq, wq[-1]) <= tol and rel_l2(fp, wp[-1]) <= tol
+    ev = gs.evaluate(q, p, t, cfg)
+    rep, g, _, _ = ref_lmd.evaluate(q, p, t, sigma, 1.0, 10, 1, threads=8)
+    assert ev.report["total"] == pytest.approx(rep[2], rel=tol)
+    assert rel_l2(ev.gradient, g) <= tol * 10

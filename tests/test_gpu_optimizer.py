@@ -76,3 +76,23 @@ def test_register_subjects_single_rank(gs, ref):
     for k, r in enumerate(res):
         assert np.array_equal(r["p0"], out["p0"][k])
         assert r["iterations"] == out["iterations"][k]
+
+
+def test_evaluate_batch_equals_single(gs):
+    """gs_evaluate_batch: subjects of different N on concurrent streams give the
+    one-at-a-time results bitwise; evaluate_subjects (one rank) the same."""
+    from paper_1907_04834_b200.shard import evaluate_subjects
+    from tests.util import ellipsoid, smooth_momenta
+    qs = [ellipsoid(400 + 150 * k, seed=70 + k) for k in range(3)]
+    ps = [smooth_momenta(q, 0.01, 80 + k) for k, q in enumerate(qs)]
+    ts = [q + 0.3 for q in qs]
+    for backend in (EXACT, BARNES_HUT):
+        cfg = ShootingConfig(sigma=3.0, lambda_=10.0, timesteps=5, backend=backend, precision=F32)
+        evs = gs.evaluate_batch(qs, ps, ts, cfg)
+        for q, p, t, e in zip(qs, ps, ts, evs):
+            one = gs.evaluate(q, p, t, cfg)
+            assert np.array_equal(e.gradient, one.gradient)
+            assert e.report == one.report
+        res = evaluate_subjects(gs, qs, ps, ts, cfg)
+        assert [r["subject"] for r in res] == [0, 1, 2]
+        assert all(np.array_equal(r["gradient"], e.gradient) for r, e in zip(res, evs))

@@ -167,3 +167,21 @@ def test_fd_adjoint(port):
                   port.evaluate(q, p - e, t, 1.1, 0.8, 10)[0][2]) / (2 * h)
             assert abs(g[i, a] - fp) <= 1e-5 * max(abs(fp), abs(g[i, a]), 1e-6)
     assert rel_l2(g, g) == 0.0
+
+
+def test_ref_literal_mean_dot_build():
+    """The GEOSHOOT_BH_LITERAL_MEAN_DOT build of the reference (oracle/Makefile)
+    changes only the aggregate dot (dH/dq), never dH/dp or the exact path."""
+    import oracle
+    if not os.path.exists(oracle.REF_LMD_SO):
+        pytest.skip("literal-mean-dot reference build absent")
+    rng = np.random.default_rng(17)
+    q, p = rng.uniform(0, 1, (800, 3)), rng.uniform(-1, 1, (800, 3))
+    R, L = oracle.ref(), oracle.ref_lmd()
+    dp0, dq0, per0 = R.tree(q, p).bh_rhs(0.03, 0.09)
+    dp1, dq1, per1 = L.tree(q, p).bh_rhs(0.03, 0.09)
+    assert np.array_equal(per0, per1) and np.array_equal(dp0, dp1)
+    assert not np.array_equal(dq0, dq1)
+    a = R.exact_rhs(q, p, 0.03)
+    b = L.exact_rhs(q, p, 0.03)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
