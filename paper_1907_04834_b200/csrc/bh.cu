@@ -320,7 +320,10 @@ __device__ __forceinline__ R warp_box_diag2(const V4<R>& x, bool valid) {
 // range's points (lane-strided, coalesced loads), each accumulates the owner's
 // terms, then a fixed butterfly reduction hands the sum to the owner. Fixed
 // assignment + fixed reduction tree keep the result deterministic.
-constexpr int kBigRange = 48;
+#ifndef GS_BH_BIG_RANGE
+#define GS_BH_BIG_RANGE 24
+#endif
+constexpr int kBigRange = GS_BH_BIG_RANGE;
 
 template <typename R>
 __device__ __forceinline__ V4<R> shfl4(const V4<R>& v, int src) {
@@ -328,41 +331,66 @@ __device__ __forceinline__ V4<R> shfl4(const V4<R>& v, int src) {
                 __shfl_sync(0xffffffffu, v.z, src), R(0));
 }
 
+#ifndef GS_BH_COOP_GL
+#define GS_BH_COOP_GL 32
+#endif
+// Lanes per owner in a cooperative sweep: the warp splits into 32/GL groups
+// that sweep up to 32/GL owners' ranges at once (stride GL), then a log2(GL)
+// butterfly inside each group and one shuffle hand each sum to its owner --
+// 6x fewer reduction shuffles per range than a whole-warp sweep for GL = 8.
 template <typename R, int MODE, bool LMD = false>
 __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc<R>& acc,
                                             uint32_t& c_dir, const V4<R>& xs, const V4<R>& px,
                                             const V4<R>& ai, const V4<R>& bi,
                                             const BhArgs<R>& a) {
-  const int lane = threadIdx.x & 31;
+  constexpr int GL = GS_BH_COOP_GL, NG = 32 / GL;
+  const int lane = threadIdx.x & 31, g = lane / GL, sub = lane % GL;
   constexpr int kAcc = MODE == kBhHess ? 12 : (MODE == kBhRhs ? (LMD ? 7 : 6) : 3);
   while (owners) {
-    const int o = __ffs(owners) - 1;
-    owners &= owners - 1;
-    const int rb = __shfl_sync(0xffffffffu, j, o), re = __shfl_sync(0xffffffffu, je, o);
-    const V4<R> oxs = shfl4<R>(xs, o), opx = shfl4<R>(px, o);
+    // this round: the first NG owners; group g serves the g-th of them
+    unsigned sel = 0;
+    int og = -1;
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      if (owners) {
+        const int b = __ffs(owners) - 1;
+        if (k == g) og = b;
+        sel |= 1u << b;
+        owners &= owners - 1;
+      }
+    }
+    const int src = og >= 0 ? og : 0;
+    const int rb = __shfl_sync(0xffffffffu, j, src), re = __shfl_sync(0xffffffffu, je, src);
+    const V4<R> oxs = shfl4<R>(xs, src), opx = shfl4<R>(px, src);
     V4<R> oai = ai, obi = bi;
-    if (MODE == kBhHess) { oai = shfl4<R>(ai, o); obi = shfl4<R>(bi, o); }
+    if (MODE == kBhHess) { oai = shfl4<R>(ai, src); obi = shfl4<R>(bi, src); }
     Acc<R> part;
 #pragma unroll
     for (int c = 0; c < 12; ++c) part.v[c] = R(0);
     const V4<R> zero = mk4<R>(0, 0, 0);
-    for (int s = rb + lane; s <= re; s += 32) {
-      const V4<R> Q = ld4(a.srec + 2 * s), P = ld4(a.srec + 2 * s + 1);
-      if (MODE == kBhHess)
-        unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
-      else
-        unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, zero, zero, a);
+    if (og >= 0) {
+      for (int s = rb + sub; s <= re; s += GL) {
+        const V4<R> Q = ld4(a.srec + 2 * s), P = ld4(a.srec + 2 * s + 1);
+        if (MODE == kBhHess)
+          unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
+        else
+          unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, zero, zero, a);
+      }
     }
+    // fixed butterfly inside each group, then owner lane <- its group's lane 0
+    const bool mine = (sel >> lane) & 1u;
+    const int from = mine ? GL * __popc(sel & ((1u << lane) - 1u)) : 0;
 #pragma unroll
     for (int c = 0; c < kAcc; ++c) {
       R v = part.v[c];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == o) acc.v[c] += v;
+      for (int off = GL / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      v = __shfl_sync(0xffffffffu, v, from);
+      if (mine) acc.v[c] += v;
     }
-    if (lane == o) {
-      c_dir += (uint32_t)(re - rb + 1);
-      j = re + 1;
+    if (mine) {
+      c_dir += (uint32_t)(je - j + 1);
+      j = je + 1;
     }
   }
 }
@@ -437,7 +465,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);  // one 32-B sector (FP32)
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
-      const int skip = code & 0x3fffffff;
+      const int skip = code & 0x1fffffff;
       const bool own = nd >= A;  // the node itself is in this block's window
       if (a.prefetch && skip < B) prefetch_l1(a.nrec + 4 * skip);
       next = skip;
@@ -461,7 +489,8 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
             have = true;
             ++c_app;
           }
-        } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
+        } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
+          // a twig (children all leaves) or every descendant opens: range
           j = max(begin, bA);
           je = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
           c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
@@ -610,7 +639,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
     const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);
     const int code = code_of(l.w);
     const int begin = code_of(h.w);
-    const int skip = code & 0x3fffffff;
+    const int skip = code & 0x1fffffff;
     const bool here = next == nd;
     if (a.prefetch && skip < B && lane_is_first_parked(here)) prefetch_l1(a.nrec + 4 * skip);
     bool have = false, ranged = false;
@@ -639,7 +668,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
             have = true;
             ++c_app;
           }
-        } else if (all_inside(l, h, x, a.thr2_in)) {  // every descendant opens: range
+        } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
+          // a twig (children all leaves) or every descendant opens: range
           ranged = true;
           rb = max(begin, bA);
           re = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
@@ -748,7 +778,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
       const int code = code_of(NL.w);
       const int begin = code_of(NH.w);
       ++c_vis;
-      next = code & 0x3fffffff;
+      next = code & 0x1fffffff;
       if (code < 0) {  // single-point leaf
         j = begin;
         je = begin;

@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 // (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
 // Compact traversal record (2 vec4 per node, one 32-B sector in FP32):
 //   {lo.xyz, code} {hi.xyz, begin} {centroid, count} {momentum sum, count},
-//   code = skip | single-point leaf << 31 | bucket leaf << 30: 64 B (FP32),
+//   code = skip | single-point leaf << 31 | bucket leaf << 30 | twig << 29
+//   (skip < 2^29: tree_build caps n accordingly): 64 B (FP32),
 //   one cache-line half, so a far node's centroid/momentum loads after the
 //   gate hit L1; the point count rides in mom.w.
 __device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
@@ -504,7 +505,7 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
                            const double4* s1, double kap, double c0x, double c0y, double c0z,
                            int scaled, V4<R>* o0, V4<R>* o1, const V4<R>* lo = nullptr,
                            const V4<R>* hi = nullptr, V4<R>* nrec = nullptr,
-                           const V4<R>* srec = nullptr) {
+                           const V4<R>* srec = nullptr, const int* nchild = nullptr) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= *mp) return;
   const int4 mi = meta[i];
@@ -513,7 +514,11 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
   const double4 a = s0[i], b = s1[i];
   if (mode == 0 && nrec) {
     const bool leaf = mi.w & 1;
-    const int code = mi.x | ((leaf && cnt == 1) ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0);
+    // twig: an internal node whose children are all leaves (subtree = itself +
+    // its children); opening it makes every point of it direct, no child gated
+    const bool twig = !leaf && nchild && mi.x - (int)i - 1 == nchild[i];
+    const int code = mi.x | ((leaf && cnt == 1) ? (int)0x80000000u : 0) |
+                     ((leaf && cnt > 1) ? 0x40000000 : 0) | (twig ? 0x20000000 : 0);
     // a single-point leaf is always direct (leaf-first, bh_kernel.cpp:40-45), so
     // its record carries the point itself -- interaction coords and momentum --
     // and the traversal needs no second, dependent load for it
@@ -712,6 +717,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // *overflow instead of writing out of bounds. No host round trip per build.
   t.m = -1;
   const int64_t cap = 4 * n + 64;
+  if (cap >= (int64_t(1) << 29)) return GS_INVALID_ARGUMENT;  // node index must fit the 29-bit skip field
   t.cap = cap;
   GS_TRY_INT(t.meta.ensure(sizeof(int4) * cap));
   GS_TRY_INT(t.parent.ensure(4 * cap));
@@ -757,9 +763,9 @@ int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t
   const int scaled = prec == kF32;
   t.kc = kc;
   if (prec == kF32)
-    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.nrec.as<float4>(), t.srec.as<float4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<float4>(), t.mom.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.nrec.as<float4>(), t.srec.as<float4>(), t.nchild.as<int>());
   else
-    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.nrec.as<double4>(), t.srec.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(0, t.meta.as<int4>(), mp, t.psum.as<double4>(), t.msum.as<double4>(), kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.cen.as<double4>(), t.mom.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.nrec.as<double4>(), t.srec.as<double4>(), t.nchild.as<int>());
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
