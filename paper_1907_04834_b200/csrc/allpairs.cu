@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "engine.h"
+#include "gs_exp.cuh"
 
 namespace gsb {
 
@@ -391,6 +392,8 @@ __global__ void __launch_bounds__(NT) k_rhs_f64(const double4* __restrict__ rec,
                                                 double inv_two_s, double4* __restrict__ part) {
   __shared__ double4 sq[kTile / 2];
   __shared__ double4 sp[kTile / 2];
+  __shared__ double stab[64];  // 2^(j/64) for exp_nonpos (published by the first tile barrier)
+  if (threadIdx.x < 64) stab[threadIdx.x] = kExp2Tab64[threadIdx.x];
   constexpr int tile = kTile / 2;
   double qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
   double ax[TPT], ay[TPT], az[TPT], bx[TPT], by[TPT], bz[TPT];
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(NT) k_rhs_f64(const double4* __restrict__ rec,
       for (int k = 0; k < TPT; ++k) {
         const double dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
         const double r2 = dx * dx + dy * dy + dz * dz;
-        const double g = exp(-r2 * inv_two_s);
+        const double g = exp_nonpos(-r2 * inv_two_s, stab);
         const double pp = px[k] * b.x + py[k] * b.y + pz[k] * b.z;
         const double c = pp * g;
         ax[k] += g * b.x; ay[k] += g * b.y; az[k] += g * b.z;
@@ -549,6 +552,8 @@ __global__ void __launch_bounds__(NT) k_hess_f64(const double4* __restrict__ rec
                                                  double4* __restrict__ part) {
   constexpr int tile = kTile / 4;
   __shared__ double4 sq[tile], sp[tile], sa[tile], sb[tile];
+  __shared__ double stab[64];  // 2^(j/64) for exp_nonpos (published by the first tile barrier)
+  if (threadIdx.x < 64) stab[threadIdx.x] = kExp2Tab64[threadIdx.x];
   double qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
   double ix[TPT], iy[TPT], iz[TPT], jx[TPT], jy[TPT], jz[TPT];
   double A[TPT][12];
@@ -584,7 +589,7 @@ __global__ void __launch_bounds__(NT) k_hess_f64(const double4* __restrict__ rec
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
         const double dx = qx[k] - Q.x, dy = qy[k] - Q.y, dz = qz[k] - Q.z;
-        const double g = exp(-(dx * dx + dy * dy + dz * dz) * inv_two_s);
+        const double g = exp_nonpos(-(dx * dx + dy * dy + dz * dz) * inv_two_s, stab);
         const double dbx = jx[k] - Be.x, dby = jy[k] - Be.y, dbz = jz[k] - Be.z;
         const double ddb = dx * dbx + dy * dby + dz * dbz;
         const double s1 = (P.x * ix[k] + P.y * iy[k] + P.z * iz[k]) +
@@ -675,6 +680,8 @@ __global__ void __launch_bounds__(NT) k_vel_f64(const double4* __restrict__ rec,
                                                 double inv_two_s, double4* __restrict__ part) {
   constexpr int tile = kTile / 2;
   __shared__ double4 sq[tile], sp[tile];
+  __shared__ double stab[64];  // 2^(j/64) for exp_nonpos (published by the first tile barrier)
+  if (threadIdx.x < 64) stab[threadIdx.x] = kExp2Tab64[threadIdx.x];
   double qx[TPT], qy[TPT], qz[TPT], ax[TPT], ay[TPT], az[TPT];
   const int tb = blockIdx.x * NT * TPT + threadIdx.x;
 #pragma unroll
@@ -701,7 +708,7 @@ __global__ void __launch_bounds__(NT) k_vel_f64(const double4* __restrict__ rec,
 #pragma unroll
       for (int k = 0; k < TPT; ++k) {
         const double dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
-        const double g = exp(-(dx * dx + dy * dy + dz * dz) * inv_two_s);
+        const double g = exp_nonpos(-(dx * dx + dy * dy + dz * dz) * inv_two_s, stab);
         ax[k] += g * b.x; ay[k] += g * b.y; az[k] += g * b.z;
       }
     }

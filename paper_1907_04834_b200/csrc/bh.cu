@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "bh.h"
+#include "gs_exp.cuh"
 
 namespace gsb {
 
@@ -139,7 +140,7 @@ __device__ __forceinline__ float kern(float dx, float dy, float dz, const BhArgs
   return ex2(nr2);
 }
 __device__ __forceinline__ double kern(double dx, double dy, double dz, const BhArgs<double>& a) {
-  return exp(-(dx * dx + dy * dy + dz * dz) * a.inv_two_s);
+  return exp_nonpos(-(dx * dx + dy * dy + dz * dz) * a.inv_two_s, kExp2Tab64);
 }
 
 __device__ __forceinline__ int code_of(float v) { return __float_as_int(v); }
