@@ -354,7 +354,8 @@ def run_ours(args):
             "steps_per_s": 2 / (ms64 / 1e3),
             "peak_dfma_lane_per_s": dfma.value,
             "frac_16dp_basis": pps64 * 16.0 / dfma.value if dfma.value else None,
-            "frac_34dp_basis_incl_exp": pps64 * 34.0 / dfma.value if dfma.value else None,
+            # + the 10-DP table-driven exp of the FP64 kernels (csrc/gs_exp.cuh)
+            "frac_26dp_basis_incl_exp": pps64 * 26.0 / dfma.value if dfma.value else None,
         }
         ms1, pr1 = timed_flow(100_000, F32, RK4, 3)
         line["n100k"] = {

@@ -19,12 +19,44 @@
 #include <cmath>
 #include <deque>
 #include <limits>
+#include <mutex>
 #include <thread>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "geoshoot_b200.h"
 
 namespace {
+
+// Contexts for the batched entry points, kept for the life of the process: a
+// context owns a stream and grown device buffers, so creating and destroying
+// one per subject per call (cudaFree synchronises the device) would cost more
+// than the evaluation itself.
+struct CtxPool {
+  std::mutex mu;
+  std::vector<std::pair<int, gs_ctx*>> idle;
+  gs_ctx* acquire(int device, gs_status* st) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      for (std::size_t k = 0; k < idle.size(); ++k)
+        if (idle[k].first == device) {
+          gs_ctx* c = idle[k].second;
+          idle.erase(idle.begin() + (std::ptrdiff_t)k);
+          return c;
+        }
+    }
+    return gs_create(device, st);
+  }
+  void release(int device, gs_ctx* c) {
+    std::lock_guard<std::mutex> g(mu);
+    idle.emplace_back(device, c);
+  }
+};
+CtxPool& ctx_pool() {
+  static CtxPool* p = new CtxPool;  // never destroyed: outlives static teardown order
+  return *p;
+}
 
 using Vec = std::vector<double>;
 constexpr double kInf = std::numeric_limits<double>::infinity();
@@ -311,7 +343,8 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
   for (int32_t b = 0; b < batch; ++b)
     pool.emplace_back([&, b] {
       gs_status cs = GS_OK;
-      gs_ctx* c = gs_create(device, &cs);
+      cudaSetDevice(device);  // pooled contexts move between host threads
+      gs_ctx* c = ctx_pool().acquire(device, &cs);
       if (!c) {
         st[b] = cs;
         return;
@@ -324,7 +357,7 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
       if (iterations) iterations[b] = it;
       if (evaluations) evaluations[b] = ev;
       if (final_total) final_total[b] = tl > 0 ? trace[6 * (size_t)(tl - 1) + 1] : 0.0;
-      gs_destroy(c);
+      ctx_pool().release(device, c);
     });
   for (auto& t : pool) t.join();
   for (gs_status s : st)
@@ -343,14 +376,15 @@ gs_status gs_evaluate_batch(int device, const gs_config* cfg, int32_t batch, con
   for (int32_t b = 0; b < batch; ++b)
     pool.emplace_back([&, b] {
       gs_status cs = GS_OK;
-      gs_ctx* c = gs_create(device, &cs);
+      cudaSetDevice(device);  // pooled contexts move between host threads
+      gs_ctx* c = ctx_pool().acquire(device, &cs);
       if (!c) {
         st[b] = cs;
         return;
       }
       st[b] = gs_evaluate(c, cfg, n[b], q0[b], p0[b], target[b], reports + b, grad_out[b],
                           stats ? stats + b : nullptr);
-      gs_destroy(c);
+      ctx_pool().release(device, c);
     });
   for (auto& t : pool) t.join();
   for (gs_status s : st)

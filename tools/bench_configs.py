@@ -40,6 +40,7 @@ def timed(fn, reps=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cpu", action="store_true", help="also time the reference CPU path")
+    ap.add_argument("--full", action="store_true", help="also run full C3 / C5 registrations")
     a = ap.parse_args()
     from paper_1907_04834_b200 import BARNES_HUT, EXACT, F32, F64, Geoshoot, ShootingConfig
     gs = Geoshoot(0)
@@ -113,6 +114,37 @@ def main():
     t = time.perf_counter() - t0
     print(json.dumps({"config": "C5", "what": "8 subjects x evaluate BH FP32 N=30k T=20 (sequential)",
                       "gpu_s": t, "per_subject_s": t / 8}), flush=True)
+    cfg5 = subj[0][2]
+    qs, ts = [q for q, _, _ in subj], [t for _, t, _ in subj]
+    ps = [np.zeros_like(q) + 1e-3 for q in qs]
+    gs.evaluate_batch(qs, ps, ts, cfg5)  # warm the per-subject contexts
+    t0 = time.perf_counter()
+    gs.evaluate_batch(qs, ps, ts, cfg5)
+    t = time.perf_counter() - t0
+    print(json.dumps({"config": "C5", "what": "8 subjects x evaluate BH FP32 N=30k T=20 "
+                      "(gs_evaluate_batch: concurrent streams)", "gpu_s": t, "per_subject_s": t / 8}),
+          flush=True)
+
+    if a.full:
+        # full registrations (BASELINE configs 3 and 5: L-BFGS)
+        q = tube(50000, seed=3)
+        tgt, _, _, _ = gs.shoot_forward(q, smooth_momenta(q, 0.01, 4), ShootingConfig(sigma=5.0, timesteps=20),
+                                        keep_trajectory=False)
+        for backend, bname in ((EXACT, "exact"), (BARNES_HUT, "BH")):
+            cfg = ShootingConfig(sigma=5.0, lambda_=100.0, timesteps=20, backend=backend, precision=F32)
+            t0 = time.perf_counter()
+            out = gs.optimize(q, tgt, cfg, max_iterations=100)
+            t = time.perf_counter() - t0
+            print(json.dumps({"config": "C3", "what": f"optimize {bname} FP32 N=50k T=20, 100 iterations",
+                              "gpu_s": t, "iterations": out["iterations"],
+                              "evaluations": out["evaluations"], "reason": out["reason"]}), flush=True)
+        t0 = time.perf_counter()
+        res = gs.optimize_batch(qs, ts, cfg5, max_iterations=50)
+        t = time.perf_counter() - t0
+        print(json.dumps({"config": "C5", "what": "8 subjects x optimize BH FP32 N=30k T=20, 50 iterations "
+                          "(gs_optimize_batch, one GPU's share of 64)", "gpu_s": t,
+                          "iterations": res["iterations"], "evaluations": res["evaluations"]}),
+              flush=True)
 
 
 if __name__ == "__main__":
