@@ -262,7 +262,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
       if (ranged) {
         c_dir += (uint32_t)(e - b + 1);
         for (int j = b; j <= e; ++j) {
-          const V4<R> Q = ld4(a.srec + 2 * j), P = ld4(a.srec + 2 * j + 1);
+          V4<R> Q, P;
+        ld8(a.srec + 2 * j, Q, P);
           if (MODE == kBhHess)
             unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
           else
@@ -371,7 +372,8 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
     const V4<R> zero = mk4<R>(0, 0, 0);
     if (og >= 0) {
       for (int s = rb + sub; s <= re; s += GL) {
-        const V4<R> Q = ld4(a.srec + 2 * s), P = ld4(a.srec + 2 * s + 1);
+        V4<R> Q, P;
+        ld8(a.srec + 2 * s, Q, P);
         if (MODE == kBhHess)
           unit<R, MODE, LMD>(part, oxs, opx, oai, obi, Q, P, ld4(a.sadj + 2 * s), ld4(a.sadj + 2 * s + 1), a);
         else
@@ -463,7 +465,8 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     R dsc = R(1);
     if (j > je && next < m) {
       const int nd = next;
-      const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);  // one 32-B sector (FP32)
+      V4<R> l, h;
+      ld8(a.nrec + 4 * nd, l, h);  // one 32-B sector (FP32)
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
       const int skip = code & 0x1fffffff;
@@ -483,8 +486,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
           je = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
         } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
           if (own) {
-            Q = ld4(a.nrec + 4 * nd + 2);
-            P = ld4(a.nrec + 4 * nd + 3);
+            ld8(a.nrec + 4 * nd + 2, Q, P);
             if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
             if (LMD) dsc = R(1) / Q.w;  // Q.w = count
             have = true;
@@ -505,8 +507,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
     if (big) coop_ranges<R, MODE, LMD>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
     if (!have && j <= je) {
-      Q = ld4(a.srec + 2 * j);
-      P = ld4(a.srec + 2 * j + 1);
+      ld8(a.srec + 2 * j, Q, P);
       if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * j); Be = ld4(a.sadj + 2 * j + 1); }
       have = true;
       ++j;
@@ -575,7 +576,8 @@ __device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Ac
       c_dir += (uint32_t)(seg_end - cursor);
 #pragma unroll 4
       for (int j = cursor; j < seg_end; ++j) {
-        const V4<R> Q = ld4(a.srec + 2 * j), P = ld4(a.srec + 2 * j + 1);
+        V4<R> Q, P;
+        ld8(a.srec + 2 * j, Q, P);
         if (MODE == kBhHess)
           unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
         else
@@ -637,7 +639,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
     if (nd == INT_MAX) break;
     ++n_iter;
     // the node's compact record, loaded by every lane (one broadcast sector)
-    const V4<R> l = ld4(a.nrec + 4 * nd), h = ld4(a.nrec + 4 * nd + 1);
+    V4<R> l, h;
+      ld8(a.nrec + 4 * nd, l, h);
     const int code = code_of(l.w);
     const int begin = code_of(h.w);
     const int skip = code & 0x1fffffff;
@@ -663,8 +666,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
           re = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
         } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
           if (own) {
-            Q = ld4(a.nrec + 4 * nd + 2);
-            P = ld4(a.nrec + 4 * nd + 3);
+            ld8(a.nrec + 4 * nd + 2, Q, P);
             if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
             have = true;
             ++c_app;

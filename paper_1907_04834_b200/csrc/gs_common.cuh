@@ -32,6 +32,18 @@ __device__ __forceinline__ double4 ld4(const double4* p) {
   const double2 a = q[0], b = q[1];
   return make_double4(a.x, a.y, b.x, b.y);
 }
+// Two consecutive 4-vectors (32 B, 32-B aligned) in one load: sm_100's 256-bit
+// LDG (LDG.E.ENL2.256) for FP32 -- one LSU instruction and one sector per lane
+// instead of two 128-bit loads; FP64 (64 B) stays at 16-B transactions.
+__device__ __forceinline__ void ld8(const float4* p, float4& a, float4& b) {
+  asm("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void ld8(const double4* p, double4& a, double4& b) {
+  a = ld4(p);
+  b = ld4(p + 1);
+}
 __device__ __forceinline__ void st4(float4* p, float4 v) { *p = v; }
 __device__ __forceinline__ void st4(double4* p, double4 v) {
   double2* q = reinterpret_cast<double2*>(p);
