@@ -321,6 +321,39 @@ def run_ours(args):
         }
         del fb
 
+    # ---- exact with the FP32 underflow cutoff (GS_FLAG_EXACT_CUTOFF, opt-in) ------
+    # The same exact sum over Morton-ordered points, skipping tile pairs whose
+    # Gaussian weights are all exactly 0 in FP32 (bit-identical to evaluating
+    # them in that order; tests/test_gpu_exact.py). Not the headline: the
+    # headline `value` evaluates all N^2 pairs.
+    if not args.no_extra and world == 1:
+        cfg_c = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=EXACT, integrator=RK4,
+                               precision=F32, exact_cutoff=True)
+        fc = gs.flow(cfg_c, N)
+        sc = torch.cuda.ExternalStream(fc.stream())
+        fc.upload(q0, p0)
+        fc.advance(max(1, args.warmup))
+        fc.sync()
+        fc.upload(q0, p0)  # time the first steps of the config-4 flow
+        fc.sync()
+        kc_ = max(1, args.steps)
+        with torch.cuda.stream(sc):
+            flush.zero_()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(sc)
+        fc.advance(kc_)
+        c1.record(sc)
+        torch.cuda.synchronize()
+        fc.sync()
+        cms = c0.elapsed_time(c1)
+        line["exact_cutoff"] = {
+            "value": kc_ / (cms / 1e3), "unit": "flow steps/s", "ms_per_step": cms / kc_,
+            "speedup_vs_all_pairs": (kc_ / (cms / 1e3)) / value,
+            "note": "exact FP32 sum in Morton order; (target group, source tile) pairs beyond "
+                    "the FP32 underflow radius of 2^-r'^2 skipped (their terms are exactly 0)",
+        }
+        del fc
+
     # ---- exact FP64 and N = 100k FP32 lines (same workload family) -------------
     if not args.no_extra and world == 1:
         def timed_flow(n, prec, integ, steps):

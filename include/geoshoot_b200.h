@@ -77,8 +77,19 @@ typedef struct gs_config {
   /* Barnes-Hut aggregate dot scale: 0 = 1 (reference default), 1 = 1/count
    * (the reference built with GEOSHOOT_BH_LITERAL_MEAN_DOT, bh_kernel.cpp:19-26). */
   int32_t literal_mean_dot;
-  int32_t reserved0;           /* must be 0 */
+  uint32_t flags;              /* gs_config_flag bits (0 = reference behaviour) */
 } gs_config;
+
+/* gs_config.flags. GS_FLAG_EXACT_CUTOFF: FP32 exact flows evaluate the
+ * all-pairs sum over Morton-ordered points and skip (target block, source
+ * tile) pairs farther apart than the FP32 underflow radius of the Gaussian
+ * (every weight there is exactly 0): bit-identical to evaluating those pairs,
+ * in the same Morton order (GS_FLAG_EXACT_MORTON, the no-skip counterpart,
+ * exists to test exactly that). Unsharded FP32 flows only; ignored otherwise. */
+typedef enum gs_config_flag {
+  GS_FLAG_EXACT_CUTOFF = 1u,
+  GS_FLAG_EXACT_MORTON = 2u
+} gs_config_flag;
 
 /* Reference defaults (core.hpp:204-213): sigma 2, lambda 1, 40 steps, exact,
  * 3 sigma; Euler; F64. */

@@ -31,6 +31,7 @@ GS_DEGENERATE = 13
 GS_F64, GS_F32 = 0, 1
 GS_EXACT, GS_BARNES_HUT = 0, 1
 GS_EULER, GS_RK4 = 0, 1
+GS_FLAG_EXACT_CUTOFF, GS_FLAG_EXACT_MORTON = 1, 2
 
 
 class gs_config(C.Structure):
@@ -43,7 +44,7 @@ class gs_config(C.Structure):
         ("integrator", C.c_int32),
         ("precision", C.c_int32),
         ("literal_mean_dot", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("flags", C.c_uint32),
     ]
 
 

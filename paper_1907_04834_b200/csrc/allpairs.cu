@@ -20,6 +20,7 @@
 // (gs_common.cuh): 3 FADD (d) + FMUL+2 FFMA (-r^2) + MUFU.EX2 (g) + FMUL+2 FFMA
 // (p_i.p_j) + FMUL (c) + 3 FFMA (sum g p_j) + 3 FFMA (sum c d) = 16 FP32 + 1 SFU.
 // No tensor cores: the contraction dimension is 3.
+#include <cstdio>
 #include <cstdlib>
 
 #include "engine.h"
@@ -271,6 +272,161 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
         o[1] = make_float4(b0[h][0], b0[h][1], b0[h][2], 0.f);
       }
     }
+  }
+}
+
+// ---- exact RHS in Morton order with the FP32 underflow cutoff -----------------
+// Same packed arithmetic as k_rhs_f32x2, but targets and sources are the
+// points in Morton (leaf) order (t.srec: interaction coordinates already
+// scaled, p), so a CTA's 1024 targets and a 256-source tile each occupy a small
+// box. If the two boxes are farther apart than cut2 (scaled units: every pair
+// has -r'^2 <= -cut2 < -150), every weight 2^(-r'^2) of the tile is exactly
+// 0 in FP32 (ex2.approx.ftz flushes below 2^-126; 2^-150 rounds to 0), so
+// every term the tile would add is +-0 and the accumulators (never -0) are
+// unchanged bit for bit: the tile is skipped. With cut2 = +inf nothing is
+// skipped; the two runs are bitwise identical (tests/test_gpu_exact.py).
+// Partials are written by point index (perm) for the usual epilogue.
+template <int TPT, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_rhs_f32x2_sorted(const float4* __restrict__ srec, const int* __restrict__ perm, int n,
+                       int chunk, const float4* __restrict__ tbox, const float4* __restrict__ sbox,
+                       float cut2, float4* __restrict__ part, unsigned long long* cnt) {
+  constexpr int TP = TPT / 2;
+  __shared__ float4 sq[kTile];
+  __shared__ float4 sp[kTile];
+  f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
+  f2 ax[TP], ay[TP], az[TP], bx[TP], by[TP], bz[TP];
+  // each warp owns 32 * TPT consecutive (Morton-adjacent) targets, so its box
+  // is the 256-point group box sbox[blockIdx.x * NT / 32 + warp] (32 * TPT = kTile)
+  static_assert(32 * TPT == kTile, "warp target group = source tile size");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tb = blockIdx.x * NT * TPT + warp * 32 * TPT + lane;
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float4 q[2], p[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * 32;
+      q[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      p[h] = q[h];
+      if (t < n) {
+        q[h] = srec[2 * t];
+        p[h] = srec[2 * t + 1];
+      }
+    }
+    qx[k] = pk2(q[0].x, q[1].x); qy[k] = pk2(q[0].y, q[1].y); qz[k] = pk2(q[0].z, q[1].z);
+    px[k] = pk2(p[0].x, p[1].x); py[k] = pk2(p[0].y, p[1].y); pz[k] = pk2(p[0].z, p[1].z);
+    ax[k] = ay[k] = az[k] = bx[k] = by[k] = bz[k] = pk2(0.f, 0.f);
+  }
+  const float4 tl = tbox[2 * blockIdx.x], th = tbox[2 * blockIdx.x + 1];
+  const int wg = blockIdx.x * (NT / 32) + warp;
+  const bool wvalid = wg * kTile < n;
+  const float4 wl = wvalid ? sbox[2 * wg] : tl, wh = wvalid ? sbox[2 * wg + 1] : th;
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTile) {
+    const float4 sl = sbox[2 * (jt / kTile)], sh = sbox[2 * (jt / kTile) + 1];
+    const float gx = fmaxf(0.f, fmaxf(sl.x - th.x, tl.x - sh.x));
+    const float gy = fmaxf(0.f, fmaxf(sl.y - th.y, tl.y - sh.y));
+    const float gz = fmaxf(0.f, fmaxf(sl.z - th.z, tl.z - sh.z));
+    if (gx * gx + gy * gy + gz * gz > cut2) continue;  // CTA-uniform: every weight is 0
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < j1) {
+        q = srec[2 * j];
+        p = srec[2 * j + 1];
+      }
+      sq[u] = q;  // zero records contribute exactly 0 (p = 0)
+      sp[u] = p;
+    }
+    __syncthreads();
+    {  // the same test on this warp's own box: warp-uniform skip of the compute
+      const float hx = fmaxf(0.f, fmaxf(sl.x - wh.x, wl.x - sh.x));
+      const float hy = fmaxf(0.f, fmaxf(sl.y - wh.y, wl.y - sh.y));
+      const float hz = fmaxf(0.f, fmaxf(sl.z - wh.z, wl.z - sh.z));
+      if (!wvalid || hx * hx + hy * hy + hz * hz > cut2) continue;
+    }
+    if (cnt && lane == 0) atomicAdd(cnt, 1ull);  // GS_EXACT_CUT_DEBUG: computed (warp, tile) pairs
+#pragma unroll 2
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u];
+      const float4 b = sp[u];
+      const f2 axx = bc2(a.x), ayy = bc2(a.y), azz = bc2(a.z);
+      const f2 bxx = bc2(b.x), byy = bc2(b.y), bzz = bc2(b.z);
+      f2 dx[TP], dy[TP], dz[TP], g[TP];
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        dx[k] = sub2(qx[k], axx);
+        dy[k] = sub2(qy[k], ayy);
+        dz[k] = sub2(qz[k], azz);
+        f2 r2 = mul2(dx[k], dx[k]);
+        r2 = fma2(dy[k], dy[k], r2);
+        r2 = fma2(dz[k], dz[k], r2);
+        g[k] = nex2x2(r2);
+      }
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        f2 pp = mul2(px[k], bxx);
+        pp = fma2(py[k], byy, pp);
+        pp = fma2(pz[k], bzz, pp);
+        const f2 c = mul2(pp, g[k]);
+        ax[k] = fma2(g[k], bxx, ax[k]);
+        ay[k] = fma2(g[k], byy, ay[k]);
+        az[k] = fma2(g[k], bzz, az[k]);
+        bx[k] = fma2(c, dx[k], bx[k]);
+        by[k] = fma2(c, dy[k], by[k]);
+        bz[k] = fma2(c, dz[k], bz[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float a0[2][3], b0[2][3];
+    up2(ax[k], a0[0][0], a0[1][0]); up2(ay[k], a0[0][1], a0[1][1]); up2(az[k], a0[0][2], a0[1][2]);
+    up2(bx[k], b0[0][0], b0[1][0]); up2(by[k], b0[0][1], b0[1][1]); up2(bz[k], b0[0][2], b0[1][2]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * 32;
+      if (t < n) {
+        float4* o = part + 2 * ((size_t)blockIdx.y * n + perm[t]);
+        o[0] = make_float4(a0[h][0], a0[h][1], a0[h][2], 0.f);
+        o[1] = make_float4(b0[h][0], b0[h][1], b0[h][2], 0.f);
+      }
+    }
+  }
+}
+
+// Tight boxes of consecutive groups of `group` points of srec (lo, hi per group).
+__global__ void __launch_bounds__(256) k_group_boxes(const float4* __restrict__ srec, int n,
+                                                     int group, float4* __restrict__ box) {
+  __shared__ float red[6][8];
+  const int g0 = blockIdx.x * group, g1 = min(n, g0 + group);
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int j = g0 + threadIdx.x; j < g1; j += 256) {
+    const float4 q = srec[2 * j];
+    lo[0] = fminf(lo[0], q.x); lo[1] = fminf(lo[1], q.y); lo[2] = fminf(lo[2], q.z);
+    hi[0] = fmaxf(hi[0], q.x); hi[1] = fmaxf(hi[1], q.y); hi[2] = fmaxf(hi[2], q.z);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int a = 0; a < 3; ++a) { red[a][w] = lo[a]; red[3 + a][w] = hi[a]; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int v = 1; v < 8; ++v)
+      for (int a = 0; a < 3; ++a) {
+        red[a][0] = fminf(red[a][0], red[a][v]);
+        red[3 + a][0] = fmaxf(red[3 + a][0], red[3 + a][v]);
+      }
+    box[2 * blockIdx.x] = make_float4(red[0][0], red[1][0], red[2][0], 0.f);
+    box[2 * blockIdx.x + 1] = make_float4(red[3][0], red[4][0], red[5][0], 0.f);
   }
 }
 
@@ -827,6 +983,43 @@ static void launch_rhs_f32x2(const Plan& pl, cudaStream_t st, const float4* rec,
 template <int TPT, int MINB>
 static int occ_rhs_f32x2() {
   return occupancy(k_rhs_f32x2<TPT, kNT, MINB>, kNT);
+}
+
+// Exact FP32 RHS over Morton-ordered points (morton_order) with the
+// underflow cutoff cut2 (scaled units; +inf: no tile skipped). Returns S.
+int rhs_sorted_partials(const Device& dev, const void* srec, const int* perm, int n,
+                        void* part, int part_cap_chunks, DBuf& boxes, float cut2,
+                        cudaStream_t st) {
+  // one warp per CTA: the CTA's 256 targets are one Morton group, so a tile is
+  // skipped (load and compute) at the granularity of the group boxes
+  constexpr int TPT = 8, NT = 32, MINB = 12;
+  const int tgt_group = NT * TPT;
+  const int nbt = (n + tgt_group - 1) / tgt_group, nbs = (n + kTile - 1) / kTile;
+  GS_TRY_INT(boxes.ensure(sizeof(float4) * 2 * (size_t)(nbt + nbs)));
+  float4* tbox = boxes.as<float4>();
+  float4* sbox = tbox + 2 * nbt;
+  k_group_boxes<<<nbt, 256, 0, st>>>((const float4*)srec, n, tgt_group, tbox);
+  k_group_boxes<<<nbs, 256, 0, st>>>((const float4*)srec, n, kTile, sbox);
+  static int occ = occupancy(k_rhs_f32x2_sorted<TPT, NT, MINB>, NT);
+  const int tp[] = {TPT};
+  Plan pl = plan(n, n, NT, tp, 1, kTile, occ, dev.sms);
+  if (pl.S > part_cap_chunks) return -1;
+  static const bool dbg = std::getenv("GS_EXACT_CUT_DEBUG") != nullptr;
+  static unsigned long long* cnt = nullptr;
+  if (dbg && !cnt) cudaMalloc(&cnt, 8);
+  if (dbg) cudaMemsetAsync(cnt, 0, 8, st);
+  k_rhs_f32x2_sorted<TPT, NT, MINB><<<pl.grid, NT, 0, st>>>(
+      (const float4*)srec, perm, n, pl.chunk, tbox, sbox, cut2, (float4*)part, dbg ? cnt : nullptr);
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  if (dbg) {
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double all = (double)((n + 255) / 256) * ((n + 255) / 256);
+    std::fprintf(stderr, "[exact cut] S %d computed warp-tile pairs %llu of %.0f (%.2f %%)\n", pl.S, h,
+                 all, 100.0 * h / all);
+  }
+  return pl.S;
 }
 
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,

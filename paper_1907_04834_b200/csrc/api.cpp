@@ -80,7 +80,7 @@ gs_config to_c(const ShootingConfig& c) {
   g.integrator = c.integrator == Integrator::RK4 ? GS_RK4 : GS_EULER;
   g.precision = prec_of(c.precision);
   g.literal_mean_dot = c.literal_mean_dot ? 1 : 0;
-  g.reserved0 = 0;
+  g.flags = c.exact_underflow_cutoff ? GS_FLAG_EXACT_CUTOFF : 0u;
   return g;
 }
 

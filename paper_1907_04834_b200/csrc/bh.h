@@ -54,6 +54,10 @@ struct DevTree {
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
                DevTree& t, cudaStream_t st, const double* root_box = nullptr,
                int* overflow = nullptr);
+// Morton (leaf) order of the points only: t.perm, t.srec (FP32 interaction
+// coordinates, p) -- the locality order of the exact path's underflow cutoff.
+int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
+                 DevTree& t, cudaStream_t st);
 // exact node count (host round trip on first call after a build)
 int64_t tree_node_count(DevTree& t, cudaStream_t st);
 // (re)writes the interaction coordinates (FP32: scaled by kc.kappa) and centroids

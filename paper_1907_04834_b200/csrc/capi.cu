@@ -75,6 +75,7 @@ struct gs_flow {
   int64_t n = 0, shard_begin = 0, shard_count = 0;
   KernelConsts kc{};
   DBuf rec, rec_next, y, ks, part, dhdp0, epart, flags, scal;
+  DBuf boxes;  // exact underflow cutoff: target-block and source-tile boxes
   int steps_done = 0;
   int64_t launches = 0;
   bool want_energy = false;
@@ -118,7 +119,7 @@ gs_config gs_default_config(void) {
   c.integrator = GS_EULER;
   c.precision = GS_F64;
   c.literal_mean_dot = 0;
-  c.reserved0 = 0;
+  c.flags = 0;
   return c;
 }
 
@@ -249,6 +250,34 @@ double fwd_cq(int prec, const KernelConsts& kc) {
   return prec == kF32 ? -kc.two_over_s / kc.kappa : -kc.two_over_s;
 }
 
+// FP32 underflow radius of the scaled Gaussian 2^(-r'^2): beyond r'^2 = 150
+// every weight is exactly 0; 160 leaves margin for the FP32 box arithmetic.
+constexpr float kExactCut2 = 160.0f;
+
+// one exact FP32 RHS over Morton-ordered points (GS_FLAG_EXACT_CUTOFF /
+// GS_FLAG_EXACT_MORTON) for all n targets + its epilogue
+int exact_sorted_stage(const Device& dev, const KernelConsts& kc, const void* rec, int64_t n,
+                       DevTree& t, DBuf& part, DBuf& boxes, bool skip, FwdEpi e,
+                       cudaStream_t st, int64_t* launches, int* energy_blocks) {
+  GS_TRY(part.ensure((size_t)kMaxChunks * 2 * sizeof(float4) * std::max<int64_t>(n, 1)));
+  GS_TRY(morton_order(dev, kF32, kc, rec, n, t, st));
+  kt_mark(0, st);
+  const int S = rhs_sorted_partials(dev, t.srec.ptr, t.perm.as<int>(), (int)n, part.ptr,
+                                    kMaxChunks, boxes, skip ? kExactCut2 : INFINITY, st);
+  kt_mark(0, st);
+  if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
+  GS_CUDA_OK(cudaGetLastError());
+  e.S = S;
+  e.part = part.ptr;
+  e.n_tgt = (int)n;
+  e.tgt_begin = 0;
+  e.cp = 2.0;
+  e.cq = fwd_cq(kF32, kc);
+  GS_TRY(fwd_epilogue(kF32, e, st, energy_blocks));
+  if (launches) *launches += 33;  // Morton order (~28) + boxes (2) + RHS + epilogue
+  return GS_OK;
+}
+
 // one exact RHS over all n sources for targets [tb, tb + nt) + its epilogue
 int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
                 int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
@@ -318,7 +347,16 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
     explicit Install(KTimer* t) : prev(g_ktimer) { g_ktimer = t; }
     ~Install() { g_ktimer = prev; }
   } install(f->timer);
-  if (f->cfg.backend == GS_EXACT) {
+  const bool sorted = f->cfg.backend == GS_EXACT && f->prec == kF32 &&
+                      (f->cfg.flags & (GS_FLAG_EXACT_CUTOFF | GS_FLAG_EXACT_MORTON)) &&
+                      f->shard_begin == 0 && f->shard_count == f->n;
+  if (sorted) {
+    GS_TRY(exact_sorted_stage(c->dev, f->kc, rec_in, f->n, f->bh.cur, f->part, f->boxes,
+                              (f->cfg.flags & GS_FLAG_EXACT_CUTOFF) != 0, e, st, &f->launches,
+                              &blocks));
+    f->stats.direct_interactions += (uint64_t)f->n * (uint64_t)f->shard_count;
+    f->stats.traversal_queries += (uint64_t)f->shard_count;
+  } else if (f->cfg.backend == GS_EXACT) {
     GS_TRY(exact_stage(c->dev, f->prec, f->kc, rec_in, f->n, f->shard_begin, f->shard_count,
                        f->part, e, st, &f->launches, &blocks));
     f->stats.direct_interactions += (uint64_t)f->n * (uint64_t)f->shard_count;

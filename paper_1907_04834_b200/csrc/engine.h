@@ -90,6 +90,11 @@ inline void kt_mark(int ch, cudaStream_t st) {
 
 inline size_t vec_bytes(int prec) { return prec == kF32 ? sizeof(float4) : sizeof(double4); }
 
+// ---- exact RHS in Morton order with the FP32 underflow cutoff (allpairs.cu)
+int rhs_sorted_partials(const Device& dev, const void* srec, const int* perm, int n,
+                        void* part, int part_cap_chunks, DBuf& boxes, float cut2,
+                        cudaStream_t st);
+
 // ---- all-pairs (allpairs.cu); return the number of source chunks S used,
 // ---- or -1 if S would exceed part_cap_chunks.
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,

@@ -757,6 +757,60 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   return fs;
 }
 
+// Points in Morton (leaf) order for locality only -- the exact path's
+// underflow cutoff (allpairs.cu): bbox, 63-bit keys, an 8-pass index-stable
+// radix sort on them, then the leaf-order copy of the records (t.srec: FP32
+// interaction coordinates, p) and t.perm. No topology, no aggregates.
+int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
+                 DevTree& t, cudaStream_t st) {
+  t.prec = prec;
+  t.n = n;
+  t.kc = kc;
+  const size_t vb = vec_bytes(prec);
+  GS_TRY_INT(t.key_hi.ensure(8 * n));
+  GS_TRY_INT(t.key_lo.ensure(8 * n));
+  GS_TRY_INT(t.skey_hi.ensure(8 * n));
+  GS_TRY_INT(t.perm.ensure(4 * n));
+  GS_TRY_INT(t.tmp_k.ensure(8 * n));
+  GS_TRY_INT(t.tmp_v.ensure(4 * n));
+  GS_TRY_INT(t.root.ensure(8 * 8));
+  GS_TRY_INT(t.srec.ensure(2 * vb * n));
+  GS_TRY_INT(t.squ.ensure(vb * n));
+  const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
+  GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
+  if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
+  else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
+  k_bbox_final<<<1, kNT, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+  const int nb = nblocks(n, kNT);
+  if (prec == kF32)
+    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+  else
+    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+  const int ipt = n >= (1 << 19) ? 8 : 4;
+  const int ntiles = nblocks(n, kRsNT * ipt);
+  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
+  const uint64_t* ka = t.key_hi.as<uint64_t>();
+  const int* va = nullptr;
+  for (int p = 0; p < 8; ++p) {  // (key_hi, index) -> (tmp_k, tmp_v) -> (skey_hi, perm) -> ...
+    uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
+    int* vb2 = (p & 1) ? t.perm.as<int>() : t.tmp_v.as<int>();
+    unsigned* gh = t.hist.as<unsigned>();
+    if (ipt == 8) k_rs_hist<8><<<ntiles, kRsNT, 0, st>>>(ka, n, 8 * p, gh, ntiles);
+    else k_rs_hist<4><<<ntiles, kRsNT, 0, st>>>(ka, n, 8 * p, gh, ntiles);
+    k_rs_digit_scan<<<32, 256, 0, st>>>(gh, ntiles);
+    if (ipt == 8) k_rs_scatter<8><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, gh, ntiles);
+    else k_rs_scatter<4><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, gh, ntiles);
+    ka = kb;
+    va = vb2;
+  }
+  if (prec == kF32)
+    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>());
+  else
+    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>());
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
 int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st) {
   const int* mp = t.first.as<int>() + t.n;
   const int mb = nblocks(t.cap, kNT);

@@ -136,6 +136,8 @@ class ShootingConfig:
     integrator: int = EULER
     precision: int = F64
     literal_mean_dot: bool = False  # GEOSHOOT_BH_LITERAL_MEAN_DOT (bh_kernel.cpp:19-26)
+    exact_cutoff: bool = False  # FP32 exact flows: skip tile pairs whose weights underflow to 0
+    flags: int = 0              # raw gs_config.flags bits (GS_FLAG_*)
 
     def opening_threshold(self) -> float:
         return self.threshold_multiplier * self.sigma
@@ -143,7 +145,8 @@ class ShootingConfig:
     def c(self) -> L.gs_config:
         return L.gs_config(self.sigma, self.lambda_, self.timesteps, self.backend,
                            self.threshold_multiplier, self.integrator, self.precision,
-                           1 if self.literal_mean_dot else 0, 0)
+                           1 if self.literal_mean_dot else 0,
+                           self.flags | (L.GS_FLAG_EXACT_CUTOFF if self.exact_cutoff else 0))
 
 
 def _arr(a, name="array") -> np.ndarray:

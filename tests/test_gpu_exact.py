@@ -240,3 +240,38 @@ def test_bitwise_determinism(gs):
         b = gs.evaluate(q, p, t, cfg)
         assert a.report["total"] == b.report["total"]
         assert np.array_equal(a.gradient, b.gradient)
+
+
+# ---- Morton-ordered exact path with the FP32 underflow cutoff ------------------
+def _flow_final(gs, q, p, cfg, steps):
+    f = gs.flow(cfg, len(q))
+    f.upload(q, p)
+    f.advance(steps)
+    f.sync()
+    return f.download()
+
+
+@pytest.mark.parametrize("n,sigma", [(4000, 0.01), (200_000, 0.0131)])
+def test_exact_cutoff_is_bitwise_the_unskipped_sum(gs, n, sigma):
+    """Skipping tiles beyond the FP32 underflow radius changes no bit: the
+    same Morton-ordered sum without skipping gives identical states."""
+    from paper_1907_04834_b200._lib import GS_FLAG_EXACT_MORTON
+    rng = np.random.default_rng(n)
+    q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+    base = dict(sigma=sigma, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    a = _flow_final(gs, q, p, ShootingConfig(exact_cutoff=True, **base), 2)
+    b = _flow_final(gs, q, p, ShootingConfig(flags=GS_FLAG_EXACT_MORTON, **base), 2)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    c = _flow_final(gs, q, p, ShootingConfig(**base), 2)  # index-order sum: rounding only
+    assert rel_l2(a[0], c[0]) < 1e-6 and rel_l2(a[1], c[1]) < 1e-5
+
+
+def test_exact_cutoff_matches_reference(gs, port):
+    n, sigma = 3000, 0.02
+    q, p = f32(uniform(n, 1.0, 531)), f32(sym_uniform(n, 1e-3, 532))
+    cfg = ShootingConfig(sigma=sigma, timesteps=4, backend=EXACT, integrator=RK4, precision=F32,
+                         exact_cutoff=True)
+    fq, fp, e, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    w = port.shoot_forward(q, p, sigma, 4, integrator=1, keep_traj=False)
+    assert rel_l2(fq, w["q"]) < F32_TRAJ_TOL and rel_l2(fp, w["p"]) < F32_TRAJ_TOL
+    assert e == pytest.approx(w["energy"], rel=1e-5)
