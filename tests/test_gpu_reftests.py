@@ -1,0 +1,70 @@
+"""The reference's own hot-path unit suites run against the B200 library.
+
+oracle/Makefile (target `reftests`) compiles proj/tests/test_{core,
+kernel_exact,octree,bh_kernel,shooting}.cpp BY PATH with the doctest-compatible
+harness written here (tests/cpp/doctest_shim/doctest.h) against the B200
+library's C++ API (include/geoshoot/*.hpp + libgeoshoot_b200.so): the suites
+compile and link unchanged, i.e. the API is a drop-in, and every check passes
+except one documented class: bitwise equality of FP64 node sums (Sum q, Sum p,
+Sum alpha, Sum beta) with a running sum in point-index order. The reference
+accumulates node statistics sequentially in insertion order
+(octree.cpp:47-57); the B200 build sums each node from its children in child
+order in parallel -- equal to 1e-12 relative, the tolerance the reference
+itself applies when the order changes (test_octree.cpp:227-268, which passes
+here), and checked at that tolerance in tests/test_gpu_bh.py.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+RT = os.path.join(ROOT, "oracle", "_ref", "reftests")
+SUITES = ["test_core", "test_kernel_exact", "test_octree", "test_bh_kernel", "test_shooting"]
+
+# (suite, source line, failed expression): the summation-order class above
+ALLOWED = {
+    ("test_octree", 36, "nd.position_sum == pos_sum"),
+    ("test_octree", 37, "nd.momentum_sum == mom_sum"),
+    ("test_octree", 182, "tree.node(k).alpha_sum == a"),
+    ("test_octree", 183, "tree.node(k).beta_sum == b"),
+}
+
+
+def run_suite(name):
+    exe = os.path.join(RT, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (make -C oracle reftests where /root/reference exists)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    summary = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed \| checks: (\d+) \| (\d+) failed",
+                        r.stdout)
+    assert summary, r.stdout + r.stderr
+    fails = re.findall(r"/(test_\w+)\.cpp:(\d+): FAILED: (.*)", r.stderr)
+    return r.returncode, [int(x) for x in summary.groups()], [(s, int(l), e.strip()) for s, l, e in fails]
+
+
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_reference(suite):
+    """Harness check: every case of the suite passes against the reference itself."""
+    rc, (cases, passed, failed, checks, fchecks), fails = run_suite("ref_" + suite)
+    assert rc == 0 and failed == 0 and fchecks == 0 and passed == cases > 0, fails
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_b200(suite):
+    rc, (cases, passed, failed, checks, fchecks), fails = run_suite("b200_" + suite)
+    unexpected = [f for f in fails if f not in ALLOWED]
+    assert not unexpected, unexpected
+    if suite != "test_octree":
+        assert rc == 0 and passed == cases > 0
+    else:  # only the three cases holding the index-order bitwise sum checks
+        assert failed <= 3 and passed >= cases - 3
+    assert checks > 0
+
+
+def test_reference_core_suite_on_b200_host():
+    """test_core needs no device (config validation, value types): runs here too."""
+    rc, (cases, passed, failed, _, _), fails = run_suite("b200_test_core")
+    assert rc == 0 and passed == cases and not fails
