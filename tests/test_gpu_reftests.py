@@ -68,3 +68,37 @@ def test_reference_core_suite_on_b200_host():
     """test_core needs no device (config validation, value types): runs here too."""
     rc, (cases, passed, failed, _, _), fails = run_suite("b200_test_core")
     assert rc == 0 and passed == cases and not fails
+
+
+# The reference's acceptance program (acceptance_main.cpp) linked against the
+# B200 library. Correctness criteria must pass: 1 (FD gradient), 2 (BH at
+# infinite threshold == exact), 7 (first-order drift), 9 (positive Jacobians of
+# the warp), 10 (Procrustes). Not asserted, with the reason:
+#   3 -- the residual gap of two 60-iteration registrations; the reference
+#        itself fails it here (gap 0.51, tests/golden/acceptance_c3_reference.json,
+#        tools/ref_acceptance_c3.py);
+#   4, 5, 6 -- single-thread CPU speed ratios (BH faster/slower than exact,
+#        x4 per doubling): timing properties of the CPU algorithm, not of the
+#        results; on a B200 exact is faster than BH at these sizes;
+#   8 -- bitwise node statistics in insertion order (see ALLOWED above).
+REQUIRED_CRITERIA = {1, 2, 7, 9, 10}
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_program_on_b200():
+    exe = os.path.join(RT, "b200_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("b200_acceptance not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
+    got = {int(c): s for s, c in re.findall(r"\[(PASS|FAIL)\] criterion\s+(\d+):", r.stdout)}
+    assert len(got) == 10, r.stdout + r.stderr
+    failed = {c for c, s in got.items() if s != "PASS"}
+    assert not (failed & REQUIRED_CRITERIA), r.stdout
+
+
+def test_reference_fails_its_own_criterion_3():
+    """The committed run of criterion 3's computation on the reference itself."""
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "acceptance_c3_reference.json")) as f:
+        d = json.load(f)
+    assert d["gap"] > 0.05 and not d["criterion3_pass"]
