@@ -18,6 +18,7 @@
 #include "geoshoot/pipeline.hpp"
 #include "geoshoot/shooting.hpp"
 #include "geoshoot_b200.h"
+#include "lbfgs.h"
 
 namespace geoshoot {
 namespace {
@@ -553,20 +554,45 @@ void OptimizationTrace::write_csv(std::ostream& os) const {
   }
 }
 
+namespace {
+gs_opt_config to_c(const OptimizerConfig& o) {
+  gs_opt_config oc = gs_default_opt_config();
+  oc.max_iterations = o.max_iterations;
+  oc.memory = o.memory;
+  oc.gradient_tolerance = o.gradient_tolerance;
+  oc.relative_objective_tolerance = o.relative_objective_tolerance;
+  oc.sufficient_decrease = o.line_search.sufficient_decrease;
+  oc.curvature = o.line_search.curvature;
+  oc.max_trials = o.line_search.max_trials;
+  return oc;
+}
+}  // namespace
+
+MinimizeResult minimize(const ObjectiveFn& objective, std::vector<double> x0,
+                        const OptimizerConfig& config, const IterateCallback& on_iterate) {
+  gsb::LbfgsResult r;
+  try {
+    r = gsb::lbfgs_minimize(objective, std::move(x0), to_c(config), on_iterate);
+  } catch (const gsb::NonFiniteStart&) {
+    throw NonFiniteObjectiveAtStart("objective is non-finite at the start point");
+  }
+  MinimizeResult out;
+  out.x = std::move(r.x);
+  out.f = r.f;
+  out.grad_inf = r.grad_inf;
+  out.reason = static_cast<TerminationReason>(r.reason);
+  out.iterations = r.iterations;
+  out.evaluations = r.evaluations;
+  return out;
+}
+
 std::pair<MomentumSet, OptimizationTrace> optimize(const PointSet& q0, const PointSet& target,
                                                    const ShootingConfig& config,
                                                    EvalStats* eval_stats, int) {
   validate_config(config);
   require_aligned(q0.size(), target.size(), "optimize");
   const gs_config c = to_c(config);
-  gs_opt_config oc = gs_default_opt_config();
-  oc.max_iterations = config.optimizer.max_iterations;
-  oc.memory = config.optimizer.memory;
-  oc.gradient_tolerance = config.optimizer.gradient_tolerance;
-  oc.relative_objective_tolerance = config.optimizer.relative_objective_tolerance;
-  oc.sufficient_decrease = config.optimizer.line_search.sufficient_decrease;
-  oc.curvature = config.optimizer.line_search.curvature;
-  oc.max_trials = config.optimizer.line_search.max_trials;
+  const gs_opt_config oc = to_c(config.optimizer);
   const std::size_t n = q0.size();
   std::vector<Vec3> p(n);
   std::vector<double> trace(6 * (std::size_t)(oc.max_iterations + 1));

@@ -20,12 +20,14 @@
 #include <deque>
 #include <limits>
 #include <mutex>
+#include <new>
 #include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "geoshoot_b200.h"
+#include "lbfgs.h"
 
 namespace {
 
@@ -99,19 +101,32 @@ Vec direction(const Vec& g, const std::deque<Pair>& hist) {
   return d;
 }
 
-struct Objective {
+// Counts evaluations around any objective (minimize's Evaluator).
+struct Eval {
+  const gsb::LbfgsObjective& fn;
+  int evaluations = 0;
+  double operator()(const Vec& x, Vec& g) {
+    ++evaluations;
+    return fn(x, g);
+  }
+};
+
+// A device failure inside the objective aborts the whole optimization.
+struct DeviceFailure {
+  gs_status status;
+};
+
+// The registration objective: one device evaluate() per call.
+struct DeviceObjective {
   gs_ctx* ctx;
   const gs_config* cfg;
   int64_t n;
   const double* q0;
   const double* target;
-  int evaluations = 0;
   gs_report last{};
   gs_stats stats{};
-  gs_status hard_error = GS_OK;  // a device failure aborts the optimization
 
   double operator()(const Vec& x, Vec& g) {
-    ++evaluations;
     g.assign(x.size(), 0.0);
     for (double v : x)
       if (!std::isfinite(v)) return kInf;  // MomentumSet rejects it (invalid_argument)
@@ -119,10 +134,7 @@ struct Objective {
     gs_stats s{};
     const gs_status st = gs_evaluate(ctx, cfg, n, q0, x.data(), target, &r, g.data(), &s);
     if (st == GS_NONFINITE || st == GS_INVALID_ARGUMENT) return kInf;
-    if (st != GS_OK) {
-      hard_error = st;
-      return kInf;
-    }
+    if (st != GS_OK) throw DeviceFailure{st};
     last = r;
     stats.direct_interactions += s.direct_interactions;
     stats.approximated_interactions += s.approximated_interactions;
@@ -141,7 +153,7 @@ struct Step {
   Vec x, g;
 };
 
-Step wolfe(Objective& F, const Vec& x0, double f0, const Vec& g0, const Vec& d, double a0,
+Step wolfe(Eval& F, const Vec& x0, double f0, const Vec& g0, const Vec& d, double a0,
            const gs_opt_config& c) {
   Step out;
   const double slope0 = vdot(g0, d);
@@ -165,7 +177,6 @@ Step wolfe(Objective& F, const Vec& x0, double f0, const Vec& g0, const Vec& d, 
     Vec x = point(at);
     const double fa = F(x, g);
     ++trials;
-    if (F.hard_error != GS_OK) return out;
     const double slope = std::isfinite(fa) ? vdot(g, d) : 0.0;
     if (!bracketed) {
       if (!std::isfinite(fa) || !decreases(at, fa) || (trials > 1 && fa >= f_prev)) {
@@ -236,6 +247,85 @@ gs_opt_config gs_default_opt_config(void) {
   return c;
 }
 
+}  // extern "C"
+
+namespace gsb {
+
+// minimize(), optimizer.cpp:215-299: L-BFGS from x0 with the strong-Wolfe
+// search above; the same termination order and history rules.
+LbfgsResult lbfgs_minimize(const LbfgsObjective& objective, std::vector<double> x0,
+                           const gs_opt_config& oc, const LbfgsCallback& on_iterate) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  Eval F{objective};
+  LbfgsResult res;
+  res.x = std::move(x0);
+  Vec g;
+  res.f = F(res.x, g);
+  if (!std::isfinite(res.f)) throw NonFiniteStart{};
+  res.grad_inf = vmax_abs(g);
+  if (on_iterate) on_iterate(0, res.f, res.grad_inf, ms());
+  std::deque<Pair> hist;
+  res.reason = -1;
+  for (int it = 1; it <= oc.max_iterations; ++it) {
+    if (res.grad_inf <= oc.gradient_tolerance) {
+      res.reason = GS_TERM_GRADIENT_TOLERANCE;
+      break;
+    }
+    Vec d = direction(g, hist);
+    if (vdot(g, d) >= 0.0) {  // stale curvature: restart from steepest descent
+      hist.clear();
+      d = g;
+      for (double& v : d) v = -v;
+    }
+    const double a0 = hist.empty() ? 1.0 / std::max(1.0, res.grad_inf) : 1.0;
+    Step s = wolfe(F, res.x, res.f, g, d, a0, oc);
+    if (!s.ok) {
+      res.reason = GS_TERM_LINE_SEARCH_FAILURE;
+      break;
+    }
+    if (!std::isfinite(vmax_abs(s.g))) {
+      res.reason = GS_TERM_NON_FINITE;
+      break;
+    }
+    Pair pr;
+    pr.s.resize(res.x.size());
+    pr.y.resize(res.x.size());
+    for (std::size_t k = 0; k < res.x.size(); ++k) {
+      pr.s[k] = s.x[k] - res.x[k];
+      pr.y[k] = s.g[k] - g[k];
+    }
+    const double sy = vdot(pr.s, pr.y);
+    if (sy > 1e-10 * std::sqrt(vdot(pr.s, pr.s)) * std::sqrt(vdot(pr.y, pr.y))) {
+      pr.rho = 1.0 / sy;
+      hist.push_back(std::move(pr));
+      if ((int)hist.size() > oc.memory) hist.pop_front();
+    }
+    const double f_prev = res.f;
+    res.x = std::move(s.x);
+    res.f = s.f;
+    g = std::move(s.g);
+    res.grad_inf = vmax_abs(g);
+    res.iterations = it;
+    if (on_iterate) on_iterate(it, res.f, res.grad_inf, ms());
+    if (std::abs(f_prev - res.f) <= oc.relative_objective_tolerance * std::max(1.0, std::abs(res.f))) {
+      res.reason = GS_TERM_OBJECTIVE_TOLERANCE;
+      break;
+    }
+  }
+  if (res.reason < 0)
+    res.reason = res.grad_inf <= oc.gradient_tolerance ? GS_TERM_GRADIENT_TOLERANCE
+                                                       : GS_TERM_MAX_ITERATIONS;
+  res.evaluations = F.evaluations;
+  return res;
+}
+
+}  // namespace gsb
+
+extern "C" {
+
 gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc, int64_t n,
                       const double* q0, const double* target, double* p_out, int32_t* reason,
                       int32_t* iterations, int32_t* evaluations, double* trace,
@@ -243,13 +333,10 @@ gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc
   if (!ctx || !cfg || !oc || !q0 || !target || !p_out) return GS_INVALID_ARGUMENT;
   gs_status st = gs_validate_config(cfg, nullptr);
   if (st != GS_OK) return st;
-  const auto t0 = std::chrono::steady_clock::now();
-  auto ms = [&] {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  };
-  Objective F{ctx, cfg, n, q0, target};
+  DeviceObjective F{ctx, cfg, n, q0, target};
   int32_t tl = 0;
-  auto record = [&](int it, double ginf) {  // trace row: iter,total,energy,attachment,grad_inf,wall_ms
+  // trace row per iterate: iter,total,energy,attachment,grad_inf,wall_ms (optimizer.cpp:204-213)
+  auto record = [&](int it, double, double ginf, double wall_ms) {
     if (!trace) return;
     double* r = trace + 6 * (size_t)tl;
     r[0] = it;
@@ -257,74 +344,24 @@ gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc
     r[2] = F.last.energy;
     r[3] = F.last.attachment;
     r[4] = ginf;
-    r[5] = ms();
+    r[5] = wall_ms;
     ++tl;
   };
-
-  Vec x((size_t)3 * n, 0.0), g;
-  double f = F(x, g);
-  if (F.hard_error != GS_OK) return F.hard_error;
-  if (!std::isfinite(f)) return GS_NONFINITE;  // NonFiniteObjectiveAtStart
-  double ginf = vmax_abs(g);
-  record(0, ginf);
-  int32_t why = GS_TERM_MAX_ITERATIONS, iters = 0;
-  std::deque<Pair> hist;
-  bool done = false;
-  for (int it = 1; it <= oc->max_iterations && !done; ++it) {
-    if (ginf <= oc->gradient_tolerance) {
-      why = GS_TERM_GRADIENT_TOLERANCE;
-      done = true;
-      break;
-    }
-    Vec d = direction(g, hist);
-    if (vdot(g, d) >= 0.0) {
-      hist.clear();
-      d = g;
-      for (double& v : d) v = -v;
-    }
-    const double a0 = hist.empty() ? 1.0 / std::max(1.0, ginf) : 1.0;
-    Step s = wolfe(F, x, f, g, d, a0, *oc);
-    if (F.hard_error != GS_OK) return F.hard_error;
-    if (!s.ok) {
-      why = GS_TERM_LINE_SEARCH_FAILURE;
-      done = true;
-      break;
-    }
-    if (!std::isfinite(vmax_abs(s.g))) {
-      why = GS_TERM_NON_FINITE;
-      done = true;
-      break;
-    }
-    Pair pr;
-    pr.s.resize(x.size());
-    pr.y.resize(x.size());
-    for (std::size_t k = 0; k < x.size(); ++k) {
-      pr.s[k] = s.x[k] - x[k];
-      pr.y[k] = s.g[k] - g[k];
-    }
-    const double sy = vdot(pr.s, pr.y);
-    if (sy > 1e-10 * std::sqrt(vdot(pr.s, pr.s)) * std::sqrt(vdot(pr.y, pr.y))) {
-      pr.rho = 1.0 / sy;
-      hist.push_back(std::move(pr));
-      if ((int)hist.size() > oc->memory) hist.pop_front();
-    }
-    const double f_prev = f;
-    x = std::move(s.x);
-    f = s.f;
-    g = std::move(s.g);
-    ginf = vmax_abs(g);
-    iters = it;
-    record(it, ginf);
-    if (std::abs(f_prev - f) <= oc->relative_objective_tolerance * std::max(1.0, std::abs(f))) {
-      why = GS_TERM_OBJECTIVE_TOLERANCE;
-      done = true;
-    }
+  gsb::LbfgsResult res;
+  try {
+    res = gsb::lbfgs_minimize([&](const Vec& x, Vec& g) { return F(x, g); }, Vec((size_t)3 * n, 0.0),
+                              *oc, record);
+  } catch (const DeviceFailure& e) {
+    return e.status;
+  } catch (const gsb::NonFiniteStart&) {
+    return GS_NONFINITE;  // NonFiniteObjectiveAtStart
+  } catch (const std::bad_alloc&) {
+    return GS_INTERNAL;
   }
-  if (!done) why = ginf <= oc->gradient_tolerance ? GS_TERM_GRADIENT_TOLERANCE : GS_TERM_MAX_ITERATIONS;
-  std::copy(x.begin(), x.end(), p_out);
-  if (reason) *reason = why;
-  if (iterations) *iterations = iters;
-  if (evaluations) *evaluations = F.evaluations;
+  std::copy(res.x.begin(), res.x.end(), p_out);
+  if (reason) *reason = res.reason;
+  if (iterations) *iterations = res.iterations;
+  if (evaluations) *evaluations = res.evaluations;
   if (trace_len) *trace_len = tl;
   if (stats) *stats = F.stats;
   return GS_OK;

@@ -1,4 +1,4 @@
-"""The reference's own hot-path unit suites run against the B200 library.
+"""The reference's own unit suites run against the B200 library.
 
 oracle/Makefile (target `reftests`) compiles proj/tests/test_{core,
 kernel_exact,octree,bh_kernel,shooting}.cpp BY PATH with the doctest-compatible
@@ -21,7 +21,16 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 RT = os.path.join(ROOT, "oracle", "_ref", "reftests")
-SUITES = ["test_core", "test_kernel_exact", "test_octree", "test_bh_kernel", "test_shooting"]
+SUITES = ["test_core", "test_kernel_exact", "test_octree", "test_bh_kernel", "test_shooting",
+          "test_optimizer"]
+# checks the REFERENCE itself fails in this build (reference library, same
+# harness): the B200 library must fail exactly these too (same algorithm)
+REFERENCE_OWN_FAILURES = {
+    "test_optimizer": [("test_optimizer", 29, "res.reason == TerminationReason::GradientTolerance"),
+                       ("test_optimizer", 145, "final_report.residual_sse < 1e-6"),
+                       ("test_optimizer", 145, "final_report.residual_sse < 1e-6"),
+                       ("test_optimizer", 145, "final_report.residual_sse < 1e-6")],
+}
 
 # (suite, source line, failed expression): the summation-order class above
 ALLOWED = {
@@ -46,15 +55,21 @@ def run_suite(name):
 
 @pytest.mark.parametrize("suite", SUITES)
 def test_reference_suite_on_reference(suite):
-    """Harness check: every case of the suite passes against the reference itself."""
+    """Harness check: the suite against the reference itself passes, except the
+    checks the reference fails on its own (REFERENCE_OWN_FAILURES)."""
     rc, (cases, passed, failed, checks, fchecks), fails = run_suite("ref_" + suite)
-    assert rc == 0 and failed == 0 and fchecks == 0 and passed == cases > 0, fails
+    assert sorted(fails) == sorted(REFERENCE_OWN_FAILURES.get(suite, [])), fails
+    assert checks > 0 and passed + failed == cases > 0
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", SUITES)
+@pytest.mark.parametrize("suite", SUITES + ["test_pipeline"])
 def test_reference_suite_on_b200(suite):
     rc, (cases, passed, failed, checks, fchecks), fails = run_suite("b200_" + suite)
+    own = REFERENCE_OWN_FAILURES.get(suite, [])
+    if own:  # fails exactly where the reference fails itself
+        assert sorted(fails) == sorted(own), fails
+        return
     unexpected = [f for f in fails if f not in ALLOWED]
     assert not unexpected, unexpected
     if suite != "test_octree":
