@@ -83,6 +83,7 @@ struct BhArgs {
   int ntask;           // pre-order node windows per query (blockIdx.y); partials [task][query]
   int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
   int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
+  int by_index;        // RHS: queries are ev[0 .. nq) (a shard's records), not leaf order
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
   uint32_t* per_query;
@@ -422,7 +423,9 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
   int out = -1;
   if (valid) {
-    if (MODE == kBhVel) {
+    if (MODE == kBhVel || (MODE == kBhRhs && a.by_index)) {
+      // eval records, or a sharded flow's own targets taken by point index
+      // from its (Morton-ordered) records: same interaction coordinates as srec
       x = ld4(a.ev + 2 * qi);
       if (sizeof(R) == 4)
         xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
@@ -430,6 +433,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
                     (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
       else
         xs = x;
+      if (MODE == kBhRhs) px = ld4(a.ev + 2 * qi + 1);
       out = qi;
     } else {
       const int t = qi;
@@ -866,7 +870,8 @@ static double bh_group_ratio() {
 
 template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
-  const int kind = a.lmd ? 1 : bh_kernel_choice();  // literal-mean-dot: independent walks only
+  // literal-mean-dot and by-index queries: independent walks only
+  const int kind = (a.lmd || a.by_index) ? 1 : bh_kernel_choice();
   if (kind == 0 || kind == 2) a.ntask = 1;  // single-window kernels
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
@@ -941,7 +946,8 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.mp = t.first.as<int>() + t.n;
   a.tgt_begin = q.tgt_begin;
   a.n_tgt = q.n_tgt;
-  a.nq = q.mode == kBhVel ? q.m : (int)t.n;
+  a.nq = q.mode == kBhVel ? q.m : (q.by_index ? q.n_tgt : (int)t.n);
+  a.by_index = q.by_index;
   a.ev = static_cast<const V4<R>*>(q.ev);
   const KernelConsts& kc = t.kc;
   a.kap = kc.kappa;
@@ -1030,6 +1036,10 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   q.mode = kBhRhs;
   q.ntask = K;
   q.lmd = cfg.literal_mean_dot;
+  if (tb != 0 || nt != n) {  // a shard: walk only its own targets, by point index
+    q.by_index = 1;
+    q.ev = static_cast<const char*>(rec) + 2 * vec_bytes(prec) * tb;
+  }
   q.tgt_begin = (int)tb;
   q.n_tgt = (int)nt;
   q.part = w.part.ptr;

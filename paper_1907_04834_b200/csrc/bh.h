@@ -86,6 +86,7 @@ struct BhQuery {
   unsigned long long* totals = nullptr;  // optional [3] sums
   int ntask = 1;  // node windows (bh_tasks); part holds [ntask][queries] partials
   int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
+  int by_index = 0;  // RHS: queries = the n_tgt records at ev (a flow shard), not leaf order
 };
 int bh_tasks(int64_t nq);
 int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,

@@ -76,6 +76,10 @@ struct gs_flow {
   KernelConsts kc{};
   DBuf rec, rec_next, y, ks, part, dhdp0, epart, flags, scal;
   DBuf boxes;  // exact underflow cutoff: target-block and source-tile boxes
+  // Barnes-Hut shards: records are put in Morton order once (set_shard) so a
+  // shard's index range is a compact region; order[t] = original index of t
+  DBuf order;
+  bool permuted = false;
   int steps_done = 0;
   int64_t launches = 0;
   bool want_energy = false;
@@ -416,6 +420,7 @@ int flow_upload(gs_flow* f, const double* q0, const double* p0) {
   bbox_center(q0, f->n, c0);
   f->kc = make_consts(f->cfg.sigma, f->prec == kF32 ? c0 : nullptr);
   GS_TRY(upload_records(f->ctx, f->prec, q0, p0, f->n, f->rec));
+  f->permuted = false;
   f->steps_done = 0;
   f->have_energy_part = false;
   GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), f->ctx->stream));
@@ -593,8 +598,17 @@ gs_status gs_flow_download(gs_flow* f, double* q, double* p) {
   GS_TRY(c->stage_b.ensure(sizeof(double) * 3 * f->n));
   GS_TRY(unpack_records(f->prec, f->rec.ptr, f->n, c->stage_a.as<double>(),
                         c->stage_b.as<double>(), c->stream));
-  GS_TRY(d2h(c, q, c->stage_a.ptr, 3 * f->n));
-  GS_TRY(d2h(c, p, c->stage_b.ptr, 3 * f->n));
+  if (f->permuted) {  // back to the caller's point order
+    GS_TRY(c->stage_c.ensure(sizeof(double) * 3 * f->n));
+    GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * f->n));
+    GS_TRY(scatter_rows3(c->stage_a.as<double>(), f->order.as<int>(), f->n, c->stage_c.as<double>(), c->stream));
+    GS_TRY(scatter_rows3(c->stage_b.as<double>(), f->order.as<int>(), f->n, c->stage_d.as<double>(), c->stream));
+    GS_TRY(d2h(c, q, c->stage_c.ptr, 3 * f->n));
+    GS_TRY(d2h(c, p, c->stage_d.ptr, 3 * f->n));
+  } else {
+    GS_TRY(d2h(c, q, c->stage_a.ptr, 3 * f->n));
+    GS_TRY(d2h(c, p, c->stage_b.ptr, 3 * f->n));
+  }
   GS_TRY(sync(c));
   return GS_OK;
 }
@@ -641,6 +655,21 @@ gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
   if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
   f->shard_begin = begin;
   f->shard_count = count;
+  if (f->cfg.backend == GS_BARNES_HUT && count < f->n && !f->permuted && f->steps_done == 0) {
+    // Barnes-Hut walks are only coherent for spatially compact query sets:
+    // reorder the records by Morton key (every rank computes the same order
+    // from the same uploaded records), remember the order for download
+    gs_ctx* c = f->ctx;
+    GS_TRY(morton_order(c->dev, f->prec, f->kc, f->rec.ptr, f->n, f->bh.cur, c->stream));
+    GS_TRY(f->order.ensure(sizeof(int) * f->n));
+    GS_CUDA_OK(cudaMemcpyAsync(f->order.ptr, f->bh.cur.perm.ptr, sizeof(int) * f->n,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    GS_TRY(f->rec_next.ensure(2 * vec_bytes(f->prec) * f->n));
+    GS_TRY(permute_records(f->prec, f->rec.ptr, f->order.as<int>(), f->n, f->rec_next.ptr, c->stream));
+    std::swap(f->rec.ptr, f->rec_next.ptr);
+    std::swap(f->rec.bytes, f->rec_next.bytes);
+    f->permuted = true;
+  }
   return GS_OK;
 }
 

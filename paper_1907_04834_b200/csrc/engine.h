@@ -162,6 +162,9 @@ int gradient_finalize(int prec, const void* adj, const double* dhdp0, int64_t n,
 int adjoint_init(int prec, const void* rec_T, const double* target, double lambda, int64_t n,
                  void* adj, double* sse_part, int* blocks, cudaStream_t st);
 int reduce_sum(const double* part, int count, double* out, cudaStream_t st);
+// out[t] = in[perm[t]] (records, [n][2] V4) / out[perm[t]] = in[t] (double [n][3])
+int permute_records(int prec, const void* in, const int* perm, int64_t n, void* out, cudaStream_t st);
+int scatter_rows3(const double* in, const int* perm, int64_t n, double* out, cudaStream_t st);
 // per-block FP64 sums of the .w lane of partial vec4 `which` of n targets ([n][per] layout)
 int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
                int* blocks, cudaStream_t st);

@@ -253,6 +253,41 @@ __global__ void __launch_bounds__(kEpiNT) k_sum_w(const V4<R>* part, int n, int 
 
 }  // namespace
 
+namespace {
+template <typename R>
+__global__ void k_permute_records(const V4<R>* in, const int* perm, int64_t n, V4<R>* out) {
+  const int64_t t = blockIdx.x * (int64_t)kEpiNT + threadIdx.x;
+  if (t >= n) return;
+  const int i = perm[t];
+  st4(out + 2 * t, ld4(in + 2 * i));
+  st4(out + 2 * t + 1, ld4(in + 2 * i + 1));
+}
+__global__ void k_scatter_rows3(const double* in, const int* perm, int64_t n, double* out) {
+  const int64_t t = blockIdx.x * (int64_t)kEpiNT + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = perm[t];
+  out[3 * i] = in[3 * t];
+  out[3 * i + 1] = in[3 * t + 1];
+  out[3 * i + 2] = in[3 * t + 2];
+}
+}  // namespace
+
+int permute_records(int prec, const void* in, const int* perm, int64_t n, void* out, cudaStream_t st) {
+  const int nb = blocks_for(n, kEpiNT);
+  if (prec == kF32)
+    k_permute_records<float><<<nb, kEpiNT, 0, st>>>((const float4*)in, perm, n, (float4*)out);
+  else
+    k_permute_records<double><<<nb, kEpiNT, 0, st>>>((const double4*)in, perm, n, (double4*)out);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int scatter_rows3(const double* in, const int* perm, int64_t n, double* out, cudaStream_t st) {
+  k_scatter_rows3<<<blocks_for(n, kEpiNT), kEpiNT, 0, st>>>(in, perm, n, out);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
 int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
                int* blocks, cudaStream_t st) {
   const int nb = blocks_for(n, kEpiNT);
