@@ -321,6 +321,40 @@ def run_ours(args):
         }
         del fb
 
+    # ---- Barnes-Hut across ranks: target shards (Morton-ordered at set_shard),
+    # one in-place all-gather per stage; device time = max over ranks ----------
+    if not args.no_bh and world > 1:
+        cfg_bh = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=BARNES_HUT,
+                                integrator=RK4, precision=F32)
+        fb = gs.flow(cfg_bh, N)
+        fb.upload(q0, p0)
+        sb = torch.cuda.ExternalStream(fb.stream())
+        drb = ShardedFlow(fb, 4, stream=sb)
+        drb.step(max(1, args.warmup))
+        fb.sync()
+        # time the first kb steps of the config-4 flow (as on one GPU): re-upload,
+        # re-shard (Morton order again, fresh record view)
+        fb.upload(q0, p0)
+        drb = ShardedFlow(fb, 4, stream=sb)
+        barrier()
+        kb = max(1, args.steps)
+        with torch.cuda.stream(sb):
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sb)
+        drb.step(kb)
+        e1.record(sb)
+        torch.cuda.synchronize()
+        barrier()
+        fb.sync()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        bms = float(t.item())
+        line["bh"] = {"value": kb / (bms / 1e3), "unit": "flow steps/s", "ms_per_step": bms / kb,
+                      "n2_equivalent_pairs_per_s": 4.0 * N * float(N) * kb / (bms / 1e3),
+                      "parallelism": f"target-shard x{world} (each rank rebuilds the tree)"}
+        del drb, fb
+
     # ---- exact with the FP32 underflow cutoff (GS_FLAG_EXACT_CUTOFF, opt-in) ------
     # The same exact sum over Morton-ordered points, skipping tile pairs whose
     # Gaussian weights are all exactly 0 in FP32 (bit-identical to evaluating
