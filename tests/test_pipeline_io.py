@@ -92,3 +92,23 @@ def test_parse_matches_reference(tmp_path, ref, case):
 def test_missing_file(tmp_path):
     with pytest.raises(OSError):
         read_points(str(tmp_path / "nope.xyz"))
+
+
+# ---- property: every finite double survives a write/read round trip ----------
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_finite = st.floats(allow_nan=False, allow_infinity=False, width=64)
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.lists(st.tuples(_finite, _finite, _finite), min_size=1, max_size=40),
+       st.sampled_from([(XYZ, "xyz"), (VTK, "vtk")]))
+def test_round_trip_property(tmp_path_factory, rows, fmt_ext):
+    fmt, ext = fmt_ext
+    pts = np.array(rows, dtype=np.float64).reshape(-1, 3)
+    f = str(tmp_path_factory.mktemp("rt") / f"p.{ext}")
+    write_points(pts, f, fmt)
+    back = read_points(f, fmt)
+    assert back.shape == pts.shape
+    # bit-exact, -0.0 included (%.17g keeps the sign)
+    assert back.tobytes() == pts.tobytes()
