@@ -45,6 +45,10 @@ double gate_t2(double thr) {
 namespace {
 
 constexpr int kBhNT = 128;
+#ifndef GS_BH_WHOLE_RECORD
+#define GS_BH_WHOLE_RECORD 1
+#endif
+constexpr bool kLoadWholeRecord = GS_BH_WHOLE_RECORD != 0;
 #ifndef GS_BH_WS_NOWIN_MINB
 #define GS_BH_WS_NOWIN_MINB 7
 #endif
@@ -469,8 +473,12 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     R dsc = R(1);
     if (j > je && next < m) {
       const int nd = next;
-      V4<R> l, h;
-      ld8(a.nrec + 4 * nd, l, h);  // one 32-B sector (FP32)
+      V4<R> l, h, C, M;
+      // the whole 64-B record at once (two independent 256-bit loads): the
+      // far-field half (centroid, momentum sum, count) is needed for far and
+      // range nodes, and a dependent second trip would cost a full latency
+      ld8(a.nrec + 4 * nd, l, h);
+      if (kLoadWholeRecord) ld8(a.nrec + 4 * nd + 2, C, M);
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
       const int skip = code & 0x1fffffff;
@@ -485,24 +493,28 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
           if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
           have = true;
           ++c_dir;
-        } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
-          j = begin;
-          je = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
-        } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
-          if (own) {
-            ld8(a.nrec + 4 * nd + 2, Q, P);
-            if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
-            if (LMD) dsc = R(1) / Q.w;  // Q.w = count
-            have = true;
-            ++c_app;
-          }
-        } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
-          // a twig (children all leaves) or every descendant opens: range
-          j = max(begin, bA);
-          je = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
-          c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
         } else {
-          next = nd + 1;
+          if (!kLoadWholeRecord) ld8(a.nrec + 4 * nd + 2, C, M);
+          if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
+            j = begin;
+            je = begin + code_of(M.w) - 1;
+          } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
+            if (own) {
+              Q = C;
+              P = M;
+              if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+              if (LMD) dsc = R(1) / Q.w;  // Q.w = count
+              have = true;
+              ++c_app;
+            }
+          } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
+            // a twig (children all leaves) or every descendant opens: range
+            j = max(begin, bA);
+            je = min(begin + code_of(M.w), bB) - 1;
+            c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+          } else {
+            next = nd + 1;
+          }
         }
       }
       if (next >= B || next <= nd) next = INT_MAX;  // window done; never loop on a corrupt skip
