@@ -81,3 +81,42 @@ def test_bh_full_size_covers_every_point_once(gs, prec):
     assert d["skip"][0] == m and (d["skip"] > np.arange(m)).all()
     assert d["count"][0] == N
     assert np.array_equal(d["count"], d["range"][:, 1] - d["range"][:, 0] + 1)
+
+
+def test_bh_infinite_threshold_equals_exact_config2_fp64(gs):
+    """Config 2 size (N = 20k ellipsoid, sigma 3, 20 Euler steps, FP64): with an
+    infinite gate every unit is direct, so Barnes-Hut must reproduce the exact
+    flow (the reference's own property, test_bh_kernel.cpp:58-110, here at the
+    config's full size)."""
+    from paper_1907_04834_b200 import BARNES_HUT, EXACT, ShootingConfig
+    from tests.util import ellipsoid, rel_l2, smooth_momenta
+    q = ellipsoid(20000, seed=44)
+    p = smooth_momenta(q, 0.005, 43)
+    base = dict(sigma=3.0, timesteps=20, precision=F64)
+    eq, ep, ee, _ = gs.shoot_forward(q, p, ShootingConfig(backend=EXACT, **base),
+                                     keep_trajectory=False)
+    bq, bp, be, st = gs.shoot_forward(
+        q, p, ShootingConfig(backend=BARNES_HUT, threshold_multiplier=float("inf"), **base),
+        keep_trajectory=False)
+    assert st["approximated_interactions"] == 0
+    assert st["direct_interactions"] == 20 * 20000 ** 2
+    assert rel_l2(bq, eq) < 1e-12 and rel_l2(bp, ep) < 1e-10
+    assert be == pytest.approx(ee, rel=1e-12)
+
+
+def test_bh_infinite_threshold_equals_exact_config3_evaluate(gs):
+    """Config 3 size (N = 50k tube, sigma 5, T = 20, FP32): the fused forward +
+    adjoint evaluate() through the tree with an infinite gate equals the exact
+    evaluate() (objective and gradient)."""
+    from paper_1907_04834_b200 import BARNES_HUT, EXACT, ShootingConfig
+    from tests.util import rel_l2, smooth_momenta, tube
+    q = f32(tube(50000, seed=3))
+    p = f32(smooth_momenta(q, 0.01, 4))
+    t = f32(q + 0.05)
+    base = dict(sigma=5.0, lambda_=100.0, timesteps=20, precision=F32)
+    a = gs.evaluate(q, p, t, ShootingConfig(backend=EXACT, **base))
+    b = gs.evaluate(q, p, t, ShootingConfig(backend=BARNES_HUT, threshold_multiplier=float("inf"),
+                                            **base))
+    assert b.stats["approximated_interactions"] == 0
+    assert b.report["total"] == pytest.approx(a.report["total"], rel=1e-5)
+    assert rel_l2(b.gradient, a.gradient) < 1e-4
