@@ -467,11 +467,19 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
   int next = out >= 0 ? 0 : INT_MAX;
   int j = 0, je = -1;  // pending direct range
   const V4<R> zero = mk4<R>(0, 0, 0);
+#ifdef GS_BH_WS_STATS
+  unsigned dbg_iter = 0, dbg_visit = 0, dbg_unit = 0;
+#define GS_WS_COUNT(x) (x)
+#else
+#define GS_WS_COUNT(x) ((void)0)
+#endif
   while (__any_sync(0xffffffffu, next < m || j <= je)) {
+    GS_WS_COUNT(++dbg_iter);
     bool have = false;
     V4<R> Q = zero, P = zero, Al = zero, Be = zero;  // this iteration's unit
     R dsc = R(1);
     if (j > je && next < m) {
+      GS_WS_COUNT(++dbg_visit);
       const int nd = next;
       V4<R> l, h, C, M;
       // the whole 64-B record at once (two independent 256-bit loads): the
@@ -530,7 +538,24 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       ++c_dir;
     }
     if (have) unit<R, MODE, LMD>(acc, xs, px, ai, bi, Q, P, Al, Be, a, dsc);
+    GS_WS_COUNT(dbg_unit += have);
   }
+#ifdef GS_BH_WS_STATS
+  if (a.dbg) {  // GS_BH_DEBUG (build with -DGS_BH_WS_STATS): warp iterations, lane visits, lane units
+    unsigned long long v = dbg_visit, u = dbg_unit;
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_down_sync(0xffffffffu, v, o);
+      u += __shfl_down_sync(0xffffffffu, u, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(a.dbg + 4, 1ull);
+      atomicAdd(a.dbg + 5, (unsigned long long)dbg_iter);
+      atomicAdd(a.dbg + 6, v);
+      atomicAdd(a.dbg + 7, u);
+    }
+  }
+#endif
+#undef GS_WS_COUNT
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
     const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
@@ -908,6 +933,22 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
     }
     if (kind == 3) return GS_OK;
   }
+  struct DbgPrint {
+    bool on;
+    unsigned long long* buf;
+    cudaStream_t st;
+    int mode, nq;
+    ~DbgPrint() {
+      if (!on) return;
+      unsigned long long h[8];
+      cudaMemcpyAsync(h, buf, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (h[4])
+        std::fprintf(stderr, "[bh ws mode %d nq %d] warps %llu iters/warp %.1f visits/lane %.1f units/lane %.1f simt %.1f\n",
+                     mode, nq, h[4], (double)h[5] / h[4], (double)h[6] / (32.0 * h[4]),
+                     (double)h[7] / (32.0 * h[4]), (double)(h[6] + h[7]) / h[5]);
+    }
+  } dbg_print{dbg, dbuf, st, mode, a.nq};
   if (kind == 2) {
     if (mode == kBhRhs) k_bh_pipe<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
     else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
