@@ -30,9 +30,12 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   return GS_CUDA_ERROR;
 }
 
+std::atomic<unsigned long long> g_dbuf_epoch{0};
+
 int DBuf::ensure(size_t need) {
   if (need <= bytes && ptr) return GS_OK;
   release();
+  ++g_dbuf_epoch;
   need = std::max<size_t>(need, 256);
   GS_CUDA_OK(cudaMalloc(&ptr, need));
   bytes = need;
@@ -40,7 +43,10 @@ int DBuf::ensure(size_t need) {
 }
 
 void DBuf::release() {
-  if (ptr) cudaFree(ptr);
+  if (ptr) {
+    cudaFree(ptr);
+    ++g_dbuf_epoch;
+  }
   ptr = nullptr;
   bytes = 0;
 }
@@ -95,6 +101,8 @@ struct gs_flow {
   KernelConsts gkc{};
   gs_config gcfg{};
   int64_t gn = -1, glaunches = 0;
+  unsigned long long gepoch = 0;  // g_dbuf_epoch at capture
+  uint64_t gsig = 0;              // the flow's buffer pointers at capture
   void drop_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
@@ -446,6 +454,26 @@ bool graphs_enabled() {
 
 // Capture one step (the kernel parameters -- buffers, constants -- are fixed
 // for a given flow configuration and input scaling), instantiate, keep.
+// Every device buffer a captured step can touch: a graph replays raw pointers.
+uint64_t flow_sig(const gs_flow* f) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const DBuf& b) {
+    h = (h ^ (uint64_t)(uintptr_t)b.ptr) * 1099511628211ull;
+    h = (h ^ (uint64_t)b.bytes) * 1099511628211ull;
+  };
+  for (const DBuf* b : {&f->rec, &f->rec_next, &f->y, &f->ks, &f->part, &f->flags, &f->stepctr,
+                        &f->boxes, &f->bh.part, &f->bh.stats})
+    mix(*b);
+  const DevTree& t = f->bh.cur;
+  for (const DBuf* b : {&t.key_hi, &t.key_lo, &t.perm, &t.skey_hi, &t.skey_lo, &t.lcp, &t.first,
+                        &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.counter, &t.lo,
+                        &t.hi, &t.cen, &t.mom, &t.nrec, &t.nadj_a, &t.nadj_b, &t.psum, &t.msum,
+                        &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist,
+                        &t.scan_tmp, &t.scal})
+    mix(*b);
+  return h;
+}
+
 int flow_capture_step(gs_flow* f) {
   f->drop_graph();
   cudaStream_t st = f->ctx->stream;
@@ -467,6 +495,8 @@ int flow_capture_step(gs_flow* f) {
   GS_CUDA_OK(ie);
   f->glaunches = f->launches - l0 + 1;
   f->launches = l0;
+  f->gepoch = g_dbuf_epoch.load();
+  f->gsig = flow_sig(f);
   std::memcpy(&f->gkc, &f->kc, sizeof f->kc);  // byte copies: compared with memcmp
   std::memcpy(&f->gcfg, &f->cfg, sizeof f->cfg);
   f->gn = f->n;
@@ -481,9 +511,13 @@ int flow_advance(gs_flow* f, int steps) {
       GS_TRY(flow_step_eager(f));
       continue;
     }
-    if (!f->gexec || f->gn != f->n || std::memcmp(&f->gkc, &f->kc, sizeof f->kc) != 0 ||
-        std::memcmp(&f->gcfg, &f->cfg, sizeof f->cfg) != 0)
-      GS_TRY(flow_capture_step(f));
+    bool stale = !f->gexec || f->gn != f->n || std::memcmp(&f->gkc, &f->kc, sizeof f->kc) != 0 ||
+                 std::memcmp(&f->gcfg, &f->cfg, sizeof f->cfg) != 0;
+    if (!stale && f->gepoch != g_dbuf_epoch.load()) {  // some buffer somewhere moved: ours?
+      stale = flow_sig(f) != f->gsig;
+      if (!stale) f->gepoch = g_dbuf_epoch.load();
+    }
+    if (stale) GS_TRY(flow_capture_step(f));
     GS_CUDA_OK(cudaGraphLaunch(f->gexec, f->ctx->stream));
     f->launches += f->glaunches;
     ++f->steps_done;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -32,6 +33,10 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 void set_error(const std::string& msg);
 
 // Growable device buffer (cudaMalloc, never shrinks).
+// bumped on every device (re)allocation or free of a DBuf: cached CUDA graphs
+// hold raw buffer pointers and re-validate them when it moved
+extern std::atomic<unsigned long long> g_dbuf_epoch;
+
 struct DBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
