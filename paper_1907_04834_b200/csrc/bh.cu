@@ -137,6 +137,28 @@ __device__ __forceinline__ bool all_inside(const V4<R>& l, const V4<R>& h, const
   return mx * mx + my * my + mz * mz <= lim;
 }
 
+// Gate and fully-inside test of one node from the same per-axis differences
+// a = lo - x, b = x - hi: min distance per axis max(a, b, 0) (the reference
+// gate, octree.cpp:141-149), max distance per axis -min(a, b). Returns
+// 1 = far (approximate), 2 = every descendant opens (direct range), 0 = open.
+__device__ __forceinline__ int classify(const float4& l, const float4& h, const float4& x,
+                                        const BhArgs<float>& a) {
+  const float ax = l.x - x.x, ay = l.y - x.y, az = l.z - x.z;
+  const float bx = x.x - h.x, by = x.y - h.y, bz = x.z - h.z;
+  const float gx = fmaxf(fmaxf(ax, bx), 0.f), gy = fmaxf(fmaxf(ay, by), 0.f),
+              gz = fmaxf(fmaxf(az, bz), 0.f);
+  const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+  if (d2 > a.thr2_hi) return 1;
+  if (d2 >= a.thr2_lo && gate_exact(l.x, l.y, l.z, h.x, h.y, h.z, x.x, x.y, x.z, a.T2)) return 1;
+  const float mx = fminf(ax, bx), my = fminf(ay, by), mz = fminf(az, bz);
+  return mx * mx + my * my + mz * mz <= a.thr2_in ? 2 : 0;
+}
+__device__ __forceinline__ int classify(const double4& l, const double4& h, const double4& x,
+                                        const BhArgs<double>& a) {
+  if (gate(l, h, x, a)) return 1;
+  return all_inside(l, h, x, a.thr2_in) ? 2 : 0;
+}
+
 // Gaussian weight between the query and a source in interaction coordinates.
 __device__ __forceinline__ float kern(float dx, float dy, float dz, const BhArgs<float>&) {
   float nr2 = -dx * dx;
@@ -490,10 +512,10 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       const int code = code_of(l.w);
       const int begin = code_of(h.w);
       const int skip = code & 0x1fffffff;
-      const bool own = nd >= A;  // the node itself is in this block's window
+      const bool own = !WIN || nd >= A;  // the node itself is in this block's window
       if (a.prefetch && skip < B) prefetch_l1(a.nrec + 4 * skip);
       next = skip;
-      if (skip > A) {  // the subtree reaches into the window (else: pass it by)
+      if (!WIN || skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
         if (code < 0) {  // single-point leaf (always own): the record holds the point itself
           Q = l;
@@ -503,10 +525,11 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
           ++c_dir;
         } else {
           if (!kLoadWholeRecord) ld8(a.nrec + 4 * nd + 2, C, M);
-          if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
+          const int cls = (code & 0x40000000) ? 3 : classify(l, h, x, a);
+          if (cls == 3) {  // depth-32 bucket (always own): all its points
             j = begin;
             je = begin + code_of(M.w) - 1;
-          } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
+          } else if (cls == 1) {  // far: one aggregate term at the centroid
             if (own) {
               Q = C;
               P = M;
@@ -515,11 +538,17 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
               have = true;
               ++c_app;
             }
-          } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
-            // a twig (children all leaves) or every descendant opens: range
-            j = max(begin, bA);
-            je = min(begin + code_of(M.w), bB) - 1;
-            c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+          } else if (cls == 2 || (code & 0x20000000)) {
+            // every descendant opens, or a twig (children all leaves): range
+            if (WIN) {
+              j = max(begin, bA);
+              je = min(begin + code_of(M.w), bB) - 1;
+              c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+            } else {
+              j = begin;
+              je = begin + code_of(M.w) - 1;
+              c_vis += (uint32_t)(skip - nd - 1);
+            }
           } else {
             next = nd + 1;
           }
