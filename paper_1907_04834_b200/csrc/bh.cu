@@ -367,7 +367,7 @@ __device__ __forceinline__ V4<R> shfl4(const V4<R>& v, int src) {
 // that sweep up to 32/GL owners' ranges at once (stride GL), then a log2(GL)
 // butterfly inside each group and one shuffle hand each sum to its owner --
 // 6x fewer reduction shuffles per range than a whole-warp sweep for GL = 8.
-template <typename R, int MODE, bool LMD = false>
+template <typename R, int MODE, bool LMD = false, bool COUNT = true>
 __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc<R>& acc,
                                             uint32_t& c_dir, const V4<R>& xs, const V4<R>& px,
                                             const V4<R>& ai, const V4<R>& bi,
@@ -419,7 +419,7 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
       if (mine) acc.v[c] += v;
     }
     if (mine) {
-      c_dir += (uint32_t)(je - j + 1);
+      if (COUNT) c_dir += (uint32_t)(je - j + 1);  // (k_bh_ws counts a range when it starts)
       j = je + 1;
     }
   }
@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
           if (cls == 3) {  // depth-32 bucket (always own): all its points
             j = begin;
             je = begin + code_of(M.w) - 1;
+            c_dir += (uint32_t)(je - j + 1);  // counted once per range
           } else if (cls == 1) {  // far: one aggregate term at the centroid
             if (own) {
               Q = C;
@@ -544,10 +545,12 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
               j = max(begin, bA);
               je = min(begin + code_of(M.w), bB) - 1;
               c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+              c_dir += (uint32_t)max(0, je - j + 1);
             } else {
               j = begin;
               je = begin + code_of(M.w) - 1;
               c_vis += (uint32_t)(skip - nd - 1);
+              c_dir += (uint32_t)(je - j + 1);
             }
           } else {
             next = nd + 1;
@@ -558,13 +561,12 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     }
     // long direct ranges (dense near field) are swept by the whole warp
     const unsigned big = __ballot_sync(0xffffffffu, !have && je - j + 1 >= kBigRange);
-    if (big) coop_ranges<R, MODE, LMD>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
+    if (big) coop_ranges<R, MODE, LMD, false>(big, j, je, acc, c_dir, xs, px, ai, bi, a);
     if (!have && j <= je) {
       ld8(a.srec + 2 * j, Q, P);
       if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * j); Be = ld4(a.sadj + 2 * j + 1); }
       have = true;
       ++j;
-      ++c_dir;
     }
     if (have) unit<R, MODE, LMD>(acc, xs, px, ai, bi, Q, P, Al, Be, a, dsc);
     GS_WS_COUNT(dbg_unit += have);
