@@ -498,7 +498,8 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
   while (__any_sync(0xffffffffu, next < m || j <= je)) {
     GS_WS_COUNT(++dbg_iter);
     bool have = false;
-    V4<R> Q = zero, P = zero, Al = zero, Be = zero;  // this iteration's unit
+    V4<R> Q, P, Al, Be;  // this iteration's unit (read only when have)
+    if (MODE == kBhHess) Al = Be = zero;
     R dsc = R(1);
     if (j > je && next < m) {
       GS_WS_COUNT(++dbg_visit);
