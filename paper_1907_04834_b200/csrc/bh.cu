@@ -8,16 +8,18 @@
 //
 // Here the nodes are in depth-first pre-order with skip pointers, so a query's
 // walk is a monotone sweep: visit n; leaf/far -> next = skip[n]; open ->
-// next = n + 1. A warp holds 32 Morton-adjacent queries and always serves the
-// smallest pending node of its lanes (__reduce_min_sync); the lanes parked at
-// that node classify it, so every lane visits exactly its own reference node
-// set, in lock step with its neighbours (coherent loads, little divergence).
-// Direct work is batched: a leaf -- or a node whose FARTHEST box point is
-// within the threshold, all of whose descendants the reference would open
-// down to their leaves -- is a contiguous range of leaf-order points that the
-// lanes parked there sweep together with broadcast loads. The interaction set
-// and the per-query (direct, approximated, visited) counts equal the
-// reference's exactly; only the summation order differs.
+// next = n + 1. Queries are the tree's points in leaf (Morton) order, so a
+// warp holds 32 neighbours. k_bh_ws (default) walks each lane independently:
+// per iteration a lane visits one node (64-B record = its unit + its box,
+// two 256-bit loads) or takes one point of its pending direct range, and all
+// lanes holding a unit evaluate it together. A leaf, a twig (children all
+// leaves) or a node whose FARTHEST box point is within the threshold -- all
+// of whose descendants the reference would open down to their leaves -- is a
+// contiguous range of leaf-order points; long ranges are swept by the whole
+// warp. k_bh_grp walks the union of the warp's node sets and sweeps the union
+// of the lanes' direct ranges with broadcast loads (dense regimes). The
+// interaction set and the per-query (direct, approximated, visited) counts
+// equal the reference's exactly; only the summation order differs.
 //
 // The gate min_distance(tight box, x) > thr (octree.cpp:141-149) is evaluated
 // bit-exactly: FP64 with the reference's operation order and no contraction,
@@ -62,14 +64,9 @@ constexpr bool kLoadWholeRecord = GS_BH_WHOLE_RECORD != 0;
 
 template <typename R>
 struct BhArgs {
-  const int4* meta;
-  const V4<R>* lo;
-  const V4<R>* hi;
-  const V4<R>* cen;
-  const V4<R>* mom;
   const V4<R>* nadj_a;
   const V4<R>* nadj_b;
-  const V4<R>* nrec;  // [m][4] node records {lo, code} {hi, begin} {centroid} {momentum}
+  const V4<R>* nrec;  // [m][4] node records {unit, code} {unit, begin} {lo, count} {hi}
   const V4<R>* srec;  // [n][2] interaction coords (scaled FP32), p
   const V4<R>* squ;   // [n] unscaled q
   const V4<R>* sadj;  // [n][2] alpha, beta (leaf order)
@@ -214,116 +211,6 @@ __device__ __forceinline__ void unit(Acc<R>& acc, const V4<R>& xs, const V4<R>& 
   }
 }
 
-template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT) k_bh(const BhArgs<R> a) {
-  const int qi = blockIdx.x * kBhNT + threadIdx.x;
-  const bool valid = qi < a.nq;
-  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
-  int out = -1;
-  if (valid) {
-    if (MODE == kBhVel) {
-      x = ld4(a.ev + 2 * qi);
-      if (sizeof(R) == 4)
-        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
-                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
-                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
-      else
-        xs = x;
-      out = qi;
-    } else {
-      const int t = qi;  // leaf-order position
-      x = ld4(a.squ + t);
-      xs = ld4(a.srec + 2 * t);
-      px = ld4(a.srec + 2 * t + 1);
-      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
-      const int i = a.perm[t] - a.tgt_begin;
-      out = (i >= 0 && i < a.n_tgt) ? i : -1;
-    }
-  }
-  Acc<R> acc;
-#pragma unroll
-  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
-  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
-  const int m = *a.mp;
-  int next = out >= 0 ? 0 : INT_MAX;
-  const V4<R> zero = mk4<R>(0, 0, 0);
-  for (;;) {
-    const int nd = __reduce_min_sync(0xffffffffu, next);
-    if (nd == INT_MAX) break;
-    bool ranged = false;
-    int4 mi = make_int4(0, 0, 0, 0);
-    if (next == nd) {
-      // the three node loads are independent: issue them together
-      mi = a.meta[nd];
-      const V4<R> l = ld4(a.lo + nd), h = ld4(a.hi + nd);
-      ++c_vis;
-      if (mi.w & 1) {  // leaf: its point(s) directly
-        ranged = true;
-        next = mi.x;
-      } else {
-        if (gate(l, h, x, a)) {  // far: one aggregate term
-          const V4<R> C = ld4(a.cen + nd), P = ld4(a.mom + nd);
-          if (MODE == kBhHess)
-            unit<R, MODE>(acc, xs, px, ai, bi, C, P, ld4(a.nadj_a + nd), ld4(a.nadj_b + nd), a);
-          else
-            unit<R, MODE>(acc, xs, px, ai, bi, C, P, zero, zero, a);
-          ++c_app;
-          next = mi.x;
-        } else if (all_inside(l, h, x, a.thr2_in)) {  // whole subtree opens: range
-          ranged = true;
-          c_vis += (uint32_t)(mi.x - nd - 1);
-          next = mi.x;
-        } else {
-          next = nd + 1;
-        }
-      }
-      // past the last node (skip == m): this query is done; a non-advancing skip
-      // (cannot happen on a valid tree) must never loop
-      if (next >= m || next <= nd) next = INT_MAX;
-    }
-    const unsigned rm = __ballot_sync(0xffffffffu, ranged);
-    if (rm) {
-      const int src = __ffs(rm) - 1;
-      const int b = __shfl_sync(0xffffffffu, mi.y, src);
-      const int e = __shfl_sync(0xffffffffu, mi.z, src);
-      if (ranged) {
-        c_dir += (uint32_t)(e - b + 1);
-        for (int j = b; j <= e; ++j) {
-          V4<R> Q, P;
-        ld8(a.srec + 2 * j, Q, P);
-          if (MODE == kBhHess)
-            unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
-          else
-            unit<R, MODE>(acc, xs, px, ai, bi, Q, P, zero, zero, a);
-        }
-      }
-    }
-  }
-  if (out >= 0) {
-    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
-    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
-    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
-    if (a.per_query) {
-      a.per_query[3 * out] = c_dir;
-      a.per_query[3 * out + 1] = c_app;
-      a.per_query[3 * out + 2] = c_vis;
-    }
-  }
-  if (a.totals) {
-    unsigned long long d = c_dir, p = c_app, v = c_vis;
-    for (int o = 16; o > 0; o >>= 1) {
-      d += __shfl_down_sync(0xffffffffu, d, o);
-      p += __shfl_down_sync(0xffffffffu, p, o);
-      v += __shfl_down_sync(0xffffffffu, v, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(a.totals, d);
-      atomicAdd(a.totals + 1, p);
-      atomicAdd(a.totals + 2, v);
-    }
-  }
-}
 
 // Squared diagonal of the warp's query box (valid lanes only): decides, per
 // warp and identically in both kernels of a split launch, whether the warp's
@@ -504,39 +391,35 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     if (j > je && next < m) {
       GS_WS_COUNT(++dbg_visit);
       const int nd = next;
-      V4<R> l, h, C, M;
-      // the whole 64-B record at once (two independent 256-bit loads): the
-      // far-field half (centroid, momentum sum, count) is needed for far and
-      // range nodes, and a dependent second trip would cost a full latency
-      ld8(a.nrec + 4 * nd, l, h);
-      if (kLoadWholeRecord) ld8(a.nrec + 4 * nd + 2, C, M);
-      const int code = code_of(l.w);
-      const int begin = code_of(h.w);
+      // the whole 64-B record at once, two independent 256-bit loads: half A
+      // straight into the unit operands (a single leaf's point, or a node's
+      // centroid + momentum sum), half B (tight box + count) for the gate
+      V4<R> l, h;
+      ld8(a.nrec + 4 * nd, Q, P);
+      ld8(a.nrec + 4 * nd + 2, l, h);
+      const int code = code_of(Q.w);
+      const int begin = code_of(P.w);
       const int skip = code & 0x1fffffff;
       const bool own = !WIN || nd >= A;  // the node itself is in this block's window
       if (a.prefetch && skip < B) prefetch_l1(a.nrec + 4 * skip);
       next = skip;
       if (!WIN || skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
-        if (code < 0) {  // single-point leaf (always own): the record holds the point itself
-          Q = l;
-          P = h;
+        if (code < 0) {  // single-point leaf (always own): half A holds the point itself
           if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
           have = true;
           ++c_dir;
         } else {
-          if (!kLoadWholeRecord) ld8(a.nrec + 4 * nd + 2, C, M);
+          const int cnt = code_of(l.w);
           const int cls = (code & 0x40000000) ? 3 : classify(l, h, x, a);
           if (cls == 3) {  // depth-32 bucket (always own): all its points
             j = begin;
-            je = begin + code_of(M.w) - 1;
-            c_dir += (uint32_t)(je - j + 1);  // counted once per range
+            je = begin + cnt - 1;
+            c_dir += (uint32_t)cnt;  // counted once per range
           } else if (cls == 1) {  // far: one aggregate term at the centroid
             if (own) {
-              Q = C;
-              P = M;
               if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
-              if (LMD) dsc = R(1) / Q.w;  // Q.w = count
+              if (LMD) dsc = R(1) / R(cnt);
               have = true;
               ++c_app;
             }
@@ -544,14 +427,14 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
             // every descendant opens, or a twig (children all leaves): range
             if (WIN) {
               j = max(begin, bA);
-              je = min(begin + code_of(M.w), bB) - 1;
+              je = min(begin + cnt, bB) - 1;
               c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
               c_dir += (uint32_t)max(0, je - j + 1);
             } else {
               j = begin;
-              je = begin + code_of(M.w) - 1;
+              je = begin + cnt - 1;
               c_vis += (uint32_t)(skip - nd - 1);
-              c_dir += (uint32_t)(je - j + 1);
+              c_dir += (uint32_t)cnt;
             }
           } else {
             next = nd + 1;
@@ -711,47 +594,50 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
     const int nd = __reduce_min_sync(0xffffffffu, next);
     if (nd == INT_MAX) break;
     ++n_iter;
-    // the node's compact record, loaded by every lane (one broadcast sector)
-    V4<R> l, h;
-      ld8(a.nrec + 4 * nd, l, h);
-    const int code = code_of(l.w);
-    const int begin = code_of(h.w);
+    // the node's 64-B record, loaded by every lane (broadcast): half A = the
+    // node's unit (point or centroid + momentum sum), half B = box + count
+    V4<R> Q, P, l, h;
+    ld8(a.nrec + 4 * nd, Q, P);
+    ld8(a.nrec + 4 * nd + 2, l, h);
+    const int code = code_of(Q.w);
+    const int begin = code_of(P.w);
     const int skip = code & 0x1fffffff;
     const bool here = next == nd;
     if (a.prefetch && skip < B && lane_is_first_parked(here)) prefetch_l1(a.nrec + 4 * skip);
     bool have = false, ranged = false;
-    V4<R> Q = zero, P = zero, Al = zero, Be = zero;
+    V4<R> Al = zero, Be = zero;
     int rb = 0, re = -1;
     if (here) {
       const bool own = nd >= A;  // the node itself is in this block's window
       next = skip;
       if (skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
-        if (code < 0) {  // single-point leaf (always own): the record holds the point itself
-          Q = l;
-          P = h;
+        if (code < 0) {  // single-point leaf (always own): half A holds the point itself
           if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
           have = true;
           ++c_dir;
-        } else if (code & 0x40000000) {  // depth-32 bucket (always own): all its points
-          ranged = true;
-          rb = begin;
-          re = begin + code_of(ld4(a.nrec + 4 * nd + 3).w) - 1;
-        } else if (gate(l, h, x, a)) {  // far: one aggregate term at the centroid
-          if (own) {
-            ld8(a.nrec + 4 * nd + 2, Q, P);
-            if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
-            have = true;
-            ++c_app;
-          }
-        } else if ((code & 0x20000000) || all_inside(l, h, x, a.thr2_in)) {
-          // a twig (children all leaves) or every descendant opens: range
-          ranged = true;
-          rb = max(begin, bA);
-          re = min(begin + code_of(ld4(a.nrec + 4 * nd + 3).w), bB) - 1;
-          c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
         } else {
-          next = nd + 1;
+          const int cnt = code_of(l.w);
+          const int cls = (code & 0x40000000) ? 3 : classify(l, h, x, a);
+          if (cls == 3) {  // depth-32 bucket (always own): all its points
+            ranged = true;
+            rb = begin;
+            re = begin + cnt - 1;
+          } else if (cls == 1) {  // far: one aggregate term at the centroid
+            if (own) {
+              if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+              have = true;
+              ++c_app;
+            }
+          } else if (cls == 2 || (code & 0x20000000)) {
+            // every descendant opens, or a twig (children all leaves): range
+            ranged = true;
+            rb = max(begin, bA);
+            re = min(begin + cnt, bB) - 1;
+            c_vis += (uint32_t)max(0, min(skip, B) - max(nd + 1, A));
+          } else {
+            next = nd + 1;
+          }
         }
       }
       if (next >= B || next <= nd) next = INT_MAX;
@@ -796,128 +682,12 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
   }
 }
 
-// Software-pipelined work-stream variant: the loads of iteration i+1 (the
-// next node's compact record + its centroid/momentum, or the next range
-// point) are issued before the interaction of iteration i is computed, so one
-// iteration of arithmetic covers the next iteration's memory latency.
-template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT) k_bh_pipe(const BhArgs<R> a) {
-  const int qi = blockIdx.x * kBhNT + threadIdx.x;
-  const bool valid = qi < a.nq;
-  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
-  int out = -1;
-  if (valid) {
-    if (MODE == kBhVel) {
-      x = ld4(a.ev + 2 * qi);
-      if (sizeof(R) == 4)
-        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
-                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
-                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
-      else
-        xs = x;
-      out = qi;
-    } else {
-      const int t = qi;
-      x = ld4(a.squ + t);
-      xs = ld4(a.srec + 2 * t);
-      px = ld4(a.srec + 2 * t + 1);
-      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
-      const int i = a.perm[t] - a.tgt_begin;
-      out = (i >= 0 && i < a.n_tgt) ? i : -1;
-    }
-  }
-  Acc<R> acc;
-#pragma unroll
-  for (int c = 0; c < 12; ++c) acc.v[c] = R(0);
-  uint32_t c_dir = 0, c_app = 0, c_vis = 0;
-  const int m = *a.mp;
-  int next = out >= 0 ? 0 : INT_MAX;
-  int j = 0, je = -1;
-  const V4<R> zero = mk4<R>(0, 0, 0);
-  // prefetched node (record, centroid, momentum[, adjoint aggregates]) and source
-  V4<R> NL = zero, NH = zero, NC = zero, NM = zero, NA = zero, NB = zero;
-  V4<R> SQ = zero, SP = zero, SA = zero, SB = zero;
-  if (next < m) {
-    NL = ld4(a.nrec); NH = ld4(a.nrec + 1); NC = ld4(a.cen); NM = ld4(a.mom);
-    if (MODE == kBhHess) { NA = ld4(a.nadj_a); NB = ld4(a.nadj_b); }
-  }
-  while (__any_sync(0xffffffffu, next < m || j <= je)) {
-    bool have = false;
-    V4<R> Q = zero, P = zero, Al = zero, Be = zero;
-    if (j <= je) {  // continue the pending direct range (point j prefetched)
-      Q = SQ; P = SP; Al = SA; Be = SB;
-      have = true;
-      ++j;
-      ++c_dir;
-    } else if (next < m) {  // visit node `next` (prefetched)
-      const int nd = next;
-      const int code = code_of(NL.w);
-      const int begin = code_of(NH.w);
-      ++c_vis;
-      next = code & 0x1fffffff;
-      if (code < 0) {  // single-point leaf
-        j = begin;
-        je = begin;
-      } else if (code & 0x40000000) {  // depth-32 bucket
-        j = begin;
-        je = begin + code_of(NM.w) - 1;
-      } else if (gate(NL, NH, x, a)) {  // far: one aggregate term
-        Q = NC; P = NM; Al = NA; Be = NB;
-        have = true;
-        ++c_app;
-      } else if (all_inside(NL, NH, x, a.thr2_in)) {  // whole subtree direct
-        j = begin;
-        je = begin + code_of(NM.w) - 1;
-        c_vis += (uint32_t)(next - nd - 1);
-      } else {
-        next = nd + 1;
-      }
-      if (next <= nd) next = INT_MAX;  // never loop on a corrupt skip
-    }
-    // issue the next iteration's loads before this iteration's arithmetic
-    if (j <= je) {
-      SQ = ld4(a.srec + 2 * j);
-      SP = ld4(a.srec + 2 * j + 1);
-      if (MODE == kBhHess) { SA = ld4(a.sadj + 2 * j); SB = ld4(a.sadj + 2 * j + 1); }
-    } else if (next < m) {
-      NL = ld4(a.nrec + 4 * next);
-      NH = ld4(a.nrec + 4 * next + 1);
-      NC = ld4(a.cen + next);
-      NM = ld4(a.mom + next);
-      if (MODE == kBhHess) { NA = ld4(a.nadj_a + next); NB = ld4(a.nadj_b + next); }
-    }
-    if (have) unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Al, Be, a);
-  }
-  if (out >= 0) {
-    const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
-    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
-    for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
-    if (a.per_query) {
-      a.per_query[3 * out] = c_dir;
-      a.per_query[3 * out + 1] = c_app;
-      a.per_query[3 * out + 2] = c_vis;
-    }
-  }
-  if (a.totals) {
-    unsigned long long d = c_dir, p = c_app, v = c_vis;
-    for (int o = 16; o > 0; o >>= 1) {
-      d += __shfl_down_sync(0xffffffffu, d, o);
-      p += __shfl_down_sync(0xffffffffu, p, o);
-      v += __shfl_down_sync(0xffffffffu, v, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(a.totals, d);
-      atomicAdd(a.totals + 1, p);
-      atomicAdd(a.totals + 2, v);
-    }
-  }
-}
 
 // GS_BH_KERNEL: 1 (default) = independent walks (k_bh_ws), 3 = group walk
 // (k_bh_grp), 4 = split launch (group walk for warps whose query box is small
-// against the threshold, independent walks for the rest), 0 = warp-synchronous
-// min-node walk, 2 = pipelined independent walks. Measured (B200, FP32): the
+// against the threshold, independent walks for the rest). The first two
+// designs (a warp-synchronous min-node walk over separate node arrays, and a
+// software-pipelined independent walk) were slower and are retired. Measured (B200, FP32): the
 // group walk wins on config 3 (tube, sigma 5: 3.8 vs 4.6 ms per RHS) and loses
 // on configs 2, 4 and 5, so independent walks are the default.
 static int bh_kernel_choice() {
@@ -941,7 +711,6 @@ template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
   // literal-mean-dot and by-index queries: independent walks only
   const int kind = (a.lmd || a.by_index) ? 1 : bh_kernel_choice();
-  if (kind == 0 || kind == 2) a.ntask = 1;  // single-window kernels
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
@@ -981,11 +750,7 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
                      (double)h[7] / (32.0 * h[4]), (double)(h[6] + h[7]) / h[5]);
     }
   } dbg_print{dbg, dbuf, st, mode, a.nq};
-  if (kind == 2) {
-    if (mode == kBhRhs) k_bh_pipe<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
-    else if (mode == kBhHess) k_bh_pipe<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
-    else k_bh_pipe<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
-  } else if (kind == 1 || kind == 4) {
+  {  // 1 (default), 4 (after the group warps); retired designs 0, 2 map here
     if (a.lmd && mode != kBhVel) {  // the dot scale has no effect on velocities
       if (a.ntask > 1) {
         if (mode == kBhRhs) k_bh_ws<R, kBhRhs, true, true><<<nb, kBhNT, 0, st>>>(a);
@@ -1003,10 +768,6 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
       else if (mode == kBhHess) k_bh_ws<R, kBhHess, false><<<nb, kBhNT, 0, st>>>(a);
       else k_bh_ws<R, kBhVel, false><<<nb, kBhNT, 0, st>>>(a);
     }
-  } else {
-    if (mode == kBhRhs) k_bh<R, kBhRhs><<<nb, kBhNT, 0, st>>>(a);
-    else if (mode == kBhHess) k_bh<R, kBhHess><<<nb, kBhNT, 0, st>>>(a);
-    else k_bh<R, kBhVel><<<nb, kBhNT, 0, st>>>(a);
   }
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
@@ -1015,11 +776,6 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
 template <typename R>
 BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   BhArgs<R> a{};
-  a.meta = t.meta.as<int4>();
-  a.lo = t.lo.as<V4<R>>();
-  a.hi = t.hi.as<V4<R>>();
-  a.cen = t.cen.as<V4<R>>();
-  a.mom = t.mom.as<V4<R>>();
   a.nadj_a = t.nadj_a.as<V4<R>>();
   a.nadj_b = t.nadj_b.as<V4<R>>();
   a.srec = t.srec.as<V4<R>>();

@@ -33,7 +33,7 @@ struct DevTree {
   DBuf counter;         // i32 bottom-up arrival counters
   DBuf lo, hi;          // V4<R> tight AABB (unscaled)
   DBuf cen, mom;        // V4<R> centroid (scaled in FP32) + count / momentum sum + count bits
-  DBuf nrec;            // [cap][4] V4<R> traversal record {lo, code} {hi, begin} {centroid} {momentum}
+  DBuf nrec;            // [cap][4] V4<R> traversal record {centroid|point, code} {momentum|p, begin} {lo, count} {hi}
   DBuf nadj_a, nadj_b;  // V4<R> alpha sum / beta mean
   DBuf psum, msum;      // double4 exact-order-independent aggregates
   DBuf asum, bsum;      // double4

@@ -491,12 +491,11 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 
 // traversal-format node fields: centroid = position_sum * (1 / count)
 // (octree.hpp:35), scaled for FP32; momentum sum; adjoint sum / beta mean.
-// Compact traversal record (2 vec4 per node, one 32-B sector in FP32):
-//   {lo.xyz, code} {hi.xyz, begin} {centroid, count} {momentum sum, count},
+// Traversal record (4 vec4 per node):
+//   {centroid | point, code} {momentum sum | p, begin} {lo.xyz, count} {hi.xyz, -},
 //   code = skip | single-point leaf << 31 | bucket leaf << 30 | twig << 29
-//   (skip < 2^29: tree_build caps n accordingly): 64 B (FP32),
-//   one cache-line half, so a far node's centroid/momentum loads after the
-//   gate hit L1; the point count rides in mom.w.
+//   (skip < 2^29: tree_build caps n accordingly): 64 B (FP32), loaded whole
+//   by two 256-bit loads; the first half is the node's interaction unit.
 __device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
 __device__ __forceinline__ double ival(double, int v) { return (double)v; }
 
@@ -512,23 +511,6 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
   const int cnt = mi.z - mi.y + 1;
   const double inv = 1.0 / cnt;
   const double4 a = s0[i], b = s1[i];
-  if (mode == 0 && nrec) {
-    const bool leaf = mi.w & 1;
-    // twig: an internal node whose children are all leaves (subtree = itself +
-    // its children); opening it makes every point of it direct, no child gated
-    const bool twig = !leaf && nchild && mi.x - (int)i - 1 == nchild[i];
-    const int code = mi.x | ((leaf && cnt == 1) ? (int)0x80000000u : 0) |
-                     ((leaf && cnt > 1) ? 0x40000000 : 0) | (twig ? 0x20000000 : 0);
-    // a single-point leaf is always direct (leaf-first, bh_kernel.cpp:40-45), so
-    // its record carries the point itself -- interaction coords and momentum --
-    // and the traversal needs no second, dependent load for it
-    V4<R> l = (leaf && cnt == 1) ? ld4(srec + 2 * mi.y) : ld4(lo + i);
-    V4<R> h = (leaf && cnt == 1) ? ld4(srec + 2 * mi.y + 1) : ld4(hi + i);
-    l.w = ival(R(0), code);
-    h.w = ival(R(0), mi.y);
-    st4(nrec + 4 * i, l);
-    st4(nrec + 4 * i + 1, h);
-  }
   if (mode == 0) {
     double cx = __dmul_rn(a.x, inv), cy = __dmul_rn(a.y, inv), cz = __dmul_rn(a.z, inv);
     const V4<R> cen = scaled ? mk4<R>((R)fmaf((float)kap, (float)cx, -(float)(kap * c0x)),
@@ -538,9 +520,30 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
     const V4<R> mom = mk4<R>(R(b.x), R(b.y), R(b.z), ival(R(0), cnt));
     st4(o0 + i, cen);
     st4(o1 + i, mom);
-    if (nrec && !((mi.w & 1) && cnt == 1)) {  // the record's far-field half
-      st4(nrec + 4 * i + 2, cen);
-      st4(nrec + 4 * i + 3, mom);
+    if (nrec) {
+      const bool leaf = mi.w & 1;
+      const bool single = leaf && cnt == 1;
+      // twig: an internal node whose children are all leaves (subtree = itself +
+      // its children); opening it makes every point of it direct, no child gated
+      const bool twig = !leaf && nchild && mi.x - (int)i - 1 == nchild[i];
+      const int code = mi.x | (single ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0) |
+                       (twig ? 0x20000000 : 0);
+      // half A = the unit this node contributes: its centroid and momentum sum,
+      // or -- a single-point leaf being always direct (leaf-first,
+      // bh_kernel.cpp:40-45) -- the point itself; the walk loads it straight
+      // into the interaction operands. Half B = the tight box for the gate.
+      V4<R> ua = single ? ld4(srec + 2 * mi.y) : cen;
+      V4<R> ub = single ? ld4(srec + 2 * mi.y + 1) : mom;
+      ua.w = ival(R(0), code);
+      ub.w = ival(R(0), mi.y);
+      st4(nrec + 4 * i, ua);
+      st4(nrec + 4 * i + 1, ub);
+      if (!single) {
+        V4<R> l = ld4(lo + i);
+        l.w = ival(R(0), cnt);
+        st4(nrec + 4 * i + 2, l);
+        st4(nrec + 4 * i + 3, ld4(hi + i));
+      }
     }
   } else {
     st4(o0 + i, mk4<R>(R(a.x), R(a.y), R(a.z)));
