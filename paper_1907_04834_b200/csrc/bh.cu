@@ -64,8 +64,7 @@ constexpr bool kLoadWholeRecord = GS_BH_WHOLE_RECORD != 0;
 
 template <typename R>
 struct BhArgs {
-  const V4<R>* nadj_a;
-  const V4<R>* nadj_b;
+  const V4<R>* nadj;  // [m][2] {alpha sum, beta mean} (HESS)
   const V4<R>* nrec;  // [m][4] node records {unit, code} {unit, begin} {lo, count} {hi}
   const V4<R>* srec;  // [n][2] interaction coords (scaled FP32), p
   const V4<R>* squ;   // [n] unscaled q
@@ -386,7 +385,6 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     GS_WS_COUNT(++dbg_iter);
     bool have = false;
     V4<R> Q, P, Al, Be;  // this iteration's unit (read only when have)
-    if (MODE == kBhHess) Al = Be = zero;
     R dsc = R(1);
     if (j > je && next < m) {
       GS_WS_COUNT(++dbg_visit);
@@ -397,6 +395,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       V4<R> l, h;
       ld8(a.nrec + 4 * nd, Q, P);
       ld8(a.nrec + 4 * nd + 2, l, h);
+      if (MODE == kBhHess) ld8(a.nadj + 2 * nd, Al, Be);  // the unit's adjoints (leaf or node)
       const int code = code_of(Q.w);
       const int begin = code_of(P.w);
       const int skip = code & 0x1fffffff;
@@ -406,7 +405,6 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
       if (!WIN || skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
         if (code < 0) {  // single-point leaf (always own): half A holds the point itself
-          if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
           have = true;
           ++c_dir;
         } else {
@@ -418,7 +416,6 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
             c_dir += (uint32_t)cnt;  // counted once per range
           } else if (cls == 1) {  // far: one aggregate term at the centroid
             if (own) {
-              if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
               if (LMD) dsc = R(1) / R(cnt);
               have = true;
               ++c_app;
@@ -613,7 +610,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
       if (skip > A) {  // the subtree reaches into the window (else: pass it by)
         c_vis += own;
         if (code < 0) {  // single-point leaf (always own): half A holds the point itself
-          if (MODE == kBhHess) { Al = ld4(a.sadj + 2 * begin); Be = ld4(a.sadj + 2 * begin + 1); }
+          if (MODE == kBhHess) ld8(a.nadj + 2 * nd, Al, Be);
           have = true;
           ++c_dir;
         } else {
@@ -625,7 +622,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
             re = begin + cnt - 1;
           } else if (cls == 1) {  // far: one aggregate term at the centroid
             if (own) {
-              if (MODE == kBhHess) { Al = ld4(a.nadj_a + nd); Be = ld4(a.nadj_b + nd); }
+              if (MODE == kBhHess) ld8(a.nadj + 2 * nd, Al, Be);
               have = true;
               ++c_app;
             }
@@ -776,8 +773,7 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
 template <typename R>
 BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   BhArgs<R> a{};
-  a.nadj_a = t.nadj_a.as<V4<R>>();
-  a.nadj_b = t.nadj_b.as<V4<R>>();
+  a.nadj = t.nadj.as<V4<R>>();
   a.srec = t.srec.as<V4<R>>();
   a.nrec = t.nrec.as<V4<R>>();
   a.squ = t.squ.as<V4<R>>();

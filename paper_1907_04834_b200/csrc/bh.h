@@ -34,7 +34,7 @@ struct DevTree {
   DBuf lo, hi;          // V4<R> tight AABB (unscaled)
   DBuf cen, mom;        // V4<R> centroid (scaled in FP32) + count / momentum sum + count bits
   DBuf nrec;            // [cap][4] V4<R> traversal record {centroid|point, code} {momentum|p, begin} {lo, count} {hi}
-  DBuf nadj_a, nadj_b;  // V4<R> alpha sum / beta mean
+  DBuf nadj;            // [cap][2] V4<R> {alpha sum, beta mean} per node
   DBuf psum, msum;      // double4 exact-order-independent aggregates
   DBuf asum, bsum;      // double4
   DBuf root;            // double[6] padded root box

@@ -546,9 +546,12 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
       }
     }
   } else {
-    st4(o0 + i, mk4<R>(R(a.x), R(a.y), R(a.z)));
+    // interleaved {alpha sum, beta mean} per node (one 256-bit load in the walk);
+    // for a single-point leaf these are exactly the point's alpha and beta
+    st4(o0 + 2 * i, mk4<R>(R(a.x), R(a.y), R(a.z)));
     // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
-    st4(o1 + i, mk4<R>(R(__dmul_rn(inv, b.x)), R(__dmul_rn(inv, b.y)), R(__dmul_rn(inv, b.z))));
+    st4(o0 + 2 * i + 1, mk4<R>(R(__dmul_rn(inv, b.x)), R(__dmul_rn(inv, b.y)), R(__dmul_rn(inv, b.z))));
+    (void)o1;
   }
 }
 
@@ -855,18 +858,17 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   GS_TRY_INT(t.sadj.ensure(2 * vb * n));
   GS_TRY_INT(t.asum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.bsum.ensure(sizeof(double4) * cap));
-  GS_TRY_INT(t.nadj_a.ensure(vb * cap));
-  GS_TRY_INT(t.nadj_b.ensure(vb * cap));
+  GS_TRY_INT(t.nadj.ensure(2 * vb * cap));
   const int nb = nblocks(n, kNT), mb = nblocks(cap, kNT);
   GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
   if (prec == kF32) {
     k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
     k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<float4>(), t.nadj_b.as<float4>());
+    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<float4>(), nullptr);
   } else {
     k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
     k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj_a.as<double4>(), t.nadj_b.as<double4>());
+    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<double4>(), nullptr);
   }
   GS_CUDA_OK(cudaGetLastError());
   t.adj_valid = true;
