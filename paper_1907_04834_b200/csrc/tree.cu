@@ -22,6 +22,8 @@
 #include <chrono>
 #include <cstdlib>
 
+#include <cuda/atomic>
+
 #include "bh.h"
 
 namespace gsb {
@@ -465,10 +467,11 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
   for (;;) {
     const int par = parent[node];
     if (par < 0) return;
-    __threadfence();
-    const int old = atomicAdd(counter + par, 1);
+    // acq_rel arrival: this child's sums are released to, and the siblings'
+    // acquired by, whichever child arrives last (no separate fences)
+    cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
+    const int old = arrive.fetch_add(1, cuda::memory_order_acq_rel);
     if (old != nchild[par] - 1) return;
-    __threadfence();
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
