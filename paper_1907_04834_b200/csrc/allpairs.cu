@@ -29,6 +29,9 @@
 namespace gsb {
 
 constexpr int kTile = 256;
+#ifndef GS_HESS_MINB
+#define GS_HESS_MINB 1
+#endif
 
 // ----------------------------------------------------------------------------
 // forward RHS partials: A = sum_j g p_j, B = sum_j (p_i.p_j) g d'_ij
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(256) k_group_boxes(const float4* __restrict__ 
 // Packed (FFMA2) Hessian-product kernel: TPT targets as TPT/2 pairs; 40
 // packed FP32 + 2 MUFU issue slots per two (target, source) pairs.
 template <int TPT, int NT>
-__global__ void __launch_bounds__(NT) k_hess_f32x2(const float4* __restrict__ rec,
+__global__ void __launch_bounds__(NT, GS_HESS_MINB) k_hess_f32x2(const float4* __restrict__ rec,
                                                    const float4* __restrict__ adj, int n,
                                                    int tgt_begin, int n_tgt, int chunk, float kap,
                                                    float kc0x, float kc0y, float kc0z, float c1,
