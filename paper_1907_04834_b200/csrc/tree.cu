@@ -127,47 +127,9 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
 }
 
 // ------------------------------------------------------------ radix sort ---
-// Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, 3 kernels per
-// pass: per-tile digit histograms, one exclusive scan (digit-major), and a
-// stable scatter that ranks keys inside a tile with warp match/popc.
+// Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, one-sweep
+// passes (below): stable within-tile ranking with warp match/popc.
 constexpr int kRsNT = 256;  // items per thread (tile = 256 * IPT keys): template parameter
-
-template <int kRsIPT>
-__global__ void __launch_bounds__(kRsNT) k_rs_hist(const uint64_t* keys, int64_t n, int shift,
-                                                  unsigned* ghist, int ntiles) {
-  __shared__ unsigned h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * (kRsNT * kRsIPT);
-#pragma unroll 4
-  for (int r = 0; r < kRsIPT; ++r) {
-    const int64_t i = base + r * kRsNT + threadIdx.x;
-    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
-  }
-  __syncthreads();
-  ghist[(int64_t)blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];  // tile-major
-}
-
-// ghist[tile][digit] -> exclusive prefix over tiles per digit, one warp per
-// digit (256 warps); row ntiles receives the digit totals (the scatter forms
-// the digit base offsets from them).
-__global__ void __launch_bounds__(256) k_rs_digit_scan(unsigned* ghist, int ntiles) {
-  const int d = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  unsigned run = 0;
-  for (int t0 = 0; t0 < ntiles; t0 += 32) {
-    const int t = t0 + lane;
-    const unsigned v = t < ntiles ? ghist[(int64_t)t * 256 + d] : 0u;
-    unsigned x = v;  // inclusive warp scan
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (t < ntiles) ghist[(int64_t)t * 256 + d] = run + x - v;
-    run += __shfl_sync(0xffffffffu, x, 31);
-  }
-  if (lane == 0) ghist[(int64_t)ntiles * 256 + d] = run;
-}
 
 // exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
 __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
@@ -192,16 +154,57 @@ __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
   }
 }
 
+// ---- one-sweep passes ---------------------------------------------------------
+// Digit histograms are independent of the key order, so ONE kernel counts every
+// pass's digits up front (k0: p0 passes, then k1: p1 passes); each pass is then
+// ONE kernel: a tile takes its id from an atomic counter (so every earlier tile
+// has started), ranks its keys with warp match_any, publishes its per-digit
+// count, and looks back over earlier tiles' published counts / inclusive
+// prefixes (decoupled look-back, one 32-bit status word per tile and digit:
+// flag << 30 | count) for its global offsets, then scatters. 1 launch per pass
+// instead of 3, and no ntiles x 256 prefix pass.
+constexpr unsigned kRsFlagAgg = 1u << 30, kRsFlagPrefix = 2u << 30, kRsCountMask = (1u << 30) - 1;
+
 template <int kRsIPT>
-__global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const int* vin,
-                                                     uint64_t* kout, int* vout, int64_t n,
-                                                     int shift, const unsigned* ghist,
-                                                     int ntiles) {
-  __shared__ unsigned wh[kRsNT / 32][256];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
+__global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* k0, int p0, const uint64_t* k1,
+                                                      int p1, int64_t n, unsigned* hist) {
+  extern __shared__ unsigned hs[];  // (p0 + p1) x 256
+  const int np = p0 + p1;
+  for (int t = threadIdx.x; t < np * 256; t += kRsNT) hs[t] = 0;
   __syncthreads();
-  const int64_t seg = (int64_t)blockIdx.x * (kRsNT * kRsIPT) + (int64_t)warp * (32 * kRsIPT);
+  const int64_t base = (int64_t)blockIdx.x * (kRsNT * kRsIPT);
+  for (int r = 0; r < kRsIPT; ++r) {
+    const int64_t i = base + r * kRsNT + threadIdx.x;
+    if (i >= n) break;
+    if (p0) {
+      const uint64_t k = k0[i];
+      for (int q = 0; q < p0; ++q) atomicAdd(&hs[q * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
+    }
+    if (p1) {
+      const uint64_t k = k1[i];
+      for (int q = 0; q < p1; ++q) atomicAdd(&hs[(p0 + q) * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < np * 256; t += kRsNT)
+    if (hs[t]) atomicAdd(&hist[t], hs[t]);
+}
+
+template <int kRsIPT>
+__global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, const int* vin,
+                                                      uint64_t* kout, int* vout, int64_t n,
+                                                      int shift, const unsigned* dig_tot,
+                                                      unsigned* desc, unsigned* tile_ctr) {
+  __shared__ unsigned wh[kRsNT / 32][256];
+  __shared__ unsigned base[256];
+  __shared__ int s_tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
+  for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
+  base[threadIdx.x] = dig_tot[threadIdx.x];
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t seg = (int64_t)tile * (kRsNT * kRsIPT) + (int64_t)warp * (32 * kRsIPT);
   uint64_t key[kRsIPT];
   int val[kRsIPT];
   unsigned loc[kRsIPT];
@@ -225,10 +228,8 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
     }
     __syncwarp();
   }
-  // digit base offsets: exclusive prefix of the digit totals (row ntiles)
-  __shared__ unsigned base[256];
-  base[threadIdx.x] = ghist[(int64_t)ntiles * 256 + threadIdx.x];
   __syncthreads();
+  // digit base offsets (exclusive prefix of the digit totals) ...
   for (int o = 1; o < 256; o <<= 1) {
     const unsigned v = threadIdx.x >= o ? base[threadIdx.x - o] : 0u;
     __syncthreads();
@@ -236,8 +237,27 @@ __global__ void __launch_bounds__(kRsNT) k_rs_scatter(const uint64_t* kin, const
     __syncthreads();
   }
   {
+    // ... and this tile's offset inside each digit by look-back over earlier tiles
     const unsigned d = threadIdx.x;
-    unsigned run = ghist[(int64_t)blockIdx.x * 256 + d] + base[d] - ghist[(int64_t)ntiles * 256 + d];
+    unsigned tot = 0;
+    for (int w = 0; w < kRsNT / 32; ++w) tot += wh[w][d];
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
+    unsigned excl = 0;
+    if (tile == 0) {
+      mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
+    } else {
+      mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
+      for (int t = tile - 1;;) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)t * 256 + d]);
+        const unsigned v = prev.load(cuda::memory_order_relaxed);
+        if (!(v & (kRsFlagAgg | kRsFlagPrefix))) continue;  // that tile has not published yet
+        excl += v & kRsCountMask;
+        if (v & kRsFlagPrefix) break;
+        --t;
+      }
+      mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
+    }
+    unsigned run = base[d] - dig_tot[d] + excl;
     for (int w = 0; w < kRsNT / 32; ++w) {
       const unsigned t = wh[w][d];
       wh[w][d] = run;
@@ -677,17 +697,24 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   }();
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
   const int ntiles = nblocks(n, kRsNT * ipt);
-  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
-  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift) {
-    unsigned* gh = t.hist.as<unsigned>();
-    if (ipt == 16) k_rs_hist<16><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
-    else if (ipt == 8) k_rs_hist<8><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
-    else k_rs_hist<4><<<ntiles, kRsNT, 0, st>>>(ki, n, shift, gh, ntiles);
-    k_rs_digit_scan<<<32, 256, 0, st>>>(gh, ntiles);
-    if (ipt == 16) k_rs_scatter<16><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
-    else if (ipt == 8) k_rs_scatter<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
-    else k_rs_scatter<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, gh, ntiles);
+  // one-sweep scratch: 13 digit histograms, 13 tile counters, 13 x ntiles x 256
+  // look-back status words -- zeroed by one memset
+  constexpr int kPasses = 13;
+  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256;
+  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
+  GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
+  unsigned* hist = t.hist.as<unsigned>();
+  unsigned* ctr = hist + kPasses * 256;
+  unsigned* desc = ctr + 32;
+  if (ipt == 16) k_rs_hist_all<16><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  else if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q) {
+    unsigned* dq = desc + (size_t)q * ntiles * 256;
+    if (ipt == 16) k_rs_onesweep<16><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
+    else if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
+    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
   };
   {
     const uint64_t* ka = t.key_lo.as<uint64_t>();
@@ -695,7 +722,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     for (int p = 0; p < 5; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_lo.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.tmp_v2.as<int>() : t.tmp_v.as<int>();
-      pass(ka, va, kb, vb, 8 * p);
+      pass(ka, va, kb, vb, 8 * p, p);
       ka = kb;
       va = vb;
     }
@@ -707,7 +734,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     for (int p = 0; p < 8; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      pass(ka, va, kb, vb, 8 * p);
+      pass(ka, va, kb, vb, 8 * p, 5 + p);
       ka = kb;
       va = vb;
     }
@@ -797,18 +824,22 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
     k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
-  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * 256 * (ntiles + 1)));
+  const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;
+  GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
+  GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
+  unsigned* hist = t.hist.as<unsigned>();
+  unsigned* ctr = hist + 8 * 256;
+  unsigned* desc = ctr + 32;
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist);
   const uint64_t* ka = t.key_hi.as<uint64_t>();
   const int* va = nullptr;
   for (int p = 0; p < 8; ++p) {  // (key_hi, index) -> (tmp_k, tmp_v) -> (skey_hi, perm) -> ...
     uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
     int* vb2 = (p & 1) ? t.perm.as<int>() : t.tmp_v.as<int>();
-    unsigned* gh = t.hist.as<unsigned>();
-    if (ipt == 8) k_rs_hist<8><<<ntiles, kRsNT, 0, st>>>(ka, n, 8 * p, gh, ntiles);
-    else k_rs_hist<4><<<ntiles, kRsNT, 0, st>>>(ka, n, 8 * p, gh, ntiles);
-    k_rs_digit_scan<<<32, 256, 0, st>>>(gh, ntiles);
-    if (ipt == 8) k_rs_scatter<8><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, gh, ntiles);
-    else k_rs_scatter<4><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, gh, ntiles);
+    unsigned* dq = desc + (size_t)p * ntiles * 256;
+    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
+    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
     ka = kb;
     va = vb2;
   }
