@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
   int j = 0, je = -1;  // pending direct range
   const V4<R> zero = mk4<R>(0, 0, 0);
 #ifdef GS_BH_WS_STATS
-  unsigned dbg_iter = 0, dbg_visit = 0, dbg_unit = 0;
+  unsigned dbg_iter = 0, dbg_visit = 0, dbg_unit = 0, dbg_leaf = 0, dbg_far = 0, dbg_open = 0,
+           dbg_range = 0, dbg_rpts = 0;
 #define GS_WS_COUNT(x) (x)
 #else
 #define GS_WS_COUNT(x) ((void)0)
@@ -407,9 +408,11 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
         if (code < 0) {  // single-point leaf (always own): half A holds the point itself
           have = true;
           ++c_dir;
+          GS_WS_COUNT(++dbg_leaf);
         } else {
           const int cnt = code_of(l.w);
           const int cls = (code & 0x40000000) ? 3 : classify(l, h, x, a);
+          GS_WS_COUNT(cls == 1 ? ++dbg_far : (cls == 2 || cls == 3 || (code & 0x20000000)) ? (++dbg_range, dbg_rpts += cnt) : ++dbg_open);
           if (cls == 3) {  // depth-32 bucket (always own): all its points
             j = begin;
             je = begin + cnt - 1;
@@ -455,15 +458,18 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
 #ifdef GS_BH_WS_STATS
   if (a.dbg) {  // GS_BH_DEBUG (build with -DGS_BH_WS_STATS): warp iterations, lane visits, lane units
     unsigned long long v = dbg_visit, u = dbg_unit;
+    unsigned long long ex[5] = {dbg_leaf, dbg_far, dbg_open, dbg_range, dbg_rpts};
     for (int o = 16; o > 0; o >>= 1) {
       v += __shfl_down_sync(0xffffffffu, v, o);
       u += __shfl_down_sync(0xffffffffu, u, o);
+      for (int k = 0; k < 5; ++k) ex[k] += __shfl_down_sync(0xffffffffu, ex[k], o);
     }
     if ((threadIdx.x & 31) == 0) {
       atomicAdd(a.dbg + 4, 1ull);
       atomicAdd(a.dbg + 5, (unsigned long long)dbg_iter);
       atomicAdd(a.dbg + 6, v);
       atomicAdd(a.dbg + 7, u);
+      for (int k = 0; k < 5; ++k) atomicAdd(a.dbg + 8 + k, ex[k]);
     }
   }
 #endif
@@ -711,9 +717,9 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
-  if (dbg && !dbuf) cudaMalloc(&dbuf, 64);
+  if (dbg && !dbuf) cudaMalloc(&dbuf, 128);
   if (dbg) {
-    cudaMemsetAsync(dbuf, 0, 64, st);
+    cudaMemsetAsync(dbuf, 0, 128, st);
     a.dbg = dbuf;
   }
   if (kind == 3 || kind == 4) {
@@ -738,13 +744,16 @@ int launch(int mode, BhArgs<R> a, cudaStream_t st) {
     int mode, nq;
     ~DbgPrint() {
       if (!on) return;
-      unsigned long long h[8];
+      unsigned long long h[16];
       cudaMemcpyAsync(h, buf, sizeof h, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      if (h[4])
-        std::fprintf(stderr, "[bh ws mode %d nq %d] warps %llu iters/warp %.1f visits/lane %.1f units/lane %.1f simt %.1f\n",
-                     mode, nq, h[4], (double)h[5] / h[4], (double)h[6] / (32.0 * h[4]),
-                     (double)h[7] / (32.0 * h[4]), (double)(h[6] + h[7]) / h[5]);
+      if (h[4]) {
+        const double L = 32.0 * h[4];
+        std::fprintf(stderr, "[bh ws mode %d nq %d] warps %llu iters/warp %.1f visits/lane %.1f units/lane %.1f simt %.1f"
+                     " | leaf %.1f far %.1f open %.1f range %.1f (pts %.1f)\n",
+                     mode, nq, h[4], (double)h[5] / h[4], (double)h[6] / L, (double)h[7] / L,
+                     (double)(h[6] + h[7]) / h[5], h[8] / L, h[9] / L, h[10] / L, h[11] / L, h[12] / L);
+      }
     }
   } dbg_print{dbg, dbuf, st, mode, a.nq};
   {  // 1 (default), 4 (after the group warps); retired designs 0, 2 map here
