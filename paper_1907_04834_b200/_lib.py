@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgeoshoot_b200.so")
+# GS_LIB_PATH: load a variant build instead (kernel experiments, tools/)
+LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(HERE, "libgeoshoot_b200.so")
 
 # gs_status (include/geoshoot_b200.h)
 GS_OK = 0
