@@ -460,6 +460,19 @@ def run_ours(args):
             "kind": kind, "pair_interactions_per_s": rate,
             "sample": f"{used} concurrent reference hamiltonian_gradients calls at N={args.cpu_sample} "
                       f"(FP64, serial by construction per call), extrapolated to N={N} by N^2 x 4 RHS/step"}
+        if "bh" in line and kind == "reference":
+            # the reference's Barnes-Hut path on the same flow: one Euler step of
+            # shoot_forward (serial octree build + one parallel_for RHS,
+            # bh_kernel.cpp:193-210) at the full N; an RK4 step is 4 of them
+            import oracle
+            t0 = time.perf_counter()
+            oracle.ref().shoot_forward(q0, p0, SIGMA, 1, backend=1)
+            t_rhs = time.perf_counter() - t0
+            line["bh"]["cpu_baseline"] = {
+                "value": 1.0 / (4.0 * t_rhs), "unit": "flow steps/s", "cores": threads,
+                "kind": "reference", "seconds_per_rhs": t_rhs,
+                "sample": f"reference shoot_forward, Barnes-Hut, T=1 (one tree build + one RHS) at "
+                          f"N={N}, FP64, GEOSHOOT_THREADS default ({threads} host threads); x4 RHS per RK4 step"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
