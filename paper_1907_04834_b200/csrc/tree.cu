@@ -195,8 +195,13 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
                                                       unsigned* desc, unsigned* tile_ctr) {
-  __shared__ unsigned wh[kRsNT / 32][256];
-  __shared__ unsigned base[256];
+  constexpr int kTile = kRsNT * kRsIPT;
+  __shared__ unsigned wh[kRsNT / 32][256];  // per-warp digit counts -> offsets within the tile's digit run
+  __shared__ unsigned base[256];            // global digit starts (scan of dig_tot)
+  __shared__ unsigned ts[256];              // tile digit counts -> tile-local digit starts
+  __shared__ unsigned gofs[256];            // global position of tile-local slot 0 of each digit run
+  __shared__ uint64_t sk[kTile];            // the tile in digit order (coalesced write-out)
+  __shared__ int sv[kTile];
   __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
@@ -204,7 +209,8 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   base[threadIdx.x] = dig_tot[threadIdx.x];
   __syncthreads();
   const int tile = s_tile;
-  const int64_t seg = (int64_t)tile * (kRsNT * kRsIPT) + (int64_t)warp * (32 * kRsIPT);
+  const int64_t t0 = (int64_t)tile * kTile;
+  const int64_t seg = t0 + (int64_t)warp * (32 * kRsIPT);
   uint64_t key[kRsIPT];
   int val[kRsIPT];
   unsigned loc[kRsIPT];
@@ -229,50 +235,68 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
     __syncwarp();
   }
   __syncthreads();
-  // digit base offsets (exclusive prefix of the digit totals) ...
+  const unsigned d = threadIdx.x;
+  unsigned tot = 0;
+  for (int w = 0; w < kRsNT / 32; ++w) {
+    const unsigned t = wh[w][d];
+    wh[w][d] = tot;
+    tot += t;
+  }
+  // publish this tile's count for digit d as early as possible (look-back)
+  cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
+  if (tile != 0) mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
+  ts[d] = tot;
+  __syncthreads();
+  // inclusive scans over digits: global digit totals and this tile's counts
   for (int o = 1; o < 256; o <<= 1) {
-    const unsigned v = threadIdx.x >= o ? base[threadIdx.x - o] : 0u;
+    const unsigned v1 = d >= (unsigned)o ? base[d - o] : 0u, v2 = d >= (unsigned)o ? ts[d - o] : 0u;
     __syncthreads();
-    base[threadIdx.x] += v;
+    base[d] += v1;
+    ts[d] += v2;
     __syncthreads();
   }
-  {
-    // ... and this tile's offset inside each digit by look-back over earlier tiles
-    const unsigned d = threadIdx.x;
-    unsigned tot = 0;
-    for (int w = 0; w < kRsNT / 32; ++w) tot += wh[w][d];
-    cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
-    unsigned excl = 0;
-    if (tile == 0) {
-      mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
-    } else {
-      mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
-      for (int t = tile - 1;;) {
-        cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)t * 256 + d]);
-        const unsigned v = prev.load(cuda::memory_order_relaxed);
-        if (!(v & (kRsFlagAgg | kRsFlagPrefix))) continue;  // that tile has not published yet
-        excl += v & kRsCountMask;
-        if (v & kRsFlagPrefix) break;
-        --t;
-      }
-      mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
+  const unsigned tstart = ts[d] - tot;
+  // this tile's offset inside digit d: decoupled look-back over earlier tiles
+  unsigned excl = 0;
+  if (tile == 0) {
+    mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
+  } else {
+    for (int t = tile - 1;;) {
+      cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)t * 256 + d]);
+      const unsigned v = prev.load(cuda::memory_order_relaxed);
+      if (!(v & (kRsFlagAgg | kRsFlagPrefix))) continue;  // that tile has not published yet
+      excl += v & kRsCountMask;
+      if (v & kRsFlagPrefix) break;
+      --t;
     }
-    unsigned run = base[d] - dig_tot[d] + excl;
-    for (int w = 0; w < kRsNT / 32; ++w) {
-      const unsigned t = wh[w][d];
-      wh[w][d] = run;
-      run += t;
+    mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
+  }
+  gofs[d] = base[d] - dig_tot[d] + excl - tstart;
+  __syncthreads();  // every thread's ts[] read is done
+  ts[d] = tstart;
+  __syncthreads();
+  // stage the tile in (digit, rank) order ...
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    if (seg + r * 32 + lane < n) {
+      const unsigned dd = (unsigned)(key[r] >> shift) & 255u;
+      const unsigned slot = ts[dd] + wh[warp][dd] + loc[r];
+      sk[slot] = key[r];
+      sv[slot] = val[r];
     }
   }
   __syncthreads();
+  // ... and write it out: consecutive slots of one digit run are consecutive
+  // output positions (coalesced), instead of 12-B scatters per key
+  const int cnt = n - t0 < kTile ? (int)(n - t0) : kTile;
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
-    const int64_t i = seg + r * 32 + lane;
-    if (i < n) {
-      const unsigned d = (unsigned)(key[r] >> shift) & 255u;
-      const unsigned pos = wh[warp][d] + loc[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+    const int i = r * kRsNT + threadIdx.x;
+    if (i < cnt) {
+      const uint64_t k = sk[i];
+      const unsigned pos = gofs[(unsigned)(k >> shift) & 255u] + (unsigned)i;
+      kout[pos] = k;
+      vout[pos] = sv[i];
     }
   }
 }
@@ -693,7 +717,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   static const int ipt_env = [] {
     const char* e = std::getenv("GS_RS_IPT");
     const int v = e ? std::atoi(e) : 0;
-    return (v == 4 || v == 8 || v == 16) ? v : 0;
+    return (v == 4 || v == 8) ? v : 0;
   }();
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
   const int ntiles = nblocks(n, kRsNT * ipt);
@@ -707,13 +731,11 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   unsigned* hist = t.hist.as<unsigned>();
   unsigned* ctr = hist + kPasses * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 16) k_rs_hist_all<16><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
-  else if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
   else k_rs_hist_all<4><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
   auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q) {
     unsigned* dq = desc + (size_t)q * ntiles * 256;
-    if (ipt == 16) k_rs_onesweep<16><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
-    else if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
+    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
     else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
   };
   {
