@@ -84,6 +84,7 @@ struct BhArgs {
   int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
   int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
   int by_index;        // RHS: queries are ev[0 .. nq) (a shard's records), not leaf order
+  int* sm_ctr;         // non-null: blocks claim SM-local contiguous query blocks (claim_block)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
   uint32_t* per_query;
@@ -326,11 +327,40 @@ constexpr int ws_min_blocks() {
                                           : (MODE == kBhHess ? GS_BH_WS_HESS_MINB : 5));
 }
 
+// Query block of this CTA. With sm_ctr, the query blocks are dealt out in
+// contiguous runs per SM (SM s owns blocks [s*per, (s+1)*per), claimed in
+// order through its counter; an SM whose run is exhausted takes blocks from
+// the others' runs): the warps resident on one SM then walk Morton-adjacent
+// queries and share their near-field node records in L1. Each block id is
+// claimed exactly once, so every query is walked once, by one thread.
+__device__ __forceinline__ int claim_block(int* sm_ctr, int nblk) {
+  __shared__ int s_blk;
+  if (threadIdx.x == 0) {
+    unsigned sm, nsm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    nsm = min(nsm, 1024u);
+    const int per = (nblk + (int)nsm - 1) / (int)nsm;
+    int b = -1;
+    for (unsigned k = 0; k < nsm && b < 0; ++k) {
+      const unsigned s = (sm + k) % nsm;
+      const int lo = (int)s * per;
+      if (lo >= nblk) continue;
+      const int c = atomicAdd(sm_ctr + s, 1);
+      if (c < per && lo + c < nblk) b = lo + c;
+    }
+    s_blk = b;
+  }
+  __syncthreads();
+  return s_blk;
+}
+
 // WIN: node windows (ntask > 1); the single-window instantiation drops the
 // window bookkeeping (registers and instructions) for large N.
 template <typename R, int MODE, bool WIN, bool LMD = false>
 __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_ws(const BhArgs<R> a) {
-  const int qi = blockIdx.x * kBhNT + threadIdx.x;
+  const int blk = (!WIN && a.sm_ctr) ? claim_block(a.sm_ctr, gridDim.x) : (int)blockIdx.x;
+  const int qi = blk * kBhNT + threadIdx.x;
   const bool valid = qi < a.nq;
   V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
   int out = -1;
@@ -838,8 +868,24 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
 
 int bh_traverse(const Device&, int prec, DevTree& t, double sigma, double thr, const BhQuery& q,
                 cudaStream_t st) {
-  if (prec == kF32) return launch<float>(q.mode, make_args<float>(t, sigma, thr, q), st);
-  return launch<double>(q.mode, make_args<double>(t, sigma, thr, q), st);
+  static const int sm_local = [] {
+    const char* e = std::getenv("GS_BH_SM_LOCAL");
+    return e ? std::atoi(e) : 1;
+  }();
+  int* ctr = nullptr;
+  if (sm_local && q.ntask <= 1) {
+    GS_TRY_INT(t.sm_ctr.ensure(4 * 1024));
+    GS_CUDA_OK(cudaMemsetAsync(t.sm_ctr.ptr, 0, 4 * 1024, st));
+    ctr = t.sm_ctr.as<int>();
+  }
+  if (prec == kF32) {
+    BhArgs<float> a = make_args<float>(t, sigma, thr, q);
+    a.sm_ctr = ctr;
+    return launch<float>(q.mode, a, st);
+  }
+  BhArgs<double> a = make_args<double>(t, sigma, thr, q);
+  a.sm_ctr = ctr;
+  return launch<double>(q.mode, a, st);
 }
 
 // Node windows per query: a latency-bound walk needs many resident warps, and

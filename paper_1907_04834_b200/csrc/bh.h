@@ -41,6 +41,7 @@ struct DevTree {
   // radix-sort scratch
   DBuf tmp_k, tmp_v, tmp_v2, hist;
   DBuf scan_tmp;
+  DBuf sm_ctr;          // i32 [1024] per-SM query-block counters of the walk (k_bh_ws)
   DBuf scal;
   KernelConsts kc{};
   double thr = 0.0;
