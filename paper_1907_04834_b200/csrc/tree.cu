@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
 // ------------------------------------------------------------ radix sort ---
 // Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, one-sweep
 // passes (below): stable within-tile ranking with warp match/popc.
-constexpr int kRsNT = 256;  // items per thread (tile = 256 * IPT keys): template parameter
+constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a template parameter
 
 // exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
 __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
