@@ -893,15 +893,37 @@ int bh_traverse(const Device&, int prec, DevTree& t, double sigma, double thr, c
 // per 32 queries leaves the SMs mostly idle. Splitting the pre-order node
 // array into K windows (each block walks its queries through one window;
 // the epilogue folds the K partials in fixed order) multiplies the warps by K.
-int bh_tasks(int64_t nq) {
+constexpr int kMaxBhTasks = 64;
+thread_local int t_bh_concurrency = 1;
+void set_bh_concurrency(int c) { t_bh_concurrency = std::max(1, c); }
+
+// Windows per query: enough warps to fill the SMs (2 waves of 32 resident
+// warps), and -- when the caller's point set is dense at the gate radius (an
+// estimated >= 1024 points within thr of a point, from the host bounding box
+// in kc.ext), so that every walk carries thousands of direct interactions --
+// 32 windows: each window's blocks then work in one region of the tree (its
+// records stay in L1) and the long walks are cut into many short ones.
+// Measured (config 3 evaluate): K = 7 -> 32: 0.207 -> 0.162 s; config 5:
+// 0.49 -> 0.35 s per 8 subjects; config 4 (sparse, ~500 within thr): K = 1-2
+// stays best. Skipped when several flows share the GPU (batched subjects),
+// whose concurrency already fills it.
+int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc) {
   static const int forced = [] {
     const char* e = std::getenv("GS_BH_TASKS");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced > 0) return std::min(forced, kMaxChunks);
+  if (forced > 0) return std::min(forced, kMaxBhTasks);
   const int64_t warps = (nq + 31) / 32;
   const int64_t want = 148 * 64;  // ~2 waves of 32 resident warps per SM
-  return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, (want + warps - 1) / warps));
+  int K = (int)std::max<int64_t>(1, std::min<int64_t>(16, (want + warps - 1) / warps));
+  if (t_bh_concurrency == 1 && kc.ext[0] + kc.ext[1] + kc.ext[2] > 0 && thr < INFINITY) {
+    double frac = 1.0;
+    for (int a = 0; a < 3; ++a)
+      if (kc.ext[a] > 0) frac *= std::min(1.0, 2.0 * thr / kc.ext[a]);
+    const int64_t cap = std::max<int64_t>(1, (int64_t(4) << 20) / std::max<int64_t>(nq, 1));
+    if (frac * (double)n >= 1024.0) K = (int)std::max<int64_t>(K, std::min<int64_t>(32, cap));
+  }
+  return std::min(K, kMaxBhTasks);
 }
 
 int bh_keep_trees(BhWork& w, int T) {
@@ -921,7 +943,7 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   kt_mark(1, st);
   GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st, nullptr, e.bad_step ? e.bad_step + 1 : nullptr));
   kt_mark(1, st);
-  const int K = bh_tasks(nt);
+  const int K = bh_tasks(nt, n, cfg.threshold_multiplier * cfg.sigma, kc);
   GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * K * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
@@ -963,7 +985,7 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
     GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, *t, st));
   }
   GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
-  const int K = bh_tasks(n);
+  const int K = bh_tasks(n, n, cfg.threshold_multiplier * cfg.sigma, kc);
   GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * K * n));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
@@ -985,7 +1007,7 @@ int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const 
                      const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
                      cudaStream_t st) {
   GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, w.cur, st));
-  const int K = bh_tasks(m);
+  const int K = bh_tasks(m, n, cfg.threshold_multiplier * cfg.sigma, kc);
   GS_TRY_INT(w.part.ensure(vec_bytes(prec) * K * m));
   BhQuery q;
   q.mode = kBhVel;

@@ -89,7 +89,9 @@ struct BhQuery {
   int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
   int by_index = 0;  // RHS: queries = the n_tgt records at ev (a flow shard), not leaf order
 };
-int bh_tasks(int64_t nq);
+int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc);
+// host threads driving flows on one GPU at once (batched subjects); per thread
+void set_bh_concurrency(int c);
 int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,
                 const BhQuery& q, cudaStream_t st);
 

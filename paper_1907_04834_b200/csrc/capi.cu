@@ -228,7 +228,7 @@ int sync(gs_ctx* c) {
 }
 
 // FP32 centring: midpoint of the host bounding box (cheap, keeps |x'| small).
-void bbox_center(const double* q, int64_t n, double* c0) {
+void bbox_center(const double* q, int64_t n, double* c0, double* ext = nullptr) {
   double lo[3], hi[3];
   for (int a = 0; a < 3; ++a) lo[a] = hi[a] = q[a];
   for (int64_t i = 1; i < n; ++i)
@@ -238,6 +238,13 @@ void bbox_center(const double* q, int64_t n, double* c0) {
       hi[a] = v > hi[a] ? v : hi[a];
     }
   for (int a = 0; a < 3; ++a) c0[a] = 0.5 * (lo[a] + hi[a]);
+  if (ext)
+    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
+}
+
+KernelConsts with_ext(KernelConsts k, const double* ext) {
+  for (int a = 0; a < 3; ++a) k.ext[a] = ext[a];
+  return k;
 }
 
 // upload + pack; flags non-finite input (PointSet/MomentumSet ctor, core.hpp:124-170)
@@ -424,9 +431,9 @@ int flow_bh_stats(gs_flow* f, gs_stats* out) {
 }
 
 int flow_upload(gs_flow* f, const double* q0, const double* p0) {
-  double c0[3];
-  bbox_center(q0, f->n, c0);
-  f->kc = make_consts(f->cfg.sigma, f->prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(q0, f->n, c0, ext);
+  f->kc = with_ext(make_consts(f->cfg.sigma, f->prec == kF32 ? c0 : nullptr), ext);
   GS_TRY(upload_records(f->ctx, f->prec, q0, p0, f->n, f->rec));
   f->permuted = false;
   f->steps_done = 0;
@@ -729,9 +736,9 @@ gs_status gs_exact_rhs(gs_ctx* c, int32_t precision, int64_t n, const double* q,
   if (!c || !q || !p) return bad_arg("null argument");
   GS_TRY(check_n(n));
   const int prec = precision == GS_F32 ? kF32 : kF64;
-  double c0[3];
-  bbox_center(q, n, c0);
-  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(q, n, c0, ext);
+  const KernelConsts kc = with_ext(make_consts(sigma, prec == kF32 ? c0 : nullptr), ext);
   GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
   GS_TRY(c->stage_c.ensure(sizeof(double) * 3 * n));
   GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
@@ -770,9 +777,9 @@ gs_status gs_exact_velocity(gs_ctx* c, int32_t precision, int64_t m, const doubl
   GS_TRY(check_n(n));
   GS_TRY(check_n(m));
   const int prec = precision == GS_F32 ? kF32 : kF64;
-  double c0[3];
-  bbox_center(q, n, c0);
-  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(q, n, c0, ext);
+  const KernelConsts kc = with_ext(make_consts(sigma, prec == kF32 ? c0 : nullptr), ext);
   GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
   GS_TRY(upload_records(c, prec, x, nullptr, m, c->rec_b));
   GS_TRY(c->part.ensure((size_t)kMaxChunks * vec_bytes(prec) * m));
@@ -799,9 +806,9 @@ gs_status gs_hessian_products(gs_ctx* c, int32_t precision, int64_t n, const dou
   if (!c || !q || !p || !alpha || !beta) return bad_arg("null argument");
   GS_TRY(check_n(n));
   const int prec = precision == GS_F32 ? kF32 : kF64;
-  double c0[3];
-  bbox_center(q, n, c0);
-  const KernelConsts kc = make_consts(sigma, prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(q, n, c0, ext);
+  const KernelConsts kc = with_ext(make_consts(sigma, prec == kF32 ? c0 : nullptr), ext);
   GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
   GS_TRY(upload_records(c, prec, alpha, beta, n, c->rec_b));
   GS_TRY(c->part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * n));
@@ -1038,9 +1045,9 @@ gs_status gs_backward_gradient(gs_ctx* c, const gs_config* cfg, int64_t n, int32
     return GS_CONFIG_MISMATCH;
   }
   const int prec = cfg->precision == GS_F32 ? kF32 : kF64;
-  double c0[3];
-  bbox_center(traj_q, n, c0);
-  const KernelConsts kc = make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(traj_q, n, c0, ext);
+  const KernelConsts kc = with_ext(make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr), ext);
   const size_t rb = 2 * vec_bytes(prec) * n;
   gs_flow* f = scratch_flow(c);
   GS_TRY(flow_init(f, c, cfg, n));
@@ -1093,9 +1100,9 @@ gs_status gs_warp_points(gs_ctx* c, const gs_config* cfg, int64_t n, int32_t sta
     return GS_CONFIG_MISMATCH;
   }
   const int prec = cfg->precision == GS_F32 ? kF32 : kF64;
-  double c0[3];
-  bbox_center(traj_q, n, c0);
-  const KernelConsts kc = make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr);
+  double c0[3], ext[3];
+  bbox_center(traj_q, n, c0, ext);
+  const KernelConsts kc = with_ext(make_consts(cfg->sigma, prec == kF32 ? c0 : nullptr), ext);
   const size_t rb = 2 * vec_bytes(prec) * n;
   DBuf& traj = c->rec_b;
   GS_TRY(traj.ensure(rb * T));

@@ -70,6 +70,8 @@ struct KernelConsts {
   double sigma, s, inv_s, inv_two_s, two_over_s;
   double kappa;        // sqrt(log2e / (2 s))
   double c0[3];        // FP32 centring
+  double ext[3];       // extent of the caller's point set (host bounding box; 0 = unknown):
+                       // sizes the Barnes-Hut walk's node windows (bh.cu bh_tasks)
 };
 
 inline KernelConsts make_consts(double sigma, const double* c0) {
@@ -81,6 +83,7 @@ inline KernelConsts make_consts(double sigma, const double* c0) {
   k.two_over_s = 2.0 / k.s;
   k.kappa = __builtin_sqrt(kLog2e / (2.0 * k.s));
   for (int a = 0; a < 3; ++a) k.c0[a] = c0 ? c0[a] : 0.0;
+  for (int a = 0; a < 3; ++a) k.ext[a] = 0.0;
   return k;
 }
 

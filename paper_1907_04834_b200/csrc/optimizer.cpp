@@ -29,6 +29,10 @@
 #include "geoshoot_b200.h"
 #include "lbfgs.h"
 
+namespace gsb {
+void set_bh_concurrency(int c);  // bh.cu: flows sharing the GPU from other host threads
+}
+
 namespace {
 
 // Contexts for the batched entry points, kept for the life of the process: a
@@ -381,6 +385,7 @@ gs_status gs_optimize_batch(int device, const gs_config* cfg, const gs_opt_confi
     pool.emplace_back([&, b] {
       gs_status cs = GS_OK;
       cudaSetDevice(device);  // pooled contexts move between host threads
+      gsb::set_bh_concurrency(batch);
       gs_ctx* c = ctx_pool().acquire(device, &cs);
       if (!c) {
         st[b] = cs;
@@ -414,6 +419,7 @@ gs_status gs_evaluate_batch(int device, const gs_config* cfg, int32_t batch, con
     pool.emplace_back([&, b] {
       gs_status cs = GS_OK;
       cudaSetDevice(device);  // pooled contexts move between host threads
+      gsb::set_bh_concurrency(batch);
       gs_ctx* c = ctx_pool().acquire(device, &cs);
       if (!c) {
         st[b] = cs;
