@@ -84,6 +84,7 @@ struct BhArgs {
   int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
   int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
   int by_index;        // RHS: queries are ev[0 .. nq) (a shard's records), not leaf order
+  int dense;           // dense near fields: k_bh_grp unless GS_BH_KERNEL says otherwise
   int* sm_ctr;         // non-null: blocks claim SM-local contiguous query blocks (claim_block)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
 static int bh_kernel_choice() {
   static int v = [] {
     const char* e = std::getenv("GS_BH_KERNEL");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;  // 0: by regime (dense near fields -> 3, else 1)
   }();
   return v;
 }
@@ -743,7 +744,8 @@ static double bh_group_ratio() {
 template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
   // literal-mean-dot and by-index queries: independent walks only
-  const int kind = (a.lmd || a.by_index) ? 1 : bh_kernel_choice();
+  const int choice = bh_kernel_choice();
+  const int kind = (a.lmd || a.by_index) ? 1 : (choice ? choice : (a.dense ? 3 : 1));
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
@@ -824,6 +826,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.n_tgt = q.n_tgt;
   a.nq = q.mode == kBhVel ? q.m : (q.by_index ? q.n_tgt : (int)t.n);
   a.by_index = q.by_index;
+  a.dense = q.dense && !q.per_query;
   a.ev = static_cast<const V4<R>*>(q.ev);
   const KernelConsts& kc = t.kc;
   a.kap = kc.kappa;
@@ -907,7 +910,8 @@ void set_bh_concurrency(int c) { t_bh_concurrency = std::max(1, c); }
 // 0.49 -> 0.35 s per 8 subjects; config 4 (sparse, ~500 within thr): K = 1-2
 // stays best. Skipped when several flows share the GPU (batched subjects),
 // whose concurrency already fills it.
-int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc) {
+int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* dense) {
+  if (dense) *dense = 0;
   static const int forced = [] {
     const char* e = std::getenv("GS_BH_TASKS");
     return e ? std::atoi(e) : 0;
@@ -921,7 +925,10 @@ int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc) {
     for (int a = 0; a < 3; ++a)
       if (kc.ext[a] > 0) frac *= std::min(1.0, 2.0 * thr / kc.ext[a]);
     const int64_t cap = std::max<int64_t>(1, (int64_t(4) << 20) / std::max<int64_t>(nq, 1));
-    if (frac * (double)n >= 1024.0) K = (int)std::max<int64_t>(K, std::min<int64_t>(32, cap));
+    if (frac * (double)n >= 1024.0) {
+      K = (int)std::max<int64_t>(K, std::min<int64_t>(32, cap));
+      if (dense) *dense = 1;
+    }
   }
   return std::min(K, kMaxBhTasks);
 }
@@ -943,12 +950,14 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
   kt_mark(1, st);
   GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st, nullptr, e.bad_step ? e.bad_step + 1 : nullptr));
   kt_mark(1, st);
-  const int K = bh_tasks(nt, n, cfg.threshold_multiplier * cfg.sigma, kc);
+  int dense = 0;
+  const int K = bh_tasks(nt, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
   GS_TRY_INT(w.part.ensure(2 * vec_bytes(prec) * K * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
   q.mode = kBhRhs;
   q.ntask = K;
+  q.dense = dense;
   q.lmd = cfg.literal_mean_dot;
   if (tb != 0 || nt != n) {  // a shard: walk only its own targets, by point index
     q.by_index = 1;
@@ -985,12 +994,14 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
     GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, *t, st));
   }
   GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
-  const int K = bh_tasks(n, n, cfg.threshold_multiplier * cfg.sigma, kc);
+  int dense = 0;
+  const int K = bh_tasks(n, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
   GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * K * n));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
   q.mode = kBhHess;
   q.ntask = K;
+  q.dense = dense;
   q.lmd = cfg.literal_mean_dot;
   q.tgt_begin = 0;
   q.n_tgt = (int)n;
@@ -1007,11 +1018,13 @@ int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const 
                      const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
                      cudaStream_t st) {
   GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, w.cur, st));
-  const int K = bh_tasks(m, n, cfg.threshold_multiplier * cfg.sigma, kc);
+  int dense = 0;
+  const int K = bh_tasks(m, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
   GS_TRY_INT(w.part.ensure(vec_bytes(prec) * K * m));
   BhQuery q;
   q.mode = kBhVel;
   q.ntask = K;
+  q.dense = dense;
   q.ev = ev;
   q.m = (int)m;
   q.part = w.part.ptr;

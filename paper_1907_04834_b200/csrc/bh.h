@@ -88,8 +88,9 @@ struct BhQuery {
   int ntask = 1;  // node windows (bh_tasks); part holds [ntask][queries] partials
   int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
   int by_index = 0;  // RHS: queries = the n_tgt records at ev (a flow shard), not leaf order
+  int dense = 0;     // dense near fields (bh_tasks): the group walk is the default kernel
 };
-int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc);
+int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* dense = nullptr);
 // host threads driving flows on one GPU at once (batched subjects); per thread
 void set_bh_concurrency(int c);
 int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,
