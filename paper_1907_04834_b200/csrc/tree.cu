@@ -194,7 +194,9 @@ template <int kRsIPT>
 __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, const int* vin,
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
-                                                      unsigned* desc, unsigned* tile_ctr) {
+                                                      unsigned* desc, unsigned* tile_ctr,
+                                                      const unsigned* run_if = nullptr) {
+  if (run_if && *run_if == 0) return;  // conditional pass (tree_build's tie fallback)
   constexpr int kTile = kRsNT * kRsIPT;
   __shared__ unsigned wh[kRsNT / 32][256];  // per-warp digit counts -> offsets within the tile's digit run
   __shared__ unsigned base[256];            // global digit starts (scan of dig_tot)
@@ -302,9 +304,19 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
 }
 
 // out[t] = key[perm[t]]
-__global__ void k_gather_u64(const int* perm, const uint64_t* key, uint64_t* out, int64_t n) {
+__global__ void k_gather_u64(const int* perm, const uint64_t* key, uint64_t* out, int64_t n,
+                             const unsigned* run_if = nullptr) {
+  if (run_if && *run_if == 0) return;
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t < n) out[t] = key[perm[t]];
+}
+
+// flag = 1 if two neighbours of the key_hi-sorted order share key_hi (the
+// deep key must then order them: tree_build re-sorts by the full key)
+__global__ void k_tie_check(const uint64_t* skh, int64_t n, unsigned* flag) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  const bool tie = t + 1 < n && skh[t] == skh[t + 1];
+  if (__any_sync(0xffffffffu, tie) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 // ------------------------------------------------------------- topology ---
@@ -706,12 +718,16 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
-  // 3. stable LSD radix sort by (key_hi, key_lo, index): 5 passes over the 33
-  // significant bits of key_lo, then the keys' key_hi in that order, then 8
-  // passes over key_hi; 8-bit digits, no copies (buffers ping-pong):
-  //   lo: (key_lo, index) -> (tmp_k, tmp_v) -> (skey_lo, tmp_v2) -> ... -> (tmp_k, tmp_v)
-  //   hi: (skey_lo := key_hi[tmp_v], tmp_v) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
-  // Ties in all 32 levels (depth-32 buckets) keep ascending index.
+  // 3. stable LSD radix sort by (key_hi, key_lo, index). key_lo (levels
+  // 22-32) only orders points that share all 21 levels of key_hi -- almost
+  // never outside depth-32 clusters -- so: 8 passes over key_hi with the index
+  // as value (ties keep ascending index), a check for equal neighbours, and
+  // only if there is one the full sort, whose kernels otherwise return at once:
+  //   hi: (key_hi, index) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
+  //   [ties] lo: (key_lo, index) -> (tmp_k, tmp_v) -> (skey_lo, tmp_v2) -> ... -> (tmp_k, tmp_v)
+  //          hi: (skey_lo := key_hi[tmp_v], tmp_v) -> (tmp_k, tmp_v2) -> ... -> (skey_hi, perm)
+  // 8-bit digits, no copies (buffers ping-pong); ties in all 32 levels
+  // (depth-32 buckets) keep ascending index.
   // keys per thread: small tiles (more CTAs) for small n, 8 from ~0.5M points
   // (measured sort per build: 50k 0.22 ms at 4 vs 0.28 at 8; 1M 0.48 at 8 vs 0.52 at 4)
   static const int ipt_env = [] {
@@ -722,45 +738,50 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
   const int ntiles = nblocks(n, kRsNT * ipt);
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
-  // one-sweep scratch: 13 digit histograms, 13 tile counters, 13 x ntiles x 256
-  // look-back status words -- zeroed by one memset
-  constexpr int kPasses = 13;
-  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256;
+  // one-sweep scratch: 13 digit histograms (5 lo + 8 hi), 32 counters (21
+  // passes' tile counters, the tie flag), 21 x ntiles x 256 look-back status
+  // words -- zeroed by one memset
+  constexpr int kHist = 13, kPasses = 21;
+  const size_t words = (size_t)kHist * 256 + 32 + (size_t)kPasses * ntiles * 256;
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
   GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
   unsigned* hist = t.hist.as<unsigned>();
-  unsigned* ctr = hist + kPasses * 256;
+  unsigned* ctr = hist + kHist * 256;
+  unsigned* tie = ctr + 31;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, kPasses * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
-  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q) {
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kHist * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, kHist * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  // pass q (0..20) over digit histogram hq (0..4 lo, 5..12 hi)
+  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q, int hq,
+                  const unsigned* run_if) {
     unsigned* dq = desc + (size_t)q * ntiles * 256;
-    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
-    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + q * 256, dq, ctr + q);
+    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + hq * 256, dq, ctr + q, run_if);
+    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + hq * 256, dq, ctr + q, run_if);
   };
+  auto hi_sort = [&](const uint64_t* ka, const int* va, int q0, const unsigned* run_if) {
+    for (int p = 0; p < 8; ++p) {
+      uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
+      int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
+      pass(ka, va, kb, vb, 8 * p, q0 + p, 5 + p, run_if);
+      ka = kb;
+      va = vb;
+    }
+  };
+  hi_sort(t.key_hi.as<uint64_t>(), nullptr, 0, nullptr);  // values: the index
+  k_tie_check<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), n, tie);
   {
     const uint64_t* ka = t.key_lo.as<uint64_t>();
     const int* va = nullptr;  // implicit: the index
     for (int p = 0; p < 5; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_lo.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.tmp_v2.as<int>() : t.tmp_v.as<int>();
-      pass(ka, va, kb, vb, 8 * p, p);
+      pass(ka, va, kb, vb, 8 * p, 8 + p, p, tie);
       ka = kb;
       va = vb;
     }
   }
-  k_gather_u64<<<nb, kNT, 0, st>>>(t.tmp_v.as<int>(), t.key_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
-  {
-    const uint64_t* ka = t.skey_lo.as<uint64_t>();
-    const int* va = t.tmp_v.as<int>();
-    for (int p = 0; p < 8; ++p) {
-      uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
-      int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      pass(ka, va, kb, vb, 8 * p, 5 + p);
-      ka = kb;
-      va = vb;
-    }
-  }
+  k_gather_u64<<<nb, kNT, 0, st>>>(t.tmp_v.as<int>(), t.key_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, tie);
+  hi_sort(t.skey_lo.as<uint64_t>(), t.tmp_v.as<int>(), 13, tie);
   GS_CUDA_OK(cudaGetLastError());
   k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
   kt_mark(3, st);
