@@ -523,10 +523,12 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
   for (;;) {
     const int par = parent[node];
     if (par < 0) return;
-    // acq_rel arrival: this child's sums are released to, and the siblings'
-    // acquired by, whichever child arrives last (no separate fences)
+    // release arrival: this child's sums are published before its count; the
+    // last child reads its siblings' sums with L2 loads (ld.cg, never through
+    // L1), so no acquire-side L1 invalidation (CCTL.IVALL) is needed -- it was
+    // 20 % of this kernel's stall samples
     cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
-    const int old = arrive.fetch_add(1, cuda::memory_order_acq_rel);
+    const int old = arrive.fetch_add(1, cuda::memory_order_release);
     if (old != nchild[par] - 1) return;
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
