@@ -58,6 +58,14 @@ SETS = {
     "cluster": lambda: (np.concatenate([uniform(3000, 1e-7, 8), np.array([[-1e3, -1e3, -1e3],
                                                                           [1e3, 1e3, 1e3]])]),
                         sym_uniform(3002, 1.0, 9)),
+    # sizes with hundreds of radix-sort tiles (decoupled look-back across
+    # tiles), with and without neighbours sharing the 63-bit key (the tie check
+    # and the full-key fallback sort)
+    "cube_200k": lambda: (uniform(200_000, 1.0, 10), sym_uniform(200_000, 1.0, 11)),
+    "clusters_120k": lambda: (np.concatenate([uniform(80_000, 1.0, 12)]
+                                             + [c + uniform(2_000, 1e-8, 13 + k) for k, c in
+                                                enumerate(uniform(20, 1.0, 40))]),
+                              sym_uniform(120_000, 1.0, 14)),
     "corners": lambda: (np.array([[1.0 if i & 1 else -1.0, 1.0 if i & 2 else -1.0,
                                    1.0 if i & 4 else -1.0] for i in range(8)]), np.zeros((8, 3))),
 }
