@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--phases", action="store_true")
     ap.add_argument("--shape", default="cube", choices=["cube", "tube", "ellipsoid"])
     ap.add_argument("--amp", type=float, default=0.01)
+    ap.add_argument("--no-profile", action="store_true", help="CUDA-graph replay (profiling forces eager launches)")
     a = ap.parse_args()
     import numpy as np
     from paper_1907_04834_b200 import BARNES_HUT, EULER, EXACT, F32, F64, RK4, Geoshoot, ShootingConfig
@@ -41,12 +42,13 @@ def main():
     f.upload(q, p)
     f.advance(a.warmup)
     f.sync()
-    f.profile(True)
+    if not a.no_profile:
+        f.profile(True)
     t0 = time.perf_counter()
     f.advance(a.steps)
     f.sync()
     dt = time.perf_counter() - t0
-    pr = f.profile_phases() if a.phases else f.profile_read()
+    pr = {} if a.no_profile else (f.profile_phases() if a.phases else f.profile_read())
     print(json.dumps({"backend": a.backend, "n": a.n, "steps": a.steps, "wall_s": dt,
                       "steps_per_s": a.steps / dt, "profile": pr}))
 
