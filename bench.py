@@ -35,7 +35,7 @@ SIGMA = 0.0131
 T_STEPS = 10
 METRIC = "flow steps/s (RK4, 4 RHS/step) & G pair-interactions/s, config 4"
 # Algorithmic DRAM bytes per point of one FP32 tree build (DESIGN.md §4 table)
-BUILD_BYTES_PER_POINT = 1256
+BUILD_BYTES_PER_POINT = 1080
 
 
 def workload(n: int, seed: int = 2024):
