@@ -499,8 +499,9 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
   starts(L, n, a, Lm, Lp, ci, lf);
   if (!lf) return;
   int node = first[a] + ci;
-  {
-    const int4 mi = meta[node];
+  // a single-point leaf's sums are its point: nothing is stored for it (its
+  // parent reads the point itself; k_fill_leaves materialises it for downloads)
+  if (const int4 mi = meta[node]; !((mi.w & 1) && mi.y == mi.z)) {
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
     for (int t = mi.y; t <= mi.z; ++t) {
@@ -533,15 +534,31 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
-    for (int ch = par + 1; ch < end; ch = max(ch + 1, meta[ch].x)) {
-      const double4 a0 = ldcg4(s0 + ch), a1 = ldcg4(s1 + ch);
-      A.x += a0.x; A.y += a0.y; A.z += a0.z;
-      B.x += a1.x; B.y += a1.y; B.z += a1.z;
-      if (mode == 0) {
-        const V4<R> cl = ldcg4(lo + ch), chh = ldcg4(hi + ch);
-        l.x = min(l.x, cl.x); l.y = min(l.y, cl.y); l.z = min(l.z, cl.z);
-        h.x = max(h.x, chh.x); h.y = max(h.y, chh.y); h.z = max(h.z, chh.z);
+    for (int ch = par + 1; ch < end;) {
+      const int4 mc = meta[ch];
+      if ((mc.w & 1) && mc.y == mc.z) {  // single-point leaf: its point (same values as stored sums)
+        if (mode == 0) {
+          const V4<R> q = ld4(squ + mc.y), p = ld4(srec + 2 * mc.y + 1);
+          A.x += q.x; A.y += q.y; A.z += q.z;
+          B.x += p.x; B.y += p.y; B.z += p.z;
+          l.x = min(l.x, q.x); l.y = min(l.y, q.y); l.z = min(l.z, q.z);
+          h.x = max(h.x, q.x); h.y = max(h.y, q.y); h.z = max(h.z, q.z);
+        } else {
+          const V4<R> al = ld4(sadj + 2 * mc.y), be = ld4(sadj + 2 * mc.y + 1);
+          A.x += al.x; A.y += al.y; A.z += al.z;
+          B.x += be.x; B.y += be.y; B.z += be.z;
+        }
+      } else {
+        const double4 a0 = ldcg4(s0 + ch), a1 = ldcg4(s1 + ch);
+        A.x += a0.x; A.y += a0.y; A.z += a0.z;
+        B.x += a1.x; B.y += a1.y; B.z += a1.z;
+        if (mode == 0) {
+          const V4<R> cl = ldcg4(lo + ch), chh = ldcg4(hi + ch);
+          l.x = min(l.x, cl.x); l.y = min(l.y, cl.y); l.z = min(l.z, cl.z);
+          h.x = max(h.x, chh.x); h.y = max(h.y, chh.y); h.z = max(h.z, chh.z);
+        }
       }
+      ch = max(ch + 1, mc.x);
     }
     if (mode == 0) { st4(lo + par, l); st4(hi + par, h); }
     s0[par] = A;
@@ -571,7 +588,9 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
   const int4 mi = meta[i];
   const int cnt = mi.z - mi.y + 1;
   const double inv = 1.0 / cnt;
-  const double4 a = s0[i], b = s1[i];
+  const bool single = (mi.w & 1) && cnt == 1;  // no stored sums (k_aggregate)
+  const double4 z4 = make_double4(0, 0, 0, 0);
+  const double4 a = single ? z4 : s0[i], b = single ? z4 : s1[i];
   if (mode == 0) {
     double cx = __dmul_rn(a.x, inv), cy = __dmul_rn(a.y, inv), cz = __dmul_rn(a.z, inv);
     const V4<R> cen = scaled ? mk4<R>((R)fmaf((float)kap, (float)cx, -(float)(kap * c0x)),
@@ -579,11 +598,8 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
                                       (R)fmaf((float)kap, (float)cz, -(float)(kap * c0z)), R(cnt))
                              : mk4<R>(R(cx), R(cy), R(cz), R(cnt));
     const V4<R> mom = mk4<R>(R(b.x), R(b.y), R(b.z), ival(R(0), cnt));
-    st4(o0 + i, cen);
-    st4(o1 + i, mom);
     if (nrec) {
       const bool leaf = mi.w & 1;
-      const bool single = leaf && cnt == 1;
       // twig: an internal node whose children are all leaves (subtree = itself +
       // its children); opening it makes every point of it direct, no child gated
       const bool twig = !leaf && nchild && mi.x - (int)i - 1 == nchild[i];
@@ -609,6 +625,12 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
   } else {
     // interleaved {alpha sum, beta mean} per node (one 256-bit load in the walk);
     // for a single-point leaf these are exactly the point's alpha and beta
+    // (read from the leaf-order adjoints, passed as srec)
+    if (single) {
+      st4(o0 + 2 * i, ld4(srec + 2 * mi.y));
+      st4(o0 + 2 * i + 1, ld4(srec + 2 * mi.y + 1));
+      return;
+    }
     st4(o0 + 2 * i, mk4<R>(R(a.x), R(a.y), R(a.z)));
     // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
     st4(o0 + 2 * i + 1, mk4<R>(R(__dmul_rn(inv, b.x)), R(__dmul_rn(inv, b.y)), R(__dmul_rn(inv, b.z))));
@@ -806,8 +828,6 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.counter.ensure(4 * cap));
   GS_TRY_INT(t.lo.ensure(vb * cap));
   GS_TRY_INT(t.hi.ensure(vb * cap));
-  GS_TRY_INT(t.cen.ensure(vb * cap));
-  GS_TRY_INT(t.mom.ensure(vb * cap));
   GS_TRY_INT(t.nrec.ensure(4 * vb * cap));
   GS_TRY_INT(t.psum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.msum.ensure(sizeof(double4) * cap));
@@ -943,11 +963,11 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   if (prec == kF32) {
     k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
     k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<float4>(), nullptr);
+    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<float4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<float4>());
   } else {
     k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
     k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<double4>(), nullptr);
+    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<double4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<double4>());
   }
   GS_CUDA_OK(cudaGetLastError());
   t.adj_valid = true;
@@ -955,6 +975,28 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
 }
 
 namespace {
+
+// single-point leaves' stored fields for a download (k_aggregate leaves them
+// out): box = the point, sums = the point, its momentum, alpha and beta
+template <typename R>
+__global__ void k_fill_leaves(const int4* meta, int64_t m, const V4<R>* squ, const V4<R>* srec,
+                              const V4<R>* sadj, V4<R>* lo, V4<R>* hi, double4* psum,
+                              double4* msum, double4* asum, double4* bsum) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= m) return;
+  const int4 mi = meta[i];
+  if (!((mi.w & 1) && mi.y == mi.z)) return;
+  const V4<R> q = ld4(squ + mi.y), p = ld4(srec + 2 * mi.y + 1);
+  st4(lo + i, q);
+  st4(hi + i, q);
+  psum[i] = make_double4(q.x, q.y, q.z, 0);
+  msum[i] = make_double4(p.x, p.y, p.z, 0);
+  if (asum) {
+    const V4<R> al = ld4(sadj + 2 * mi.y), be = ld4(sadj + 2 * mi.y + 1);
+    asum[i] = make_double4(al.x, al.y, al.z, 0);
+    bsum[i] = make_double4(be.x, be.y, be.z, 0);
+  }
+}
 
 template <typename R>
 __global__ void k_dl_nodes(const int4* meta, const int* parent, int64_t m, const V4<R>* lo,
@@ -1024,10 +1066,13 @@ int tree_download(DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
   const int mb = nblocks(m, kNT);
   const double4* as = t.adj_valid ? t.asum.as<double4>() : nullptr;
   const double4* bs = t.adj_valid ? t.bsum.as<double4>() : nullptr;
-  if (t.prec == kF32)
+  if (t.prec == kF32) {
+    k_fill_leaves<float><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.squ.as<float4>(), t.srec.as<float4>(), t.sadj.as<float4>(), t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), (double4*)as, (double4*)bs);
     k_dl_nodes<float><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.parent.as<int>(), m, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), as, bs, b_level.as<int32_t>(), b_par.as<int32_t>(), b_skip.as<int32_t>(), b_range.as<int32_t>(), b_boxes.as<double>(), b_sums.as<double>(), b_count.as<uint32_t>());
-  else
+  } else {
+    k_fill_leaves<double><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.squ.as<double4>(), t.srec.as<double4>(), t.sadj.as<double4>(), t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), (double4*)as, (double4*)bs);
     k_dl_nodes<double><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.parent.as<int>(), m, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), as, bs, b_level.as<int32_t>(), b_par.as<int32_t>(), b_skip.as<int32_t>(), b_range.as<int32_t>(), b_boxes.as<double>(), b_sums.as<double>(), b_count.as<uint32_t>());
+  }
   if (boxes)
     k_cells<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), m, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.root.as<double>(), b_boxes.as<double>());
   GS_CUDA_OK(cudaGetLastError());
