@@ -501,7 +501,10 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
   int node = first[a] + ci;
   // a single-point leaf's sums are its point: nothing is stored for it (its
   // parent reads the point itself; k_fill_leaves materialises it for downloads)
+  // and it has nothing to publish, so its arrival needs no release fence
+  bool publish = false;
   if (const int4 mi = meta[node]; !((mi.w & 1) && mi.y == mi.z)) {
+    publish = true;
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
     for (int t = mi.y; t <= mi.z; ++t) {
@@ -529,7 +532,9 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
     // L1), so no acquire-side L1 invalidation (CCTL.IVALL) is needed -- it was
     // 20 % of this kernel's stall samples
     cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
-    const int old = arrive.fetch_add(1, cuda::memory_order_release);
+    const int old = publish ? arrive.fetch_add(1, cuda::memory_order_release)
+                            : arrive.fetch_add(1, cuda::memory_order_relaxed);
+    publish = true;
     if (old != nchild[par] - 1) return;
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
