@@ -8,6 +8,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 
 #include "bh.h"
@@ -72,6 +73,11 @@ struct gs_ctx {
   DBuf stage_a, stage_b, stage_c, stage_d, scal;
   DBuf rec_a, rec_b, part, epart;
   gs_flow* scratch = nullptr;
+  // caller-owned flows and trees made on this context: gs_destroy detaches
+  // them (their ctx becomes null) so that destroying them afterwards only
+  // frees their device memory instead of touching a dead context
+  std::unordered_set<gs_flow*> flows;
+  std::unordered_set<gs_tree*> trees;
 };
 
 struct gs_flow {
@@ -112,6 +118,8 @@ struct gs_flow {
     delete timer;
   }
 };
+
+static void detach_trees(gs_ctx* c);  // after struct gs_tree
 
 extern "C" {
 
@@ -169,6 +177,9 @@ gs_ctx* gs_create(int device, gs_status* status) {
 
 void gs_destroy(gs_ctx* ctx) {
   if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (gs_flow* f : ctx->flows) f->ctx = nullptr;
+  detach_trees(ctx);
   if (ctx->scratch) gs_flow_destroy(ctx->scratch);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
@@ -607,13 +618,17 @@ gs_status gs_flow_create(gs_ctx* ctx, const gs_config* cfg, int64_t n, gs_flow**
     delete f;
     return (gs_status)s;
   }
+  ctx->flows.insert(f);
   *out = f;
   return GS_OK;
 }
 
 void gs_flow_destroy(gs_flow* flow) {
   if (!flow) return;
-  if (flow->ctx) cudaStreamSynchronize(flow->ctx->stream);
+  if (flow->ctx) {
+    cudaStreamSynchronize(flow->ctx->stream);
+    flow->ctx->flows.erase(flow);
+  }
   delete flow;
 }
 
@@ -1172,6 +1187,10 @@ struct gs_tree {
   int64_t last_queries = 0;
 };
 
+static void detach_trees(gs_ctx* c) {
+  for (gs_tree* t : c->trees) t->ctx = nullptr;
+}
+
 namespace {
 
 int tree_for_sigma(gs_tree* tr, double sigma) {
@@ -1255,6 +1274,7 @@ gs_status gs_tree_build(gs_ctx* c, int32_t precision, int64_t n, const double* q
     delete tr;
     return (gs_status)s;
   }
+  c->trees.insert(tr);
   *out = tr;
   return GS_OK;
 }
@@ -1286,13 +1306,17 @@ gs_status gs_tree_build_in_cell(gs_ctx* c, int32_t precision, int64_t n, const d
     delete tr;
     return (gs_status)s;
   }
+  c->trees.insert(tr);
   *out = tr;
   return GS_OK;
 }
 
 void gs_tree_free(gs_tree* tr) {
   if (!tr) return;
-  cudaStreamSynchronize(tr->ctx->stream);
+  if (tr->ctx) {
+    cudaStreamSynchronize(tr->ctx->stream);
+    tr->ctx->trees.erase(tr);
+  }
   delete tr;
 }
 

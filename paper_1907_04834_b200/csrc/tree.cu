@@ -485,6 +485,16 @@ __device__ __forceinline__ double4 ldcg4(const double4* p) {
 __device__ __forceinline__ float4 ldcg4(const float4* p) { return __ldcg(p); }
 
 // mode 0: forward (lo, hi, psum, msum from squ/srec p); mode 1: adjoint sums
+// Node aggregates (tight box, FP64 position / momentum sums; mode 1: alpha /
+// beta sums). One thread per node: a leaf, or a node of at most kAggDirect
+// points, sums its own leaf-order range directly (no dependencies, full
+// warps); larger internal nodes are completed bottom-up -- each small node whose parent is large
+// arrives at the parent's counter, and the last arrival computes the parent
+// from its children and climbs on. A single-point leaf stores nothing: its
+// sums are its point, read by whoever needs them (k_fill_leaves for
+// downloads). Summation order is fixed by the tree (deterministic).
+constexpr int kAggDirect = 16;
+
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64_t n,
                                                    const int* first, const int4* meta,
@@ -493,18 +503,16 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
                                                    const V4<R>* srec, const V4<R>* sadj,
                                                    V4<R>* lo, V4<R>* hi, double4* s0, double4* s1,
                                                    int64_t cap) {
-  const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (a >= n || first[n] > cap) return;
-  int Lm, Lp, ci, lf;
-  starts(L, n, a, Lm, Lp, ci, lf);
-  if (!lf) return;
-  int node = first[a] + ci;
-  // a single-point leaf's sums are its point: nothing is stored for it (its
-  // parent reads the point itself; k_fill_leaves materialises it for downloads)
-  // and it has nothing to publish, so its arrival needs no release fence
-  bool publish = false;
-  if (const int4 mi = meta[node]; !((mi.w & 1) && mi.y == mi.z)) {
-    publish = true;
+  (void)L;
+  const int m = first[n];
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (m > cap || i >= m) return;
+  const int4 mi = meta[i];
+  const int cnt = mi.z - mi.y + 1;
+  const bool leaf = mi.w & 1;
+  if (cnt > kAggDirect && !leaf) return;  // completed by the climb below (leaves: always here)
+  const bool single = leaf && cnt == 1;
+  if (!single) {
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
     for (int t = mi.y; t <= mi.z; ++t) {
@@ -520,17 +528,24 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
         B.x += be.x; B.y += be.y; B.z += be.z;
       }
     }
-    if (mode == 0) { st4(lo + node, l); st4(hi + node, h); }
-    s0[node] = A;
-    s1[node] = B;
+    if (mode == 0) { st4(lo + i, l); st4(hi + i, h); }
+    s0[i] = A;
+    s1[i] = B;
   }
+  int node = (int)i;
+  {
+    const int par = parent[node];
+    if (par < 0) return;
+    const int4 mp4 = meta[par];  // (a parent is internal)
+    if (mp4.z - mp4.y + 1 <= kAggDirect) return;  // the parent sums its own range
+  }
+  bool publish = !single;  // a single-point leaf has nothing to publish
   for (;;) {
     const int par = parent[node];
     if (par < 0) return;
     // release arrival: this child's sums are published before its count; the
     // last child reads its siblings' sums with L2 loads (ld.cg, never through
-    // L1), so no acquire-side L1 invalidation (CCTL.IVALL) is needed -- it was
-    // 20 % of this kernel's stall samples
+    // L1), so no acquire-side L1 invalidation (CCTL.IVALL) is needed
     cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
     const int old = publish ? arrive.fetch_add(1, cuda::memory_order_release)
                             : arrive.fetch_add(1, cuda::memory_order_relaxed);
@@ -853,9 +868,9 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<double4>(), (double4*)squ);
   GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
   if (prec == kF32)
-    k_aggregate<float><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
+    k_aggregate<float><<<nblocks(t.cap, kNT), kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
   else
-    k_aggregate<double><<<nb, kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
+    k_aggregate<double><<<nblocks(t.cap, kNT), kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
   GS_CUDA_OK(cudaGetLastError());
   (void)mb;
   const int fs = tree_finalize_fwd(prec, t, kc, st);
@@ -967,11 +982,11 @@ int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
   if (prec == kF32) {
     k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
-    k_aggregate<float><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
+    k_aggregate<float><<<nblocks(t.cap, kNT), kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
     k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<float4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<float4>());
   } else {
     k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
-    k_aggregate<double><<<nb, kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
+    k_aggregate<double><<<nblocks(t.cap, kNT), kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
     k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<double4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<double4>());
   }
   GS_CUDA_OK(cudaGetLastError());

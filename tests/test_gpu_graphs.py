@@ -51,3 +51,28 @@ def test_graph_replay_bitwise_equals_eager(tmp_path):
     for k in g.files:
         assert np.array_equal(g[k], e[k]), k
 
+
+
+LIFETIME = r"""
+import numpy as np
+from paper_1907_04834_b200 import Geoshoot, ShootingConfig, BARNES_HUT
+g = Geoshoot(0)
+q = np.random.default_rng(1).uniform(0, 1, (2000, 3))
+p = np.zeros_like(q)
+f = g.flow(ShootingConfig(sigma=0.05, timesteps=2, backend=BARNES_HUT), len(q))
+f.upload(q, p)
+f.advance(1)
+t = g.build_tree(q, p)
+g.close()      # the context goes first ...
+del f, t       # ... its flow and tree are still destroyable (gs_destroy detaches them)
+print("ok")
+"""
+
+
+def test_flow_and_tree_outlive_their_context():
+    """gs_destroy before gs_flow_destroy / gs_tree_free (e.g. objects kept
+    alive by a traceback past a fixture's teardown) must not touch the dead
+    context."""
+    r = subprocess.run([sys.executable, "-c", LIFETIME], cwd=ROOT, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.returncode, r.stderr[-2000:])
