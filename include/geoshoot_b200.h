@@ -118,6 +118,8 @@ typedef struct gs_ctx gs_ctx;
 
 /* ---- context --------------------------------------------------------------- */
 gs_ctx* gs_create(int device, gs_status* status);
+/* Flows and trees made on the context are detached, not freed: afterwards
+   they may only be released (gs_flow_destroy / gs_tree_free). */
 void gs_destroy(gs_ctx* ctx);
 const char* gs_last_error(const gs_ctx* ctx);
 /* Literal-mean-dot mode of the context's tree-level Barnes-Hut calls
