@@ -47,10 +47,6 @@ double gate_t2(double thr) {
 namespace {
 
 constexpr int kBhNT = 128;
-#ifndef GS_BH_WHOLE_RECORD
-#define GS_BH_WHOLE_RECORD 1
-#endif
-constexpr bool kLoadWholeRecord = GS_BH_WHOLE_RECORD != 0;
 #ifndef GS_BH_WS_NOWIN_MINB
 #define GS_BH_WS_NOWIN_MINB 7
 #endif
@@ -100,17 +96,6 @@ __device__ __forceinline__ bool gate_exact(double lx, double ly, double lz, doub
   const double dz = fmax(fmax(__dsub_rn(lz, z), 0.0), __dsub_rn(z, hz));
   const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
   return d2 > T2;
-}
-
-__device__ __forceinline__ bool gate(const float4& l, const float4& h, const float4& x,
-                                     const BhArgs<float>& a) {
-  const float dx = fmaxf(fmaxf(l.x - x.x, 0.f), x.x - h.x);
-  const float dy = fmaxf(fmaxf(l.y - x.y, 0.f), x.y - h.y);
-  const float dz = fmaxf(fmaxf(l.z - x.z, 0.f), x.z - h.z);
-  const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  if (d2 > a.thr2_hi) return true;
-  if (d2 < a.thr2_lo) return false;
-  return gate_exact(l.x, l.y, l.z, h.x, h.y, h.z, x.x, x.y, x.z, a.T2);
 }
 
 __device__ __forceinline__ bool gate(const double4& l, const double4& h, const double4& x,
