@@ -263,13 +263,30 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   if (tile == 0) {
     mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
   } else {
+    // four predecessors' status words per round trip (independent loads),
+    // consumed in order; an unpublished one is polled again from there
     for (int t = tile - 1;;) {
-      cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)t * 256 + d]);
-      const unsigned v = prev.load(cuda::memory_order_relaxed);
-      if (!(v & (kRsFlagAgg | kRsFlagPrefix))) continue;  // that tile has not published yet
-      excl += v & kRsCountMask;
-      if (v & kRsFlagPrefix) break;
-      --t;
+      unsigned v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = kRsFlagPrefix;  // (before tile 0: never reached, tile 0 is a prefix)
+        if (t - k >= 0) {
+          cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)(t - k) * 256 + d]);
+          v[k] = prev.load(cuda::memory_order_relaxed);
+        }
+      }
+      bool done = false;
+      int used = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (done || used < k) break;  // stopped at a prefix or an unpublished tile
+        if (!(v[k] & (kRsFlagAgg | kRsFlagPrefix))) break;  // that tile has not published yet
+        excl += v[k] & kRsCountMask;
+        ++used;
+        if (v[k] & kRsFlagPrefix) done = true;
+      }
+      if (done) break;
+      t -= used;
     }
     mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
   }
