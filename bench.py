@@ -244,7 +244,7 @@ def run_ours(args):
         "peak_register_operand_ffma": ffma_reg.value / 16.0 / 1e9,
         "peak_packed_ffma2": ffma2.value / 16.0 / 1e9,
         "sfu_frac": achieved * 1e9 / ex2.value if ex2.value else None,
-        "kernel": "k_rhs_f32x2<8,128,3> (packed FFMA2)", "kernel_ms_avg": k_ms,
+        "kernel": "k_rhs_f32x2<12,128,2,8> (packed FFMA2, source loop unrolled 8)", "kernel_ms_avg": k_ms,
         "kernel_share_of_step": prof["kernel_ms"] / ms if ms else None,
         "algorithmic_per_launch": f"{pairs_per_launch:.3e} ordered pairs x 16 FP32 + 1 MUFU",
     }

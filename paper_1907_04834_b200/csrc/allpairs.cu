@@ -184,7 +184,7 @@ __device__ __forceinline__ f2 nex2x2(f2 r2) {
 // 2 MUFU + FMUL2 + 2 FFMA2 (p_i.p_j) + FMUL2 (c) + 3 FFMA2 (sum g p_j) +
 // 3 FFMA2 (sum c d') = 16 packed FP32 + 2 SFU issue slots (9 per pair instead
 // of 17); identical arithmetic per target to the scalar kernel.
-template <int TPT, int NT, int MINB>
+template <int TPT, int NT, int MINB, int UNR = 2>
 __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict__ rec, int n,
                                                         int tgt_begin, int n_tgt, int chunk,
                                                         float kap, float kc0x, float kc0y,
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
       sp[u] = p;
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll UNR
     for (int u = 0; u < kTile; ++u) {
       const float4 a = sq[u];
       const float4 b = sp[u];
@@ -950,13 +950,15 @@ struct RhsVariant {
 static const RhsVariant kRhsVariants[] = {
     {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true},
     // packed FP32x2 (FFMA2) variants
-    {8, 3, true}, {8, 4, true}, {4, 6, true}, {2, 8, true}};
+    {8, 3, true}, {8, 4, true}, {4, 6, true}, {2, 8, true},
+    // packed, source loop unrolled 4 / 8 (fewer loop-carried register copies), TPT 12
+    {8, 3, true}, {8, 3, true}, {12, 2, true}, {12, 2, true}, {16, 2, true}, {16, 1, true}};
 constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
 
 static int rhs_variant() {
   static int v = [] {
     const char* e = std::getenv("GS_RHS_VARIANT");
-    const int x = e ? std::atoi(e) : 8;
+    const int x = e ? std::atoi(e) : 13;
     return (x >= 0 && x < kNumRhsVariants) ? x : 0;
   }();
   return v;
@@ -975,17 +977,17 @@ static int occ_rhs_f32() {
   return occupancy(k_rhs_f32<TPT, kNT, MINB, PH>, kNT);
 }
 
-template <int TPT, int MINB>
+template <int TPT, int MINB, int UNR = 2>
 static void launch_rhs_f32x2(const Plan& pl, cudaStream_t st, const float4* rec, int n, int tb,
                              int nt, const KernelConsts& kc, float4* part) {
-  k_rhs_f32x2<TPT, kNT, MINB><<<pl.grid, kNT, 0, st>>>(
+  k_rhs_f32x2<TPT, kNT, MINB, UNR><<<pl.grid, kNT, 0, st>>>(
       rec, n, tb, nt, pl.chunk, (float)kc.kappa, (float)(kc.kappa * kc.c0[0]),
       (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), part);
 }
 
-template <int TPT, int MINB>
+template <int TPT, int MINB, int UNR = 2>
 static int occ_rhs_f32x2() {
-  return occupancy(k_rhs_f32x2<TPT, kNT, MINB>, kNT);
+  return occupancy(k_rhs_f32x2<TPT, kNT, MINB, UNR>, kNT);
 }
 
 // Exact FP32 RHS over Morton-ordered points (morton_order) with the
@@ -1033,6 +1035,9 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     // small problems: fall back to narrower target blocks so the grid fills the GPU
     const long slots = 3L * dev.sms;
     int use = vi;
+    // default: TPT 12 once the grid holds many waves of its larger blocks
+    // (measured: 1.933 vs 1.913 Tpair/s at 1M; 1.81 vs 1.89 at 100k)
+    if (!std::getenv("GS_RHS_VARIANT") && n_tgt >= 500000) use = 15;
     // (packed TPT 2 when the chosen variant is packed, scalar TPT 1 for tiny N)
     if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = vi >= 8 ? 11 : 6;
     if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;
@@ -1042,7 +1047,9 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
         occ_rhs_f32<4, 6, true>(), occ_rhs_f32<4, 4, false>(), occ_rhs_f32<6, 4, true>(),
         occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>(),
         occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>(),
-        occ_rhs_f32x2<2, 8>()};
+        occ_rhs_f32x2<2, 8>(), occ_rhs_f32x2<8, 3, 4>(), occ_rhs_f32x2<8, 3, 8>(),
+        occ_rhs_f32x2<12, 2, 4>(), occ_rhs_f32x2<12, 2, 8>(), occ_rhs_f32x2<16, 2, 4>(),
+        occ_rhs_f32x2<16, 1, 4>()};
     const int tp[] = {u.tpt};
     Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
     if (pl.S > part_cap_chunks) return -1;
@@ -1060,6 +1067,12 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
       case 9: launch_rhs_f32x2<8, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 10: launch_rhs_f32x2<4, 6>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 11: launch_rhs_f32x2<2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 12: launch_rhs_f32x2<8, 3, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 13: launch_rhs_f32x2<8, 3, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 14: launch_rhs_f32x2<12, 2, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 15: launch_rhs_f32x2<12, 2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 16: launch_rhs_f32x2<16, 2, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 17: launch_rhs_f32x2<16, 1, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
     }
     return pl.S;
