@@ -29,6 +29,12 @@
 namespace gsb {
 
 constexpr int kTile = 256;
+#ifndef GS_SORTED_UNR
+#define GS_SORTED_UNR 8
+#endif
+#ifndef GS_F64_UNR
+#define GS_F64_UNR 4
+#endif
 #ifndef GS_HESS_MINB
 #define GS_HESS_MINB 1
 #endif
@@ -36,6 +42,9 @@ constexpr int kTile = 256;
 // ----------------------------------------------------------------------------
 // forward RHS partials: A = sum_j g p_j, B = sum_j (p_i.p_j) g d'_ij
 // ----------------------------------------------------------------------------
+constexpr int kSortedUnr = GS_SORTED_UNR;  // source-loop unroll, k_rhs_f32x2_sorted
+constexpr int kF64Unr = GS_F64_UNR;        // source-loop unroll, k_rhs_f64
+
 template <int TPT, int NT, int MINB, bool PHASED>
 __global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__ rec, int n,
                                                       int tgt_begin, int n_tgt, int chunk,
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (!wvalid || hx * hx + hy * hy + hz * hz > cut2) continue;
     }
     if (cnt && lane == 0) atomicAdd(cnt, 1ull);  // GS_EXACT_CUT_DEBUG: computed (warp, tile) pairs
-#pragma unroll 2
+#pragma unroll kSortedUnr
     for (int u = 0; u < kTile; ++u) {
       const float4 a = sq[u];
       const float4 b = sp[u];
@@ -584,6 +593,7 @@ __global__ void __launch_bounds__(NT) k_rhs_f64(const double4* __restrict__ rec,
       sp[u] = p;
     }
     __syncthreads();
+#pragma unroll kF64Unr
     for (int u = 0; u < tile; ++u) {
       const double4 a = sq[u];
       const double4 b = sp[u];
