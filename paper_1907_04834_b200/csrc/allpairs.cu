@@ -962,7 +962,9 @@ static const RhsVariant kRhsVariants[] = {
     // packed FP32x2 (FFMA2) variants
     {8, 3, true}, {8, 4, true}, {4, 6, true}, {2, 8, true},
     // packed, source loop unrolled 4 / 8 (fewer loop-carried register copies), TPT 12
-    {8, 3, true}, {8, 3, true}, {12, 2, true}, {12, 2, true}, {16, 2, true}, {16, 1, true}};
+    {8, 3, true}, {8, 3, true}, {12, 2, true}, {12, 2, true}, {16, 2, true}, {16, 1, true},
+    // small grids (default's fallback), source loop unrolled 8
+    {2, 8, true}};
 constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
 
 static int rhs_variant() {
@@ -1049,7 +1051,7 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     // (measured: 1.933 vs 1.913 Tpair/s at 1M; 1.81 vs 1.89 at 100k)
     if (!std::getenv("GS_RHS_VARIANT") && n_tgt >= 500000) use = 15;
     // (packed TPT 2 when the chosen variant is packed, scalar TPT 1 for tiny N)
-    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = vi >= 8 ? 11 : 6;
+    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = vi >= 12 ? 18 : (vi >= 8 ? 11 : 6);
     if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;
     const RhsVariant u = kRhsVariants[use];
     static int occs[kNumRhsVariants] = {
@@ -1059,7 +1061,7 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
         occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>(),
         occ_rhs_f32x2<2, 8>(), occ_rhs_f32x2<8, 3, 4>(), occ_rhs_f32x2<8, 3, 8>(),
         occ_rhs_f32x2<12, 2, 4>(), occ_rhs_f32x2<12, 2, 8>(), occ_rhs_f32x2<16, 2, 4>(),
-        occ_rhs_f32x2<16, 1, 4>()};
+        occ_rhs_f32x2<16, 1, 4>(), occ_rhs_f32x2<2, 8, 8>()};
     const int tp[] = {u.tpt};
     Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
     if (pl.S > part_cap_chunks) return -1;
@@ -1083,6 +1085,7 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
       case 15: launch_rhs_f32x2<12, 2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 16: launch_rhs_f32x2<16, 2, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 17: launch_rhs_f32x2<16, 1, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 18: launch_rhs_f32x2<2, 8, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
     }
     return pl.S;
