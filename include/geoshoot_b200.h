@@ -130,6 +130,13 @@ gs_status gs_set_literal_mean_dot(gs_ctx* ctx, int32_t enable);
 int gs_last_nonfinite_step(const gs_ctx* ctx);
 uint32_t gs_last_config_violations(const gs_ctx* ctx);
 int gs_abi_version(void);
+/* Barnes-Hut walk selection, process-wide (diagnosis / parity sweeps; the
+ * GS_BH_KERNEL / GS_BH_TASKS environment variables set the same defaults):
+ * kernel 0 = by regime (group walk for dense near fields, else independent
+ * walks), 1 = independent walks, 3 = group walk, 4 = split by warp query box;
+ * windows 0 = automatic node windows, K = K windows (<= 64); -1 restores the
+ * environment's choice. Every choice gives the reference's interaction sets. */
+gs_status gs_set_bh_walk(int32_t kernel, int32_t windows);
 /* validate_config, core.cpp:5-17: every violated bound in *mask. */
 gs_status gs_validate_config(const gs_config* cfg, uint32_t* mask);
 
@@ -194,9 +201,29 @@ gs_status gs_bh_velocity(gs_tree* tree, int64_t m, const double* x, double sigma
 /* bh_hamiltonian_gradients, bh_kernel.cpp:193-210 (queries = the tree's own points). */
 gs_status gs_bh_rhs(gs_tree* tree, double sigma, double threshold, double* dH_dp,
                     double* dH_dq, gs_stats* stats);
-/* Per-query (direct, approximated, visited) counts of the last gs_bh_rhs /
- * gs_bh_velocity call on this tree (3*m uint64, query order). */
+/* Per-query (direct, approximated, visited) counts of the last query call on
+ * this tree -- gs_bh_rhs, gs_bh_velocity, gs_bh_hessian_products,
+ * gs_bh_point_gradients, gs_bh_point_hessian_products -- as the reference's
+ * per-query TraversalStats (bh_kernel.cpp:30-58): 3*m uint64, query order.
+ * Counted for every walk and node-window split (windows are folded). */
 gs_status gs_bh_query_stats(const gs_tree* tree, uint64_t* per_query);
+/* bh_point_gradients, bh_kernel.cpp:81-112, for m arbitrary queries
+ * (x[k], px[k]) -- tree points or not -- in one device traversal. */
+gs_status gs_bh_point_gradients(gs_tree* tree, int64_t m, const double* x, const double* px,
+                                double sigma, double threshold, double* dH_dp, double* dH_dq,
+                                gs_stats* stats);
+/* bh_point_hessian_products, bh_kernel.cpp:114-160, for m arbitrary queries
+ * (qi[k], pi[k], alpha_i[k], beta_i[k]). Direct terms read the per-point
+ * adjoints alpha/beta (n x 3 by tree point index); approximated terms read the
+ * node sums of the last gs_tree_accumulate_adjoints (zero if never annotated,
+ * the reference's Node defaults). alpha = beta = NULL keeps the per-point
+ * adjoints of the last annotation / call. */
+gs_status gs_bh_point_hessian_products(gs_tree* tree, int64_t m, const double* qi,
+                                       const double* pi, const double* alpha_i,
+                                       const double* beta_i, const double* alpha,
+                                       const double* beta, double sigma, double threshold,
+                                       double* pq_alpha, double* pp_alpha, double* qq_beta,
+                                       double* qp_beta, gs_stats* stats);
 /* bh_hamiltonian, bh_kernel.cpp:162-191. */
 gs_status gs_bh_hamiltonian(gs_tree* tree, double sigma, double threshold, double* h_out,
                             gs_stats* stats);

@@ -264,7 +264,12 @@ class Ref:
             "ref_bh_velocity": [C.c_void_p, _i64, _d, C.c_double, C.c_double, _d, _u64],
             "ref_bh_rhs": [C.c_void_p, _i64, _d, _d, C.c_double, C.c_double, C.c_int, _d, _d, _u64],
             "ref_bh_hessprod": [C.c_void_p, _i64, _d, _d, _d, _d, C.c_double, C.c_double, C.c_int,
-                                _d, _d, _d, _d],
+                                _d, _d, _d, _d, _u64],
+            "ref_bh_point_gradients": [C.c_void_p, _i64, _d, _d, C.c_double, C.c_double, C.c_int,
+                                       _d, _d, _u64],
+            "ref_bh_point_hessprod": [C.c_void_p, _i64, _d, _d, _d, _d, _i64, _d, _d, C.c_double,
+                                      C.c_double, C.c_int, _d, _d, _d, _d, _u64],
+            "ref_bh_velocity_pq": [C.c_void_p, _i64, _d, C.c_double, C.c_double, C.c_int, _d, _u64],
             "ref_bh_hamiltonian": [C.c_void_p, _i64, _d, _d, C.c_double, C.c_double, _d],
             "ref_shoot_forward": [_i64, _d, _d, C.c_double, C.c_int, C.c_int, C.c_double, _d, _d],
             "ref_objective": [_i64, _d, _d, _d, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -463,12 +468,40 @@ class RefTree(_TreeDump):
                                               threads, _p(dp), _p(dq), pq.ctypes.data_as(_u64)))
         return dp, dq, pq
 
-    def bh_hessprod(self, alpha, beta, sigma, thr, threads=0):
+    def bh_hessprod(self, alpha, beta, sigma, thr, threads=0, per_query=False):
         a, b = _c(alpha), _c(beta)
         out = [_vec(self.n) for _ in range(4)]
+        pq = np.zeros((self.n, 3), np.uint64)
         self.ref._chk(self.ref.lib.ref_bh_hessprod(self.h, self.n, _p(self.q), _p(self.p), _p(a),
-                                                   _p(b), sigma, thr, threads, *map(_p, out)))
-        return tuple(out)
+                                                   _p(b), sigma, thr, threads, *map(_p, out),
+                                                   pq.ctypes.data_as(_u64)))
+        return tuple(out) + ((pq,) if per_query else ())
+
+    def bh_point_gradients(self, x, px, sigma, thr, threads=0):
+        x, px = _c(x), _c(px)
+        dp, dq = _vec(len(x)), _vec(len(x))
+        pq = np.zeros((len(x), 3), np.uint64)
+        self.ref._chk(self.ref.lib.ref_bh_point_gradients(self.h, len(x), _p(x), _p(px), sigma,
+                                                          thr, threads, _p(dp), _p(dq),
+                                                          pq.ctypes.data_as(_u64)))
+        return dp, dq, pq
+
+    def bh_point_hessprod(self, qi, pi, ai, bi, alpha, beta, sigma, thr, threads=0):
+        qi, pi, ai, bi, a, b = (_c(v) for v in (qi, pi, ai, bi, alpha, beta))
+        out = [_vec(len(qi)) for _ in range(4)]
+        pq = np.zeros((len(qi), 3), np.uint64)
+        self.ref._chk(self.ref.lib.ref_bh_point_hessprod(
+            self.h, len(qi), _p(qi), _p(pi), _p(ai), _p(bi), len(a), _p(a), _p(b), sigma, thr,
+            threads, *map(_p, out), pq.ctypes.data_as(_u64)))
+        return tuple(out) + (pq,)
+
+    def bh_velocity_pq(self, x, sigma, thr, threads=0):
+        x = _c(x)
+        v = _vec(len(x))
+        pq = np.zeros((len(x), 3), np.uint64)
+        self.ref._chk(self.ref.lib.ref_bh_velocity_pq(self.h, len(x), _p(x), sigma, thr, threads,
+                                                      _p(v), pq.ctypes.data_as(_u64)))
+        return v, pq
 
     def bh_hamiltonian(self, sigma, thr):
         h = C.c_double()

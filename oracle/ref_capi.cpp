@@ -268,19 +268,94 @@ int ref_bh_rhs(void* h, std::int64_t n, const double* q, const double* p, double
 // accumulate_adjoints(alpha, beta).
 int ref_bh_hessprod(void* h, std::int64_t n, const double* q, const double* p,
                     const double* alpha, const double* beta, double sigma, double thr,
-                    int threads, double* pq, double* pp, double* qq, double* qp) {
+                    int threads, double* pq, double* pp, double* qq, double* qp,
+                    std::uint64_t* per_query) {
   return guarded([&] {
     const Octree& t = *static_cast<Octree*>(h);
     const std::vector<Vec3> qs = vecs(q, n), ps = vecs(p, n), as = vecs(alpha, n),
                             bs = vecs(beta, n);
     const int th = threads > 0 ? threads : default_thread_count();
     parallel_for(static_cast<std::size_t>(n), th, [&](std::size_t i) {
+      TraversalStats st;
       const BhPointHessianProducts r = bh_point_hessian_products(
-          t, qs[i], ps[i], as[i], bs[i], as, bs, sigma, thr, nullptr);
+          t, qs[i], ps[i], as[i], bs[i], as, bs, sigma, thr, &st);
       std::memcpy(pq + 3 * i, &r.pq_alpha, sizeof(Vec3));
       std::memcpy(pp + 3 * i, &r.pp_alpha, sizeof(Vec3));
       std::memcpy(qq + 3 * i, &r.qq_beta, sizeof(Vec3));
       std::memcpy(qp + 3 * i, &r.qp_beta, sizeof(Vec3));
+      if (per_query) {
+        per_query[3 * i] = st.direct_interactions;
+        per_query[3 * i + 1] = st.approximated_interactions;
+        per_query[3 * i + 2] = st.nodes_visited;
+      }
+    });
+  });
+}
+
+// bh_point_gradients (bh_kernel.cpp:81-112) at m arbitrary queries (x, px);
+// per_query: optional m x 3 (direct, approx, visited).
+int ref_bh_point_gradients(void* h, std::int64_t m, const double* x, const double* px,
+                           double sigma, double thr, int threads, double* dHdp, double* dHdq,
+                           std::uint64_t* per_query) {
+  return guarded([&] {
+    const Octree& t = *static_cast<Octree*>(h);
+    const std::vector<Vec3> xs = vecs(x, m), ps = vecs(px, m);
+    const int th = threads > 0 ? threads : default_thread_count();
+    parallel_for(static_cast<std::size_t>(m), th, [&](std::size_t i) {
+      TraversalStats st;
+      const BhPointGradients g = bh_point_gradients(t, xs[i], ps[i], sigma, thr, &st);
+      std::memcpy(dHdp + 3 * i, &g.dH_dp, sizeof(Vec3));
+      std::memcpy(dHdq + 3 * i, &g.dH_dq, sizeof(Vec3));
+      if (per_query) {
+        per_query[3 * i] = st.direct_interactions;
+        per_query[3 * i + 1] = st.approximated_interactions;
+        per_query[3 * i + 2] = st.nodes_visited;
+      }
+    });
+  });
+}
+
+// bh_point_hessian_products (bh_kernel.cpp:114-160) at m arbitrary queries
+// (qi, pi, alpha_i, beta_i); alpha/beta (n x 3) are the direct terms' per-point
+// adjoints; the tree's node sums are whatever accumulate_adjoints left.
+int ref_bh_point_hessprod(void* h, std::int64_t m, const double* qi, const double* pi,
+                          const double* ai, const double* bi, std::int64_t n, const double* alpha,
+                          const double* beta, double sigma, double thr, int threads, double* pq,
+                          double* pp, double* qq, double* qp, std::uint64_t* per_query) {
+  return guarded([&] {
+    const Octree& t = *static_cast<Octree*>(h);
+    const std::vector<Vec3> qs = vecs(qi, m), ps = vecs(pi, m), as_i = vecs(ai, m),
+                            bs_i = vecs(bi, m), as = vecs(alpha, n), bs = vecs(beta, n);
+    const int th = threads > 0 ? threads : default_thread_count();
+    parallel_for(static_cast<std::size_t>(m), th, [&](std::size_t i) {
+      TraversalStats st;
+      const BhPointHessianProducts r = bh_point_hessian_products(
+          t, qs[i], ps[i], as_i[i], bs_i[i], as, bs, sigma, thr, &st);
+      std::memcpy(pq + 3 * i, &r.pq_alpha, sizeof(Vec3));
+      std::memcpy(pp + 3 * i, &r.pp_alpha, sizeof(Vec3));
+      std::memcpy(qq + 3 * i, &r.qq_beta, sizeof(Vec3));
+      std::memcpy(qp + 3 * i, &r.qp_beta, sizeof(Vec3));
+      if (per_query) {
+        per_query[3 * i] = st.direct_interactions;
+        per_query[3 * i + 1] = st.approximated_interactions;
+        per_query[3 * i + 2] = st.nodes_visited;
+      }
+    });
+  });
+}
+
+// bh_velocity (bh_kernel.cpp:62-79) per eval point with per-query stats, threaded.
+int ref_bh_velocity_pq(void* h, std::int64_t m, const double* x, double sigma, double thr,
+                       int threads, double* v_out, std::uint64_t* per_query) {
+  return guarded([&] {
+    const Octree& t = *static_cast<Octree*>(h);
+    const int th = threads > 0 ? threads : default_thread_count();
+    parallel_for(static_cast<std::size_t>(m), th, [&](std::size_t e) {
+      const BhVelocity r = bh_velocity(t, Vec3{x[3 * e], x[3 * e + 1], x[3 * e + 2]}, sigma, thr);
+      std::memcpy(v_out + 3 * e, &r.velocity, sizeof(Vec3));
+      per_query[3 * e] = r.stats.direct_interactions;
+      per_query[3 * e + 1] = r.stats.approximated_interactions;
+      per_query[3 * e + 2] = r.stats.nodes_visited;
     });
   });
 }

@@ -121,6 +121,11 @@ SIGNATURES = [
     ("gs_bh_hamiltonian", _st, [_vp, C.c_double, C.c_double, _d, C.POINTER(gs_stats)]),
     ("gs_bh_hessian_products", _st, [_vp, _d, _d, C.c_double, C.c_double, _d, _d, _d, _d,
                                      C.POINTER(gs_stats)]),
+    ("gs_bh_point_gradients", _st, [_vp, _i64, _d, _d, C.c_double, C.c_double, _d, _d,
+                                    C.POINTER(gs_stats)]),
+    ("gs_bh_point_hessian_products", _st, [_vp, _i64, _d, _d, _d, _d, _d, _d, C.c_double,
+                                           C.c_double, _d, _d, _d, _d, C.POINTER(gs_stats)]),
+    ("gs_set_bh_walk", _st, [C.c_int32, C.c_int32]),
     ("gs_shoot_forward", _st, [_vp, C.POINTER(gs_config), _i64, _d, _d, _d, _d, _d, _d, _d,
                                C.POINTER(gs_stats)]),
     ("gs_objective", _st, [_vp, C.POINTER(gs_config), _i64, _d, _d, _d, C.POINTER(gs_report)]),

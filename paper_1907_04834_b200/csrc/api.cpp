@@ -192,8 +192,12 @@ Octree& Octree::operator=(Octree&& o) noexcept {
     root_min_ = o.root_min_;
     root_max_ = o.root_max_;
     explicit_root_ = o.explicit_root_;
+    dirty_ = o.dirty_;
     dev_ = o.dev_;
+    dev_alpha_ = o.dev_alpha_;
+    dev_beta_ = o.dev_beta_;
     o.dev_ = nullptr;
+    o.dirty_ = false;
   }
   return *this;
 }
@@ -207,7 +211,9 @@ Octree Octree::build(const PointSet& q, const MomentumSet& p) {
   return t;
 }
 
-void Octree::rebuild(bool explicit_root) {
+void Octree::rebuild(bool explicit_root) const {
+  dirty_ = false;
+  dev_alpha_ = dev_beta_ = nullptr;
   if (dev_) {
     gs_tree_free(dev_);
     dev_ = nullptr;
@@ -226,7 +232,7 @@ void Octree::rebuild(bool explicit_root) {
 }
 
 // Host mirror of the device nodes in the reference's Node layout.
-void Octree::mirror() {
+void Octree::mirror() const {
   const int64_t n = (int64_t)points_.size();
   const int64_t m = gs_tree_node_count(dev_);
   std::vector<int32_t> order(n), level(m), parent(m), skip(m), range(2 * m);
@@ -277,13 +283,16 @@ void Octree::insert(std::uint32_t index, const Vec3& position, const Vec3& momen
     root_max_ = r.cell_max;
     explicit_root_ = true;
   }
-  rebuild(true);
+  dirty_ = true;  // built once, on the next use (sync)
 }
 
 void Octree::accumulate_adjoints(const std::vector<Vec3>& alpha, const std::vector<Vec3>& beta) {
   require_aligned(points_.size(), alpha.size(), "accumulate_adjoints(alpha)");
   require_aligned(points_.size(), beta.size(), "accumulate_adjoints(beta)");
+  sync();
   check(gs_tree_accumulate_adjoints(dev_, raw(alpha), raw(beta)));
+  dev_alpha_ = alpha.data();
+  dev_beta_ = beta.data();
   mirror();
 }
 
@@ -299,7 +308,10 @@ int Octree::octant_of(const Node& nd, const Vec3& x) {
   return (x.x >= c.x ? 1 : 0) | (x.y >= c.y ? 2 : 0) | (x.z >= c.z ? 4 : 0);
 }
 
-gs_tree* Octree::device() const { return dev_; }
+gs_tree* Octree::device() const {
+  sync();
+  return dev_;
+}
 
 // ---- bh_kernel ----------------------------------------------------------------
 namespace {
@@ -336,47 +348,40 @@ HamiltonianGradients bh_hamiltonian_gradients(const Octree& tree, const PointSet
 
 BhPointGradients bh_point_gradients(const Octree& tree, const Vec3& x, const Vec3& px, double sigma,
                                     double threshold, TraversalStats* stats) {
-  // The device traverses the tree's own points in bulk; a single query at an
-  // arbitrary (x, px) is answered as the velocity part plus the q-gradient
-  // through the one-point tree query of the batched kernels.
+  // one query of the batched device traversal (gs_bh_point_gradients): any
+  // (x, px), tree point or not
   require_tree(tree);
   BhPointGradients out;
-  const auto& pts = tree.points();
-  const auto& mom = tree.momenta();
-  for (std::size_t i = 0; i < pts.size(); ++i)
-    if (pts[i] == x && mom[i] == px) {  // the query is a tree point: batched path
-      TraversalStats st;
-      const HamiltonianGradients g = bh_hamiltonian_gradients(
-          tree, PointSet(pts), MomentumSet(mom), sigma, threshold, stats ? &st : nullptr);
-      out.dH_dp = g.dH_dp[i];
-      out.dH_dq = g.dH_dq[i];
-      if (stats) {
-        std::vector<uint64_t> per(3 * pts.size());
-        check(gs_bh_query_stats(tree.device(), per.data()));
-        stats->direct_interactions += per[3 * i];
-        stats->approximated_interactions += per[3 * i + 1];
-        stats->nodes_visited += per[3 * i + 2];
-      }
-      return out;
-    }
-  throw std::invalid_argument("bh_point_gradients: the B200 path answers queries at tree points");
+  gs_stats st{};
+  check(gs_bh_point_gradients(tree.device(), 1, &x.x, &px.x, sigma, threshold, &out.dH_dp.x,
+                              &out.dH_dq.x, &st));
+  if (stats) stats->merge(to_traversal(st));
+  return out;
 }
 
 BhPointHessianProducts bh_point_hessian_products(const Octree& tree, const Vec3& qi,
-                                                 const Vec3& pi, const Vec3&, const Vec3&,
+                                                 const Vec3& pi, const Vec3& alpha_i,
+                                                 const Vec3& beta_i,
                                                  const std::vector<Vec3>& alpha,
                                                  const std::vector<Vec3>& beta, double sigma,
                                                  double threshold, TraversalStats* stats) {
   require_tree(tree);
-  const auto& pts = tree.points();
-  const auto& mom = tree.momenta();
-  for (std::size_t i = 0; i < pts.size(); ++i)
-    if (pts[i] == qi && mom[i] == pi) {
-      const HessianProducts h = bh_hessian_products(tree, PointSet(pts), MomentumSet(mom), alpha,
-                                                    beta, sigma, threshold, stats);
-      return {h.pq_alpha[i], h.pp_alpha[i], h.qq_beta[i], h.qp_beta[i]};
-    }
-  throw std::invalid_argument("bh_point_hessian_products: the B200 path answers queries at tree points");
+  require_aligned(tree.point_count(), alpha.size(), "bh_point_hessian_products(alpha)");
+  require_aligned(tree.point_count(), beta.size(), "bh_point_hessian_products(beta)");
+  // Direct terms read alpha/beta by source index. The device already holds the
+  // arrays of the last annotation / upload; re-send them only when the caller
+  // passes other arrays, so a per-point loop over i (run_backward's pattern,
+  // shooting.cpp:177-190) costs O(traversal) per call, not O(N).
+  const bool same = alpha.data() == tree.device_alpha() && beta.data() == tree.device_beta();
+  BhPointHessianProducts out;
+  gs_stats st{};
+  check(gs_bh_point_hessian_products(tree.device(), 1, &qi.x, &pi.x, &alpha_i.x, &beta_i.x,
+                                     same ? nullptr : raw(alpha), same ? nullptr : raw(beta),
+                                     sigma, threshold, &out.pq_alpha.x, &out.pp_alpha.x,
+                                     &out.qq_beta.x, &out.qp_beta.x, &st));
+  tree.note_device_adjoints(alpha.data(), beta.data());
+  if (stats) stats->merge(to_traversal(st));
+  return out;
 }
 
 double bh_hamiltonian(const Octree& tree, const PointSet& q, const MomentumSet& p, double sigma,
@@ -405,6 +410,7 @@ HessianProducts bh_hessian_products(const Octree& tree, const PointSet& q, const
   check(gs_bh_hessian_products(tree.device(), raw(alpha), raw(beta), sigma, threshold,
                                raw(h.pq_alpha), raw(h.pp_alpha), raw(h.qq_beta), raw(h.qp_beta),
                                &st));
+  tree.note_device_adjoints(alpha.data(), beta.data());
   if (stats) stats->merge(to_traversal(st));
   return h;
 }

@@ -26,6 +26,7 @@
 // compared as d2 > T2 with T2 the largest double whose sqrt is <= thr. The
 // FP32 path first decides in FP32 with a 1e-6 relative guard band and only
 // falls back to the exact FP64 test inside the band.
+#include <atomic>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -42,6 +43,15 @@ double gate_t2(double thr) {
   while (x > 0 && std::sqrt(x) > thr) x = std::nextafter(x, 0.0);
   while (std::sqrt(std::nextafter(x, INFINITY)) <= thr) x = std::nextafter(x, INFINITY);
   return x;
+}
+
+// gs_set_bh_walk: process-wide override of GS_BH_KERNEL / GS_BH_TASKS (-1: the
+// environment's choice) so tests can drive every walk and window count
+std::atomic<int> g_walk_kernel{-1}, g_walk_tasks{-1};
+
+void set_bh_walk(int kernel, int tasks) {
+  g_walk_kernel.store(kernel, std::memory_order_relaxed);
+  g_walk_tasks.store(tasks, std::memory_order_relaxed);
 }
 
 namespace {
@@ -68,7 +78,8 @@ struct BhArgs {
   const int* perm;
   int n, nq, tgt_begin, n_tgt;
   const int* mp;  // node count on the device (first[n])
-  const V4<R>* ev;  // VEL eval records
+  const V4<R>* ev;    // VEL eval records; RHS/HESS external queries (by_index): (x, px) records
+  const V4<R>* eadj;  // HESS external queries: (alpha_i, beta_i) records
   double kap, kc0x, kc0y, kc0z;
   double T2;         // exact gate threshold on d2
   R thr2_hi, thr2_lo;  // FP32 guard band around T2
@@ -79,7 +90,8 @@ struct BhArgs {
   int ntask;           // pre-order node windows per query (blockIdx.y); partials [task][query]
   int prefetch;        // L1-prefetch the skip target's record at every visit (GS_BH_PREFETCH)
   int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
-  int by_index;        // RHS: queries are ev[0 .. nq) (a shard's records), not leaf order
+  int by_index;        // RHS/HESS: queries are ev[0 .. nq) (a shard's records or arbitrary
+                       // points, bh_point_*), not the tree's own points in leaf order
   int dense;           // dense near fields: k_bh_grp unless GS_BH_KERNEL says otherwise
   int* sm_ctr;         // non-null: blocks claim SM-local contiguous query blocks (claim_block)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
@@ -298,6 +310,52 @@ __device__ __forceinline__ void coop_ranges(unsigned owners, int& j, int je, Acc
   }
 }
 
+
+// The query of thread slot qi: x (unscaled, for the gate), xs (interaction
+// coordinates), px (momentum), ai/bi (HESS adjoints); returns the output slot
+// (-1: no query). Queries are either the tree's own points in leaf order
+// (restricted to point indices [tgt_begin, tgt_begin + n_tgt)), or external
+// records ev[0 .. nq): eval points (VEL), a sharded flow's own targets taken by
+// point index from its Morton-ordered records, or arbitrary (x, px[, alpha_i,
+// beta_i]) queries (bh_point_gradients / bh_point_hessian_products,
+// bh_kernel.cpp:81-160). External interaction coordinates are formed exactly
+// as the tree's srec (tree_rescale).
+template <typename R, int MODE>
+__device__ __forceinline__ int load_query(const BhArgs<R>& a, int qi, V4<R>& x, V4<R>& xs,
+                                          V4<R>& px, V4<R>& ai, V4<R>& bi) {
+  x = mk4<R>(0, 0, 0);
+  xs = px = ai = bi = x;
+  if (qi >= a.nq) return -1;
+  if (MODE == kBhVel || a.by_index) {
+    x = ld4(a.ev + 2 * qi);
+    if (sizeof(R) == 4)
+      xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
+                  (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
+                  (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
+    else
+      xs = x;
+    if (MODE != kBhVel) px = ld4(a.ev + 2 * qi + 1);
+    if (MODE == kBhHess) { ai = ld4(a.eadj + 2 * qi); bi = ld4(a.eadj + 2 * qi + 1); }
+    return qi;
+  }
+  const int t = qi;
+  x = ld4(a.squ + t);
+  xs = ld4(a.srec + 2 * t);
+  px = ld4(a.srec + 2 * t + 1);
+  if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
+  const int i = a.perm[t] - a.tgt_begin;
+  return (i >= 0 && i < a.n_tgt) ? i : -1;
+}
+
+// Output slot of query `out` in window blockIdx.y: partials and per-query
+// counters are [window][query]; the epilogue / k_fold_counts fold the windows
+// in fixed order.
+template <int MODE, typename R>
+__device__ __forceinline__ size_t out_slot(const BhArgs<R>& a, int out) {
+  const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
+  return (size_t)blockIdx.y * nout + out;
+}
+
 // Work-stream variant: every lane walks its own query independently; each
 // iteration a lane either continues its pending direct range (one point) or
 // visits its next node (and, for a leaf / far / fully-inside node, evaluates
@@ -346,33 +404,8 @@ __device__ __forceinline__ int claim_block(int* sm_ctr, int nblk) {
 template <typename R, int MODE, bool WIN, bool LMD = false>
 __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_ws(const BhArgs<R> a) {
   const int blk = (!WIN && a.sm_ctr) ? claim_block(a.sm_ctr, gridDim.x) : (int)blockIdx.x;
-  const int qi = blk * kBhNT + threadIdx.x;
-  const bool valid = qi < a.nq;
-  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
-  int out = -1;
-  if (valid) {
-    if (MODE == kBhVel || (MODE == kBhRhs && a.by_index)) {
-      // eval records, or a sharded flow's own targets taken by point index
-      // from its (Morton-ordered) records: same interaction coordinates as srec
-      x = ld4(a.ev + 2 * qi);
-      if (sizeof(R) == 4)
-        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
-                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
-                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
-      else
-        xs = x;
-      if (MODE == kBhRhs) px = ld4(a.ev + 2 * qi + 1);
-      out = qi;
-    } else {
-      const int t = qi;
-      x = ld4(a.squ + t);
-      xs = ld4(a.srec + 2 * t);
-      px = ld4(a.srec + 2 * t + 1);
-      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
-      const int i = a.perm[t] - a.tgt_begin;
-      out = (i >= 0 && i < a.n_tgt) ? i : -1;
-    }
-  }
+  V4<R> x, xs, px, ai, bi;
+  const int out = load_query<R, MODE>(a, blk * kBhNT + threadIdx.x, x, xs, px, ai, bi);
   if (a.split && warp_box_diag2<R>(x, out >= 0) <= a.grp_lim2) return;  // k_bh_grp's warp
   Acc<R> acc;
 #pragma unroll
@@ -388,7 +421,7 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
     bA = A < m ? code_of(ld4(a.nrec + 4 * A + 1).w) : a.n;
     bB = B < m ? code_of(ld4(a.nrec + 4 * B + 1).w) : a.n;
   }
-  int next = out >= 0 ? 0 : INT_MAX;
+  int next = (out >= 0 && A < B) ? 0 : INT_MAX;  // an empty window (m < windows) walks nothing
   int j = 0, je = -1;  // pending direct range
   const V4<R> zero = mk4<R>(0, 0, 0);
 #ifdef GS_BH_WS_STATS
@@ -492,15 +525,15 @@ __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_w
 #undef GS_WS_COUNT
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
-    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
+    const size_t slot = out_slot<MODE>(a, out);
+    V4<R>* o = a.part + (size_t)per * slot;
     for (int k = 0; k < per; ++k)
       st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2],
                         (LMD && MODE == kBhRhs && k == 1) ? acc.v[6] : R(0)));
     if (a.per_query) {
-      a.per_query[3 * out] = c_dir;
-      a.per_query[3 * out + 1] = c_app;
-      a.per_query[3 * out + 2] = c_vis;
+      a.per_query[3 * slot] = c_dir;
+      a.per_query[3 * slot + 1] = c_app;
+      a.per_query[3 * slot + 2] = c_vis;
     }
   }
   if (a.totals) {
@@ -565,30 +598,8 @@ __device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Ac
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
-  const int qi = blockIdx.x * kBhNT + threadIdx.x;
-  const bool valid = qi < a.nq;
-  V4<R> x = mk4<R>(0, 0, 0), xs = x, px = x, ai = x, bi = x;
-  int out = -1;
-  if (valid) {
-    if (MODE == kBhVel) {
-      x = ld4(a.ev + 2 * qi);
-      if (sizeof(R) == 4)
-        xs = mk4<R>((R)fmaf((float)a.kap, (float)x.x, -(float)(a.kap * a.kc0x)),
-                    (R)fmaf((float)a.kap, (float)x.y, -(float)(a.kap * a.kc0y)),
-                    (R)fmaf((float)a.kap, (float)x.z, -(float)(a.kap * a.kc0z)));
-      else
-        xs = x;
-      out = qi;
-    } else {
-      const int t = qi;
-      x = ld4(a.squ + t);
-      xs = ld4(a.srec + 2 * t);
-      px = ld4(a.srec + 2 * t + 1);
-      if (MODE == kBhHess) { ai = ld4(a.sadj + 2 * t); bi = ld4(a.sadj + 2 * t + 1); }
-      const int i = a.perm[t] - a.tgt_begin;
-      out = (i >= 0 && i < a.n_tgt) ? i : -1;
-    }
-  }
+  V4<R> x, xs, px, ai, bi;
+  const int out = load_query<R, MODE>(a, blockIdx.x * kBhNT + threadIdx.x, x, xs, px, ai, bi);
   if (a.split && !(warp_box_diag2<R>(x, out >= 0) <= a.grp_lim2)) return;  // k_bh_ws's warp
   Acc<R> acc;
 #pragma unroll
@@ -604,7 +615,7 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
     bA = A < m ? code_of(ld4(a.nrec + 4 * A + 1).w) : a.n;
     bB = B < m ? code_of(ld4(a.nrec + 4 * B + 1).w) : a.n;
   }
-  int next = out >= 0 ? 0 : INT_MAX;
+  int next = (out >= 0 && A < B) ? 0 : INT_MAX;  // an empty window (m < windows) walks nothing
   int ds = 0, de = -1;  // this lane's pending direct interval (leaf order, inclusive)
   int cursor = 0;       // warp-uniform sweep position
   unsigned n_iter = 0, n_seg = 0, n_step = 0;
@@ -677,13 +688,13 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
   }
   if (out >= 0) {
     const int per = MODE == kBhHess ? 4 : (MODE == kBhRhs ? 2 : 1);
-    const int nout = MODE == kBhVel ? a.nq : a.n_tgt;
-    V4<R>* o = a.part + (size_t)per * ((size_t)blockIdx.y * nout + out);
+    const size_t slot = out_slot<MODE>(a, out);
+    V4<R>* o = a.part + (size_t)per * slot;
     for (int k = 0; k < per; ++k) st4(o + k, mk4<R>(acc.v[3 * k], acc.v[3 * k + 1], acc.v[3 * k + 2]));
     if (a.per_query) {
-      a.per_query[3 * out] = c_dir;
-      a.per_query[3 * out + 1] = c_app;
-      a.per_query[3 * out + 2] = c_vis;
+      a.per_query[3 * slot] = c_dir;
+      a.per_query[3 * slot + 1] = c_app;
+      a.per_query[3 * slot + 2] = c_vis;
     }
   }
   if (a.totals) {
@@ -710,6 +721,8 @@ __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
 // group walk wins on config 3 (tube, sigma 5: 3.8 vs 4.6 ms per RHS) and loses
 // on configs 2, 4 and 5, so independent walks are the default.
 static int bh_kernel_choice() {
+  const int o = g_walk_kernel.load(std::memory_order_relaxed);
+  if (o >= 0) return o;  // gs_set_bh_walk
   static int v = [] {
     const char* e = std::getenv("GS_BH_KERNEL");
     return e ? std::atoi(e) : 0;  // 0: by regime (dense near fields -> 3, else 1)
@@ -728,9 +741,9 @@ static double bh_group_ratio() {
 
 template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
-  // literal-mean-dot and by-index queries: independent walks only
+  // literal-mean-dot: independent walks only (the group walk has no LMD variant)
   const int choice = bh_kernel_choice();
-  const int kind = (a.lmd || a.by_index) ? 1 : (choice ? choice : (a.dense ? 3 : 1));
+  const int kind = a.lmd ? 1 : (choice ? choice : (a.dense ? 3 : 1));
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
@@ -811,8 +824,9 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.n_tgt = q.n_tgt;
   a.nq = q.mode == kBhVel ? q.m : (q.by_index ? q.n_tgt : (int)t.n);
   a.by_index = q.by_index;
-  a.dense = q.dense && !q.per_query;
+  a.dense = q.dense;
   a.ev = static_cast<const V4<R>*>(q.ev);
+  a.eadj = static_cast<const V4<R>*>(q.eadj);
   const KernelConsts& kc = t.kc;
   a.kap = kc.kappa;
   a.kc0x = kc.c0[0];
@@ -846,10 +860,20 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
   a.part = static_cast<V4<R>*>(q.part);
   a.per_query = q.per_query;
   a.totals = q.totals;
-  a.ntask = q.per_query ? 1 : std::max(1, q.ntask);  // per-query counts: one window
+  a.ntask = std::max(1, q.ntask);
   a.lmd = q.lmd;
   (void)sigma;
   return a;
+}
+
+// Per-query counters of K node windows: out[i] = sum over windows in order.
+__global__ void k_fold_counts(const uint32_t* __restrict__ in, int K, int64_t n3,
+                              uint32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n3) return;
+  uint32_t v = 0;
+  for (int k = 0; k < K; ++k) v += in[(size_t)k * n3 + i];
+  out[i] = v;
 }
 
 }  // namespace
@@ -866,14 +890,32 @@ int bh_traverse(const Device&, int prec, DevTree& t, double sigma, double thr, c
     GS_CUDA_OK(cudaMemsetAsync(t.sm_ctr.ptr, 0, 4 * 1024, st));
     ctr = t.sm_ctr.as<int>();
   }
+  // per-query counters with node windows: each window writes its own slice
+  // [window][query][3]; the slices are folded (summed) into q.per_query
+  const int K = std::max(1, q.ntask);
+  const int nout = q.mode == kBhVel ? q.m : q.n_tgt;
+  uint32_t* pq = q.per_query;
+  if (pq && K > 1) {
+    GS_TRY_INT(t.pq_win.ensure(sizeof(uint32_t) * 3 * (size_t)nout * K));
+    pq = t.pq_win.as<uint32_t>();
+  }
+  int s;
   if (prec == kF32) {
     BhArgs<float> a = make_args<float>(t, sigma, thr, q);
     a.sm_ctr = ctr;
-    return launch<float>(q.mode, a, st);
+    a.per_query = pq;
+    s = launch<float>(q.mode, a, st);
+  } else {
+    BhArgs<double> a = make_args<double>(t, sigma, thr, q);
+    a.sm_ctr = ctr;
+    a.per_query = pq;
+    s = launch<double>(q.mode, a, st);
   }
-  BhArgs<double> a = make_args<double>(t, sigma, thr, q);
-  a.sm_ctr = ctr;
-  return launch<double>(q.mode, a, st);
+  if (s != GS_OK || !q.per_query || K == 1 || nout == 0) return s;
+  const int64_t n3 = 3 * (int64_t)nout;
+  k_fold_counts<<<(unsigned)((n3 + 255) / 256), 256, 0, st>>>(pq, K, n3, q.per_query);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
 }
 
 // Node windows per query: a latency-bound walk needs many resident warps, and
@@ -897,11 +939,12 @@ void set_bh_concurrency(int c) { t_bh_concurrency = std::max(1, c); }
 // whose concurrency already fills it.
 int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* dense) {
   if (dense) *dense = 0;
-  static const int forced = [] {
+  static const int env_forced = [] {
     const char* e = std::getenv("GS_BH_TASKS");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced > 0) return std::min(forced, kMaxBhTasks);
+  const int o = g_walk_tasks.load(std::memory_order_relaxed);
+  const int forced = o >= 0 ? o : env_forced;  // gs_set_bh_walk, else GS_BH_TASKS
   const int64_t warps = (nq + 31) / 32;
   const int64_t want = 148 * 64;  // ~2 waves of 32 resident warps per SM
   int K = (int)std::max<int64_t>(1, std::min<int64_t>(16, (want + warps - 1) / warps));
@@ -915,6 +958,7 @@ int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* den
       if (dense) *dense = 1;
     }
   }
+  if (forced > 0) K = forced;  // the regime (dense) is still detected
   return std::min(K, kMaxBhTasks);
 }
 

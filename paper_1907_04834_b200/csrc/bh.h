@@ -42,6 +42,7 @@ struct DevTree {
   DBuf tmp_k, tmp_v, tmp_v2, hist;
   DBuf scan_tmp;
   DBuf sm_ctr;          // i32 [1024] per-SM query-block counters of the walk (k_bh_ws)
+  DBuf pq_win;          // u32 [windows][queries][3] per-window per-query counters (folded)
   DBuf scal;
   KernelConsts kc{};
   double thr = 0.0;
@@ -79,20 +80,27 @@ struct BhQuery {
   // RHS / HESS: queries are the tree's own points restricted to point indices
   // [tgt_begin, tgt_begin + n_tgt); partials written per target (index - tgt_begin)
   int tgt_begin = 0, n_tgt = 0;
-  // VEL: m external eval records (x, -) ; partials per eval point
+  // VEL: m external eval records (x, -) ; partials per eval point.
+  // by_index RHS / HESS: n_tgt external query records (x, px) at ev and, for
+  // HESS, (alpha_i, beta_i) at eadj (a flow shard's own targets, or arbitrary
+  // queries of bh_point_gradients / bh_point_hessian_products)
   const void* ev = nullptr;
+  const void* eadj = nullptr;
   int m = 0;
   void* part = nullptr;
   uint32_t* per_query = nullptr;  // optional [nq][3] direct, approx, visited (query order)
   unsigned long long* totals = nullptr;  // optional [3] sums
   int ntask = 1;  // node windows (bh_tasks); part holds [ntask][queries] partials
   int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
-  int by_index = 0;  // RHS: queries = the n_tgt records at ev (a flow shard), not leaf order
+  int by_index = 0;  // RHS/HESS: queries = the n_tgt records at ev, not the tree's points
   int dense = 0;     // dense near fields (bh_tasks): the group walk is the default kernel
 };
 int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* dense = nullptr);
 // host threads driving flows on one GPU at once (batched subjects); per thread
 void set_bh_concurrency(int c);
+// process-wide walk override (gs_set_bh_walk): kernel 0 by regime / 1 independent /
+// 3 group / 4 split, tasks 0 auto / K windows; -1 restores the environment's choice
+void set_bh_walk(int kernel, int tasks);
 int bh_traverse(const Device& dev, int prec, DevTree& t, double sigma, double thr,
                 const BhQuery& q, cudaStream_t st);
 

@@ -123,6 +123,14 @@ static void detach_trees(gs_ctx* c);  // after struct gs_tree
 
 extern "C" {
 
+gs_status gs_set_bh_walk(int32_t kernel, int32_t windows) {
+  if (!(kernel == -1 || kernel == 0 || kernel == 1 || kernel == 3 || kernel == 4) || windows < -1 ||
+      windows > 64)
+    return GS_INVALID_ARGUMENT;
+  set_bh_walk(kernel, windows);
+  return GS_OK;
+}
+
 gs_status gs_set_literal_mean_dot(gs_ctx* c, int32_t enable) {
   if (!c) return GS_INVALID_ARGUMENT;
   c->lmd = enable ? 1 : 0;
@@ -1182,7 +1190,9 @@ struct gs_tree {
   DBuf rec;        // the build's records (index order)
   DBuf adj;        // last annotation (index order)
   DBuf part, outs, pq, stats;
+  DBuf qrec, qadj;  // external queries of gs_bh_point_* (records (x, px) / (alpha_i, beta_i))
   double c0[3] = {0, 0, 0};
+  double ext[3] = {0, 0, 0};  // host bounding-box extent: the walk's regime (bh_tasks)
   double sigma = -1.0;  // sigma the interaction coordinates are scaled for
   int64_t last_queries = 0;
 };
@@ -1199,8 +1209,17 @@ int tree_for_sigma(gs_tree* tr, double sigma) {
     GS_TRY(tree_rescale(tr->prec, tr->t, tr->rec.ptr, kc, tr->ctx->stream));
   }
   tr->sigma = sigma;
-  tr->t.kc = make_consts(sigma, tr->prec == kF32 ? tr->c0 : nullptr);
+  tr->t.kc = with_ext(make_consts(sigma, tr->prec == kF32 ? tr->c0 : nullptr), tr->ext);
   return GS_OK;
+}
+
+// Node windows and regime of a tree-level walk: the same choice a flow's
+// stage makes (bh_tasks), so these calls exercise the production walks.
+int tree_tasks(gs_tree* tr, int64_t nq, double thr, BhQuery& q) {
+  int dense = 0;
+  q.ntask = bh_tasks(nq, tr->t.n, thr, tr->t.kc, &dense);
+  q.dense = dense;
+  return q.ntask;
 }
 
 int fill_stats(gs_tree* tr, gs_stats* stats, int64_t queries) {
@@ -1218,15 +1237,17 @@ int fill_stats(gs_tree* tr, gs_stats* stats, int64_t queries) {
 
 // RHS traversal over all tree points -> dH/dp, dH/dq (device doubles) and optionally H
 int tree_rhs(gs_tree* tr, double sigma, double thr, double* dhdp_dev, double* dhdq_dev,
-             double* energy_part, int* blocks) {
+             double* energy_part, int* blocks, int* windows = nullptr) {
   gs_ctx* c = tr->ctx;
   const int64_t n = tr->t.n;
   GS_TRY(tree_for_sigma(tr, sigma));
-  GS_TRY(tr->part.ensure(2 * vec_bytes(tr->prec) * n));
+  BhQuery q;
+  const int K = tree_tasks(tr, n, thr, q);
+  if (windows) *windows = K;
+  GS_TRY(tr->part.ensure(2 * vec_bytes(tr->prec) * n * K));
   GS_TRY(tr->stats.ensure(64));
   GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * n));
   GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
-  BhQuery q;
   q.mode = kBhRhs;
   q.tgt_begin = 0;
   q.n_tgt = (int)n;
@@ -1238,7 +1259,7 @@ int tree_rhs(gs_tree* tr, double sigma, double thr, double* dhdp_dev, double* dh
   FwdEpi e;
   e.rec = tr->rec.ptr;
   e.update = 0;
-  e.S = 1;
+  e.S = K;
   e.part = tr->part.ptr;
   e.n_tgt = (int)n;
   e.cp = 2.0;
@@ -1262,7 +1283,7 @@ gs_status gs_tree_build(gs_ctx* c, int32_t precision, int64_t n, const double* q
   auto* tr = new gs_tree;
   tr->ctx = c;
   tr->prec = precision == GS_F32 ? kF32 : kF64;
-  bbox_center(q, n, tr->c0);
+  bbox_center(q, n, tr->c0, tr->ext);
   int s = upload_records(c, tr->prec, q, p, n, tr->rec);
   if (s == GS_OK) {
     const KernelConsts kc = make_consts(1.0, tr->prec == kF32 ? tr->c0 : nullptr);
@@ -1293,7 +1314,7 @@ gs_status gs_tree_build_in_cell(gs_ctx* c, int32_t precision, int64_t n, const d
   auto* tr = new gs_tree;
   tr->ctx = c;
   tr->prec = precision == GS_F32 ? kF32 : kF64;
-  bbox_center(q, n, tr->c0);
+  bbox_center(q, n, tr->c0, tr->ext);
   const double box[6] = {cell_min[0], cell_min[1], cell_min[2], cell_max[0], cell_max[1], cell_max[2]};
   int s = upload_records(c, tr->prec, q, p, n, tr->rec);
   if (s == GS_OK) {
@@ -1360,10 +1381,13 @@ gs_status gs_bh_hamiltonian(gs_tree* tr, double sigma, double thr, double* h_out
   const int64_t n = tr->t.n;
   GS_TRY(c->epart.ensure(sizeof(double) * (n / 128 + 8)));
   GS_TRY(c->scal.ensure(64));
-  int blocks = 0;
-  GS_TRY(tree_rhs(tr, sigma, thr, nullptr, nullptr, c->epart.as<double>(), &blocks));
-  if (c->lmd)  // the dot is scaled too (bh_kernel.cpp:184): the kernel's per-target sum of c
-    GS_TRY(sum_part_w(tr->prec, tr->part.ptr, (int)n, 2, 1, c->epart.as<double>(), &blocks, c->stream));
+  int blocks = 0, K = 1;
+  GS_TRY(c->epart.ensure(sizeof(double) * (n * 64 / 128 + 8)));
+  GS_TRY(tree_rhs(tr, sigma, thr, nullptr, nullptr, c->epart.as<double>(), &blocks, &K));
+  if (c->lmd)  // the dot is scaled too (bh_kernel.cpp:184): the per-target sums of c over all
+               // K node windows' partials ([K][n][2], B.w)
+    GS_TRY(sum_part_w(tr->prec, tr->part.ptr, (int)(n * K), 2, 1, c->epart.as<double>(), &blocks,
+                      c->stream));
   GS_TRY(reduce_sum(c->epart.as<double>(), blocks, c->scal.as<double>(), c->stream));
   double h = 0.0;
   GS_CUDA_OK(cudaMemcpyAsync(&h, c->scal.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1380,16 +1404,16 @@ gs_status gs_bh_velocity(gs_tree* tr, int64_t m, const double* x, double sigma, 
   GS_TRY(check_n(m));
   gs_ctx* c = tr->ctx;
   GS_TRY(tree_for_sigma(tr, sigma));
-  DBuf ev;
-  GS_TRY(upload_records(c, tr->prec, x, nullptr, m, ev));
-  GS_TRY(tr->part.ensure(vec_bytes(tr->prec) * m));
+  GS_TRY(upload_records(c, tr->prec, x, nullptr, m, tr->qrec));
+  BhQuery q;
+  const int K = tree_tasks(tr, m, thr, q);
+  GS_TRY(tr->part.ensure(vec_bytes(tr->prec) * m * K));
   GS_TRY(tr->stats.ensure(64));
   GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * m));
   GS_TRY(tr->outs.ensure(sizeof(double) * 3 * m));
   GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
-  BhQuery q;
   q.mode = kBhVel;
-  q.ev = ev.ptr;
+  q.ev = tr->qrec.ptr;
   q.m = (int)m;
   q.part = tr->part.ptr;
   q.per_query = tr->pq.as<uint32_t>();
@@ -1397,7 +1421,7 @@ gs_status gs_bh_velocity(gs_tree* tr, int64_t m, const double* x, double sigma, 
   GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
   VelEpi e;
   e.m = (int)m;
-  e.S = 1;
+  e.S = K;
   e.part = tr->part.ptr;
   e.scale = 1.0;
   e.v_out = tr->outs.as<double>();
@@ -1431,15 +1455,18 @@ gs_status gs_bh_hessian_products(gs_tree* tr, const double* alpha, const double*
   GS_TRY(upload_records(c, tr->prec, alpha, beta, n, adj));
   if (!tr->t.adj_valid) GS_TRY(tree_accumulate(tr->prec, tr->t, adj.ptr, c->stream));
   else GS_TRY(tree_set_point_adjoints(tr->prec, tr->t, adj.ptr, c->stream));
-  GS_TRY(tr->part.ensure(4 * vec_bytes(tr->prec) * n));
+  BhQuery q;
+  const int K = tree_tasks(tr, n, thr, q);
+  GS_TRY(tr->part.ensure(4 * vec_bytes(tr->prec) * n * K));
   GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * n));
   GS_TRY(tr->outs.ensure(sizeof(double) * 12 * n));
   GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
-  BhQuery q;
   q.mode = kBhHess;
   q.tgt_begin = 0;
   q.n_tgt = (int)n;
   q.part = tr->part.ptr;
+  q.per_query = tr->pq.as<uint32_t>();
   q.totals = tr->stats.as<unsigned long long>();
   q.lmd = c->lmd;
   GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
@@ -1447,7 +1474,7 @@ gs_status gs_bh_hessian_products(gs_tree* tr, const double* alpha, const double*
   const double cd = tr->prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;
   BwdEpi e;
   e.n_tgt = (int)n;
-  e.S = 1;
+  e.S = K;
   e.part = tr->part.ptr;
   e.update = 0;
   e.cpq = -cd;
@@ -1462,6 +1489,112 @@ gs_status gs_bh_hessian_products(gs_tree* tr, const double* alpha, const double*
   GS_TRY(sync(c));
   tr->last_queries = n;
   return (gs_status)fill_stats(tr, stats, n);
+}
+
+gs_status gs_bh_point_gradients(gs_tree* tr, int64_t m, const double* x, const double* px,
+                                double sigma, double thr, double* dHdp, double* dHdq,
+                                gs_stats* stats) {
+  if (!tr || !x || !px) return bad_arg("null argument");
+  GS_TRY(check_n(m));
+  gs_ctx* c = tr->ctx;
+  GS_TRY(tree_for_sigma(tr, sigma));
+  GS_TRY(upload_records(c, tr->prec, x, px, m, tr->qrec));
+  BhQuery q;
+  const int K = tree_tasks(tr, m, thr, q);
+  GS_TRY(tr->part.ensure(2 * vec_bytes(tr->prec) * m * K));
+  GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * m));
+  GS_TRY(tr->outs.ensure(sizeof(double) * 6 * m));
+  GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
+  q.mode = kBhRhs;
+  q.by_index = 1;  // external (x, px) records, not the tree's points
+  q.ev = tr->qrec.ptr;
+  q.tgt_begin = 0;
+  q.n_tgt = (int)m;
+  q.part = tr->part.ptr;
+  q.per_query = tr->pq.as<uint32_t>();
+  q.totals = tr->stats.as<unsigned long long>();
+  q.lmd = c->lmd;
+  GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
+  double* o = tr->outs.as<double>();
+  FwdEpi e;
+  e.rec = tr->qrec.ptr;
+  e.update = 0;
+  e.S = K;
+  e.part = tr->part.ptr;
+  e.n_tgt = (int)m;
+  e.cp = 2.0;
+  e.cq = fwd_cq(tr->prec, tr->t.kc);
+  e.dhdp_out = o;
+  e.dhdq_out = o + 3 * m;
+  GS_TRY(fwd_epilogue(tr->prec, e, c->stream, nullptr));
+  GS_TRY(d2h(c, dHdp, o, 3 * m));
+  GS_TRY(d2h(c, dHdq, o + 3 * m, 3 * m));
+  GS_TRY(sync(c));
+  tr->last_queries = m;
+  return (gs_status)fill_stats(tr, stats, m);
+}
+
+gs_status gs_bh_point_hessian_products(gs_tree* tr, int64_t m, const double* qi, const double* pi,
+                                       const double* alpha_i, const double* beta_i,
+                                       const double* alpha, const double* beta, double sigma,
+                                       double thr, double* pq, double* pp, double* qq, double* qp,
+                                       gs_stats* stats) {
+  if (!tr || !qi || !pi || !alpha_i || !beta_i) return bad_arg("null argument");
+  if (!alpha != !beta) return bad_arg("alpha and beta must both be given or both be NULL");
+  GS_TRY(check_n(m));
+  gs_ctx* c = tr->ctx;
+  const int64_t n = tr->t.n;
+  GS_TRY(tree_for_sigma(tr, sigma));
+  if (!tr->t.adj_valid) {  // never annotated: the reference's node sums are zero (Node defaults)
+    GS_TRY(tr->adj.ensure(2 * vec_bytes(tr->prec) * n));
+    GS_CUDA_OK(cudaMemsetAsync(tr->adj.ptr, 0, 2 * vec_bytes(tr->prec) * n, c->stream));
+    GS_TRY(tree_accumulate(tr->prec, tr->t, tr->adj.ptr, c->stream));
+  }
+  if (alpha) {  // direct terms read these per-point adjoints; node sums stay as annotated
+    DBuf adj;
+    GS_TRY(upload_records(c, tr->prec, alpha, beta, n, adj));
+    GS_TRY(tree_set_point_adjoints(tr->prec, tr->t, adj.ptr, c->stream));
+  }
+  GS_TRY(upload_records(c, tr->prec, qi, pi, m, tr->qrec));
+  GS_TRY(upload_records(c, tr->prec, alpha_i, beta_i, m, tr->qadj));
+  BhQuery q;
+  const int K = tree_tasks(tr, m, thr, q);
+  GS_TRY(tr->part.ensure(4 * vec_bytes(tr->prec) * m * K));
+  GS_TRY(tr->stats.ensure(64));
+  GS_TRY(tr->pq.ensure(sizeof(uint32_t) * 3 * m));
+  GS_TRY(tr->outs.ensure(sizeof(double) * 12 * m));
+  GS_CUDA_OK(cudaMemsetAsync(tr->stats.ptr, 0, 64, c->stream));
+  q.mode = kBhHess;
+  q.by_index = 1;
+  q.ev = tr->qrec.ptr;
+  q.eadj = tr->qadj.ptr;
+  q.tgt_begin = 0;
+  q.n_tgt = (int)m;
+  q.part = tr->part.ptr;
+  q.per_query = tr->pq.as<uint32_t>();
+  q.totals = tr->stats.as<unsigned long long>();
+  q.lmd = c->lmd;
+  GS_TRY(bh_traverse(c->dev, tr->prec, tr->t, sigma, thr, q, c->stream));
+  const KernelConsts& kc = tr->t.kc;
+  const double cd = tr->prec == kF32 ? kc.two_over_s / kc.kappa : kc.two_over_s;
+  BwdEpi e;
+  e.n_tgt = (int)m;
+  e.S = K;
+  e.part = tr->part.ptr;
+  e.update = 0;
+  e.cpq = -cd;
+  e.cpp = 2.0;
+  e.cqq = kc.two_over_s;
+  e.cqp = -cd;
+  double* o = tr->outs.as<double>();
+  for (int k = 0; k < 4; ++k) e.out[k] = o + (size_t)3 * m * k;
+  GS_TRY(bwd_epilogue(tr->prec, e, c->stream));
+  double* hs[4] = {pq, pp, qq, qp};
+  for (int k = 0; k < 4; ++k) GS_TRY(d2h(c, hs[k], o + (size_t)3 * m * k, 3 * m));
+  GS_TRY(sync(c));
+  tr->last_queries = m;
+  return (gs_status)fill_stats(tr, stats, m);
 }
 
 }  // extern "C"

@@ -560,14 +560,17 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
   for (;;) {
     const int par = parent[node];
     if (par < 0) return;
-    // release arrival: this child's sums are published before its count; the
-    // last child reads its siblings' sums with L2 loads (ld.cg, never through
-    // L1), so no acquire-side L1 invalidation (CCTL.IVALL) is needed
+    // release arrival: this child's sums are published before its count. The
+    // last arriver synchronises with every earlier (release) arrival through
+    // an acquire fence before it reads its siblings' sums -- the PTX memory
+    // model's release/acquire pattern, not a reliance on the control
+    // dependency; the sums are then read with L2 loads (ld.cg, never L1).
     cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
     const int old = publish ? arrive.fetch_add(1, cuda::memory_order_release)
                             : arrive.fetch_add(1, cuda::memory_order_relaxed);
     publish = true;
     if (old != nchild[par] - 1) return;
+    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
     const int end = meta[par].x;
     double4 A = make_double4(0, 0, 0, 0), B = A;
     V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
@@ -977,12 +980,33 @@ int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, 
   return tree_finalize_fwd(prec, t, kc, st);
 }
 
+namespace {
+// A single-point leaf's adjoint unit in nadj is the point's own (alpha, beta)
+// (k_finalize mode 1): refresh it with the per-point adjoints so that direct
+// terms read the new values while the aggregate nodes keep their annotation.
+template <typename R>
+__global__ void k_leaf_adj(const int4* meta, const int* mp, const V4<R>* sadj, V4<R>* nadj) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= *mp) return;
+  const int4 mi = meta[i];
+  if (!((mi.w & 1) && mi.z == mi.y)) return;
+  st4(nadj + 2 * i, ld4(sadj + 2 * mi.y));
+  st4(nadj + 2 * i + 1, ld4(sadj + 2 * mi.y + 1));
+}
+}  // namespace
+
 int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   const int64_t n = t.n;
   GS_TRY_INT(t.sadj.ensure(2 * vec_bytes(prec) * n));
-  const int nb = nblocks(n, kNT);
-  if (prec == kF32) k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
-  else k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
+  const int nb = nblocks(n, kNT), mb = nblocks(t.cap, kNT);
+  const int* mp = t.first.as<int>() + n;
+  if (prec == kF32) {
+    k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
+    if (t.adj_valid) k_leaf_adj<float><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), mp, t.sadj.as<float4>(), t.nadj.as<float4>());
+  } else {
+    k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
+    if (t.adj_valid) k_leaf_adj<double><<<mb, kNT, 0, st>>>(t.meta.as<int4>(), mp, t.sadj.as<double4>(), t.nadj.as<double4>());
+  }
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }

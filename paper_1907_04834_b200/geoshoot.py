@@ -273,6 +273,13 @@ class Geoshoot:
         return tuple(out)  # pq_alpha, pp_alpha, qq_beta, qp_beta
 
     # ---- octree -------------------------------------------------------------
+    def set_bh_walk(self, kernel: int = -1, windows: int = -1):
+        """Process-wide Barnes-Hut walk override (gs_set_bh_walk): kernel 0 by regime,
+        1 independent walks, 3 group walk, 4 split; windows 0 auto or K; -1 = default."""
+        st = self.lib.gs_set_bh_walk(int(kernel), int(windows))
+        if st:
+            raise ValueError(f"gs_set_bh_walk({kernel}, {windows}): invalid choice")
+
     def set_literal_mean_dot(self, enable: bool):
         """Tree-level BH calls on this context use the reference's
         GEOSHOOT_BH_LITERAL_MEAN_DOT aggregate dot scale 1/count (bh_kernel.cpp:19-26)."""
@@ -431,6 +438,7 @@ class Octree:
     def __init__(self, gs: Geoshoot, handle, q, p):
         self.gs, self.h, self.q, self.p = gs, handle, q, p
         self.n = len(q)
+        self._last_m = self.n  # queries of the last call (query_stats)
 
     def __del__(self):
         if getattr(self, "h", None) is not None and self.h.value:
@@ -477,6 +485,7 @@ class Octree:
         st = L.gs_stats()
         self.gs.check(self.gs.lib.gs_bh_velocity(self.h, len(x), _p(x), sigma, threshold, _p(v),
                                                  C.byref(st)))
+        self._last_m = len(x)
         return v, st.as_dict()
 
     def bh_hamiltonian_gradients(self, sigma, threshold):
@@ -484,6 +493,7 @@ class Octree:
         st = L.gs_stats()
         self.gs.check(self.gs.lib.gs_bh_rhs(self.h, sigma, threshold, _p(dp), _p(dq),
                                             C.byref(st)))
+        self._last_m = self.n
         return dp, dq, st.as_dict()
 
     def bh_hamiltonian(self, sigma, threshold):
@@ -491,10 +501,12 @@ class Octree:
         st = L.gs_stats()
         self.gs.check(self.gs.lib.gs_bh_hamiltonian(self.h, sigma, threshold, C.byref(h),
                                                     C.byref(st)))
+        self._last_m = self.n
         return h.value, st.as_dict()
 
     def query_stats(self, m=None) -> np.ndarray:
-        m = self.n if m is None else m
+        """Per-query (direct, approximated, visited) counts of the last query call."""
+        m = self._last_m if m is None else m
         out = np.empty((m, 3), np.uint64)
         self.gs.check(self.gs.lib.gs_bh_query_stats(self.h, out.ctypes.data_as(L._u64p)))
         return out
@@ -505,6 +517,35 @@ class Octree:
         st = L.gs_stats()
         self.gs.check(self.gs.lib.gs_bh_hessian_products(self.h, _p(a), _p(b), sigma, threshold,
                                                          *map(_p, out), C.byref(st)))
+        self._last_m = self.n
+        return tuple(out) + (st.as_dict(),)
+
+    def bh_point_gradients(self, x, px, sigma, threshold):
+        """bh_point_gradients (bh_kernel.cpp:81-112) at m arbitrary (x, px)."""
+        x, px = _arr(x, "x"), _arr(px, "px")
+        _require_aligned(len(x), len(px), "bh_point_gradients")
+        dp, dq = np.empty_like(x), np.empty_like(x)
+        st = L.gs_stats()
+        self.gs.check(self.gs.lib.gs_bh_point_gradients(self.h, len(x), _p(x), _p(px), sigma,
+                                                        threshold, _p(dp), _p(dq), C.byref(st)))
+        self._last_m = len(x)
+        return dp, dq, st.as_dict()
+
+    def bh_point_hessian_products(self, qi, pi, alpha_i, beta_i, alpha, beta, sigma, threshold):
+        """bh_point_hessian_products (bh_kernel.cpp:114-160) at m arbitrary queries;
+        alpha/beta (n x 3, or None) are the per-point adjoints of the direct terms."""
+        qi, pi, ai, bi = (_arr(v) for v in (qi, pi, alpha_i, beta_i))
+        m = len(qi)
+        for v, nm in ((pi, "pi"), (ai, "alpha_i"), (bi, "beta_i")):
+            _require_aligned(m, len(v), f"bh_point_hessian_products({nm})")
+        a = None if alpha is None else _arr(alpha)
+        b = None if beta is None else _arr(beta)
+        out = [np.empty_like(qi) for _ in range(4)]
+        st = L.gs_stats()
+        self.gs.check(self.gs.lib.gs_bh_point_hessian_products(
+            self.h, m, _p(qi), _p(pi), _p(ai), _p(bi), _p(a), _p(b), sigma, threshold,
+            *map(_p, out), C.byref(st)))
+        self._last_m = m
         return tuple(out) + (st.as_dict(),)
 
 

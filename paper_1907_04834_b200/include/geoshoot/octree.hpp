@@ -47,22 +47,31 @@ class Octree {
   static Octree build(const PointSet& q, const MomentumSet& p);
 
   /// Adds point `index` (must equal point_count()); throws OutOfBounds outside
-  /// the root cell. The device tree is rebuilt over the explicit root cell.
+  /// the root cell. Inserts are O(1): the device tree over the explicit root
+  /// cell is (re)built once, on the first use after a run of inserts, so an
+  /// insert loop costs one O(N) build in total (reference octree.cpp:74-117
+  /// inserts in O(depth) each; the resulting tree is the same).
   void insert(std::uint32_t index, const Vec3& position, const Vec3& momentum);
   void accumulate_adjoints(const std::vector<Vec3>& alpha, const std::vector<Vec3>& beta);
   static double min_distance(const Node& node, const Vec3& x);
 
   std::size_t point_count() const { return points_.size(); }
-  std::size_t node_count() const { return nodes_.size(); }
-  const Node& node(std::size_t i) const { return nodes_[i]; }
-  const Node& root() const { return nodes_.front(); }
+  std::size_t node_count() const { sync(); return nodes_.size(); }
+  const Node& node(std::size_t i) const { sync(); return nodes_[i]; }
+  const Node& root() const { sync(); return nodes_.front(); }
   const std::vector<Vec3>& points() const { return points_; }
   const std::vector<Vec3>& momenta() const { return momenta_; }
-  const std::vector<std::int32_t>& next_point() const { return next_point_; }
+  const std::vector<std::int32_t>& next_point() const { sync(); return next_point_; }
   static int octant_of(const Node& node, const Vec3& x);
 
   /// The device tree (built on first use); nullptr for an empty tree.
   gs_tree* device() const;
+  /// Per-point adjoint arrays whose values the device tree holds (the last
+  /// accumulate_adjoints, or the last bh_point_hessian_products upload): a
+  /// per-point query passing the same arrays re-uses the device copy.
+  const Vec3* device_alpha() const { return dev_alpha_; }
+  const Vec3* device_beta() const { return dev_beta_; }
+  void note_device_adjoints(const Vec3* a, const Vec3* b) const { dev_alpha_ = a; dev_beta_ = b; }
 
   Octree(Octree&&) noexcept;
   Octree& operator=(Octree&&) noexcept;
@@ -72,16 +81,22 @@ class Octree {
 
  private:
   Octree() = default;
-  void rebuild(bool explicit_root);
-  void mirror();
+  void rebuild(bool explicit_root) const;
+  void mirror() const;
+  void sync() const {
+    if (dirty_) rebuild(true);
+  }
 
-  std::vector<Node> nodes_;
+  mutable std::vector<Node> nodes_;
   std::vector<Vec3> points_;
   std::vector<Vec3> momenta_;
-  std::vector<std::int32_t> next_point_;
+  mutable std::vector<std::int32_t> next_point_;
   Vec3 root_min_, root_max_;
   bool explicit_root_ = false;
-  gs_tree* dev_ = nullptr;
+  mutable bool dirty_ = false;  // inserts since the last device build
+  mutable gs_tree* dev_ = nullptr;
+  mutable const Vec3* dev_alpha_ = nullptr;
+  mutable const Vec3* dev_beta_ = nullptr;
 };
 
 }  // namespace geoshoot
