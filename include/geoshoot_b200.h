@@ -118,6 +118,28 @@ typedef struct gs_ctx gs_ctx;
 
 /* ---- context --------------------------------------------------------------- */
 gs_ctx* gs_create(int device, gs_status* status);
+/* Multi-device context over devices[0..count) (1 <= count <= 16) in one
+ * process (replaces running the reference's parallel_for on one
+ * host): one sub-context (device, stream, workspaces) per target shard, peer
+ * access enabled between the distinct devices. gs_shoot_forward, gs_objective,
+ * gs_evaluate, gs_optimize and the gs_flow_* calls on it shard the target
+ * points into `count` contiguous ranges (Barnes-Hut: of the Morton-ordered
+ * points). Every device holds all records; each stage epilogue stores its
+ * shard's updated records into every peer's buffer (P2P stores over NVLink /
+ * NVSwitch -- the per-stage all-gather fused into the epilogue; explicit peer
+ * copies where P2P is unavailable), records ping-pong between stages and one
+ * event wait per peer orders them. The adjoint pass exchanges the (alpha,
+ * beta) shards the same way. Exact results are bit-identical to a
+ * one-device context (shards are planned as the full problem); Barnes-Hut
+ * results have the same interaction sets (summation order may differ).
+ * A device may be listed more than once: its shards then run on separate
+ * streams of that device (used to test the sharding on one GPU). The other
+ * entry points run on devices[0]. */
+gs_ctx* gs_create_multi(int32_t count, const int32_t* devices, gs_status* status);
+/* Devices (shards) of a context: 1 for gs_create. */
+int32_t gs_ctx_device_count(const gs_ctx* ctx);
+/* 1 if the multi-device exchange uses P2P stores from the epilogues. */
+int32_t gs_ctx_peer_stores(const gs_ctx* ctx);
 /* Flows and trees made on the context are detached, not freed: afterwards
    they may only be released (gs_flow_destroy / gs_tree_free). */
 void gs_destroy(gs_ctx* ctx);

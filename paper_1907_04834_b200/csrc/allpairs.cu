@@ -912,14 +912,27 @@ Plan plan(int n_src, int n_tgt, int nt, const int* tpts, int ntpt, int tile, int
   }
   const long B = (n_tgt + (long)nt * tpt - 1) / ((long)nt * tpt);
   const int smax = (int)std::max(1L, std::min((long)kMaxChunks, ((long)n_src + tile - 1) / tile));
+  // S is chosen for the whole problem AND its 2/4/8-way target shards (those
+  // that can fill a wave at all): score = worst wave efficiency over them +
+  // half the unsharded one. Multi-device shards launch under this same plan
+  // (rhs_partials plan_tgt), so one S -- hence bit-identical per-target sums --
+  // serves every device count while each shard's grid still fills its GPU
+  // (N = 1M, TPT 12: S = 14, 99.5 % of the last wave used unsharded, >= 96 %
+  // for 2-8 shards).
   int bestS = 1;
   double best = -1.0;
   for (int s = 1; s <= smax; ++s) {
-    const double w = (double)(B * s) / slots;
-    const double eff = w / std::ceil(w);
+    double worst = 2.0;
+    for (int g = 1; g <= 8; g *= 2) {
+      const long Bg = (B + g - 1) / g;
+      if (g > 1 && Bg * smax < slots) continue;  // this shard cannot fill a wave anyway
+      const double w = (double)(Bg * s) / slots;
+      worst = std::min(worst, w / std::ceil(w));
+    }
+    const double w1 = (double)(B * s) / slots;
+    const double score = worst + 0.5 * (w1 / std::ceil(w1));
     // prefer fewer chunks unless clearly better balanced
-    if (eff > best + 0.01) { best = eff; bestS = s; }
-    if (w > 8.0 && eff > 0.97) break;
+    if (score > best + 0.01) { best = score; bestS = s; }
   }
   pl.tpt = tpt;
   pl.S = bestS;
@@ -1039,8 +1052,20 @@ int rhs_sorted_partials(const Device& dev, const void* srec, const int* perm, in
   return pl.S;
 }
 
+// Grid of n_tgt targets under a plan made for plan_tgt targets: the kernel
+// variant, targets per thread, source chunk count S and chunk length are those
+// of the plan_tgt problem (so every target's partial sums are bit-identical to
+// that problem's), only the target blocks are resized.
+static Plan fit(Plan pl, int n_tgt) {
+  pl.grid.x = (unsigned)std::max(1L, ((long)n_tgt + (long)kNT * pl.tpt - 1) / ((long)kNT * pl.tpt));
+  return pl;
+}
+
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
-                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st,
+                 int plan_tgt) {
+  const int real_tgt = n_tgt;
+  if (plan_tgt > 0) n_tgt = plan_tgt;  // plan as if for plan_tgt targets (multi-device shards)
   if (prec == kF32) {
     const int vi = rhs_variant();
     const RhsVariant v = kRhsVariants[vi];
@@ -1063,10 +1088,11 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
         occ_rhs_f32x2<12, 2, 4>(), occ_rhs_f32x2<12, 2, 8>(), occ_rhs_f32x2<16, 2, 4>(),
         occ_rhs_f32x2<16, 1, 4>(), occ_rhs_f32x2<2, 8, 8>()};
     const int tp[] = {u.tpt};
-    Plan pl = plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms);
+    Plan pl = fit(plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms), real_tgt);
     if (pl.S > part_cap_chunks) return -1;
     const float4* r = (const float4*)rec;
     float4* o = (float4*)part;
+    n_tgt = real_tgt;
     switch (use) {
       case 0: launch_rhs_f32<8, 3, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
       case 1: launch_rhs_f32<8, 3, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
@@ -1092,8 +1118,9 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
   }
   static const int tpts[] = {4, 2, 1};
   static int occ = occupancy(k_rhs_f64<4, kNT>, kNT);
-  Plan pl = plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms);
+  Plan pl = fit(plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms), real_tgt);
   if (pl.S > part_cap_chunks) return -1;
+  n_tgt = real_tgt;
   switch (pl.tpt) {
     case 4: k_rhs_f64<4, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
     case 2: k_rhs_f64<2, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
@@ -1104,12 +1131,15 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
 
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
                   int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
-                  int part_cap_chunks, cudaStream_t st) {
+                  int part_cap_chunks, cudaStream_t st, int plan_tgt) {
+  const int real_tgt = n_tgt;
+  if (plan_tgt > 0) n_tgt = plan_tgt;
   if (prec == kF32) {
     static const int tpts[] = {4, 2, 1};
     static int occ = occupancy(k_hess_f32x2<4, kNT>, kNT);
-    Plan pl = plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms);
+    Plan pl = fit(plan(n, n_tgt, kNT, tpts, 3, kTile / 2, occ, dev.sms), real_tgt);
     if (pl.S > part_cap_chunks) return -1;
+    n_tgt = real_tgt;
     static const bool packed = [] {
       const char* e = std::getenv("GS_HESS_PACKED");
       return e ? std::atoi(e) != 0 : true;
@@ -1138,8 +1168,9 @@ int hess_partials(const Device& dev, int prec, const void* rec, const void* adj,
   }
   static const int tpts[] = {2, 1};
   static int occ = occupancy(k_hess_f64<2, kNT>, kNT);
-  Plan pl = plan(n, n_tgt, kNT, tpts, 2, kTile / 4, occ, dev.sms);
+  Plan pl = fit(plan(n, n_tgt, kNT, tpts, 2, kTile / 4, occ, dev.sms), real_tgt);
   if (pl.S > part_cap_chunks) return -1;
+  n_tgt = real_tgt;
   switch (pl.tpt) {
     case 2: k_hess_f64<2, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, (const double4*)adj, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, kc.inv_s, (double4*)part); break;
     default: k_hess_f64<1, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, (const double4*)adj, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, kc.inv_s, (double4*)part); break;

@@ -26,7 +26,9 @@ namespace {
 const double* raw(const std::vector<Vec3>& v) { return reinterpret_cast<const double*>(v.data()); }
 double* raw(std::vector<Vec3>& v) { return reinterpret_cast<double*>(v.data()); }
 
-// one device context per host thread (device from GEOSHOOT_DEVICE, default 0)
+// one device context per host thread: device GEOSHOOT_DEVICE (default 0), or
+// -- GEOSHOOT_DEVICES="0,1,2,3" -- a multi-device context whose shooting calls
+// (shoot_forward, objective, evaluate, optimize) shard the targets across them
 struct Ctx {
   gs_ctx* c = nullptr;
   ~Ctx() {
@@ -37,9 +39,21 @@ struct Ctx {
 gs_ctx* ctx() {
   thread_local Ctx holder;
   if (!holder.c) {
-    const char* env = std::getenv("GEOSHOOT_DEVICE");
     gs_status st = GS_OK;
-    holder.c = gs_create(env ? std::atoi(env) : 0, &st);
+    if (const char* list = std::getenv("GEOSHOOT_DEVICES")) {
+      std::vector<int32_t> devs;
+      for (const char* p = list; *p;) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) break;
+        devs.push_back((int32_t)v);
+        p = *end == ',' ? end + 1 : end;
+      }
+      holder.c = gs_create_multi((int32_t)devs.size(), devs.data(), &st);
+    } else {
+      const char* env = std::getenv("GEOSHOOT_DEVICE");
+      holder.c = gs_create(env ? std::atoi(env) : 0, &st);
+    }
     if (!holder.c) throw DeviceError(std::string("geoshoot: no B200 device: ") + gs_last_error(nullptr));
   }
   return holder.c;

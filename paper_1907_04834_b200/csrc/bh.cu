@@ -1013,8 +1013,8 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
 }
 
 int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
-                     const void* rec_k, void* adj, int64_t n, int k, BhWork& w, bool cached,
-                     BwdEpi e, cudaStream_t st, gs_stats*) {
+                     const void* rec_k, void* adj, int64_t n, int64_t tb, int64_t nt, int k,
+                     BhWork& w, bool cached, BwdEpi e, cudaStream_t st, gs_stats*) {
   DevTree* t = nullptr;
   if (cached && k < (int)w.kept.size()) {
     t = w.kept[k].get();
@@ -1024,16 +1024,21 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
   }
   GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
   int dense = 0;
-  const int K = bh_tasks(n, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
-  GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * K * n));
+  const int K = bh_tasks(nt, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
+  GS_TRY_INT(w.part.ensure(4 * vec_bytes(prec) * K * std::max<int64_t>(nt, 1)));
   GS_TRY_INT(w.stats.ensure(64));
   BhQuery q;
   q.mode = kBhHess;
   q.ntask = K;
   q.dense = dense;
   q.lmd = cfg.literal_mean_dot;
-  q.tgt_begin = 0;
-  q.n_tgt = (int)n;
+  if (tb != 0 || nt != n) {  // a shard: its own targets by point index (records + adjoints)
+    q.by_index = 1;
+    q.ev = static_cast<const char*>(rec_k) + 2 * vec_bytes(prec) * tb;
+    q.eadj = static_cast<const char*>(adj) + 2 * vec_bytes(prec) * tb;
+  }
+  q.tgt_begin = (int)tb;
+  q.n_tgt = (int)nt;
   q.part = w.part.ptr;
   q.totals = w.stats.as<unsigned long long>();
   GS_TRY_INT(bh_traverse(dev, prec, *t, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));

@@ -118,9 +118,10 @@ int bh_keep_trees(BhWork& w, int T);
 int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
                      const void* rec, int64_t n, int64_t tb, int64_t nt, BhWork& w, FwdEpi e,
                      cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats* stats);
+// adj: the full (alpha, beta) records (node sums); targets [tb, tb + nt)
 int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
-                     const void* rec_k, void* adj, int64_t n, int k, BhWork& w, bool cached,
-                     BwdEpi e, cudaStream_t st, gs_stats* stats);
+                     const void* rec_k, void* adj, int64_t n, int64_t tb, int64_t nt, int k,
+                     BhWork& w, bool cached, BwdEpi e, cudaStream_t st, gs_stats* stats);
 int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
                      const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
                      cudaStream_t st);

@@ -78,6 +78,11 @@ struct gs_ctx {
   // frees their device memory instead of touching a dead context
   std::unordered_set<gs_flow*> flows;
   std::unordered_set<gs_tree*> trees;
+  // multi-device context (gs_create_multi): one sub-context (device, stream,
+  // workspaces) per target shard; shooting calls shard across them
+  std::vector<gs_ctx*> subs;
+  bool peer_stores = true;  // epilogues store into peers' buffers (else peer copies)
+  std::vector<cudaEvent_t> ev;  // per-shard stage-completion events
 };
 
 struct gs_flow {
@@ -100,6 +105,12 @@ struct gs_flow {
   BhWork bh;
   gs_stats stats{};
   KTimer* timer = nullptr;  // gs_flow_profile
+  // multi-device flow: one sub-flow per shard (on the sub-contexts); the
+  // records ping-pong between rec and rec_next, each stage epilogue storing
+  // its shard into every sub-flow's rec_next (PeerOut)
+  std::vector<gs_flow*> subs;
+  PeerOut peers;     // set by the multi-device driver for the next stage
+  int plan_tgt = -1; // exact RHS planned for this many targets (bitwise shards)
   // CUDA graph of one integrator step (all stages + the step-counter bump),
   // captured after the first eager step and replayed for the following ones
   DBuf stepctr;
@@ -113,11 +124,17 @@ struct gs_flow {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
   }
-  ~gs_flow() {
-    drop_graph();
-    delete timer;
-  }
+  ~gs_flow();
 };
+
+gs_flow::~gs_flow() {
+  drop_graph();
+  delete timer;
+  for (gs_flow* s : subs) {
+    if (s->ctx) cudaSetDevice(s->ctx->dev.id);
+    delete s;
+  }
+}
 
 static void detach_trees(gs_ctx* c);  // after struct gs_tree
 
@@ -185,10 +202,18 @@ gs_ctx* gs_create(int device, gs_status* status) {
 
 void gs_destroy(gs_ctx* ctx) {
   if (!ctx) return;
+  cudaSetDevice(ctx->dev.id);
   cudaStreamSynchronize(ctx->stream);
   for (gs_flow* f : ctx->flows) f->ctx = nullptr;
   detach_trees(ctx);
   if (ctx->scratch) gs_flow_destroy(ctx->scratch);
+  for (gs_ctx* s : ctx->subs) {  // multi-device: the shards' contexts
+    cudaSetDevice(s->dev.id);
+    cudaStreamSynchronize(s->stream);
+  }
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  for (gs_ctx* s : ctx->subs) gs_destroy(s);
+  cudaSetDevice(ctx->dev.id);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -319,10 +344,11 @@ int exact_sorted_stage(const Device& dev, const KernelConsts& kc, const void* re
 // one exact RHS over all n sources for targets [tb, tb + nt) + its epilogue
 int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
                 int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
-                int* energy_blocks) {
+                int* energy_blocks, int plan_tgt = -1) {
   GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
   kt_mark(0, st);
-  const int S = rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr, kMaxChunks, st);
+  const int S = rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr, kMaxChunks, st,
+                             plan_tgt);
   kt_mark(0, st);
   if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
   GS_CUDA_OK(cudaGetLastError());
@@ -372,6 +398,7 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
   e.bad_step = f->flags.as<int>();
   e.step = f->steps_done + 1;
   e.step_dev = f->stepctr.as<int>();
+  e.peers = f->peers;
   const bool first = f->want_energy && f->steps_done == 0 && stage == 0;
   if (first) {
     GS_TRY(f->epart.ensure(sizeof(double) * (f->shard_count / 128 + 8)));
@@ -396,7 +423,7 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
     f->stats.traversal_queries += (uint64_t)f->shard_count;
   } else if (f->cfg.backend == GS_EXACT) {
     GS_TRY(exact_stage(c->dev, f->prec, f->kc, rec_in, f->n, f->shard_begin, f->shard_count,
-                       f->part, e, st, &f->launches, &blocks));
+                       f->part, e, st, &f->launches, &blocks, f->plan_tgt));
     f->stats.direct_interactions += (uint64_t)f->n * (uint64_t)f->shard_count;
     f->stats.traversal_queries += (uint64_t)f->shard_count;
   } else {
@@ -417,6 +444,7 @@ int flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
   f->n = n;
   f->shard_begin = 0;
   f->shard_count = n;
+  f->plan_tgt = -1;
   f->steps_done = 0;
   f->launches = 0;
   f->want_energy = false;
@@ -591,6 +619,36 @@ gs_flow* scratch_flow(gs_ctx* c) {
   return c->scratch;
 }
 
+// Barnes-Hut walks are only coherent for spatially compact query sets: a
+// sharded flow reorders its records by Morton key once (every shard computes
+// the same order from the same uploaded records) and remembers the order for
+// download.
+int flow_morton_permute(gs_flow* f) {
+  gs_ctx* c = f->ctx;
+  GS_TRY(morton_order(c->dev, f->prec, f->kc, f->rec.ptr, f->n, f->bh.cur, c->stream));
+  GS_TRY(f->order.ensure(sizeof(int) * f->n));
+  GS_CUDA_OK(cudaMemcpyAsync(f->order.ptr, f->bh.cur.perm.ptr, sizeof(int) * f->n,
+                             cudaMemcpyDeviceToDevice, c->stream));
+  GS_TRY(f->rec_next.ensure(2 * vec_bytes(f->prec) * f->n));
+  GS_TRY(permute_records(f->prec, f->rec.ptr, f->order.as<int>(), f->n, f->rec_next.ptr, c->stream));
+  std::swap(f->rec.ptr, f->rec_next.ptr);
+  std::swap(f->rec.bytes, f->rec_next.bytes);
+  f->permuted = true;
+  return GS_OK;
+}
+
+// multi-device contexts (definitions at the end of this file)
+bool is_multi(const gs_ctx* c) { return c && !c->subs.empty(); }
+int multi_flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n);
+int multi_flow_upload(gs_flow* f, const double* q0, const double* p0);
+int multi_flow_advance(gs_flow* f, int steps);
+int multi_flow_check(gs_flow* f);
+int multi_flow_download(gs_flow* f, double* q, double* p);
+int multi_flow_stats(gs_flow* f, gs_stats* out);
+int multi_flow_energy(gs_flow* f, double* out);
+int multi_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0, const double* p0,
+                   const double* target, gs_report* report, double* grad_out, gs_stats* stats);
+
 struct Timer {
   cudaEvent_t a{}, b{};
   cudaStream_t s;
@@ -621,7 +679,7 @@ gs_status gs_flow_create(gs_ctx* ctx, const gs_config* cfg, int64_t n, gs_flow**
   GS_TRY(gs_validate_config(cfg, nullptr));
   GS_TRY(check_n(n));
   auto* f = new gs_flow;
-  const int s = flow_init(f, ctx, cfg, n);
+  const int s = is_multi(ctx) ? multi_flow_init(f, ctx, cfg, n) : flow_init(f, ctx, cfg, n);
   if (s != GS_OK) {
     delete f;
     return (gs_status)s;
@@ -642,21 +700,25 @@ void gs_flow_destroy(gs_flow* flow) {
 
 gs_status gs_flow_upload(gs_flow* f, const double* q0, const double* p0) {
   if (!f || !q0 || !p0) return bad_arg("null argument");
+  if (!f->subs.empty()) return (gs_status)multi_flow_upload(f, q0, p0);
   return (gs_status)flow_upload(f, q0, p0);
 }
 
 gs_status gs_flow_advance(gs_flow* f, int32_t steps) {
   if (!f) return bad_arg("null flow");
+  if (!f->subs.empty()) return (gs_status)multi_flow_advance(f, steps);
   return (gs_status)flow_advance(f, steps);
 }
 
 gs_status gs_flow_sync(gs_flow* f) {
   if (!f) return bad_arg("null flow");
+  if (!f->subs.empty()) return (gs_status)multi_flow_check(f);
   return (gs_status)flow_check(f);
 }
 
 gs_status gs_flow_download(gs_flow* f, double* q, double* p) {
   if (!f) return bad_arg("null flow");
+  if (!f->subs.empty()) return (gs_status)multi_flow_download(f, q, p);
   gs_ctx* c = f->ctx;
   GS_TRY(c->stage_a.ensure(sizeof(double) * 3 * f->n));
   GS_TRY(c->stage_b.ensure(sizeof(double) * 3 * f->n));
@@ -682,6 +744,7 @@ void* gs_flow_stream(const gs_flow* f) { return f ? (void*)f->ctx->stream : null
 
 gs_status gs_flow_profile(gs_flow* f, int32_t enable) {
   if (!f) return bad_arg("null flow");
+  if (!f->subs.empty()) return bad_arg("profiling is per device: not on a multi-device flow");
   if (enable && !f->timer) f->timer = new KTimer;
   if (!enable) {
     delete f->timer;
@@ -710,6 +773,7 @@ gs_status gs_flow_profile_phases(gs_flow* f, double* ms, int64_t* counts, int32_
 
 gs_status gs_flow_stats(gs_flow* f, gs_stats* out) {
   if (!f || !out) return bad_arg("null argument");
+  if (!f->subs.empty()) return (gs_status)multi_flow_stats(f, out);
   *out = f->stats;
   GS_TRY(flow_bh_stats(f, out));
   return GS_OK;
@@ -717,23 +781,12 @@ gs_status gs_flow_stats(gs_flow* f, gs_stats* out) {
 
 gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
   if (!f || begin < 0 || count < 0 || begin + count > f->n) return bad_arg("bad shard range");
+  if (!f->subs.empty()) return bad_arg("a multi-device flow shards itself");
   f->shard_begin = begin;
   f->shard_count = count;
-  if (f->cfg.backend == GS_BARNES_HUT && count < f->n && !f->permuted && f->steps_done == 0) {
-    // Barnes-Hut walks are only coherent for spatially compact query sets:
-    // reorder the records by Morton key (every rank computes the same order
-    // from the same uploaded records), remember the order for download
-    gs_ctx* c = f->ctx;
-    GS_TRY(morton_order(c->dev, f->prec, f->kc, f->rec.ptr, f->n, f->bh.cur, c->stream));
-    GS_TRY(f->order.ensure(sizeof(int) * f->n));
-    GS_CUDA_OK(cudaMemcpyAsync(f->order.ptr, f->bh.cur.perm.ptr, sizeof(int) * f->n,
-                               cudaMemcpyDeviceToDevice, c->stream));
-    GS_TRY(f->rec_next.ensure(2 * vec_bytes(f->prec) * f->n));
-    GS_TRY(permute_records(f->prec, f->rec.ptr, f->order.as<int>(), f->n, f->rec_next.ptr, c->stream));
-    std::swap(f->rec.ptr, f->rec_next.ptr);
-    std::swap(f->rec.bytes, f->rec_next.bytes);
-    f->permuted = true;
-  }
+  f->plan_tgt = (int)f->n;  // shards run the full problem's plan: bit-identical sums
+  if (f->cfg.backend == GS_BARNES_HUT && count < f->n && !f->permuted && f->steps_done == 0)
+    GS_TRY(flow_morton_permute(f));
   return GS_OK;
 }
 
@@ -742,6 +795,7 @@ int64_t gs_flow_record_bytes(const gs_flow* f) { return f ? 2 * (int64_t)vec_byt
 
 gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
   if (!f || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");
+  if (!f->subs.empty()) return bad_arg("a multi-device flow advances with gs_flow_advance");
   f->launches = 0;
   GS_TRY(flow_stage(f, stage, nullptr, nullptr));
   if (stage == flow_stages(f) - 1) {
@@ -869,6 +923,39 @@ gs_status gs_shoot_forward(gs_ctx* c, const gs_config* cfg, int64_t n, const dou
   GS_TRY(gs_validate_config(cfg, nullptr));
   GS_TRY(check_n(n));
   gs_flow* f = scratch_flow(c);
+  if (is_multi(c)) {  // target shards across the context's devices
+    GS_TRY(multi_flow_init(f, c, cfg, n));
+    for (gs_flow* s : f->subs) s->want_energy = energy_out != nullptr;
+    GS_TRY(multi_flow_upload(f, q0, p0));
+    const int T = cfg->timesteps;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int k = 0; k <= T; ++k) {
+      if (traj_q || traj_p) {
+        std::vector<double> tq((size_t)3 * n), tp((size_t)3 * n);
+        GS_TRY(multi_flow_download(f, tq.data(), tp.data()));
+        if (traj_q) std::memcpy(traj_q + (size_t)3 * n * k, tq.data(), sizeof(double) * 3 * n);
+        if (traj_p) std::memcpy(traj_p + (size_t)3 * n * k, tp.data(), sizeof(double) * 3 * n);
+        if (k < T) GS_TRY(multi_flow_advance(f, 1));
+      } else if (k == 0) {
+        GS_TRY(multi_flow_advance(f, T));
+      }
+    }
+    GS_TRY(multi_flow_check(f));
+    const double fwd_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (final_q || final_p) {
+      std::vector<double> fq((size_t)3 * n), fp((size_t)3 * n);
+      GS_TRY(multi_flow_download(f, fq.data(), fp.data()));
+      if (final_q) std::memcpy(final_q, fq.data(), sizeof(double) * 3 * n);
+      if (final_p) std::memcpy(final_p, fp.data(), sizeof(double) * 3 * n);
+    }
+    if (energy_out) GS_TRY(multi_flow_energy(f, energy_out));
+    if (stats) {
+      GS_TRY(multi_flow_stats(f, stats));
+      stats->forward_ms = fwd_ms;
+    }
+    return GS_OK;
+  }
   GS_TRY(flow_init(f, c, cfg, n));
   GS_TRY(flow_upload(f, q0, p0));
   f->want_energy = energy_out != nullptr;
@@ -916,6 +1003,36 @@ gs_status gs_shoot_forward(gs_ctx* c, const gs_config* cfg, int64_t n, const dou
 
 namespace {
 
+// One adjoint step k (shooting.cpp:177-214) for targets [tb, tb + nt): the
+// Hessian products of state rk against the full adjoints adj_in, then
+// alpha += dt (pq - qq), beta += dt (pp - qp) into e.adj_out (in place if
+// null; plus e.peers on a multi-device context).
+int backward_step(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts& kc, int64_t n,
+                  int64_t tb, int64_t nt, const void* rk, void* adj_in, int k, BhWork* bh,
+                  bool trees_cached, DBuf& part, BwdEpi e, gs_stats* stats, int plan_tgt = -1) {
+  cudaStream_t st = c->stream;
+  e.n_tgt = (int)nt;
+  e.tgt_begin = (int)tb;
+  e.adj = adj_in;
+  if (cfg->backend == GS_EXACT) {
+    GS_TRY(part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+    const int S = hess_partials(c->dev, prec, rk, adj_in, (int)n, (int)tb, (int)nt, kc, part.ptr,
+                                kMaxChunks, st, plan_tgt);
+    if (S < 0) return GS_INTERNAL;
+    GS_CUDA_OK(cudaGetLastError());
+    e.S = S;
+    e.part = part.ptr;
+    GS_TRY(bwd_epilogue(prec, e, st));
+    if (stats) {
+      stats->direct_interactions += (uint64_t)n * nt;
+      stats->traversal_queries += nt;
+    }
+    return GS_OK;
+  }
+  return bh_backward_step(c->dev, prec, kc, *cfg, rk, adj_in, n, tb, nt, k, *bh, trees_cached, e,
+                          st, stats);
+}
+
 // Adjoint recursion over device-resident trajectory records traj[0..T]
 // (run_backward, shooting.cpp:143-240). dhdp0 must hold dH/dp(q0, p0).
 int backward_pass(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts& kc, int64_t n,
@@ -941,26 +1058,9 @@ int backward_pass(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts&
   e.cpp = 2.0;
   e.cqq = kc.two_over_s;
   e.cqp = -cd;
-  for (int k = T - 1; k >= 0; --k) {
-    const void* rk = traj + (size_t)k * rec_bytes;
-    if (cfg->backend == GS_EXACT) {
-      GS_TRY(part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * n));
-      const int S = hess_partials(c->dev, prec, rk, adj.ptr, (int)n, 0, (int)n, kc, part.ptr,
-                                  kMaxChunks, st);
-      if (S < 0) return GS_INTERNAL;
-      GS_CUDA_OK(cudaGetLastError());
-      e.S = S;
-      e.part = part.ptr;
-      GS_TRY(bwd_epilogue(prec, e, st));
-      if (stats) {
-        stats->direct_interactions += (uint64_t)n * n;
-        stats->traversal_queries += n;
-      }
-    } else {
-      GS_TRY(bh_backward_step(c->dev, prec, kc, *cfg, rk, adj.ptr, n, k, *bh, trees_cached, e, st,
-                              stats));
-    }
-  }
+  for (int k = T - 1; k >= 0; --k)
+    GS_TRY(backward_step(c, cfg, prec, kc, n, 0, n, traj + (size_t)k * rec_bytes, adj.ptr, k, bh,
+                         trees_cached, part, e, stats));
   GS_TRY(gradient_finalize(prec, adj.ptr, dhdp0, n, grad_dev, st));
   return GS_OK;
 }
@@ -976,6 +1076,7 @@ gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* 
   if (cfg->integrator != GS_EULER) return bad_arg("evaluate: the adjoint is the transpose of Euler");
   GS_TRY(gs_validate_config(cfg, nullptr));
   GS_TRY(check_n(n));
+  if (is_multi(c)) return (gs_status)multi_evaluate(c, cfg, n, q0, p0, target, report, grad_out, stats);
   const int T = cfg->timesteps;
   gs_flow* f = scratch_flow(c);
   GS_TRY(flow_init(f, c, cfg, n));
@@ -1596,5 +1697,399 @@ gs_status gs_bh_point_hessian_products(gs_tree* tr, int64_t m, const double* qi,
   tr->last_queries = m;
   return (gs_status)fill_stats(tr, stats, m);
 }
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------
+// Multi-device contexts: one process drives G devices. Target
+// points are cut into G contiguous shards (Barnes-Hut: of the Morton-ordered
+// records, so a shard is a compact region). Every device holds all n records
+// and computes its shard's RHS against all of them; the stage epilogue stores
+// the shard's updated records into its own next buffer AND into every peer's
+// (P2P stores over NVLink / NVSwitch: the all-gather is fused into the
+// epilogue). Buffers ping-pong per stage, so a peer never overwrites records
+// a device is still reading; one event wait per peer and stage orders them.
+// The adjoint pass does the same with the (alpha, beta) records. Exact RHS
+// shards are planned as the full problem (rhs_partials plan_tgt), so their
+// partial sums -- and the flow -- are bit-identical to one device's.
+// ----------------------------------------------------------------------------
+namespace {
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void shard_of(int64_t n, int G, int d, int64_t* b, int64_t* cnt) {
+  const int64_t base = n / G, extra = n % G;
+  *b = d * base + std::min<int64_t>(d, extra);
+  *cnt = base + (d < extra ? 1 : 0);
+}
+
+int sub_dev(const gs_flow* s) { return s->ctx->dev.id; }
+
+// every shard's stream waits for every other shard's last recorded event
+int multi_wait_all(gs_ctx* c) {
+  const int G = (int)c->subs.size();
+  for (int d = 0; d < G; ++d) {
+    DevGuard g(c->subs[d]->dev.id);
+    for (int o = 0; o < G; ++o)
+      if (o != d) GS_CUDA_OK(cudaStreamWaitEvent(c->subs[d]->stream, c->ev[o], 0));
+  }
+  return GS_OK;
+}
+
+int multi_record(gs_ctx* c, int d) {
+  GS_CUDA_OK(cudaEventRecord(c->ev[d], c->subs[d]->stream));
+  return GS_OK;
+}
+
+// The peers' copies of a shard written by shard d: P2P stores from the
+// epilogue (peer_stores), else explicit peer copies after it.
+PeerOut peer_bufs(gs_ctx* c, const std::vector<void*>& bufs, int d) {
+  PeerOut po;
+  if (!c->peer_stores) return po;
+  for (int o = 0; o < (int)bufs.size(); ++o)
+    if (o != d) po.buf[po.n++] = bufs[o];
+  return po;
+}
+
+int peer_copies(gs_ctx* c, const std::vector<void*>& bufs, int d, size_t off, size_t bytes) {
+  if (c->peer_stores || bytes == 0) return GS_OK;
+  for (int o = 0; o < (int)bufs.size(); ++o)
+    if (o != d)
+      GS_CUDA_OK(cudaMemcpyPeerAsync(static_cast<char*>(bufs[o]) + off, c->subs[o]->dev.id,
+                                     static_cast<char*>(bufs[d]) + off, c->subs[d]->dev.id, bytes,
+                                     c->subs[d]->stream));
+  return GS_OK;
+}
+
+int multi_flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
+  const int G = (int)c->subs.size();
+  f->ctx = c;
+  f->cfg = *cfg;
+  f->prec = cfg->precision == GS_F32 ? kF32 : kF64;
+  f->n = n;
+  f->shard_begin = 0;
+  f->shard_count = n;
+  f->steps_done = 0;
+  while ((int)f->subs.size() < G) f->subs.push_back(new gs_flow);
+  for (int d = 0; d < G; ++d) {
+    DevGuard g(c->subs[d]->dev.id);
+    gs_flow* s = f->subs[d];
+    GS_TRY(flow_init(s, c->subs[d], cfg, n));
+    shard_of(n, G, d, &s->shard_begin, &s->shard_count);
+    s->plan_tgt = (int)n;  // bit-identical partial sums to the unsharded RHS
+    GS_TRY(s->rec_next.ensure(2 * vec_bytes(s->prec) * n));
+  }
+  return GS_OK;
+}
+
+int multi_flow_upload(gs_flow* f, const double* q0, const double* p0) {
+  gs_ctx* c = f->ctx;
+  GS_TRY(multi_wait_all(c));  // nothing may still write into the buffers
+  for (int d = 0; d < (int)f->subs.size(); ++d) {
+    gs_flow* s = f->subs[d];
+    DevGuard g(sub_dev(s));
+    GS_TRY(flow_upload(s, q0, p0));
+    if (s->cfg.backend == GS_BARNES_HUT && f->subs.size() > 1) GS_TRY(flow_morton_permute(s));
+    GS_TRY(multi_record(c, d));
+  }
+  f->steps_done = 0;
+  return GS_OK;
+}
+
+int multi_flow_advance(gs_flow* f, int steps) {
+  gs_ctx* c = f->ctx;
+  const int G = (int)f->subs.size();
+  const size_t rb = 2 * vec_bytes(f->prec);
+  for (int k = 0; k < steps; ++k) {
+    for (int stage = 0; stage < flow_stages(f); ++stage) {
+      GS_TRY(multi_wait_all(c));  // the previous stage of every shard is in every buffer
+      std::vector<void*> next(G);
+      for (int d = 0; d < G; ++d) next[d] = f->subs[d]->rec_next.ptr;
+      for (int d = 0; d < G; ++d) {
+        gs_flow* s = f->subs[d];
+        DevGuard g(sub_dev(s));
+        s->peers = peer_bufs(c, next, d);
+        GS_TRY(flow_stage(s, stage, s->rec.ptr, s->rec_next.ptr));
+        s->peers = PeerOut{};
+        GS_TRY(peer_copies(c, next, d, rb * s->shard_begin, rb * s->shard_count));
+        GS_TRY(multi_record(c, d));
+      }
+      for (gs_flow* s : f->subs) {
+        std::swap(s->rec.ptr, s->rec_next.ptr);
+        std::swap(s->rec.bytes, s->rec_next.bytes);
+      }
+    }
+    for (gs_flow* s : f->subs) {
+      DevGuard g(sub_dev(s));
+      GS_TRY(step_counter_inc(s->stepctr.as<int>(), s->ctx->stream));
+      ++s->steps_done;
+    }
+    ++f->steps_done;
+  }
+  return GS_OK;
+}
+
+int multi_flow_check(gs_flow* f) {
+  int first = GS_OK;
+  int step = INT32_MAX;
+  for (gs_flow* s : f->subs) {
+    DevGuard g(sub_dev(s));
+    const int st = flow_check(s);
+    if (st == GS_NONFINITE) step = std::min(step, g_nonfinite);
+    if (st != GS_OK && first == GS_OK) first = st;
+  }
+  if (first == GS_NONFINITE) {
+    g_nonfinite = step;
+    g_err = "non-finite state at timestep " + std::to_string(step);
+  }
+  return first;
+}
+
+int multi_flow_download(gs_flow* f, double* q, double* p) {
+  gs_ctx* c = f->ctx;
+  GS_TRY(multi_wait_all(c));  // shard 0's buffers hold every shard once the others are done
+  gs_flow* s = f->subs[0];
+  DevGuard g(sub_dev(s));
+  return gs_flow_download(s, q, p);
+}
+
+int multi_flow_stats(gs_flow* f, gs_stats* out) {
+  *out = gs_stats{};
+  for (gs_flow* s : f->subs) {
+    DevGuard g(sub_dev(s));
+    gs_stats t = s->stats;
+    GS_TRY(flow_bh_stats(s, &t));
+    out->direct_interactions += t.direct_interactions;
+    out->approximated_interactions += t.approximated_interactions;
+    out->nodes_visited += t.nodes_visited;
+    out->traversal_queries += t.traversal_queries;
+    out->tree_build_ms += t.tree_build_ms;
+  }
+  return GS_OK;
+}
+
+// H(q0, p0) = 1/2 <p0, dH/dp>: each shard's part, summed in shard order
+int multi_flow_energy(gs_flow* f, double* out) {
+  double h = 0.0;
+  for (gs_flow* s : f->subs) {
+    DevGuard g(sub_dev(s));
+    double e = 0.0;
+    GS_TRY(flow_energy(s, &e));
+    h += e;
+  }
+  *out = h;
+  return GS_OK;
+}
+
+int multi_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0, const double* p0,
+                   const double* target, gs_report* report, double* grad_out, gs_stats* stats) {
+  const int T = cfg->timesteps;
+  const int G = (int)c->subs.size();
+  gs_flow* f = scratch_flow(c);
+  GS_TRY(multi_flow_init(f, c, cfg, n));
+  for (gs_flow* s : f->subs) s->want_energy = true;
+  GS_TRY(multi_flow_upload(f, q0, p0));
+  const int prec = f->prec;
+  const size_t rb = 2 * vec_bytes(prec) * n, rec1 = 2 * vec_bytes(prec);
+  const bool bh = cfg->backend == GS_BARNES_HUT;
+  const bool permuted = f->subs[0]->permuted;
+  const auto t0 = std::chrono::steady_clock::now();
+  // per shard: trajectory traj[0..T] (all n records, sub-context rec_b), the
+  // target (stage_c, in the records' order), the adjoints (rec_a / rec_next)
+  std::vector<char*> traj(G);
+  for (int d = 0; d < G; ++d) {
+    gs_flow* s = f->subs[d];
+    gs_ctx* sc = s->ctx;
+    DevGuard g(sc->dev.id);
+    GS_TRY(sc->rec_b.ensure(rb * (T + 1)));
+    traj[d] = sc->rec_b.as<char>();
+    GS_CUDA_OK(cudaMemcpyAsync(traj[d], s->rec.ptr, rb, cudaMemcpyDeviceToDevice, sc->stream));
+    GS_TRY(h2d(sc, sc->stage_c, target, n));
+    if (permuted) {
+      GS_TRY(sc->stage_d.ensure(sizeof(double) * 3 * n));
+      GS_TRY(gather_rows3(sc->stage_c.as<double>(), s->order.as<int>(), n, sc->stage_d.as<double>(),
+                          sc->stream));
+      std::swap(sc->stage_c.ptr, sc->stage_d.ptr);
+      std::swap(sc->stage_c.bytes, sc->stage_d.bytes);
+    }
+    if (bh) GS_TRY(bh_keep_trees(s->bh, T));
+    GS_TRY(multi_record(c, d));
+  }
+  // forward: step k reads traj[k], the epilogues store traj[k+1] on every device
+  for (int k = 0; k < T; ++k) {
+    GS_TRY(multi_wait_all(c));
+    std::vector<void*> next(G);
+    for (int d = 0; d < G; ++d) next[d] = traj[d] + (size_t)(k + 1) * rb;
+    for (int d = 0; d < G; ++d) {
+      gs_flow* s = f->subs[d];
+      DevGuard g(sub_dev(s));
+      s->peers = peer_bufs(c, next, d);
+      s->bh.cache_slot = bh ? k : -1;
+      const int st = flow_stage(s, 0, traj[d] + (size_t)k * rb, next[d]);
+      s->bh.cache_slot = -1;
+      s->peers = PeerOut{};
+      GS_TRY(st);
+      GS_TRY(peer_copies(c, next, d, rec1 * s->shard_begin, rec1 * s->shard_count));
+      ++s->steps_done;
+      GS_TRY(multi_record(c, d));
+    }
+  }
+  GS_TRY(multi_flow_check(f));
+  double energy = 0.0;
+  GS_TRY(multi_flow_energy(f, &energy));
+  const auto t1 = std::chrono::steady_clock::now();
+  // backward: every device initialises the full adjoints from traj[T] (same
+  // values everywhere), then each step updates its shard into every device
+  std::vector<void*> acur(G), anext(G);
+  double sse = 0.0;
+  GS_TRY(multi_wait_all(c));
+  for (int d = 0; d < G; ++d) {
+    gs_flow* s = f->subs[d];
+    gs_ctx* sc = s->ctx;
+    DevGuard g(sc->dev.id);
+    GS_TRY(sc->rec_a.ensure(rb));
+    GS_TRY(sc->epart.ensure(sizeof(double) * (n / 128 + 8)));
+    GS_TRY(sc->scal.ensure(64));
+    acur[d] = sc->rec_a.ptr;
+    anext[d] = s->rec_next.ptr;
+    int blocks = 0;
+    GS_TRY(adjoint_init(prec, traj[d] + (size_t)T * rb, sc->stage_c.as<double>(), cfg->lambda, n,
+                        acur[d], sc->epart.as<double>(), &blocks, sc->stream));
+    if (d == 0) {
+      GS_TRY(reduce_sum(sc->epart.as<double>(), blocks, sc->scal.as<double>() + 1, sc->stream));
+      GS_CUDA_OK(cudaMemcpyAsync(&sse, sc->scal.as<double>() + 1, sizeof(double),
+                                 cudaMemcpyDeviceToHost, sc->stream));
+    }
+    GS_TRY(multi_record(c, d));
+  }
+  gs_stats bst{};
+  for (int k = T - 1; k >= 0; --k) {
+    GS_TRY(multi_wait_all(c));
+    for (int d = 0; d < G; ++d) {
+      gs_flow* s = f->subs[d];
+      gs_ctx* sc = s->ctx;
+      DevGuard g(sc->dev.id);
+      const double cd = prec == kF32 ? s->kc.two_over_s / s->kc.kappa : s->kc.two_over_s;
+      BwdEpi e;
+      e.update = 1;
+      e.dt = 1.0 / T;
+      e.cpq = -cd;
+      e.cpp = 2.0;
+      e.cqq = s->kc.two_over_s;
+      e.cqp = -cd;
+      e.adj_out = anext[d];
+      e.peers = peer_bufs(c, anext, d);
+      GS_TRY(backward_step(sc, cfg, prec, s->kc, n, s->shard_begin, s->shard_count,
+                           traj[d] + (size_t)k * rb, acur[d], k, &s->bh, true, sc->part, e, &bst,
+                           (int)n));
+      GS_TRY(peer_copies(c, anext, d, rec1 * s->shard_begin, rec1 * s->shard_count));
+      GS_TRY(multi_record(c, d));
+    }
+    std::swap(acur, anext);
+  }
+  // gradient = beta_0 + dH/dp(q0, p0) per shard, back to the caller's order
+  std::vector<double> g_host(permuted ? (size_t)3 * n : 0);
+  double* gdst = permuted ? g_host.data() : grad_out;
+  for (int d = 0; d < G; ++d) {
+    gs_flow* s = f->subs[d];
+    gs_ctx* sc = s->ctx;
+    DevGuard g(sc->dev.id);
+    GS_TRY(sc->stage_d.ensure(sizeof(double) * 3 * std::max<int64_t>(s->shard_count, 1)));
+    GS_TRY(gradient_finalize(prec, static_cast<char*>(acur[d]) + rec1 * s->shard_begin,
+                             s->dhdp0.as<double>(), s->shard_count, sc->stage_d.as<double>(),
+                             sc->stream));
+    if (gdst) GS_TRY(d2h(sc, gdst + 3 * s->shard_begin, sc->stage_d.ptr, 3 * s->shard_count));
+  }
+  std::vector<int32_t> order(permuted ? n : 0);
+  if (permuted) {
+    gs_ctx* sc = f->subs[0]->ctx;
+    DevGuard g(sc->dev.id);
+    GS_CUDA_OK(cudaMemcpyAsync(order.data(), f->subs[0]->order.ptr, sizeof(int32_t) * n,
+                               cudaMemcpyDeviceToHost, sc->stream));
+  }
+  for (gs_ctx* sc : c->subs) {
+    DevGuard g(sc->dev.id);
+    GS_TRY(sync(sc));
+  }
+  if (permuted && grad_out)
+    for (int64_t t = 0; t < n; ++t)
+      for (int a = 0; a < 3; ++a) grad_out[3 * order[t] + a] = g_host[3 * t + a];
+  const auto t2 = std::chrono::steady_clock::now();
+  if (report) {
+    report->energy = energy;
+    report->residual_sse = sse;
+    report->attachment = cfg->lambda * sse;
+    report->total = report->energy + report->attachment;
+  }
+  if (stats) {
+    GS_TRY(multi_flow_stats(f, stats));
+    stats->direct_interactions += bst.direct_interactions;
+    stats->approximated_interactions += bst.approximated_interactions;
+    stats->nodes_visited += bst.nodes_visited;
+    stats->traversal_queries += bst.traversal_queries;
+    stats->forward_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    stats->backward_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  }
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+gs_ctx* gs_create_multi(int32_t count, const int32_t* devices, gs_status* status) {
+  if (count < 1 || count > kMaxPeers + 1 || !devices) {
+    g_err = "gs_create_multi: 1.." + std::to_string(kMaxPeers + 1) + " devices";
+    if (status) *status = GS_INVALID_ARGUMENT;
+    return nullptr;
+  }
+  gs_ctx* c = gs_create(devices[0], status);
+  if (!c) return nullptr;
+  for (int d = 0; d < count; ++d) {
+    gs_ctx* s = gs_create(devices[d], status);
+    if (!s) {
+      gs_destroy(c);
+      return nullptr;
+    }
+    c->subs.push_back(s);
+    cudaEvent_t e{};
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    c->ev.push_back(e);
+  }
+  // P2P stores need peer access between every pair of distinct devices
+  bool p2p = true;
+  for (int a = 0; a < count && p2p; ++a)
+    for (int b = 0; b < count && p2p; ++b) {
+      if (devices[a] == devices[b]) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]);
+      if (!ok) { p2p = false; break; }
+      cudaSetDevice(devices[a]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) p2p = false;
+      cudaGetLastError();  // clear "already enabled"
+    }
+  // GS_MULTI_COPIES=1: exchange by explicit peer copies instead (A/B, tests)
+  if (const char* e = std::getenv("GS_MULTI_COPIES")) p2p = p2p && std::atoi(e) == 0;
+  c->peer_stores = p2p;
+  cudaSetDevice(devices[0]);
+  if (status) *status = GS_OK;
+  return c;
+}
+
+int32_t gs_ctx_device_count(const gs_ctx* c) {
+  return c ? (c->subs.empty() ? 1 : (int32_t)c->subs.size()) : 0;
+}
+
+int32_t gs_ctx_peer_stores(const gs_ctx* c) { return c && !c->subs.empty() && c->peer_stores ? 1 : 0; }
 
 }  // extern "C"

@@ -102,16 +102,29 @@ int rhs_sorted_partials(const Device& dev, const void* srec, const int* perm, in
 
 // ---- all-pairs (allpairs.cu); return the number of source chunks S used,
 // ---- or -1 if S would exceed part_cap_chunks.
+// plan_tgt > 0: launch n_tgt targets under the plan of a plan_tgt-target
+// problem (kernel variant, targets per thread, source chunking), so a shard's
+// partial sums are bit-identical to the plan_tgt-target run's (multi-device).
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
-                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st);
+                 const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st,
+                 int plan_tgt = -1);
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
                   int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
-                  int part_cap_chunks, cudaStream_t st);
+                  int part_cap_chunks, cudaStream_t st, int plan_tgt = -1);
 int vel_partials(const Device& dev, int prec, const void* rec, int n, const void* ev, int m,
                  const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st);
 constexpr int kMaxChunks = 16;
 
 // ---- epilogues (epilogue.cu) -----------------------------------------------
+// Multi-device flows (gs_create_multi): a stage epilogue stores each updated
+// target record into its own buffer AND into the same slot of every peer's
+// buffer (P2P stores over NVLink / NVSwitch), so the per-stage all-gather of
+// the shards is fused into the epilogue -- no separate collective.
+constexpr int kMaxPeers = 15;
+struct PeerOut {
+  void* buf[kMaxPeers] = {};
+  int n = 0;
+};
 // Forward stage epilogue: folds partials A = sum g p, B = sum c d (per target),
 // forms dH/dp = cp * A, dH/dq = cq * B and applies the integrator.
 struct FwdEpi {
@@ -129,6 +142,7 @@ struct FwdEpi {
   int* bad_step = nullptr;        // atomicMin on non-finite output
   int step = 0;                   // step index (1-based) reported on non-finite
   const int* step_dev = nullptr;  // if set: step = *step_dev + 1 (graph-replayable)
+  PeerOut peers;                  // multi-device: the updated records go here too
 };
 int fwd_epilogue(int prec, const FwdEpi& e, cudaStream_t st, int* blocks_out);
 
@@ -136,6 +150,8 @@ struct BwdEpi {
   int n_tgt = 0, tgt_begin = 0, S = 1;
   const void* part = nullptr;
   void* adj = nullptr;  // [n][2] (alpha, beta) updated in place when update != 0
+  void* adj_out = nullptr;  // where the updated adjoints go (nullptr = adj, in place)
+  PeerOut peers;            // multi-device: the updated adjoints go here too
   int update = 1;
   double dt = 0.0, cpq = 0.0, cpp = 2.0, cqq = 0.0, cqp = 0.0;
   double* out[4] = {nullptr, nullptr, nullptr, nullptr};  // pq, pp, qq, qp (optional)
@@ -170,6 +186,8 @@ int reduce_sum(const double* part, int count, double* out, cudaStream_t st);
 // out[t] = in[perm[t]] (records, [n][2] V4) / out[perm[t]] = in[t] (double [n][3])
 int permute_records(int prec, const void* in, const int* perm, int64_t n, void* out, cudaStream_t st);
 int scatter_rows3(const double* in, const int* perm, int64_t n, double* out, cudaStream_t st);
+// out[t] = in[perm[t]] (double [n][3])
+int gather_rows3(const double* in, const int* perm, int64_t n, double* out, cudaStream_t st);
 // per-block FP64 sums of the .w lane of partial vec4 `which` of n targets ([n][per] layout)
 int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
                int* blocks, cudaStream_t st);

@@ -118,6 +118,11 @@ __global__ void __launch_bounds__(kEpiNT) k_fwd_epi(FwdEpi e) {
       V4<R>* out = e.rec_out ? static_cast<V4<R>*>(e.rec_out) : rec;
       st4(out + 2 * i, q);
       st4(out + 2 * i + 1, p);
+      for (int k = 0; k < e.peers.n; ++k) {  // fused all-gather: the peers' copies of slot i
+        V4<R>* o = static_cast<V4<R>*>(e.peers.buf[k]);
+        st4(o + 2 * i, q);
+        st4(o + 2 * i + 1, p);
+      }
       if (check && e.bad_step &&
           !(fin(q.x) && fin(q.y) && fin(q.z) && fin(p.x) && fin(p.y) && fin(p.z)))
         atomicMin(e.bad_step, e.step_dev ? *e.step_dev + 1 : e.step);
@@ -155,8 +160,14 @@ __global__ void __launch_bounds__(kEpiNT) k_bwd_epi(BwdEpi e) {
     const R dt = R(e.dt);
     a.x += dt * (pq.x - qq.x); a.y += dt * (pq.y - qq.y); a.z += dt * (pq.z - qq.z);
     b.x += dt * (pp.x - qp.x); b.y += dt * (pp.y - qp.y); b.z += dt * (pp.z - qp.z);
-    st4(adj + 2 * i, a);
-    st4(adj + 2 * i + 1, b);
+    V4<R>* out = e.adj_out ? static_cast<V4<R>*>(e.adj_out) : adj;
+    st4(out + 2 * i, a);
+    st4(out + 2 * i + 1, b);
+    for (int k = 0; k < e.peers.n; ++k) {
+      V4<R>* o = static_cast<V4<R>*>(e.peers.buf[k]);
+      st4(o + 2 * i, a);
+      st4(o + 2 * i + 1, b);
+    }
   }
 }
 
@@ -262,6 +273,14 @@ __global__ void k_permute_records(const V4<R>* in, const int* perm, int64_t n, V
   st4(out + 2 * t, ld4(in + 2 * i));
   st4(out + 2 * t + 1, ld4(in + 2 * i + 1));
 }
+__global__ void k_gather_rows3(const double* in, const int* perm, int64_t n, double* out) {
+  const int64_t t = blockIdx.x * (int64_t)kEpiNT + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = perm[t];
+  out[3 * t] = in[3 * i];
+  out[3 * t + 1] = in[3 * i + 1];
+  out[3 * t + 2] = in[3 * i + 2];
+}
 __global__ void k_scatter_rows3(const double* in, const int* perm, int64_t n, double* out) {
   const int64_t t = blockIdx.x * (int64_t)kEpiNT + threadIdx.x;
   if (t >= n) return;
@@ -278,6 +297,12 @@ int permute_records(int prec, const void* in, const int* perm, int64_t n, void* 
     k_permute_records<float><<<nb, kEpiNT, 0, st>>>((const float4*)in, perm, n, (float4*)out);
   else
     k_permute_records<double><<<nb, kEpiNT, 0, st>>>((const double4*)in, perm, n, (double4*)out);
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int gather_rows3(const double* in, const int* perm, int64_t n, double* out, cudaStream_t st) {
+  k_gather_rows3<<<blocks_for(n, kEpiNT), kEpiNT, 0, st>>>(in, perm, n, out);
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }

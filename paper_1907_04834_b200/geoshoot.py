@@ -190,14 +190,30 @@ class Evaluation:
 
 
 class Geoshoot:
-    """One device context (gs_ctx): a CUDA stream + workspaces on one B200."""
+    """A device context (gs_ctx): a CUDA stream + workspaces on one B200, or --
+    with ``devices=[...]`` -- a multi-device context (gs_create_multi) whose
+    shooting calls (shoot_forward, objective, evaluate, optimize, flows) shard
+    the target points across the devices, the per-stage exchange fused into
+    the stage epilogues as peer stores."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices=None):
         self.lib = L.load()
         st = C.c_int(0)
-        self.ctx = self.lib.gs_create(device, C.byref(st))
+        if devices is None:
+            self.ctx = self.lib.gs_create(device, C.byref(st))
+        else:
+            arr = (C.c_int32 * len(devices))(*devices)
+            self.ctx = self.lib.gs_create_multi(len(devices), arr, C.byref(st))
         if not self.ctx:
             raise DeviceError(f"gs_create failed ({st.value}): {self._err()}")
+
+    @property
+    def device_count(self) -> int:
+        return self.lib.gs_ctx_device_count(self.ctx)
+
+    @property
+    def peer_stores(self) -> bool:
+        return bool(self.lib.gs_ctx_peer_stores(self.ctx))
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -1,0 +1,206 @@
+"""Multi-device contexts through the C ABI (gs_create_multi).
+
+One process drives G shards of the target points; every shard holds all the
+records, and each stage epilogue stores its shard's updated records into
+every peer's buffer (P2P stores: the per-stage all-gather fused into the
+epilogue), records ping-ponging between stages. The adjoint pass exchanges
+the (alpha, beta) shards the same way.
+
+Only one B200 is available to the tests, so the shards are placed on the SAME
+device, each on its own stream (gs_create_multi accepts a device more than
+once): every line of the sharding, the exchange and the ordering runs --
+nothing waits in a spin loop, the streams are ordered by events exactly as
+across devices. The exchange through explicit peer copies (the fallback when
+P2P is unavailable) is forced with GS_MULTI_COPIES=1.
+
+Exact flows and evaluate() gradients must be BIT-IDENTICAL to one device
+(shards run the full problem's launch plan, allpairs.cu plan / rhs_partials
+plan_tgt); Barnes-Hut results have the same interaction sets -- equal totals
+-- and agree to summation-order rounding.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1907_04834_b200 import BARNES_HUT, EULER, EXACT, F32, F64, RK4, Geoshoot, ShootingConfig
+from tests.util import ellipsoid, f32, rel_l2, smooth_momenta, sym_uniform, tube, uniform
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=[2, 3], ids=["2shards", "3shards"])
+def multi(request):
+    g = Geoshoot(devices=[0] * request.param)
+    yield g
+    g.close()
+
+
+def cube(n, seed):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+
+
+def test_multi_context_reports_devices(multi):
+    assert multi.device_count in (2, 3)
+    assert multi.peer_stores
+
+
+@pytest.mark.parametrize("prec,integ", [(F32, RK4), (F64, EULER), (F32, EULER)])
+def test_exact_shoot_forward_bitwise_equals_one_device(gs, multi, prec, integ):
+    n = 20_001  # not divisible by the shard count
+    q, p = cube(n, 5)
+    cfg = ShootingConfig(sigma=0.05, timesteps=4, backend=EXACT, integrator=integ, precision=prec)
+    wq, wp, we, wst = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    gq, gp, ge, gst = multi.shoot_forward(q, p, cfg, keep_trajectory=False)
+    assert np.array_equal(gq, wq) and np.array_equal(gp, wp)
+    assert ge == pytest.approx(we, rel=1e-12)
+    assert gst["direct_interactions"] == wst["direct_interactions"]
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-12), (F32, 1e-5)])
+def test_bh_shoot_forward_matches_one_device(gs, multi, prec, tol):
+    n = 30_000
+    q = ellipsoid(n, seed=11)
+    p = smooth_momenta(q, 0.005, 12)
+    cfg = ShootingConfig(sigma=3.0, timesteps=5, backend=BARNES_HUT, integrator=RK4, precision=prec)
+    wq, wp, we, wst = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    gq, gp, ge, gst = multi.shoot_forward(q, p, cfg, keep_trajectory=False)
+    # same interaction sets on the same states; after the first stage the
+    # states differ by summation-order rounding, which can flip an FP32 gate
+    # decision at the threshold
+    for k in ("direct_interactions", "approximated_interactions", "nodes_visited"):
+        if prec == F64:
+            assert gst[k] == wst[k], k
+        else:
+            assert abs(gst[k] - wst[k]) <= 1e-5 * wst[k], k
+    assert rel_l2(gq, wq) < tol and rel_l2(gp, wp) < tol
+    assert ge == pytest.approx(we, rel=tol)
+
+
+def test_shoot_forward_trajectory_on_multi(gs, multi):
+    n = 5000
+    q, p = uniform(n, 2.0, 21), sym_uniform(n, 0.05, 22)
+    cfg = ShootingConfig(sigma=0.3, timesteps=3, precision=F64)
+    a = gs.shoot_forward(q, p, cfg)
+    b = multi.shoot_forward(q, p, cfg)
+    assert np.array_equal(a.q, b.q) and np.array_equal(a.p, b.p)
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+def test_exact_evaluate_bitwise_equals_one_device(gs, multi, prec):
+    n = 12_345
+    q = tube(n, seed=31)
+    p = smooth_momenta(q, 0.01, 32)
+    t = q + 0.05
+    if prec == F32:
+        q, p, t = f32(q), f32(p), f32(t)
+    cfg = ShootingConfig(sigma=5.0, lambda_=100.0, timesteps=6, backend=EXACT, precision=prec)
+    a = gs.evaluate(q, p, t, cfg)
+    b = multi.evaluate(q, p, t, cfg)
+    assert np.array_equal(a.gradient, b.gradient)
+    assert b.report["residual_sse"] == a.report["residual_sse"]
+    assert b.report["total"] == pytest.approx(a.report["total"], rel=1e-12)
+
+
+@pytest.mark.parametrize("prec,tol", [(F64, 1e-11), (F32, 1e-5)])
+def test_bh_evaluate_matches_one_device(gs, multi, prec, tol):
+    n = 20_000
+    q = ellipsoid(n, seed=41)
+    p = smooth_momenta(q, 0.005, 42)
+    t = q + np.array([0.3, -0.2, 0.1])
+    if prec == F32:
+        q, p, t = f32(q), f32(p), f32(t)
+    cfg = ShootingConfig(sigma=3.0, lambda_=1.0, timesteps=5, backend=BARNES_HUT, precision=prec)
+    a = gs.evaluate(q, p, t, cfg)
+    b = multi.evaluate(q, p, t, cfg)
+    for k in ("direct_interactions", "approximated_interactions", "nodes_visited"):
+        if prec == F64:
+            assert b.stats[k] == a.stats[k], k
+        else:  # FP32 states differ by rounding after step 1 (see above)
+            assert abs(b.stats[k] - a.stats[k]) <= 1e-5 * a.stats[k], k
+    assert b.report["total"] == pytest.approx(a.report["total"], rel=tol)
+    assert rel_l2(b.gradient, a.gradient) < 10 * tol
+
+
+def test_evaluate_on_multi_matches_reference(multi, ref):
+    n = 1500
+    q = np.stack([np.linspace(0, 100, n), np.random.default_rng(51).uniform(-2, 2, n),
+                  np.zeros(n)], 1)
+    p = sym_uniform(n, 0.05, 52)
+    t = q + np.array([0.0, 0.5, 0.1])
+    for backend in (0, 1):
+        cfg = ShootingConfig(sigma=2.0, lambda_=1.0, timesteps=10,
+                             backend=BARNES_HUT if backend else EXACT)
+        ev = multi.evaluate(q, p, t, cfg)
+        rep, g, _, _ = ref.evaluate(q, p, t, 2.0, 1.0, 10, backend, threads=8)
+        assert ev.report["total"] == pytest.approx(rep[2], rel=1e-10)
+        assert rel_l2(ev.gradient, g) <= 1e-9
+
+
+def test_flow_api_on_multi(gs, multi):
+    n = 8000
+    q, p = cube(n, 61)
+    cfg = ShootingConfig(sigma=0.05, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    one = gs.flow(cfg, n)
+    one.upload(q, p)
+    one.advance(3)
+    one.sync()
+    wq, wp = one.download()
+    fl = multi.flow(cfg, n)
+    fl.upload(q, p)
+    fl.advance(1)
+    fl.advance(2)  # events carry the ordering across calls
+    fl.sync()
+    gq, gp = fl.download()
+    assert np.array_equal(gq, wq) and np.array_equal(gp, wp)
+    st = fl.stats()
+    assert st["direct_interactions"] == 3 * 4 * n * n
+    fl.upload(q, p)  # re-upload restarts the flow
+    fl.advance(3)
+    fl.sync()
+    assert np.array_equal(fl.download()[0], wq)
+
+
+def test_optimize_on_multi_matches_one_device(gs, multi):
+    n = 600
+    q = tube(n, seed=71)
+    target = q + 0.2 * np.sin(q / 7.0)
+    cfg = ShootingConfig(sigma=5.0, lambda_=100.0, timesteps=5, backend=EXACT, precision=F64)
+    a = gs.optimize(q, target, cfg, max_iterations=8)
+    b = multi.optimize(q, target, cfg, max_iterations=8)
+    assert a["iterations"] == b["iterations"] and a["reason"] == b["reason"]
+    assert rel_l2(b["p0"], a["p0"]) < 1e-9
+
+
+def test_peer_copy_exchange_equals_peer_stores(gs):
+    os.environ["GS_MULTI_COPIES"] = "1"
+    try:
+        m = Geoshoot(devices=[0, 0])
+    finally:
+        del os.environ["GS_MULTI_COPIES"]
+    try:
+        assert not m.peer_stores
+        n = 10_000
+        q, p = cube(n, 81)
+        cfg = ShootingConfig(sigma=0.05, timesteps=3, backend=EXACT, integrator=RK4, precision=F32)
+        wq, wp, _, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+        gq, gp, _, _ = m.shoot_forward(q, p, cfg, keep_trajectory=False)
+        assert np.array_equal(gq, wq) and np.array_equal(gp, wp)
+        t = q + 0.01
+        cfgb = ShootingConfig(sigma=0.05, lambda_=10.0, timesteps=3, backend=BARNES_HUT,
+                              precision=F64)
+        a, b = gs.evaluate(q, p, t, cfgb), m.evaluate(q, p, t, cfgb)
+        assert rel_l2(b.gradient, a.gradient) < 1e-11
+    finally:
+        m.close()
+
+
+def test_multi_nonfinite_is_reported(multi):
+    from paper_1907_04834_b200 import NonFiniteState
+    n = 4000
+    q, p = uniform(n, 1.0, 91), sym_uniform(n, 1e30, 92)
+    cfg = ShootingConfig(sigma=0.5, timesteps=6, backend=EXACT, precision=F32)
+    with pytest.raises(NonFiniteState) as e:
+        multi.shoot_forward(q, p, cfg, keep_trajectory=False)
+    assert e.value.timestep >= 1
