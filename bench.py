@@ -7,20 +7,35 @@ largest that fits one GPU): N = 1,000,000 points uniform i.i.d. in the unit
 cube, momenta i.i.d. N(0, 1e-4) per component (variance 1e-4), sigma = 0.0131,
 FP32, RK4 with 10 steps over [0, 1] (dt = 0.1), exact all-pairs kernel. One
 bench "step" = one RK4 flow step = 4 exact right-hand sides = 4 N^2 ordered
-pair interactions. The same flow through the Barnes-Hut back end (3 sigma
-gate, tree rebuilt at every stage) is reported under "bh".
+pair interactions (the exact kernel's cost does not depend on the positions).
+Auxiliary lines on the same JSON line:
+
+* ``bh``: the same flow through the Barnes-Hut back end (3 sigma gate, tree
+  rebuilt at every stage), timed over exactly the config's 10 RK4 steps from
+  q0 (a BH step's cost depends on the evolving positions);
+* ``exact_cutoff``: the exact flow with the opt-in FP32 underflow cutoff, the
+  same 10-step trajectory;
+* ``adjoint``: config 3's unit of work -- one evaluate() (forward flow + kept
+  trees + adjoint) at N = 50k, T = 20, FP32, exact and Barnes-Hut -- with the
+  Hessian-product kernel's roofline;
+* ``fp64``: one exact RK4 step at N = 1M in FP64 (the reference's precision:
+  the like-for-like line against the FP64 reference CPU arm);
+* ``n100k``; ``e2e`` (the public call with host buffers); ``cpu_baseline``.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n N]
 
-Multi-GPU (torchrun, one rank per GPU): targets are sharded across ranks and
-the updated (q, p) records are all-gathered over NCCL after every stage
+Multi-GPU (one process per GPU; ``--gpus N`` outside torchrun re-launches itself
+under torch.distributed.run): targets are sharded across ranks and the updated
+(q, p) records are all-gathered over NCCL after every stage
 (paper_1907_04834_b200/shard.py); time = max over ranks of the device time.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -36,6 +51,9 @@ T_STEPS = 10
 METRIC = "flow steps/s (RK4, 4 RHS/step) & G pair-interactions/s, config 4"
 # Algorithmic DRAM bytes per point of one FP32 tree build (DESIGN.md §4 table)
 BUILD_BYTES_PER_POINT = 1080
+# FP32 FMA-pipe operations per ordered pair
+RHS_FP32_PER_PAIR = 16
+HESS_FP32_PER_PAIR = 37
 
 
 def workload(n: int, seed: int = 2024):
@@ -50,6 +68,18 @@ def peaks_json():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def traffic_json(n):
+    """DRAM bytes per launch of the headline kernel from the latest committed ncu capture."""
+    for name in ("r02_rhs_traffic.json", "r01_rhs_traffic.json"):
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", name)))
+        except Exception:
+            continue
+        if tj.get("n") == n:
+            return tj["dram_bytes_per_launch"], name
+    return None, None
 
 
 class Clocks:
@@ -88,7 +118,8 @@ class Clocks:
 def cpu_reference(n_sample: int, threads: int, reps: int = 1):
     """The reference's own exact RHS (kernel_exact.cpp:29-61, compiled by path
     into oracle/_ref) on `threads` host threads concurrently, each on the same
-    n_sample-point input. Returns ordered pair interactions per second."""
+    n_sample-point input (the reference's exact path is serial per call).
+    Returns ordered pair interactions per second."""
     import oracle
     R = oracle.ref() if oracle.have_ref() else None
     q, p = workload(n_sample, seed=7)
@@ -118,6 +149,9 @@ def run_reference(args):
             rates.append(r)
     rate = float(np.mean(rates))
     value = rate / (4.0 * float(args.n) ** 2)
+    sample = (f"{used} concurrent reference hamiltonian_gradients calls (FP64, serial per call) at "
+              f"N={n_s} per step ({n_s}^2 ordered pairs each), extrapolated to N={args.n} by N^2 x "
+              f"4 RHS/step (a full N={args.n} RHS takes hours on the host)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "flow steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -127,9 +161,7 @@ def run_reference(args):
                    "n": args.n, "sigma": SIGMA, "integrator": "rk4", "timesteps": T_STEPS},
         "pair_interactions_per_s": rate,
         "cpu_baseline": {"value": value, "unit": "flow steps/s", "cores": used, "kind": kind,
-                         "sample": f"{used} concurrent reference hamiltonian_gradients calls at "
-                                   f"N={n_s} per step ({n_s}^2 ordered pairs each), extrapolated "
-                                   f"to N={args.n} by N^2 x 4 RHS/step"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "flow steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -137,13 +169,34 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------
+def spawn_ranks(args) -> int:
+    """--gpus N outside torchrun: re-launch this script with N ranks (one per GPU)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def microbench(lib, dev):
+    out = {}
+    for kind, name in ((0, "ffma"), (1, "ex2"), (2, "dfma"), (3, "ffma_reg"), (4, "ffma2")):
+        v = C.c_double()
+        lib.gs_microbench(dev, kind, C.byref(v))
+        out[name] = v.value
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1907_04834_b200 import BARNES_HUT, EXACT, F32, RK4, Geoshoot, ShootingConfig
-    from paper_1907_04834_b200 import _lib
+    from paper_1907_04834_b200 import (BARNES_HUT, EULER, EXACT, F32, F64, RK4, Geoshoot,
+                                       ShootingConfig, _lib)
     from paper_1907_04834_b200.shard import ShardedFlow
+    from tests.util import smooth_momenta, tube
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -153,8 +206,28 @@ def run_ours(args):
         dist.init_process_group("nccl")
     N = args.n
     q0, p0 = workload(N)
-
     gs = Geoshoot(local)
+    lib = _lib.load()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def ev_pair():
+        return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # L2 is 126 MB and the records are 32 MB: flush it before every timed step
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # ---- headline: exact all-pairs RK4 steps --------------------------------
     cfg = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=EXACT, integrator=RK4,
                          precision=F32)
     flow = gs.flow(cfg, N)
@@ -166,24 +239,17 @@ def run_ours(args):
     def step():
         if drv is None:
             flow.advance(1)
-        else:
-            drv.step(1)
-
-    # L2 is 126 MB and the records are 32 MB: flush it before every timed step
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+            return flow.last_launches()
+        l0 = drv.launches
+        drv.step(1)
+        return drv.launches - l0
 
     for _ in range(args.warmup):
         step()
     flow.sync()
     barrier()
     flow.profile(True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    ev = [ev_pair() for _ in range(args.steps)]
     clocks = Clocks(local)
     launches = 0
     barrier()
@@ -191,64 +257,44 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             flush.zero_()
         ev[k][0].record(stream)
-        step()
+        launches += step()
         ev[k][1].record(stream)
-        launches += flow.last_launches() if drv is None else 8
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     flow.sync()  # raises NonFiniteState if the flow blew up
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
     prof = flow.profile_read()
     flow.profile(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     value = args.steps / (ms / 1e3)
     pairs_per_s = 4.0 * N * float(N) * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel (all-pairs RHS): issue-bound at 16 FP32
-    # instructions per pair; peak from a live FFMA microbenchmark
-    lib = _lib.load()
-    import ctypes as C
-    ffma = C.c_double()
-    lib.gs_microbench(local, 0, C.byref(ffma))
-    ex2 = C.c_double()
-    lib.gs_microbench(local, 1, C.byref(ex2))
-    ffma_reg = C.c_double()
-    lib.gs_microbench(local, 3, C.byref(ffma_reg))
-    ffma2 = C.c_double()
-    lib.gs_microbench(local, 4, C.byref(ffma2))
+    # roofline of the dominant kernel (all-pairs RHS): FMA-pipe bound at 16 FP32
+    # per pair; peak from a live FFMA microbenchmark
+    mb = microbench(lib, local)
     k_ms = prof["kernel_ms"] / max(1, prof["kernel_launches"])
     pairs_per_launch = float(N) * shard
     achieved = pairs_per_launch / (k_ms * 1e-3) / 1e9  # Gpair/s
-    peak = ffma.value / 16.0 / 1e9
+    peak = mb["ffma"] / RHS_FP32_PER_PAIR / 1e9
     mp = peaks_json()
-    nominal = 148 * 128 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 16.0 / 1e9
-    traffic = None
-    try:  # dram bytes per launch of the same kernel from the committed ncu capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_rhs_traffic.json")))
-        if tj.get("n") == N and world == 1:
-            traffic = tj["dram_bytes_per_launch"]
-    except Exception:
-        pass
+    nominal = 148 * 128 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / RHS_FP32_PER_PAIR / 1e9
+    traffic, tsrc = traffic_json(N) if world == 1 else (None, None)
     roofline = {
-        "bound": "fp32-issue", "achieved": achieved, "peak": peak, "unit": "Gpair/s",
+        "bound": "fp32-fma-pipe", "achieved": achieved, "peak": peak, "unit": "Gpair/s",
         "frac": achieved / peak, "traffic": traffic,
-        "traffic_unit": "DRAM bytes per launch (ncu, profiles/r01_rhs_traffic.json)",
+        "traffic_unit": f"DRAM bytes per launch (ncu, profiles/{tsrc})" if tsrc else None,
         "peak_source": "live FFMA microbenchmark (gs_microbench kind 0): "
-                       f"{ffma.value / 1e12:.2f} T lane-FFMA/s / 16 FP32 instructions per pair; "
+                       f"{mb['ffma'] / 1e12:.2f} T lane-FFMA/s / 16 FP32 instructions per pair; "
                        "MEASURED_PEAKS.json has no FP32 figure",
         "nominal_peak": nominal, "frac_of_nominal": achieved / nominal,
-        "peak_register_operand_ffma": ffma_reg.value / 16.0 / 1e9,
-        "peak_packed_ffma2": ffma2.value / 16.0 / 1e9,
-        "sfu_frac": achieved * 1e9 / ex2.value if ex2.value else None,
-        "kernel": "k_rhs_f32x2<12,128,2,8> (packed FFMA2, source loop unrolled 8)", "kernel_ms_avg": k_ms,
-        "kernel_share_of_step": prof["kernel_ms"] / ms if ms else None,
+        "peak_register_operand_ffma": mb["ffma_reg"] / RHS_FP32_PER_PAIR / 1e9,
+        "peak_packed_ffma2": mb["ffma2"] / RHS_FP32_PER_PAIR / 1e9,
+        "sfu_frac": achieved * 1e9 / mb["ex2"] if mb["ex2"] else None,
+        "kernel": "k_rhs_f32x2<12,128,2,8> (packed FFMA2, source loop unrolled 8)",
+        "kernel_ms_avg": k_ms,
+        "kernel_share_of_step": prof["kernel_ms"] / (ms / 1) if ms else None,
         "algorithmic_per_launch": f"{pairs_per_launch:.3e} ordered pairs x 16 FP32 + 1 MUFU",
     }
-
     line = {
         "metric": METRIC, "value": value, "unit": "flow steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -264,142 +310,181 @@ def run_ours(args):
         "clocks": clk,
         "roofline": roofline,
     }
+    del drv, flow
 
-    # ---- Barnes-Hut back end on the same workload (rank 0 reporting) -----------
-    if not args.no_bh and world == 1:
+    # ---- end to end through the public API, host buffers ---------------------
+    pin_q = torch.empty((N, 3), dtype=torch.float64, pin_memory=True).numpy()
+    pin_p = torch.empty((N, 3), dtype=torch.float64, pin_memory=True).numpy()
+    pin_q[:] = q0
+    pin_p[:] = p0
+    if world == 1:
+        t0 = time.perf_counter()
+        gs.shoot_forward(pin_q, pin_p, cfg, keep_trajectory=False)
+        dt = time.perf_counter() - t0
+        call = f"gs_shoot_forward (10 RK4 steps, final state only) x1, {dt:.2f} s"
+    else:
+        fe = gs.flow(cfg, N)
+        de = ShardedFlow(fe, 4)
+        barrier()
+        t0 = time.perf_counter()
+        fe.upload(pin_q, pin_p)
+        de.step(T_STEPS)
+        fe.sync()
+        fe.download()
+        dt = max_over_ranks(time.perf_counter() - t0)
+        call = (f"per rank: gs_flow_upload + {T_STEPS} sharded RK4 steps (NCCL all-gather per "
+                f"stage) + gs_flow_download; max over ranks {dt:.2f} s")
+        del de, fe
+    line["e2e"] = {"value": T_STEPS / dt, "unit": "flow steps/s",
+                   "h2d_bytes_per_step": 2 * N * 24 // T_STEPS,
+                   "d2h_bytes_per_step": 2 * N * 24 // T_STEPS, "call": call}
+
+    # ---- Barnes-Hut: exactly the config's 10 RK4 steps from q0 ----------------
+    def bh_line():
         cfg_bh = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=BARNES_HUT,
                                 integrator=RK4, precision=F32)
         fb = gs.flow(cfg_bh, N)
-        fb.upload(q0, p0)
         sb = torch.cuda.ExternalStream(fb.stream())
-        fb.advance(max(1, args.warmup))
-        fb.sync()
-        # time the first kb steps of the config-4 flow itself (the point
-        # distribution, hence the traversal work, evolves along the flow)
-        fb.upload(q0, p0)
-        fb.sync()
-        st0 = fb.stats()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        kb = max(1, args.steps)
-        with torch.cuda.stream(sb):
-            flush.zero_()
-        e0.record(sb)
-        fb.advance(kb)  # production path: steps after the first replay a CUDA graph
-        e1.record(sb)
-        torch.cuda.synchronize()
-        fb.sync()
-        bms = e0.elapsed_time(e1)
-        st1 = fb.stats()
-        # per-phase kernel times: the same steps again, profiled (eager launches)
-        fb.upload(q0, p0)
-        fb.sync()
-        fb.profile(True)
-        fb.advance(kb)
-        fb.sync()
-        ph = fb.profile_phases(6)
-        fb.profile(False)
-        rhs = 4 * kb
+
+        def trajectory(timed):
+            fb.upload(q0, p0)
+            d = ShardedFlow(fb, 4, stream=sb) if world > 1 else None
+            fb.sync()
+            barrier()
+            st0 = fb.stats()
+            with torch.cuda.stream(sb):
+                flush.zero_()
+            e0, e1 = ev_pair()
+            e0.record(sb)
+            if d is None:
+                fb.advance(T_STEPS)  # steps after the first replay a CUDA graph
+            else:
+                d.step(T_STEPS)
+            e1.record(sb)
+            torch.cuda.synchronize()
+            barrier()
+            fb.sync()
+            return e0.elapsed_time(e1), st0, fb.stats(), (d.launches if d else fb.last_launches())
+
+        trajectory(False)  # warm-up trajectory (allocations, graph capture)
+        bms, st0, st1, bl = trajectory(True)
+        bms = max_over_ranks(bms)
         d = st1["direct_interactions"] - st0["direct_interactions"]
         a_ = st1["approximated_interactions"] - st0["approximated_interactions"]
         v = st1["nodes_visited"] - st0["nodes_visited"]
-        trav_s = ph["kernel"]["ms"] / 1e3
-        build_ms = ph["build"]["ms"] / max(1, ph["build"]["count"])
-        lane_peak = ffma.value  # lane FFMA/s (live microbenchmark)
-        line["bh"] = {
-            "value": kb / (bms / 1e3), "unit": "flow steps/s", "ms_per_step": bms / kb,
-            "n2_equivalent_pairs_per_s": 4.0 * N * float(N) * kb / (bms / 1e3),
-            "interactions_per_s": (d + a_) / (bms / 1e3),
-            "per_query_per_rhs": {"direct": d / (rhs * N), "approximated": a_ / (rhs * N),
-                                  "visited": v / (rhs * N)},
-            "traversal_ms_per_rhs": ph["kernel"]["ms"] / max(1, ph["kernel"]["count"]),
-            "tree_build_ms_per_rhs": build_ms,
-            "build_phases_ms_per_rhs": {k: ph[k]["ms"] / max(1, ph[k]["count"])
-                                        for k in ("bbox_keys", "sort", "topology", "aggregate")},
-            # 16 FP32 per interaction + 12 per visited node
-            "traversal_fp32_issue_frac": ((16.0 * (d + a_) + 12.0 * v) / trav_s) / lane_peak
-            if trav_s > 0 else None,
-            # algorithmic bytes of the build kernels, FP32 (per point)
-            "build_gbs_algorithmic": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9,
-            "build_hbm_frac": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9
-            / float(mp.get("hbm_gbs", 6550.0)),
-            "kernel": "k_bh_ws<float> (independent walks); tree: radix sort + LCP topology",
-        }
-        del fb
+        rhs = 4 * T_STEPS
+        out = {"value": T_STEPS / (bms / 1e3), "unit": "flow steps/s", "ms_per_step": bms / T_STEPS,
+               "timed": f"one full trajectory: {T_STEPS} RK4 steps from q0 (L2 flushed before)",
+               "n2_equivalent_pairs_per_s": 4.0 * N * float(N) * T_STEPS / (bms / 1e3),
+               "interactions_per_s": (d + a_) / (bms / 1e3) * world,
+               "per_query_per_rhs": {"direct": d / (rhs * shard), "approximated": a_ / (rhs * shard),
+                                     "visited": v / (rhs * shard)},
+               "gpu_launches": bl, "parallelism": f"target-shard x{world}"}
+        if world == 1:
+            # per-phase kernel times: the same trajectory again, profiled (eager)
+            fb.upload(q0, p0)
+            fb.sync()
+            fb.profile(True)
+            fb.advance(T_STEPS)
+            fb.sync()
+            ph = fb.profile_phases(6)
+            fb.profile(False)
+            trav_s = ph["kernel"]["ms"] / 1e3
+            build_ms = ph["build"]["ms"] / max(1, ph["build"]["count"])
+            out.update({
+                "traversal_ms_per_rhs": ph["kernel"]["ms"] / max(1, ph["kernel"]["count"]),
+                "tree_build_ms_per_rhs": build_ms,
+                "build_phases_ms_per_rhs": {k: ph[k]["ms"] / max(1, ph[k]["count"])
+                                            for k in ("bbox_keys", "sort", "topology", "aggregate")},
+                # 16 FP32 per interaction + 12 per visited node
+                "traversal_fp32_issue_frac": ((16.0 * (d + a_) + 12.0 * v) / trav_s) / mb["ffma"]
+                if trav_s > 0 else None,
+                # algorithmic bytes of the build kernels, FP32 (per point)
+                "build_gbs_algorithmic": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9,
+                "build_hbm_frac": BUILD_BYTES_PER_POINT * N / (build_ms * 1e-3) / 1e9
+                / float(mp.get("hbm_gbs", 6540.0)),
+                "kernel": "k_bh_ws<float> (independent walks); tree: radix sort + LCP topology",
+            })
+        return out
 
-    # ---- Barnes-Hut across ranks: target shards (Morton-ordered at set_shard),
-    # one in-place all-gather per stage; device time = max over ranks ----------
-    def bh_sharded():
-        cfg_bh = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=BARNES_HUT,
-                                integrator=RK4, precision=F32)
-        fb = gs.flow(cfg_bh, N)
-        fb.upload(q0, p0)
-        sb = torch.cuda.ExternalStream(fb.stream())
-        drb = ShardedFlow(fb, 4, stream=sb)
-        drb.step(max(1, args.warmup))
-        fb.sync()
-        # time the first kb steps of the config-4 flow (as on one GPU): re-upload,
-        # re-shard (Morton order again, fresh record view)
-        fb.upload(q0, p0)
-        drb = ShardedFlow(fb, 4, stream=sb)
-        barrier()
-        kb = max(1, args.steps)
-        with torch.cuda.stream(sb):
-            flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(sb)
-        drb.step(kb)
-        e1.record(sb)
-        torch.cuda.synchronize()
-        barrier()
-        fb.sync()
-        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        bms = float(t.item())
-        line["bh"] = {"value": kb / (bms / 1e3), "unit": "flow steps/s", "ms_per_step": bms / kb,
-                      "n2_equivalent_pairs_per_s": 4.0 * N * float(N) * kb / (bms / 1e3),
-                      "parallelism": f"target-shard x{world} (each rank rebuilds the tree)"}
-        del drb, fb
-
-    if not args.no_bh and world > 1:
+    if not args.no_bh:
         try:  # an auxiliary line: never let it take the headline down
-            bh_sharded()
+            line["bh"] = bh_line()
         except Exception as exc:  # noqa: BLE001
             line["bh"] = {"error": f"{type(exc).__name__}: {exc}"}
 
-    # ---- exact with the FP32 underflow cutoff (GS_FLAG_EXACT_CUTOFF, opt-in) ------
-    # The same exact sum over Morton-ordered points, skipping tile pairs whose
-    # Gaussian weights are all exactly 0 in FP32 (bit-identical to evaluating
-    # them in that order; tests/test_gpu_exact.py). Not the headline: the
-    # headline `value` evaluates all N^2 pairs.
+    # ---- exact with the FP32 underflow cutoff (opt-in), the same trajectory ----
     if not args.no_extra and world == 1:
         cfg_c = ShootingConfig(sigma=SIGMA, timesteps=T_STEPS, backend=EXACT, integrator=RK4,
                                precision=F32, exact_cutoff=True)
         fc = gs.flow(cfg_c, N)
         sc = torch.cuda.ExternalStream(fc.stream())
         fc.upload(q0, p0)
-        fc.advance(max(1, args.warmup))
+        fc.advance(T_STEPS)  # warm-up trajectory
         fc.sync()
-        fc.upload(q0, p0)  # time the first steps of the config-4 flow
+        fc.upload(q0, p0)
         fc.sync()
-        kc_ = max(1, args.steps)
         with torch.cuda.stream(sc):
             flush.zero_()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0, c1 = ev_pair()
         c0.record(sc)
-        fc.advance(kc_)
+        fc.advance(T_STEPS)
         c1.record(sc)
         torch.cuda.synchronize()
         fc.sync()
         cms = c0.elapsed_time(c1)
         line["exact_cutoff"] = {
-            "value": kc_ / (cms / 1e3), "unit": "flow steps/s", "ms_per_step": cms / kc_,
-            "speedup_vs_all_pairs": (kc_ / (cms / 1e3)) / value,
+            "value": T_STEPS / (cms / 1e3), "unit": "flow steps/s", "ms_per_step": cms / T_STEPS,
+            "timed": f"one full trajectory: {T_STEPS} RK4 steps from q0",
+            "speedup_vs_all_pairs": (T_STEPS / (cms / 1e3)) / value,
             "note": "exact FP32 sum in Morton order; (target group, source tile) pairs beyond "
                     "the FP32 underflow radius of 2^-r'^2 skipped (their terms are exactly 0)",
         }
         del fc
 
-    # ---- exact FP64 and N = 100k FP32 lines (same workload family) -------------
+    # ---- adjoint: config 3's evaluate() (forward + kept trees + adjoint) ------
+    if not args.no_extra and world == 1:
+        n3 = 50_000
+        q3 = tube(n3, seed=3)
+        p_true = smooth_momenta(q3, 0.01, 4)  # well-conditioned amplitude
+        tgt, _, _, _ = gs.shoot_forward(q3, p_true, ShootingConfig(sigma=5.0, timesteps=20),
+                                        keep_trajectory=False)
+        p3 = np.full_like(q3, 1e-3)
+        adj = {"workload": f"config3 evaluate(): N={n3} tube, sigma 5, lambda 100, T=20 Euler, "
+                           "FP32, forward flow + kept trees + adjoint, host buffers in/out"}
+        for backend, name in ((EXACT, "exact"), (BARNES_HUT, "bh")):
+            c3 = ShootingConfig(sigma=5.0, lambda_=100.0, timesteps=20, backend=backend, precision=F32)
+            gs.evaluate(q3, p3, tgt, c3)  # warm
+            gs.profile(True)
+            reps = 3
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                evr = gs.evaluate(q3, p3, tgt, c3)
+            dt = (time.perf_counter() - t0) / reps
+            ph = gs.profile_phases()
+            gs.profile(False)
+            rec = {"evaluate_s": dt, "evaluations_per_s": 1.0 / dt,
+                   "forward_ms": evr.stats["forward_ms"], "backward_ms": evr.stats["backward_ms"]}
+            ak = ph["adjoint_kernel"]
+            if backend == EXACT and ak["count"]:
+                h_ms = ak["ms"] / ak["count"]
+                pps = float(n3) * n3 / (h_ms * 1e-3)
+                hpeak = mb["ffma"] / HESS_FP32_PER_PAIR
+                rec["roofline"] = {
+                    "bound": "fp32-fma-pipe", "kernel": "k_hess_f32x2<4,128> (packed FFMA2)",
+                    "achieved": pps / 1e9, "peak": hpeak / 1e9, "unit": "Gpair/s",
+                    "frac": pps / hpeak, "kernel_ms_avg": h_ms,
+                    "algorithmic_per_launch": f"{float(n3) * n3:.3e} ordered pairs x "
+                                              f"{HESS_FP32_PER_PAIR} FP32 + 1 MUFU",
+                    "peak_source": "live FFMA microbenchmark / 37 FP32 per pair"}
+            elif ak["count"]:
+                rec["adjoint_walk_ms_avg"] = ak["ms"] / ak["count"]
+                rec["interactions"] = (evr.stats["direct_interactions"]
+                                       + evr.stats["approximated_interactions"])
+            adj[name] = rec
+        line["adjoint"] = adj
+
+    # ---- exact FP64 at N = 1M (one RK4 step) and N = 100k FP32 ----------------
     if not args.no_extra and world == 1:
         def timed_flow(n, prec, integ, steps):
             qq, pp = workload(n)
@@ -411,29 +496,25 @@ def run_ours(args):
             fl.advance(1)
             fl.sync()
             fl.profile(True)
-            t0_, t1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0_, t1_ = ev_pair()
             t0_.record(s_)
             fl.advance(steps)
             t1_.record(s_)
             torch.cuda.synchronize()
             fl.sync()
             pr = fl.profile_read()
+            fl.profile(False)
             return t0_.elapsed_time(t1_), pr
-        from paper_1907_04834_b200 import EULER, F64
-        n64 = 200_000
-        ms64, pr64 = timed_flow(n64, F64, EULER, 2)
-        dfma = C.c_double()
-        lib.gs_microbench(local, 2, C.byref(dfma))
+        ms64, pr64 = timed_flow(N, F64, RK4, 1)
         k64 = pr64["kernel_ms"] / max(1, pr64["kernel_launches"])
-        pps64 = float(n64) * n64 / (k64 * 1e-3)
+        pps64 = float(N) * N / (k64 * 1e-3)
         line["fp64"] = {
-            "workload": f"exact FP64 RHS, N={n64}, Euler (config-4 distribution)",
-            "pair_interactions_per_s": pps64, "kernel_ms": k64,
-            "steps_per_s": 2 / (ms64 / 1e3),
-            "peak_dfma_lane_per_s": dfma.value,
-            "frac_16dp_basis": pps64 * 16.0 / dfma.value if dfma.value else None,
+            "workload": f"exact FP64, N={N}, one RK4 step (4 RHS), config-4 distribution",
+            "value": 1.0 / (ms64 / 1e3), "unit": "flow steps/s", "pair_interactions_per_s": pps64,
+            "kernel_ms": k64, "peak_dfma_lane_per_s": mb["dfma"],
+            "frac_16dp_basis": pps64 * 16.0 / mb["dfma"] if mb["dfma"] else None,
             # + the 10-DP table-driven exp of the FP64 kernels (csrc/gs_exp.cuh)
-            "frac_26dp_basis_incl_exp": pps64 * 26.0 / dfma.value if dfma.value else None,
+            "frac_26dp_basis_incl_exp": pps64 * 26.0 / mb["dfma"] if mb["dfma"] else None,
         }
         ms1, pr1 = timed_flow(100_000, F32, RK4, 3)
         line["n100k"] = {
@@ -441,20 +522,6 @@ def run_ours(args):
             "pair_interactions_per_s": 4.0 * 1e10 * 3 / (ms1 / 1e3),
             "frac_of_ffma_peak": (4.0 * 1e10 * 3 / (ms1 / 1e3)) / peak / 1e9,
         }
-
-    # ---- end to end through the public C-ABI call, host buffers ----------------
-    if world == 1:
-        pin_q = torch.empty((N, 3), dtype=torch.float64, pin_memory=True).numpy()
-        pin_p = torch.empty((N, 3), dtype=torch.float64, pin_memory=True).numpy()
-        pin_q[:] = q0
-        pin_p[:] = p0
-        t0 = time.perf_counter()
-        fq, fp, energy, _ = gs.shoot_forward(pin_q, pin_p, cfg, keep_trajectory=False)
-        dt = time.perf_counter() - t0
-        line["e2e"] = {"value": T_STEPS / dt, "unit": "flow steps/s",
-                       "h2d_bytes_per_step": 2 * N * 24 // T_STEPS,
-                       "d2h_bytes_per_step": 2 * N * 24 // T_STEPS,
-                       "call": f"gs_shoot_forward (10 RK4 steps, final state only) x1, {dt:.2f} s"}
 
     # ---- CPU baseline: the reference's own exact RHS on the host cores ---------
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -465,7 +532,9 @@ def run_ours(args):
             "kind": kind, "pair_interactions_per_s": rate,
             "sample": f"{used} concurrent reference hamiltonian_gradients calls at N={args.cpu_sample} "
                       f"(FP64, serial by construction per call), extrapolated to N={N} by N^2 x 4 RHS/step"}
-        if "bh" in line and kind == "reference":
+        if "fp64" in line:
+            line["fp64"]["vs_cpu_baseline_fp64"] = line["fp64"]["pair_interactions_per_s"] / rate
+        if "bh" in line and "error" not in line["bh"] and kind == "reference":
             # the reference's Barnes-Hut path on the same flow: one Euler step of
             # shoot_forward (serial octree build + one parallel_for RHS,
             # bh_kernel.cpp:193-210) at the full N; an RK4 step is 4 of them
@@ -491,13 +560,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1_000_000)
-    ap.add_argument("--cpu-sample", type=int, default=8192)
-    ap.add_argument("--no-extra", action="store_true", help="skip the FP64 / N=100k lines")
+    ap.add_argument("--cpu-sample", type=int, default=20_000)
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the cutoff / adjoint / FP64 / N=100k lines")
     ap.add_argument("--no-bh", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         run_ours(args)
 

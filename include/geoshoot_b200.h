@@ -319,6 +319,13 @@ gs_status gs_flow_profile_read(gs_flow* flow, double* kernel_ms, int64_t* kernel
  * aggregates); ms[c] summed, counts[c] pairs recorded. */
 gs_status gs_flow_profile_phases(gs_flow* flow, double* ms, int64_t* counts, int32_t channels);
 
+/* Event timing inside the context's shooting calls (gs_shoot_forward,
+ * gs_evaluate, gs_optimize): channels as gs_flow_profile_phases, plus
+ * 6 = the adjoint pass's dominant kernel (Hessian products / Barnes-Hut
+ * Hessian walk). gs_profile_phases drains: ms[c] summed, counts[c] pairs. */
+gs_status gs_profile(gs_ctx* ctx, int32_t enable);
+gs_status gs_profile_phases(gs_ctx* ctx, double* ms, int64_t* counts, int32_t channels);
+
 /* Sharded stage API (one rank = one flow): */
 gs_status gs_flow_set_shard(gs_flow* flow, int64_t shard_begin, int64_t shard_count);
 /* Device pointer and byte size of the packed per-point source records

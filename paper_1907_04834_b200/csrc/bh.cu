@@ -1041,7 +1041,9 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
   q.n_tgt = (int)nt;
   q.part = w.part.ptr;
   q.totals = w.stats.as<unsigned long long>();
+  kt_mark(6, st);
   GS_TRY_INT(bh_traverse(dev, prec, *t, cfg.sigma, cfg.threshold_multiplier * cfg.sigma, q, st));
+  kt_mark(6, st);
   e.S = K;
   e.part = w.part.ptr;
   GS_TRY_INT(bwd_epilogue(prec, e, st));

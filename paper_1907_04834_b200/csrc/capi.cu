@@ -83,6 +83,7 @@ struct gs_ctx {
   std::vector<gs_ctx*> subs;
   bool peer_stores = true;  // epilogues store into peers' buffers (else peer copies)
   std::vector<cudaEvent_t> ev;  // per-shard stage-completion events
+  KTimer* timer = nullptr;      // gs_profile: event timing inside shooting calls
 };
 
 struct gs_flow {
@@ -216,6 +217,7 @@ void gs_destroy(gs_ctx* ctx) {
   cudaSetDevice(ctx->dev.id);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
+  delete ctx->timer;
   delete ctx;
 }
 
@@ -378,6 +380,16 @@ namespace {
 
 int flow_stages(const gs_flow* f) { return f->cfg.integrator == GS_RK4 ? 4 : 1; }
 
+// Makes t (if any) the thread's kernel timer for a scope (gs_flow_profile,
+// gs_profile); a null t keeps the enclosing one.
+struct TimerInstall {
+  KTimer* prev;
+  explicit TimerInstall(KTimer* t) : prev(g_ktimer) {
+    if (t) g_ktimer = t;
+  }
+  ~TimerInstall() { g_ktimer = prev; }
+};
+
 // One integrator stage for the shard: RHS (exact or Barnes-Hut) + epilogue.
 // rec_in (default: the flow's records) holds all n source records; the
 // shard's updated records go to rec_out (default: in place).
@@ -407,11 +419,7 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
     e.dhdp_out = f->dhdp0.as<double>();
   }
   int blocks = 0;
-  struct Install {
-    KTimer* prev;
-    explicit Install(KTimer* t) : prev(g_ktimer) { g_ktimer = t; }
-    ~Install() { g_ktimer = prev; }
-  } install(f->timer);
+  TimerInstall install(f->timer);
   const bool sorted = f->cfg.backend == GS_EXACT && f->prec == kF32 &&
                       (f->cfg.flags & (GS_FLAG_EXACT_CUTOFF | GS_FLAG_EXACT_MORTON)) &&
                       f->shard_begin == 0 && f->shard_count == f->n;
@@ -771,6 +779,23 @@ gs_status gs_flow_profile_phases(gs_flow* f, double* ms, int64_t* counts, int32_
   return GS_OK;
 }
 
+gs_status gs_profile(gs_ctx* c, int32_t enable) {
+  if (!c) return bad_arg("null context");
+  if (enable && !c->timer) c->timer = new KTimer;
+  if (!enable) {
+    delete c->timer;
+    c->timer = nullptr;
+  }
+  return GS_OK;
+}
+
+gs_status gs_profile_phases(gs_ctx* c, double* ms, int64_t* counts, int32_t channels) {
+  if (!c || !c->timer) return bad_arg("profiling not enabled");
+  GS_CUDA_OK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < channels && k < KTimer::kChannels; ++k) ms[k] = c->timer->drain(k, counts + k);
+  return GS_OK;
+}
+
 gs_status gs_flow_stats(gs_flow* f, gs_stats* out) {
   if (!f || !out) return bad_arg("null argument");
   if (!f->subs.empty()) return (gs_status)multi_flow_stats(f, out);
@@ -920,6 +945,7 @@ gs_status gs_shoot_forward(gs_ctx* c, const gs_config* cfg, int64_t n, const dou
                            const double* p0, double* traj_q, double* traj_p, double* final_q,
                            double* final_p, double* energy_out, gs_stats* stats) {
   if (!c || !cfg || !q0 || !p0) return bad_arg("null argument");
+  TimerInstall install(c->timer);
   GS_TRY(gs_validate_config(cfg, nullptr));
   GS_TRY(check_n(n));
   gs_flow* f = scratch_flow(c);
@@ -1016,8 +1042,10 @@ int backward_step(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts&
   e.adj = adj_in;
   if (cfg->backend == GS_EXACT) {
     GS_TRY(part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+    kt_mark(6, st);
     const int S = hess_partials(c->dev, prec, rk, adj_in, (int)n, (int)tb, (int)nt, kc, part.ptr,
                                 kMaxChunks, st, plan_tgt);
+    kt_mark(6, st);
     if (S < 0) return GS_INTERNAL;
     GS_CUDA_OK(cudaGetLastError());
     e.S = S;
@@ -1073,6 +1101,7 @@ gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* 
                       const double* p0, const double* target, gs_report* report,
                       double* grad_out, gs_stats* stats) {
   if (!c || !cfg || !q0 || !p0 || !target) return bad_arg("null argument");
+  TimerInstall install(c->timer);
   if (cfg->integrator != GS_EULER) return bad_arg("evaluate: the adjoint is the transpose of Euler");
   GS_TRY(gs_validate_config(cfg, nullptr));
   GS_TRY(check_n(n));

@@ -215,6 +215,19 @@ class Geoshoot:
     def peer_stores(self) -> bool:
         return bool(self.lib.gs_ctx_peer_stores(self.ctx))
 
+    PHASES = ("kernel", "build", "bbox_keys", "sort", "topology", "aggregate", "adjoint_kernel")
+
+    def profile(self, enable: bool = True):
+        """Event timing of the dominant kernels inside shooting calls (gs_profile)."""
+        self.check(self.lib.gs_profile(self.ctx, 1 if enable else 0))
+
+    def profile_phases(self) -> dict:
+        k = len(self.PHASES)
+        ms = np.zeros(k)
+        cnt = (C.c_int64 * k)()
+        self.check(self.lib.gs_profile_phases(self.ctx, _p(ms), cnt, k))
+        return {name: {"ms": float(ms[i]), "count": int(cnt[i])} for i, name in enumerate(self.PHASES)}
+
     def close(self):
         if getattr(self, "ctx", None):
             self.lib.gs_destroy(self.ctx)

@@ -5,8 +5,14 @@ owns targets [r*N/G, (r+1)*N/G), computes their RHS against all N sources and
 updates its own records in the fused stage epilogue; then the ranks all-gather
 the updated shards (torch.distributed, NCCL over NVLink/NVSwitch on B200s,
 gloo in the CPU tests). The all-gather is in place: every rank's record buffer
-is the gather output and its own shard is the input slice. Per-target
-arithmetic does not depend on G, so results are bitwise identical to 1 GPU.
+is the gather output and its own shard is the input slice. An exact shard
+launches under the full problem's plan (gs_flow_set_shard), so its per-target
+sums -- and the flow -- are bit-identical to one GPU's; Barnes-Hut shards have
+the reference's interaction sets, equal to summation-order rounding.
+
+(Inside ONE process, gs_create_multi / Geoshoot(devices=[...]) shards across
+devices without torch.distributed: the exchange is fused into the stage
+epilogues as P2P stores.)
 """
 from __future__ import annotations
 
@@ -116,7 +122,12 @@ class ShardedFlow:
         self.world = dist.get_world_size(group)
         self.begin, self.count = shard_range(flow.n, self.rank, self.world)
         flow.set_shard(self.begin, self.count)
+        if stream is None and hasattr(flow, "stream") and torch.cuda.is_available():
+            # the flow launches on its own (non-blocking) stream: the gather must
+            # be ordered after the stage epilogue and before the next stage
+            stream = torch.cuda.ExternalStream(flow.stream())
         self.stream = stream
+        self.launches = 0  # kernels of this rank's stages (gs_flow_last_launches)
         self._rec = flow.records() if hasattr(flow, "records") else records_view(flow)
         per = self._rec.numel() // flow.n
         self._mine = self._rec[self.begin * per:(self.begin + self.count) * per]
@@ -136,4 +147,6 @@ class ShardedFlow:
         for _ in range(steps):
             for s in range(self.stages):
                 self.flow.stage(s)
+                if hasattr(self.flow, "last_launches"):
+                    self.launches += self.flow.last_launches()
                 self._gather()
