@@ -30,7 +30,8 @@ struct DevTree {
   DBuf meta;            // int4 {skip, begin, end, leaf | level << 8}
   DBuf parent;          // i32
   DBuf nchild;          // i32
-  DBuf counter;         // i32 bottom-up arrival counters
+  DBuf outer;           // i32 outer (chunk-spanning) nodes + count (tree.cu aggregates)
+  DBuf parts;           // per-chunk total / head / tail partial aggregates
   DBuf lo, hi;          // V4<R> tight AABB (unscaled)
   DBuf cen, mom;        // V4<R> centroid (scaled in FP32) + count / momentum sum + count bits
   DBuf nrec;            // [cap][4] V4<R> traversal record {centroid|point, code} {momentum|p, begin} {lo, count} {hi}

@@ -528,10 +528,10 @@ uint64_t flow_sig(const gs_flow* f) {
     mix(*b);
   const DevTree& t = f->bh.cur;
   for (const DBuf* b : {&t.key_hi, &t.key_lo, &t.perm, &t.skey_hi, &t.skey_lo, &t.lcp, &t.first,
-                        &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.counter, &t.lo,
+                        &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.lo,
                         &t.hi, &t.cen, &t.mom, &t.nrec, &t.nadj, &t.psum, &t.msum,
                         &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist,
-                        &t.scan_tmp, &t.scal})
+                        &t.scan_tmp, &t.scal, &t.outer, &t.parts, &t.sm_ctr})
     mix(*b);
   return h;
 }

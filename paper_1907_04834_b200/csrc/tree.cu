@@ -451,15 +451,6 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
   }
 }
 
-__global__ void k_nchild(const int4* meta, const int* mp, int* nchild) {
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= *mp) return;
-  const int4 mi = meta[i];
-  int c = 0;
-  if (!(mi.w & 1))
-    for (int ch = (int)i + 1; ch < mi.x && c < 8; ch = max(ch + 1, meta[ch].x)) ++c;
-  nchild[i] = c;
-}
 
 // ------------------------------------------------------------ aggregates ---
 // Forward: tight AABB + sums of q and p; backward: sums of alpha and beta.
@@ -494,6 +485,34 @@ __global__ void k_gather_adj(const V4<R>* adj, const int* perm, int64_t n, V4<R>
   st4(sadj + 2 * t + 1, ld4(adj + 2 * i + 1));
 }
 
+// ------------------------------------------------------------ aggregates ---
+// Node aggregates (tight AABB + FP64 sums of q and p: mode 0; FP64 sums of
+// alpha and beta: mode 1) and the traversal records, after k_children. The
+// leaf order is cut into chunks of C points (1024 FP32 / 512 FP64), one CTA
+// each (k_agg_chunk). The CTA gathers its chunk's points (by perm, writing the
+// leaf-order copies srec / squ or sadj on the way -- the build's gather fused
+// in) into shared memory. The nodes that start in the chunk are a contiguous
+// pre-order range [first[c0], first[c1]); those lying inside the chunk are
+// summed from shared memory in range order (small ones by a thread, larger by
+// a warp) and their records written. A node spanning chunks ("outer") is
+// split at the chunk boundaries: its TAIL in its first chunk, whole chunks,
+// its HEAD in its last chunk. Per level at most one outer node starts in a
+// chunk and at most one (the one containing the chunk's first point) ends in
+// it, so the CTA computes, from shared memory, its chunk's total and the tail
+// and head ranges of every level (heads found from the lcp array: the level-l
+// node containing the chunk's first point ends at the first position whose
+// lcp with the next is < l). k_agg_outer then sums each outer node as tail +
+// chunk totals + head, in chunk order. Every reduction order is fixed
+// (deterministic), every point is read from HBM once per aggregate, and no
+// kernel waits on another's partial results.
+template <typename R> constexpr int chunk_of() { return sizeof(R) == 4 ? 1024 : 512; }
+constexpr int kSmallNode = 16;  // inside nodes above this are summed by a warp
+constexpr int kLevels = 33;     // levels 0..32 (32: depth-32 buckets)
+constexpr int kPartPerChunk = 1 + 2 * kLevels;  // total, head[33], tail[33]
+
+__device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
+__device__ __forceinline__ double ival(double, int v) { return (double)v; }
+
 __device__ __forceinline__ double4 ldcg4(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   const double2 a = __ldcg(q), b = __ldcg(q + 1);
@@ -501,109 +520,321 @@ __device__ __forceinline__ double4 ldcg4(const double4* p) {
 }
 __device__ __forceinline__ float4 ldcg4(const float4* p) { return __ldcg(p); }
 
-// mode 0: forward (lo, hi, psum, msum from squ/srec p); mode 1: adjoint sums
-// Node aggregates (tight box, FP64 position / momentum sums; mode 1: alpha /
-// beta sums). One thread per node: a leaf, or a node of at most kAggDirect
-// points, sums its own leaf-order range directly (no dependencies, full
-// warps); larger internal nodes are completed bottom-up -- each small node whose parent is large
-// arrives at the parent's counter, and the last arrival computes the parent
-// from its children and climbs on. A single-point leaf stores nothing: its
-// sums are its point, read by whoever needs them (k_fill_leaves for
-// downloads). Summation order is fixed by the tree (deterministic).
-constexpr int kAggDirect = 16;
+__device__ __forceinline__ bool is_single(const int4& mi) { return (mi.w & 1) && mi.y == mi.z; }
+
+// per node: child count (the twig flag of the traversal record)
+__global__ void __launch_bounds__(kNT) k_children(const int4* meta, const int* mp, int* nchild) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= *mp) return;
+  const int4 mi = meta[i];
+  int c = 0;
+  if (!(mi.w & 1))
+    for (int ch = (int)i + 1; ch < mi.x && c < 8; ++c) ch = max(ch + 1, meta[ch].x);
+  nchild[i] = c;
+}
 
 template <typename R>
-__global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64_t n,
-                                                   const int* first, const int4* meta,
-                                                   const int* parent, const int* nchild,
-                                                   int* counter, const V4<R>* squ,
-                                                   const V4<R>* srec, const V4<R>* sadj,
-                                                   V4<R>* lo, V4<R>* hi, double4* s0, double4* s1,
-                                                   int64_t cap) {
-  (void)L;
-  const int m = first[n];
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (m > cap || i >= m) return;
-  const int4 mi = meta[i];
+struct AggArgs {
+  const int4* meta;
+  const int* nchild;
+  const int* first;  // [n + 1] pre-order index of the first node starting at each position
+  const int* lcp;    // [n - 1] common digits of leaf-order neighbours
+  const int* perm;
+  int64_t n;
+  const V4<R>* rec;  // by point index: records (q, p) in mode 0, adjoints (alpha, beta) in mode 1
+  V4<R>*srec, *squ, *sadj;  // leaf-order copies written on the way
+  V4<R>*lo, *hi;
+  double4 *s0, *s1;
+  V4<R>*nrec, *nadj;
+  // per chunk: total, head[level], tail[level] partial aggregates
+  double4 *ps0, *ps1;
+  V4<R>*plo, *phi;
+  int* outer;      // outer nodes (listed by the chunk they start in)
+  int* outer_cnt;
+  double kap, c0x, c0y, c0z;
+  int scaled;
+};
+
+// FP32 interaction coordinates, same rounding as the all-pairs path
+template <typename R>
+__device__ __forceinline__ V4<R> scaled_q(const AggArgs<R>& a, const V4<R>& q) {
+  if (!a.scaled) return mk4<R>(q.x, q.y, q.z);
+  const float kf = (float)a.kap;
+  return mk4<R>((R)fmaf(kf, (float)q.x, -(float)(a.kap * a.c0x)),
+                (R)fmaf(kf, (float)q.y, -(float)(a.kap * a.c0y)),
+                (R)fmaf(kf, (float)q.z, -(float)(a.kap * a.c0z)));
+}
+
+struct Sums {
+  double a[3], b[3];
+};
+template <typename R>
+struct Box {
+  R l[3], h[3];
+};
+
+template <typename R>
+__device__ __forceinline__ void box_init(Box<R>& x) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    x.l[k] = R(INFINITY);
+    x.h[k] = -R(INFINITY);
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ void add_point(Sums& s, Box<R>& x, const V4<R>& u, const V4<R>& v, bool box) {
+  s.a[0] += u.x; s.a[1] += u.y; s.a[2] += u.z;
+  s.b[0] += v.x; s.b[1] += v.y; s.b[2] += v.z;
+  if (box) {
+    x.l[0] = min(x.l[0], u.x); x.l[1] = min(x.l[1], u.y); x.l[2] = min(x.l[2], u.z);
+    x.h[0] = max(x.h[0], u.x); x.h[1] = max(x.h[1], u.y); x.h[2] = max(x.h[2], u.z);
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ void add_part(Sums& s, Box<R>& x, const double4& d0, const double4& d1,
+                                         const V4<R>& l, const V4<R>& h) {
+  s.a[0] += d0.x; s.a[1] += d0.y; s.a[2] += d0.z;
+  s.b[0] += d1.x; s.b[1] += d1.y; s.b[2] += d1.z;
+  x.l[0] = min(x.l[0], l.x); x.l[1] = min(x.l[1], l.y); x.l[2] = min(x.l[2], l.z);
+  x.h[0] = max(x.h[0], h.x); x.h[1] = max(x.h[1], h.y); x.h[2] = max(x.h[2], h.z);
+}
+
+// The traversal record of node i (mode 0) -- {centroid | point, code}
+// {momentum sum | p, begin} {lo, count} {hi}, code = skip | single << 31 |
+// bucket << 30 | twig << 29 (skip < 2^29) -- or its adjoint unit (mode 1)
+// {alpha sum, beta mean}; plus the FP64 sums and the box of a non-single node.
+// u, v: a single node's own point (q unscaled, p) / (alpha, beta).
+template <typename R, int MODE>
+__device__ void write_node(const AggArgs<R>& a, int i, const int4& mi, int nch, const Sums& s,
+                           const Box<R>& x, const V4<R>& u, const V4<R>& v) {
   const int cnt = mi.z - mi.y + 1;
+  const bool single = is_single(mi);
+  if (MODE == 1) {
+    if (single) {
+      st4(a.nadj + 2 * i, mk4<R>(u.x, u.y, u.z));
+      st4(a.nadj + 2 * i + 1, mk4<R>(v.x, v.y, v.z));
+      return;
+    }
+    const double inv = 1.0 / cnt;
+    st4(a.nadj + 2 * i, mk4<R>(R(s.a[0]), R(s.a[1]), R(s.a[2])));
+    // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
+    st4(a.nadj + 2 * i + 1, mk4<R>(R(__dmul_rn(inv, s.b[0])), R(__dmul_rn(inv, s.b[1])),
+                                   R(__dmul_rn(inv, s.b[2]))));
+    a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
+    a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    return;
+  }
   const bool leaf = mi.w & 1;
-  if (cnt > kAggDirect && !leaf) return;  // completed by the climb below (leaves: always here)
-  const bool single = leaf && cnt == 1;
-  if (!single) {
-    double4 A = make_double4(0, 0, 0, 0), B = A;
-    V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
-    for (int t = mi.y; t <= mi.z; ++t) {
-      if (mode == 0) {
-        const V4<R> q = ld4(squ + t), p = ld4(srec + 2 * t + 1);
-        l.x = min(l.x, q.x); l.y = min(l.y, q.y); l.z = min(l.z, q.z);
-        h.x = max(h.x, q.x); h.y = max(h.y, q.y); h.z = max(h.z, q.z);
-        A.x += q.x; A.y += q.y; A.z += q.z;
-        B.x += p.x; B.y += p.y; B.z += p.z;
-      } else {
-        const V4<R> al = ld4(sadj + 2 * t), be = ld4(sadj + 2 * t + 1);
-        A.x += al.x; A.y += al.y; A.z += al.z;
-        B.x += be.x; B.y += be.y; B.z += be.z;
+  // twig: an internal node whose children are all leaves (subtree = itself +
+  // its children); opening it makes every point of it direct, no child gated
+  const bool twig = !leaf && mi.x - i - 1 == nch;
+  const int code = mi.x | (single ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0) |
+                   (twig ? 0x20000000 : 0);
+  V4<R> ua, ub;
+  if (single) {  // a single-point leaf is always direct: its record holds the point itself
+    ua = scaled_q(a, u);
+    ub = mk4<R>(v.x, v.y, v.z);
+  } else {
+    const double inv = 1.0 / cnt;
+    // centroid = position_sum * (1 / count) (octree.hpp:35)
+    ua = scaled_q(a, mk4<R>(R(__dmul_rn(s.a[0], inv)), R(__dmul_rn(s.a[1], inv)),
+                            R(__dmul_rn(s.a[2], inv))));
+    ub = mk4<R>(R(s.b[0]), R(s.b[1]), R(s.b[2]));
+    const V4<R> l = mk4<R>(x.l[0], x.l[1], x.l[2]), h = mk4<R>(x.h[0], x.h[1], x.h[2]);
+    st4(a.lo + i, l);
+    st4(a.hi + i, h);
+    a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
+    a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    st4(a.nrec + 4 * i + 2, mk4<R>(l.x, l.y, l.z, ival(R(0), cnt)));
+    st4(a.nrec + 4 * i + 3, h);
+  }
+  ua.w = ival(R(0), code);
+  ub.w = ival(R(0), mi.y);
+  st4(a.nrec + 4 * i, ua);
+  st4(a.nrec + 4 * i + 1, ub);
+}
+
+// sum over chunk-local positions [b0, b1] of the staged points, by a warp
+// (lane-strided + a fixed butterfly; every lane gets the result)
+template <typename R>
+__device__ __forceinline__ void warp_range(const V4<R>* su, const V4<R>* sv, int b0, int b1, int lane,
+                                           bool box, Sums& s, Box<R>& x) {
+  s = Sums{};
+  box_init(x);
+  for (int t = b0 + lane; t <= b1; t += 32) add_point(s, x, su[t], sv[t], box);
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      s.a[c] += __shfl_xor_sync(0xffffffffu, s.a[c], o);
+      s.b[c] += __shfl_xor_sync(0xffffffffu, s.b[c], o);
+      x.l[c] = min(x.l[c], __shfl_xor_sync(0xffffffffu, x.l[c], o));
+      x.h[c] = max(x.h[c], __shfl_xor_sync(0xffffffffu, x.h[c], o));
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ bool is_outer(const int4& mi) {
+  return mi.y / chunk_of<R>() != mi.z / chunk_of<R>();
+}
+
+// work items of a chunk's warps: a big inside node, the chunk total, a head
+// or a tail range
+enum { kItemNode = 0, kItemTotal = 1, kItemHead = 2, kItemTail = 3 };
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
+  constexpr int C = chunk_of<R>();
+  __shared__ V4<R> su[C], sv[C];
+  __shared__ int sl[C + 1];        // sl[1 + j] = lcp(c0 + j, c0 + j + 1); sl[0] = lcp(c0 - 1, c0)
+  __shared__ int pm[C];            // pm[j] = min(sl[1 .. 1 + j]) (prefix minimum)
+  __shared__ int4 items[C / 4];    // {kind, node / level, b0, b1}
+  __shared__ int nitems;
+  const int chunk = blockIdx.x;
+  const int64_t c0 = (int64_t)chunk * C;
+  const int cl = (int)min((int64_t)C, a.n - c0);
+  const int nb = a.first[c0], ne = a.first[c0 + cl];
+  // this thread's first node (the usual case: ~1.5 nodes per position),
+  // loaded alongside the gather
+  const int d0 = nb + (int)threadIdx.x;
+  int4 md0 = make_int4(0, 0, 0, 0);
+  int nch0 = 0;
+  if (d0 < ne) {
+    md0 = a.meta[d0];
+    nch0 = a.nchild[d0];
+  }
+  if (threadIdx.x == 0) nitems = 0;
+  for (int k = threadIdx.x; k < cl; k += kNT) {  // gather the chunk (leaf-order copies on the way)
+    const int64_t t = c0 + k;
+    const int pi = a.perm[t];
+    const V4<R> u = ld4(a.rec + 2 * pi), v = ld4(a.rec + 2 * pi + 1);
+    if (MODE == 0) {
+      st4(a.squ + t, mk4<R>(u.x, u.y, u.z));
+      st4(a.srec + 2 * t, scaled_q(a, u));
+      st4(a.srec + 2 * t + 1, mk4<R>(v.x, v.y, v.z));
+    } else {
+      st4(a.sadj + 2 * t, u);
+      st4(a.sadj + 2 * t + 1, v);
+    }
+    su[k] = u;
+    sv[k] = v;
+  }
+  for (int k = threadIdx.x; k <= cl; k += kNT) {
+    const int64_t t = c0 + k - 1;  // lcp(t, t + 1); none before the first / after the last point
+    sl[k] = (t >= 0 && t + 1 < a.n) ? a.lcp[t] : -1;
+  }
+  __syncthreads();
+  // heads: for every level l <= lcp(c0 - 1, c0) the level-l node holding the
+  // chunk's first point started earlier; it ends at the first chunk position
+  // j with lcp(j, j + 1) < l (a head [0, j]) or covers the whole chunk.
+  // j = first position with pm[j] < l: a prefix minimum + binary search.
+  const int H = min(sl[0], 32);
+  if (H >= 0) {  // (block-uniform)
+    for (int k = threadIdx.x; k < C; k += kNT) pm[k] = k < cl ? sl[1 + k] : -1;
+    __syncthreads();
+    for (int o = 1; o < C; o <<= 1) {  // Hillis-Steele inclusive min-scan
+      int v[C / kNT];
+#pragma unroll
+      for (int r = 0; r < C / kNT; ++r) {
+        const int k = threadIdx.x + r * kNT;
+        v[r] = k >= o ? min(pm[k], pm[k - o]) : pm[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < C / kNT; ++r) pm[threadIdx.x + r * kNT] = v[r];
+      __syncthreads();
+    }
+    for (int l = threadIdx.x; l <= H; l += kNT) {
+      if (pm[cl - 1] >= l) continue;  // covers the whole chunk
+      int lo = 0, hi = cl - 1;         // pm non-increasing: first j with pm[j] < l
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pm[mid] < l) hi = mid;
+        else lo = mid + 1;
+      }
+      items[atomicAdd(&nitems, 1)] = make_int4(kItemHead, l, 0, lo);
+    }
+  }
+  if (threadIdx.x == 0) items[atomicAdd(&nitems, 1)] = make_int4(kItemTotal, 0, 0, cl - 1);
+  // the nodes starting in the chunk
+  for (int d = d0; d < ne; d += kNT) {
+    const int4 md = d == d0 ? md0 : a.meta[d];
+    const int nch = d == d0 ? nch0 : a.nchild[d];
+    if (is_outer<R>(md)) {  // its tail here; completed by k_agg_outer
+      items[atomicAdd(&nitems, 1)] = make_int4(kItemTail, md.w >> 8, md.y - (int)c0, cl - 1);
+      a.outer[atomicAdd(a.outer_cnt, 1)] = d;
+      continue;
+    }
+    const int b0 = md.y - (int)c0, b1 = md.z - (int)c0;
+    if (b1 - b0 + 1 > kSmallNode) {
+      items[atomicAdd(&nitems, 1)] = make_int4(kItemNode, d, b0, b1);
+      continue;
+    }
+    Sums s{};
+    Box<R> x;
+    box_init(x);
+    if (!is_single(md))
+      for (int t = b0; t <= b1; ++t) add_point(s, x, su[t], sv[t], MODE == 0);
+    write_node<R, MODE>(a, d, md, nch, s, x, su[b0], sv[b0]);
+  }
+  __syncthreads();
+  // the warps' items: big inside nodes, the total, heads and tails
+  const int lane = threadIdx.x & 31;
+  for (int k = threadIdx.x >> 5; k < nitems; k += kNT / 32) {
+    const int4 it = items[k];
+    Sums s;
+    Box<R> x;
+    warp_range(su, sv, it.z, it.w, lane, MODE == 0, s, x);
+    if (lane) continue;
+    if (it.x == kItemNode) {
+      const int d = it.y;
+      write_node<R, MODE>(a, d, a.meta[d], a.nchild[d], s, x, su[it.z], sv[it.z]);
+    } else {
+      const size_t slot = (size_t)chunk * kPartPerChunk +
+                          (it.x == kItemTotal ? 0 : (it.x == kItemHead ? 1 : 1 + kLevels) + it.y);
+      a.ps0[slot] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
+      a.ps1[slot] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+      if (MODE == 0) {
+        st4(a.plo + slot, mk4<R>(x.l[0], x.l[1], x.l[2]));
+        st4(a.phi + slot, mk4<R>(x.h[0], x.h[1], x.h[2]));
       }
     }
-    if (mode == 0) { st4(lo + i, l); st4(hi + i, h); }
-    s0[i] = A;
-    s1[i] = B;
   }
-  int node = (int)i;
-  {
-    const int par = parent[node];
-    if (par < 0) return;
-    const int4 mp4 = meta[par];  // (a parent is internal)
-    if (mp4.z - mp4.y + 1 <= kAggDirect) return;  // the parent sums its own range
-  }
-  bool publish = !single;  // a single-point leaf has nothing to publish
-  for (;;) {
-    const int par = parent[node];
-    if (par < 0) return;
-    // release arrival: this child's sums are published before its count. The
-    // last arriver synchronises with every earlier (release) arrival through
-    // an acquire fence before it reads its siblings' sums -- the PTX memory
-    // model's release/acquire pattern, not a reliance on the control
-    // dependency; the sums are then read with L2 loads (ld.cg, never L1).
-    cuda::atomic_ref<int, cuda::thread_scope_device> arrive(counter[par]);
-    const int old = publish ? arrive.fetch_add(1, cuda::memory_order_release)
-                            : arrive.fetch_add(1, cuda::memory_order_relaxed);
-    publish = true;
-    if (old != nchild[par] - 1) return;
-    cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
-    const int end = meta[par].x;
-    double4 A = make_double4(0, 0, 0, 0), B = A;
-    V4<R> l = mk4<R>(R(INFINITY), R(INFINITY), R(INFINITY)), h = mk4<R>(-R(INFINITY), -R(INFINITY), -R(INFINITY));
-    for (int ch = par + 1; ch < end;) {
-      const int4 mc = meta[ch];
-      if ((mc.w & 1) && mc.y == mc.z) {  // single-point leaf: its point (same values as stored sums)
-        if (mode == 0) {
-          const V4<R> q = ld4(squ + mc.y), p = ld4(srec + 2 * mc.y + 1);
-          A.x += q.x; A.y += q.y; A.z += q.z;
-          B.x += p.x; B.y += p.y; B.z += p.z;
-          l.x = min(l.x, q.x); l.y = min(l.y, q.y); l.z = min(l.z, q.z);
-          h.x = max(h.x, q.x); h.y = max(h.y, q.y); h.z = max(h.z, q.z);
-        } else {
-          const V4<R> al = ld4(sadj + 2 * mc.y), be = ld4(sadj + 2 * mc.y + 1);
-          A.x += al.x; A.y += al.y; A.z += al.z;
-          B.x += be.x; B.y += be.y; B.z += be.z;
-        }
-      } else {
-        const double4 a0 = ldcg4(s0 + ch), a1 = ldcg4(s1 + ch);
-        A.x += a0.x; A.y += a0.y; A.z += a0.z;
-        B.x += a1.x; B.y += a1.y; B.z += a1.z;
-        if (mode == 0) {
-          const V4<R> cl = ldcg4(lo + ch), chh = ldcg4(hi + ch);
-          l.x = min(l.x, cl.x); l.y = min(l.y, cl.y); l.z = min(l.z, cl.z);
-          h.x = max(h.x, chh.x); h.y = max(h.y, chh.y); h.z = max(h.z, chh.z);
-        }
-      }
-      ch = max(ch + 1, mc.x);
+}
+
+// Outer nodes: tail (first chunk) + whole chunks + head (last chunk). One
+// warp per node: lanes take the chunk partials strided, a fixed butterfly
+// combines them (a fixed order: deterministic).
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
+  constexpr int C = chunk_of<R>();
+  const int c = *a.outer_cnt;
+  const int lane = threadIdx.x & 31;
+  for (int k = (blockIdx.x * kNT + threadIdx.x) >> 5; k < c; k += (gridDim.x * kNT) >> 5) {
+    const int d = a.outer[k];
+    const int4 md = a.meta[d];
+    const int lev = md.w >> 8, cb = md.y / C, ce = md.z / C;
+    Sums s{};
+    Box<R> x;
+    box_init(x);
+    const V4<R> z = mk4<R>(0, 0, 0);
+    // slot sequence: tail(cb), total(cb + 1 .. ce - 1), head(ce)
+    for (int ch = cb + lane; ch <= ce; ch += 32) {
+      const size_t slot = (size_t)ch * kPartPerChunk +
+                          (ch == cb ? 1 + kLevels + lev : (ch == ce ? 1 + lev : 0));
+      add_part(s, x, ldcg4(a.ps0 + slot), ldcg4(a.ps1 + slot),
+               MODE == 0 ? ldcg4(a.plo + slot) : z, MODE == 0 ? ldcg4(a.phi + slot) : z);
     }
-    if (mode == 0) { st4(lo + par, l); st4(hi + par, h); }
-    s0[par] = A;
-    s1[par] = B;
-    node = par;
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        s.a[q] += __shfl_xor_sync(0xffffffffu, s.a[q], o);
+        s.b[q] += __shfl_xor_sync(0xffffffffu, s.b[q], o);
+        x.l[q] = min(x.l[q], __shfl_xor_sync(0xffffffffu, x.l[q], o));
+        x.h[q] = max(x.h[q], __shfl_xor_sync(0xffffffffu, x.h[q], o));
+      }
+    if (lane == 0) write_node<R, MODE>(a, d, md, a.nchild[d], s, x, z, z);
   }
 }
 
@@ -614,9 +845,6 @@ __global__ void __launch_bounds__(kNT) k_aggregate(int mode, const int* L, int64
 //   code = skip | single-point leaf << 31 | bucket leaf << 30 | twig << 29
 //   (skip < 2^29: tree_build caps n accordingly): 64 B (FP32), loaded whole
 //   by two 256-bit loads; the first half is the node's interaction unit.
-__device__ __forceinline__ float ival(float, int v) { return __int_as_float(v); }
-__device__ __forceinline__ double ival(double, int v) { return (double)v; }
-
 template <typename R>
 __global__ void k_finalize(int mode, const int4* meta, const int* mp, const double4* s0,
                            const double4* s1, double kap, double c0x, double c0y, double c0z,
@@ -728,6 +956,65 @@ __global__ void k_scan_add(int* out, int64_t n, const int* bsum_scanned, int nb)
 }  // namespace
 
 int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t st);
+
+// Node aggregates + traversal records: mode 0 (boxes, sums of q and p, nrec;
+// the leaf-order copies srec / squ of the records `src`), mode 1 (sums of
+// alpha and beta, nadj; the leaf-order copy sadj of the adjoints `src`).
+template <typename R>
+static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts& kc, cudaStream_t st) {
+  constexpr int C = chunk_of<R>();
+  const int64_t nch = (t.n + C - 1) / C;
+  AggArgs<R> a{};
+  a.meta = t.meta.as<int4>();
+  a.nchild = t.nchild.as<int>();
+  a.first = t.first.as<int>();
+  a.lcp = t.lcp.as<int>();
+  a.perm = t.perm.as<int>();
+  a.n = t.n;
+  a.rec = static_cast<const V4<R>*>(src);
+  a.kap = kc.kappa;
+  a.c0x = kc.c0[0];
+  a.c0y = kc.c0[1];
+  a.c0z = kc.c0[2];
+  a.scaled = sizeof(R) == 4;
+  const size_t parts = (size_t)nch * kPartPerChunk;
+  GS_TRY_INT(t.parts.ensure(parts * (2 * sizeof(double4) + 2 * sizeof(V4<R>))));
+  a.ps0 = t.parts.as<double4>();
+  a.ps1 = a.ps0 + parts;
+  a.plo = reinterpret_cast<V4<R>*>(a.ps1 + parts);
+  a.phi = a.plo + parts;
+  // outer nodes: per level at most one starts in each chunk
+  GS_TRY_INT(t.outer.ensure(sizeof(int) * (64 + kLevels * (nch + 1))));
+  a.outer_cnt = t.outer.as<int>();
+  a.outer = a.outer_cnt + 64;
+  GS_CUDA_OK(cudaMemsetAsync(a.outer_cnt, 0, sizeof(int), st));
+  if (mode == 0) {
+    a.srec = t.srec.as<V4<R>>();
+    a.squ = t.squ.as<V4<R>>();
+    a.lo = t.lo.as<V4<R>>();
+    a.hi = t.hi.as<V4<R>>();
+    a.s0 = t.psum.as<double4>();
+    a.s1 = t.msum.as<double4>();
+    a.nrec = t.nrec.as<V4<R>>();
+    k_agg_chunk<R, 0><<<(unsigned)nch, kNT, 0, st>>>(a);
+    k_agg_outer<R, 0><<<4 * 148, kNT, 0, st>>>(a);
+  } else {
+    a.sadj = t.sadj.as<V4<R>>();
+    a.s0 = t.asum.as<double4>();
+    a.s1 = t.bsum.as<double4>();
+    a.nadj = t.nadj.as<V4<R>>();
+    k_agg_chunk<R, 1><<<(unsigned)nch, kNT, 0, st>>>(a);
+    k_agg_outer<R, 1><<<4 * 148, kNT, 0, st>>>(a);
+  }
+  GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+static int aggregate(int mode, int prec, DevTree& t, const void* src, const KernelConsts& kc,
+                     cudaStream_t st) {
+  return prec == kF32 ? aggregate_t<float>(mode, t, src, kc, st)
+                      : aggregate_t<double>(mode, t, src, kc, st);
+}
 
 // exclusive scan of n ints into out[0..n] (out[n] = total); bsum scratch
 static int scan_ints(const int* in, int64_t n, int* out, DBuf& scratch, cudaStream_t st) {
@@ -865,7 +1152,6 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.meta.ensure(sizeof(int4) * cap));
   GS_TRY_INT(t.parent.ensure(4 * cap));
   GS_TRY_INT(t.nchild.ensure(4 * cap));
-  GS_TRY_INT(t.counter.ensure(4 * cap));
   GS_TRY_INT(t.lo.ensure(vb * cap));
   GS_TRY_INT(t.hi.ensure(vb * cap));
   GS_TRY_INT(t.nrec.ensure(4 * vb * cap));
@@ -876,26 +1162,14 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
                               t.first.as<int>(), n, cap, t.meta.as<int4>(), t.parent.as<int>(),
                               overflow);
   const int mb = nblocks(cap, kNT);
-  k_nchild<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>());
+  k_children<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>());
+  GS_CUDA_OK(cudaGetLastError());
   kt_mark(4, st);
   kt_mark(5, st);
-  // 5. leaf-order records + aggregates
-  const int scaled = prec == kF32;
-  void* squ = t.squ.ptr;  // unscaled q in leaf order
-  if (prec == kF32)
-    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<float4>(), (float4*)squ);
-  else
-    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], scaled, t.srec.as<double4>(), (double4*)squ);
-  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
-  if (prec == kF32)
-    k_aggregate<float><<<nblocks(t.cap, kNT), kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const float4*)squ, t.srec.as<float4>(), nullptr, t.lo.as<float4>(), t.hi.as<float4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
-  else
-    k_aggregate<double><<<nblocks(t.cap, kNT), kNT, 0, st>>>(0, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), (const double4*)squ, t.srec.as<double4>(), nullptr, t.lo.as<double4>(), t.hi.as<double4>(), t.psum.as<double4>(), t.msum.as<double4>(), t.cap);
-  GS_CUDA_OK(cudaGetLastError());
-  (void)mb;
-  const int fs = tree_finalize_fwd(prec, t, kc, st);
+  // 5. leaf-order records + aggregates + traversal records, one kernel
+  GS_TRY_INT(aggregate(0, prec, t, rec, kc, st));
   kt_mark(5, st);
-  return fs;
+  return GS_OK;
 }
 
 // Points in Morton (leaf) order for locality only -- the exact path's
@@ -1013,24 +1287,12 @@ int tree_set_point_adjoints(int prec, DevTree& t, const void* adj, cudaStream_t 
 
 int tree_accumulate(int prec, DevTree& t, const void* adj, cudaStream_t st) {
   const int64_t n = t.n, cap = t.cap;
-  const int* mp = t.first.as<int>() + n;
   const size_t vb = vec_bytes(prec);
   GS_TRY_INT(t.sadj.ensure(2 * vb * n));
   GS_TRY_INT(t.asum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.bsum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.nadj.ensure(2 * vb * cap));
-  const int nb = nblocks(n, kNT), mb = nblocks(cap, kNT);
-  GS_CUDA_OK(cudaMemsetAsync(t.counter.ptr, 0, 4 * cap, st));
-  if (prec == kF32) {
-    k_gather_adj<float><<<nb, kNT, 0, st>>>((const float4*)adj, t.perm.as<int>(), n, t.sadj.as<float4>());
-    k_aggregate<float><<<nblocks(t.cap, kNT), kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<float4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<float><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<float4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<float4>());
-  } else {
-    k_gather_adj<double><<<nb, kNT, 0, st>>>((const double4*)adj, t.perm.as<int>(), n, t.sadj.as<double4>());
-    k_aggregate<double><<<nblocks(t.cap, kNT), kNT, 0, st>>>(1, t.lcp.as<int>(), n, t.first.as<int>(), t.meta.as<int4>(), t.parent.as<int>(), t.nchild.as<int>(), t.counter.as<int>(), nullptr, nullptr, t.sadj.as<double4>(), nullptr, nullptr, t.asum.as<double4>(), t.bsum.as<double4>(), t.cap);
-    k_finalize<double><<<mb, kNT, 0, st>>>(1, t.meta.as<int4>(), mp, t.asum.as<double4>(), t.bsum.as<double4>(), 0, 0, 0, 0, 0, t.nadj.as<double4>(), nullptr, nullptr, nullptr, nullptr, t.sadj.as<double4>());
-  }
-  GS_CUDA_OK(cudaGetLastError());
+  GS_TRY_INT(aggregate(1, prec, t, adj, t.kc, st));
   t.adj_valid = true;
   return GS_OK;
 }

@@ -1,0 +1,51 @@
+"""Octree build timing at config 4 (N = 1M unit cube, FP32): per-phase CUDA-event
+times of the builds inside a Barnes-Hut RK4 flow (gs_flow_profile_phases).
+
+  python tools/profile_build.py [--n N] [--steps K]
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+      --clock-control none --csv python tools/profile_build.py --steps 1   # per kernel
+
+Algorithmic bytes per point: bench.py BUILD_BYTES_PER_POINT.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    a = ap.parse_args()
+    from paper_1907_04834_b200 import BARNES_HUT, F32, RK4, Geoshoot, ShootingConfig
+    from bench import BUILD_BYTES_PER_POINT, workload
+    gs = Geoshoot(0)
+    q, p = workload(a.n)
+    cfg = ShootingConfig(sigma=0.0131, timesteps=10, backend=BARNES_HUT, integrator=RK4,
+                         precision=F32)
+    f = gs.flow(cfg, a.n)
+    f.upload(q, p)
+    f.advance(a.warmup)
+    f.sync()
+    f.upload(q, p)
+    f.profile(True)
+    f.advance(a.steps)
+    f.sync()
+    ph = f.profile_phases(6)
+    builds = max(1, ph["build"]["count"])
+    out = {k: v["ms"] / max(1, v["count"]) for k, v in ph.items()}
+    out["n"] = a.n
+    out["builds"] = builds
+    out["build_gbs_algorithmic"] = BUILD_BYTES_PER_POINT * a.n / (out["build"] * 1e-3) / 1e9
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
