@@ -28,6 +28,7 @@ struct DevTree {
   DBuf sadj;            // [n][2] V4<R>: alpha, beta in leaf order
   // per node
   DBuf meta;            // int4 {skip, begin, end, leaf | level << 8}
+  DBuf start;           // i32 start position of each node (k_nodes)
   DBuf parent;          // i32
   DBuf nchild;          // i32
   DBuf outer;           // i32 outer (chunk-spanning) nodes + count (tree.cu aggregates)

@@ -531,7 +531,7 @@ uint64_t flow_sig(const gs_flow* f) {
                         &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.lo,
                         &t.hi, &t.cen, &t.mom, &t.nrec, &t.nadj, &t.psum, &t.msum,
                         &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist,
-                        &t.scan_tmp, &t.scal, &t.outer, &t.parts, &t.sm_ctr})
+                        &t.scan_tmp, &t.scal, &t.outer, &t.parts, &t.start, &t.sm_ctr})
     mix(*b);
   return h;
 }

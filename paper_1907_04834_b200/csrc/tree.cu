@@ -99,17 +99,20 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
 
 // ------------------------------------------------------------------ keys ---
 // Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo.
+// key_lo only orders points that share all 21 levels of key_hi (depth-32
+// clusters), so it is computed lazily: by k_keys_lo only when the sorted
+// key_hi has equal neighbours (or for a download).
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
-                                              uint64_t* kh, uint64_t* kl) {
+                                              uint64_t* kh) {
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= n) return;
   const V4<R> q = ld4(rec + 2 * i);
   const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
   double lo[3] = {root[0], root[1], root[2]}, hi[3] = {root[3], root[4], root[5]};
-  uint64_t h = 0, l = 0;
+  uint64_t h = 0;
 #pragma unroll
-  for (int lev = 1; lev <= 32; ++lev) {
+  for (int lev = 1; lev <= 21; ++lev) {
     unsigned dig = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -119,11 +122,66 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
       hi[a] = up ? hi[a] : c;
       dig |= (unsigned)up << a;
     }
-    if (lev <= 21) h = (h << 3) | dig;
-    else l = (l << 3) | dig;
+    h = (h << 3) | dig;
   }
   kh[i] = h;
-  kl[i] = l;
+}
+
+// levels 22..32 of point x whose levels 1..21 are h: the level-21 cell is
+// replayed from h's digits (the same midpoints as the comparisons produced)
+__device__ __forceinline__ uint64_t key_lo_of(const double x[3], uint64_t h, const double* root) {
+  double lo[3] = {root[0], root[1], root[2]}, hi[3] = {root[3], root[4], root[5]};
+  for (int lev = 1; lev <= 21; ++lev) {
+    const unsigned dig = (unsigned)(h >> (3 * (21 - lev))) & 7u;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[a], hi[a]));
+      if ((dig >> a) & 1u) lo[a] = c;
+      else hi[a] = c;
+    }
+  }
+  uint64_t l = 0;
+  for (int lev = 22; lev <= 32; ++lev) {
+    unsigned dig = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[a], hi[a]));
+      const bool up = x[a] >= c;
+      lo[a] = up ? c : lo[a];
+      hi[a] = up ? hi[a] : c;
+      dig |= (unsigned)up << a;
+    }
+    l = (l << 3) | dig;
+  }
+  return l;
+}
+
+// key_lo by point index (before the sort); skipped unless *run_if
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_keys_lo(const V4<R>* rec, int64_t n, const double* root,
+                                                 const uint64_t* kh, uint64_t* kl,
+                                                 const unsigned* run_if) {
+  if (run_if && *run_if == 0) return;
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= n) return;
+  const V4<R> q = ld4(rec + 2 * i);
+  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
+  kl[i] = key_lo_of(x, kh[i], root);
+}
+
+// key_lo of the built tree from its leaf-order points (downloads): sorted
+// (skl) and by point index (kl)
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_keys_lo_leaf(const V4<R>* squ, const int* perm, int64_t n,
+                                                      const double* root, const uint64_t* skh,
+                                                      uint64_t* skl, uint64_t* kl) {
+  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (t >= n) return;
+  const V4<R> q = ld4(squ + t);
+  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
+  const uint64_t l = key_lo_of(x, skh[t], root);
+  skl[t] = l;
+  kl[perm[t]] = l;
 }
 
 // ------------------------------------------------------------ radix sort ---
@@ -167,7 +225,9 @@ constexpr unsigned kRsFlagAgg = 1u << 30, kRsFlagPrefix = 2u << 30, kRsCountMask
 
 template <int kRsIPT>
 __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* k0, int p0, const uint64_t* k1,
-                                                      int p1, int64_t n, unsigned* hist) {
+                                                      int p1, int64_t n, unsigned* hist,
+                                                      const unsigned* run_if = nullptr) {
+  if (run_if && *run_if == 0) return;
   extern __shared__ unsigned hs[];  // (p0 + p1) x 256
   const int np = p0 + p1;
   for (int t = threadIdx.x; t < np * 256; t += kRsNT) hs[t] = 0;
@@ -346,7 +406,8 @@ __device__ __forceinline__ int lcp_digits(uint64_t ah, uint64_t al, uint64_t bh,
 }
 
 __global__ void k_gather_lo_lcp(const int* perm, const uint64_t* kl, const uint64_t* skh,
-                                uint64_t* skl, int64_t n) {
+                                uint64_t* skl, int64_t n, const unsigned* run_if) {
+  if (run_if && *run_if == 0) return;
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t < n) skl[t] = kl[perm[t]];
 }
@@ -368,13 +429,6 @@ __device__ __forceinline__ void starts(const int* L, int64_t n, int64_t a, int& 
   leaf = Lm < 32 ? 1 : 0;
 }
 
-__global__ void k_count(const int* L, int64_t n, int* cnt) {
-  const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (a >= n) return;
-  int Lm, Lp, ci, lf;
-  starts(L, n, a, Lm, Lp, ci, lf);
-  cnt[a] = ci + lf;
-}
 
 // largest b >= a with lcp(a, b) >= l
 __device__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t n, int64_t a,
@@ -417,40 +471,64 @@ __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, c
   return first[s] + (plevel - (lm_of(L, s) + 1));
 }
 
-__global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
-                        int64_t n, int64_t cap, int4* meta, int* parent, int* overflow) {
+// The start position of every node: position a starts nodes
+// [first[a], first[a + 1]) -- cheap writes, so the searches below run one
+// node per thread (a position starting many levels no longer serialises them).
+__global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start, int* overflow) {
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (a >= n) return;
   if (first[n] > cap) {  // more nodes than the arrays hold (degenerate clustering)
     if (a == 0 && overflow) atomicExch(overflow, 1);
     return;
   }
-  int Lm, Lp, ci, lf;
-  starts(L, n, a, Lm, Lp, ci, lf);
-  const int base = first[a];
-  const int l0 = Lm + 1;
-  for (int k = 0; k < ci; ++k) {
-    const int l = l0 + k;
-    const int idx = base + k;
-    const int64_t b = search_right(kh, kl, n, a, l);
-    meta[idx] = make_int4(first[b + 1], (int)a, (int)b, l << 8);
-    parent[idx] = l == 0 ? -1 : (k > 0 ? idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
-  }
-  if (lf) {
-    const int idx = base + ci;
-    int level;
-    int64_t b = a;
-    if (Lp == 32) {
-      level = 32;
-      b = search_right(kh, kl, n, a, 32);
-    } else {
-      level = max(Lm, Lp) + 1;
-    }
-    meta[idx] = make_int4(first[b + 1], (int)a, (int)b, (level << 8) | 1);
-    parent[idx] = level == 0 ? -1 : (level - 1 >= l0 ? idx - 1 : parent_of(kh, kl, L, first, a, level - 1));
-  }
+  for (int idx = first[a]; idx < first[a + 1]; ++idx) start[idx] = (int)a;
 }
 
+// One node per thread: node idx starts at a = start[idx]; it is internal
+// node k = idx - first[a] of the levels L[a-1]+1 .. min(L[a], 31) starting
+// there, or a's leaf (last). Its range end b is the last position whose key
+// shares the node's level-l prefix (exponential + binary search on the sorted
+// keys); its parent is the node above it at the same start, or -- for the
+// first node at a position -- the level-(l-1) node found by a left search.
+__global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
+                        const int* start, int64_t n, int64_t cap, int4* meta, int* parent) {
+  const int64_t idx = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  const int m = first[n];
+  if (m > cap || idx >= m) return;
+  const int64_t a = start[idx];
+  int Lm, Lp, ci, lf;
+  starts(L, n, a, Lm, Lp, ci, lf);
+  const int k = (int)(idx - first[a]);
+  const int l0 = Lm + 1;
+  if (k < ci) {  // internal node of level l0 + k
+    const int l = l0 + k;
+    const int64_t b = search_right(kh, kl, n, a, l);
+    meta[idx] = make_int4(first[b + 1], (int)a, (int)b, l << 8);
+    parent[idx] = l == 0 ? -1 : (k > 0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
+    return;
+  }
+  int level;
+  int64_t b = a;
+  if (Lp == 32) {
+    level = 32;
+    b = search_right(kh, kl, n, a, 32);
+  } else {
+    level = max(Lm, Lp) + 1;
+  }
+  meta[idx] = make_int4(first[b + 1], (int)a, (int)b, (level << 8) | 1);
+  parent[idx] = level == 0 ? -1 : (level - 1 >= l0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, level - 1));
+}
+
+// per node: child count (the twig flag of the traversal record)
+__global__ void __launch_bounds__(kNT) k_children(const int4* meta, const int* mp, int* nchild) {
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  if (i >= *mp) return;
+  const int4 mi = meta[i];
+  int c = 0;
+  if (!(mi.w & 1))
+    for (int ch = (int)i + 1; ch < mi.x && c < 8; ++c) ch = max(ch + 1, meta[ch].x);
+  nchild[i] = c;
+}
 
 // ------------------------------------------------------------ aggregates ---
 // Forward: tight AABB + sums of q and p; backward: sums of alpha and beta.
@@ -522,16 +600,6 @@ __device__ __forceinline__ float4 ldcg4(const float4* p) { return __ldcg(p); }
 
 __device__ __forceinline__ bool is_single(const int4& mi) { return (mi.w & 1) && mi.y == mi.z; }
 
-// per node: child count (the twig flag of the traversal record)
-__global__ void __launch_bounds__(kNT) k_children(const int4* meta, const int* mp, int* nchild) {
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= *mp) return;
-  const int4 mi = meta[i];
-  int c = 0;
-  if (!(mi.w & 1))
-    for (int ch = (int)i + 1; ch < mi.x && c < 8; ++c) ch = max(ch + 1, meta[ch].x);
-  nchild[i] = c;
-}
 
 template <typename R>
 struct AggArgs {
@@ -930,11 +998,17 @@ __global__ void k_cells(const int4* meta, int64_t m, const uint64_t* skh, const 
   }
 }
 
-// int exclusive scan (n + 1 outputs: out[n] = total), 3 phases
-__global__ void __launch_bounds__(1024) k_scan_blocks(const int* in, int64_t n, int* out, int* bsum) {
+// exclusive scan of the node counts per position (k_count's, computed
+// inline from the lcp array; n + 1 outputs: out[n] = total), 3 phases
+__global__ void __launch_bounds__(1024) k_scan_blocks(const int* L, int64_t n, int* out, int* bsum) {
   __shared__ int s[1024];
   const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
-  const int v = i < n ? in[i] : 0;
+  int v = 0;
+  if (i < n) {
+    int Lm, Lp, ci, lf;
+    starts(L, n, i, Lm, Lp, ci, lf);
+    v = ci + lf;
+  }
   s[threadIdx.x] = v;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
@@ -1016,12 +1090,12 @@ static int aggregate(int mode, int prec, DevTree& t, const void* src, const Kern
                       : aggregate_t<double>(mode, t, src, kc, st);
 }
 
-// exclusive scan of n ints into out[0..n] (out[n] = total); bsum scratch
-static int scan_ints(const int* in, int64_t n, int* out, DBuf& scratch, cudaStream_t st) {
+// first[0..n]: exclusive scan of the node counts per position (out[n] = m)
+static int scan_ints(const int* L, int64_t n, int* out, DBuf& scratch, cudaStream_t st) {
   const int nb = nblocks(n, 1024);
   GS_TRY_INT(scratch.ensure(sizeof(unsigned) * (nb + 2)));
   unsigned* bs = scratch.as<unsigned>();
-  k_scan_blocks<<<nb, 1024, 0, st>>>(in, n, out, (int*)bs);
+  k_scan_blocks<<<nb, 1024, 0, st>>>(L, n, out, (int*)bs);
   // scan the block sums (nb + 1 entries, last = 0 -> becomes the total)
   GS_CUDA_OK(cudaMemsetAsync(bs + nb, 0, sizeof(unsigned), st));
   k_rs_scan<<<1, 1024, 0, st>>>(bs, nb + 1);
@@ -1063,9 +1137,9 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // 2. keys
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
   else
-    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
@@ -1100,8 +1174,8 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   unsigned* ctr = hist + kHist * 256;
   unsigned* tie = ctr + 31;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, kHist * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, kHist * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, t.key_hi.as<uint64_t>(), 8, n, hist);
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist + 5 * 256);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist + 5 * 256);
   // pass q (0..20) over digit histogram hq (0..4 lo, 5..12 hi)
   auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q, int hq,
                   const unsigned* run_if) {
@@ -1120,6 +1194,13 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   };
   hi_sort(t.key_hi.as<uint64_t>(), nullptr, 0, nullptr);  // values: the index
   k_tie_check<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), n, tie);
+  // [ties only] key_lo and its digit histograms
+  if (prec == kF32)
+    k_keys_lo<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), tie);
+  else
+    k_keys_lo<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), tie);
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 5 * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, nullptr, 0, n, hist, tie);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, 5 * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, nullptr, 0, n, hist, tie);
   {
     const uint64_t* ka = t.key_lo.as<uint64_t>();
     const int* va = nullptr;  // implicit: the index
@@ -1134,13 +1215,13 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   k_gather_u64<<<nb, kNT, 0, st>>>(t.tmp_v.as<int>(), t.key_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, tie);
   hi_sort(t.skey_lo.as<uint64_t>(), t.tmp_v.as<int>(), 13, tie);
   GS_CUDA_OK(cudaGetLastError());
-  k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n);
+  // sorted key_lo: only consulted where sorted key_hi neighbours are equal
+  k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, tie);
   kt_mark(3, st);
   kt_mark(4, st);
   // 4. topology
   k_lcp<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>());
-  k_count<<<nb, kNT, 0, st>>>(t.lcp.as<int>(), n, t.tmp_v.as<int>());
-  GS_TRY_INT(scan_ints(t.tmp_v.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
+  GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
   // The node count m = first[n] stays on the device: node arrays are sized
   // for 4n + 64 nodes (m ~ 1.5n for volumes and surfaces) and every kernel
   // reads m from first[n]; more nodes than that (degenerate clustering) raise
@@ -1158,10 +1239,12 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.psum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.msum.ensure(sizeof(double4) * cap));
   GS_TRY_INT(t.squ.ensure(vb * n));
-  k_nodes<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
-                              t.first.as<int>(), n, cap, t.meta.as<int4>(), t.parent.as<int>(),
-                              overflow);
   const int mb = nblocks(cap, kNT);
+  GS_TRY_INT(t.start.ensure(4 * cap));
+  k_node_starts<<<nb, kNT, 0, st>>>(t.first.as<int>(), n, cap, t.start.as<int>(), overflow);
+  k_nodes<<<mb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
+                              t.first.as<int>(), t.start.as<int>(), n, cap, t.meta.as<int4>(),
+                              t.parent.as<int>());
   k_children<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>());
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(4, st);
@@ -1198,9 +1281,9 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   k_bbox_final<<<1, kNT, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
   else
-    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>());
+    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
   const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;
@@ -1387,6 +1470,13 @@ int tree_download(DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
   if (sums) GS_TRY_INT(b_sums.ensure(96 * m));
   if (count) GS_TRY_INT(b_count.ensure(4 * m));
   const int mb = nblocks(m, kNT);
+  {  // key_lo (computed lazily by the build: only with equal key_hi neighbours)
+    const int nb = nblocks(n, kNT);
+    if (t.prec == kF32)
+      k_keys_lo_leaf<float><<<nb, kNT, 0, st>>>(t.squ.as<float4>(), t.perm.as<int>(), n, t.root.as<double>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.key_lo.as<uint64_t>());
+    else
+      k_keys_lo_leaf<double><<<nb, kNT, 0, st>>>(t.squ.as<double4>(), t.perm.as<int>(), n, t.root.as<double>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.key_lo.as<uint64_t>());
+  }
   const double4* as = t.adj_valid ? t.asum.as<double4>() : nullptr;
   const double4* bs = t.adj_valid ? t.bsum.as<double4>() : nullptr;
   if (t.prec == kF32) {
