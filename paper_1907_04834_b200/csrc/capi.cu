@@ -1097,21 +1097,42 @@ int backward_pass(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts&
 
 extern "C" {
 
-gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
-                      const double* p0, const double* target, gs_report* report,
-                      double* grad_out, gs_stats* stats) {
-  if (!c || !cfg || !q0 || !p0 || !target) return bad_arg("null argument");
-  TimerInstall install(c->timer);
-  if (cfg->integrator != GS_EULER) return bad_arg("evaluate: the adjoint is the transpose of Euler");
-  GS_TRY(gs_validate_config(cfg, nullptr));
-  GS_TRY(check_n(n));
-  if (is_multi(c)) return (gs_status)multi_evaluate(c, cfg, n, q0, p0, target, report, grad_out, stats);
+}  // extern "C"
+
+namespace gsb {
+
+// evaluate() (shooting.cpp:302-314) with the inputs either on the host
+// (gs_evaluate) or already resident in HBM (the device optimizer:
+// evaluate_resident): q0, p0, target double [n][3]; `box` = the host bounding
+// box {c0[3], ext[3]} of q0 (its kernel constants). The gradient goes to the
+// host (grad_host) or stays in HBM (grad_dev).
+static int evaluate_impl(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
+                         const double* p0, const double* target, bool resident, const double* box,
+                         gs_report* report, double* grad_host, double* grad_dev, gs_stats* stats) {
   const int T = cfg->timesteps;
   gs_flow* f = scratch_flow(c);
   GS_TRY(flow_init(f, c, cfg, n));
-  GS_TRY(flow_upload(f, q0, p0));
+  if (resident) {  // records packed straight from the device arrays
+    f->kc = with_ext(make_consts(cfg->sigma, f->prec == kF32 ? box : nullptr), box + 3);
+    GS_TRY(c->scal.ensure(64));
+    int* bad = c->scal.as<int>();
+    GS_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    GS_TRY(pack_records(f->prec, q0, p0, n, f->rec.ptr, bad, c->stream));
+    int hbad = 0;
+    GS_CUDA_OK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GS_TRY(sync(c));
+    if (hbad) return bad_arg("non-finite coordinate in input");
+    f->permuted = false;
+    f->steps_done = 0;
+    f->have_energy_part = false;
+    GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), c->stream));
+    GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), c->stream));
+  } else {
+    GS_TRY(flow_upload(f, q0, p0));
+    GS_TRY(h2d(c, c->stage_c, target, n));
+    target = c->stage_c.as<double>();
+  }
   f->want_energy = true;
-  GS_TRY(h2d(c, c->stage_c, target, n));
   const size_t rb = 2 * vec_bytes(f->prec) * n;
   // trajectory records traj[0..T] resident in HBM
   GS_TRY(c->rec_b.ensure(rb * (T + 1)));
@@ -1131,18 +1152,20 @@ gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* 
   GS_TRY(flow_check(f));
   double energy = 0.0;
   GS_TRY(flow_energy(f, &energy));
-  GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
+  if (!grad_dev) {
+    GS_TRY(c->stage_d.ensure(sizeof(double) * 3 * n));
+    grad_dev = c->stage_d.as<double>();
+  }
   GS_TRY(c->scal.ensure(64));
   gs_stats bst{};
   Timer tb(c->stream);
-  GS_TRY(backward_pass(c, cfg, f->prec, f->kc, n, traj, rb, c->stage_c.as<double>(),
-                       f->dhdp0.as<double>(), &f->bh, true, c->rec_a, c->part,
-                       c->stage_d.as<double>(), c->scal.as<double>() + 1, &bst));
+  GS_TRY(backward_pass(c, cfg, f->prec, f->kc, n, traj, rb, target, f->dhdp0.as<double>(), &f->bh,
+                       true, c->rec_a, c->part, grad_dev, c->scal.as<double>() + 1, &bst));
   const double bwd_ms = tb.ms();
   double sse = 0.0;
   GS_CUDA_OK(cudaMemcpyAsync(&sse, c->scal.as<double>() + 1, sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream));
-  GS_TRY(d2h(c, grad_out, c->stage_d.ptr, 3 * n));
+  if (grad_host) GS_TRY(d2h(c, grad_host, grad_dev, 3 * n));
   GS_TRY(sync(c));
   if (report) {
     report->energy = energy;
@@ -1162,6 +1185,36 @@ gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* 
     stats->backward_ms = bwd_ms;
   }
   return GS_OK;
+}
+
+int evaluate_resident(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0_dev,
+                      const double* box, const double* p0_dev, const double* target_dev,
+                      gs_report* report, double* grad_dev, gs_stats* stats) {
+  TimerInstall install(c->timer);
+  return evaluate_impl(c, cfg, n, q0_dev, p0_dev, target_dev, true, box, report, nullptr, grad_dev,
+                       stats);
+}
+
+bool context_is_multi(const gs_ctx* c) { return is_multi(c); }
+cudaStream_t context_stream(const gs_ctx* c) { return c->stream; }
+
+void host_box(const double* q, int64_t n, double* box) { bbox_center(q, n, box, box + 3); }
+
+}  // namespace gsb
+
+extern "C" {
+
+gs_status gs_evaluate(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,
+                      const double* p0, const double* target, gs_report* report,
+                      double* grad_out, gs_stats* stats) {
+  if (!c || !cfg || !q0 || !p0 || !target) return bad_arg("null argument");
+  TimerInstall install(c->timer);
+  if (cfg->integrator != GS_EULER) return bad_arg("evaluate: the adjoint is the transpose of Euler");
+  GS_TRY(gs_validate_config(cfg, nullptr));
+  GS_TRY(check_n(n));
+  if (is_multi(c)) return (gs_status)multi_evaluate(c, cfg, n, q0, p0, target, report, grad_out, stats);
+  return (gs_status)evaluate_impl(c, cfg, n, q0, p0, target, false, nullptr, report, grad_out,
+                                  nullptr, stats);
 }
 
 gs_status gs_objective(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0,

@@ -195,3 +195,17 @@ int sum_part_w(int prec, const void* part, int n, int per, int which, double* bl
 int step_counter_inc(int* counter, cudaStream_t st);
 
 }  // namespace gsb
+
+struct gs_ctx;
+namespace gsb {
+// evaluate() with device-resident inputs (capi.cu): q0_dev / p0_dev /
+// target_dev double [n][3]; box = {c0, ext} of q0's host bounding box; the
+// gradient stays in grad_dev. Used by the device-resident optimizer.
+int evaluate_resident(gs_ctx* c, const gs_config* cfg, int64_t n, const double* q0_dev,
+                      const double* box, const double* p0_dev, const double* target_dev,
+                      gs_report* report, double* grad_dev, gs_stats* stats);
+bool context_is_multi(const gs_ctx* c);
+cudaStream_t context_stream(const gs_ctx* c);
+void host_box(const double* q, int64_t n, double* box);
+
+}  // namespace gsb

@@ -10,10 +10,13 @@
 // (:82-189), curvature-gated history updates (:271-277) and the same
 // termination order (:235-298). Non-finite flows map to +inf (:328-332).
 //
-// Every objective/gradient is one gs_evaluate call: the forward flow, trees,
-// adjoint and gradient run on the B200; the O(N m) L-BFGS vector algebra
-// stays on the host in FP64 (as in the reference), which keeps the control
-// flow of the search identical to the reference given the same evaluations.
+// Every objective/gradient is one evaluate(): the forward flow, trees,
+// adjoint and gradient run on the B200. On a single-device context the whole
+// search state is device-resident too (lbfgs_dev.cu: q0 / target uploaded
+// once, the O(N m) two-loop and line-search vector algebra as device kernels,
+// only the steering scalars on the host); on a multi-device context the
+// vectors stay on the host (below). Either way the control flow of the search
+// is the reference's given the same evaluations.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -26,6 +29,7 @@
 
 #include <cuda_runtime.h>
 
+#include "engine.h"
 #include "geoshoot_b200.h"
 #include "lbfgs.h"
 
@@ -139,6 +143,50 @@ struct DeviceObjective {
     const gs_status st = gs_evaluate(ctx, cfg, n, q0, x.data(), target, &r, g.data(), &s);
     if (st == GS_NONFINITE || st == GS_INVALID_ARGUMENT) return kInf;
     if (st != GS_OK) throw DeviceFailure{st};
+    last = r;
+    stats.direct_interactions += s.direct_interactions;
+    stats.approximated_interactions += s.approximated_interactions;
+    stats.nodes_visited += s.nodes_visited;
+    stats.traversal_queries += s.traversal_queries;
+    stats.tree_build_ms += s.tree_build_ms;
+    stats.forward_ms += s.forward_ms;
+    stats.backward_ms += s.backward_ms;
+    return r.total;
+  }
+};
+
+// The same objective with device-resident inputs (evaluate_resident).
+struct ResidentObjective {
+  gs_ctx* ctx;
+  const gs_config* cfg;
+  int64_t n;
+  gsb::DBuf q0, target;
+  double box[6] = {0, 0, 0, 0, 0, 0};
+  gs_report last{};
+  gs_stats stats{};
+
+  gs_status upload(const double* q0h, const double* th) {
+    const size_t b = sizeof(double) * 3 * (size_t)n;
+    if (q0.ensure(b) != GS_OK || target.ensure(b) != GS_OK) return GS_CUDA_ERROR;
+    cudaStream_t st = gsb::context_stream(ctx);
+    if (cudaMemcpyAsync(q0.ptr, q0h, b, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(target.ptr, th, b, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return GS_CUDA_ERROR;
+    gsb::host_box(q0h, n, box);
+    return GS_OK;
+  }
+
+  double operator()(const double* x, double* g) {
+    gs_report r{};
+    gs_stats s{};
+    const int st = gsb::evaluate_resident(ctx, cfg, n, q0.as<double>(), box, x, target.as<double>(),
+                                          &r, g, &s);
+    if (st == GS_NONFINITE || st == GS_INVALID_ARGUMENT) {  // rejected trial point: +inf, g = 0
+      cudaMemsetAsync(g, 0, sizeof(double) * 3 * (size_t)n, gsb::context_stream(ctx));
+      return kInf;
+    }
+    if (st != GS_OK) throw DeviceFailure{(gs_status)st};
     last = r;
     stats.direct_interactions += s.direct_interactions;
     stats.approximated_interactions += s.approximated_interactions;
@@ -353,8 +401,26 @@ gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc
   };
   gsb::LbfgsResult res;
   try {
-    res = gsb::lbfgs_minimize([&](const Vec& x, Vec& g) { return F(x, g); }, Vec((size_t)3 * n, 0.0),
-                              *oc, record);
+    if (!gsb::context_is_multi(ctx)) {
+      // device-resident state: q0 and the target uploaded once, every vector
+      // of the search in HBM, evaluate() straight from them
+      ResidentObjective R{ctx, cfg, n};
+      const gs_status us = R.upload(q0, target);
+      if (us != GS_OK) return us;
+      auto rec = [&](int it, double f, double ginf, double wall_ms) {
+        F.last = R.last;
+        record(it, f, ginf, wall_ms);
+      };
+      const int s = gsb::lbfgs_minimize_device([&](const double* x, double* g) { return R(x, g); },
+                                               3 * n, *oc, gsb::context_stream(ctx), rec, p_out,
+                                               res);
+      if (s != GS_OK) return (gs_status)s;
+      F.stats = R.stats;
+    } else {  // a multi-device context: host vectors, sharded evaluate()
+      res = gsb::lbfgs_minimize([&](const Vec& x, Vec& g) { return F(x, g); },
+                                Vec((size_t)3 * n, 0.0), *oc, record);
+      std::copy(res.x.begin(), res.x.end(), p_out);
+    }
   } catch (const DeviceFailure& e) {
     return e.status;
   } catch (const gsb::NonFiniteStart&) {
@@ -362,7 +428,6 @@ gs_status gs_optimize(gs_ctx* ctx, const gs_config* cfg, const gs_opt_config* oc
   } catch (const std::bad_alloc&) {
     return GS_INTERNAL;
   }
-  std::copy(res.x.begin(), res.x.end(), p_out);
   if (reason) *reason = res.reason;
   if (iterations) *iterations = res.iterations;
   if (evaluations) *evaluations = res.evaluations;
