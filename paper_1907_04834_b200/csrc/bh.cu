@@ -183,9 +183,9 @@ template <typename R, int MODE, bool LMD = false>
 __device__ __forceinline__ void unit(Acc<R>& acc, const V4<R>& xs, const V4<R>& px,
                                      const V4<R>& ai, const V4<R>& bi, const V4<R>& Q,
                                      const V4<R>& P, const V4<R>& Al, const V4<R>& Be,
-                                     const BhArgs<R>& a, R dsc = R(1)) {
+                                     const BhArgs<R>& a, R dsc = R(1), bool on = true) {
   const R dx = xs.x - Q.x, dy = xs.y - Q.y, dz = xs.z - Q.z;
-  const R g = kern(dx, dy, dz, a);
+  const R g = on ? kern(dx, dy, dz, a) : R(0);  // on = false: a masked lane adds exact zeros
   if (MODE == kBhVel) {
     acc.v[0] += g * P.x; acc.v[1] += g * P.y; acc.v[2] += g * P.z;
   } else if (MODE == kBhRhs) {
@@ -571,28 +571,36 @@ __device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Ac
                                           const V4<R>& ai, const V4<R>& bi, const BhArgs<R>& a,
                                           unsigned& n_seg, unsigned& n_step) {
   for (;;) {
-    const int from = max(ds, cursor);
+    const int from = max(ds, cursor);  // this lane's unswept part: [from, de]
     const int start = __reduce_min_sync(0xffffffffu, (de >= from) ? from : INT_MAX);
     if (start >= F) return;
-    cursor = start;
-    const bool cover = ds <= cursor && cursor <= de;
-    const int lim = cover ? de + 1 : ((ds > cursor && de >= ds) ? ds : INT_MAX);
-    const int seg_end = min(F, __reduce_min_sync(0xffffffffu, lim));
-    ++n_seg;
-    n_step += (unsigned)(seg_end - cursor);
-    if (cover) {
-      c_dir += (uint32_t)(seg_end - cursor);
-#pragma unroll 4
-      for (int j = cursor; j < seg_end; ++j) {
-        V4<R> Q, P;
-        ld8(a.srec + 2 * j, Q, P);
-        if (MODE == kBhHess)
-          unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a);
-        else
-          unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Q, Q, a);
-      }
+    // the maximal run [start, E) of the union of the lanes' pending parts
+    // (chained overlapping / adjacent intervals), clipped at F; every point
+    // of it is loaded once (broadcast) and evaluated by all lanes, masked to
+    // each lane's own interval -- long branch-free sweeps instead of one
+    // segment per interval endpoint
+    int E = start + 1;
+    for (;;) {
+      const int e = __reduce_max_sync(0xffffffffu, (de >= from && from <= E) ? de + 1 : 0);
+      if (e <= E) break;
+      E = e;
     }
-    cursor = seg_end;
+    E = min(E, F);
+    const int lo = max(from, start), hi = min(de + 1, E);  // this lane's part of the run
+    if (hi > lo) c_dir += (uint32_t)(hi - lo);
+    ++n_seg;
+    n_step += (unsigned)(E - start);
+#pragma unroll 4
+    for (int j = start; j < E; ++j) {
+      V4<R> Q, P;
+      ld8(a.srec + 2 * j, Q, P);
+      const bool on = j >= lo && j < hi;
+      if (MODE == kBhHess)
+        unit<R, MODE>(acc, xs, px, ai, bi, Q, P, ld4(a.sadj + 2 * j), ld4(a.sadj + 2 * j + 1), a, R(1), on);
+      else
+        unit<R, MODE>(acc, xs, px, ai, bi, Q, P, Q, Q, a, R(1), on);
+    }
+    cursor = E;
   }
 }
 

@@ -567,7 +567,7 @@ int flow_capture_step(gs_flow* f) {
 
 int flow_advance(gs_flow* f, int steps) {
   f->launches = 0;
-  const bool graphs = graphs_enabled() && !f->timer && f->shard_begin == 0 && f->shard_count == f->n;
+  const bool graphs = graphs_enabled() && !f->timer && !g_ktimer && f->shard_begin == 0 && f->shard_count == f->n;
   for (int k = 0; k < steps; ++k) {
     if (!graphs || f->steps_done == 0) {  // the first step runs eagerly (energy, allocations)
       GS_TRY(flow_step_eager(f));

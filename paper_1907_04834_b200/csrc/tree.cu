@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include "bh.h"
@@ -156,19 +157,6 @@ __device__ __forceinline__ uint64_t key_lo_of(const double x[3], uint64_t h, con
   return l;
 }
 
-// key_lo by point index (before the sort); skipped unless *run_if
-template <typename R>
-__global__ void __launch_bounds__(kNT) k_keys_lo(const V4<R>* rec, int64_t n, const double* root,
-                                                 const uint64_t* kh, uint64_t* kl,
-                                                 const unsigned* run_if) {
-  if (run_if && *run_if == 0) return;
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= n) return;
-  const V4<R> q = ld4(rec + 2 * i);
-  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
-  kl[i] = key_lo_of(x, kh[i], root);
-}
-
 // key_lo of the built tree from its leaf-order points (downloads): sorted
 // (skl) and by point index (kl)
 template <typename R>
@@ -223,44 +211,36 @@ __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
 // instead of 3, and no ntiles x 256 prefix pass.
 constexpr unsigned kRsFlagAgg = 1u << 30, kRsFlagPrefix = 2u << 30, kRsCountMask = (1u << 30) - 1;
 
+// digit histograms of all 8 passes in one read of the keys
 template <int kRsIPT>
-__global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* k0, int p0, const uint64_t* k1,
-                                                      int p1, int64_t n, unsigned* hist,
-                                                      const unsigned* run_if = nullptr) {
-  if (run_if && *run_if == 0) return;
-  extern __shared__ unsigned hs[];  // (p0 + p1) x 256
-  const int np = p0 + p1;
-  for (int t = threadIdx.x; t < np * 256; t += kRsNT) hs[t] = 0;
+__global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int64_t n, unsigned* hist) {
+  __shared__ unsigned hs[8 * 256];
+  for (int t = threadIdx.x; t < 8 * 256; t += kRsNT) hs[t] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * (kRsNT * kRsIPT);
   for (int r = 0; r < kRsIPT; ++r) {
     const int64_t i = base + r * kRsNT + threadIdx.x;
     if (i >= n) break;
-    if (p0) {
-      const uint64_t k = k0[i];
-      for (int q = 0; q < p0; ++q) atomicAdd(&hs[q * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
-    }
-    if (p1) {
-      const uint64_t k = k1[i];
-      for (int q = 0; q < p1; ++q) atomicAdd(&hs[(p0 + q) * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
-    }
+    const uint64_t k = key[i];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) atomicAdd(&hs[q * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < np * 256; t += kRsNT)
+  for (int t = threadIdx.x; t < 8 * 256; t += kRsNT)
     if (hs[t]) atomicAdd(&hist[t], hs[t]);
 }
 
+// (4 tiles per SM at 8 keys per thread: 1M points = 489 tiles in one wave)
+constexpr int kLB = 8;  // look-back: predecessors' status words loaded per round trip
 template <int kRsIPT>
-__global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, const int* vin,
+__global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, const int* vin,
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
-                                                      unsigned* desc, unsigned* tile_ctr,
-                                                      const unsigned* run_if = nullptr) {
-  if (run_if && *run_if == 0) return;  // conditional pass (tree_build's tie fallback)
+                                                      unsigned* desc, unsigned* tile_ctr) {
   constexpr int kTile = kRsNT * kRsIPT;
   __shared__ unsigned wh[kRsNT / 32][256];  // per-warp digit counts -> offsets within the tile's digit run
-  __shared__ unsigned base[256];            // global digit starts (scan of dig_tot)
-  __shared__ unsigned ts[256];              // tile digit counts -> tile-local digit starts
+  __shared__ unsigned wsum[2][kRsNT / 32];  // per-warp sums of the two digit scans
+  __shared__ unsigned ts[256];              // tile-local digit starts
   __shared__ unsigned gofs[256];            // global position of tile-local slot 0 of each digit run
   __shared__ uint64_t sk[kTile];            // the tile in digit order (coalesced write-out)
   __shared__ int sv[kTile];
@@ -268,7 +248,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
   for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
-  base[threadIdx.x] = dig_tot[threadIdx.x];
+  const unsigned dtot = dig_tot[threadIdx.x];
   __syncthreads();
   const int tile = s_tile;
   const int64_t t0 = (int64_t)tile * kTile;
@@ -276,25 +256,35 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   uint64_t key[kRsIPT];
   int val[kRsIPT];
   unsigned loc[kRsIPT];
+  // all loads in flight before the first warp-synchronous digit match
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
     const int64_t i = seg + r * 32 + lane;
     const bool ok = i < n;
     key[r] = ok ? kin[i] : 0ull;
     val[r] = ok ? (vin ? vin[i] : (int)i) : 0;  // first pass: values are the indices
+  }
+  // per key: the lanes with the same digit (match.any),
+  // the group's leader reserves cnt slots of the warp's digit counter with one
+  // shared atomic (issued back to back for the kRsIPT keys: same-address
+  // atomics of one warp stay in program order), lanes rank by lane order
+  unsigned peers[kRsIPT], old[kRsIPT];
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    const bool ok = seg + r * 32 + lane < n;
     const unsigned d = (unsigned)(key[r] >> shift) & 255u;
-    const unsigned act = __ballot_sync(0xffffffffu, ok);
-    loc[r] = 0;
-    if (ok) {
-      const unsigned peers = __match_any_sync(act, d);
-      const int leader = __ffs(peers) - 1;
-      const unsigned cnt = __popc(peers);
-      const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-      if (lane == leader) wh[warp][d] += cnt;
-      __syncwarp(act);
-      loc[r] = wh[warp][d] - cnt + rank;
-    }
-    __syncwarp();
+    // (invalid lanes -- tail tile only -- match among themselves on digit 256)
+    const unsigned pm = __match_any_sync(0xffffffffu, ok ? d : 256u);
+    peers[r] = ok ? pm : 0u;
+    old[r] = 0;
+    if (ok && lane == __ffs(pm) - 1) old[r] = atomicAdd(&wh[warp][d], (unsigned)__popc(pm));
+  }
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    const unsigned pm = peers[r];
+    const int leader = pm ? __ffs(pm) - 1 : lane;
+    const unsigned base = __shfl_sync(0xffffffffu, old[r], leader);
+    loc[r] = base + __popc(pm & ((1u << lane) - 1u));
   }
   __syncthreads();
   const unsigned d = threadIdx.x;
@@ -307,28 +297,29 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   // publish this tile's count for digit d as early as possible (look-back)
   cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
   if (tile != 0) mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
-  ts[d] = tot;
-  __syncthreads();
-  // inclusive scans over digits: global digit totals and this tile's counts
-  for (int o = 1; o < 256; o <<= 1) {
-    const unsigned v1 = d >= (unsigned)o ? base[d - o] : 0u, v2 = d >= (unsigned)o ? ts[d - o] : 0u;
-    __syncthreads();
-    base[d] += v1;
-    ts[d] += v2;
-    __syncthreads();
+  // inclusive scans over digits (thread d = digit d): global digit totals and
+  // this tile's counts -- warp shuffles, then the 8 warp sums
+  unsigned gi = dtot, ti = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned g = __shfl_up_sync(0xffffffffu, gi, o), t = __shfl_up_sync(0xffffffffu, ti, o);
+    if (lane >= o) gi += g, ti += t;
   }
-  const unsigned tstart = ts[d] - tot;
+  if (lane == 31) wsum[0][warp] = gi, wsum[1][warp] = ti;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) gi += wsum[0][w], ti += wsum[1][w];
+  const unsigned tstart = ti - tot;
   // this tile's offset inside digit d: decoupled look-back over earlier tiles
   unsigned excl = 0;
   if (tile == 0) {
     mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
   } else {
-    // four predecessors' status words per round trip (independent loads),
+    // kLB predecessors' status words per round trip (independent loads),
     // consumed in order; an unpublished one is polled again from there
     for (int t = tile - 1;;) {
-      unsigned v[4];
+      unsigned v[kLB];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kLB; ++k) {
         v[k] = kRsFlagPrefix;  // (before tile 0: never reached, tile 0 is a prefix)
         if (t - k >= 0) {
           cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)(t - k) * 256 + d]);
@@ -338,7 +329,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
       bool done = false;
       int used = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kLB; ++k) {
         if (done || used < k) break;  // stopped at a prefix or an unpublished tile
         if (!(v[k] & (kRsFlagAgg | kRsFlagPrefix))) break;  // that tile has not published yet
         excl += v[k] & kRsCountMask;
@@ -350,8 +341,7 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
     }
     mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
   }
-  gofs[d] = base[d] - dig_tot[d] + excl - tstart;
-  __syncthreads();  // every thread's ts[] read is done
+  gofs[d] = gi - dtot + excl - tstart;
   ts[d] = tstart;
   __syncthreads();
   // stage the tile in (digit, rank) order ...
@@ -380,20 +370,219 @@ __global__ void __launch_bounds__(kRsNT) k_rs_onesweep(const uint64_t* kin, cons
   }
 }
 
-// out[t] = key[perm[t]]
-__global__ void k_gather_u64(const int* perm, const uint64_t* key, uint64_t* out, int64_t n,
-                             const unsigned* run_if = nullptr) {
-  if (run_if && *run_if == 0) return;
-  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (t < n) out[t] = key[perm[t]];
+// one one-sweep pass, IPT keys per thread
+void onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi, uint64_t* ko,
+              int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc, unsigned* ctr) {
+  if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, dig_tot, desc, ctr);
+  else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, dig_tot, desc, ctr);
 }
 
-// flag = 1 if two neighbours of the key_hi-sorted order share key_hi (the
-// deep key must then order them: tree_build re-sorts by the full key)
-__global__ void k_tie_check(const uint64_t* skh, int64_t n, unsigned* flag) {
+// ---------------------------------------------------------------- ties ---
+// Points sharing all 21 levels of key_hi form runs of equal keys in the
+// key_hi-sorted order (the sort is stable: a run is in ascending index). The
+// full order sorts each run by (key_lo, index) -- key_lo (levels 22-32) is
+// computed for the run members only, as the unique 64-bit code
+// (key_lo << 31) | index. k_tie_runs lists the runs (and sets the tie flag);
+// k_tie_sort, one cooperative grid, sorts them in place: a warp per run of
+// <= 32 points (rank by comparison); longer runs in 2048-code chunks (bitonic
+// sort in shared memory, a CTA per chunk across all runs), then merge passes
+// (w -> 2w) whose 2048-output segments are spread over the grid (merge path),
+// grid-synchronised. Two launches whatever the data -- no second full-key
+// radix sort behind no-op launches -- and a single run of the whole cloud (a
+// diverged flow whose root box dwarfs the points) still uses every SM.
+namespace cg = cooperative_groups;
+constexpr int kTieChunk = 2048;
+constexpr int kTieSmallCtr = 28, kTieBigCtr = 29, kTieMaxLen = 30, kTieFlag = 31;  // sort counters
+
+__global__ void k_tie_runs(const uint64_t* skh, int64_t n, unsigned* ctr, int2* small_runs,
+                           int4* big_runs) {
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  const bool tie = t + 1 < n && skh[t] == skh[t + 1];
-  if (__any_sync(0xffffffffu, tie) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+  if (t + 1 >= n) return;
+  const uint64_t k = skh[t];
+  if (skh[t + 1] != k || (t > 0 && skh[t - 1] == k)) return;  // not a run start
+  // last index of the run: exponential then binary search on equality
+  int64_t step = 1, good = t + 1;
+  while (good + step < n && skh[good + step] == k) {
+    good += step;
+    step <<= 1;
+  }
+  int64_t lo = good, hi = min(n - 1, good + step);
+  while (hi > lo) {
+    const int64_t mid = lo + (hi - lo + 1) / 2;
+    if (skh[mid] == k) lo = mid;
+    else hi = mid - 1;
+  }
+  const int len = (int)(lo - t + 1);
+  if (len <= 32) {
+    small_runs[atomicAdd(ctr + kTieSmallCtr, 1u)] = make_int2((int)t, len);
+  } else {
+    big_runs[atomicAdd(ctr + kTieBigCtr, 1u)] = make_int4((int)t, len, 0, 0);
+    atomicMax(ctr + kTieMaxLen, (unsigned)len);
+  }
+  atomicOr(ctr + kTieFlag, 1u);
+}
+
+// (key_lo << 31) | index: unique per point (n < 2^31), ordered as the full key
+template <typename R>
+__device__ __forceinline__ uint64_t tie_code(const V4<R>* rec, const int* perm, const uint64_t* skh,
+                                             const double* root, int64_t j) {
+  const int p = perm[j];
+  const V4<R> q = ld4(rec + 2 * (int64_t)p);
+  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
+  return (key_lo_of(x, skh[j], root) << 31) | (uint64_t)p;
+}
+
+__device__ __forceinline__ void tie_put(int* perm, uint64_t* skl, int64_t j, uint64_t c) {
+  perm[j] = (int)(c & 0x7fffffffu);
+  skl[j] = c >> 31;
+}
+
+// bitonic sort of s[0, P) (P a power of two) by the CTA
+__device__ void bitonic_smem(uint64_t* s, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ij = i ^ j;
+        if (ij > i) {
+          const uint64_t u = s[i], v = s[ij];
+          if ((u > v) == ((i & k) == 0)) {
+            s[i] = v;
+            s[ij] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// chunk task g -> (big run, chunk in it): binary search over the runs' chunk
+// prefix (.z); returns the run index
+__device__ __forceinline__ int tie_task_run(const int4* big, int nbig, int g) {
+  int lo = 0, hi = nbig - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (big[mid].z <= g) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64_t* skh,
+                                                  const double* root, const unsigned* ctr,
+                                                  const int2* small_runs, int4* big_runs,
+                                                  int* perm, uint64_t* skl, uint64_t* bufa,
+                                                  uint64_t* bufb) {
+  if (ctr[kTieFlag] == 0) return;  // (uniform over the grid)
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint64_t s[kTieChunk];
+  const int lane = threadIdx.x & 31;
+  // runs of <= 32 points: a warp each, rank = number of smaller codes
+  const int nsmall = (int)ctr[kTieSmallCtr];
+  const int gw = (blockIdx.x * kNT + threadIdx.x) >> 5, nw = (gridDim.x * kNT) >> 5;
+  for (int r = gw; r < nsmall; r += nw) {
+    const int2 run = small_runs[r];
+    const uint64_t c = lane < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + lane) : ~0ull;
+    int rank = 0;
+    for (int k = 0; k < run.y; ++k) rank += __shfl_sync(0xffffffffu, c, k) < c;
+    __syncwarp();
+    if (lane < run.y) tie_put(perm, skl, (int64_t)run.x + rank, c);
+  }
+  const int nbig = (int)ctr[kTieBigCtr];
+  if (nbig == 0) return;
+  // chunk prefix over the long runs (.z), by CTA 0
+  if (blockIdx.x == 0) {
+    __shared__ int s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nbig; b0 += kNT) {
+      const int r = b0 + threadIdx.x;
+      const int c = r < nbig ? (big_runs[r].y + kTieChunk - 1) / kTieChunk : 0;
+      int v = c;  // inclusive block scan
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      __shared__ int ws[kNT / 32];
+      if (lane == 31) ws[threadIdx.x >> 5] = v;
+      __syncthreads();
+      int add = s_carry;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) add += ws[w];
+      if (r < nbig) big_runs[r].z = add + v - c;
+      __syncthreads();
+      if (threadIdx.x == kNT - 1) s_carry = add + v;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) big_runs[nbig].z = s_carry;  // total chunks (sentinel entry)
+  }
+  grid.sync();
+  const int nchunks = big_runs[nbig].z;
+  const int maxlen = (int)ctr[kTieMaxLen];
+  // sorted chunks (a run that fits one chunk is finished here)
+  for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
+    const int r = tie_task_run(big_runs, nbig, g);
+    const int4 run = big_runs[r];
+    const int c0 = (g - run.z) * kTieChunk, cl = min(kTieChunk, run.y - c0);
+    int P = 1;
+    while (P < cl) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += kNT)
+      s[i] = i < cl ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + c0 + i) : ~0ull;
+    __syncthreads();
+    bitonic_smem(s, P);
+    for (int i = threadIdx.x; i < cl; i += kNT) {
+      if (run.y <= kTieChunk) tie_put(perm, skl, (int64_t)run.x + i, s[i]);
+      else bufa[(int64_t)run.x + c0 + i] = s[i];
+    }
+    __syncthreads();
+  }
+  // merge passes: sorted blocks of width w -> 2w; task g = one 2048-output
+  // segment of one run (segments never straddle a pair: 2w is a multiple)
+  uint64_t* src = bufa;
+  uint64_t* dst = bufb;
+  for (int w = kTieChunk; w < maxlen; w <<= 1) {
+    grid.sync();
+    for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
+      const int r = tie_task_run(big_runs, nbig, g);
+      const int4 run = big_runs[r];
+      if (run.y <= kTieChunk) continue;  // done in the chunk phase
+      const int o0 = (g - run.z) * kTieChunk;   // first output of this segment
+      const int a0 = (o0 / (2 * w)) * (2 * w);  // its pair
+      const uint64_t* A = src + run.x + a0;
+      const int la = min(w, run.y - a0);
+      const uint64_t* B = A + la;
+      const int lb = max(0, min(w, run.y - a0 - la));
+      const int seg = min(kTieChunk, run.y - o0);
+      constexpr int kPer = kTieChunk / kNT;
+      int d = (o0 - a0) + (int)threadIdx.x * kPer;
+      const int dend = min((o0 - a0) + seg, d + kPer);
+      if (d < dend) {
+        int lo = max(0, d - lb), hi = min(d, la);  // merge path: i from A, d - i from B (unique keys)
+        while (lo < hi) {
+          const int i = (lo + hi) / 2;
+          if (A[i] < B[d - i - 1]) lo = i + 1;
+          else hi = i;
+        }
+        int i = lo, j = d - lo;
+        uint64_t* out = dst + run.x + a0;
+        for (; d < dend; ++d) {
+          const bool takeA = j >= lb || (i < la && A[i] < B[j]);
+          out[d] = takeA ? A[i++] : B[j++];
+        }
+      }
+    }
+    uint64_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  grid.sync();
+  for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
+    const int r = tie_task_run(big_runs, nbig, g);
+    const int4 run = big_runs[r];
+    if (run.y <= kTieChunk) continue;
+    const int o0 = (g - run.z) * kTieChunk, seg = min(kTieChunk, run.y - o0);
+    for (int i = threadIdx.x; i < seg; i += kNT)
+      tie_put(perm, skl, (int64_t)run.x + o0 + i, src[(int64_t)run.x + o0 + i]);
+  }
 }
 
 // ------------------------------------------------------------- topology ---
@@ -405,12 +594,6 @@ __device__ __forceinline__ int lcp_digits(uint64_t ah, uint64_t al, uint64_t bh,
   return 32;
 }
 
-__global__ void k_gather_lo_lcp(const int* perm, const uint64_t* kl, const uint64_t* skh,
-                                uint64_t* skl, int64_t n, const unsigned* run_if) {
-  if (run_if && *run_if == 0) return;
-  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (t < n) skl[t] = kl[perm[t]];
-}
 
 __device__ __forceinline__ int lm_of(const int* L, int64_t a) { return a > 0 ? L[a - 1] : -1; }
 
@@ -430,19 +613,30 @@ __device__ __forceinline__ void starts(const int* L, int64_t n, int64_t a, int& 
 }
 
 
+// lcp(a, x) >= l from the sorted keys: levels <= 21 need key_hi only (one
+// 8-B load per probe); key_lo is read only when the key_hi are equal -- which
+// only happens when neighbours tie (the lazily computed key_lo exists then)
+__device__ __forceinline__ bool prefix_ge(uint64_t ah, uint64_t al, const uint64_t* kh,
+                                          const uint64_t* kl, int64_t x, int l) {
+  const uint64_t bh = kh[x];
+  if (l <= 21) return ((ah ^ bh) >> (3 * (21 - l))) == 0;
+  if (ah != bh) return false;
+  return ((al ^ kl[x]) >> (3 * (32 - l))) == 0;
+}
+
 // largest b >= a with lcp(a, b) >= l
 __device__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t n, int64_t a,
                                 int l) {
-  const uint64_t ah = kh[a], al = kl[a];
+  const uint64_t ah = kh[a], al = l > 21 ? kl[a] : 0;
   int64_t step = 1, good = a;
-  while (a + step < n && lcp_digits(ah, al, kh[a + step], kl[a + step]) >= l) {
+  while (a + step < n && prefix_ge(ah, al, kh, kl, a + step, l)) {
     good = a + step;
     step <<= 1;
   }
   int64_t lo = good, hi = min(n - 1, a + step);  // lo good, (hi bad or end)
   while (hi > lo) {
     const int64_t mid = lo + (hi - lo + 1) / 2;
-    if (lcp_digits(ah, al, kh[mid], kl[mid]) >= l) lo = mid;
+    if (prefix_ge(ah, al, kh, kl, mid, l)) lo = mid;
     else hi = mid - 1;
   }
   return lo;
@@ -450,16 +644,16 @@ __device__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t 
 
 // smallest s <= a with lcp(s, a) >= l
 __device__ int64_t search_left(const uint64_t* kh, const uint64_t* kl, int64_t a, int l) {
-  const uint64_t ah = kh[a], al = kl[a];
+  const uint64_t ah = kh[a], al = l > 21 ? kl[a] : 0;
   int64_t step = 1, good = a;
-  while (a - step >= 0 && lcp_digits(ah, al, kh[a - step], kl[a - step]) >= l) {
+  while (a - step >= 0 && prefix_ge(ah, al, kh, kl, a - step, l)) {
     good = a - step;
     step <<= 1;
   }
   int64_t hi = good, lo = max((int64_t)0, a - step);
   while (hi > lo) {
     const int64_t mid = lo + (hi - lo) / 2;
-    if (lcp_digits(ah, al, kh[mid], kl[mid]) >= l) hi = mid;
+    if (prefix_ge(ah, al, kh, kl, mid, l)) hi = mid;
     else lo = mid + 1;
   }
   return hi;
@@ -1104,6 +1298,34 @@ static int scan_ints(const int* L, int64_t n, int* out, DBuf& scratch, cudaStrea
   return GS_OK;
 }
 
+// k_tie_sort as a cooperative launch: as many CTAs as can be co-resident (at
+// most 2 per SM), so grid.sync() is legal
+static int tie_sort(const Device& dev, int prec, const void* rec, DevTree& t, unsigned* ctr,
+                    cudaStream_t st) {
+  static int per_sm[2] = {0, 0};
+  const int pi = prec == kF32 ? 0 : 1;
+  void* fn = prec == kF32 ? (void*)k_tie_sort<float> : (void*)k_tie_sort<double>;
+  if (!per_sm[pi]) {
+    int b = 0;
+    GS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kNT, 0));
+    per_sm[pi] = std::max(1, std::min(2, b));
+  }
+  const int grid = std::max(1, std::min(nblocks(t.n, kNT), per_sm[pi] * dev.sms));
+  const uint64_t* skh = t.skey_hi.as<uint64_t>();
+  const double* root = t.root.as<double>();
+  const int2* small_runs = (const int2*)t.tmp_v.ptr;
+  int4* big_runs = (int4*)t.tmp_v2.ptr;
+  int* perm = t.perm.as<int>();
+  uint64_t* skl = t.skey_lo.as<uint64_t>();
+  uint64_t* bufa = t.tmp_k.as<uint64_t>();
+  uint64_t* bufb = t.key_lo.as<uint64_t>();
+  const unsigned* cctr = ctr;
+  void* args[] = {(void*)&rec, (void*)&skh, (void*)&root, (void*)&cctr, (void*)&small_runs,
+                  (void*)&big_runs, (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb};
+  GS_CUDA_OK(cudaLaunchCooperativeKernel(fn, grid, kNT, args, 0, st));
+  return GS_OK;
+}
+
 int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
                DevTree& t, cudaStream_t st, const double* root_box, int* overflow) {
   t.prec = prec;
@@ -1143,18 +1365,12 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
-  // 3. stable LSD radix sort by (key_hi, key_lo, index). key_lo (levels
-  // 22-32) only orders points that share all 21 levels of key_hi -- almost
-  // never outside depth-32 clusters -- so: 8 passes over key_hi with the index
-  // as value (ties keep ascending index), a check for equal neighbours, and
-  // only if there is one the full sort, whose kernels otherwise return at once:
-  //   hi: (key_hi, index) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
-  //   [ties] lo: (key_lo, index) -> (tmp_k, tmp_v) -> (skey_lo, tmp_v2) -> ... -> (tmp_k, tmp_v)
-  //          hi: (skey_lo := key_hi[tmp_v], tmp_v) -> (tmp_k, tmp_v2) -> ... -> (skey_hi, perm)
-  // 8-bit digits, no copies (buffers ping-pong); ties in all 32 levels
-  // (depth-32 buckets) keep ascending index.
+  // 3. order by the full key (key_hi, key_lo, index): a stable LSD radix sort
+  // of key_hi with the index as value -- 8 passes of 8-bit digits, ping-pong
+  //   (key_hi, index) -> (tmp_k, tmp_v2) -> (skey_hi, perm) -> ... -> (skey_hi, perm)
+  // -- then the runs of equal key_hi (only below the 21st level: duplicates,
+  // depth-32 clusters) sorted in place by (key_lo, index) (k_tie_runs/_sort).
   // keys per thread: small tiles (more CTAs) for small n, 8 from ~0.5M points
-  // (measured sort per build: 50k 0.22 ms at 4 vs 0.28 at 8; 1M 0.48 at 8 vs 0.52 at 4)
   static const int ipt_env = [] {
     const char* e = std::getenv("GS_RS_IPT");
     const int v = e ? std::atoi(e) : 0;
@@ -1163,60 +1379,36 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
   const int ntiles = nblocks(n, kRsNT * ipt);
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
-  // one-sweep scratch: 13 digit histograms (5 lo + 8 hi), 32 counters (21
-  // passes' tile counters, the tie flag), 21 x ntiles x 256 look-back status
-  // words -- zeroed by one memset
-  constexpr int kHist = 13, kPasses = 21;
-  const size_t words = (size_t)kHist * 256 + 32 + (size_t)kPasses * ntiles * 256;
+  // one-sweep scratch: 8 digit histograms, 32 counters (8 passes' tile
+  // counters; the tie lists' counters and flag), 8 x ntiles x 256 look-back
+  // status words -- zeroed by one memset
+  constexpr int kPasses = 8;
+  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256;
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
   GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
   unsigned* hist = t.hist.as<unsigned>();
-  unsigned* ctr = hist + kHist * 256;
-  unsigned* tie = ctr + 31;
+  unsigned* ctr = hist + kPasses * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist + 5 * 256);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist + 5 * 256);
-  // pass q (0..20) over digit histogram hq (0..4 lo, 5..12 hi)
-  auto pass = [&](const uint64_t* ki, const int* vi, uint64_t* ko, int* vo, int shift, int q, int hq,
-                  const unsigned* run_if) {
-    unsigned* dq = desc + (size_t)q * ntiles * 256;
-    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + hq * 256, dq, ctr + q, run_if);
-    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, hist + hq * 256, dq, ctr + q, run_if);
-  };
-  auto hi_sort = [&](const uint64_t* ka, const int* va, int q0, const unsigned* run_if) {
-    for (int p = 0; p < 8; ++p) {
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
+  {
+    const uint64_t* ka = t.key_hi.as<uint64_t>();
+    const int* va = nullptr;  // first pass: the value is the index
+    for (int p = 0; p < kPasses; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      pass(ka, va, kb, vb, 8 * p, q0 + p, 5 + p, run_if);
-      ka = kb;
-      va = vb;
-    }
-  };
-  hi_sort(t.key_hi.as<uint64_t>(), nullptr, 0, nullptr);  // values: the index
-  k_tie_check<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), n, tie);
-  // [ties only] key_lo and its digit histograms
-  if (prec == kF32)
-    k_keys_lo<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), tie);
-  else
-    k_keys_lo<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), tie);
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 5 * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, nullptr, 0, n, hist, tie);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, 5 * 256 * 4, st>>>(t.key_lo.as<uint64_t>(), 5, nullptr, 0, n, hist, tie);
-  {
-    const uint64_t* ka = t.key_lo.as<uint64_t>();
-    const int* va = nullptr;  // implicit: the index
-    for (int p = 0; p < 5; ++p) {
-      uint64_t* kb = (p & 1) ? t.skey_lo.as<uint64_t>() : t.tmp_k.as<uint64_t>();
-      int* vb = (p & 1) ? t.tmp_v2.as<int>() : t.tmp_v.as<int>();
-      pass(ka, va, kb, vb, 8 * p, 8 + p, p, tie);
+      onesweep(ipt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
+               desc + (size_t)p * ntiles * 256, ctr + p);
       ka = kb;
       va = vb;
     }
   }
-  k_gather_u64<<<nb, kNT, 0, st>>>(t.tmp_v.as<int>(), t.key_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, tie);
-  hi_sort(t.skey_lo.as<uint64_t>(), t.tmp_v.as<int>(), 13, tie);
+  // ties: runs of equal key_hi sorted by (key_lo, index) in place (perm,
+  // skey_lo of the run members); tmp_v / tmp_v2 hold the run lists, tmp_k /
+  // key_lo the long runs' merge buffers (all free after the key_hi sort)
+  k_tie_runs<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), n, ctr, (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr);
+  GS_TRY_INT(tie_sort(dev, prec, rec, t, ctr, st));
   GS_CUDA_OK(cudaGetLastError());
-  // sorted key_lo: only consulted where sorted key_hi neighbours are equal
-  k_gather_lo_lcp<<<nb, kNT, 0, st>>>(t.perm.as<int>(), t.key_lo.as<uint64_t>(), t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, tie);
   kt_mark(3, st);
   kt_mark(4, st);
   // 4. topology
@@ -1292,16 +1484,15 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   unsigned* hist = t.hist.as<unsigned>();
   unsigned* ctr = hist + 8 * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, 8 * 256 * 4, st>>>(nullptr, 0, t.key_hi.as<uint64_t>(), 8, n, hist);
+  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
+  else k_rs_hist_all<4><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
   const uint64_t* ka = t.key_hi.as<uint64_t>();
   const int* va = nullptr;
   for (int p = 0; p < 8; ++p) {  // (key_hi, index) -> (tmp_k, tmp_v) -> (skey_hi, perm) -> ...
     uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
     int* vb2 = (p & 1) ? t.perm.as<int>() : t.tmp_v.as<int>();
     unsigned* dq = desc + (size_t)p * ntiles * 256;
-    if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
-    else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
+    onesweep(ipt, ntiles, st, ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
     ka = kb;
     va = vb2;
   }

@@ -66,6 +66,20 @@ SETS = {
                                              + [c + uniform(2_000, 1e-8, 13 + k) for k, c in
                                                 enumerate(uniform(20, 1.0, 40))]),
                               sym_uniform(120_000, 1.0, 14)),
+    # one run of 12k equal 63-bit keys: k_tie_sort's chunked bitonic sort +
+    # three merge passes
+    "cluster_12k": lambda: (np.concatenate([uniform(12_000, 1e-7, 15), np.array([[-1e3, -1e3, -1e3],
+                                                                                [1e3, 1e3, 1e3]])]),
+                            sym_uniform(12_002, 1.0, 16)),
+    # the whole cloud in one run (a root box that dwarfs the points, as after a
+    # diverged flow): 50 sorted chunks merged over the grid in 6 passes
+    "one_run_100k": lambda: (np.concatenate([uniform(100_000, 1.0, 21), np.array([[-1e7, -1e7, -1e7],
+                                                                                 [1e7, 1e7, 1e7]])]),
+                             sym_uniform(100_002, 1.0, 22)),
+    # thousands of short runs (warp-sorted): exact triplicates (ordered by
+    # index) and near pairs that differ below level 21 (ordered by key_lo)
+    "short_runs": lambda: (lambda b: (np.concatenate([b, b[:100], b[:100], b[100:500] + uniform(400, 1e-8, 18)])[
+        np.random.default_rng(19).permutation(6600)], sym_uniform(6600, 1.0, 20)))(uniform(6000, 1.0, 17)),
     "corners": lambda: (np.array([[1.0 if i & 1 else -1.0, 1.0 if i & 2 else -1.0,
                                    1.0 if i & 4 else -1.0] for i in range(8)]), np.zeros((8, 3))),
 }
