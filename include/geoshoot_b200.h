@@ -326,6 +326,16 @@ gs_status gs_flow_profile_phases(gs_flow* flow, double* ms, int64_t* counts, int
 gs_status gs_profile(gs_ctx* ctx, int32_t enable);
 gs_status gs_profile_phases(gs_ctx* ctx, double* ms, int64_t* counts, int32_t channels);
 
+/* Kernel start-time trace (profiling; valid inside captured CUDA graphs,
+ * where host events cannot look): while enabled, every traced kernel of the
+ * tree build, the Barnes-Hut walks and the epilogues appends {tag, device
+ * %globaltimer ns} when its first CTA starts; tag = unit << 16 | source line
+ * (unit 1 tree.cu, 2 bh.cu, 3 epilogue.cu). gs_trace_read copies up to max
+ * entries, returns their number in *count and clears the trace. */
+gs_status gs_trace(gs_ctx* ctx, int32_t enable);
+gs_status gs_trace_read(gs_ctx* ctx, uint64_t* tags, uint64_t* times_ns, int64_t max,
+                        int64_t* count);
+
 /* Sharded stage API (one rank = one flow): */
 gs_status gs_flow_set_shard(gs_flow* flow, int64_t shard_begin, int64_t shard_count);
 /* Device pointer and byte size of the packed per-point source records

@@ -131,6 +131,8 @@ SIGNATURES = [
     ("gs_ctx_peer_stores", C.c_int32, [_vp]),
     ("gs_profile", _st, [_vp, C.c_int32]),
     ("gs_profile_phases", _st, [_vp, _d, C.POINTER(_i64), C.c_int32]),
+    ("gs_trace", _st, [_vp, C.c_int32]),
+    ("gs_trace_read", _st, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _i64, C.POINTER(_i64)]),
     ("gs_shoot_forward", _st, [_vp, C.POINTER(gs_config), _i64, _d, _d, _d, _d, _d, _d, _d,
                                C.POINTER(gs_stats)]),
     ("gs_objective", _st, [_vp, C.POINTER(gs_config), _i64, _d, _d, _d, C.POINTER(gs_report)]),

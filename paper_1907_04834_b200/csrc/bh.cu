@@ -34,6 +34,8 @@
 
 #include "bh.h"
 #include "gs_exp.cuh"
+#define GS_TRACE_TU 2
+#include "trace.cuh"
 
 namespace gsb {
 
@@ -403,6 +405,7 @@ __device__ __forceinline__ int claim_block(int* sm_ctr, int nblk) {
 // window bookkeeping (registers and instructions) for large N.
 template <typename R, int MODE, bool WIN, bool LMD = false>
 __global__ void __launch_bounds__(kBhNT, (ws_min_blocks<R, MODE, WIN>())) k_bh_ws(const BhArgs<R> a) {
+  GS_TRACE_HERE();
   const int blk = (!WIN && a.sm_ctr) ? claim_block(a.sm_ctr, gridDim.x) : (int)blockIdx.x;
   V4<R> x, xs, px, ai, bi;
   const int out = load_query<R, MODE>(a, blk * kBhNT + threadIdx.x, x, xs, px, ai, bi);
@@ -606,6 +609,7 @@ __device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Ac
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
+  GS_TRACE_HERE();
   V4<R> x, xs, px, ai, bi;
   const int out = load_query<R, MODE>(a, blockIdx.x * kBhNT + threadIdx.x, x, xs, px, ai, bi);
   if (a.split && !(warp_box_diag2<R>(x, out >= 0) <= a.grp_lim2)) return;  // k_bh_ws's warp
@@ -877,6 +881,7 @@ BhArgs<R> make_args(DevTree& t, double sigma, double thr, const BhQuery& q) {
 // Per-query counters of K node windows: out[i] = sum over windows in order.
 __global__ void k_fold_counts(const uint32_t* __restrict__ in, int K, int64_t n3,
                               uint32_t* __restrict__ out) {
+  GS_TRACE_HERE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n3) return;
   uint32_t v = 0;
@@ -985,6 +990,7 @@ int bh_forward_stage(const Device& dev, int prec, const KernelConsts& kc, const 
                      cudaStream_t st, int64_t* launches, int* energy_blocks, gs_stats*) {
   DevTree& t = tree_for(w);
   kt_mark(1, st);
+  t.lean = true;  // walked only: no FP64 node sums / boxes
   GS_TRY_INT(tree_build(dev, prec, kc, rec, n, t, st, nullptr, e.bad_step ? e.bad_step + 1 : nullptr));
   kt_mark(1, st);
   int dense = 0;
@@ -1028,6 +1034,7 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
     t = w.kept[k].get();
   } else {
     t = &w.cur;
+    t->lean = true;
     GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, *t, st));
   }
   GS_TRY_INT(tree_accumulate(prec, *t, adj, st));
@@ -1061,6 +1068,7 @@ int bh_backward_step(const Device& dev, int prec, const KernelConsts& kc, const 
 int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const gs_config& cfg,
                      const void* rec_k, int64_t n, void* ev, int64_t m, BhWork& w, VelEpi e,
                      cudaStream_t st) {
+  w.cur.lean = true;
   GS_TRY_INT(tree_build(dev, prec, kc, rec_k, n, w.cur, st));
   int dense = 0;
   const int K = bh_tasks(m, n, cfg.threshold_multiplier * cfg.sigma, kc, &dense);
@@ -1076,6 +1084,11 @@ int bh_velocity_step(const Device& dev, int prec, const KernelConsts& kc, const 
   e.S = K;
   e.part = w.part.ptr;
   GS_TRY_INT(vel_epilogue(prec, e, st));
+  return GS_OK;
+}
+
+int trace_install_bh(unsigned long long* buf) {
+  GS_CUDA_OK(trace_install_here(buf));
   return GS_OK;
 }
 

@@ -42,6 +42,7 @@ struct DevTree {
   DBuf root;            // double[6] padded root box
   // radix-sort scratch
   DBuf tmp_k, tmp_v, tmp_v2, hist;
+  DBuf tie_scr;         // k_tie_sort's digit counts (long runs of equal key_hi)
   DBuf scan_tmp;
   DBuf sm_ctr;          // i32 [1024] per-SM query-block counters of the walk (k_bh_ws)
   DBuf pq_win;          // u32 [windows][queries][3] per-window per-query counters (folded)
@@ -49,6 +50,10 @@ struct DevTree {
   KernelConsts kc{};
   double thr = 0.0;
   bool adj_valid = false;
+  // lean: the aggregates write only the traversal records (nrec / nadj), not
+  // the FP64 node sums and boxes that downloads and rescales read -- set by
+  // the flows, whose trees are only ever walked
+  bool lean = false;
 };
 
 // root_box (host, {lo xyz, hi xyz}) overrides the padded bounding box

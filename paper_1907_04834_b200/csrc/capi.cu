@@ -530,7 +530,7 @@ uint64_t flow_sig(const gs_flow* f) {
   for (const DBuf* b : {&t.key_hi, &t.key_lo, &t.perm, &t.skey_hi, &t.skey_lo, &t.lcp, &t.first,
                         &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.lo,
                         &t.hi, &t.cen, &t.mom, &t.nrec, &t.nadj, &t.psum, &t.msum,
-                        &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist,
+                        &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist, &t.tie_scr,
                         &t.scan_tmp, &t.scal, &t.outer, &t.parts, &t.start, &t.sm_ctr})
     mix(*b);
   return h;
@@ -793,6 +793,50 @@ gs_status gs_profile_phases(gs_ctx* c, double* ms, int64_t* counts, int32_t chan
   if (!c || !c->timer) return bad_arg("profiling not enabled");
   GS_CUDA_OK(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < channels && k < KTimer::kChannels; ++k) ms[k] = c->timer->drain(k, counts + k);
+  return GS_OK;
+}
+
+namespace {
+unsigned long long* g_trace_buf = nullptr;  // device: [0] count, then {tag, t} pairs (trace.cuh)
+constexpr int64_t kTraceCap = 16384;
+}  // namespace
+
+gs_status gs_trace(gs_ctx* c, int32_t enable) {
+  if (!c) return bad_arg("null context");
+  GS_CUDA_OK(cudaSetDevice(c->dev.id));
+  GS_CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (enable && !g_trace_buf) {
+    GS_CUDA_OK(cudaMalloc(&g_trace_buf, sizeof(unsigned long long) * (1 + 2 * kTraceCap)));
+    GS_CUDA_OK(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long)));
+  }
+  unsigned long long* b = enable ? g_trace_buf : nullptr;
+  GS_TRY(trace_install_tree(b));
+  GS_TRY(trace_install_bh(b));
+  GS_TRY(trace_install_epi(b));
+  if (!enable && g_trace_buf) {
+    GS_CUDA_OK(cudaFree(g_trace_buf));
+    g_trace_buf = nullptr;
+  }
+  return GS_OK;
+}
+
+gs_status gs_trace_read(gs_ctx* c, uint64_t* tags, uint64_t* times_ns, int64_t max, int64_t* count) {
+  if (!c || !count || (max > 0 && (!tags || !times_ns))) return bad_arg("null argument");
+  if (!g_trace_buf) return bad_arg("tracing not enabled");
+  GS_CUDA_OK(cudaStreamSynchronize(c->stream));
+  unsigned long long k = 0;
+  GS_CUDA_OK(cudaMemcpy(&k, g_trace_buf, sizeof k, cudaMemcpyDeviceToHost));
+  const int64_t got = std::min<int64_t>({(int64_t)k, kTraceCap, max});
+  std::vector<unsigned long long> h(2 * std::max<int64_t>(got, 1));
+  if (got > 0)
+    GS_CUDA_OK(cudaMemcpy(h.data(), g_trace_buf + 1, sizeof(unsigned long long) * 2 * got,
+                          cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < got; ++i) {
+    tags[i] = h[2 * i];
+    times_ns[i] = h[2 * i + 1];
+  }
+  *count = got;
+  GS_CUDA_OK(cudaMemset(g_trace_buf, 0, sizeof(unsigned long long)));
   return GS_OK;
 }
 

@@ -93,6 +93,11 @@ inline void kt_mark(int ch, cudaStream_t st) {
   if (g_ktimer) g_ktimer->mark(ch, st);
 }
 
+// kernel start-time trace (trace.cuh): installs the buffer in each traced unit
+int trace_install_tree(unsigned long long* buf);
+int trace_install_bh(unsigned long long* buf);
+int trace_install_epi(unsigned long long* buf);
+
 inline size_t vec_bytes(int prec) { return prec == kF32 ? sizeof(float4) : sizeof(double4); }
 
 // ---- exact RHS in Morton order with the FP32 underflow cutoff (allpairs.cu)

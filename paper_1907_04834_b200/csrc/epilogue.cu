@@ -11,6 +11,8 @@
 // Backward: the adjoint update alpha += dt (pq - qq), beta += dt (pp - qp)
 // (shooting.cpp:211-214).
 #include "engine.h"
+#define GS_TRACE_TU 3
+#include "trace.cuh"
 
 namespace gsb {
 
@@ -47,6 +49,7 @@ constexpr int kEpiNT = 256;
 
 template <typename R>
 __global__ void __launch_bounds__(kEpiNT) k_fwd_epi(FwdEpi e) {
+  GS_TRACE_HERE();
   const int t = blockIdx.x * kEpiNT + threadIdx.x;
   double edot = 0.0;
   if (t < e.n_tgt) {
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(kEpiNT) k_fwd_epi(FwdEpi e) {
 
 template <typename R>
 __global__ void __launch_bounds__(kEpiNT) k_bwd_epi(BwdEpi e) {
+  GS_TRACE_HERE();
   const int t = blockIdx.x * kEpiNT + threadIdx.x;
   if (t >= e.n_tgt) return;
   const int i = e.tgt_begin + t;
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(kEpiNT) k_bwd_epi(BwdEpi e) {
 
 template <typename R>
 __global__ void __launch_bounds__(kEpiNT) k_vel_epi(VelEpi e) {
+  GS_TRACE_HERE();
   const int t = blockIdx.x * kEpiNT + threadIdx.x;
   if (t >= e.m) return;
   const Vec<R> A = fold<R>(static_cast<const V4<R>*>(e.part), e.S, e.m, 1, t, 0);
@@ -240,7 +245,10 @@ __global__ void __launch_bounds__(kEpiNT) k_adj_init(const V4<R>* recT, const do
   if (threadIdx.x == 0 && sse_part) sse_part[blockIdx.x] = s;
 }
 
-__global__ void k_step_inc(int* c) { *c += 1; }
+__global__ void k_step_inc(int* c) {
+  GS_TRACE_HERE();
+  *c += 1;
+}
 
 __global__ void k_reduce(const double* part, int count, double* out) {
   // one warp, fixed order per lane then fixed tree: deterministic
@@ -397,6 +405,11 @@ int step_counter_inc(int* counter, cudaStream_t st) {
 int reduce_sum(const double* part, int count, double* out, cudaStream_t st) {
   k_reduce<<<1, 32, 0, st>>>(part, count, out);
   GS_CUDA_OK(cudaGetLastError());
+  return GS_OK;
+}
+
+int trace_install_epi(unsigned long long* buf) {
+  GS_CUDA_OK(trace_install_here(buf));
   return GS_OK;
 }
 

@@ -103,3 +103,37 @@ struct StatusCode {
   } while (0)
 
 }  // namespace gsb
+
+// Programmatic dependent launch (PDL): kernels launched with pdl_launch()
+// may be scheduled while their predecessor in the stream is still running;
+// GS_PDL_ENTRY, the first statement of every such kernel, lets the NEXT
+// kernel start launching (its CTAs then park at their own entry) and waits
+// for the predecessor's completion and memory before touching its outputs.
+// In a kernel launched normally both instructions are no-ops. Chains of short
+// dependent kernels (the tree build) overlap each launch with the previous
+// kernel's tail instead of paying it in full.
+#ifndef GS_TRACE_HERE
+#define GS_TRACE_HERE() ((void)0)  // trace.cuh: kernel start times (GS_TRACE tooling)
+#endif
+#define GS_PDL_ENTRY()                                         \
+  do {                                                         \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");         \
+    GS_TRACE_HERE();                                           \
+  } while (0)
+
+template <typename... P, typename... A>
+inline cudaError_t pdl_launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<A&&>(args)...);
+}

@@ -26,6 +26,8 @@
 #include <cuda/atomic>
 
 #include "bh.h"
+#define GS_TRACE_TU 1
+#include "trace.cuh"
 
 namespace gsb {
 
@@ -38,6 +40,7 @@ inline int nblocks(int64_t n, int nt) { return (int)std::max<int64_t>(1, (n + nt
 // ------------------------------------------------------------------ bbox ---
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, double* part) {
+  GS_PDL_ENTRY();
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
     const V4<R> q = ld4(rec + 2 * i);
@@ -71,6 +74,7 @@ __global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, doubl
 
 // root = [lo - pad, hi + pad], pad = 1e-9 * (hi - lo)   (octree.cpp:9,27-35)
 __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, double* root) {
+  GS_PDL_ENTRY();
   __shared__ double s[6][kNT / 32];
   double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
   for (int b = threadIdx.x; b < nb; b += kNT)
@@ -106,6 +110,7 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
                                               uint64_t* kh) {
+  GS_PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= n) return;
   const V4<R> q = ld4(rec + 2 * i);
@@ -179,6 +184,7 @@ constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a temp
 
 // exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
 __global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
+  GS_PDL_ENTRY();
   __shared__ unsigned sums[1024];
   const int64_t per = (count + 1023) / 1024;
   const int64_t b = threadIdx.x * per, e = min(count, b + per);
@@ -214,6 +220,7 @@ constexpr unsigned kRsFlagAgg = 1u << 30, kRsFlagPrefix = 2u << 30, kRsCountMask
 // digit histograms of all 8 passes in one read of the keys
 template <int kRsIPT>
 __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int64_t n, unsigned* hist) {
+  GS_PDL_ENTRY();
   __shared__ unsigned hs[8 * 256];
   for (int t = threadIdx.x; t < 8 * 256; t += kRsNT) hs[t] = 0;
   __syncthreads();
@@ -237,6 +244,7 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
                                                       unsigned* desc, unsigned* tile_ctr) {
+  GS_PDL_ENTRY();
   constexpr int kTile = kRsNT * kRsIPT;
   __shared__ unsigned wh[kRsNT / 32][256];  // per-warp digit counts -> offsets within the tile's digit run
   __shared__ unsigned wsum[2][kRsNT / 32];  // per-warp sums of the two digit scans
@@ -371,31 +379,36 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
 }
 
 // one one-sweep pass, IPT keys per thread
-void onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi, uint64_t* ko,
+int onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi, uint64_t* ko,
               int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc, unsigned* ctr) {
-  if (ipt == 8) k_rs_onesweep<8><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, dig_tot, desc, ctr);
-  else k_rs_onesweep<4><<<ntiles, kRsNT, 0, st>>>(ki, vi, ko, vo, n, shift, dig_tot, desc, ctr);
+  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_onesweep<8>, ntiles, kRsNT, 0, st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  else GS_CUDA_OK(pdl_launch(k_rs_onesweep<4>, ntiles, kRsNT, 0, st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  return GS_OK;
 }
 
 // ---------------------------------------------------------------- ties ---
 // Points sharing all 21 levels of key_hi form runs of equal keys in the
 // key_hi-sorted order (the sort is stable: a run is in ascending index). The
-// full order sorts each run by (key_lo, index) -- key_lo (levels 22-32) is
-// computed for the run members only, as the unique 64-bit code
+// full order sorts each run stably by key_lo (levels 22-32), computed for the
+// run members only and carried with the index as the 64-bit code
 // (key_lo << 31) | index. k_tie_runs lists the runs (and sets the tie flag);
-// k_tie_sort, one cooperative grid, sorts them in place: a warp per run of
-// <= 32 points (rank by comparison); longer runs in 2048-code chunks (bitonic
-// sort in shared memory, a CTA per chunk across all runs), then merge passes
-// (w -> 2w) whose 2048-output segments are spread over the grid (merge path),
-// grid-synchronised. Two launches whatever the data -- no second full-key
-// radix sort behind no-op launches -- and a single run of the whole cloud (a
-// diverged flow whose root box dwarfs the points) still uses every SM.
+// k_tie_sort, one cooperative grid, sorts them in place:
+//  * a run of <= 32 points: a warp, rank by comparison;
+//  * a run of <= 2048 points: a CTA, bitonic sort in shared memory;
+//  * longer runs (a diverged flow whose root box dwarfs the cloud -- config
+//    4's puts 77 % of the points in such runs): a segmented LSD radix sort of
+//    key_lo, 5 passes of 8 bits over 2048-point chunks spread across the
+//    grid: per-chunk digit counts, per-run offsets (run-local, digit-major),
+//    stable scatter (warp match.any ranking as in k_rs_onesweep) -- each pass
+//    three grid.sync()s apart.
+// Two launches whatever the data, and no no-op passes when there is no tie.
 namespace cg = cooperative_groups;
 constexpr int kTieChunk = 2048;
-constexpr int kTieSmallCtr = 28, kTieBigCtr = 29, kTieMaxLen = 30, kTieFlag = 31;  // sort counters
+constexpr int kTieSmallCtr = 28, kTieBigCtr = 29, kTieFlag = 31;  // sort counters
 
 __global__ void k_tie_runs(const uint64_t* skh, int64_t n, unsigned* ctr, int2* small_runs,
                            int4* big_runs) {
+  GS_PDL_ENTRY();
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t + 1 >= n) return;
   const uint64_t k = skh[t];
@@ -413,12 +426,8 @@ __global__ void k_tie_runs(const uint64_t* skh, int64_t n, unsigned* ctr, int2* 
     else hi = mid - 1;
   }
   const int len = (int)(lo - t + 1);
-  if (len <= 32) {
-    small_runs[atomicAdd(ctr + kTieSmallCtr, 1u)] = make_int2((int)t, len);
-  } else {
-    big_runs[atomicAdd(ctr + kTieBigCtr, 1u)] = make_int4((int)t, len, 0, 0);
-    atomicMax(ctr + kTieMaxLen, (unsigned)len);
-  }
+  if (len <= 32) small_runs[atomicAdd(ctr + kTieSmallCtr, 1u)] = make_int2((int)t, len);
+  else big_runs[atomicAdd(ctr + kTieBigCtr, 1u)] = make_int4((int)t, len, 0, 0);
   atomicOr(ctr + kTieFlag, 1u);
 }
 
@@ -455,28 +464,64 @@ __device__ void bitonic_smem(uint64_t* s, int P) {
     }
 }
 
-// chunk task g -> (big run, chunk in it): binary search over the runs' chunk
-// prefix (.z); returns the run index
+// exclusive prefix of f(run) over the long-run list by CTA 0 (block scan in
+// rounds of kNT runs); writes it through put(run, prefix), returns the total
+template <typename F, typename P>
+__device__ int tie_prefix(int nbig, F f, P put) {
+  __shared__ int s_carry;
+  __shared__ int ws[kNT / 32];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nbig; b0 += kNT) {
+    const int r = b0 + threadIdx.x;
+    const int c = r < nbig ? f(r) : 0;
+    int v = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int add = s_carry;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) add += ws[w];
+    if (r < nbig) put(r, add + v - c);
+    __syncthreads();
+    if (threadIdx.x == kNT - 1) s_carry = add + v;
+    __syncthreads();
+  }
+  return s_carry;
+}
+
+// task g -> the run whose task prefix (field F of the list) covers it
+template <int F>
 __device__ __forceinline__ int tie_task_run(const int4* big, int nbig, int g) {
   int lo = 0, hi = nbig - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) / 2;
-    if (big[mid].z <= g) lo = mid;
+    if ((F == 2 ? big[mid].z : big[mid].w) <= g) lo = mid;
     else hi = mid - 1;
   }
   return lo;
 }
+
+constexpr int kTieGroup = 16;  // chunks per digit-count group (look-up of a chunk's offsets)
 
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64_t* skh,
                                                   const double* root, const unsigned* ctr,
                                                   const int2* small_runs, int4* big_runs,
                                                   int* perm, uint64_t* skl, uint64_t* bufa,
-                                                  uint64_t* bufb) {
+                                                  uint64_t* bufb, unsigned* scr) {
+  GS_PDL_ENTRY();
   if (ctr[kTieFlag] == 0) return;  // (uniform over the grid)
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s[kTieChunk];
-  const int lane = threadIdx.x & 31;
+  __shared__ unsigned wh[kNT / 32][256];
+  __shared__ unsigned soff[256];
+  __shared__ unsigned ws[kNT / 32];
+  __shared__ int s_nt[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // runs of <= 32 points: a warp each, rank = number of smaller codes
   const int nsmall = (int)ctr[kTieSmallCtr];
   const int gw = (blockIdx.x * kNT + threadIdx.x) >> 5, nw = (gridDim.x * kNT) >> 5;
@@ -490,98 +535,171 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
   }
   const int nbig = (int)ctr[kTieBigCtr];
   if (nbig == 0) return;
-  // chunk prefix over the long runs (.z), by CTA 0
+  // task numbering (CTA 0): .z = chunk prefix over all long runs (phase A);
+  // .w = slot prefix of the multi-chunk runs' chunks, each run padded to
+  // whole groups of kTieGroup slots; totals in the sentinel big_runs[nbig]
   if (blockIdx.x == 0) {
-    __shared__ int s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < nbig; b0 += kNT) {
-      const int r = b0 + threadIdx.x;
-      const int c = r < nbig ? (big_runs[r].y + kTieChunk - 1) / kTieChunk : 0;
-      int v = c;  // inclusive block scan
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      __shared__ int ws[kNT / 32];
-      if (lane == 31) ws[threadIdx.x >> 5] = v;
-      __syncthreads();
-      int add = s_carry;
-      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) add += ws[w];
-      if (r < nbig) big_runs[r].z = add + v - c;
-      __syncthreads();
-      if (threadIdx.x == kNT - 1) s_carry = add + v;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) big_runs[nbig].z = s_carry;  // total chunks (sentinel entry)
+    const int ta = tie_prefix(nbig, [&](int r) { return (big_runs[r].y + kTieChunk - 1) / kTieChunk; },
+                              [&](int r, int v) { big_runs[r].z = v; });
+    const int tb = tie_prefix(nbig, [&](int r) {
+      const int L = big_runs[r].y;
+      const int nc = (L + kTieChunk - 1) / kTieChunk;
+      return L > kTieChunk ? (nc + kTieGroup - 1) / kTieGroup * kTieGroup : 0; },
+      [&](int r, int v) { big_runs[r].w = v; });
+    if (threadIdx.x == 0) big_runs[nbig] = make_int4(0, 0, ta, tb);
   }
   grid.sync();
-  const int nchunks = big_runs[nbig].z;
-  const int maxlen = (int)ctr[kTieMaxLen];
-  // sorted chunks (a run that fits one chunk is finished here)
-  for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
-    const int r = tie_task_run(big_runs, nbig, g);
-    const int4 run = big_runs[r];
+  if (threadIdx.x == 0) {
+    const int4 tot = big_runs[nbig];
+    s_nt[0] = tot.z;
+    s_nt[1] = tot.w;
+  }
+  __syncthreads();
+  const int na = s_nt[0], nm = s_nt[1];  // nm: slots (a multiple of kTieGroup)
+  const int ngrp = nm / kTieGroup;
+  // scratch: per-slot digit counts [nm][256], per-group sums [2][ngrp][256]
+  unsigned* chist = scr;
+  unsigned* gsum = scr + (size_t)nm * 256;
+  // phase A: codes; a single-chunk run is sorted (bitonic) and finished here
+  for (int g = blockIdx.x; g < na; g += gridDim.x) {
+    const int4 run = big_runs[tie_task_run<2>(big_runs, nbig, g)];
     const int c0 = (g - run.z) * kTieChunk, cl = min(kTieChunk, run.y - c0);
+    if (run.y > kTieChunk) {
+      for (int i = threadIdx.x; i < cl; i += kNT)
+        bufa[(int64_t)run.x + c0 + i] = tie_code<R>(rec, perm, skh, root, (int64_t)run.x + c0 + i);
+      continue;
+    }
     int P = 1;
     while (P < cl) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kNT)
-      s[i] = i < cl ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + c0 + i) : ~0ull;
+      s[i] = i < cl ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + i) : ~0ull;
     __syncthreads();
     bitonic_smem(s, P);
-    for (int i = threadIdx.x; i < cl; i += kNT) {
-      if (run.y <= kTieChunk) tie_put(perm, skl, (int64_t)run.x + i, s[i]);
-      else bufa[(int64_t)run.x + c0 + i] = s[i];
-    }
+    for (int i = threadIdx.x; i < cl; i += kNT) tie_put(perm, skl, (int64_t)run.x + i, s[i]);
     __syncthreads();
   }
-  // merge passes: sorted blocks of width w -> 2w; task g = one 2048-output
-  // segment of one run (segments never straddle a pair: 2w is a multiple)
+  if (nm == 0) return;  // (uniform)
+  for (int64_t k = blockIdx.x * (int64_t)kNT + threadIdx.x; k < (int64_t)ngrp * 256;
+       k += (int64_t)gridDim.x * kNT)
+    gsum[k] = 0;
+  // segmented LSD radix passes over key_lo (code bits 31..63), two
+  // grid-synchronised phases each: digit counts, then offsets + scatter
+  constexpr int kIPT = kTieChunk / kNT;  // 8 codes per thread: element 256 w + 32 r + lane
   uint64_t* src = bufa;
   uint64_t* dst = bufb;
-  for (int w = kTieChunk; w < maxlen; w <<= 1) {
+  for (int pass = 0; pass < 5; ++pass) {
+    const int shift = 31 + 8 * pass;
+    unsigned* gs = gsum + (size_t)(pass & 1) * ngrp * 256;
+    unsigned* gnext = gsum + (size_t)((pass + 1) & 1) * ngrp * 256;
     grid.sync();
-    for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
-      const int r = tie_task_run(big_runs, nbig, g);
+    // (1) digit counts per chunk, summed per group; the next pass's group sums zeroed
+    for (int g = blockIdx.x; g < nm; g += gridDim.x) {
+      const int r = tie_task_run<3>(big_runs, nbig, g);
       const int4 run = big_runs[r];
-      if (run.y <= kTieChunk) continue;  // done in the chunk phase
-      const int o0 = (g - run.z) * kTieChunk;   // first output of this segment
-      const int a0 = (o0 / (2 * w)) * (2 * w);  // its pair
-      const uint64_t* A = src + run.x + a0;
-      const int la = min(w, run.y - a0);
-      const uint64_t* B = A + la;
-      const int lb = max(0, min(w, run.y - a0 - la));
-      const int seg = min(kTieChunk, run.y - o0);
-      constexpr int kPer = kTieChunk / kNT;
-      int d = (o0 - a0) + (int)threadIdx.x * kPer;
-      const int dend = min((o0 - a0) + seg, d + kPer);
-      if (d < dend) {
-        int lo = max(0, d - lb), hi = min(d, la);  // merge path: i from A, d - i from B (unique keys)
-        while (lo < hi) {
-          const int i = (lo + hi) / 2;
-          if (A[i] < B[d - i - 1]) lo = i + 1;
-          else hi = i;
+      const int c0 = (g - run.w) * kTieChunk;
+      if (c0 >= run.y) continue;  // a padding slot (uniform)
+      const int cl = min(kTieChunk, run.y - c0);
+      unsigned* hs = &wh[0][0];
+      hs[threadIdx.x] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < cl; i += kNT)
+        atomicAdd(&hs[(unsigned)(src[(int64_t)run.x + c0 + i] >> shift) & 255u], 1u);
+      __syncthreads();
+      const unsigned v = hs[threadIdx.x];
+      chist[(size_t)g * 256 + threadIdx.x] = v;
+      if (v) atomicAdd(&gs[(size_t)(g / kTieGroup) * 256 + threadIdx.x], v);
+      __syncthreads();
+    }
+    for (int64_t k = blockIdx.x * (int64_t)kNT + threadIdx.x; k < (int64_t)ngrp * 256;
+         k += (int64_t)gridDim.x * kNT)
+      gnext[k] = 0;
+    grid.sync();
+    // (2) each chunk: run-local digit starts (scan of the run's group sums),
+    // its offset within each digit (earlier groups + earlier chunks of its
+    // group), then the stable scatter
+    for (int g = blockIdx.x; g < nm; g += gridDim.x) {
+      const int r = tie_task_run<3>(big_runs, nbig, g);
+      const int4 run = big_runs[r];
+      const int c0 = (g - run.w) * kTieChunk;
+      if (c0 >= run.y) continue;
+      const int cl = min(kTieChunk, run.y - c0);
+      const int nc = (run.y + kTieChunk - 1) / kTieChunk;
+      const int G0 = run.w / kTieGroup, G1 = G0 + (nc + kTieGroup - 1) / kTieGroup, G = g / kTieGroup;
+      {
+        const unsigned d = threadIdx.x;
+        unsigned tot = 0, pre = 0;
+#pragma unroll 8
+        for (int q = G0; q < G1; ++q) {
+          const unsigned x = __ldcg(gs + (size_t)q * 256 + d);
+          tot += x;
+          pre += q < G ? x : 0u;
         }
-        int i = lo, j = d - lo;
-        uint64_t* out = dst + run.x + a0;
-        for (; d < dend; ++d) {
-          const bool takeA = j >= lb || (i < la && A[i] < B[j]);
-          out[d] = takeA ? A[i++] : B[j++];
+#pragma unroll 8
+        for (int c = G * kTieGroup; c < g; ++c) pre += __ldcg(chist + (size_t)c * 256 + d);
+        unsigned v = tot;  // exclusive scan over the 256 digits
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += u;
+        }
+        if (lane == 31) ws[warp] = v;
+        __syncthreads();
+        unsigned base = v - tot;
+        for (int w = 0; w < warp; ++w) base += ws[w];
+        soff[d] = base + pre;
+      }
+      for (int w = 0; w < kNT / 32; ++w) wh[w][threadIdx.x] = 0;
+      __syncthreads();
+      uint64_t key[kIPT];
+      unsigned loc[kIPT];
+#pragma unroll
+      for (int q = 0; q < kIPT; ++q) {
+        const int i = warp * 32 * kIPT + q * 32 + lane;
+        key[q] = i < cl ? __ldcg(src + (int64_t)run.x + c0 + i) : 0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < kIPT; ++q) {
+        const int i = warp * 32 * kIPT + q * 32 + lane;
+        const bool ok = i < cl;
+        const unsigned dg = (unsigned)(key[q] >> shift) & 255u;
+        const unsigned pm = __match_any_sync(0xffffffffu, ok ? dg : 256u);
+        unsigned old = 0;
+        if (ok && lane == __ffs(pm) - 1) old = atomicAdd(&wh[warp][dg], (unsigned)__popc(pm));
+        const unsigned b = __shfl_sync(0xffffffffu, old, __ffs(pm) - 1);
+        loc[q] = b + __popc(pm & ((1u << lane) - 1u));
+      }
+      __syncthreads();
+      {  // warp offsets within the chunk's digit runs
+        const unsigned d = threadIdx.x;
+        unsigned acc = 0;
+        for (int w = 0; w < kNT / 32; ++w) {
+          const unsigned x = wh[w][d];
+          wh[w][d] = acc;
+          acc += x;
         }
       }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kIPT; ++q) {
+        const int i = warp * 32 * kIPT + q * 32 + lane;
+        if (i < cl) {
+          const unsigned dg = (unsigned)(key[q] >> shift) & 255u;
+          dst[(int64_t)run.x + soff[dg] + wh[warp][dg] + loc[q]] = key[q];
+        }
+      }
+      __syncthreads();
     }
     uint64_t* t = src;
     src = dst;
     dst = t;
   }
   grid.sync();
-  for (int g = blockIdx.x; g < nchunks; g += gridDim.x) {
-    const int r = tie_task_run(big_runs, nbig, g);
-    const int4 run = big_runs[r];
-    if (run.y <= kTieChunk) continue;
-    const int o0 = (g - run.z) * kTieChunk, seg = min(kTieChunk, run.y - o0);
-    for (int i = threadIdx.x; i < seg; i += kNT)
-      tie_put(perm, skl, (int64_t)run.x + o0 + i, src[(int64_t)run.x + o0 + i]);
+  for (int g = blockIdx.x; g < nm; g += gridDim.x) {
+    const int4 run = big_runs[tie_task_run<3>(big_runs, nbig, g)];
+    const int c0 = (g - run.w) * kTieChunk;
+    if (c0 >= run.y) continue;
+    const int cl = min(kTieChunk, run.y - c0);
+    for (int i = threadIdx.x; i < cl; i += kNT)
+      tie_put(perm, skl, (int64_t)run.x + c0 + i, __ldcg(src + (int64_t)run.x + c0 + i));
   }
 }
 
@@ -598,6 +716,7 @@ __device__ __forceinline__ int lcp_digits(uint64_t ah, uint64_t al, uint64_t bh,
 __device__ __forceinline__ int lm_of(const int* L, int64_t a) { return a > 0 ? L[a - 1] : -1; }
 
 __global__ void k_lcp(const uint64_t* skh, const uint64_t* skl, int64_t n, int* L) {
+  GS_PDL_ENTRY();
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t + 1 < n) L[t] = lcp_digits(skh[t], skl[t], skh[t + 1], skl[t + 1]);
 }
@@ -669,6 +788,7 @@ __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, c
 // [first[a], first[a + 1]) -- cheap writes, so the searches below run one
 // node per thread (a position starting many levels no longer serialises them).
 __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start, int* overflow) {
+  GS_PDL_ENTRY();
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (a >= n) return;
   if (first[n] > cap) {  // more nodes than the arrays hold (degenerate clustering)
@@ -686,6 +806,7 @@ __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* sta
 // first node at a position -- the level-(l-1) node found by a left search.
 __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
                         const int* start, int64_t n, int64_t cap, int4* meta, int* parent) {
+  GS_PDL_ENTRY();
   const int64_t idx = blockIdx.x * (int64_t)kNT + threadIdx.x;
   const int m = first[n];
   if (m > cap || idx >= m) return;
@@ -715,6 +836,7 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
 
 // per node: child count (the twig flag of the traversal record)
 __global__ void __launch_bounds__(kNT) k_children(const int4* meta, const int* mp, int* nchild) {
+  GS_PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= *mp) return;
   const int4 mi = meta[i];
@@ -733,6 +855,7 @@ template <typename R>
 __global__ void __launch_bounds__(kNT) k_gather(const V4<R>* rec, const int* perm, int64_t n,
                                                 double kap, double c0x, double c0y, double c0z,
                                                 int scaled, V4<R>* srec, V4<R>* squ) {
+  GS_PDL_ENTRY();
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t >= n) return;
   const int i = perm[t];
@@ -815,6 +938,7 @@ struct AggArgs {
   int* outer_cnt;
   double kap, c0x, c0y, c0z;
   int scaled;
+  int full;  // write the FP64 sums and boxes too (DevTree::lean = false)
 };
 
 // FP32 interaction coordinates, same rounding as the all-pairs path
@@ -884,8 +1008,10 @@ __device__ void write_node(const AggArgs<R>& a, int i, const int4& mi, int nch, 
     // db = beta_i - (1 / count) * beta_sum, bh_kernel.cpp:146
     st4(a.nadj + 2 * i + 1, mk4<R>(R(__dmul_rn(inv, s.b[0])), R(__dmul_rn(inv, s.b[1])),
                                    R(__dmul_rn(inv, s.b[2]))));
-    a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
-    a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    if (a.full) {
+      a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
+      a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    }
     return;
   }
   const bool leaf = mi.w & 1;
@@ -905,10 +1031,12 @@ __device__ void write_node(const AggArgs<R>& a, int i, const int4& mi, int nch, 
                             R(__dmul_rn(s.a[2], inv))));
     ub = mk4<R>(R(s.b[0]), R(s.b[1]), R(s.b[2]));
     const V4<R> l = mk4<R>(x.l[0], x.l[1], x.l[2]), h = mk4<R>(x.h[0], x.h[1], x.h[2]);
-    st4(a.lo + i, l);
-    st4(a.hi + i, h);
-    a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
-    a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    if (a.full) {
+      st4(a.lo + i, l);
+      st4(a.hi + i, h);
+      a.s0[i] = make_double4(s.a[0], s.a[1], s.a[2], 0.0);
+      a.s1[i] = make_double4(s.b[0], s.b[1], s.b[2], 0.0);
+    }
     st4(a.nrec + 4 * i + 2, mk4<R>(l.x, l.y, l.z, ival(R(0), cnt)));
     st4(a.nrec + 4 * i + 3, h);
   }
@@ -947,6 +1075,7 @@ enum { kItemNode = 0, kItemTotal = 1, kItemHead = 2, kItemTail = 3 };
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
+  GS_PDL_ENTRY();
   constexpr int C = chunk_of<R>();
   __shared__ V4<R> su[C], sv[C];
   __shared__ int sl[C + 1];        // sl[1 + j] = lcp(c0 + j, c0 + j + 1); sl[0] = lcp(c0 - 1, c0)
@@ -1070,6 +1199,7 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
 // combines them (a fixed order: deterministic).
 template <typename R, int MODE>
 __global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
+  GS_PDL_ENTRY();
   constexpr int C = chunk_of<R>();
   const int c = *a.outer_cnt;
   const int lane = threadIdx.x & 31;
@@ -1195,6 +1325,7 @@ __global__ void k_cells(const int4* meta, int64_t m, const uint64_t* skh, const 
 // exclusive scan of the node counts per position (k_count's, computed
 // inline from the lcp array; n + 1 outputs: out[n] = total), 3 phases
 __global__ void __launch_bounds__(1024) k_scan_blocks(const int* L, int64_t n, int* out, int* bsum) {
+  GS_PDL_ENTRY();
   __shared__ int s[1024];
   const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
   int v = 0;
@@ -1216,6 +1347,7 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(const int* L, int64_t n, i
 }
 
 __global__ void k_scan_add(int* out, int64_t n, const int* bsum_scanned, int nb) {
+  GS_PDL_ENTRY();
   const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
   if (i < n && blockIdx.x > 0) out[i] += bsum_scanned[blockIdx.x];
   if (i == 0) out[n] = bsum_scanned[nb];
@@ -1245,6 +1377,7 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
   a.c0y = kc.c0[1];
   a.c0z = kc.c0[2];
   a.scaled = sizeof(R) == 4;
+  a.full = !t.lean;
   const size_t parts = (size_t)nch * kPartPerChunk;
   GS_TRY_INT(t.parts.ensure(parts * (2 * sizeof(double4) + 2 * sizeof(V4<R>))));
   a.ps0 = t.parts.as<double4>();
@@ -1264,15 +1397,15 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
     a.s0 = t.psum.as<double4>();
     a.s1 = t.msum.as<double4>();
     a.nrec = t.nrec.as<V4<R>>();
-    k_agg_chunk<R, 0><<<(unsigned)nch, kNT, 0, st>>>(a);
-    k_agg_outer<R, 0><<<4 * 148, kNT, 0, st>>>(a);
+    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 0>, (unsigned)nch, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 0>, 4 * 148, kNT, 0, st, a));
   } else {
     a.sadj = t.sadj.as<V4<R>>();
     a.s0 = t.asum.as<double4>();
     a.s1 = t.bsum.as<double4>();
     a.nadj = t.nadj.as<V4<R>>();
-    k_agg_chunk<R, 1><<<(unsigned)nch, kNT, 0, st>>>(a);
-    k_agg_outer<R, 1><<<4 * 148, kNT, 0, st>>>(a);
+    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 1>, (unsigned)nch, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 1>, 4 * 148, kNT, 0, st, a));
   }
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
@@ -1289,11 +1422,11 @@ static int scan_ints(const int* L, int64_t n, int* out, DBuf& scratch, cudaStrea
   const int nb = nblocks(n, 1024);
   GS_TRY_INT(scratch.ensure(sizeof(unsigned) * (nb + 2)));
   unsigned* bs = scratch.as<unsigned>();
-  k_scan_blocks<<<nb, 1024, 0, st>>>(L, n, out, (int*)bs);
+  GS_CUDA_OK(pdl_launch(k_scan_blocks, nb, 1024, 0, st, L, n, out, (int*)bs));
   // scan the block sums (nb + 1 entries, last = 0 -> becomes the total)
   GS_CUDA_OK(cudaMemsetAsync(bs + nb, 0, sizeof(unsigned), st));
-  k_rs_scan<<<1, 1024, 0, st>>>(bs, nb + 1);
-  k_scan_add<<<nb, 1024, 0, st>>>(out, n, (const int*)bs, nb);
+  GS_CUDA_OK(pdl_launch(k_rs_scan, 1, 1024, 0, st, bs, nb + 1));
+  GS_CUDA_OK(pdl_launch(k_scan_add, nb, 1024, 0, st, out, n, (const int*)bs, nb));
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
@@ -1319,9 +1452,15 @@ static int tie_sort(const Device& dev, int prec, const void* rec, DevTree& t, un
   uint64_t* skl = t.skey_lo.as<uint64_t>();
   uint64_t* bufa = t.tmp_k.as<uint64_t>();
   uint64_t* bufb = t.key_lo.as<uint64_t>();
+  // scratch of the long-run radix passes: slots (chunks of runs > 2048 points,
+  // <= n / 1024, each run padded to whole groups of kTieGroup: <= 8.5 n / 1024)
+  // x 256 digit counts + 2 x groups x 256 group sums: < 2.5 n words
+  GS_TRY_INT(t.tie_scr.ensure(sizeof(unsigned) * (3 * (size_t)t.n + 4096)));
+  unsigned* chist = t.tie_scr.as<unsigned>();
   const unsigned* cctr = ctr;
   void* args[] = {(void*)&rec, (void*)&skh, (void*)&root, (void*)&cctr, (void*)&small_runs,
-                  (void*)&big_runs, (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb};
+                  (void*)&big_runs, (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb,
+                  (void*)&chist};
   GS_CUDA_OK(cudaLaunchCooperativeKernel(fn, grid, kNT, args, 0, st));
   return GS_OK;
 }
@@ -1352,16 +1491,16 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   if (root_box) {
     GS_CUDA_OK(cudaMemcpyAsync(t.root.ptr, root_box, 6 * sizeof(double), cudaMemcpyHostToDevice, st));
   } else {
-    if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
-    else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
-    k_bbox_final<<<1, kNT, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+    if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>()));
+    else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>()));
+    GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
   }
   // 2. keys
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
   else
-    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
@@ -1389,16 +1528,16 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   unsigned* hist = t.hist.as<unsigned>();
   unsigned* ctr = hist + kPasses * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
+  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   {
     const uint64_t* ka = t.key_hi.as<uint64_t>();
     const int* va = nullptr;  // first pass: the value is the index
     for (int p = 0; p < kPasses; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      onesweep(ipt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
-               desc + (size_t)p * ntiles * 256, ctr + p);
+      GS_TRY_INT(onesweep(ipt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
+               desc + (size_t)p * ntiles * 256, ctr + p));
       ka = kb;
       va = vb;
     }
@@ -1406,13 +1545,13 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // ties: runs of equal key_hi sorted by (key_lo, index) in place (perm,
   // skey_lo of the run members); tmp_v / tmp_v2 hold the run lists, tmp_k /
   // key_lo the long runs' merge buffers (all free after the key_hi sort)
-  k_tie_runs<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), n, ctr, (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr);
+  GS_CUDA_OK(pdl_launch(k_tie_runs, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), n, ctr, (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr));
   GS_TRY_INT(tie_sort(dev, prec, rec, t, ctr, st));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(3, st);
   kt_mark(4, st);
   // 4. topology
-  k_lcp<<<nb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>());
+  GS_CUDA_OK(pdl_launch(k_lcp, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>()));
   GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
   // The node count m = first[n] stays on the device: node arrays are sized
   // for 4n + 64 nodes (m ~ 1.5n for volumes and surfaces) and every kernel
@@ -1433,11 +1572,11 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.squ.ensure(vb * n));
   const int mb = nblocks(cap, kNT);
   GS_TRY_INT(t.start.ensure(4 * cap));
-  k_node_starts<<<nb, kNT, 0, st>>>(t.first.as<int>(), n, cap, t.start.as<int>(), overflow);
-  k_nodes<<<mb, kNT, 0, st>>>(t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
+  GS_CUDA_OK(pdl_launch(k_node_starts, nb, kNT, 0, st, t.first.as<int>(), n, cap, t.start.as<int>(), overflow));
+  GS_CUDA_OK(pdl_launch(k_nodes, mb, kNT, 0, st, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
                               t.first.as<int>(), t.start.as<int>(), n, cap, t.meta.as<int4>(),
-                              t.parent.as<int>());
-  k_children<<<mb, kNT, 0, st>>>(t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>());
+                              t.parent.as<int>()));
+  GS_CUDA_OK(pdl_launch(k_children, mb, kNT, 0, st, t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>()));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(4, st);
   kt_mark(5, st);
@@ -1468,14 +1607,14 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   GS_TRY_INT(t.squ.ensure(vb * n));
   const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
   GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
-  if (prec == kF32) k_bbox<float><<<bb, kNT, 0, st>>>((const float4*)rec, n, t.scan_tmp.as<double>());
-  else k_bbox<double><<<bb, kNT, 0, st>>>((const double4*)rec, n, t.scan_tmp.as<double>());
-  k_bbox_final<<<1, kNT, 0, st>>>(t.scan_tmp.as<double>(), bb, t.root.as<double>());
+  if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>()));
+  else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>()));
+  GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_keys<float><<<nb, kNT, 0, st>>>((const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
   else
-    k_keys<double><<<nb, kNT, 0, st>>>((const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>());
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
   const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;
@@ -1484,22 +1623,22 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   unsigned* hist = t.hist.as<unsigned>();
   unsigned* ctr = hist + 8 * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) k_rs_hist_all<8><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
-  else k_rs_hist_all<4><<<ntiles, kRsNT, 0, st>>>(t.key_hi.as<uint64_t>(), n, hist);
+  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   const uint64_t* ka = t.key_hi.as<uint64_t>();
   const int* va = nullptr;
   for (int p = 0; p < 8; ++p) {  // (key_hi, index) -> (tmp_k, tmp_v) -> (skey_hi, perm) -> ...
     uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
     int* vb2 = (p & 1) ? t.perm.as<int>() : t.tmp_v.as<int>();
     unsigned* dq = desc + (size_t)p * ntiles * 256;
-    onesweep(ipt, ntiles, st, ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p);
+    GS_TRY_INT(onesweep(ipt, ntiles, st, ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p));
     ka = kb;
     va = vb2;
   }
   if (prec == kF32)
-    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>());
+    GS_CUDA_OK(pdl_launch(k_gather<float>, nb, kNT, 0, st, (const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>()));
   else
-    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>());
+    GS_CUDA_OK(pdl_launch(k_gather<double>, nb, kNT, 0, st, (const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>()));
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
 }
@@ -1521,9 +1660,9 @@ int tree_rescale(int prec, DevTree& t, const void* rec, const KernelConsts& kc, 
   const int64_t n = t.n;
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    k_gather<float><<<nb, kNT, 0, st>>>((const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>());
+    GS_CUDA_OK(pdl_launch(k_gather<float>, nb, kNT, 0, st, (const float4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 1, t.srec.as<float4>(), t.squ.as<float4>()));
   else
-    k_gather<double><<<nb, kNT, 0, st>>>((const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>());
+    GS_CUDA_OK(pdl_launch(k_gather<double>, nb, kNT, 0, st, (const double4*)rec, t.perm.as<int>(), n, kc.kappa, kc.c0[0], kc.c0[1], kc.c0[2], 0, t.srec.as<double4>(), t.squ.as<double4>()));
   GS_CUDA_OK(cudaGetLastError());
   return tree_finalize_fwd(prec, t, kc, st);
 }
@@ -1691,6 +1830,11 @@ int tree_download(DevTree& t, cudaStream_t st, int32_t* order, uint64_t* key_hi,
   GS_TRY_INT(dl(sums, b_sums, 12 * m, st));
   GS_TRY_INT(dl(count, b_count, m, st));
   GS_CUDA_OK(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+int trace_install_tree(unsigned long long* buf) {
+  GS_CUDA_OK(trace_install_here(buf));
   return GS_OK;
 }
 

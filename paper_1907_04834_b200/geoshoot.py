@@ -228,6 +228,21 @@ class Geoshoot:
         self.check(self.lib.gs_profile_phases(self.ctx, _p(ms), cnt, k))
         return {name: {"ms": float(ms[i]), "count": int(cnt[i])} for i, name in enumerate(self.PHASES)}
 
+    def trace(self, enable: bool = True):
+        """Kernel start-time trace (gs_trace): valid inside captured graphs."""
+        self.check(self.lib.gs_trace(self.ctx, 1 if enable else 0))
+
+    def trace_read(self, max_entries: int = 16384):
+        """[(unit, line, t_ns)] of the traced kernel starts since the last read."""
+        tags = np.zeros(max_entries, np.uint64)
+        times = np.zeros(max_entries, np.uint64)
+        cnt = C.c_int64()
+        self.check(self.lib.gs_trace_read(self.ctx, tags.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          times.ctypes.data_as(C.POINTER(C.c_uint64)), max_entries,
+                                          C.byref(cnt)))
+        k = cnt.value
+        return [(int(t) >> 16, int(t) & 0xffff, int(v)) for t, v in zip(tags[:k], times[:k])]
+
     def close(self):
         if getattr(self, "ctx", None):
             self.lib.gs_destroy(self.ctx)
