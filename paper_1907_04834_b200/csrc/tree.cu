@@ -393,7 +393,7 @@ int onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int
 // run members only and carried with the index as the 64-bit code
 // (key_lo << 31) | index. k_tie_runs lists the runs (and sets the tie flag);
 // k_tie_sort, one cooperative grid, sorts them in place:
-//  * a run of <= 32 points: a warp, rank by comparison;
+//  * a run of <= 64 points: a warp, rank by comparison;
 //  * a run of <= 2048 points: a CTA, bitonic sort in shared memory;
 //  * longer runs (a diverged flow whose root box dwarfs the cloud -- config
 //    4's puts 77 % of the points in such runs): a segmented LSD radix sort of
@@ -426,7 +426,7 @@ __global__ void k_tie_runs(const uint64_t* skh, int64_t n, unsigned* ctr, int2* 
     else hi = mid - 1;
   }
   const int len = (int)(lo - t + 1);
-  if (len <= 32) small_runs[atomicAdd(ctr + kTieSmallCtr, 1u)] = make_int2((int)t, len);
+  if (len <= 64) small_runs[atomicAdd(ctr + kTieSmallCtr, 1u)] = make_int2((int)t, len);
   else big_runs[atomicAdd(ctr + kTieBigCtr, 1u)] = make_int4((int)t, len, 0, 0);
   atomicOr(ctr + kTieFlag, 1u);
 }
@@ -522,16 +522,28 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
   __shared__ unsigned ws[kNT / 32];
   __shared__ int s_nt[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // runs of <= 32 points: a warp each, rank = number of smaller codes
+  // runs of <= 64 points: a warp each
   const int nsmall = (int)ctr[kTieSmallCtr];
   const int gw = (blockIdx.x * kNT + threadIdx.x) >> 5, nw = (gridDim.x * kNT) >> 5;
   for (int r = gw; r < nsmall; r += nw) {
     const int2 run = small_runs[r];
-    const uint64_t c = lane < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + lane) : ~0ull;
-    int rank = 0;
-    for (int k = 0; k < run.y; ++k) rank += __shfl_sync(0xffffffffu, c, k) < c;
+    // two codes per lane (runs of <= 64): rank = number of smaller codes
+    const uint64_t c0 = lane < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + lane) : ~0ull;
+    const uint64_t c1 = lane + 32 < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + 32 + lane) : ~0ull;
+    int r0 = 0, r1 = 0;
+    for (int k = 0; k < min(run.y, 32); ++k) {
+      const uint64_t u = __shfl_sync(0xffffffffu, c0, k);
+      r0 += u < c0;
+      r1 += u < c1;
+    }
+    for (int k = 32; k < run.y; ++k) {
+      const uint64_t u = __shfl_sync(0xffffffffu, c1, k - 32);
+      r0 += u < c0;
+      r1 += u < c1;
+    }
     __syncwarp();
-    if (lane < run.y) tie_put(perm, skl, (int64_t)run.x + rank, c);
+    if (lane < run.y) tie_put(perm, skl, (int64_t)run.x + r0, c0);
+    if (lane + 32 < run.y) tie_put(perm, skl, (int64_t)run.x + r1, c1);
   }
   const int nbig = (int)ctr[kTieBigCtr];
   if (nbig == 0) return;
@@ -579,6 +591,17 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     __syncthreads();
   }
   if (nm == 0) return;  // (uniform)
+  // this CTA's slots g = blockIdx.x + k gridDim.x: their runs, looked up once
+  __shared__ int s_run[64];
+  for (int k = threadIdx.x; k < 64; k += kNT) {
+    const int g = blockIdx.x + k * gridDim.x;
+    s_run[k] = g < nm ? tie_task_run<3>(big_runs, nbig, g) : 0;
+  }
+  __syncthreads();
+  auto run_of = [&](int g) {
+    const int k = (g - (int)blockIdx.x) / (int)gridDim.x;
+    return k < 64 ? s_run[k] : tie_task_run<3>(big_runs, nbig, g);
+  };
   for (int64_t k = blockIdx.x * (int64_t)kNT + threadIdx.x; k < (int64_t)ngrp * 256;
        k += (int64_t)gridDim.x * kNT)
     gsum[k] = 0;
@@ -594,7 +617,7 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     grid.sync();
     // (1) digit counts per chunk, summed per group; the next pass's group sums zeroed
     for (int g = blockIdx.x; g < nm; g += gridDim.x) {
-      const int r = tie_task_run<3>(big_runs, nbig, g);
+      const int r = run_of(g);
       const int4 run = big_runs[r];
       const int c0 = (g - run.w) * kTieChunk;
       if (c0 >= run.y) continue;  // a padding slot (uniform)
@@ -618,7 +641,7 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     // its offset within each digit (earlier groups + earlier chunks of its
     // group), then the stable scatter
     for (int g = blockIdx.x; g < nm; g += gridDim.x) {
-      const int r = tie_task_run<3>(big_runs, nbig, g);
+      const int r = run_of(g);
       const int4 run = big_runs[r];
       const int c0 = (g - run.w) * kTieChunk;
       if (c0 >= run.y) continue;
@@ -694,7 +717,7 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
   }
   grid.sync();
   for (int g = blockIdx.x; g < nm; g += gridDim.x) {
-    const int4 run = big_runs[tie_task_run<3>(big_runs, nbig, g)];
+    const int4 run = big_runs[run_of(g)];
     const int c0 = (g - run.w) * kTieChunk;
     if (c0 >= run.y) continue;
     const int cl = min(kTieChunk, run.y - c0);
