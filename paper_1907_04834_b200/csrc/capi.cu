@@ -410,6 +410,7 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
   e.bad_step = f->flags.as<int>();
   e.step = f->steps_done + 1;
   e.step_dev = f->stepctr.as<int>();
+  if (stage == flow_stages(f) - 1) e.step_inc = f->stepctr.as<int>();
   e.peers = f->peers;
   const bool first = f->want_energy && f->steps_done == 0 && stage == 0;
   if (first) {
@@ -469,7 +470,7 @@ int flow_init(gs_flow* f, gs_ctx* c, const gs_config* cfg, int64_t n) {
   GS_TRY(f->bh.stats.ensure(64));
   GS_CUDA_OK(cudaMemsetAsync(f->bh.stats.ptr, 0, 64, c->stream));
   GS_TRY(f->stepctr.ensure(64));
-  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), c->stream));
+  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, 2 * sizeof(int), c->stream));
   return GS_OK;
 }
 
@@ -494,14 +495,12 @@ int flow_upload(gs_flow* f, const double* q0, const double* p0) {
   f->steps_done = 0;
   f->have_energy_part = false;
   GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), f->ctx->stream));
-  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), f->ctx->stream));
+  GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, 2 * sizeof(int), f->ctx->stream));
   return GS_OK;
 }
 
 int flow_step_eager(gs_flow* f) {
   for (int s = 0; s < flow_stages(f); ++s) GS_TRY(flow_stage(f, s, nullptr, nullptr));
-  GS_TRY(step_counter_inc(f->stepctr.as<int>(), f->ctx->stream));
-  ++f->launches;
   ++f->steps_done;
   return GS_OK;
 }
@@ -546,7 +545,6 @@ int flow_capture_step(gs_flow* f) {
   GS_CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   int s = GS_OK;
   for (int k = 0; k < flow_stages(f) && s == GS_OK; ++k) s = flow_stage(f, k, nullptr, nullptr);
-  if (s == GS_OK) s = step_counter_inc(f->stepctr.as<int>(), st);
   const cudaError_t ce = cudaStreamEndCapture(st, &g);
   f->stats = saved;  // nothing ran during capture
   f->steps_done = steps_saved;
@@ -867,10 +865,7 @@ gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
   if (!f->subs.empty()) return bad_arg("a multi-device flow advances with gs_flow_advance");
   f->launches = 0;
   GS_TRY(flow_stage(f, stage, nullptr, nullptr));
-  if (stage == flow_stages(f) - 1) {
-    GS_TRY(step_counter_inc(f->stepctr.as<int>(), f->ctx->stream));
-    ++f->steps_done;
-  }
+  if (stage == flow_stages(f) - 1) ++f->steps_done;  // (the epilogue advanced the step counter)
   return GS_OK;
 }
 
@@ -1170,7 +1165,7 @@ static int evaluate_impl(gs_ctx* c, const gs_config* cfg, int64_t n, const doubl
     f->steps_done = 0;
     f->have_energy_part = false;
     GS_CUDA_OK(cudaMemsetAsync(f->flags.ptr, 0x7f, 2 * sizeof(int), c->stream));
-    GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, sizeof(int), c->stream));
+    GS_CUDA_OK(cudaMemsetAsync(f->stepctr.ptr, 0, 2 * sizeof(int), c->stream));
   } else {
     GS_TRY(flow_upload(f, q0, p0));
     GS_TRY(h2d(c, c->stage_c, target, n));
@@ -1955,8 +1950,6 @@ int multi_flow_advance(gs_flow* f, int steps) {
       }
     }
     for (gs_flow* s : f->subs) {
-      DevGuard g(sub_dev(s));
-      GS_TRY(step_counter_inc(s->stepctr.as<int>(), s->ctx->stream));
       ++s->steps_done;
     }
     ++f->steps_done;

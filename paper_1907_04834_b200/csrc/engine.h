@@ -147,6 +147,8 @@ struct FwdEpi {
   int* bad_step = nullptr;        // atomicMin on non-finite output
   int step = 0;                   // step index (1-based) reported on non-finite
   const int* step_dev = nullptr;  // if set: step = *step_dev + 1 (graph-replayable)
+  int* step_inc = nullptr;  // a step's final stage: the last block to finish increments
+                            // step_inc[0] (the step counter; step_inc[1]: arrivals)
   PeerOut peers;                  // multi-device: the updated records go here too
 };
 int fwd_epilogue(int prec, const FwdEpi& e, cudaStream_t st, int* blocks_out);
@@ -197,7 +199,6 @@ int gather_rows3(const double* in, const int* perm, int64_t n, double* out, cuda
 int sum_part_w(int prec, const void* part, int n, int per, int which, double* block_out,
                int* blocks, cudaStream_t st);
 // ++*counter on the device (the step counter of graph-replayed flows)
-int step_counter_inc(int* counter, cudaStream_t st);
 
 }  // namespace gsb
 

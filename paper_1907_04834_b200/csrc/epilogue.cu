@@ -135,6 +135,17 @@ __global__ void __launch_bounds__(kEpiNT) k_fwd_epi(FwdEpi e) {
     const double s = block_sum<kEpiNT>(edot);
     if (threadIdx.x == 0) e.energy_part[blockIdx.x] = s;
   }
+  if (e.step_inc) {  // (every block's read of *step_dev precedes its arrival)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned* arrivals = reinterpret_cast<unsigned*>(e.step_inc) + 1;
+      if (atomicAdd(arrivals, 1u) == gridDim.x - 1) {
+        e.step_inc[0] += 1;
+        *arrivals = 0;
+      }
+    }
+  }
 }
 
 template <typename R>
@@ -245,10 +256,6 @@ __global__ void __launch_bounds__(kEpiNT) k_adj_init(const V4<R>* recT, const do
   if (threadIdx.x == 0 && sse_part) sse_part[blockIdx.x] = s;
 }
 
-__global__ void k_step_inc(int* c) {
-  GS_TRACE_HERE();
-  *c += 1;
-}
 
 __global__ void k_reduce(const double* part, int count, double* out) {
   // one warp, fixed order per lane then fixed tree: deterministic
@@ -396,11 +403,6 @@ int adjoint_init(int prec, const void* rec_T, const double* target, double lambd
   return GS_OK;
 }
 
-int step_counter_inc(int* counter, cudaStream_t st) {
-  k_step_inc<<<1, 1, 0, st>>>(counter);
-  GS_CUDA_OK(cudaGetLastError());
-  return GS_OK;
-}
 
 int reduce_sum(const double* part, int count, double* out, cudaStream_t st) {
   k_reduce<<<1, 32, 0, st>>>(part, count, out);

@@ -182,29 +182,6 @@ __global__ void __launch_bounds__(kNT) k_keys_lo_leaf(const V4<R>* squ, const in
 // passes (below): stable within-tile ranking with warp match/popc.
 constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a template parameter
 
-// exclusive scan of `count` u32 in place, one CTA (count up to a few 1e5)
-__global__ void __launch_bounds__(1024) k_rs_scan(unsigned* a, int64_t count) {
-  GS_PDL_ENTRY();
-  __shared__ unsigned sums[1024];
-  const int64_t per = (count + 1023) / 1024;
-  const int64_t b = threadIdx.x * per, e = min(count, b + per);
-  unsigned s = 0;
-  for (int64_t i = b; i < e; ++i) s += a[i];
-  sums[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const unsigned v = threadIdx.x >= o ? sums[threadIdx.x - o] : 0u;
-    __syncthreads();
-    sums[threadIdx.x] += v;
-    __syncthreads();
-  }
-  unsigned run = sums[threadIdx.x] - s;
-  for (int64_t i = b; i < e; ++i) {
-    const unsigned v = a[i];
-    a[i] = run;
-    run += v;
-  }
-}
 
 // ---- one-sweep passes ---------------------------------------------------------
 // Digit histograms are independent of the key order, so ONE kernel counts every
@@ -405,14 +382,19 @@ int onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int
 namespace cg = cooperative_groups;
 constexpr int kTieChunk = 2048;
 constexpr int kTieSmallCtr = 28, kTieBigCtr = 29, kTieFlag = 31;  // sort counters
+constexpr int kScanTicket = 27;
 
-__global__ void k_tie_runs(const uint64_t* skh, int64_t n, unsigned* ctr, int2* small_runs,
+// L[t] = common digits of sorted neighbours t, t + 1 from key_hi (21 where
+// they tie: k_tie_sort completes those from key_lo), and the runs listed
+__global__ void k_lcp_runs(const uint64_t* skh, int64_t n, int* L, unsigned* ctr, int2* small_runs,
                            int4* big_runs) {
   GS_PDL_ENTRY();
   const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (t + 1 >= n) return;
-  const uint64_t k = skh[t];
-  if (skh[t + 1] != k || (t > 0 && skh[t - 1] == k)) return;  // not a run start
+  const uint64_t k = skh[t], k1 = skh[t + 1];
+  const uint64_t x = k ^ k1;
+  L[t] = x ? (__clzll((long long)x) - 1) / 3 : 21;
+  if (k1 != k || (t > 0 && skh[t - 1] == k)) return;  // not a run start
   // last index of the run: exponential then binary search on equality
   int64_t step = 1, good = t + 1;
   while (good + step < n && skh[good + step] == k) {
@@ -444,6 +426,12 @@ __device__ __forceinline__ uint64_t tie_code(const V4<R>* rec, const int* perm, 
 __device__ __forceinline__ void tie_put(int* perm, uint64_t* skl, int64_t j, uint64_t c) {
   perm[j] = (int)(c & 0x7fffffffu);
   skl[j] = c >> 31;
+}
+
+// common digits of two tied neighbours (equal key_hi) from their codes
+__device__ __forceinline__ int tie_lcp(uint64_t ca, uint64_t cb) {
+  const uint64_t y = (ca ^ cb) >> 31;
+  return y ? 21 + (__clzll((long long)y) - 31) / 3 : 32;
 }
 
 // bitonic sort of s[0, P) (P a power of two) by the CTA
@@ -512,7 +500,7 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
                                                   const double* root, const unsigned* ctr,
                                                   const int2* small_runs, int4* big_runs,
                                                   int* perm, uint64_t* skl, uint64_t* bufa,
-                                                  uint64_t* bufb, unsigned* scr) {
+                                                  uint64_t* bufb, unsigned* scr, int* L) {
   GS_PDL_ENTRY();
   if (ctr[kTieFlag] == 0) return;  // (uniform over the grid)
   cg::grid_group grid = cg::this_grid();
@@ -544,6 +532,16 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     __syncwarp();
     if (lane < run.y) tie_put(perm, skl, (int64_t)run.x + r0, c0);
     if (lane + 32 < run.y) tie_put(perm, skl, (int64_t)run.x + r1, c1);
+    // the run's internal neighbour lcps: each code's successor in the order
+    // is the smallest larger code
+    uint64_t n0 = ~0ull, n1 = ~0ull;
+    for (int k = 0; k < run.y; ++k) {
+      const uint64_t u = __shfl_sync(0xffffffffu, k < 32 ? c0 : c1, k & 31);
+      if (u > c0 && u < n0) n0 = u;
+      if (u > c1 && u < n1) n1 = u;
+    }
+    if (lane < run.y && r0 + 1 < run.y) L[run.x + r0] = tie_lcp(c0, n0);
+    if (lane + 32 < run.y && r1 + 1 < run.y) L[run.x + r1] = tie_lcp(c1, n1);
   }
   const int nbig = (int)ctr[kTieBigCtr];
   if (nbig == 0) return;
@@ -587,7 +585,10 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
       s[i] = i < cl ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + i) : ~0ull;
     __syncthreads();
     bitonic_smem(s, P);
-    for (int i = threadIdx.x; i < cl; i += kNT) tie_put(perm, skl, (int64_t)run.x + i, s[i]);
+    for (int i = threadIdx.x; i < cl; i += kNT) {
+      tie_put(perm, skl, (int64_t)run.x + i, s[i]);
+      if (i + 1 < cl) L[run.x + i] = tie_lcp(s[i], s[i + 1]);
+    }
     __syncthreads();
   }
   if (nm == 0) return;  // (uniform)
@@ -721,28 +722,20 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     const int c0 = (g - run.w) * kTieChunk;
     if (c0 >= run.y) continue;
     const int cl = min(kTieChunk, run.y - c0);
-    for (int i = threadIdx.x; i < cl; i += kNT)
-      tie_put(perm, skl, (int64_t)run.x + c0 + i, __ldcg(src + (int64_t)run.x + c0 + i));
+    for (int i = threadIdx.x; i < cl; i += kNT) {
+      const int64_t j = (int64_t)run.x + c0 + i;
+      const uint64_t c = __ldcg(src + j);
+      tie_put(perm, skl, j, c);
+      if (c0 + i + 1 < run.y) L[j] = tie_lcp(c, __ldcg(src + j + 1));
+    }
   }
 }
 
 // ------------------------------------------------------------- topology ---
-__device__ __forceinline__ int lcp_digits(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl) {
-  const uint64_t x = ah ^ bh;
-  if (x) return (__clzll((long long)x) - 1) / 3;
-  const uint64_t y = al ^ bl;
-  if (y) return 21 + (__clzll((long long)y) - 31) / 3;
-  return 32;
-}
 
 
 __device__ __forceinline__ int lm_of(const int* L, int64_t a) { return a > 0 ? L[a - 1] : -1; }
 
-__global__ void k_lcp(const uint64_t* skh, const uint64_t* skl, int64_t n, int* L) {
-  GS_PDL_ENTRY();
-  const int64_t t = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (t + 1 < n) L[t] = lcp_digits(skh[t], skl[t], skh[t + 1], skl[t + 1]);
-}
 
 // nodes starting at position a: internal levels (Lm, min(Lp,31)] + one leaf
 // unless a continues a depth-32 bucket.
@@ -810,7 +803,8 @@ __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, c
 // The start position of every node: position a starts nodes
 // [first[a], first[a + 1]) -- cheap writes, so the searches below run one
 // node per thread (a position starting many levels no longer serialises them).
-__global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start, int* overflow) {
+__global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start, int* inner,
+                              int* overflow) {
   GS_PDL_ENTRY();
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (a >= n) return;
@@ -818,7 +812,10 @@ __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* sta
     if (a == 0 && overflow) atomicExch(overflow, 1);
     return;
   }
-  for (int idx = first[a]; idx < first[a + 1]; ++idx) start[idx] = (int)a;
+  for (int idx = first[a]; idx < first[a + 1]; ++idx) {
+    start[idx] = (int)a;
+    inner[idx] = 0;  // set by k_nodes when an internal child names this node its parent
+  }
 }
 
 // One node per thread: node idx starts at a = start[idx]; it is internal
@@ -827,8 +824,11 @@ __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* sta
 // shares the node's level-l prefix (exponential + binary search on the sorted
 // keys); its parent is the node above it at the same start, or -- for the
 // first node at a position -- the level-(l-1) node found by a left search.
+// inner[p] = 1: node p has an internal child (else, if internal, it is a
+// twig: all children leaves -- the flag the traversal records carry)
 __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
-                        const int* start, int64_t n, int64_t cap, int4* meta, int* parent) {
+                        const int* start, int64_t n, int64_t cap, int4* meta, int* parent,
+                        int* inner) {
   GS_PDL_ENTRY();
   const int64_t idx = blockIdx.x * (int64_t)kNT + threadIdx.x;
   const int m = first[n];
@@ -842,7 +842,9 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
     const int l = l0 + k;
     const int64_t b = search_right(kh, kl, n, a, l);
     meta[idx] = make_int4(first[b + 1], (int)a, (int)b, l << 8);
-    parent[idx] = l == 0 ? -1 : (k > 0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
+    const int par = l == 0 ? -1 : (k > 0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
+    parent[idx] = par;
+    if (par >= 0) inner[par] = 1;
     return;
   }
   int level;
@@ -858,16 +860,6 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
 }
 
 // per node: child count (the twig flag of the traversal record)
-__global__ void __launch_bounds__(kNT) k_children(const int4* meta, const int* mp, int* nchild) {
-  GS_PDL_ENTRY();
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  if (i >= *mp) return;
-  const int4 mi = meta[i];
-  int c = 0;
-  if (!(mi.w & 1))
-    for (int ch = (int)i + 1; ch < mi.x && c < 8; ++c) ch = max(ch + 1, meta[ch].x);
-  nchild[i] = c;
-}
 
 // ------------------------------------------------------------ aggregates ---
 // Forward: tight AABB + sums of q and p; backward: sums of alpha and beta.
@@ -1040,7 +1032,7 @@ __device__ void write_node(const AggArgs<R>& a, int i, const int4& mi, int nch, 
   const bool leaf = mi.w & 1;
   // twig: an internal node whose children are all leaves (subtree = itself +
   // its children); opening it makes every point of it direct, no child gated
-  const bool twig = !leaf && mi.x - i - 1 == nch;
+  const bool twig = !leaf && nch == 0;  // nch: has an internal child (k_nodes)
   const int code = mi.x | (single ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0) |
                    (twig ? 0x20000000 : 0);
   V4<R> ua, ub;
@@ -1285,7 +1277,7 @@ __global__ void k_finalize(int mode, const int4* meta, const int* mp, const doub
       const bool leaf = mi.w & 1;
       // twig: an internal node whose children are all leaves (subtree = itself +
       // its children); opening it makes every point of it direct, no child gated
-      const bool twig = !leaf && nchild && mi.x - (int)i - 1 == nchild[i];
+      const bool twig = !leaf && nchild && nchild[i] == 0;
       const int code = mi.x | (single ? (int)0x80000000u : 0) | ((leaf && cnt > 1) ? 0x40000000 : 0) |
                        (twig ? 0x20000000 : 0);
       // half A = the unit this node contributes: its centroid and momentum sum,
@@ -1345,35 +1337,77 @@ __global__ void k_cells(const int4* meta, int64_t m, const uint64_t* skh, const 
   }
 }
 
-// exclusive scan of the node counts per position (k_count's, computed
-// inline from the lcp array; n + 1 outputs: out[n] = total), 3 phases
-__global__ void __launch_bounds__(1024) k_scan_blocks(const int* L, int64_t n, int* out, int* bsum) {
+// first[0..n]: exclusive scan of the node counts per position (computed
+// inline from the lcp array; first[n] = node count). One pass: 1024-position
+// tiles in the order of an atomic ticket, each publishing its sum and then
+// its inclusive prefix (flag << 30 | value), a warp looking back over 32
+// predecessors per round trip.
+constexpr unsigned kScanAgg = 1u << 30, kScanPre = 2u << 30, kScanVal = (1u << 30) - 1;
+__global__ void __launch_bounds__(1024) k_scan_nodes(const int* L, int64_t n, int* out,
+                                                     unsigned* desc, unsigned* ticket) {
   GS_PDL_ENTRY();
-  __shared__ int s[1024];
-  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  __shared__ int s_tile;
+  __shared__ int ws[32];
+  __shared__ unsigned s_excl;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t i = tile * 1024LL + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int v = 0;
   if (i < n) {
     int Lm, Lp, ci, lf;
     starts(L, n, i, Lm, Lp, ci, lf);
     v = ci + lf;
   }
-  s[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int t = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
-    __syncthreads();
-    s[threadIdx.x] += t;
-    __syncthreads();
+  int x = v;  // inclusive block scan
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
   }
-  if (i < n) out[i] = s[threadIdx.x] - v;
-  if (threadIdx.x == 1023) bsum[blockIdx.x] = s[1023];
-}
-
-__global__ void k_scan_add(int* out, int64_t n, const int* bsum_scanned, int nb) {
-  GS_PDL_ENTRY();
-  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
-  if (i < n && blockIdx.x > 0) out[i] += bsum_scanned[blockIdx.x];
-  if (i == 0) out[n] = bsum_scanned[nb];
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = ws[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    ws[lane] = w;  // inclusive over warps
+    const unsigned total = (unsigned)__shfl_sync(0xffffffffu, w, 31);
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[tile]);
+    unsigned excl = 0;
+    if (tile == 0) {
+      if (lane == 0) mine.store(kScanPre | total, cuda::memory_order_release);
+    } else {
+      if (lane == 0) mine.store(kScanAgg | total, cuda::memory_order_release);
+      for (int t = tile - 1; t >= 0;) {
+        const int p = t - lane;
+        unsigned st = kScanPre;  // (before tile 0: never consulted)
+        if (p >= 0) {
+          cuda::atomic_ref<unsigned, cuda::thread_scope_device> d(desc[p]);
+          st = d.load(cuda::memory_order_acquire);
+        }
+        const unsigned ready = __ballot_sync(0xffffffffu, (st & (kScanAgg | kScanPre)) != 0);
+        const unsigned pre = __ballot_sync(0xffffffffu, (st & kScanPre) != 0);
+        // lanes up to the nearest prefix must all have published
+        const int stop = pre ? __ffs(pre) - 1 : 31;
+        const unsigned need = stop == 31 ? 0xffffffffu : ((2u << stop) - 1u);
+        if ((ready & need) != need) continue;  // poll the same window again
+        unsigned add = lane <= stop ? (st & kScanVal) : 0u;
+        for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+        excl += add;
+        if (pre) break;
+        t -= 32;
+      }
+      if (lane == 0) mine.store(kScanPre | (excl + total), cuda::memory_order_release);
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  const int before = warp ? ws[warp - 1] : 0;
+  if (i < n) out[i] = (int)s_excl + before + x - v;
+  if (i == n - 1) out[n] = (int)s_excl + before + x;
 }
 
 }  // namespace
@@ -1440,17 +1474,10 @@ static int aggregate(int mode, int prec, DevTree& t, const void* src, const Kern
                       : aggregate_t<double>(mode, t, src, kc, st);
 }
 
-// first[0..n]: exclusive scan of the node counts per position (out[n] = m)
-static int scan_ints(const int* L, int64_t n, int* out, DBuf& scratch, cudaStream_t st) {
-  const int nb = nblocks(n, 1024);
-  GS_TRY_INT(scratch.ensure(sizeof(unsigned) * (nb + 2)));
-  unsigned* bs = scratch.as<unsigned>();
-  GS_CUDA_OK(pdl_launch(k_scan_blocks, nb, 1024, 0, st, L, n, out, (int*)bs));
-  // scan the block sums (nb + 1 entries, last = 0 -> becomes the total)
-  GS_CUDA_OK(cudaMemsetAsync(bs + nb, 0, sizeof(unsigned), st));
-  GS_CUDA_OK(pdl_launch(k_rs_scan, 1, 1024, 0, st, bs, nb + 1));
-  GS_CUDA_OK(pdl_launch(k_scan_add, nb, 1024, 0, st, out, n, (const int*)bs, nb));
-  GS_CUDA_OK(cudaGetLastError());
+// first[0..n] (out[n] = m) by k_scan_nodes; desc / ticket: zeroed scratch
+static int scan_ints(const int* L, int64_t n, int* out, unsigned* desc, unsigned* ticket,
+                     cudaStream_t st) {
+  GS_CUDA_OK(pdl_launch(k_scan_nodes, nblocks(n, 1024), 1024, 0, st, L, n, out, desc, ticket));
   return GS_OK;
 }
 
@@ -1481,9 +1508,10 @@ static int tie_sort(const Device& dev, int prec, const void* rec, DevTree& t, un
   GS_TRY_INT(t.tie_scr.ensure(sizeof(unsigned) * (3 * (size_t)t.n + 4096)));
   unsigned* chist = t.tie_scr.as<unsigned>();
   const unsigned* cctr = ctr;
+  int* L = t.lcp.as<int>();
   void* args[] = {(void*)&rec, (void*)&skh, (void*)&root, (void*)&cctr, (void*)&small_runs,
                   (void*)&big_runs, (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb,
-                  (void*)&chist};
+                  (void*)&chist, (void*)&L};
   GS_CUDA_OK(cudaLaunchCooperativeKernel(fn, grid, kNT, args, 0, st));
   return GS_OK;
 }
@@ -1545,7 +1573,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // counters; the tie lists' counters and flag), 8 x ntiles x 256 look-back
   // status words -- zeroed by one memset
   constexpr int kPasses = 8;
-  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256;
+  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256 + nblocks(n, 1024);
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
   GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
   unsigned* hist = t.hist.as<unsigned>();
@@ -1568,14 +1596,15 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // ties: runs of equal key_hi sorted by (key_lo, index) in place (perm,
   // skey_lo of the run members); tmp_v / tmp_v2 hold the run lists, tmp_k /
   // key_lo the long runs' merge buffers (all free after the key_hi sort)
-  GS_CUDA_OK(pdl_launch(k_tie_runs, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), n, ctr, (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr));
+  GS_CUDA_OK(pdl_launch(k_lcp_runs, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), n, t.lcp.as<int>(), ctr,
+                        (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr));
   GS_TRY_INT(tie_sort(dev, prec, rec, t, ctr, st));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(3, st);
   kt_mark(4, st);
   // 4. topology
-  GS_CUDA_OK(pdl_launch(k_lcp, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), n, t.lcp.as<int>()));
-  GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), t.scan_tmp, st));
+  GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), desc + (size_t)kPasses * ntiles * 256,
+                       ctr + kScanTicket, st));
   // The node count m = first[n] stays on the device: node arrays are sized
   // for 4n + 64 nodes (m ~ 1.5n for volumes and surfaces) and every kernel
   // reads m from first[n]; more nodes than that (degenerate clustering) raise
@@ -1595,11 +1624,11 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.squ.ensure(vb * n));
   const int mb = nblocks(cap, kNT);
   GS_TRY_INT(t.start.ensure(4 * cap));
-  GS_CUDA_OK(pdl_launch(k_node_starts, nb, kNT, 0, st, t.first.as<int>(), n, cap, t.start.as<int>(), overflow));
+  GS_CUDA_OK(pdl_launch(k_node_starts, nb, kNT, 0, st, t.first.as<int>(), n, cap, t.start.as<int>(),
+                        t.nchild.as<int>(), overflow));
   GS_CUDA_OK(pdl_launch(k_nodes, mb, kNT, 0, st, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
                               t.first.as<int>(), t.start.as<int>(), n, cap, t.meta.as<int4>(),
-                              t.parent.as<int>()));
-  GS_CUDA_OK(pdl_launch(k_children, mb, kNT, 0, st, t.meta.as<int4>(), t.first.as<int>() + n, t.nchild.as<int>()));
+                              t.parent.as<int>(), t.nchild.as<int>()));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(4, st);
   kt_mark(5, st);

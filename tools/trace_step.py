@@ -67,13 +67,17 @@ def main():
     gs.trace(False)
     names = kernel_names()
     ev = [(names.get((u, l), f"{u}:{l}"), t) for u, l, t in tr]
-    # steps end at k_step_inc (flow step counter); skip the first two (eager, capture)
-    steps, cur = [], []
+    # a step ends with its final stage's epilogue (which also advances the
+    # step counter); skip the first two steps (eager, capture)
+    stages = 4 if a.config == "c4bh" else 1
+    steps, cur, epis = [], [], 0
     for nm, t in ev:
         cur.append((nm, t))
-        if nm == "k_step_inc":
-            steps.append(cur)
-            cur = []
+        if nm == "k_fwd_epi":
+            epis += 1
+            if epis % stages == 0:
+                steps.append(cur)
+                cur = []
     share = collections.defaultdict(list)
     step_ns = []
     for k in range(2, len(steps)):
