@@ -898,7 +898,8 @@ __global__ void k_gather_adj(const V4<R>* adj, const int* perm, int64_t n, V4<R>
 // ------------------------------------------------------------ aggregates ---
 // Node aggregates (tight AABB + FP64 sums of q and p: mode 0; FP64 sums of
 // alpha and beta: mode 1) and the traversal records, after k_children. The
-// leaf order is cut into chunks of C points (1024 FP32 / 512 FP64), one CTA
+// leaf order is cut into chunks of C points (256 up to 256k points, else
+// 1024 FP32 / 512 FP64), one CTA
 // each (k_agg_chunk). The CTA gathers its chunk's points (by perm, writing the
 // leaf-order copies srec / squ or sadj on the way -- the build's gather fused
 // in) into shared memory. The nodes that start in the chunk are a contiguous
@@ -915,7 +916,6 @@ __global__ void k_gather_adj(const V4<R>* adj, const int* perm, int64_t n, V4<R>
 // chunk totals + head, in chunk order. Every reduction order is fixed
 // (deterministic), every point is read from HBM once per aggregate, and no
 // kernel waits on another's partial results.
-template <typename R> constexpr int chunk_of() { return sizeof(R) == 4 ? 1024 : 512; }
 constexpr int kSmallNode = 16;  // inside nodes above this are summed by a warp
 constexpr int kLevels = 33;     // levels 0..32 (32: depth-32 buckets)
 constexpr int kPartPerChunk = 1 + 2 * kLevels;  // total, head[33], tail[33]
@@ -1079,24 +1079,28 @@ __device__ __forceinline__ void warp_range(const V4<R>* su, const V4<R>* sv, int
     }
 }
 
-template <typename R>
+template <int C>
 __device__ __forceinline__ bool is_outer(const int4& mi) {
-  return mi.y / chunk_of<R>() != mi.z / chunk_of<R>();
+  return mi.y / C != mi.z / C;
 }
 
 // work items of a chunk's warps: a big inside node, the chunk total, a head
 // or a tail range
 enum { kItemNode = 0, kItemTotal = 1, kItemHead = 2, kItemTail = 3 };
 
-template <typename R, int MODE>
+// item slots: [0, kFixItems) heads (<= 33), the total and tails (<= 33);
+// [kFixItems, +C/4) big inside nodes -- more than that (chunks of many tight
+// clusters, each a chain of nested > 16-point nodes) are summed by their thread
+constexpr int kFixItems = 2 * kLevels + 2;
+
+template <typename R, int MODE, int C>
 __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
   GS_PDL_ENTRY();
-  constexpr int C = chunk_of<R>();
   __shared__ V4<R> su[C], sv[C];
   __shared__ int sl[C + 1];        // sl[1 + j] = lcp(c0 + j, c0 + j + 1); sl[0] = lcp(c0 - 1, c0)
   __shared__ int pm[C];            // pm[j] = min(sl[1 .. 1 + j]) (prefix minimum)
-  __shared__ int4 items[C / 4];    // {kind, node / level, b0, b1}
-  __shared__ int nitems;
+  __shared__ int4 items[kFixItems + C / 4];  // {kind, node / level, b0, b1}
+  __shared__ int nitems, nbig;
   const int chunk = blockIdx.x;
   const int64_t c0 = (int64_t)chunk * C;
   const int cl = (int)min((int64_t)C, a.n - c0);
@@ -1110,7 +1114,7 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
     md0 = a.meta[d0];
     nch0 = a.nchild[d0];
   }
-  if (threadIdx.x == 0) nitems = 0;
+  if (threadIdx.x == 0) nitems = nbig = 0;
   for (int k = threadIdx.x; k < cl; k += kNT) {  // gather the chunk (leaf-order copies on the way)
     const int64_t t = c0 + k;
     const int pi = a.perm[t];
@@ -1167,15 +1171,18 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
   for (int d = d0; d < ne; d += kNT) {
     const int4 md = d == d0 ? md0 : a.meta[d];
     const int nch = d == d0 ? nch0 : a.nchild[d];
-    if (is_outer<R>(md)) {  // its tail here; completed by k_agg_outer
+    if (is_outer<C>(md)) {  // its tail here; completed by k_agg_outer
       items[atomicAdd(&nitems, 1)] = make_int4(kItemTail, md.w >> 8, md.y - (int)c0, cl - 1);
       a.outer[atomicAdd(a.outer_cnt, 1)] = d;
       continue;
     }
     const int b0 = md.y - (int)c0, b1 = md.z - (int)c0;
     if (b1 - b0 + 1 > kSmallNode) {
-      items[atomicAdd(&nitems, 1)] = make_int4(kItemNode, d, b0, b1);
-      continue;
+      const int k = atomicAdd(&nbig, 1);
+      if (k < C / 4) {
+        items[kFixItems + k] = make_int4(kItemNode, d, b0, b1);
+        continue;
+      }
     }
     Sums s{};
     Box<R> x;
@@ -1187,8 +1194,9 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
   __syncthreads();
   // the warps' items: big inside nodes, the total, heads and tails
   const int lane = threadIdx.x & 31;
-  for (int k = threadIdx.x >> 5; k < nitems; k += kNT / 32) {
-    const int4 it = items[k];
+  const int nfix = nitems, nall = nfix + min(nbig, C / 4);
+  for (int k = threadIdx.x >> 5; k < nall; k += kNT / 32) {
+    const int4 it = items[k < nfix ? k : kFixItems + (k - nfix)];
     Sums s;
     Box<R> x;
     warp_range(su, sv, it.z, it.w, lane, MODE == 0, s, x);
@@ -1212,10 +1220,9 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
 // Outer nodes: tail (first chunk) + whole chunks + head (last chunk). One
 // warp per node: lanes take the chunk partials strided, a fixed butterfly
 // combines them (a fixed order: deterministic).
-template <typename R, int MODE>
+template <typename R, int MODE, int C>
 __global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
   GS_PDL_ENTRY();
-  constexpr int C = chunk_of<R>();
   const int c = *a.outer_cnt;
   const int lane = threadIdx.x & 31;
   for (int k = (blockIdx.x * kNT + threadIdx.x) >> 5; k < c; k += (gridDim.x * kNT) >> 5) {
@@ -1417,9 +1424,10 @@ int tree_finalize_fwd(int prec, DevTree& t, const KernelConsts& kc, cudaStream_t
 // Node aggregates + traversal records: mode 0 (boxes, sums of q and p, nrec;
 // the leaf-order copies srec / squ of the records `src`), mode 1 (sums of
 // alpha and beta, nadj; the leaf-order copy sadj of the adjoints `src`).
-template <typename R>
+// chunk of C leaf-order points per CTA: 256 below 256k points (more CTAs in
+// flight), else 1024 (FP32) / 512 (FP64)
+template <typename R, int C>
 static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts& kc, cudaStream_t st) {
-  constexpr int C = chunk_of<R>();
   const int64_t nch = (t.n + C - 1) / C;
   AggArgs<R> a{};
   a.meta = t.meta.as<int4>();
@@ -1454,15 +1462,15 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
     a.s0 = t.psum.as<double4>();
     a.s1 = t.msum.as<double4>();
     a.nrec = t.nrec.as<V4<R>>();
-    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 0>, (unsigned)nch, kNT, 0, st, a));
-    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 0>, 4 * 148, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 0, C>, (unsigned)nch, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 0, C>, 4 * 148, kNT, 0, st, a));
   } else {
     a.sadj = t.sadj.as<V4<R>>();
     a.s0 = t.asum.as<double4>();
     a.s1 = t.bsum.as<double4>();
     a.nadj = t.nadj.as<V4<R>>();
-    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 1>, (unsigned)nch, kNT, 0, st, a));
-    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 1>, 4 * 148, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_chunk<R, 1, C>, (unsigned)nch, kNT, 0, st, a));
+    GS_CUDA_OK(pdl_launch(k_agg_outer<R, 1, C>, 4 * 148, kNT, 0, st, a));
   }
   GS_CUDA_OK(cudaGetLastError());
   return GS_OK;
@@ -1470,8 +1478,10 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
 
 static int aggregate(int mode, int prec, DevTree& t, const void* src, const KernelConsts& kc,
                      cudaStream_t st) {
-  return prec == kF32 ? aggregate_t<float>(mode, t, src, kc, st)
-                      : aggregate_t<double>(mode, t, src, kc, st);
+  const bool small = t.n <= (1 << 18);
+  if (prec == kF32)
+    return small ? aggregate_t<float, 256>(mode, t, src, kc, st) : aggregate_t<float, 1024>(mode, t, src, kc, st);
+  return small ? aggregate_t<double, 256>(mode, t, src, kc, st) : aggregate_t<double, 512>(mode, t, src, kc, st);
 }
 
 // first[0..n] (out[n] = m) by k_scan_nodes; desc / ticket: zeroed scratch
