@@ -607,8 +607,20 @@ __device__ __forceinline__ void grp_sweep(int F, int& cursor, int ds, int de, Ac
   }
 }
 
+#ifndef GS_BH_GRP_MINB
+#define GS_BH_GRP_MINB 7
+#endif
+#ifndef GS_BH_GRP_HESS_MINB
+#define GS_BH_GRP_HESS_MINB 7
+#endif
+// FP32: registers capped for occupancy (the walk is load-latency bound)
 template <typename R, int MODE>
-__global__ void __launch_bounds__(kBhNT) k_bh_grp(const BhArgs<R> a) {
+constexpr int grp_min_blocks() {
+  return sizeof(R) != 4 ? 1 : (MODE == kBhHess ? GS_BH_GRP_HESS_MINB : GS_BH_GRP_MINB);
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(kBhNT, (grp_min_blocks<R, MODE>())) k_bh_grp(const BhArgs<R> a) {
   GS_TRACE_HERE();
   V4<R> x, xs, px, ai, bi;
   const int out = load_query<R, MODE>(a, blockIdx.x * kBhNT + threadIdx.x, x, xs, px, ai, bi);

@@ -567,15 +567,20 @@ int flow_advance(gs_flow* f, int steps) {
   f->launches = 0;
   const bool graphs = graphs_enabled() && !f->timer && !g_ktimer && f->shard_begin == 0 && f->shard_count == f->n;
   for (int k = 0; k < steps; ++k) {
-    if (!graphs || f->steps_done == 0) {  // the first step runs eagerly (energy, allocations)
+    bool stale = true;
+    if (graphs) {
+      stale = !f->gexec || f->gn != f->n || std::memcmp(&f->gkc, &f->kc, sizeof f->kc) != 0 ||
+              std::memcmp(&f->gcfg, &f->cfg, sizeof f->cfg) != 0;
+      if (!stale && f->gepoch != g_dbuf_epoch.load()) {  // some buffer somewhere moved: ours?
+        stale = flow_sig(f) != f->gsig;
+        if (!stale) f->gepoch = g_dbuf_epoch.load();
+      }
+    }
+    // the first step runs eagerly (its energy term, first-use allocations)
+    // unless an earlier run of this flow left a valid graph and no energy is wanted
+    if (!graphs || (f->steps_done == 0 && (stale || f->want_energy))) {
       GS_TRY(flow_step_eager(f));
       continue;
-    }
-    bool stale = !f->gexec || f->gn != f->n || std::memcmp(&f->gkc, &f->kc, sizeof f->kc) != 0 ||
-                 std::memcmp(&f->gcfg, &f->cfg, sizeof f->cfg) != 0;
-    if (!stale && f->gepoch != g_dbuf_epoch.load()) {  // some buffer somewhere moved: ours?
-      stale = flow_sig(f) != f->gsig;
-      if (!stale) f->gepoch = g_dbuf_epoch.load();
     }
     if (stale) GS_TRY(flow_capture_step(f));
     GS_CUDA_OK(cudaGraphLaunch(f->gexec, f->ctx->stream));
