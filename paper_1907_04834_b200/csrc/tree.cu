@@ -1234,6 +1234,8 @@ __global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
     box_init(x);
     const V4<R> z = mk4<R>(0, 0, 0);
     // slot sequence: tail(cb), total(cb + 1 .. ce - 1), head(ce)
+    // (the root spans every chunk: 4 chunks' partials in flight per lane)
+#pragma unroll 4
     for (int ch = cb + lane; ch <= ce; ch += 32) {
       const size_t slot = (size_t)ch * kPartPerChunk +
                           (ch == cb ? 1 + kLevels + lev : (ch == ce ? 1 + lev : 0));
@@ -1346,10 +1348,11 @@ __global__ void k_cells(const int4* meta, int64_t m, const uint64_t* skh, const 
 
 // first[0..n]: exclusive scan of the node counts per position (computed
 // inline from the lcp array; first[n] = node count). One pass: 1024-position
-// tiles in the order of an atomic ticket, each publishing its sum and then
+// tiles (4096 positions) in the order of an atomic ticket, each publishing its sum and then
 // its inclusive prefix (flag << 30 | value), a warp looking back over 32
 // predecessors per round trip.
 constexpr unsigned kScanAgg = 1u << 30, kScanPre = 2u << 30, kScanVal = (1u << 30) - 1;
+constexpr int kScanIPT = 4;  // positions per thread: 4096-position tiles
 __global__ void __launch_bounds__(1024) k_scan_nodes(const int* L, int64_t n, int* out,
                                                      unsigned* desc, unsigned* ticket) {
   GS_PDL_ENTRY();
@@ -1359,15 +1362,20 @@ __global__ void __launch_bounds__(1024) k_scan_nodes(const int* L, int64_t n, in
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t i = tile * 1024LL + threadIdx.x;
+  const int64_t i0 = (tile * 1024LL + threadIdx.x) * kScanIPT;  // this thread's positions
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int v = 0;
-  if (i < n) {
-    int Lm, Lp, ci, lf;
-    starts(L, n, i, Lm, Lp, ci, lf);
-    v = ci + lf;
+  int cnt[kScanIPT], v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanIPT; ++k) {
+    cnt[k] = 0;
+    if (i0 + k < n) {
+      int Lm, Lp, ci, lf;
+      starts(L, n, i0 + k, Lm, Lp, ci, lf);
+      cnt[k] = ci + lf;
+    }
+    v += cnt[k];
   }
-  int x = v;  // inclusive block scan
+  int x = v;  // inclusive block scan of the per-thread sums
   for (int o = 1; o < 32; o <<= 1) {
     const int u = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += u;
@@ -1412,9 +1420,13 @@ __global__ void __launch_bounds__(1024) k_scan_nodes(const int* L, int64_t n, in
     if (lane == 0) s_excl = excl;
   }
   __syncthreads();
-  const int before = warp ? ws[warp - 1] : 0;
-  if (i < n) out[i] = (int)s_excl + before + x - v;
-  if (i == n - 1) out[n] = (int)s_excl + before + x;
+  int run = (int)s_excl + (warp ? ws[warp - 1] : 0) + x - v;
+#pragma unroll
+  for (int k = 0; k < kScanIPT; ++k) {
+    if (i0 + k < n) out[i0 + k] = run;
+    run += cnt[k];
+    if (i0 + k == n - 1) out[n] = run;
+  }
 }
 
 }  // namespace
@@ -1487,7 +1499,7 @@ static int aggregate(int mode, int prec, DevTree& t, const void* src, const Kern
 // first[0..n] (out[n] = m) by k_scan_nodes; desc / ticket: zeroed scratch
 static int scan_ints(const int* L, int64_t n, int* out, unsigned* desc, unsigned* ticket,
                      cudaStream_t st) {
-  GS_CUDA_OK(pdl_launch(k_scan_nodes, nblocks(n, 1024), 1024, 0, st, L, n, out, desc, ticket));
+  GS_CUDA_OK(pdl_launch(k_scan_nodes, nblocks(n, 1024 * kScanIPT), 1024, 0, st, L, n, out, desc, ticket));
   return GS_OK;
 }
 

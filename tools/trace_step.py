@@ -4,7 +4,10 @@ kernel's share = time from its start to the next traced kernel's start (its
 run time plus the launch gap after it). Host-side events cannot time inside a
 captured graph; this can.
 
-  python tools/trace_step.py [--config c2|c4bh] [--prec f32|f64] [--backend bh|exact]
+  python tools/trace_step.py [--config c2|c4bh|c4bh0] [--prec f32|f64] [--backend bh|exact]
+
+c4bh: config 4 (N = 1M, RK4) through shoot_forward (10 steps; the flow
+diverges from step 4); c4bh0: its first steps only (no divergence).
 """
 import argparse
 import collections
@@ -59,17 +62,29 @@ def main():
         from bench import workload
         q, p = workload(1_000_000)
         cfg = ShootingConfig(sigma=0.0131, timesteps=10, backend=backend, integrator=RK4, precision=prec)
-    run = lambda: gs.shoot_forward(q, p, cfg, keep_trajectory=False)  # noqa: E731
-    run()
-    gs.trace(True)
-    run()
+    if a.config == "c4bh0":
+        # config 4's first RK4 steps only (its flow diverges from step 4 on:
+        # extent 1e9, most points in runs of equal 63-bit keys)
+        f = gs.flow(cfg, len(q))
+        f.upload(q, p)
+        f.advance(3)
+        f.sync()
+        f.upload(q, p)
+        gs.trace(True)
+        f.advance(3)  # graph-replayed from step 1 (captured above): steps 1-2 measured
+        f.sync()
+    else:
+        run = lambda: gs.shoot_forward(q, p, cfg, keep_trajectory=False)  # noqa: E731
+        run()
+        gs.trace(True)
+        run()
     tr = gs.trace_read()
     gs.trace(False)
     names = kernel_names()
     ev = [(names.get((u, l), f"{u}:{l}"), t) for u, l, t in tr]
     # a step ends with its final stage's epilogue (which also advances the
     # step counter); skip the first two steps (eager, capture)
-    stages = 4 if a.config == "c4bh" else 1
+    stages = 4 if a.config.startswith("c4") else 1
     steps, cur, epis = [], [], 0
     for nm, t in ev:
         cur.append((nm, t))
@@ -80,7 +95,7 @@ def main():
                 cur = []
     share = collections.defaultdict(list)
     step_ns = []
-    for k in range(2, len(steps)):
+    for k in range(0 if a.config == "c4bh0" else 2, len(steps)):
         st = steps[k]
         nxt = steps[k + 1][0][1] if k + 1 < len(steps) else None
         if nxt is None:
@@ -94,7 +109,7 @@ def main():
             share[nm].append(v)
     out = {"config": a.config, "prec": a.prec, "backend": a.backend, "steps_traced": len(step_ns),
            "step_us": float(np.mean(step_ns)) / 1e3 if step_ns else None,
-           "kernels_per_step": len(steps[2]) if len(steps) > 2 else None,
+           "kernels_per_step": len(steps[-1]) if steps else None,
            "share_us": {nm: round(float(np.mean(v)) / 1e3, 2) for nm, v in
                         sorted(share.items(), key=lambda x: -np.mean(x[1]))}}
     print(json.dumps(out, indent=1))
