@@ -150,43 +150,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__
   }
 }
 
-// ---- packed FP32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2) -----------------
-// Two targets share one 64-bit register pair; a source coordinate enters as a
-// scalar operand broadcast to both halves, so one issue slot does the work of
-// two scalar FP32 instructions.
-struct f2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ f2 pk2(float lo, float hi) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void up2(f2 a, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-  return r;
-}
-__device__ __forceinline__ f2 bc2(float x) { return pk2(x, x); }
-// 2^-x on the SFU for both halves (the negation folds into MUFU's operand)
-__device__ __forceinline__ f2 nex2x2(f2 r2) {
-  float lo, hi;
-  up2(r2, lo, hi);
-  return pk2(ex2(-lo), ex2(-hi));
-}
+// packed FP32x2 arithmetic (f2, sub2, mul2, fma2, ...): gs_common.cuh
 
 // Packed variant of k_rhs_f32: TPT targets per thread as TPT/2 register
 // pairs. Per two (target, source) pairs: 3 FADD2 + FMUL2 + 2 FFMA2 (r^2) +

@@ -59,6 +59,44 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// ---- packed FP32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2) ----
+// Two targets share one 64-bit register pair; a source coordinate enters as a
+// scalar operand broadcast to both halves, so one issue slot does the work of
+// two scalar FP32 instructions.
+struct f2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(f2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ f2 bc2(float x) { return pk2(x, x); }
+// 2^-x on the SFU for both halves (the negation folds into MUFU's operand)
+__device__ __forceinline__ f2 nex2x2(f2 r2) {
+  float lo, hi;
+  up2(r2, lo, hi);
+  return pk2(ex2(-lo), ex2(-hi));
+}
+
 // Per-call constants of the Gaussian kernel G(r) = exp(-r^2 / (2 sigma^2)).
 // FP32 kernels work in pre-scaled coordinates x' = kappa (x - c0) with
 // kappa^2 = log2(e) / (2 s), so that G = 2^(-|x'_i - x'_j|^2): one MUFU.EX2 per
