@@ -1490,10 +1490,18 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
 
 static int aggregate(int mode, int prec, DevTree& t, const void* src, const KernelConsts& kc,
                      cudaStream_t st) {
-  const bool small = t.n <= (1 << 18);
-  if (prec == kF32)
-    return small ? aggregate_t<float, 256>(mode, t, src, kc, st) : aggregate_t<float, 1024>(mode, t, src, kc, st);
-  return small ? aggregate_t<double, 256>(mode, t, src, kc, st) : aggregate_t<double, 512>(mode, t, src, kc, st);
+  static const int forced = [] {  // GS_AGG_CHUNK: 256 / 512 / 1024 (experiments)
+    const char* e = std::getenv("GS_AGG_CHUNK");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int C = forced ? forced : (t.n <= (1 << 18) ? 256 : (prec == kF32 ? 1024 : 512));
+  if (prec == kF32) {
+    if (C == 256) return aggregate_t<float, 256>(mode, t, src, kc, st);
+    if (C == 512) return aggregate_t<float, 512>(mode, t, src, kc, st);
+    return aggregate_t<float, 1024>(mode, t, src, kc, st);
+  }
+  if (C == 256) return aggregate_t<double, 256>(mode, t, src, kc, st);
+  return aggregate_t<double, 512>(mode, t, src, kc, st);
 }
 
 // first[0..n] (out[n] = m) by k_scan_nodes; desc / ticket: zeroed scratch
