@@ -25,6 +25,10 @@ for be in (EXACT, BARNES_HUT):
         for integ in (EULER, RK4):
             cfg = ShootingConfig(sigma=0.4, timesteps=7, backend=be, precision=prec, integrator=integ)
             fq, fp, e, st = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+            # a second call with the same configuration replays the step graph
+            # left by the first from step 1 on (graphs on; eager otherwise)
+            fq2, fp2, _, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+            assert np.array_equal(fq, fq2) and np.array_equal(fp, fp2)
             key = f"{be}_{prec}_{integ}"
             out[key + "_q"], out[key + "_p"] = fq, fp
             out[key + "_e"] = np.array([e])
@@ -76,3 +80,25 @@ def test_flow_and_tree_outlive_their_context():
     r = subprocess.run([sys.executable, "-c", LIFETIME], cwd=ROOT, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.returncode, r.stderr[-2000:])
+
+
+def test_kernel_trace_inside_graph(gs):
+    """gs_trace: the device-side start times of the build, walk and epilogue
+    kernels of graph-replayed Barnes-Hut steps (tools/trace_step.py)."""
+    from paper_1907_04834_b200 import BARNES_HUT, F32, ShootingConfig
+    from tests.util import sym_uniform, uniform
+    q, p = uniform(3000, 1.0, 31), sym_uniform(3000, 0.01, 32)
+    cfg = ShootingConfig(sigma=0.05, timesteps=4, backend=BARNES_HUT, precision=F32)
+    gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    gs.trace(True)
+    try:
+        gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+        tr = gs.trace_read()
+    finally:
+        gs.trace(False)
+    units = {u for u, _, _ in tr}
+    assert units == {1, 2, 3}  # tree.cu, bh.cu, epilogue.cu
+    t = np.array([v for _, _, v in tr], np.float64)
+    assert len(tr) >= 4 * 15 and (np.diff(t) >= 0).all()  # 4 steps in stream order
+    with pytest.raises(ValueError):
+        gs.trace_read()  # tracing off
