@@ -331,7 +331,8 @@ gs_status gs_profile_phases(gs_ctx* ctx, double* ms, int64_t* counts, int32_t ch
  * tree build, the Barnes-Hut walks and the epilogues appends {tag, device
  * %globaltimer ns} when its first CTA starts; tag = unit << 16 | source line
  * (unit 1 tree.cu, 2 bh.cu, 3 epilogue.cu). gs_trace_read copies up to max
- * entries, returns their number in *count and clears the trace. */
+ * entries, returns their number in *count and clears the trace. One trace per
+ * process, on the context's (first) device; entries beyond 16384 are dropped. */
 gs_status gs_trace(gs_ctx* ctx, int32_t enable);
 gs_status gs_trace_read(gs_ctx* ctx, uint64_t* tags, uint64_t* times_ns, int64_t max,
                         int64_t* count);
