@@ -103,13 +103,14 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
 }
 
 // ------------------------------------------------------------------ keys ---
-// Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo.
-// key_lo only orders points that share all 21 levels of key_hi (depth-32
-// clusters), so it is computed lazily: by k_keys_lo only when the sorted
-// key_hi has equal neighbours (or for a download).
+// Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo
+// (33 bits). key_lo only orders points that share all 21 levels of key_hi: the
+// sort uses it for those runs only, but computing it here (11 more levels of
+// the same replay) is cheaper than replaying 32 levels per run member later --
+// a diverged flow puts most points in such runs.
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
-                                              uint64_t* kh) {
+                                              uint64_t* kh, uint64_t* kl) {
   GS_PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= n) return;
@@ -131,6 +132,21 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
     h = (h << 3) | dig;
   }
   kh[i] = h;
+  uint64_t l = 0;
+#pragma unroll
+  for (int lev = 22; lev <= 32; ++lev) {
+    unsigned dig = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[a], hi[a]));
+      const bool up = x[a] >= c;
+      lo[a] = up ? c : lo[a];
+      hi[a] = up ? hi[a] : c;
+      dig |= (unsigned)up << a;
+    }
+    l = (l << 3) | dig;
+  }
+  kl[i] = l;
 }
 
 // levels 22..32 of point x whose levels 1..21 are h: the level-21 cell is
@@ -414,13 +430,9 @@ __global__ void k_lcp_runs(const uint64_t* skh, int64_t n, int* L, unsigned* ctr
 }
 
 // (key_lo << 31) | index: unique per point (n < 2^31), ordered as the full key
-template <typename R>
-__device__ __forceinline__ uint64_t tie_code(const V4<R>* rec, const int* perm, const uint64_t* skh,
-                                             const double* root, int64_t j) {
+__device__ __forceinline__ uint64_t tie_code(const uint64_t* klo, const int* perm, int64_t j) {
   const int p = perm[j];
-  const V4<R> q = ld4(rec + 2 * (int64_t)p);
-  const double x[3] = {(double)q.x, (double)q.y, (double)q.z};
-  return (key_lo_of(x, skh[j], root) << 31) | (uint64_t)p;
+  return (klo[p] << 31) | (uint64_t)p;
 }
 
 __device__ __forceinline__ void tie_put(int* perm, uint64_t* skl, int64_t j, uint64_t c) {
@@ -495,9 +507,7 @@ __device__ __forceinline__ int tie_task_run(const int4* big, int nbig, int g) {
 
 constexpr int kTieGroup = 16;  // chunks per digit-count group (look-up of a chunk's offsets)
 
-template <typename R>
-__global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64_t* skh,
-                                                  const double* root, const unsigned* ctr,
+__global__ void __launch_bounds__(kNT) k_tie_sort(const uint64_t* klo, const unsigned* ctr,
                                                   const int2* small_runs, int4* big_runs,
                                                   int* perm, uint64_t* skl, uint64_t* bufa,
                                                   uint64_t* bufb, unsigned* scr, int* L) {
@@ -516,8 +526,8 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
   for (int r = gw; r < nsmall; r += nw) {
     const int2 run = small_runs[r];
     // two codes per lane (runs of <= 64): rank = number of smaller codes
-    const uint64_t c0 = lane < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + lane) : ~0ull;
-    const uint64_t c1 = lane + 32 < run.y ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + 32 + lane) : ~0ull;
+    const uint64_t c0 = lane < run.y ? tie_code(klo, perm, (int64_t)run.x + lane) : ~0ull;
+    const uint64_t c1 = lane + 32 < run.y ? tie_code(klo, perm, (int64_t)run.x + 32 + lane) : ~0ull;
     int r0 = 0, r1 = 0;
     for (int k = 0; k < min(run.y, 32); ++k) {
       const uint64_t u = __shfl_sync(0xffffffffu, c0, k);
@@ -576,13 +586,13 @@ __global__ void __launch_bounds__(kNT) k_tie_sort(const V4<R>* rec, const uint64
     const int c0 = (g - run.z) * kTieChunk, cl = min(kTieChunk, run.y - c0);
     if (run.y > kTieChunk) {
       for (int i = threadIdx.x; i < cl; i += kNT)
-        bufa[(int64_t)run.x + c0 + i] = tie_code<R>(rec, perm, skh, root, (int64_t)run.x + c0 + i);
+        bufa[(int64_t)run.x + c0 + i] = tie_code(klo, perm, (int64_t)run.x + c0 + i);
       continue;
     }
     int P = 1;
     while (P < cl) P <<= 1;
     for (int i = threadIdx.x; i < P; i += kNT)
-      s[i] = i < cl ? tie_code<R>(rec, perm, skh, root, (int64_t)run.x + i) : ~0ull;
+      s[i] = i < cl ? tie_code(klo, perm, (int64_t)run.x + i) : ~0ull;
     __syncthreads();
     bitonic_smem(s, P);
     for (int i = threadIdx.x; i < cl; i += kNT) {
@@ -1513,25 +1523,23 @@ static int scan_ints(const int* L, int64_t n, int* out, unsigned* desc, unsigned
 
 // k_tie_sort as a cooperative launch: as many CTAs as can be co-resident (at
 // most 2 per SM), so grid.sync() is legal
-static int tie_sort(const Device& dev, int prec, const void* rec, DevTree& t, unsigned* ctr,
-                    cudaStream_t st) {
-  static int per_sm[2] = {0, 0};
-  const int pi = prec == kF32 ? 0 : 1;
-  void* fn = prec == kF32 ? (void*)k_tie_sort<float> : (void*)k_tie_sort<double>;
-  if (!per_sm[pi]) {
+static int tie_sort(const Device& dev, DevTree& t, unsigned* ctr, cudaStream_t st) {
+  static int per_sm = 0;
+  void* fn = (void*)k_tie_sort;
+  if (!per_sm) {
     int b = 0;
     GS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kNT, 0));
-    per_sm[pi] = std::max(1, std::min(2, b));
+    per_sm = std::max(1, std::min(2, b));
   }
-  const int grid = std::max(1, std::min(nblocks(t.n, kNT), per_sm[pi] * dev.sms));
-  const uint64_t* skh = t.skey_hi.as<uint64_t>();
-  const double* root = t.root.as<double>();
+  const int grid = std::max(1, std::min(nblocks(t.n, kNT), per_sm * dev.sms));
+  const uint64_t* klo = t.key_lo.as<uint64_t>();
   const int2* small_runs = (const int2*)t.tmp_v.ptr;
   int4* big_runs = (int4*)t.tmp_v2.ptr;
   int* perm = t.perm.as<int>();
   uint64_t* skl = t.skey_lo.as<uint64_t>();
   uint64_t* bufa = t.tmp_k.as<uint64_t>();
-  uint64_t* bufb = t.key_lo.as<uint64_t>();
+  GS_TRY_INT(t.tie_buf.ensure(8 * (size_t)t.n));
+  uint64_t* bufb = t.tie_buf.as<uint64_t>();
   // scratch of the long-run radix passes: slots (chunks of runs > 2048 points,
   // <= n / 1024, each run padded to whole groups of kTieGroup: <= 8.5 n / 1024)
   // x 256 digit counts + 2 x groups x 256 group sums: < 2.5 n words
@@ -1539,9 +1547,8 @@ static int tie_sort(const Device& dev, int prec, const void* rec, DevTree& t, un
   unsigned* chist = t.tie_scr.as<unsigned>();
   const unsigned* cctr = ctr;
   int* L = t.lcp.as<int>();
-  void* args[] = {(void*)&rec, (void*)&skh, (void*)&root, (void*)&cctr, (void*)&small_runs,
-                  (void*)&big_runs, (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb,
-                  (void*)&chist, (void*)&L};
+  void* args[] = {(void*)&klo, (void*)&cctr, (void*)&small_runs, (void*)&big_runs, (void*)&perm,
+                  (void*)&skl, (void*)&bufa, (void*)&bufb, (void*)&chist, (void*)&L};
   GS_CUDA_OK(cudaLaunchCooperativeKernel(fn, grid, kNT, args, 0, st));
   return GS_OK;
 }
@@ -1579,9 +1586,9 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // 2. keys
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
   else
-    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
@@ -1628,7 +1635,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // key_lo the long runs' merge buffers (all free after the key_hi sort)
   GS_CUDA_OK(pdl_launch(k_lcp_runs, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), n, t.lcp.as<int>(), ctr,
                         (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr));
-  GS_TRY_INT(tie_sort(dev, prec, rec, t, ctr, st));
+  GS_TRY_INT(tie_sort(dev, t, ctr, st));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(3, st);
   kt_mark(4, st);
@@ -1694,9 +1701,9 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
   else
-    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
   const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;
