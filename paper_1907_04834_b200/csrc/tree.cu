@@ -907,7 +907,7 @@ __global__ void k_gather_adj(const V4<R>* adj, const int* perm, int64_t n, V4<R>
 
 // ------------------------------------------------------------ aggregates ---
 // Node aggregates (tight AABB + FP64 sums of q and p: mode 0; FP64 sums of
-// alpha and beta: mode 1) and the traversal records, after k_children. The
+// alpha and beta: mode 1) and the traversal records, after k_nodes. The
 // leaf order is cut into chunks of C points (256 up to 256k points, else
 // 1024 FP32 / 512 FP64), one CTA
 // each (k_agg_chunk). The CTA gathers its chunk's points (by perm, writing the
