@@ -960,7 +960,8 @@ struct AggArgs {
   double4 *ps0, *ps1;
   V4<R>*plo, *phi;
   int* outer;      // outer nodes (listed by the chunk they start in)
-  int* outer_cnt;
+  int* outer_big;  // outer nodes spanning > kBigSpan chunks (a CTA each in k_agg_outer)
+  int* outer_cnt;  // [0] outer, [1] outer_big
   double kap, c0x, c0y, c0z;
   int scaled;
   int full;  // write the FP64 sums and boxes too (DevTree::lean = false)
@@ -1102,6 +1103,7 @@ enum { kItemNode = 0, kItemTotal = 1, kItemHead = 2, kItemTail = 3 };
 // [kFixItems, +C/4) big inside nodes -- more than that (chunks of many tight
 // clusters, each a chain of nested > 16-point nodes) are summed by their thread
 constexpr int kFixItems = 2 * kLevels + 2;
+constexpr int kBigSpan = 128;  // chunks: outer nodes spanning more get a CTA in k_agg_outer
 
 template <typename R, int MODE, int C>
 __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
@@ -1183,7 +1185,8 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
     const int nch = d == d0 ? nch0 : a.nchild[d];
     if (is_outer<C>(md)) {  // its tail here; completed by k_agg_outer
       items[atomicAdd(&nitems, 1)] = make_int4(kItemTail, md.w >> 8, md.y - (int)c0, cl - 1);
-      a.outer[atomicAdd(a.outer_cnt, 1)] = d;
+      if (md.z / C - md.y / C + 1 > kBigSpan) a.outer_big[atomicAdd(a.outer_cnt + 1, 1)] = d;
+      else a.outer[atomicAdd(a.outer_cnt, 1)] = d;
       continue;
     }
     const int b0 = md.y - (int)c0, b1 = md.z - (int)c0;
@@ -1233,8 +1236,62 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
 template <typename R, int MODE, int C>
 __global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
   GS_PDL_ENTRY();
-  const int c = *a.outer_cnt;
-  const int lane = threadIdx.x & 31;
+  const int c = a.outer_cnt[0], cbig = a.outer_cnt[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const V4<R> z = mk4<R>(0, 0, 0);
+  // nodes spanning many chunks (the root spans all): a CTA each, chunks
+  // strided over its threads, then warp butterflies and the 8 warp sums in
+  // order (fixed: deterministic)
+  for (int k = blockIdx.x; k < cbig; k += gridDim.x) {
+    const int d = a.outer_big[k];
+    const int4 md = a.meta[d];
+    const int lev = md.w >> 8, cb = md.y / C, ce = md.z / C;
+    Sums s{};
+    Box<R> x;
+    box_init(x);
+#pragma unroll 2
+    for (int ch = cb + (int)threadIdx.x; ch <= ce; ch += kNT) {
+      const size_t slot = (size_t)ch * kPartPerChunk +
+                          (ch == cb ? 1 + kLevels + lev : (ch == ce ? 1 + lev : 0));
+      add_part(s, x, ldcg4(a.ps0 + slot), ldcg4(a.ps1 + slot),
+               MODE == 0 ? ldcg4(a.plo + slot) : z, MODE == 0 ? ldcg4(a.phi + slot) : z);
+    }
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        s.a[q] += __shfl_xor_sync(0xffffffffu, s.a[q], o);
+        s.b[q] += __shfl_xor_sync(0xffffffffu, s.b[q], o);
+        x.l[q] = min(x.l[q], __shfl_xor_sync(0xffffffffu, x.l[q], o));
+        x.h[q] = max(x.h[q], __shfl_xor_sync(0xffffffffu, x.h[q], o));
+      }
+    __shared__ double ws[kNT / 32][6];
+    __shared__ R wb[kNT / 32][6];
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        ws[warp][q] = s.a[q];
+        ws[warp][3 + q] = s.b[q];
+        wb[warp][q] = x.l[q];
+        wb[warp][3 + q] = x.h[q];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Sums t{};
+      Box<R> y;
+      box_init(y);
+      for (int w = 0; w < kNT / 32; ++w)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          t.a[q] += ws[w][q];
+          t.b[q] += ws[w][3 + q];
+          y.l[q] = min(y.l[q], wb[w][q]);
+          y.h[q] = max(y.h[q], wb[w][3 + q]);
+        }
+      write_node<R, MODE>(a, d, md, a.nchild[d], t, y, z, z);
+    }
+    __syncthreads();
+  }
   for (int k = (blockIdx.x * kNT + threadIdx.x) >> 5; k < c; k += (gridDim.x * kNT) >> 5) {
     const int d = a.outer[k];
     const int4 md = a.meta[d];
@@ -1242,10 +1299,8 @@ __global__ void __launch_bounds__(kNT) k_agg_outer(const AggArgs<R> a) {
     Sums s{};
     Box<R> x;
     box_init(x);
-    const V4<R> z = mk4<R>(0, 0, 0);
     // slot sequence: tail(cb), total(cb + 1 .. ce - 1), head(ce)
-    // (the root spans every chunk: 4 chunks' partials in flight per lane)
-#pragma unroll 4
+#pragma unroll 2
     for (int ch = cb + lane; ch <= ce; ch += 32) {
       const size_t slot = (size_t)ch * kPartPerChunk +
                           (ch == cb ? 1 + kLevels + lev : (ch == ce ? 1 + lev : 0));
@@ -1472,10 +1527,14 @@ static int aggregate_t(int mode, DevTree& t, const void* src, const KernelConsts
   a.plo = reinterpret_cast<V4<R>*>(a.ps1 + parts);
   a.phi = a.plo + parts;
   // outer nodes: per level at most one starts in each chunk
-  GS_TRY_INT(t.outer.ensure(sizeof(int) * (64 + kLevels * (nch + 1))));
+  // (per level at most one outer node starts in a chunk; those spanning more
+  // than kBigSpan chunks are at most one per kBigSpan chunks per level)
+  const size_t nbig_cap = (size_t)kLevels * (nch / kBigSpan + 2);
+  GS_TRY_INT(t.outer.ensure(sizeof(int) * (64 + kLevels * (nch + 1) + nbig_cap)));
   a.outer_cnt = t.outer.as<int>();
   a.outer = a.outer_cnt + 64;
-  GS_CUDA_OK(cudaMemsetAsync(a.outer_cnt, 0, sizeof(int), st));
+  a.outer_big = a.outer + kLevels * (nch + 1);
+  GS_CUDA_OK(cudaMemsetAsync(a.outer_cnt, 0, 2 * sizeof(int), st));
   if (mode == 0) {
     a.srec = t.srec.as<V4<R>>();
     a.squ = t.squ.as<V4<R>>();
