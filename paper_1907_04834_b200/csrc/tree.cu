@@ -758,50 +758,63 @@ __device__ __forceinline__ void starts(const int* L, int64_t n, int64_t a, int& 
 }
 
 
-// lcp(a, x) >= l from the sorted keys: levels <= 21 need key_hi only (one
-// 8-B load per probe); key_lo is read only when the key_hi are equal -- which
-// only happens when neighbours tie (the lazily computed key_lo exists then)
+// lcp(a, x) >= l from the sorted keys. Levels <= 21 need key_hi only (one
+// 8-B load per probe); deeper levels exist only where neighbours tie and also
+// compare key_lo. Two instantiations, so the common search carries no key_lo
+// code at all (a merged version executed the deep branch predicated off: 12 %
+// of the node table's instructions).
+template <bool DEEP>
 __device__ __forceinline__ bool prefix_ge(uint64_t ah, uint64_t al, const uint64_t* kh,
                                           const uint64_t* kl, int64_t x, int l) {
   const uint64_t bh = kh[x];
-  if (l <= 21) return ((ah ^ bh) >> (3 * (21 - l))) == 0;
+  if (!DEEP) return ((ah ^ bh) >> (3 * (21 - l))) == 0;
   if (ah != bh) return false;
   return ((al ^ kl[x]) >> (3 * (32 - l))) == 0;
 }
 
 // largest b >= a with lcp(a, b) >= l
-__device__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t n, int64_t a,
-                                int l) {
-  const uint64_t ah = kh[a], al = l > 21 ? kl[a] : 0;
+template <bool DEEP>
+__device__ int64_t search_right_t(const uint64_t* kh, const uint64_t* kl, int64_t n, int64_t a,
+                                  int l) {
+  const uint64_t ah = kh[a], al = DEEP ? kl[a] : 0;
   int64_t step = 1, good = a;
-  while (a + step < n && prefix_ge(ah, al, kh, kl, a + step, l)) {
+  while (a + step < n && prefix_ge<DEEP>(ah, al, kh, kl, a + step, l)) {
     good = a + step;
     step <<= 1;
   }
   int64_t lo = good, hi = min(n - 1, a + step);  // lo good, (hi bad or end)
   while (hi > lo) {
     const int64_t mid = lo + (hi - lo + 1) / 2;
-    if (prefix_ge(ah, al, kh, kl, mid, l)) lo = mid;
+    if (prefix_ge<DEEP>(ah, al, kh, kl, mid, l)) lo = mid;
     else hi = mid - 1;
   }
   return lo;
 }
+__device__ __forceinline__ int64_t search_right(const uint64_t* kh, const uint64_t* kl, int64_t n,
+                                                int64_t a, int l) {
+  return l > 21 ? search_right_t<true>(kh, kl, n, a, l) : search_right_t<false>(kh, kl, n, a, l);
+}
 
 // smallest s <= a with lcp(s, a) >= l
-__device__ int64_t search_left(const uint64_t* kh, const uint64_t* kl, int64_t a, int l) {
-  const uint64_t ah = kh[a], al = l > 21 ? kl[a] : 0;
+template <bool DEEP>
+__device__ int64_t search_left_t(const uint64_t* kh, const uint64_t* kl, int64_t a, int l) {
+  const uint64_t ah = kh[a], al = DEEP ? kl[a] : 0;
   int64_t step = 1, good = a;
-  while (a - step >= 0 && prefix_ge(ah, al, kh, kl, a - step, l)) {
+  while (a - step >= 0 && prefix_ge<DEEP>(ah, al, kh, kl, a - step, l)) {
     good = a - step;
     step <<= 1;
   }
   int64_t hi = good, lo = max((int64_t)0, a - step);
   while (hi > lo) {
     const int64_t mid = lo + (hi - lo) / 2;
-    if (prefix_ge(ah, al, kh, kl, mid, l)) hi = mid;
+    if (prefix_ge<DEEP>(ah, al, kh, kl, mid, l)) hi = mid;
     else lo = mid + 1;
   }
   return hi;
+}
+__device__ __forceinline__ int64_t search_left(const uint64_t* kh, const uint64_t* kl, int64_t a,
+                                               int l) {
+  return l > 21 ? search_left_t<true>(kh, kl, a, l) : search_left_t<false>(kh, kl, a, l);
 }
 
 __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
