@@ -826,7 +826,7 @@ __device__ int parent_of(const uint64_t* kh, const uint64_t* kl, const int* L, c
 // The start position of every node: position a starts nodes
 // [first[a], first[a + 1]) -- cheap writes, so the searches below run one
 // node per thread (a position starting many levels no longer serialises them).
-__global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start, int* inner,
+__global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* start,
                               int* overflow) {
   GS_PDL_ENTRY();
   const int64_t a = blockIdx.x * (int64_t)kNT + threadIdx.x;
@@ -835,10 +835,7 @@ __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* sta
     if (a == 0 && overflow) atomicExch(overflow, 1);
     return;
   }
-  for (int idx = first[a]; idx < first[a + 1]; ++idx) {
-    start[idx] = (int)a;
-    inner[idx] = 0;  // set by k_nodes when an internal child names this node its parent
-  }
+  for (int idx = first[a]; idx < first[a + 1]; ++idx) start[idx] = (int)a;
 }
 
 // One node per thread: node idx starts at a = start[idx]; it is internal
@@ -847,11 +844,16 @@ __global__ void k_node_starts(const int* first, int64_t n, int64_t cap, int* sta
 // shares the node's level-l prefix (exponential + binary search on the sorted
 // keys); its parent is the node above it at the same start, or -- for the
 // first node at a position -- the level-(l-1) node found by a left search.
-// inner[p] = 1: node p has an internal child (else, if internal, it is a
-// twig: all children leaves -- the flag the traversal records carry)
+// inner[idx] = 1: internal node idx has an internal child (else it is a twig:
+// all children leaves -- the flag the traversal records carry). Children are
+// the maximal runs of its positions with lcp >= l + 1, so at level l < 31 it is
+// a twig iff every neighbour lcp inside its range is exactly l (<= 8 points);
+// at level 31 every child is a leaf. Parents (read by downloads only) are
+// computed when want_parent: the node above at the same start, or -- for the
+// first node at a position -- the level-(l-1) node found by a left search.
 __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, const int* first,
                         const int* start, int64_t n, int64_t cap, int4* meta, int* parent,
-                        int* inner) {
+                        int* inner, int want_parent) {
   GS_PDL_ENTRY();
   const int64_t idx = blockIdx.x * (int64_t)kNT + threadIdx.x;
   const int m = first[n];
@@ -865,9 +867,14 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
     const int l = l0 + k;
     const int64_t b = search_right(kh, kl, n, a, l);
     meta[idx] = make_int4(first[b + 1], (int)a, (int)b, l << 8);
-    const int par = l == 0 ? -1 : (k > 0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
-    parent[idx] = par;
-    if (par >= 0) inner[par] = 1;
+    bool twig = l == 31;
+    if (!twig && b - a < 8) {
+      twig = true;
+      for (int64_t t = a; t < b; ++t) twig = twig && L[t] == l;
+    }
+    inner[idx] = twig ? 0 : 1;
+    if (want_parent)
+      parent[idx] = l == 0 ? -1 : (k > 0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, l - 1));
     return;
   }
   int level;
@@ -879,7 +886,9 @@ __global__ void k_nodes(const uint64_t* kh, const uint64_t* kl, const int* L, co
     level = max(Lm, Lp) + 1;
   }
   meta[idx] = make_int4(first[b + 1], (int)a, (int)b, (level << 8) | 1);
-  parent[idx] = level == 0 ? -1 : (level - 1 >= l0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, level - 1));
+  inner[idx] = 0;
+  if (want_parent)
+    parent[idx] = level == 0 ? -1 : (level - 1 >= l0 ? (int)idx - 1 : parent_of(kh, kl, L, first, a, level - 1));
 }
 
 // per node: child count (the twig flag of the traversal record)
@@ -1734,10 +1743,10 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   const int mb = nblocks(cap, kNT);
   GS_TRY_INT(t.start.ensure(4 * cap));
   GS_CUDA_OK(pdl_launch(k_node_starts, nb, kNT, 0, st, t.first.as<int>(), n, cap, t.start.as<int>(),
-                        t.nchild.as<int>(), overflow));
+                        overflow));
   GS_CUDA_OK(pdl_launch(k_nodes, mb, kNT, 0, st, t.skey_hi.as<uint64_t>(), t.skey_lo.as<uint64_t>(), t.lcp.as<int>(),
                               t.first.as<int>(), t.start.as<int>(), n, cap, t.meta.as<int4>(),
-                              t.parent.as<int>(), t.nchild.as<int>()));
+                              t.parent.as<int>(), t.nchild.as<int>(), t.lean ? 0 : 1));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(4, st);
   kt_mark(5, st);
