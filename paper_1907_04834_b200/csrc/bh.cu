@@ -94,7 +94,7 @@ struct BhArgs {
   int lmd;             // literal-mean-dot aggregate dot scale (gs_config.literal_mean_dot)
   int by_index;        // RHS/HESS: queries are ev[0 .. nq) (a shard's records or arbitrary
                        // points, bh_point_*), not the tree's own points in leaf order
-  int dense;           // dense near fields: k_bh_grp unless GS_BH_KERNEL says otherwise
+  int dense;           // 1: dense near fields (windows); 2: very dense (k_bh_grp by default)
   int* sm_ctr;         // non-null: blocks claim SM-local contiguous query blocks (claim_block)
   unsigned long long* dbg;  // GS_BH_DEBUG: group-walk counters (warps, iterations, segments, steps)
   V4<R>* part;
@@ -767,7 +767,7 @@ template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
   // literal-mean-dot: independent walks only (the group walk has no LMD variant)
   const int choice = bh_kernel_choice();
-  const int kind = a.lmd ? 1 : (choice ? choice : (a.dense ? 3 : 1));
+  const int kind = a.lmd ? 1 : (choice ? choice : (a.dense >= 2 ? 3 : 1));
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
@@ -978,9 +978,15 @@ int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* den
     for (int a = 0; a < 3; ++a)
       if (kc.ext[a] > 0) frac *= std::min(1.0, 2.0 * thr / kc.ext[a]);
     const int64_t cap = std::max<int64_t>(1, (int64_t(4) << 20) / std::max<int64_t>(nq, 1));
-    if (frac * (double)n >= 1024.0) {
+    // estimated points within thr of a point (the host bounding box at the
+    // flow's upload): >= 1024 -> 32 node windows; >= 4096 -> the group walk
+    // too (configs 3 and 5: 16k / 4.9k; config 2's 2.9k keeps the independent
+    // walk -- its flow spreads: 5.90 vs 6.07 ms over 20 steps, config 5
+    // 39.7 vs 35.9 ms per subject the other way)
+    const double est = frac * (double)n;
+    if (est >= 1024.0) {
       K = (int)std::max<int64_t>(K, std::min<int64_t>(32, cap));
-      if (dense) *dense = 1;
+      if (dense) *dense = est >= 4096.0 ? 2 : 1;
     }
   }
   if (forced > 0) K = forced;  // the regime (dense) is still detected

@@ -101,7 +101,7 @@ struct BhQuery {
   int ntask = 1;  // node windows (bh_tasks); part holds [ntask][queries] partials
   int lmd = 0;    // literal-mean-dot dot scale (RHS also sums c into the B partial's .w)
   int by_index = 0;  // RHS/HESS: queries = the n_tgt records at ev, not the tree's points
-  int dense = 0;     // dense near fields (bh_tasks): the group walk is the default kernel
+  int dense = 0;     // bh_tasks: 1 dense near fields (32 windows), 2 very dense (group walk)
 };
 int bh_tasks(int64_t nq, int64_t n, double thr, const KernelConsts& kc, int* dense = nullptr);
 // host threads driving flows on one GPU at once (batched subjects); per thread
