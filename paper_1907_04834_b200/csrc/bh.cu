@@ -767,7 +767,9 @@ template <typename R>
 int launch(int mode, BhArgs<R> a, cudaStream_t st) {
   // literal-mean-dot: independent walks only (the group walk has no LMD variant)
   const int choice = bh_kernel_choice();
-  const int kind = a.lmd ? 1 : (choice ? choice : (a.dense >= 2 ? 3 : 1));
+  // (FP64: the group walk from dense on -- config 2 FP64 8.75 vs 9.0 ms)
+  const int grp_from = sizeof(R) == 8 ? 1 : 2;
+  const int kind = a.lmd ? 1 : (choice ? choice : (a.dense >= grp_from ? 3 : 1));
   const dim3 nb(std::max(1, (a.nq + kBhNT - 1) / kBhNT), std::max(1, a.ntask));
   static const bool dbg = std::getenv("GS_BH_DEBUG") != nullptr;
   static unsigned long long* dbuf = nullptr;
