@@ -230,26 +230,38 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int6
     if (hs[t]) atomicAdd(&hist[t], hs[t]);
 }
 
-// (4 tiles per SM at 8 keys per thread: 1M points = 489 tiles in one wave)
+// NT threads x IPT keys per tile; the digit-parallel parts (scans, look-back)
+// run on threads 0..255, one digit each. 256 x 8 (4 tiles per SM): N = 1M is
+// one wave of 489 tiles; 512 x 8 (2 per SM): 245 tiles, half the look-back
+// chain -- the critical path of a pass (a tile finds its prefix ~tile / 16
+// round trips after the passes start).
 constexpr int kLB = 8;  // look-back: predecessors' status words loaded per round trip
-template <int kRsIPT>
-__global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, const int* vin,
+template <int kRsIPT, int NT>
+constexpr size_t onesweep_smem() {
+  return sizeof(unsigned) * (NT / 32) * 256 + sizeof(uint64_t) * NT * kRsIPT + sizeof(int) * NT * kRsIPT;
+}
+template <int kRsIPT, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 4) k_rs_onesweep(const uint64_t* kin, const int* vin,
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
                                                       unsigned* desc, unsigned* tile_ctr) {
   GS_PDL_ENTRY();
-  constexpr int kTile = kRsNT * kRsIPT;
-  __shared__ unsigned wh[kRsNT / 32][256];  // per-warp digit counts -> offsets within the tile's digit run
-  __shared__ unsigned wsum[2][kRsNT / 32];  // per-warp sums of the two digit scans
-  __shared__ unsigned ts[256];              // tile-local digit starts
-  __shared__ unsigned gofs[256];            // global position of tile-local slot 0 of each digit run
-  __shared__ uint64_t sk[kTile];            // the tile in digit order (coalesced write-out)
-  __shared__ int sv[kTile];
+  constexpr int kTile = NT * kRsIPT;
+  extern __shared__ __align__(16) unsigned char os_smem[];
+  // per-warp digit counts -> offsets within the tile's digit run; the tile in
+  // digit order (coalesced write-out)
+  unsigned (*wh)[256] = reinterpret_cast<unsigned (*)[256]>(os_smem);
+  uint64_t* sk = reinterpret_cast<uint64_t*>(os_smem + sizeof(unsigned) * (NT / 32) * 256);
+  int* sv = reinterpret_cast<int*>(sk + kTile);
+  __shared__ unsigned wsum[2][8];  // per-warp sums of the two digit scans (threads 0..255)
+  __shared__ unsigned ts[256];     // tile-local digit starts
+  __shared__ unsigned gofs[256];   // global position of tile-local slot 0 of each digit run
   __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool dig_thread = threadIdx.x < 256;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
-  for (int w = 0; w < kRsNT / 32; ++w) wh[w][threadIdx.x] = 0;
-  const unsigned dtot = dig_tot[threadIdx.x];
+  for (int i = threadIdx.x; i < (NT / 32) * 256; i += NT) (&wh[0][0])[i] = 0;
+  const unsigned dtot = dig_thread ? dig_tot[threadIdx.x] : 0u;
   __syncthreads();
   const int tile = s_tile;
   const int64_t t0 = (int64_t)tile * kTile;
@@ -288,16 +300,17 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
     loc[r] = base + __popc(pm & ((1u << lane) - 1u));
   }
   __syncthreads();
-  const unsigned d = threadIdx.x;
+  const unsigned d = threadIdx.x & 255u;
   unsigned tot = 0;
-  for (int w = 0; w < kRsNT / 32; ++w) {
-    const unsigned t = wh[w][d];
-    wh[w][d] = tot;
-    tot += t;
-  }
+  if (dig_thread)
+    for (int w = 0; w < NT / 32; ++w) {
+      const unsigned t = wh[w][d];
+      wh[w][d] = tot;
+      tot += t;
+    }
   // publish this tile's count for digit d as early as possible (look-back)
   cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
-  if (tile != 0) mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
+  if (dig_thread && tile != 0) mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
   // inclusive scans over digits (thread d = digit d): global digit totals and
   // this tile's counts -- warp shuffles, then the 8 warp sums
   unsigned gi = dtot, ti = tot;
@@ -306,13 +319,15 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
     const unsigned g = __shfl_up_sync(0xffffffffu, gi, o), t = __shfl_up_sync(0xffffffffu, ti, o);
     if (lane >= o) gi += g, ti += t;
   }
-  if (lane == 31) wsum[0][warp] = gi, wsum[1][warp] = ti;
+  if (dig_thread && lane == 31) wsum[0][warp] = gi, wsum[1][warp] = ti;
   __syncthreads();
-  for (int w = 0; w < warp; ++w) gi += wsum[0][w], ti += wsum[1][w];
+  if (dig_thread)
+    for (int w = 0; w < warp; ++w) gi += wsum[0][w], ti += wsum[1][w];
   const unsigned tstart = ti - tot;
   // this tile's offset inside digit d: decoupled look-back over earlier tiles
   unsigned excl = 0;
-  if (tile == 0) {
+  if (!dig_thread) {
+  } else if (tile == 0) {
     mine.store(kRsFlagPrefix | tot, cuda::memory_order_relaxed);
   } else {
     // kLB predecessors' status words per round trip (independent loads),
@@ -342,8 +357,10 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
     }
     mine.store(kRsFlagPrefix | (excl + tot), cuda::memory_order_relaxed);
   }
-  gofs[d] = gi - dtot + excl - tstart;
-  ts[d] = tstart;
+  if (dig_thread) {
+    gofs[d] = gi - dtot + excl - tstart;
+    ts[d] = tstart;
+  }
   __syncthreads();
   // stage the tile in (digit, rank) order ...
 #pragma unroll
@@ -361,7 +378,7 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
   const int cnt = n - t0 < kTile ? (int)(n - t0) : kTile;
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
-    const int i = r * kRsNT + threadIdx.x;
+    const int i = r * NT + threadIdx.x;
     if (i < cnt) {
       const uint64_t k = sk[i];
       const unsigned pos = gofs[(unsigned)(k >> shift) & 255u] + (unsigned)i;
@@ -372,10 +389,22 @@ __global__ void __launch_bounds__(kRsNT, 4) k_rs_onesweep(const uint64_t* kin, c
 }
 
 // one one-sweep pass, IPT keys per thread
-int onesweep(int ipt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi, uint64_t* ko,
-              int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc, unsigned* ctr) {
-  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_onesweep<8>, ntiles, kRsNT, 0, st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
-  else GS_CUDA_OK(pdl_launch(k_rs_onesweep<4>, ntiles, kRsNT, 0, st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+int onesweep(int ipt, int nt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi,
+             uint64_t* ko, int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc,
+             unsigned* ctr) {
+  if (nt == 512) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(k_rs_onesweep<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)onesweep_smem<8, 512>());
+      return true;
+    }();
+    (void)attr;
+    GS_CUDA_OK(pdl_launch(k_rs_onesweep<8, 512>, ntiles, 512, onesweep_smem<8, 512>(), st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  } else if (ipt == 8) {
+    GS_CUDA_OK(pdl_launch(k_rs_onesweep<8, 256>, ntiles, 256, onesweep_smem<8, 256>(), st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  } else {
+    GS_CUDA_OK(pdl_launch(k_rs_onesweep<4, 256>, ntiles, 256, onesweep_smem<4, 256>(), st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  }
   return GS_OK;
 }
 
@@ -1684,8 +1713,18 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     const int v = e ? std::atoi(e) : 0;
     return (v == 4 || v == 8) ? v : 0;
   }();
+  static const int nt_env = [] {  // GS_RS_NT: 256 / 512 threads per one-sweep tile
+    const char* e = std::getenv("GS_RS_NT");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 256 || v == 512) ? v : 0;
+  }();
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
-  const int ntiles = nblocks(n, kRsNT * ipt);
+  // 512-thread tiles (half the look-back chain) while they fit one wave (2 per
+  // SM: up to ~1.2M points; 1M: sort 0.197 -> 0.176 ms); beyond, 256 x 8 tiles
+  const bool fits512 = ipt == 8 && nblocks(n, 512 * ipt) <= 2 * dev.sms;
+  const int rs_nt = nt_env ? (nt_env == 512 && ipt == 8 ? 512 : 256) : (fits512 ? 512 : 256);
+  const int ntiles = nblocks(n, rs_nt * ipt);
+  const int hblocks = nblocks(n, kRsNT * ipt);  // k_rs_hist_all: 256 x IPT keys per block
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
   // one-sweep scratch: 8 digit histograms, 32 counters (8 passes' tile
   // counters; the tie lists' counters and flag), 8 x ntiles x 256 look-back
@@ -1697,15 +1736,15 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   unsigned* hist = t.hist.as<unsigned>();
   unsigned* ctr = hist + kPasses * 256;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
-  else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   {
     const uint64_t* ka = t.key_hi.as<uint64_t>();
     const int* va = nullptr;  // first pass: the value is the index
     for (int p = 0; p < kPasses; ++p) {
       uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
       int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      GS_TRY_INT(onesweep(ipt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
+      GS_TRY_INT(onesweep(ipt, rs_nt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
                desc + (size_t)p * ntiles * 256, ctr + p));
       ka = kb;
       va = vb;
@@ -1801,7 +1840,7 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
     uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
     int* vb2 = (p & 1) ? t.perm.as<int>() : t.tmp_v.as<int>();
     unsigned* dq = desc + (size_t)p * ntiles * 256;
-    GS_TRY_INT(onesweep(ipt, ntiles, st, ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p));
+    GS_TRY_INT(onesweep(ipt, 256, ntiles, st, ka, va, kb, vb2, n, 8 * p, hist + p * 256, dq, ctr + p));
     ka = kb;
     va = vb2;
   }
