@@ -232,16 +232,16 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int6
 
 // NT threads x IPT keys per tile; the digit-parallel parts (scans, look-back)
 // run on threads 0..255, one digit each. 256 x 8 (4 tiles per SM): N = 1M is
-// one wave of 489 tiles; 512 x 8 (2 per SM): 245 tiles, half the look-back
-// chain -- the critical path of a pass (a tile finds its prefix ~tile / 16
-// round trips after the passes start).
+// one wave of 489 tiles; 512 x 8 (2 per SM) 245 tiles, 1024 x 8 (1 per SM)
+// 123 -- each halving the look-back chain, the critical path of a pass (a
+// tile finds its prefix ~tile / 16 round trips after the pass starts).
 constexpr int kLB = 8;  // look-back: predecessors' status words loaded per round trip
 template <int kRsIPT, int NT>
 constexpr size_t onesweep_smem() {
   return sizeof(unsigned) * (NT / 32) * 256 + sizeof(uint64_t) * NT * kRsIPT + sizeof(int) * NT * kRsIPT;
 }
 template <int kRsIPT, int NT>
-__global__ void __launch_bounds__(NT, NT == 512 ? 2 : 4) k_rs_onesweep(const uint64_t* kin, const int* vin,
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs_onesweep(const uint64_t* kin, const int* vin,
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
                                                       unsigned* desc, unsigned* tile_ctr) {
@@ -392,7 +392,15 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : 4) k_rs_onesweep(const uin
 int onesweep(int ipt, int nt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi,
              uint64_t* ko, int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc,
              unsigned* ctr) {
-  if (nt == 512) {
+  if (nt == 1024) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(k_rs_onesweep<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)onesweep_smem<8, 1024>());
+      return true;
+    }();
+    (void)attr;
+    GS_CUDA_OK(pdl_launch(k_rs_onesweep<8, 1024>, ntiles, 1024, onesweep_smem<8, 1024>(), st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  } else if (nt == 512) {
     static const bool attr = [] {
       cudaFuncSetAttribute(k_rs_onesweep<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)onesweep_smem<8, 512>());
@@ -1716,13 +1724,17 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   static const int nt_env = [] {  // GS_RS_NT: 256 / 512 threads per one-sweep tile
     const char* e = std::getenv("GS_RS_NT");
     const int v = e ? std::atoi(e) : 0;
-    return (v == 256 || v == 512) ? v : 0;
+    return (v == 256 || v == 512 || v == 1024) ? v : 0;
   }();
   const int ipt = ipt_env ? ipt_env : (n >= (1 << 19) ? 8 : 4);
-  // 512-thread tiles (half the look-back chain) while they fit one wave (2 per
-  // SM: up to ~1.2M points; 1M: sort 0.197 -> 0.176 ms); beyond, 256 x 8 tiles
-  const bool fits512 = ipt == 8 && nblocks(n, 512 * ipt) <= 2 * dev.sms;
-  const int rs_nt = nt_env ? (nt_env == 512 && ipt == 8 ? 512 : 256) : (fits512 ? 512 : 256);
+  // the biggest tiles that still fit one wave -- 1024 x 8 (one per SM) up to
+  // ~1.2M points, else 512 x 8 (two per SM), else 256 x 8: fewer tiles, a
+  // shorter look-back chain (1M: sort 0.197 -> 0.176 -> 0.169 ms for 489 ->
+  // 245 -> 123 tiles); beyond one wave of any, 256 x 8 (4M: 0.54 vs 0.56 ms)
+  int auto_nt = 256;
+  if (ipt == 8 && nblocks(n, 1024 * ipt) <= dev.sms) auto_nt = 1024;
+  else if (ipt == 8 && nblocks(n, 512 * ipt) <= 2 * dev.sms) auto_nt = 512;
+  const int rs_nt = nt_env ? (nt_env > 256 && ipt == 8 ? nt_env : 256) : auto_nt;
   const int ntiles = nblocks(n, rs_nt * ipt);
   const int hblocks = nblocks(n, kRsNT * ipt);  // k_rs_hist_all: 256 x IPT keys per block
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
