@@ -105,12 +105,14 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
 // ------------------------------------------------------------------ keys ---
 // Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo
 // (33 bits). key_lo only orders points that share all 21 levels of key_hi: the
-// sort uses it for those runs only, but computing it here (11 more levels of
-// the same replay) is cheaper than replaying 32 levels per run member later --
-// a diverged flow puts most points in such runs.
+// sort uses it for those runs only. Where the previous build had such runs (a
+// diverged flow puts most points in them) computing it here (11 more levels
+// of the same replay, +12 us at 1M) is cheaper than replaying 32 levels per
+// run member later; otherwise the tie sort replays it for its few members.
 template <typename R>
 __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const double* root,
-                                              uint64_t* kh, uint64_t* kl) {
+                                              uint64_t* kh, uint64_t* kl, const unsigned* want_lo,
+                                              unsigned* lo_valid) {
   GS_PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
   if (i >= n) return;
@@ -132,6 +134,12 @@ __global__ void __launch_bounds__(kNT) k_keys(const V4<R>* rec, int64_t n, const
     h = (h << 3) | dig;
   }
   kh[i] = h;
+  // the deep key when the previous build of this tree had ties (want_lo: its
+  // tie flag, still in the sort scratch; null: unknown -> yes); else the tie
+  // sort replays it for run members itself (k_tie_sort, lo_valid = 0)
+  const bool do_lo = want_lo == nullptr || *want_lo != 0;
+  if (i == 0) *lo_valid = do_lo ? 1u : 0u;
+  if (!do_lo) return;
   uint64_t l = 0;
 #pragma unroll
   for (int lev = 22; lev <= 32; ++lev) {
@@ -467,9 +475,32 @@ __global__ void k_lcp_runs(const uint64_t* skh, int64_t n, int* L, unsigned* ctr
 }
 
 // (key_lo << 31) | index: unique per point (n < 2^31), ordered as the full key
-__device__ __forceinline__ uint64_t tie_code(const uint64_t* klo, const int* perm, int64_t j) {
+// key_lo source of the tie sort: k_keys' array, or a replay from the point
+struct TieKeys {
+  const uint64_t* klo;
+  const void* rec;  // the build's records (float4 / double4 pairs)
+  const double* root;
+  const uint64_t* skh;
+  int f32;
+  int valid;  // k_keys computed klo this build
+};
+__device__ __forceinline__ uint64_t tie_code(const TieKeys& tk, const int* perm, int64_t j) {
   const int p = perm[j];
-  return (klo[p] << 31) | (uint64_t)p;
+  uint64_t l;
+  if (tk.valid) {
+    l = tk.klo[p];
+  } else {
+    double x[3];
+    if (tk.f32) {
+      const float4 q = ld4(static_cast<const float4*>(tk.rec) + 2 * (int64_t)p);
+      x[0] = q.x; x[1] = q.y; x[2] = q.z;
+    } else {
+      const double4 q = ld4(static_cast<const double4*>(tk.rec) + 2 * (int64_t)p);
+      x[0] = q.x; x[1] = q.y; x[2] = q.z;
+    }
+    l = key_lo_of(x, tk.skh[j], tk.root);
+  }
+  return (l << 31) | (uint64_t)p;
 }
 
 __device__ __forceinline__ void tie_put(int* perm, uint64_t* skl, int64_t j, uint64_t c) {
@@ -544,12 +575,14 @@ __device__ __forceinline__ int tie_task_run(const int4* big, int nbig, int g) {
 
 constexpr int kTieGroup = 16;  // chunks per digit-count group (look-up of a chunk's offsets)
 
-__global__ void __launch_bounds__(kNT) k_tie_sort(const uint64_t* klo, const unsigned* ctr,
+__global__ void __launch_bounds__(kNT) k_tie_sort(TieKeys klo, const unsigned* lo_valid,
+                                                  const unsigned* ctr,
                                                   const int2* small_runs, int4* big_runs,
                                                   int* perm, uint64_t* skl, uint64_t* bufa,
                                                   uint64_t* bufb, unsigned* scr, int* L) {
   GS_PDL_ENTRY();
   if (ctr[kTieFlag] == 0) return;  // (uniform over the grid)
+  klo.valid = (int)*lo_valid;
   cg::grid_group grid = cg::this_grid();
   __shared__ uint64_t s[kTieChunk];
   __shared__ unsigned wh[kNT / 32][256];
@@ -1641,7 +1674,7 @@ static int scan_ints(const int* L, int64_t n, int* out, unsigned* desc, unsigned
 
 // k_tie_sort as a cooperative launch: as many CTAs as can be co-resident (at
 // most 2 per SM), so grid.sync() is legal
-static int tie_sort(const Device& dev, DevTree& t, unsigned* ctr, cudaStream_t st) {
+static int tie_sort(const Device& dev, DevTree& t, const void* rec, unsigned* ctr, cudaStream_t st) {
   static int per_sm = 0;
   void* fn = (void*)k_tie_sort;
   if (!per_sm) {
@@ -1650,7 +1683,9 @@ static int tie_sort(const Device& dev, DevTree& t, unsigned* ctr, cudaStream_t s
     per_sm = std::max(1, std::min(2, b));
   }
   const int grid = std::max(1, std::min(nblocks(t.n, kNT), per_sm * dev.sms));
-  const uint64_t* klo = t.key_lo.as<uint64_t>();
+  TieKeys klo{t.key_lo.as<uint64_t>(), rec, t.root.as<double>(), t.skey_hi.as<uint64_t>(),
+              t.prec == kF32 ? 1 : 0, 1};
+  const unsigned* lo_valid = t.klo_flag.as<unsigned>();
   const int2* small_runs = (const int2*)t.tmp_v.ptr;
   int4* big_runs = (int4*)t.tmp_v2.ptr;
   int* perm = t.perm.as<int>();
@@ -1665,8 +1700,8 @@ static int tie_sort(const Device& dev, DevTree& t, unsigned* ctr, cudaStream_t s
   unsigned* chist = t.tie_scr.as<unsigned>();
   const unsigned* cctr = ctr;
   int* L = t.lcp.as<int>();
-  void* args[] = {(void*)&klo, (void*)&cctr, (void*)&small_runs, (void*)&big_runs, (void*)&perm,
-                  (void*)&skl, (void*)&bufa, (void*)&bufb, (void*)&chist, (void*)&L};
+  void* args[] = {(void*)&klo, (void*)&lo_valid, (void*)&cctr, (void*)&small_runs, (void*)&big_runs,
+                  (void*)&perm, (void*)&skl, (void*)&bufa, (void*)&bufb, (void*)&chist, (void*)&L};
   GS_CUDA_OK(cudaLaunchCooperativeKernel(fn, grid, kNT, args, 0, st));
   return GS_OK;
 }
@@ -1701,12 +1736,27 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>()));
     GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
   }
-  // 2. keys
+  // 2. keys (the deep key too when the previous build of this tree had ties:
+  // its tie flag is still in the sort scratch, whose counters sit at a fixed
+  // offset; no scratch yet -> compute it)
   const int nb = nblocks(n, kNT);
+  GS_TRY_INT(t.klo_flag.ensure(16));
+  static const int keys_lo_env = [] {  // GS_KEYS_LO: 0 never (tests the tie sort's replay), 1 always
+    const char* e = std::getenv("GS_KEYS_LO");
+    return e ? std::atoi(e) : -1;
+  }();
+  GS_TRY_INT(t.scal.ensure(64));
+  if (keys_lo_env >= 0) {  // a constant "previous tie flag" (scal word 8; static source:
+                           // a captured copy replays from it)
+    static const unsigned v = (unsigned)keys_lo_env;
+    GS_CUDA_OK(cudaMemcpyAsync(t.scal.as<unsigned>() + 8, &v, sizeof v, cudaMemcpyHostToDevice, st));
+  }
+  const unsigned* want_lo = keys_lo_env >= 0 ? t.scal.as<unsigned>() + 8
+                            : (t.hist.ptr ? t.hist.as<unsigned>() + 8 * 256 + kTieFlag : nullptr);
   if (prec == kF32)
-    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), want_lo, t.klo_flag.as<unsigned>()));
   else
-    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), want_lo, t.klo_flag.as<unsigned>()));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(2, st);
   kt_mark(3, st);
@@ -1767,7 +1817,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   // key_lo the long runs' merge buffers (all free after the key_hi sort)
   GS_CUDA_OK(pdl_launch(k_lcp_runs, nb, kNT, 0, st, t.skey_hi.as<uint64_t>(), n, t.lcp.as<int>(), ctr,
                         (int2*)t.tmp_v.ptr, (int4*)t.tmp_v2.ptr));
-  GS_TRY_INT(tie_sort(dev, t, ctr, st));
+  GS_TRY_INT(tie_sort(dev, t, rec, ctr, st));
   GS_CUDA_OK(cudaGetLastError());
   kt_mark(3, st);
   kt_mark(4, st);
@@ -1833,9 +1883,9 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
   const int nb = nblocks(n, kNT);
   if (prec == kF32)
-    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), nullptr, t.klo_flag.as<unsigned>()));
   else
-    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>()));
+    GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), nullptr, t.klo_flag.as<unsigned>()));
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
   const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;

@@ -349,3 +349,35 @@ def test_lmd_shooting_matches_reference(gs, ref_lmd, prec, tol):
     rep, g, _, _ = ref_lmd.evaluate(q, p, t, sigma, 1.0, 10, 1, threads=8)
     assert ev.report["total"] == pytest.approx(rep[2], rel=tol)
     assert rel_l2(ev.gradient, g) <= tol * 10
+
+
+REPLAY = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+from paper_1907_04834_b200 import Geoshoot, F32, F64
+from tests.test_gpu_bh import SETS, dfs_leaf_order
+import oracle
+gs, ref = Geoshoot(0), oracle.ref()
+for name in ("duplicates", "cluster", "clusters_120k", "cluster_12k", "short_runs", "one_run_100k"):
+    for prec in (F64, F32):
+        q, p = SETS[name]()
+        if prec == F32:
+            q, p = q.astype(np.float32).astype(np.float64), p.astype(np.float32).astype(np.float64)
+        d = gs.build_tree(q, p, precision=prec).download()
+        assert np.array_equal(d["order"], dfs_leaf_order(ref.tree(q, p).dump())), (name, prec)
+print("ok")
+"""
+
+
+def test_tie_sort_replays_the_deep_key():
+    """k_keys computes the deep key only when the previous build of the tree had
+    ties; otherwise the tie sort replays it for the run members. GS_KEYS_LO=0
+    forces the replay for every build: the leaf order must still be the
+    reference's on every tie set."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", REPLAY], cwd=root, capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, GS_KEYS_LO="0"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
