@@ -1271,10 +1271,17 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
     }
   }
   if (threadIdx.x == 0) items[atomicAdd(&nitems, 1)] = make_int4(kItemTotal, 0, 0, cl - 1);
-  // the nodes starting in the chunk
+  // the nodes starting in the chunk (the next node's meta loaded one
+  // iteration ahead, before this one's work)
+  int4 md_cur = md0;
+  int nch_cur = nch0;
   for (int d = d0; d < ne; d += kNT) {
-    const int4 md = d == d0 ? md0 : a.meta[d];
-    const int nch = d == d0 ? nch0 : a.nchild[d];
+    const int4 md = md_cur;
+    const int nch = nch_cur;
+    if (d + kNT < ne) {
+      md_cur = a.meta[d + kNT];
+      nch_cur = a.nchild[d + kNT];
+    }
     if (is_outer<C>(md)) {  // its tail here; completed by k_agg_outer
       items[atomicAdd(&nitems, 1)] = make_int4(kItemTail, md.w >> 8, md.y - (int)c0, cl - 1);
       if (md.z / C - md.y / C + 1 > kBigSpan) a.outer_big[atomicAdd(a.outer_cnt + 1, 1)] = d;
