@@ -1219,10 +1219,27 @@ __global__ void __launch_bounds__(kNT) k_agg_chunk(const AggArgs<R> a) {
     nch0 = a.nchild[d0];
   }
   if (threadIdx.x == 0) nitems = nbig = 0;
-  for (int k = threadIdx.x; k < cl; k += kNT) {  // gather the chunk (leaf-order copies on the way)
+  // gather the chunk (leaf-order copies on the way): all of this thread's
+  // perm loads, then all its record loads, in flight together
+  constexpr int kPer = C / kNT;
+  int pis[kPer];
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int k = threadIdx.x + r * kNT;
+    pis[r] = k < cl ? a.perm[c0 + k] : 0;
+  }
+  V4<R> us[kPer], vs[kPer];
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    us[r] = ld4(a.rec + 2 * pis[r]);
+    vs[r] = ld4(a.rec + 2 * pis[r] + 1);
+  }
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int k = threadIdx.x + r * kNT;
+    if (k >= cl) break;
     const int64_t t = c0 + k;
-    const int pi = a.perm[t];
-    const V4<R> u = ld4(a.rec + 2 * pi), v = ld4(a.rec + 2 * pi + 1);
+    const V4<R> u = us[r], v = vs[r];
     if (MODE == 0) {
       st4(a.squ + t, mk4<R>(u.x, u.y, u.z));
       st4(a.srec + 2 * t, scaled_q(a, u));
