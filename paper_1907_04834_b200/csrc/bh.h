@@ -45,6 +45,7 @@ struct DevTree {
   DBuf tie_scr;         // k_tie_sort's digit counts (long runs of equal key_hi)
   DBuf tie_buf;         // k_tie_sort's second code buffer
   DBuf klo_flag;        // u32: k_keys computed key_lo this build
+  DBuf bbox_ctr;        // u32: k_bbox's arrival counter (self-resetting)
   DBuf scan_tmp;
   DBuf sm_ctr;          // i32 [1024] per-SM query-block counters of the walk (k_bh_ws)
   DBuf pq_win;          // u32 [windows][queries][3] per-window per-query counters (folded)

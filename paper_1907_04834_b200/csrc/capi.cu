@@ -529,7 +529,7 @@ uint64_t flow_sig(const gs_flow* f) {
   for (const DBuf* b : {&t.key_hi, &t.key_lo, &t.perm, &t.skey_hi, &t.skey_lo, &t.lcp, &t.first,
                         &t.srec, &t.squ, &t.sadj, &t.meta, &t.parent, &t.nchild, &t.lo,
                         &t.hi, &t.cen, &t.mom, &t.nrec, &t.nadj, &t.psum, &t.msum,
-                        &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist, &t.tie_scr, &t.tie_buf, &t.klo_flag,
+                        &t.asum, &t.bsum, &t.root, &t.tmp_k, &t.tmp_v, &t.tmp_v2, &t.hist, &t.tie_scr, &t.tie_buf, &t.klo_flag, &t.bbox_ctr,
                         &t.scan_tmp, &t.scal, &t.outer, &t.parts, &t.start, &t.sm_ctr})
     mix(*b);
   return h;

@@ -38,43 +38,8 @@ constexpr int kNT = 256;
 inline int nblocks(int64_t n, int nt) { return (int)std::max<int64_t>(1, (n + nt - 1) / nt); }
 
 // ------------------------------------------------------------------ bbox ---
-template <typename R>
-__global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, double* part) {
-  GS_PDL_ENTRY();
-  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-    const V4<R> q = ld4(rec + 2 * i);
-    const double v[3] = {(double)q.x, (double)q.y, (double)q.z};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = fmin(lo[a], v[a]);
-      hi[a] = fmax(hi[a], v[a]);
-    }
-  }
-  __shared__ double s[6][kNT / 32];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    for (int o = 16; o > 0; o >>= 1) {
-      lo[a] = fmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], o));
-      hi[a] = fmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      s[a][threadIdx.x >> 5] = lo[a];
-      s[3 + a][threadIdx.x >> 5] = hi[a];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 6) {
-    double r = s[threadIdx.x][0];
-    for (int w = 1; w < kNT / 32; ++w)
-      r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][w]) : fmax(r, s[threadIdx.x][w]);
-    part[6 * blockIdx.x + threadIdx.x] = r;
-  }
-}
-
 // root = [lo - pad, hi + pad], pad = 1e-9 * (hi - lo)   (octree.cpp:9,27-35)
-__global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, double* root) {
-  GS_PDL_ENTRY();
+__device__ void bbox_root(const double* part, int nb, double* root) {
   __shared__ double s[6][kNT / 32];
   double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
   for (int b = threadIdx.x; b < nb; b += kNT)
@@ -101,6 +66,53 @@ __global__ void __launch_bounds__(kNT) k_bbox_final(const double* part, int nb, 
     root[3 + a] = __dadd_rn(hi, pad);
   }
 }
+
+template <typename R>
+__global__ void __launch_bounds__(kNT) k_bbox(const V4<R>* rec, int64_t n, double* part,
+                                              unsigned* done, double* root) {
+  GS_PDL_ENTRY();
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const V4<R> q = ld4(rec + 2 * i);
+    const double v[3] = {(double)q.x, (double)q.y, (double)q.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fmin(lo[a], v[a]);
+      hi[a] = fmax(hi[a], v[a]);
+    }
+  }
+  __shared__ double s[6][kNT / 32];
+  __shared__ bool s_last;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_down_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_down_sync(0xffffffffu, hi[a], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s[a][threadIdx.x >> 5] = lo[a];
+      s[3 + a][threadIdx.x >> 5] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double r = s[threadIdx.x][0];
+    for (int w = 1; w < kNT / 32; ++w)
+      r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][w]) : fmax(r, s[threadIdx.x][w]);
+    part[6 * blockIdx.x + threadIdx.x] = r;
+  }
+  // the last block to finish reduces the partials to the padded root box (the
+  // arrival counter resets itself for the next build)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *done = 0;
+  bbox_root(part, gridDim.x, root);
+}
+
 
 // ------------------------------------------------------------------ keys ---
 // Levels 1..21 -> key_hi (63 bits, level 1 most significant), 22..32 -> key_lo
@@ -1751,14 +1763,18 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   GS_TRY_INT(t.scal.ensure(64));
   const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
   GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
+  {  // k_bbox's arrival counter: zeroed when allocated, then reset by each last block
+    void* before = t.bbox_ctr.ptr;
+    GS_TRY_INT(t.bbox_ctr.ensure(16));
+    if (t.bbox_ctr.ptr != before) GS_CUDA_OK(cudaMemsetAsync(t.bbox_ctr.ptr, 0, 16, st));
+  }
   kt_mark(2, st);
   // 1. padded root box (or the caller's explicit root cell)
   if (root_box) {
     GS_CUDA_OK(cudaMemcpyAsync(t.root.ptr, root_box, 6 * sizeof(double), cudaMemcpyHostToDevice, st));
   } else {
-    if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>()));
-    else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>()));
-    GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
+    if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>(), t.bbox_ctr.as<unsigned>(), t.root.as<double>()));
+    else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>(), t.bbox_ctr.as<unsigned>(), t.root.as<double>()));
   }
   // 2. keys (the deep key too when the previous build of this tree had ties:
   // its tie flag is still in the sort scratch, whose counters sit at a fixed
@@ -1902,10 +1918,15 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
   GS_TRY_INT(t.squ.ensure(vb * n));
   const int bb = std::min(nblocks(n, kNT), 2 * dev.sms);
   GS_TRY_INT(t.scan_tmp.ensure(sizeof(double) * 6 * bb + 64));
-  if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>()));
-  else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>()));
-  GS_CUDA_OK(pdl_launch(k_bbox_final, 1, kNT, 0, st, t.scan_tmp.as<double>(), bb, t.root.as<double>()));
+  {  // k_bbox's arrival counter: zeroed when allocated, then reset by each last block
+    void* before = t.bbox_ctr.ptr;
+    GS_TRY_INT(t.bbox_ctr.ensure(16));
+    if (t.bbox_ctr.ptr != before) GS_CUDA_OK(cudaMemsetAsync(t.bbox_ctr.ptr, 0, 16, st));
+  }
+  if (prec == kF32) GS_CUDA_OK(pdl_launch(k_bbox<float>, bb, kNT, 0, st, (const float4*)rec, n, t.scan_tmp.as<double>(), t.bbox_ctr.as<unsigned>(), t.root.as<double>()));
+  else GS_CUDA_OK(pdl_launch(k_bbox<double>, bb, kNT, 0, st, (const double4*)rec, n, t.scan_tmp.as<double>(), t.bbox_ctr.as<unsigned>(), t.root.as<double>()));
   const int nb = nblocks(n, kNT);
+  GS_TRY_INT(t.klo_flag.ensure(16));
   if (prec == kF32)
     GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), nullptr, t.klo_flag.as<unsigned>()));
   else
