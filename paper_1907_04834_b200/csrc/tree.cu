@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(kNT) k_keys_lo_leaf(const V4<R>* squ, const in
 // Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, one-sweep
 // passes (below): stable within-tile ranking with warp match/popc.
 constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a template parameter
+constexpr int kHistWords = 7 * 512;  // digit histograms of every pass (8 x 256 or 7 x 512)
 
 
 // ---- one-sweep passes ---------------------------------------------------------
@@ -231,11 +232,12 @@ constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a temp
 constexpr unsigned kRsFlagAgg = 1u << 30, kRsFlagPrefix = 2u << 30, kRsCountMask = (1u << 30) - 1;
 
 // digit histograms of all 8 passes in one read of the keys
-template <int kRsIPT>
+template <int kRsIPT, int BITS = 8>
 __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int64_t n, unsigned* hist) {
   GS_PDL_ENTRY();
-  __shared__ unsigned hs[8 * 256];
-  for (int t = threadIdx.x; t < 8 * 256; t += kRsNT) hs[t] = 0;
+  constexpr int DIG = 1 << BITS, NP = (63 + BITS - 1) / BITS;
+  __shared__ unsigned hs[NP * DIG];
+  for (int t = threadIdx.x; t < NP * DIG; t += kRsNT) hs[t] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * (kRsNT * kRsIPT);
   for (int r = 0; r < kRsIPT; ++r) {
@@ -243,10 +245,10 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int6
     if (i >= n) break;
     const uint64_t k = key[i];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) atomicAdd(&hs[q * 256 + ((unsigned)(k >> (8 * q)) & 255u)], 1u);
+    for (int q = 0; q < NP; ++q) atomicAdd(&hs[q * DIG + ((unsigned)(k >> (BITS * q)) & (DIG - 1))], 1u);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 8 * 256; t += kRsNT)
+  for (int t = threadIdx.x; t < NP * DIG; t += kRsNT)
     if (hs[t]) atomicAdd(&hist[t], hs[t]);
 }
 
@@ -256,31 +258,36 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int6
 // 123 -- each halving the look-back chain, the critical path of a pass (a
 // tile finds its prefix ~tile / 16 round trips after the pass starts).
 constexpr int kLB = 8;  // look-back: predecessors' status words loaded per round trip
-template <int kRsIPT, int NT>
+template <int kRsIPT, int NT, int BITS = 8>
 constexpr size_t onesweep_smem() {
-  return sizeof(unsigned) * (NT / 32) * 256 + sizeof(uint64_t) * NT * kRsIPT + sizeof(int) * NT * kRsIPT;
+  return sizeof(unsigned) * (NT / 32) * (1 << BITS) + sizeof(unsigned) * 2 * (1 << BITS) +
+         sizeof(uint64_t) * NT * kRsIPT + sizeof(int) * NT * kRsIPT;
 }
-template <int kRsIPT, int NT>
+template <int kRsIPT, int NT, int BITS = 8>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs_onesweep(const uint64_t* kin, const int* vin,
                                                       uint64_t* kout, int* vout, int64_t n,
                                                       int shift, const unsigned* dig_tot,
                                                       unsigned* desc, unsigned* tile_ctr) {
   GS_PDL_ENTRY();
   constexpr int kTile = NT * kRsIPT;
+  constexpr int DIG = 1 << BITS;
+  constexpr unsigned kMask = DIG - 1;
+  static_assert(NT >= DIG, "one digit per thread");
   extern __shared__ __align__(16) unsigned char os_smem[];
-  // per-warp digit counts -> offsets within the tile's digit run; the tile in
-  // digit order (coalesced write-out)
-  unsigned (*wh)[256] = reinterpret_cast<unsigned (*)[256]>(os_smem);
-  uint64_t* sk = reinterpret_cast<uint64_t*>(os_smem + sizeof(unsigned) * (NT / 32) * 256);
+  // per-warp digit counts -> offsets within the tile's digit run; tile-local
+  // digit starts; global position of tile-local slot 0 of each digit run; the
+  // tile in digit order (coalesced write-out)
+  unsigned (*wh)[DIG] = reinterpret_cast<unsigned (*)[DIG]>(os_smem);
+  unsigned* ts = reinterpret_cast<unsigned*>(os_smem + sizeof(unsigned) * (NT / 32) * DIG);
+  unsigned* gofs = ts + DIG;
+  uint64_t* sk = reinterpret_cast<uint64_t*>(gofs + DIG);
   int* sv = reinterpret_cast<int*>(sk + kTile);
-  __shared__ unsigned wsum[2][8];  // per-warp sums of the two digit scans (threads 0..255)
-  __shared__ unsigned ts[256];     // tile-local digit starts
-  __shared__ unsigned gofs[256];   // global position of tile-local slot 0 of each digit run
+  __shared__ unsigned wsum[2][DIG / 32];  // per-warp sums of the two digit scans
   __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool dig_thread = threadIdx.x < 256;
+  const bool dig_thread = threadIdx.x < DIG;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < (NT / 32) * 256; i += NT) (&wh[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < (NT / 32) * DIG; i += NT) (&wh[0][0])[i] = 0;
   const unsigned dtot = dig_thread ? dig_tot[threadIdx.x] : 0u;
   __syncthreads();
   const int tile = s_tile;
@@ -305,9 +312,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
     const bool ok = seg + r * 32 + lane < n;
-    const unsigned d = (unsigned)(key[r] >> shift) & 255u;
-    // (invalid lanes -- tail tile only -- match among themselves on digit 256)
-    const unsigned pm = __match_any_sync(0xffffffffu, ok ? d : 256u);
+    const unsigned d = (unsigned)(key[r] >> shift) & kMask;
+    // (invalid lanes -- tail tile only -- match among themselves on digit DIG)
+    const unsigned pm = __match_any_sync(0xffffffffu, ok ? d : (unsigned)DIG);
     peers[r] = ok ? pm : 0u;
     old[r] = 0;
     if (ok && lane == __ffs(pm) - 1) old[r] = atomicAdd(&wh[warp][d], (unsigned)__popc(pm));
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
     loc[r] = base + __popc(pm & ((1u << lane) - 1u));
   }
   __syncthreads();
-  const unsigned d = threadIdx.x & 255u;
+  const unsigned d = threadIdx.x & kMask;
   unsigned tot = 0;
   if (dig_thread)
     for (int w = 0; w < NT / 32; ++w) {
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
       tot += t;
     }
   // publish this tile's count for digit d as early as possible (look-back)
-  cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * 256 + d]);
+  cuda::atomic_ref<unsigned, cuda::thread_scope_device> mine(desc[(int64_t)tile * DIG + d]);
   if (dig_thread && tile != 0) mine.store(kRsFlagAgg | tot, cuda::memory_order_relaxed);
   // inclusive scans over digits (thread d = digit d): global digit totals and
   // this tile's counts -- warp shuffles, then the 8 warp sums
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
       for (int k = 0; k < kLB; ++k) {
         v[k] = kRsFlagPrefix;  // (before tile 0: never reached, tile 0 is a prefix)
         if (t - k >= 0) {
-          cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)(t - k) * 256 + d]);
+          cuda::atomic_ref<unsigned, cuda::thread_scope_device> prev(desc[(int64_t)(t - k) * DIG + d]);
           v[k] = prev.load(cuda::memory_order_relaxed);
         }
       }
@@ -386,7 +393,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
     if (seg + r * 32 + lane < n) {
-      const unsigned dd = (unsigned)(key[r] >> shift) & 255u;
+      const unsigned dd = (unsigned)(key[r] >> shift) & kMask;
       const unsigned slot = ts[dd] + wh[warp][dd] + loc[r];
       sk[slot] = key[r];
       sv[slot] = val[r];
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
     const int i = r * NT + threadIdx.x;
     if (i < cnt) {
       const uint64_t k = sk[i];
-      const unsigned pos = gofs[(unsigned)(k >> shift) & 255u] + (unsigned)i;
+      const unsigned pos = gofs[(unsigned)(k >> shift) & kMask] + (unsigned)i;
       kout[pos] = k;
       vout[pos] = sv[i];
     }
@@ -411,8 +418,16 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
 // one one-sweep pass, IPT keys per thread
 int onesweep(int ipt, int nt, int ntiles, cudaStream_t st, const uint64_t* ki, const int* vi,
              uint64_t* ko, int* vo, int64_t n, int shift, const unsigned* dig_tot, unsigned* desc,
-             unsigned* ctr) {
-  if (nt == 1024) {
+             unsigned* ctr, int bits = 8) {
+  if (nt == 1024 && bits == 9) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(k_rs_onesweep<8, 1024, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)onesweep_smem<8, 1024, 9>());
+      return true;
+    }();
+    (void)attr;
+    GS_CUDA_OK(pdl_launch(k_rs_onesweep<8, 1024, 9>, ntiles, 1024, onesweep_smem<8, 1024, 9>(), st, ki, vi, ko, vo, n, shift, dig_tot, desc, ctr));
+  } else if (nt == 1024) {
     static const bool attr = [] {
       cudaFuncSetAttribute(k_rs_onesweep<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)onesweep_smem<8, 1024>());
@@ -1792,7 +1807,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
     GS_CUDA_OK(cudaMemcpyAsync(t.scal.as<unsigned>() + 8, &v, sizeof v, cudaMemcpyHostToDevice, st));
   }
   const unsigned* want_lo = keys_lo_env >= 0 ? t.scal.as<unsigned>() + 8
-                            : (t.hist.ptr ? t.hist.as<unsigned>() + 8 * 256 + kTieFlag : nullptr);
+                            : (t.hist.ptr ? t.hist.as<unsigned>() + kHistWords + kTieFlag : nullptr);
   if (prec == kF32)
     GS_CUDA_OK(pdl_launch(k_keys<float>, nb, kNT, 0, st, (const float4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), want_lo, t.klo_flag.as<unsigned>()));
   else
@@ -1828,26 +1843,38 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   const int ntiles = nblocks(n, rs_nt * ipt);
   const int hblocks = nblocks(n, kRsNT * ipt);  // k_rs_hist_all: 256 x IPT keys per block
   GS_TRY_INT(t.tmp_v2.ensure(4 * n));
-  // one-sweep scratch: 8 digit histograms, 32 counters (8 passes' tile
-  // counters; the tie lists' counters and flag), 8 x ntiles x 256 look-back
-  // status words -- zeroed by one memset
-  constexpr int kPasses = 8;
-  const size_t words = (size_t)kPasses * 256 + 32 + (size_t)kPasses * ntiles * 256 + nblocks(n, 1024);
+  // digits: 9 bits (7 passes over the 63-bit key) with the 1024-thread tiles
+  // (one digit per thread; 1M: sort 0.168 -> 0.162 ms), else 8 bits (8 passes)
+  static const int bits_env = [] {
+    const char* e = std::getenv("GS_RS_BITS");
+    const int v = e ? std::atoi(e) : 0;
+    return (v == 8 || v == 9) ? v : 0;
+  }();
+  const int bits = rs_nt == 1024 ? (bits_env ? bits_env : 9) : 8;
+  const int npass = (63 + bits - 1) / bits, dig = 1 << bits;
+  // one-sweep scratch: the passes' digit histograms (kHistWords), 32 counters
+  // (the passes' tile counters; the tie lists' counters and flag -- a fixed
+  // offset, read by the next build's k_keys), npass x ntiles x dig look-back
+  // status words, the node scan's look-back words -- zeroed by one memset
+  const size_t words = (size_t)kHistWords + 32 + (size_t)npass * ntiles * dig + nblocks(n, 1024);
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
   GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
   unsigned* hist = t.hist.as<unsigned>();
-  unsigned* ctr = hist + kPasses * 256;
+  unsigned* ctr = hist + kHistWords;
   unsigned* desc = ctr + 32;
-  if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  if (bits == 9) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8, 9>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
+  else if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, hblocks, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   {
     const uint64_t* ka = t.key_hi.as<uint64_t>();
     const int* va = nullptr;  // first pass: the value is the index
-    for (int p = 0; p < kPasses; ++p) {
-      uint64_t* kb = (p & 1) ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
-      int* vb = (p & 1) ? t.perm.as<int>() : t.tmp_v2.as<int>();
-      GS_TRY_INT(onesweep(ipt, rs_nt, ntiles, st, ka, va, kb, vb, n, 8 * p, hist + p * 256,
-               desc + (size_t)p * ntiles * 256, ctr + p));
+    for (int p = 0; p < npass; ++p) {
+      // ping-pong so that the last pass lands in (skey_hi, perm)
+      const bool to_final = ((npass - 1 - p) & 1) == 0;
+      uint64_t* kb = to_final ? t.skey_hi.as<uint64_t>() : t.tmp_k.as<uint64_t>();
+      int* vb = to_final ? t.perm.as<int>() : t.tmp_v2.as<int>();
+      GS_TRY_INT(onesweep(ipt, rs_nt, ntiles, st, ka, va, kb, vb, n, bits * p, hist + p * dig,
+               desc + (size_t)p * ntiles * dig, ctr + p, bits));
       ka = kb;
       va = vb;
     }
@@ -1862,7 +1889,7 @@ int tree_build(const Device& dev, int prec, const KernelConsts& kc, const void* 
   kt_mark(3, st);
   kt_mark(4, st);
   // 4. topology
-  GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), desc + (size_t)kPasses * ntiles * 256,
+  GS_TRY_INT(scan_ints(t.lcp.as<int>(), n, t.first.as<int>(), desc + (size_t)npass * ntiles * dig,
                        ctr + kScanTicket, st));
   // The node count m = first[n] stays on the device: node arrays are sized
   // for 4n + 64 nodes (m ~ 1.5n for volumes and surfaces) and every kernel
@@ -1933,11 +1960,11 @@ int morton_order(const Device& dev, int prec, const KernelConsts& kc, const void
     GS_CUDA_OK(pdl_launch(k_keys<double>, nb, kNT, 0, st, (const double4*)rec, n, t.root.as<double>(), t.key_hi.as<uint64_t>(), t.key_lo.as<uint64_t>(), nullptr, t.klo_flag.as<unsigned>()));
   const int ipt = n >= (1 << 19) ? 8 : 4;
   const int ntiles = nblocks(n, kRsNT * ipt);
-  const size_t words = (size_t)8 * 256 + 32 + (size_t)8 * ntiles * 256;
+  const size_t words = (size_t)kHistWords + 32 + (size_t)8 * ntiles * 256;
   GS_TRY_INT(t.hist.ensure(sizeof(unsigned) * words));
   GS_CUDA_OK(cudaMemsetAsync(t.hist.ptr, 0, sizeof(unsigned) * words, st));
   unsigned* hist = t.hist.as<unsigned>();
-  unsigned* ctr = hist + 8 * 256;
+  unsigned* ctr = hist + kHistWords;
   unsigned* desc = ctr + 32;
   if (ipt == 8) GS_CUDA_OK(pdl_launch(k_rs_hist_all<8>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
   else GS_CUDA_OK(pdl_launch(k_rs_hist_all<4>, ntiles, kRsNT, 0, st, t.key_hi.as<uint64_t>(), n, hist));
