@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kNT) k_keys_lo_leaf(const V4<R>* squ, const in
 
 // ------------------------------------------------------------ radix sort ---
 // Stable LSD radix sort of (u64 key, i32 value), 8-bit digits, one-sweep
-// passes (below): stable within-tile ranking with warp match/popc.
+// passes (below): stable within-tile ranking with warp ballots/popc.
 constexpr int kRsNT = 256;  // threads per tile; keys per thread (IPT) is a template parameter
 constexpr int kHistWords = 7 * 512;  // digit histograms of every pass (8 x 256 or 7 x 512)
 
@@ -224,7 +224,7 @@ constexpr int kHistWords = 7 * 512;  // digit histograms of every pass (8 x 256 
 // Digit histograms are independent of the key order, so ONE kernel counts every
 // pass's digits up front (k0: p0 passes, then k1: p1 passes); each pass is then
 // ONE kernel: a tile takes its id from an atomic counter (so every earlier tile
-// has started), ranks its keys with warp match_any, publishes its per-digit
+// has started), ranks its keys with warp ballots, publishes its per-digit
 // count, and looks back over earlier tiles' published counts / inclusive
 // prefixes (decoupled look-back, one 32-bit status word per tile and digit:
 // flag << 30 | count) for its global offsets, then scatters. 1 launch per pass
@@ -250,6 +250,23 @@ __global__ void __launch_bounds__(kRsNT) k_rs_hist_all(const uint64_t* key, int6
   __syncthreads();
   for (int t = threadIdx.x; t < NP * DIG; t += kRsNT)
     if (hs[t]) atomicAdd(&hist[t], hs[t]);
+}
+
+// The lanes of the warp holding the same BITS-bit digit as this one (0 for
+// !ok lanes, which are nobody's peers): one ballot per digit bit -- a lane's
+// peers agree with it on every bit. Replaces MATCH.ANY, whose cost grows with
+// the number of distinct values among the lanes (a third of a one-sweep
+// pass's time at 1M with ~32 distinct digits per warp).
+template <int BITS>
+__device__ __forceinline__ unsigned peer_mask(unsigned d, bool ok) {
+  unsigned pm = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    pm &= bit ? bal : ~bal;
+  }
+  return ok ? pm : 0u;
 }
 
 // NT threads x IPT keys per tile; the digit-parallel parts (scans, look-back)
@@ -304,20 +321,24 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 2 : 4)) k_rs
     key[r] = ok ? kin[i] : 0ull;
     val[r] = ok ? (vin ? vin[i] : (int)i) : 0;  // first pass: values are the indices
   }
-  // per key: the lanes with the same digit (match.any),
-  // the group's leader reserves cnt slots of the warp's digit counter with one
-  // shared atomic (issued back to back for the kRsIPT keys: same-address
-  // atomics of one warp stay in program order), lanes rank by lane order
+  // per key: the lanes with the same digit (peer_mask); the group's leader
+  // reserves cnt slots of the warp's digit counter with one shared atomic
+  // (issued back to back for the kRsIPT keys: same-address atomics of one
+  // warp stay in program order), lanes rank by lane order
   unsigned peers[kRsIPT], old[kRsIPT];
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
     const bool ok = seg + r * 32 + lane < n;
     const unsigned d = (unsigned)(key[r] >> shift) & kMask;
-    // (invalid lanes -- tail tile only -- match among themselves on digit DIG)
-    const unsigned pm = __match_any_sync(0xffffffffu, ok ? d : (unsigned)DIG);
-    peers[r] = ok ? pm : 0u;
+    // (invalid lanes -- tail tile only -- are nobody's peers)
+    peers[r] = peer_mask<BITS>(d, ok);
+  }
+#pragma unroll
+  for (int r = 0; r < kRsIPT; ++r) {
+    const unsigned pm = peers[r];
     old[r] = 0;
-    if (ok && lane == __ffs(pm) - 1) old[r] = atomicAdd(&wh[warp][d], (unsigned)__popc(pm));
+    if (pm && lane == __ffs(pm) - 1)
+      old[r] = atomicAdd(&wh[warp][(unsigned)(key[r] >> shift) & kMask], (unsigned)__popc(pm));
   }
 #pragma unroll
   for (int r = 0; r < kRsIPT; ++r) {
@@ -464,7 +485,8 @@ int onesweep(int ipt, int nt, int ntiles, cudaStream_t st, const uint64_t* ki, c
 //    4's puts 77 % of the points in such runs): a segmented LSD radix sort of
 //    key_lo, 5 passes of 8 bits over 2048-point chunks spread across the
 //    grid: per-chunk digit counts, per-run offsets (run-local, digit-major),
-//    stable scatter (warp match.any ranking as in k_rs_onesweep) -- each pass
+//    stable scatter (warp match.any ranking: run keys share most digits, few
+//    distinct values per warp) -- each pass
 //    three grid.sync()s apart.
 // Two launches whatever the data, and no no-op passes when there is no tie.
 namespace cg = cooperative_groups;
