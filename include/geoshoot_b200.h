@@ -159,6 +159,16 @@ int gs_abi_version(void);
  * windows 0 = automatic node windows, K = K windows (<= 64); -1 restores the
  * environment's choice. Every choice gives the reference's interaction sets. */
 gs_status gs_set_bh_walk(int32_t kernel, int32_t windows);
+/* Exact FP32 all-pairs formulation, process-wide (GS_EXACT_PAIRS sets the
+ * default): 0 = by size (symmetric above 200k points, unsharded), 1 = gather
+ * (each ordered pair per target, k_rhs_f32x2), 2 = symmetric whenever it
+ * applies (each unordered pair once, fed to both ends, as the reference's
+ * i < j sweep, kernel_exact.cpp:29-61); -1 restores the environment's choice. */
+gs_status gs_set_exact_pairs(int32_t mode);
+/* The formulation an unsharded exact RHS of n points takes under the current
+ * choice: *tiles = T (symmetric, T tiles -> T partial slots per target) or 0
+ * (gather). */
+gs_status gs_exact_pairs_plan(int32_t precision, int64_t n, int32_t* tiles);
 /* validate_config, core.cpp:5-17: every violated bound in *mask. */
 gs_status gs_validate_config(const gs_config* cfg, uint32_t* mask);
 

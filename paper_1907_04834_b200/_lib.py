@@ -126,6 +126,8 @@ SIGNATURES = [
     ("gs_bh_point_hessian_products", _st, [_vp, _i64, _d, _d, _d, _d, _d, _d, C.c_double,
                                            C.c_double, _d, _d, _d, _d, C.POINTER(gs_stats)]),
     ("gs_set_bh_walk", _st, [C.c_int32, C.c_int32]),
+    ("gs_set_exact_pairs", _st, [C.c_int32]),
+    ("gs_exact_pairs_plan", _st, [C.c_int32, C.c_int64, C.POINTER(C.c_int32)]),
     ("gs_create_multi", _vp, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int)]),
     ("gs_ctx_device_count", C.c_int32, [_vp]),
     ("gs_ctx_peer_stores", C.c_int32, [_vp]),

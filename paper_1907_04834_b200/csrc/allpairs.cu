@@ -251,6 +251,211 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
   }
 }
 
+// ---- symmetric exact FP32 RHS: every unordered pair evaluated once ----------
+// The reference sweeps i < j and scatters each pair to both ends
+// (kernel_exact.cpp:29-61); this kernel does the same at tile granularity.
+// The n points form T tiles of NT*TPT; CTA (I, k) evaluates the unordered
+// tile pair {I, J = (I + k) mod T}, k = 0 .. floor(T/2) (for even T the
+// k = T/2 pairs belong to I < T/2 only), so every unordered tile pair is
+// taken exactly once. Threads own TPT targets of tile I in registers (packed
+// pairs, as k_rhs_f32x2) and stream the sources of tile J through shared
+// memory; g, c = g p_i.p_j and d_ij of a pair are computed once and feed
+// BOTH ends:
+//   i side (registers):  A_i += g p_j,  B_i += c d_ij
+//   j side (shared):     A_j += g p_i,  B_j -= c d_ij
+// Per two unordered pairs (a packed target pair x one source): 22 packed FP32
+// + 2 MUFU issue slots = 6 per ordered pair (k_rhs_f32x2: 9).
+// The j side needs no atomics: at step s of a 32-source batch lane l takes
+// source (l + s) mod 32, so the 32 lanes of a warp always update 32 distinct
+// sources (each lane adds its TPT-target partial, folded over the packed
+// halves); each warp has its own copy of the j accumulators, summed in warp
+// order after the sub-tile.
+// Partials: target t of tile X receives exactly T partials, one per tile Y
+// (slot Y): the i side of the pair (X, Y), the j side of the pair (Y, X), or,
+// for Y = X, the diagonal pair evaluated gather-style (ordered pairs, self
+// included: the reference's explicit diagonal term). The epilogue folds the
+// T slots in fixed order, so results are deterministic (bitwise repeatable).
+#ifndef GS_SYM_UNR
+#define GS_SYM_UNR 4
+#endif
+template <int TPT, int NT, int MINB, int SB, int SYM_UNR = GS_SYM_UNR>
+__global__ void __launch_bounds__(NT, MINB)
+    k_rhs_sym_f32x2(const float4* __restrict__ rec, int n, int T, float kap, float kc0x,
+                    float kc0y, float kc0z, float4* __restrict__ part) {
+  constexpr int TP = TPT / 2, TILE = NT * TPT, NW = NT / 32;
+  static_assert(TILE % SB == 0 && SB % 32 == 0 && TPT % 2 == 0, "tile shape");
+  __shared__ float4 sq[SB];
+  __shared__ float4 sp[SB];
+  __shared__ float2 sj[NW][3][SB];
+  const int I = blockIdx.x, k = blockIdx.y;
+  if (2 * k == T && I >= k) return;  // even T: the pair {I, I + T/2} once
+  const int J = I + k < T ? I + k : I + k - T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
+  f2 ax[TP], ay[TP], az[TP], bx[TP], by[TP], bz[TP];
+  const int tb = I * TILE + threadIdx.x;
+#pragma unroll
+  for (int kk = 0; kk < TP; ++kk) {
+    float4 q[2], p[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * kk + h) * NT;
+      q[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      p[h] = q[h];
+      if (t < n) {
+        q[h] = rec[2 * t];
+        p[h] = rec[2 * t + 1];
+      }
+      q[h] = make_float4(fmaf(kap, q[h].x, -kc0x), fmaf(kap, q[h].y, -kc0y), fmaf(kap, q[h].z, -kc0z), 0.f);
+    }
+    qx[kk] = pk2(q[0].x, q[1].x); qy[kk] = pk2(q[0].y, q[1].y); qz[kk] = pk2(q[0].z, q[1].z);
+    px[kk] = pk2(p[0].x, p[1].x); py[kk] = pk2(p[0].y, p[1].y); pz[kk] = pk2(p[0].z, p[1].z);
+    ax[kk] = ay[kk] = az[kk] = bx[kk] = by[kk] = bz[kk] = pk2(0.f, 0.f);
+  }
+  const int jbase = J * TILE;
+  for (int st = 0; st < TILE; st += SB) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < n) {
+        q = rec[2 * j];
+        p = rec[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q;  // zero records contribute exactly 0 (p = 0)
+      sp[u] = p;
+    }
+    if (k != 0) {
+      for (int u = lane; u < SB; u += 32) {
+        sj[warp][0][u] = make_float2(0.f, 0.f);
+        sj[warp][1][u] = make_float2(0.f, 0.f);
+        sj[warp][2][u] = make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    if (k == 0) {
+      // diagonal tile pair: gather over the tile's own points (ordered pairs)
+#pragma unroll 4
+      for (int u = 0; u < SB; ++u) {
+        const float4 a = sq[u];
+        const float4 b = sp[u];
+        const f2 axx = bc2(a.x), ayy = bc2(a.y), azz = bc2(a.z);
+        const f2 bxx = bc2(b.x), byy = bc2(b.y), bzz = bc2(b.z);
+        f2 dx[TP], dy[TP], dz[TP], g[TP];
+#pragma unroll
+        for (int kk = 0; kk < TP; ++kk) {
+          dx[kk] = sub2(qx[kk], axx);
+          dy[kk] = sub2(qy[kk], ayy);
+          dz[kk] = sub2(qz[kk], azz);
+          f2 r2 = mul2(dx[kk], dx[kk]);
+          r2 = fma2(dy[kk], dy[kk], r2);
+          r2 = fma2(dz[kk], dz[kk], r2);
+          g[kk] = nex2x2(r2);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TP; ++kk) {
+          f2 pp = mul2(px[kk], bxx);
+          pp = fma2(py[kk], byy, pp);
+          pp = fma2(pz[kk], bzz, pp);
+          const f2 c = mul2(pp, g[kk]);
+          ax[kk] = fma2(g[kk], bxx, ax[kk]);
+          ay[kk] = fma2(g[kk], byy, ay[kk]);
+          az[kk] = fma2(g[kk], bzz, az[kk]);
+          bx[kk] = fma2(c, dx[kk], bx[kk]);
+          by[kk] = fma2(c, dy[kk], by[kk]);
+          bz[kk] = fma2(c, dz[kk], bz[kk]);
+        }
+      }
+      continue;
+    }
+    float2* sj0 = sj[warp][0];
+    float2* sj1 = sj[warp][1];
+    float2* sj2 = sj[warp][2];
+    for (int b0 = 0; b0 < SB; b0 += 32) {
+#pragma unroll SYM_UNR
+      for (int s = 0; s < 32; ++s) {
+        const int u = b0 + ((lane + s) & 31);
+        const float4 a = sq[u];
+        const float4 b = sp[u];
+        const f2 axx = bc2(a.x), ayy = bc2(a.y), azz = bc2(a.z);
+        const f2 bxx = bc2(b.x), byy = bc2(b.y), bzz = bc2(b.z);
+        f2 dx[TP], dy[TP], dz[TP], g[TP];
+#pragma unroll
+        for (int kk = 0; kk < TP; ++kk) {
+          dx[kk] = sub2(qx[kk], axx);
+          dy[kk] = sub2(qy[kk], ayy);
+          dz[kk] = sub2(qz[kk], azz);
+          f2 r2 = mul2(dx[kk], dx[kk]);
+          r2 = fma2(dy[kk], dy[kk], r2);
+          r2 = fma2(dz[kk], dz[kk], r2);
+          g[kk] = nex2x2(r2);
+        }
+        f2 jax, jay, jaz, jbx, jby, jbz;
+#pragma unroll
+        for (int kk = 0; kk < TP; ++kk) {
+          f2 pp = mul2(px[kk], bxx);
+          pp = fma2(py[kk], byy, pp);
+          pp = fma2(pz[kk], bzz, pp);
+          const f2 c = mul2(pp, g[kk]);
+          ax[kk] = fma2(g[kk], bxx, ax[kk]);
+          ay[kk] = fma2(g[kk], byy, ay[kk]);
+          az[kk] = fma2(g[kk], bzz, az[kk]);
+          bx[kk] = fma2(c, dx[kk], bx[kk]);
+          by[kk] = fma2(c, dy[kk], by[kk]);
+          bz[kk] = fma2(c, dz[kk], bz[kk]);
+          if (kk == 0) {
+            jax = mul2(g[kk], px[kk]); jay = mul2(g[kk], py[kk]); jaz = mul2(g[kk], pz[kk]);
+            jbx = mul2(c, dx[kk]); jby = mul2(c, dy[kk]); jbz = mul2(c, dz[kk]);
+          } else {
+            jax = fma2(g[kk], px[kk], jax); jay = fma2(g[kk], py[kk], jay);
+            jaz = fma2(g[kk], pz[kk], jaz);
+            jbx = fma2(c, dx[kk], jbx); jby = fma2(c, dy[kk], jby); jbz = fma2(c, dz[kk], jbz);
+          }
+        }
+        float l0, h0, l1, h1;
+        float2 v0 = sj0[u], v1 = sj1[u], v2 = sj2[u];
+        up2(jax, l0, h0); up2(jay, l1, h1); v0.x += l0 + h0; v0.y += l1 + h1;
+        up2(jaz, l0, h0); up2(jbx, l1, h1); v1.x += l0 + h0; v1.y += l1 + h1;
+        up2(jby, l0, h0); up2(jbz, l1, h1); v2.x += l0 + h0; v2.y += l1 + h1;
+        sj0[u] = v0; sj1[u] = v1; sj2[u] = v2;
+      }
+    }
+    __syncthreads();
+    // j side of this sub-tile's sources: the warp copies in warp order, slot I
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      if (j < n) {
+        float2 s0 = sj[0][0][u], s1 = sj[0][1][u], s2 = sj[0][2][u];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const float2 t0 = sj[w][0][u], t1 = sj[w][1][u], t2 = sj[w][2][u];
+          s0.x += t0.x; s0.y += t0.y; s1.x += t1.x; s1.y += t1.y; s2.x += t2.x; s2.y += t2.y;
+        }
+        float4* o = part + 2 * ((size_t)I * n + j);
+        o[0] = make_float4(s0.x, s0.y, s1.x, 0.f);
+        o[1] = make_float4(-s1.y, -s2.x, -s2.y, 0.f);
+      }
+    }
+  }
+  // i side: slot J (the diagonal pair: J = I)
+#pragma unroll
+  for (int kk = 0; kk < TP; ++kk) {
+    float a0[2][3], b0[2][3];
+    up2(ax[kk], a0[0][0], a0[1][0]); up2(ay[kk], a0[0][1], a0[1][1]); up2(az[kk], a0[0][2], a0[1][2]);
+    up2(bx[kk], b0[0][0], b0[1][0]); up2(by[kk], b0[0][1], b0[1][1]); up2(bz[kk], b0[0][2], b0[1][2]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * kk + h) * NT;
+      if (t < n) {
+        float4* o = part + 2 * ((size_t)J * n + t);
+        o[0] = make_float4(a0[h][0], a0[h][1], a0[h][2], 0.f);
+        o[1] = make_float4(b0[h][0], b0[h][1], b0[h][2], 0.f);
+      }
+    }
+  }
+}
+
 // ---- exact RHS in Morton order with the FP32 underflow cutoff -----------------
 // Same packed arithmetic as k_rhs_f32x2, but targets and sources are the
 // points in Morton (leaf) order (t.srec: interaction coordinates already
@@ -1091,6 +1296,76 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     default: k_rhs_f64<1, kNT><<<pl.grid, kNT, 0, st>>>((const double4*)rec, n, tgt_begin, n_tgt, pl.chunk, kc.inv_two_s, (double4*)part); break;
   }
   return pl.S;
+}
+
+// ---- symmetric exact FP32 RHS (k_rhs_sym_f32x2) -----------------------------
+// gs_set_exact_pairs: 0 = by size (symmetric for large unsharded problems),
+// 1 = gather (k_rhs_f32x2) always, 2 = symmetric whenever it applies.
+static int g_exact_pairs = -1;
+void set_exact_pairs(int mode) { g_exact_pairs = mode; }
+
+static int exact_pairs_mode() {
+  if (g_exact_pairs >= 0) return g_exact_pairs;
+  static int m = [] {
+    const char* e = std::getenv("GS_EXACT_PAIRS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
+#ifndef GS_SYM_VARIANT
+#define GS_SYM_VARIANT 5
+#endif
+struct SymShape {
+  int tpt, nt;
+};
+static const SymShape kSym[] = {{12, 128}, {12, 256}, {8, 128}, {8, 384}, {12, 256}, {12, 256}};
+constexpr int kNumSym = sizeof(kSym) / sizeof(kSym[0]);
+
+static int sym_variant() {
+  static int v = [] {
+    const char* e = std::getenv("GS_SYM_VARIANT");
+    const int x = e ? std::atoi(e) : GS_SYM_VARIANT;
+    return (x >= 0 && x < kNumSym) ? x : 0;
+  }();
+  return v;
+}
+
+int sym_tiles(int n) {
+  const SymShape s = kSym[sym_variant()];
+  return (int)(((long)n + (long)s.tpt * s.nt - 1) / ((long)s.tpt * s.nt));
+}
+
+bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
+  if (prec != kF32 || tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
+  const int mode = exact_pairs_mode();
+  if (mode == 1) return false;
+  const long T = sym_tiles(n);
+  // partial buffer: T slots x n targets x 32 B
+  if ((double)T * n * 32.0 > 24e9) return false;
+  if (mode == 2) return true;
+  // by size: enough tile pairs for many waves (T(T+1)/2 CTAs)
+  return n >= 200000;
+}
+
+size_t sym_part_bytes(int n) { return (size_t)sym_tiles(n) * (size_t)n * 2 * sizeof(float4); }
+
+int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st) {
+  const int T = sym_tiles(n);
+  const dim3 grid((unsigned)T, (unsigned)(T / 2 + 1), 1);
+  const float kap = (float)kc.kappa, a = (float)(kc.kappa * kc.c0[0]),
+              b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
+  const float4* r = (const float4*)rec;
+  float4* o = (float4*)part;
+  switch (sym_variant()) {
+    case 1: k_rhs_sym_f32x2<12, 256, 1, 128><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+    case 2: k_rhs_sym_f32x2<8, 128, 3, 256><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+    case 3: k_rhs_sym_f32x2<8, 384, 1, 64><<<grid, 384, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+    case 4: k_rhs_sym_f32x2<12, 256, 1, 128, 2><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+    case 5: k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+    default: k_rhs_sym_f32x2<12, 128, 2, 256><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o); break;
+  }
+  return T;
 }
 
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,

@@ -149,6 +149,12 @@ gs_status gs_set_bh_walk(int32_t kernel, int32_t windows) {
   return GS_OK;
 }
 
+gs_status gs_set_exact_pairs(int32_t mode) {
+  if (mode < -1 || mode > 2) return GS_INVALID_ARGUMENT;
+  set_exact_pairs(mode);
+  return GS_OK;
+}
+
 gs_status gs_set_literal_mean_dot(gs_ctx* c, int32_t enable) {
   if (!c) return GS_INVALID_ARGUMENT;
   c->lmd = enable ? 1 : 0;
@@ -347,10 +353,15 @@ int exact_sorted_stage(const Device& dev, const KernelConsts& kc, const void* re
 int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void* rec, int64_t n,
                 int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
                 int* energy_blocks, int plan_tgt = -1) {
-  GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+  const bool sym = use_sym(prec, (int)n, (int)tb, (int)nt, plan_tgt);
+  if (sym)
+    GS_TRY(part.ensure(sym_part_bytes((int)n)));
+  else
+    GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
   kt_mark(0, st);
-  const int S = rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr, kMaxChunks, st,
-                             plan_tgt);
+  const int S = sym ? rhs_sym_partials(rec, (int)n, kc, part.ptr, st)
+                    : rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr,
+                                   kMaxChunks, st, plan_tgt);
   kt_mark(0, st);
   if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
   GS_CUDA_OK(cudaGetLastError());
@@ -877,6 +888,14 @@ gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
 // ----------------------------------------------------------------------------
 // kernel_exact
 // ----------------------------------------------------------------------------
+gs_status gs_exact_pairs_plan(int32_t precision, int64_t n, int32_t* tiles) {
+  if (!tiles) return bad_arg("null argument");
+  GS_TRY(check_n(n));
+  const int prec = precision == GS_F32 ? kF32 : kF64;
+  *tiles = use_sym(prec, (int)n, 0, (int)n, -1) ? sym_tiles((int)n) : 0;
+  return GS_OK;
+}
+
 gs_status gs_exact_rhs(gs_ctx* c, int32_t precision, int64_t n, const double* q, const double* p,
                        double sigma, double* dHdp, double* dHdq, double* h_out) {
   if (!c || !q || !p) return bad_arg("null argument");

@@ -113,6 +113,13 @@ int rhs_sorted_partials(const Device& dev, const void* srec, const int* perm, in
 int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_begin, int n_tgt,
                  const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st,
                  int plan_tgt = -1);
+// ---- symmetric exact FP32 RHS (allpairs.cu k_rhs_sym_f32x2): each unordered
+// tile pair once, both ends fed; T = sym_tiles(n) partial slots per target.
+void set_exact_pairs(int mode);
+bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt);
+int sym_tiles(int n);
+size_t sym_part_bytes(int n);
+int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st);
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
                   int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
                   int part_cap_chunks, cudaStream_t st, int plan_tgt = -1);

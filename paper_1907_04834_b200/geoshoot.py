@@ -324,6 +324,20 @@ class Geoshoot:
         if st:
             raise ValueError(f"gs_set_bh_walk({kernel}, {windows}): invalid choice")
 
+    def set_exact_pairs(self, mode: int = -1):
+        """Process-wide exact FP32 all-pairs formulation (gs_set_exact_pairs): 0 by size,
+        1 gather (ordered pairs per target), 2 symmetric (unordered pairs once); -1 default."""
+        st = self.lib.gs_set_exact_pairs(int(mode))
+        if st:
+            raise ValueError(f"gs_set_exact_pairs({mode}): invalid choice")
+
+    def exact_pairs_plan(self, n: int, precision=F32) -> int:
+        """Tiles T of the symmetric exact RHS an unsharded n-point problem takes now
+        (0: the gather kernel) -- gs_exact_pairs_plan."""
+        t = C.c_int32()
+        self.check(self.lib.gs_exact_pairs_plan(int(precision), int(n), C.byref(t)))
+        return t.value
+
     def set_literal_mean_dot(self, enable: bool):
         """Tree-level BH calls on this context use the reference's
         GEOSHOOT_BH_LITERAL_MEAN_DOT aggregate dot scale 1/count (bh_kernel.cpp:19-26)."""

@@ -275,3 +275,52 @@ def test_exact_cutoff_matches_reference(gs, port):
     w = port.shoot_forward(q, p, sigma, 4, integrator=1, keep_traj=False)
     assert rel_l2(fq, w["q"]) < F32_TRAJ_TOL and rel_l2(fp, w["p"]) < F32_TRAJ_TOL
     assert e == pytest.approx(w["energy"], rel=1e-5)
+
+
+# ---- symmetric all-pairs (k_rhs_sym_f32x2: each unordered pair once) -----------
+@pytest.fixture
+def pairs(gs):
+    def set_mode(mode):
+        gs.set_exact_pairs(mode)
+    yield set_mode
+    gs.set_exact_pairs(-1)
+
+
+# 3072-point tiles: one tile (diagonal only), 4 tiles (even T: the k = T/2
+# pairs taken once), 5 tiles (odd T), ragged last tiles
+@pytest.mark.parametrize("n", [700, 3072 * 3 + 17, 3072 * 4 + 5])
+def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
+    """Every unordered pair evaluated once and fed to both ends, as the
+    reference's i < j sweep (kernel_exact.cpp:29-61): FP32 RHS to 1e-5 of the
+    reference on the same FP32 inputs, to rounding of the gather kernel, and
+    bitwise repeatable (the T partial slots are folded in fixed order)."""
+    q, p = f32(uniform(n, 10.0, seed=n)), f32(sym_uniform(n, 1.0, seed=n + 1))
+    pairs(2)
+    h, dp, dq = gs.hamiltonian_with_gradients(q, p, 1.1, precision=F32)
+    h2, dp2, dq2 = gs.hamiltonian_with_gradients(q, p, 1.1, precision=F32)
+    assert np.array_equal(dp, dp2) and np.array_equal(dq, dq2) and h == h2
+    wp, wq, wh = ref.exact_rhs(q, p, 1.1)
+    assert rel_l2(dp, wp) < F32_RHS_TOL
+    assert rel_l2(dq, wq) < F32_RHS_TOL
+    assert abs(h - wh) <= F32_RHS_TOL * abs(wh)
+    pairs(1)
+    _, gp, gq = gs.hamiltonian_with_gradients(q, p, 1.1, precision=F32)
+    assert rel_l2(dp, gp) < 2e-6 and rel_l2(dq, gq) < 2e-6
+
+
+def test_symmetric_flow_matches_reference(gs, port, pairs):
+    """RK4 flow through the symmetric kernel against the port's RK4 over the
+    reference RHS (FP32 trajectory tolerance)."""
+    n, sigma = 3072 * 2 + 100, 0.05
+    q, p = f32(uniform(n, 1.0, 541)), f32(sym_uniform(n, 1e-3, 542))
+    pairs(2)
+    cfg = ShootingConfig(sigma=sigma, timesteps=4, backend=EXACT, integrator=RK4, precision=F32)
+    fq, fp, e, _ = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    w = port.shoot_forward(q, p, sigma, 4, integrator=1, keep_traj=False)
+    assert rel_l2(fq, w["q"]) < F32_TRAJ_TOL and rel_l2(fp, w["p"]) < F32_TRAJ_TOL
+    assert e == pytest.approx(w["energy"], rel=1e-5)
+
+
+def test_exact_pairs_choice_is_validated(gs):
+    with pytest.raises(ValueError):
+        gs.set_exact_pairs(3)
