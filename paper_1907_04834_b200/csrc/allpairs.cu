@@ -1313,26 +1313,29 @@ static int exact_pairs_mode() {
   return m;
 }
 
-#ifndef GS_SYM_VARIANT
-#define GS_SYM_VARIANT 5
-#endif
+// Tile shapes: 0 = 12 targets x 256 threads (3072-point tiles, one CTA per
+// SM; the default from 150k points), 1 = 12 x 128 (1536-point tiles, two CTAs
+// per SM: enough tile pairs for smaller problems). Measured alternatives
+// (DESIGN.md §2): 8 x 128 / 8 x 384 / 10 x 256 / 14 x 128 targets, 64- or
+// 256-source sub-tiles, source-step unroll 2 / 4, and the j side accumulated
+// after the whole i side were all equal or slower (1.65-1.79 s per RK4 step
+// at 1M against 1.657 s).
 struct SymShape {
   int tpt, nt;
 };
-static const SymShape kSym[] = {{12, 128}, {12, 256}, {8, 128}, {8, 384}, {12, 256}, {12, 256}};
-constexpr int kNumSym = sizeof(kSym) / sizeof(kSym[0]);
+static const SymShape kSym[] = {{12, 256}, {12, 128}};
 
-static int sym_variant() {
-  static int v = [] {
+static int sym_variant(int n) {
+  static int forced = [] {
     const char* e = std::getenv("GS_SYM_VARIANT");
-    const int x = e ? std::atoi(e) : GS_SYM_VARIANT;
-    return (x >= 0 && x < kNumSym) ? x : 0;
+    return e ? std::atoi(e) : -1;
   }();
-  return v;
+  if (forced == 0 || forced == 1) return forced;
+  return n >= 150000 ? 0 : 1;
 }
 
 int sym_tiles(int n) {
-  const SymShape s = kSym[sym_variant()];
+  const SymShape s = kSym[sym_variant(n)];
   return (int)(((long)n + (long)s.tpt * s.nt - 1) / ((long)s.tpt * s.nt));
 }
 
@@ -1345,7 +1348,7 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
   if ((double)T * n * 32.0 > 24e9) return false;
   if (mode == 2) return true;
   // by size: enough tile pairs for many waves (T(T+1)/2 CTAs)
-  return n >= 200000;
+  return n >= 40000;
 }
 
 size_t sym_part_bytes(int n) { return (size_t)sym_tiles(n) * (size_t)n * 2 * sizeof(float4); }
@@ -1357,14 +1360,10 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
               b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
   const float4* r = (const float4*)rec;
   float4* o = (float4*)part;
-  switch (sym_variant()) {
-    case 1: k_rhs_sym_f32x2<12, 256, 1, 128><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-    case 2: k_rhs_sym_f32x2<8, 128, 3, 256><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-    case 3: k_rhs_sym_f32x2<8, 384, 1, 64><<<grid, 384, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-    case 4: k_rhs_sym_f32x2<12, 256, 1, 128, 2><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-    case 5: k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-    default: k_rhs_sym_f32x2<12, 128, 2, 256><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o); break;
-  }
+  if (sym_variant(n) == 0)
+    k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o);
+  else
+    k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o);
   return T;
 }
 

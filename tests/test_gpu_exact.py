@@ -286,9 +286,9 @@ def pairs(gs):
     gs.set_exact_pairs(-1)
 
 
-# 3072-point tiles: one tile (diagonal only), 4 tiles (even T: the k = T/2
-# pairs taken once), 5 tiles (odd T), ragged last tiles
-@pytest.mark.parametrize("n", [700, 3072 * 3 + 17, 3072 * 4 + 5])
+# 1536-point tiles below 150k points: one tile (diagonal only), 4 tiles (even
+# T: the k = T/2 pairs taken once), 5 tiles (odd T), ragged last tiles
+@pytest.mark.parametrize("n", [700, 1536 * 3 + 17, 1536 * 4 + 5])
 def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
     """Every unordered pair evaluated once and fed to both ends, as the
     reference's i < j sweep (kernel_exact.cpp:29-61): FP32 RHS to 1e-5 of the
@@ -311,7 +311,7 @@ def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
 def test_symmetric_flow_matches_reference(gs, port, pairs):
     """RK4 flow through the symmetric kernel against the port's RK4 over the
     reference RHS (FP32 trajectory tolerance)."""
-    n, sigma = 3072 * 2 + 100, 0.05
+    n, sigma = 1536 * 2 + 100, 0.05
     q, p = f32(uniform(n, 1.0, 541)), f32(sym_uniform(n, 1e-3, 542))
     pairs(2)
     cfg = ShootingConfig(sigma=sigma, timesteps=4, backend=EXACT, integrator=RK4, precision=F32)
