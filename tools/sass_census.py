@@ -20,8 +20,10 @@ OBJ = os.path.join(ROOT, "build", "obj")
 
 KERNELS = {
     "allpairs.o": [
-        "_ZN3gsb11k_rhs_f32x2ILi12ELi128ELi2ELi8EEEvPK6float4iiiiffffPS1_",  # headline >= 500k
-        "_ZN3gsb11k_rhs_f32x2ILi8ELi128ELi3ELi8EEEvPK6float4iiiiffffPS1_",   # < 500k targets
+        "_ZN3gsb15k_rhs_sym_f32x2ILi12ELi256ELi1ELi128ELi8EEEvPK6float4iiffffPS1_",  # headline >= 150k
+        "_ZN3gsb15k_rhs_sym_f32x2ILi12ELi128ELi2ELi256ELi4EEEvPK6float4iiffffPS1_",  # 40k - 150k
+        "_ZN3gsb11k_rhs_f32x2ILi12ELi128ELi2ELi8EEEvPK6float4iiiiffffPS1_",  # gather >= 500k (shards)
+        "_ZN3gsb11k_rhs_f32x2ILi8ELi128ELi3ELi8EEEvPK6float4iiiiffffPS1_",   # gather < 500k targets
         "_ZN3gsb12k_hess_f32x2ILi4ELi128EEEvPK6float4S3_iiiifffffPS1_",      # adjoint
         "_ZN3gsb9k_rhs_f64ILi4ELi128EEEvPK7double4iiiidPS1_",                # FP64 RHS
     ],
@@ -51,7 +53,7 @@ def functions(obj):
     return funcs
 
 
-def census(body):
+def census(body, sym=False):
     whole = Counter(op for _, op, _ in body)
     # loops: BRA to a lower address
     best, best_mufu = None, -1
@@ -62,6 +64,14 @@ def census(body):
                 lo = int(m.group(1), 16)
                 seg = [o for a, o, _ in body if lo <= a <= addr]
                 mufu = sum(1 for o in seg if o.startswith("MUFU"))
+                # symmetric kernels: the smallest loop that evaluates pairs
+                # AND updates the shared j accumulators (the source-step loop)
+                if sym:
+                    if not mufu or "STS.64" not in seg:
+                        continue
+                    if best is None or len(seg) < len(best[2]):
+                        best, best_mufu = (lo, addr, seg), mufu
+                    continue
                 if mufu > best_mufu:
                     best, best_mufu = (lo, addr, seg), mufu
     res = {"instructions": len(body), "whole_function": dict(whole.most_common(40))}
@@ -85,7 +95,7 @@ def main():
             names = [n for n in funcs if any(re.search(p, n) for p in BH_PATTERNS)]
         for n in names:
             if n in funcs:
-                report[n] = census(funcs[n])
+                report[n] = census(funcs[n], sym="sym" in n)
     json.dump(report, sys.stdout, indent=1)
     print()
 
