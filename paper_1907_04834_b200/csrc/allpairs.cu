@@ -721,6 +721,178 @@ __global__ void __launch_bounds__(NT, GS_HESS_MINB) k_hess_f32x2(const float4* _
   }
 }
 
+// Symmetric Hessian-vector products: each unordered tile pair once (the
+// tiling, slots and conflict-free j side of k_rhs_sym_f32x2). For the pair
+// (i, j), with d = x'_i - x'_j and the negated db' = beta_j - beta_i of
+// k_hess_f32x2, s1 = p_j.a_i + p_i.a_j, p_i.p_j and d.db' are symmetric; the
+// j terms follow from the i terms by d -> -d, db' -> -db':
+//   i: Apq += t1 d,  App += g a_j,  Aqq += w z,  Aqp' += m p_j
+//   j: Apq -= t1 d,  App += g a_i,  Aqq -= w z,  Aqp' += m p_i
+// (t1 = g s1, w = g p_i.p_j, z = uu d + db', uu = -c1 d.db', m = g d.db'; Aqp'
+// is stored negated as in k_hess_f32x2). Per unordered pair: 28 packed-pair
+// FP32 ops shared + 2 x 12 accumulations = 52 FP32 + 1 MUFU (gather: 74 + 2).
+template <int TPT, int NT, int MINB, int SB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_hess_sym_f32x2(const float4* __restrict__ rec, const float4* __restrict__ adj, int n,
+                     int T, float kap, float kc0x, float kc0y, float kc0z, float c1,
+                     float4* __restrict__ part) {
+  constexpr int TP = TPT / 2, TILE = NT * TPT, NW = NT / 32;
+  static_assert(TILE % SB == 0 && SB % 32 == 0 && TPT % 2 == 0, "tile shape");
+  __shared__ float4 sq[SB], sp[SB], sa[SB], sb[SB];
+  __shared__ float4 sj[NW][3][SB];
+  const int I = blockIdx.x, k = blockIdx.y;
+  if (2 * k == T && I >= k) return;  // even T: the pair {I, I + T/2} once
+  const int J = I + k < T ? I + k : I + k - T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
+  f2 ix[TP], iy[TP], iz[TP], jx[TP], jy[TP], jz[TP];  // alpha_i, beta_i
+  f2 A[TP][12];
+  const int tb = I * TILE + threadIdx.x;
+#pragma unroll
+  for (int kk = 0; kk < TP; ++kk) {
+    float4 q[2], p[2], al[2], be[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * kk + h) * NT;
+      q[h] = p[h] = al[h] = be[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < n) {
+        q[h] = rec[2 * t]; p[h] = rec[2 * t + 1]; al[h] = adj[2 * t]; be[h] = adj[2 * t + 1];
+      }
+      q[h] = make_float4(fmaf(kap, q[h].x, -kc0x), fmaf(kap, q[h].y, -kc0y), fmaf(kap, q[h].z, -kc0z), 0.f);
+    }
+    qx[kk] = pk2(q[0].x, q[1].x); qy[kk] = pk2(q[0].y, q[1].y); qz[kk] = pk2(q[0].z, q[1].z);
+    px[kk] = pk2(p[0].x, p[1].x); py[kk] = pk2(p[0].y, p[1].y); pz[kk] = pk2(p[0].z, p[1].z);
+    ix[kk] = pk2(al[0].x, al[1].x); iy[kk] = pk2(al[0].y, al[1].y); iz[kk] = pk2(al[0].z, al[1].z);
+    jx[kk] = pk2(be[0].x, be[1].x); jy[kk] = pk2(be[0].y, be[1].y); jz[kk] = pk2(be[0].z, be[1].z);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) A[kk][c] = pk2(0.f, 0.f);
+  }
+  const f2 cc1 = bc2(-c1);
+  const int jbase = J * TILE;
+  for (int st = 0; st < TILE; st += SB) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q, a = q, b = q;
+      if (j < n) {
+        q = rec[2 * j]; p = rec[2 * j + 1]; a = adj[2 * j]; b = adj[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q; sp[u] = p; sa[u] = a; sb[u] = b;  // zero records contribute exactly 0
+    }
+    if (k != 0)
+      for (int u = lane; u < SB; u += 32)
+        sj[warp][0][u] = sj[warp][1][u] = sj[warp][2][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    for (int s = 0; s < SB; ++s) {
+      // diagonal pair: gather over every source (u = s); else lane l takes
+      // source (l + s) mod 32 of the current 32-source batch
+      const int u = k == 0 ? s : (s & ~31) + ((lane + s) & 31);
+      const float4 Q = sq[u], P = sp[u], Al = sa[u], Be = sb[u];
+      const f2 Qx = bc2(Q.x), Qy = bc2(Q.y), Qz = bc2(Q.z);
+      const f2 Px = bc2(P.x), Py = bc2(P.y), Pz = bc2(P.z);
+      const f2 Ax = bc2(Al.x), Ay = bc2(Al.y), Az = bc2(Al.z);
+      const f2 Bx = bc2(Be.x), By = bc2(Be.y), Bz = bc2(Be.z);
+      f2 Jv[12];
+#pragma unroll
+      for (int kk = 0; kk < TP; ++kk) {
+        const f2 dx = sub2(qx[kk], Qx), dy = sub2(qy[kk], Qy), dz = sub2(qz[kk], Qz);
+        f2 r2 = mul2(dx, dx);
+        r2 = fma2(dy, dy, r2);
+        r2 = fma2(dz, dz, r2);
+        const f2 g = nex2x2(r2);
+        const f2 dbx = sub2(Bx, jx[kk]), dby = sub2(By, jy[kk]), dbz = sub2(Bz, jz[kk]);
+        f2 ddb = mul2(dx, dbx);
+        ddb = fma2(dy, dby, ddb);
+        ddb = fma2(dz, dbz, ddb);
+        f2 s1 = mul2(ix[kk], Px);
+        s1 = fma2(iy[kk], Py, s1);
+        s1 = fma2(iz[kk], Pz, s1);
+        s1 = fma2(px[kk], Ax, s1);
+        s1 = fma2(py[kk], Ay, s1);
+        s1 = fma2(pz[kk], Az, s1);
+        f2 pp = mul2(px[kk], Px);
+        pp = fma2(py[kk], Py, pp);
+        pp = fma2(pz[kk], Pz, pp);
+        const f2 t1 = mul2(g, s1);
+        A[kk][0] = fma2(t1, dx, A[kk][0]); A[kk][1] = fma2(t1, dy, A[kk][1]); A[kk][2] = fma2(t1, dz, A[kk][2]);
+        A[kk][3] = fma2(g, Ax, A[kk][3]); A[kk][4] = fma2(g, Ay, A[kk][4]); A[kk][5] = fma2(g, Az, A[kk][5]);
+        const f2 w = mul2(g, pp);
+        const f2 uu = mul2(ddb, cc1);  // cc1 = -c1
+        const f2 zx = fma2(uu, dx, dbx), zy = fma2(uu, dy, dby), zz = fma2(uu, dz, dbz);
+        A[kk][6] = fma2(w, zx, A[kk][6]); A[kk][7] = fma2(w, zy, A[kk][7]); A[kk][8] = fma2(w, zz, A[kk][8]);
+        const f2 m = mul2(g, ddb);
+        A[kk][9] = fma2(m, Px, A[kk][9]); A[kk][10] = fma2(m, Py, A[kk][10]); A[kk][11] = fma2(m, Pz, A[kk][11]);
+        if (k == 0) continue;
+        if (kk == 0) {
+          Jv[0] = mul2(t1, dx); Jv[1] = mul2(t1, dy); Jv[2] = mul2(t1, dz);
+          Jv[3] = mul2(g, ix[kk]); Jv[4] = mul2(g, iy[kk]); Jv[5] = mul2(g, iz[kk]);
+          Jv[6] = mul2(w, zx); Jv[7] = mul2(w, zy); Jv[8] = mul2(w, zz);
+          Jv[9] = mul2(m, px[kk]); Jv[10] = mul2(m, py[kk]); Jv[11] = mul2(m, pz[kk]);
+        } else {
+          Jv[0] = fma2(t1, dx, Jv[0]); Jv[1] = fma2(t1, dy, Jv[1]); Jv[2] = fma2(t1, dz, Jv[2]);
+          Jv[3] = fma2(g, ix[kk], Jv[3]); Jv[4] = fma2(g, iy[kk], Jv[4]); Jv[5] = fma2(g, iz[kk], Jv[5]);
+          Jv[6] = fma2(w, zx, Jv[6]); Jv[7] = fma2(w, zy, Jv[7]); Jv[8] = fma2(w, zz, Jv[8]);
+          Jv[9] = fma2(m, px[kk], Jv[9]); Jv[10] = fma2(m, py[kk], Jv[10]); Jv[11] = fma2(m, pz[kk], Jv[11]);
+        }
+      }
+      if (k == 0) continue;
+      float f[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) {
+        float lo, hi;
+        up2(Jv[c], lo, hi);
+        f[c] = lo + hi;
+      }
+      float4 v0 = sj[warp][0][u], v1 = sj[warp][1][u], v2 = sj[warp][2][u];
+      v0.x += f[0]; v0.y += f[1]; v0.z += f[2]; v0.w += f[3];
+      v1.x += f[4]; v1.y += f[5]; v1.z += f[6]; v1.w += f[7];
+      v2.x += f[8]; v2.y += f[9]; v2.z += f[10]; v2.w += f[11];
+      sj[warp][0][u] = v0; sj[warp][1][u] = v1; sj[warp][2][u] = v2;
+    }
+    if (k == 0) continue;
+    __syncthreads();
+    // j side of this sub-tile's sources, warp copies in warp order, slot I
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      if (j < n) {
+        float4 s0 = sj[0][0][u], s1 = sj[0][1][u], s2 = sj[0][2][u];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const float4 t0 = sj[w][0][u], t1 = sj[w][1][u], t2 = sj[w][2][u];
+          s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
+          s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
+          s2.x += t2.x; s2.y += t2.y; s2.z += t2.z; s2.w += t2.w;
+        }
+        // (Apq, App, Aqq, Aqp') of j = (-J0..2, J3..5, -J6..8, -J9..11)
+        float4* o = part + 4 * ((size_t)I * n + j);
+        o[0] = make_float4(-s0.x, -s0.y, -s0.z, 0.f);
+        o[1] = make_float4(s0.w, s1.x, s1.y, 0.f);
+        o[2] = make_float4(-s1.z, -s1.w, -s2.x, 0.f);
+        o[3] = make_float4(-s2.y, -s2.z, -s2.w, 0.f);
+      }
+    }
+  }
+  // i side: slot J (the diagonal pair: J = I)
+#pragma unroll
+  for (int kk = 0; kk < TP; ++kk) {
+    float v[2][12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) up2(A[kk][c], v[0][c], v[1][c]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * kk + h) * NT;
+      if (t < n) {
+        float4* o = part + 4 * ((size_t)J * n + t);
+        o[0] = make_float4(v[h][0], v[h][1], v[h][2], 0.f);
+        o[1] = make_float4(v[h][3], v[h][4], v[h][5], 0.f);
+        o[2] = make_float4(v[h][6], v[h][7], v[h][8], 0.f);
+        o[3] = make_float4(-v[h][9], -v[h][10], -v[h][11], 0.f);
+      }
+    }
+  }
+}
+
 // FP64: the reference's own expression exp(-|d|^2 * inv_two_s) in unscaled
 // coordinates; libdevice exp (no SFU path exists for FP64).
 template <int TPT, int NT>
@@ -1367,9 +1539,38 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
   return T;
 }
 
+// Symmetric Hessian products (k_hess_sym_f32x2): 768-point tiles (6 targets
+// x 128 threads, two CTAs per SM), the same choice rules as the RHS.
+constexpr int kHessSymTile = 6 * 128;
+static int hess_sym_tiles(int n) { return (n + kHessSymTile - 1) / kHessSymTile; }
+
+static bool use_sym_hess(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
+  if (prec != kF32 || tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
+  const int mode = exact_pairs_mode();
+  if (mode == 1) return false;
+  if ((double)hess_sym_tiles(n) * n * 64.0 > 24e9) return false;
+  return mode == 2 || n >= 40000;
+}
+
+size_t hess_part_bytes(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
+  if (use_sym_hess(prec, n, tgt_begin, n_tgt, plan_tgt))
+    return (size_t)hess_sym_tiles(n) * (size_t)n * 4 * sizeof(float4);
+  return (size_t)kMaxChunks * 4 * vec_bytes(prec) * (size_t)std::max(n_tgt, 1);
+}
+
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
                   int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
                   int part_cap_chunks, cudaStream_t st, int plan_tgt) {
+  if (use_sym_hess(prec, n, tgt_begin, n_tgt, plan_tgt)) {
+    // (the caller sized part with hess_part_bytes)
+    const int T = hess_sym_tiles(n);
+    const float kap = (float)kc.kappa;
+    const float c1 = (float)(1.0 / (kc.kappa * kc.kappa * kc.s));
+    k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(T / 2 + 1)), 128, 0, st>>>(
+        (const float4*)rec, (const float4*)adj, n, T, kap, (float)(kc.kappa * kc.c0[0]),
+        (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), c1, (float4*)part);
+    return T;
+  }
   const int real_tgt = n_tgt;
   if (plan_tgt > 0) n_tgt = plan_tgt;
   if (prec == kF32) {

@@ -976,7 +976,7 @@ gs_status gs_hessian_products(gs_ctx* c, int32_t precision, int64_t n, const dou
   const KernelConsts kc = with_ext(make_consts(sigma, prec == kF32 ? c0 : nullptr), ext);
   GS_TRY(upload_records(c, prec, q, p, n, c->rec_a));
   GS_TRY(upload_records(c, prec, alpha, beta, n, c->rec_b));
-  GS_TRY(c->part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * n));
+  GS_TRY(c->part.ensure(hess_part_bytes(prec, (int)n, 0, (int)n)));
   DBuf* outs[4] = {&c->stage_a, &c->stage_b, &c->stage_c, &c->stage_d};
   for (DBuf* b : outs) GS_TRY(b->ensure(sizeof(double) * 3 * n));
   const int S = hess_partials(c->dev, prec, c->rec_a.ptr, c->rec_b.ptr, (int)n, 0, (int)n, kc,
@@ -1104,7 +1104,7 @@ int backward_step(gs_ctx* c, const gs_config* cfg, int prec, const KernelConsts&
   e.tgt_begin = (int)tb;
   e.adj = adj_in;
   if (cfg->backend == GS_EXACT) {
-    GS_TRY(part.ensure((size_t)kMaxChunks * 4 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
+    GS_TRY(part.ensure(hess_part_bytes(prec, (int)n, (int)tb, (int)nt, plan_tgt)));
     kt_mark(6, st);
     const int S = hess_partials(c->dev, prec, rk, adj_in, (int)n, (int)tb, (int)nt, kc, part.ptr,
                                 kMaxChunks, st, plan_tgt);

@@ -120,6 +120,8 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt);
 int sym_tiles(int n);
 size_t sym_part_bytes(int n);
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st);
+// bytes hess_partials needs in part for this problem (symmetric: T slots x 64 B)
+size_t hess_part_bytes(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt = -1);
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,
                   int tgt_begin, int n_tgt, const KernelConsts& kc, void* part,
                   int part_cap_chunks, cudaStream_t st, int plan_tgt = -1);

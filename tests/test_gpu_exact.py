@@ -324,3 +324,35 @@ def test_symmetric_flow_matches_reference(gs, port, pairs):
 def test_exact_pairs_choice_is_validated(gs):
     with pytest.raises(ValueError):
         gs.set_exact_pairs(3)
+
+
+# 768-point tiles: one tile, 4 tiles (even T), 5 tiles (odd T), ragged
+@pytest.mark.parametrize("n", [300, 768 * 3 + 11, 768 * 4 + 3])
+def test_symmetric_hessian_products_match_reference(gs, ref, pairs, n):
+    """k_hess_sym_f32x2: each unordered pair once, the j terms by symmetry
+    (d -> -d, db -> -db), against the reference's hessian_products
+    (kernel_exact.cpp:84-135) and the gather kernel; bitwise repeatable."""
+    q, p = f32(uniform(n, 6.0, 95)), f32(sym_uniform(n, 1.0, 96))
+    a, b = f32(sym_uniform(n, 1.0, 97)), f32(sym_uniform(n, 1.0, 98))
+    pairs(2)
+    got = gs.hessian_products(q, p, a, b, 1.2, precision=F32)
+    again = gs.hessian_products(q, p, a, b, 1.2, precision=F32)
+    want = ref.hessian_products(q, p, a, b, 1.2)
+    pairs(1)
+    gather = gs.hessian_products(q, p, a, b, 1.2, precision=F32)
+    for g, g2, w, h in zip(got, again, want, gather):
+        assert np.array_equal(g, g2)
+        assert rel_l2(g, w) < 2e-5
+        assert rel_l2(g, h) < 4e-6
+
+
+def test_symmetric_evaluate_matches_reference(gs, ref, pairs):
+    """evaluate() with the symmetric forward and adjoint kernels (FP32)."""
+    n = 768 * 3 + 40
+    q, p, t = f32(uniform(n, 9.0, 471)), f32(sym_uniform(n, 0.3, 472)), f32(uniform(n, 9.0, 473))
+    pairs(2)
+    cfg = ShootingConfig(sigma=1.2, lambda_=0.7, timesteps=6, precision=F32)
+    ev = gs.evaluate(q, p, t, cfg)
+    rep, g, _, _ = ref.evaluate(q, p, t, 1.2, 0.7, 6, 0)
+    assert ev.report["total"] == pytest.approx(rep[2], rel=1e-4)
+    assert rel_l2(ev.gradient, g) <= 1e-3

@@ -69,5 +69,31 @@ def main():
         gs.set_exact_pairs(-1)
 
 
+
+
+def hess_main():
+    """python tools/check_sym.py hess N: exact evaluate() (forward + adjoint), gather vs symmetric."""
+    import numpy as np
+    from paper_1907_04834_b200 import EXACT, F32, Geoshoot, ShootingConfig
+    from tests.util import smooth_momenta, tube
+    n = int(sys.argv[2])
+    gs = Geoshoot(0)
+    q = tube(n, seed=5)
+    p = smooth_momenta(q, 1.0, 6)
+    t = q + 0.5
+    cfg = ShootingConfig(sigma=5.0, lambda_=100.0, timesteps=20, backend=EXACT, precision=F32)
+    for mode in (1, 2, 1, 2):
+        gs.set_exact_pairs(mode)
+        gs.evaluate(q, p, t, cfg)
+        t0 = time.perf_counter()
+        ev = gs.evaluate(q, p, t, cfg)
+        dt = time.perf_counter() - t0
+        print(json.dumps({"mode": mode, "n": n, "evaluate_s": dt, "total": ev.report["total"],
+                          "grad_norm": float(np.linalg.norm(ev.gradient))}), flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[1] == "hess":
+        hess_main()
+    else:
+        main()
