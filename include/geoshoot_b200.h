@@ -166,8 +166,8 @@ gs_status gs_set_bh_walk(int32_t kernel, int32_t windows);
  * i < j sweep, kernel_exact.cpp:29-61); -1 restores the environment's choice. */
 gs_status gs_set_exact_pairs(int32_t mode);
 /* The formulation an unsharded exact RHS of n points takes under the current
- * choice: *tiles = T (symmetric, T tiles -> T partial slots per target) or 0
- * (gather). */
+ * choice: *tiles = T (symmetric over T tiles: 3072 / 1536 points in FP32,
+ * 1024 in FP64) or 0 (gather). */
 gs_status gs_exact_pairs_plan(int32_t precision, int64_t n, int32_t* tiles);
 /* validate_config, core.cpp:5-17: every violated bound in *mask. */
 gs_status gs_validate_config(const gs_config* cfg, uint32_t* mask);

@@ -961,6 +961,143 @@ __global__ void __launch_bounds__(NT) k_rhs_f64(const double4* __restrict__ rec,
   }
 }
 
+// Symmetric exact FP64 RHS: the tiling and conflict-free j side of
+// k_rhs_sym_f32x2 in double precision with the reference's own expression
+// exp(-|d|^2 inv_two_s) (gs_exp.cuh). FP64 partials are 64 B, so instead of a
+// slot per tile the tile pairs are launched in groups of diagonals [k0, k1):
+// CTA (I, k) writes the i side of {I, I+k} to slot 2(k-k0) of tile I and the j
+// side to slot 2(k-k0)+1 of tile J; the diagonal (k = 0) and the skipped
+// even-T duplicates write zeros to the slot they would not otherwise fill, so
+// every target has exactly 2(k1-k0) slots per group, folded (k_fold_group)
+// into a running sum in fixed order: deterministic, with a 2 x Kg x n x 64 B
+// buffer whatever N.
+template <int TPT, int NT, int MINB, int SB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_rhs_sym_f64(const double4* __restrict__ rec, int n, int T, int k0, double inv_two_s,
+                  double4* __restrict__ part) {
+  constexpr int TILE = NT * TPT, NW = NT / 32;
+  static_assert(TILE % SB == 0 && SB % 32 == 0, "tile shape");
+  __shared__ double4 sq[SB];
+  __shared__ double4 sp[SB];
+  __shared__ double2 sj[NW][3][SB];
+  __shared__ double stab[64];
+  if (threadIdx.x < 64) stab[threadIdx.x] = kExp2Tab64[threadIdx.x];
+  const int I = blockIdx.x, k = k0 + blockIdx.y;
+  const int J = I + k < T ? I + k : I + k - T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tb = I * TILE + threadIdx.x;
+  const size_t si = (size_t)(2 * (k - k0)) * n, sjs = si + n;  // slot offsets
+  if (2 * k == T && I >= k) {
+    // even T: the pair {I, I + T/2} belongs to CTA (I - T/2, T/2); fill the
+    // slots this CTA would have written with zeros
+    const double4 z = make_double4(0, 0, 0, 0);
+    for (int u = threadIdx.x; u < TILE; u += NT) {
+      const int t = I * TILE + u, j = J * TILE + u;
+      if (t < n) { st4(part + 2 * (si + t), z); st4(part + 2 * (si + t) + 1, z); }
+      if (j < n) { st4(part + 2 * (sjs + j), z); st4(part + 2 * (sjs + j) + 1, z); }
+    }
+    return;
+  }
+  double qx[TPT], qy[TPT], qz[TPT], px[TPT], py[TPT], pz[TPT];
+  double ax[TPT], ay[TPT], az[TPT], bx[TPT], by[TPT], bz[TPT];
+#pragma unroll
+  for (int kk = 0; kk < TPT; ++kk) {
+    const int t = tb + kk * NT;
+    double4 q = make_double4(0, 0, 0, 0), p = q;
+    if (t < n) {
+      q = ld4(rec + 2 * t);
+      p = ld4(rec + 2 * t + 1);
+    }
+    qx[kk] = q.x; qy[kk] = q.y; qz[kk] = q.z;
+    px[kk] = p.x; py[kk] = p.y; pz[kk] = p.z;
+    ax[kk] = ay[kk] = az[kk] = bx[kk] = by[kk] = bz[kk] = 0.0;
+  }
+  const int jbase = J * TILE;
+  for (int st = 0; st < TILE; st += SB) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      double4 q = make_double4(0, 0, 0, 0), p = q;
+      if (j < n) {
+        q = ld4(rec + 2 * j);
+        p = ld4(rec + 2 * j + 1);
+      }
+      sq[u] = q;  // zero records (p = 0) contribute exactly 0
+      sp[u] = p;
+    }
+    if (k != 0)
+      for (int u = lane; u < SB; u += 32)
+        sj[warp][0][u] = sj[warp][1][u] = sj[warp][2][u] = make_double2(0, 0);
+    __syncthreads();
+#pragma unroll 2
+    for (int s = 0; s < SB; ++s) {
+      const int u = k == 0 ? s : (s & ~31) + ((lane + s) & 31);
+      const double4 a = sq[u];
+      const double4 b = sp[u];
+      double jax = 0, jay = 0, jaz = 0, jbx = 0, jby = 0, jbz = 0;
+#pragma unroll
+      for (int kk = 0; kk < TPT; ++kk) {
+        const double dx = qx[kk] - a.x, dy = qy[kk] - a.y, dz = qz[kk] - a.z;
+        const double r2 = dx * dx + dy * dy + dz * dz;
+        const double g = exp_nonpos(-r2 * inv_two_s, stab);
+        const double pp = px[kk] * b.x + py[kk] * b.y + pz[kk] * b.z;
+        const double c = pp * g;
+        ax[kk] += g * b.x; ay[kk] += g * b.y; az[kk] += g * b.z;
+        bx[kk] += c * dx; by[kk] += c * dy; bz[kk] += c * dz;
+        jax += g * px[kk]; jay += g * py[kk]; jaz += g * pz[kk];
+        jbx += c * dx; jby += c * dy; jbz += c * dz;
+      }
+      if (k == 0) continue;
+      double2 v0 = sj[warp][0][u], v1 = sj[warp][1][u], v2 = sj[warp][2][u];
+      v0.x += jax; v0.y += jay; v1.x += jaz; v1.y += jbx; v2.x += jby; v2.y += jbz;
+      sj[warp][0][u] = v0; sj[warp][1][u] = v1; sj[warp][2][u] = v2;
+    }
+    if (k == 0) continue;
+    __syncthreads();
+    for (int u = threadIdx.x; u < SB; u += NT) {
+      const int j = jbase + st + u;
+      if (j < n) {
+        double2 s0 = sj[0][0][u], s1 = sj[0][1][u], s2 = sj[0][2][u];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const double2 t0 = sj[w][0][u], t1 = sj[w][1][u], t2 = sj[w][2][u];
+          s0.x += t0.x; s0.y += t0.y; s1.x += t1.x; s1.y += t1.y; s2.x += t2.x; s2.y += t2.y;
+        }
+        st4(part + 2 * (sjs + j), make_double4(s0.x, s0.y, s1.x, 0.0));
+        st4(part + 2 * (sjs + j) + 1, make_double4(-s1.y, -s2.x, -s2.y, 0.0));
+      }
+    }
+  }
+#pragma unroll
+  for (int kk = 0; kk < TPT; ++kk) {
+    const int t = tb + kk * NT;
+    if (t < n) {
+      st4(part + 2 * (si + t), make_double4(ax[kk], ay[kk], az[kk], 0.0));
+      st4(part + 2 * (si + t) + 1, make_double4(bx[kk], by[kk], bz[kk], 0.0));
+      if (k == 0) {  // the diagonal has no j side: its j slot is zero
+        st4(part + 2 * (sjs + t), make_double4(0, 0, 0, 0));
+        st4(part + 2 * (sjs + t) + 1, make_double4(0, 0, 0, 0));
+      }
+    }
+  }
+}
+
+// acc[t] (+)= sum over the group's S slots of part[s][t], in slot order
+__global__ void k_fold_group(const double4* __restrict__ part, int S, int n, int first,
+                             double4* __restrict__ acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double4 a = first ? make_double4(0, 0, 0, 0) : ld4(acc + 2 * t);
+  double4 b = first ? make_double4(0, 0, 0, 0) : ld4(acc + 2 * t + 1);
+  for (int s = 0; s < S; ++s) {
+    const double4 x = ld4(part + 2 * ((size_t)s * n + t)), y = ld4(part + 2 * ((size_t)s * n + t) + 1);
+    a.x += x.x; a.y += x.y; a.z += x.z;
+    b.x += y.x; b.y += y.y; b.z += y.z;
+  }
+  st4(acc + 2 * t, a);
+  st4(acc + 2 * t + 1, b);
+}
+
 // ----------------------------------------------------------------------------
 // Hessian-vector products (kernel_exact.hpp:53-69), gather form over all j:
 //   Apq = sum g (p_j.a_i + p_i.a_j) d'     Aqq = sum g (p_i.p_j) ((d'.db) C1 d' - db)
@@ -1538,6 +1675,40 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
     k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o);
   return T;
 }
+
+// Symmetric FP64 RHS (k_rhs_sym_f64): 1024-point tiles (4 targets x 256
+// threads), diagonal groups of kSymF64Group folded into a running sum.
+constexpr int kSymF64Tile = 4 * 256, kSymF64Group = 32;
+int sym_f64_tiles(int n) { return (n + kSymF64Tile - 1) / kSymF64Tile; }
+
+bool use_sym_f64(int n, int tgt_begin, int n_tgt, int plan_tgt) {
+  if (tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
+  const int mode = exact_pairs_mode();
+  if (mode == 1) return false;
+  return mode == 2 || n >= 40000;
+}
+
+size_t sym_f64_part_bytes(int n) {
+  // running sum (n x 64 B) + one group's slots (2 x group x n x 64 B)
+  return (size_t)(1 + 2 * kSymF64Group) * (size_t)n * 2 * sizeof(double4);
+}
+
+int rhs_sym_f64_partials(const void* rec, int n, const KernelConsts& kc, void* part,
+                         cudaStream_t st) {
+  const int T = sym_f64_tiles(n);
+  double4* acc = (double4*)part;
+  double4* slots = acc + 2 * (size_t)n;
+  const int kend = T / 2 + 1;
+  for (int k0 = 0; k0 < kend; k0 += kSymF64Group) {
+    const int k1 = std::min(kend, k0 + kSymF64Group);
+    k_rhs_sym_f64<4, 256, 1, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 256, 0, st>>>(
+        (const double4*)rec, n, T, k0, kc.inv_two_s, slots);
+    k_fold_group<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);
+  }
+  return 1;  // the epilogue reads the running sum as a single partial
+}
+
+int sym_f64_launches(int n) { return 2 * ((sym_f64_tiles(n) / 2 + 1 + kSymF64Group - 1) / kSymF64Group); }
 
 // Symmetric Hessian products (k_hess_sym_f32x2): 768-point tiles (6 targets
 // x 128 threads, two CTAs per SM), the same choice rules as the RHS.

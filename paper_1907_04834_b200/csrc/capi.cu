@@ -354,14 +354,18 @@ int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void*
                 int64_t tb, int64_t nt, DBuf& part, FwdEpi e, cudaStream_t st, int64_t* launches,
                 int* energy_blocks, int plan_tgt = -1) {
   const bool sym = use_sym(prec, (int)n, (int)tb, (int)nt, plan_tgt);
+  const bool sym64 = prec == kF64 && use_sym_f64((int)n, (int)tb, (int)nt, plan_tgt);
   if (sym)
     GS_TRY(part.ensure(sym_part_bytes((int)n)));
+  else if (sym64)
+    GS_TRY(part.ensure(sym_f64_part_bytes((int)n)));
   else
     GS_TRY(part.ensure((size_t)kMaxChunks * 2 * vec_bytes(prec) * std::max<int64_t>(nt, 1)));
   kt_mark(0, st);
-  const int S = sym ? rhs_sym_partials(rec, (int)n, kc, part.ptr, st)
-                    : rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr,
-                                   kMaxChunks, st, plan_tgt);
+  const int S = sym     ? rhs_sym_partials(rec, (int)n, kc, part.ptr, st)
+                : sym64 ? rhs_sym_f64_partials(rec, (int)n, kc, part.ptr, st)
+                        : rhs_partials(dev, prec, rec, (int)n, (int)tb, (int)nt, kc, part.ptr,
+                                       kMaxChunks, st, plan_tgt);
   kt_mark(0, st);
   if (S < 0) { set_error("chunk plan overflow"); return GS_INTERNAL; }
   GS_CUDA_OK(cudaGetLastError());
@@ -372,7 +376,7 @@ int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void*
   e.cp = 2.0;
   e.cq = fwd_cq(prec, kc);
   GS_TRY(fwd_epilogue(prec, e, st, energy_blocks));
-  if (launches) *launches += 2;
+  if (launches) *launches += sym64 ? 1 + sym_f64_launches((int)n) : 2;
   return GS_OK;
 }
 
@@ -892,7 +896,10 @@ gs_status gs_exact_pairs_plan(int32_t precision, int64_t n, int32_t* tiles) {
   if (!tiles) return bad_arg("null argument");
   GS_TRY(check_n(n));
   const int prec = precision == GS_F32 ? kF32 : kF64;
-  *tiles = use_sym(prec, (int)n, 0, (int)n, -1) ? sym_tiles((int)n) : 0;
+  if (prec == kF32)
+    *tiles = use_sym(prec, (int)n, 0, (int)n, -1) ? sym_tiles((int)n) : 0;
+  else
+    *tiles = use_sym_f64((int)n, 0, (int)n, -1) ? sym_f64_tiles((int)n) : 0;
   return GS_OK;
 }
 

@@ -120,6 +120,14 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt);
 int sym_tiles(int n);
 size_t sym_part_bytes(int n);
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st);
+// FP64 symmetric RHS (k_rhs_sym_f64, diagonal groups folded into a running
+// sum): returns S = 1 (part holds the running sum first)
+bool use_sym_f64(int n, int tgt_begin, int n_tgt, int plan_tgt);
+size_t sym_f64_part_bytes(int n);
+int rhs_sym_f64_partials(const void* rec, int n, const KernelConsts& kc, void* part,
+                         cudaStream_t st);
+int sym_f64_launches(int n);
+int sym_f64_tiles(int n);
 // bytes hess_partials needs in part for this problem (symmetric: T slots x 64 B)
 size_t hess_part_bytes(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt = -1);
 int hess_partials(const Device& dev, int prec, const void* rec, const void* adj, int n,

@@ -356,3 +356,31 @@ def test_symmetric_evaluate_matches_reference(gs, ref, pairs):
     rep, g, _, _ = ref.evaluate(q, p, t, 1.2, 0.7, 6, 0)
     assert ev.report["total"] == pytest.approx(rep[2], rel=1e-4)
     assert rel_l2(ev.gradient, g) <= 1e-3
+
+
+# FP64: 1024-point tiles, diagonals in groups of 32 folded into a running sum
+@pytest.mark.parametrize("n", [300, 1024 * 3 + 17, 1024 * 4 + 5])
+def test_symmetric_rhs_f64_matches_reference(gs, ref, pairs, n):
+    q, p = uniform(n, 10.0, seed=n + 7), sym_uniform(n, 1.0, seed=n + 8)
+    pairs(2)
+    h, dp, dq = gs.hamiltonian_with_gradients(q, p, 1.1)
+    h2, dp2, dq2 = gs.hamiltonian_with_gradients(q, p, 1.1)
+    assert np.array_equal(dp, dp2) and np.array_equal(dq, dq2) and h == h2
+    wp, wq, wh = ref.exact_rhs(q, p, 1.1)
+    assert rel_l2(dp, wp) < 1e-13
+    assert rel_l2(dq, wq) < 1e-12
+    assert abs(h - wh) <= 1e-12 * abs(wh)
+
+
+def test_symmetric_rhs_f64_groups_equal_gather(gs, pairs):
+    """70k points: T = 69 tiles, 35 diagonals in two groups (32 + 3): the
+    symmetric FP64 sum against the gather kernel's to FP64 rounding."""
+    n = 70_000
+    rng = np.random.default_rng(70)
+    q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+    assert gs.exact_pairs_plan(n, F64) == 69
+    _, dp, dq = gs.hamiltonian_with_gradients(q, p, 0.03)
+    pairs(1)
+    assert gs.exact_pairs_plan(n, F64) == 0
+    _, gp, gq = gs.hamiltonian_with_gradients(q, p, 0.03)
+    assert rel_l2(dp, gp) < 1e-13 and rel_l2(dq, gq) < 1e-12

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--time-n", type=int, default=1000000)
     ap.add_argument("--time-steps", type=int, default=1)
     ap.add_argument("--modes", type=int, nargs="*", default=[1, 2, 1, 2])
+    ap.add_argument("--f64", action="store_true")
     a = ap.parse_args()
     import numpy as np
     from paper_1907_04834_b200 import EXACT, F32, F64, RK4, Geoshoot, ShootingConfig
@@ -53,7 +54,8 @@ def main():
         q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-4, (n, 3))
         for mode in a.modes:
             gs.set_exact_pairs(mode)
-            cfg = ShootingConfig(sigma=0.0131, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+            cfg = ShootingConfig(sigma=0.0131, timesteps=10, backend=EXACT, integrator=RK4,
+                                 precision=F64 if a.f64 else F32)
             f = gs.flow(cfg, n)
             f.upload(q, p)
             f.advance(1)
