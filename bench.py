@@ -55,6 +55,7 @@ BUILD_BYTES_PER_POINT = 1080
 RHS_FP32_PER_PAIR = 16
 RHS_SYM_FP32_PER_PAIR = 11  # symmetric kernel: 22 per unordered pair
 HESS_FP32_PER_PAIR = 37
+HESS_SYM_FP32_PER_PAIR = 26  # symmetric Hessian kernel: 52 per unordered pair
 
 
 def workload(n: int, seed: int = 2024):
@@ -480,14 +481,21 @@ def run_ours(args):
             if backend == EXACT and ak["count"]:
                 h_ms = ak["ms"] / ak["count"]
                 pps = float(n3) * n3 / (h_ms * 1e-3)
-                hpeak = mb["ffma"] / HESS_FP32_PER_PAIR
+                # the symmetric Hessian kernel (same size rule as the RHS) does
+                # 52 FP32 per unordered pair = 26 per ordered pair
+                hsym = gs.exact_pairs_plan(n3, F32) > 0
+                hfp = HESS_SYM_FP32_PER_PAIR if hsym else HESS_FP32_PER_PAIR
+                hpeak = mb["ffma"] / hfp
                 rec["roofline"] = {
-                    "bound": "fp32-fma-pipe", "kernel": "k_hess_f32x2<4,128> (packed FFMA2)",
+                    "bound": "fp32-fma-pipe",
+                    "kernel": ("k_hess_sym_f32x2<6,128,2,64> (each unordered pair once, packed FFMA2)"
+                               if hsym else "k_hess_f32x2<4,128> (packed FFMA2)"),
                     "achieved": pps / 1e9, "peak": hpeak / 1e9, "unit": "Gpair/s",
                     "frac": pps / hpeak, "kernel_ms_avg": h_ms,
                     "algorithmic_per_launch": f"{float(n3) * n3:.3e} ordered pairs x "
-                                              f"{HESS_FP32_PER_PAIR} FP32 + 1 MUFU",
-                    "peak_source": "live FFMA microbenchmark / 37 FP32 per pair"}
+                                              f"{hfp} FP32 + {'1/2' if hsym else '1'} MUFU",
+                    "frac_of_gather_ceiling": pps / (mb["ffma"] / HESS_FP32_PER_PAIR),
+                    "peak_source": f"live FFMA microbenchmark / {hfp} FP32 per ordered pair"}
             elif ak["count"]:
                 rec["adjoint_walk_ms_avg"] = ak["ms"] / ak["count"]
                 rec["interactions"] = (evr.stats["direct_interactions"]
@@ -519,19 +527,26 @@ def run_ours(args):
         ms64, pr64 = timed_flow(N, F64, RK4, 1)
         k64 = pr64["kernel_ms"] / max(1, pr64["kernel_launches"])
         pps64 = float(N) * N / (k64 * 1e-3)
+        # DP operations per ordered pair incl. the 10-DP table-driven exp
+        # (csrc/gs_exp.cuh): gather 26; symmetric 35 per unordered pair
+        sym64 = gs.exact_pairs_plan(N, F64) > 0
+        dp_pp = 17.5 if sym64 else 26.0
         line["fp64"] = {
             "workload": f"exact FP64, N={N}, one RK4 step (4 RHS), config-4 distribution",
             "value": 1.0 / (ms64 / 1e3), "unit": "flow steps/s", "pair_interactions_per_s": pps64,
+            "kernel": ("k_rhs_sym_f64<4,256,1,64> + k_fold_group (each unordered pair once; "
+                       "1024-point tiles, diagonals in groups of 32)") if sym64 else "k_rhs_f64<4,128>",
             "kernel_ms": k64, "peak_dfma_lane_per_s": mb["dfma"],
-            "frac_16dp_basis": pps64 * 16.0 / mb["dfma"] if mb["dfma"] else None,
-            # + the 10-DP table-driven exp of the FP64 kernels (csrc/gs_exp.cuh)
-            "frac_26dp_basis_incl_exp": pps64 * 26.0 / mb["dfma"] if mb["dfma"] else None,
+            "dp_ops_per_ordered_pair": dp_pp,
+            "frac_of_dfma_peak": pps64 * dp_pp / mb["dfma"] if mb["dfma"] else None,
         }
         ms1, pr1 = timed_flow(100_000, F32, RK4, 3)
         line["n100k"] = {
             "value": 3 / (ms1 / 1e3), "unit": "flow steps/s (RK4)",
             "pair_interactions_per_s": 4.0 * 1e10 * 3 / (ms1 / 1e3),
             "frac_of_ffma_peak": (4.0 * 1e10 * 3 / (ms1 / 1e3)) / peak / 1e9,
+            "kernel": ("k_rhs_sym_f32x2<12,128,2,256,4> (symmetric, 1536-point tiles)"
+                       if gs.exact_pairs_plan(100_000, F32) else "k_rhs_f32x2 (gather)"),
         }
 
     # ---- CPU baseline: the reference's own exact RHS on the host cores ---------

@@ -20,8 +20,18 @@ from tests.util import rel_l2
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture
+def gather(gs):
+    # shards run the gather kernel (k_rhs_f32x2): compare against the same
+    # formulation on one flow (the unsharded default at this size is the
+    # symmetric kernel, equal to FP32 rounding -- checked below)
+    gs.set_exact_pairs(1)
+    yield
+    gs.set_exact_pairs(-1)
+
+
 @pytest.mark.parametrize("backend", [EXACT, BARNES_HUT])
-def test_two_shards_equal_one_flow(gs, backend):
+def test_two_shards_equal_one_flow(gs, gather, backend):
     n = 60_000
     rng = np.random.default_rng(77)
     q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
@@ -31,6 +41,16 @@ def test_two_shards_equal_one_flow(gs, backend):
     one.advance(2)
     one.sync()
     wq, wp = one.download()
+    if backend == EXACT:
+        gs.set_exact_pairs(-1)
+        assert gs.exact_pairs_plan(n, F32) > 0
+        sym = gs.flow(cfg, n)
+        sym.upload(q, p)
+        sym.advance(2)
+        sym.sync()
+        sq, sp = sym.download()
+        assert rel_l2(sq, wq) < 1e-6 and rel_l2(sp, wp) < 1e-5
+        gs.set_exact_pairs(1)
 
     a, b = gs.flow(cfg, n), gs.flow(cfg, n)
     for f in (a, b):
