@@ -266,10 +266,14 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
 // Per two unordered pairs (a packed target pair x one source): 22 packed FP32
 // + 2 MUFU issue slots = 6 per ordered pair (k_rhs_f32x2: 9).
 // The j side needs no atomics: at step s of a 32-source batch lane l takes
-// source (l + s) mod 32, so the 32 lanes of a warp always update 32 distinct
-// sources (each lane adds its TPT-target partial, folded over the packed
-// halves); each warp has its own copy of the j accumulators, summed in warp
-// order after the sub-tile.
+// source (l + s) mod 32, so the 32 lanes of a warp always hold 32 distinct
+// sources, and the source's packed j accumulators travel with it from lane to
+// lane (lane l takes them over from lane l + 1 by one shuffle per accumulator
+// and step; round 2 first used a fold + shared read-modify-write per step:
+// 4 % slower at 1M, 8 % at 100k). After 32 steps every lane holds one source's
+// sums over the warp's 32 x TPT targets, folded over the packed halves into
+// the warp's copy of the j accumulators, summed in warp order after the
+// sub-tile.
 // Partials: target t of tile X receives exactly T partials, one per tile Y
 // (slot Y): the i side of the pair (X, Y), the j side of the pair (Y, X), or,
 // for Y = X, the diagonal pair evaluated gather-style (ordered pairs, self
@@ -326,13 +330,6 @@ __global__ void __launch_bounds__(NT, MINB)
       sq[u] = q;  // zero records contribute exactly 0 (p = 0)
       sp[u] = p;
     }
-    if (k != 0) {
-      for (int u = lane; u < SB; u += 32) {
-        sj[warp][0][u] = make_float2(0.f, 0.f);
-        sj[warp][1][u] = make_float2(0.f, 0.f);
-        sj[warp][2][u] = make_float2(0.f, 0.f);
-      }
-    }
     __syncthreads();
     if (k == 0) {
       // diagonal tile pair: gather over the tile's own points (ordered pairs)
@@ -373,6 +370,10 @@ __global__ void __launch_bounds__(NT, MINB)
     float2* sj1 = sj[warp][1];
     float2* sj2 = sj[warp][2];
     for (int b0 = 0; b0 < SB; b0 += 32) {
+      // the packed j accumulators of source (lane + s) mod 32 travel with it
+      // from lane to lane: one 64-bit shuffle per accumulator and step, no
+      // fold and no shared read-modify-write inside the loop
+      f2 tax = pk2(0.f, 0.f), tay = tax, taz = tax, tbx = tax, tby = tax, tbz = tax;
 #pragma unroll SYM_UNR
       for (int s = 0; s < 32; ++s) {
         const int u = b0 + ((lane + s) & 31);
@@ -391,7 +392,6 @@ __global__ void __launch_bounds__(NT, MINB)
           r2 = fma2(dz[kk], dz[kk], r2);
           g[kk] = nex2x2(r2);
         }
-        f2 jax, jay, jaz, jbx, jby, jbz;
 #pragma unroll
         for (int kk = 0; kk < TP; ++kk) {
           f2 pp = mul2(px[kk], bxx);
@@ -404,21 +404,22 @@ __global__ void __launch_bounds__(NT, MINB)
           bx[kk] = fma2(c, dx[kk], bx[kk]);
           by[kk] = fma2(c, dy[kk], by[kk]);
           bz[kk] = fma2(c, dz[kk], bz[kk]);
-          if (kk == 0) {
-            jax = mul2(g[kk], px[kk]); jay = mul2(g[kk], py[kk]); jaz = mul2(g[kk], pz[kk]);
-            jbx = mul2(c, dx[kk]); jby = mul2(c, dy[kk]); jbz = mul2(c, dz[kk]);
-          } else {
-            jax = fma2(g[kk], px[kk], jax); jay = fma2(g[kk], py[kk], jay);
-            jaz = fma2(g[kk], pz[kk], jaz);
-            jbx = fma2(c, dx[kk], jbx); jby = fma2(c, dy[kk], jby); jbz = fma2(c, dz[kk], jbz);
-          }
+          tax = fma2(g[kk], px[kk], tax); tay = fma2(g[kk], py[kk], tay);
+          taz = fma2(g[kk], pz[kk], taz);
+          tbx = fma2(c, dx[kk], tbx); tby = fma2(c, dy[kk], tby); tbz = fma2(c, dz[kk], tbz);
         }
+        // lane l takes over the sums of source (l + 1 + s) mod 32 from lane l + 1
+        const int from = (lane + 1) & 31;
+        tax.v = __shfl_sync(0xffffffffu, tax.v, from); tay.v = __shfl_sync(0xffffffffu, tay.v, from);
+        taz.v = __shfl_sync(0xffffffffu, taz.v, from); tbx.v = __shfl_sync(0xffffffffu, tbx.v, from);
+        tby.v = __shfl_sync(0xffffffffu, tby.v, from); tbz.v = __shfl_sync(0xffffffffu, tbz.v, from);
+      }
+      {  // after 32 steps lane l holds source l's sums over all 32 lanes
         float l0, h0, l1, h1;
-        float2 v0 = sj0[u], v1 = sj1[u], v2 = sj2[u];
-        up2(jax, l0, h0); up2(jay, l1, h1); v0.x += l0 + h0; v0.y += l1 + h1;
-        up2(jaz, l0, h0); up2(jbx, l1, h1); v1.x += l0 + h0; v1.y += l1 + h1;
-        up2(jby, l0, h0); up2(jbz, l1, h1); v2.x += l0 + h0; v2.y += l1 + h1;
-        sj0[u] = v0; sj1[u] = v1; sj2[u] = v2;
+        const int u = b0 + lane;
+        up2(tax, l0, h0); up2(tay, l1, h1); sj0[u] = make_float2(l0 + h0, l1 + h1);
+        up2(taz, l0, h0); up2(tbx, l1, h1); sj1[u] = make_float2(l0 + h0, l1 + h1);
+        up2(tby, l0, h0); up2(tbz, l1, h1); sj2[u] = make_float2(l0 + h0, l1 + h1);
       }
     }
     __syncthreads();
@@ -780,20 +781,21 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       sq[u] = q; sp[u] = p; sa[u] = a; sb[u] = b;  // zero records contribute exactly 0
     }
-    if (k != 0)
-      for (int u = lane; u < SB; u += 32)
-        sj[warp][0][u] = sj[warp][1][u] = sj[warp][2][u] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    for (int s = 0; s < SB; ++s) {
-      // diagonal pair: gather over every source (u = s); else lane l takes
-      // source (l + s) mod 32 of the current 32-source batch
-      const int u = k == 0 ? s : (s & ~31) + ((lane + s) & 31);
+    for (int b0 = 0; b0 < SB; b0 += 32) {
+     // j sums of source (lane + s) mod 32, travelling with it from lane to lane
+     f2 Jv[12];
+#pragma unroll
+     for (int c = 0; c < 12; ++c) Jv[c] = pk2(0.f, 0.f);
+     for (int s = 0; s < 32; ++s) {
+      // diagonal pair: gather over every source; else lane l takes source
+      // (l + s) mod 32 of the current 32-source batch
+      const int u = b0 + (k == 0 ? s : ((lane + s) & 31));
       const float4 Q = sq[u], P = sp[u], Al = sa[u], Be = sb[u];
       const f2 Qx = bc2(Q.x), Qy = bc2(Q.y), Qz = bc2(Q.z);
       const f2 Px = bc2(P.x), Py = bc2(P.y), Pz = bc2(P.z);
       const f2 Ax = bc2(Al.x), Ay = bc2(Al.y), Az = bc2(Al.z);
       const f2 Bx = bc2(Be.x), By = bc2(Be.y), Bz = bc2(Be.z);
-      f2 Jv[12];
 #pragma unroll
       for (int kk = 0; kk < TP; ++kk) {
         const f2 dx = sub2(qx[kk], Qx), dy = sub2(qy[kk], Qy), dz = sub2(qz[kk], Qz);
@@ -824,19 +826,17 @@ __global__ void __launch_bounds__(NT, MINB)
         const f2 m = mul2(g, ddb);
         A[kk][9] = fma2(m, Px, A[kk][9]); A[kk][10] = fma2(m, Py, A[kk][10]); A[kk][11] = fma2(m, Pz, A[kk][11]);
         if (k == 0) continue;
-        if (kk == 0) {
-          Jv[0] = mul2(t1, dx); Jv[1] = mul2(t1, dy); Jv[2] = mul2(t1, dz);
-          Jv[3] = mul2(g, ix[kk]); Jv[4] = mul2(g, iy[kk]); Jv[5] = mul2(g, iz[kk]);
-          Jv[6] = mul2(w, zx); Jv[7] = mul2(w, zy); Jv[8] = mul2(w, zz);
-          Jv[9] = mul2(m, px[kk]); Jv[10] = mul2(m, py[kk]); Jv[11] = mul2(m, pz[kk]);
-        } else {
-          Jv[0] = fma2(t1, dx, Jv[0]); Jv[1] = fma2(t1, dy, Jv[1]); Jv[2] = fma2(t1, dz, Jv[2]);
-          Jv[3] = fma2(g, ix[kk], Jv[3]); Jv[4] = fma2(g, iy[kk], Jv[4]); Jv[5] = fma2(g, iz[kk], Jv[5]);
-          Jv[6] = fma2(w, zx, Jv[6]); Jv[7] = fma2(w, zy, Jv[7]); Jv[8] = fma2(w, zz, Jv[8]);
-          Jv[9] = fma2(m, px[kk], Jv[9]); Jv[10] = fma2(m, py[kk], Jv[10]); Jv[11] = fma2(m, pz[kk], Jv[11]);
-        }
+        Jv[0] = fma2(t1, dx, Jv[0]); Jv[1] = fma2(t1, dy, Jv[1]); Jv[2] = fma2(t1, dz, Jv[2]);
+        Jv[3] = fma2(g, ix[kk], Jv[3]); Jv[4] = fma2(g, iy[kk], Jv[4]); Jv[5] = fma2(g, iz[kk], Jv[5]);
+        Jv[6] = fma2(w, zx, Jv[6]); Jv[7] = fma2(w, zy, Jv[7]); Jv[8] = fma2(w, zz, Jv[8]);
+        Jv[9] = fma2(m, px[kk], Jv[9]); Jv[10] = fma2(m, py[kk], Jv[10]); Jv[11] = fma2(m, pz[kk], Jv[11]);
       }
       if (k == 0) continue;
+      const int from = (lane + 1) & 31;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) Jv[c].v = __shfl_sync(0xffffffffu, Jv[c].v, from);
+     }
+     if (k != 0) {  // lane l now holds source b0 + l's sums over the warp's targets
       float f[12];
 #pragma unroll
       for (int c = 0; c < 12; ++c) {
@@ -844,11 +844,11 @@ __global__ void __launch_bounds__(NT, MINB)
         up2(Jv[c], lo, hi);
         f[c] = lo + hi;
       }
-      float4 v0 = sj[warp][0][u], v1 = sj[warp][1][u], v2 = sj[warp][2][u];
-      v0.x += f[0]; v0.y += f[1]; v0.z += f[2]; v0.w += f[3];
-      v1.x += f[4]; v1.y += f[5]; v1.z += f[6]; v1.w += f[7];
-      v2.x += f[8]; v2.y += f[9]; v2.z += f[10]; v2.w += f[11];
-      sj[warp][0][u] = v0; sj[warp][1][u] = v1; sj[warp][2][u] = v2;
+      const int u = b0 + lane;
+      sj[warp][0][u] = make_float4(f[0], f[1], f[2], f[3]);
+      sj[warp][1][u] = make_float4(f[4], f[5], f[6], f[7]);
+      sj[warp][2][u] = make_float4(f[8], f[9], f[10], f[11]);
+     }
     }
     if (k == 0) continue;
     __syncthreads();
@@ -1025,16 +1025,15 @@ __global__ void __launch_bounds__(NT, MINB)
       sq[u] = q;  // zero records (p = 0) contribute exactly 0
       sp[u] = p;
     }
-    if (k != 0)
-      for (int u = lane; u < SB; u += 32)
-        sj[warp][0][u] = sj[warp][1][u] = sj[warp][2][u] = make_double2(0, 0);
     __syncthreads();
+    for (int b0 = 0; b0 < SB; b0 += 32) {
+     // j sums of source (lane + s) mod 32, travelling with it from lane to lane
+     double jax = 0, jay = 0, jaz = 0, jbx = 0, jby = 0, jbz = 0;
 #pragma unroll 2
-    for (int s = 0; s < SB; ++s) {
-      const int u = k == 0 ? s : (s & ~31) + ((lane + s) & 31);
+     for (int s = 0; s < 32; ++s) {
+      const int u = b0 + (k == 0 ? s : ((lane + s) & 31));
       const double4 a = sq[u];
       const double4 b = sp[u];
-      double jax = 0, jay = 0, jaz = 0, jbx = 0, jby = 0, jbz = 0;
 #pragma unroll
       for (int kk = 0; kk < TPT; ++kk) {
         const double dx = qx[kk] - a.x, dy = qy[kk] - a.y, dz = qz[kk] - a.z;
@@ -1048,9 +1047,17 @@ __global__ void __launch_bounds__(NT, MINB)
         jbx += c * dx; jby += c * dy; jbz += c * dz;
       }
       if (k == 0) continue;
-      double2 v0 = sj[warp][0][u], v1 = sj[warp][1][u], v2 = sj[warp][2][u];
-      v0.x += jax; v0.y += jay; v1.x += jaz; v1.y += jbx; v2.x += jby; v2.y += jbz;
-      sj[warp][0][u] = v0; sj[warp][1][u] = v1; sj[warp][2][u] = v2;
+      const int from = (lane + 1) & 31;
+      jax = __shfl_sync(0xffffffffu, jax, from); jay = __shfl_sync(0xffffffffu, jay, from);
+      jaz = __shfl_sync(0xffffffffu, jaz, from); jbx = __shfl_sync(0xffffffffu, jbx, from);
+      jby = __shfl_sync(0xffffffffu, jby, from); jbz = __shfl_sync(0xffffffffu, jbz, from);
+     }
+     if (k != 0) {  // lane l now holds source b0 + l's sums over the warp's targets
+      const int u = b0 + lane;
+      sj[warp][0][u] = make_double2(jax, jay);
+      sj[warp][1][u] = make_double2(jaz, jbx);
+      sj[warp][2][u] = make_double2(jby, jbz);
+     }
     }
     if (k == 0) continue;
     __syncthreads();
