@@ -45,7 +45,7 @@ constexpr int kTile = 256;
 constexpr int kSortedUnr = GS_SORTED_UNR;  // source-loop unroll, k_rhs_f32x2_sorted
 constexpr int kF64Unr = GS_F64_UNR;        // source-loop unroll, k_rhs_f64
 
-template <int TPT, int NT, int MINB, bool PHASED>
+template <int TPT, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__ rec, int n,
                                                       int tgt_begin, int n_tgt, int chunk,
                                                       float kap, float kc0x, float kc0y, float kc0z,
@@ -83,59 +83,33 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32(const float4* __restrict__
       sp[u] = p;
     }
     __syncthreads();
-    if (PHASED) {
-      // all TPT exponentials are issued before the first one is consumed, so
-      // the MUFU latency hides behind independent work of the same warp
+    // all TPT exponentials are issued before the first one is consumed, so
+    // the MUFU latency hides behind independent work of the same warp
 #pragma unroll 2
-      for (int u = 0; u < kTile; ++u) {
-        const float4 a = sq[u];
-        const float4 b = sp[u];
-        float dx[TPT], dy[TPT], dz[TPT], g[TPT];
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u];
+      const float4 b = sp[u];
+      float dx[TPT], dy[TPT], dz[TPT], g[TPT];
 #pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          dx[k] = qx[k] - a.x; dy[k] = qy[k] - a.y; dz[k] = qz[k] - a.z;
-          float nr2 = -dx[k] * dx[k];
-          nr2 = fmaf(-dy[k], dy[k], nr2);
-          nr2 = fmaf(-dz[k], dz[k], nr2);
-          g[k] = ex2(nr2);
-        }
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          float pp = px[k] * b.x;
-          pp = fmaf(py[k], b.y, pp);
-          pp = fmaf(pz[k], b.z, pp);
-          const float c = pp * g[k];
-          ax[k] = fmaf(g[k], b.x, ax[k]);
-          ay[k] = fmaf(g[k], b.y, ay[k]);
-          az[k] = fmaf(g[k], b.z, az[k]);
-          bx[k] = fmaf(c, dx[k], bx[k]);
-          by[k] = fmaf(c, dy[k], by[k]);
-          bz[k] = fmaf(c, dz[k], bz[k]);
-        }
+      for (int k = 0; k < TPT; ++k) {
+        dx[k] = qx[k] - a.x; dy[k] = qy[k] - a.y; dz[k] = qz[k] - a.z;
+        float nr2 = -dx[k] * dx[k];
+        nr2 = fmaf(-dy[k], dy[k], nr2);
+        nr2 = fmaf(-dz[k], dz[k], nr2);
+        g[k] = ex2(nr2);
       }
-    } else {
-#pragma unroll 2
-      for (int u = 0; u < kTile; ++u) {
-        const float4 a = sq[u];
-        const float4 b = sp[u];
 #pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          const float dx = qx[k] - a.x, dy = qy[k] - a.y, dz = qz[k] - a.z;
-          float nr2 = -dx * dx;
-          nr2 = fmaf(-dy, dy, nr2);
-          nr2 = fmaf(-dz, dz, nr2);
-          const float g = ex2(nr2);
-          float pp = px[k] * b.x;
-          pp = fmaf(py[k], b.y, pp);
-          pp = fmaf(pz[k], b.z, pp);
-          const float c = pp * g;
-          ax[k] = fmaf(g, b.x, ax[k]);
-          ay[k] = fmaf(g, b.y, ay[k]);
-          az[k] = fmaf(g, b.z, az[k]);
-          bx[k] = fmaf(c, dx, bx[k]);
-          by[k] = fmaf(c, dy, by[k]);
-          bz[k] = fmaf(c, dz, bz[k]);
-        }
+      for (int k = 0; k < TPT; ++k) {
+        float pp = px[k] * b.x;
+        pp = fmaf(py[k], b.y, pp);
+        pp = fmaf(pz[k], b.z, pp);
+        const float c = pp * g[k];
+        ax[k] = fmaf(g[k], b.x, ax[k]);
+        ay[k] = fmaf(g[k], b.y, ay[k]);
+        az[k] = fmaf(g[k], b.z, az[k]);
+        bx[k] = fmaf(c, dx[k], bx[k]);
+        by[k] = fmaf(c, dy[k], by[k]);
+        bz[k] = fmaf(c, dz[k], bz[k]);
       }
     }
   }
@@ -1449,42 +1423,39 @@ constexpr int kNT = 128;
     default: KERNEL<1, kNT><<<pl.grid, kNT, 0, st>>>(__VA_ARGS__); break; \
   }
 
-// FP32 RHS variants: {TPT, min CTAs/SM, phased}. Variant 0 is the default;
-// GS_RHS_VARIANT selects another one for tuning sweeps (tools/sweep_rhs.py).
+// Gather FP32 RHS variants (shards and problems below 40k points), chosen by
+// size: 0 = packed TPT 8 (3 CTAs/SM), 1 = packed TPT 12 from 500k targets,
+// 2 = packed TPT 2 for grids that would not fill the GPU, 3 = scalar TPT 1
+// for tiny problems; all with the source loop unrolled 8. GS_RHS_VARIANT
+// forces one (the small-grid fallbacks still apply). Round 1 also measured
+// scalar TPT 4 / 6 / 8, unphased, 4-CTA, TPT 16 and 4x-unrolled variants
+// (profiles/r01_sweep_rhs_*.jsonl); they were slower and are no longer built.
 struct RhsVariant {
   int tpt, minb;
-  bool phased;
 };
-static const RhsVariant kRhsVariants[] = {
-    {8, 3, true}, {8, 3, false}, {8, 4, true}, {4, 6, true}, {4, 4, false}, {6, 4, true}, {2, 8, true}, {1, 8, true},
-    // packed FP32x2 (FFMA2) variants
-    {8, 3, true}, {8, 4, true}, {4, 6, true}, {2, 8, true},
-    // packed, source loop unrolled 4 / 8 (fewer loop-carried register copies), TPT 12
-    {8, 3, true}, {8, 3, true}, {12, 2, true}, {12, 2, true}, {16, 2, true}, {16, 1, true},
-    // small grids (default's fallback), source loop unrolled 8
-    {2, 8, true}};
+static const RhsVariant kRhsVariants[] = {{8, 3}, {12, 2}, {2, 8}, {1, 8}};
 constexpr int kNumRhsVariants = sizeof(kRhsVariants) / sizeof(kRhsVariants[0]);
 
 static int rhs_variant() {
   static int v = [] {
     const char* e = std::getenv("GS_RHS_VARIANT");
-    const int x = e ? std::atoi(e) : 13;
-    return (x >= 0 && x < kNumRhsVariants) ? x : 0;
+    const int x = e ? std::atoi(e) : -1;
+    return (x >= 0 && x < kNumRhsVariants) ? x : -1;
   }();
   return v;
 }
 
-template <int TPT, int MINB, bool PH>
+template <int TPT, int MINB>
 static void launch_rhs_f32(const Plan& pl, cudaStream_t st, const float4* rec, int n, int tb,
                            int nt, const KernelConsts& kc, float4* part) {
-  k_rhs_f32<TPT, kNT, MINB, PH><<<pl.grid, kNT, 0, st>>>(
+  k_rhs_f32<TPT, kNT, MINB><<<pl.grid, kNT, 0, st>>>(
       rec, n, tb, nt, pl.chunk, (float)kc.kappa, (float)(kc.kappa * kc.c0[0]),
       (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), part);
 }
 
-template <int TPT, int MINB, bool PH>
+template <int TPT, int MINB>
 static int occ_rhs_f32() {
-  return occupancy(k_rhs_f32<TPT, kNT, MINB, PH>, kNT);
+  return occupancy(k_rhs_f32<TPT, kNT, MINB>, kNT);
 }
 
 template <int TPT, int MINB, int UNR = 2>
@@ -1553,25 +1524,17 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
   if (plan_tgt > 0) n_tgt = plan_tgt;  // plan as if for plan_tgt targets (multi-device shards)
   if (prec == kF32) {
     const int vi = rhs_variant();
-    const RhsVariant v = kRhsVariants[vi];
-    // small problems: fall back to narrower target blocks so the grid fills the GPU
     const long slots = 3L * dev.sms;
-    int use = vi;
     // default: TPT 12 once the grid holds many waves of its larger blocks
     // (measured: 1.933 vs 1.913 Tpair/s at 1M; 1.81 vs 1.89 at 100k)
-    if (!std::getenv("GS_RHS_VARIANT") && n_tgt >= 500000) use = 15;
-    // (packed TPT 2 when the chosen variant is packed, scalar TPT 1 for tiny N)
-    if ((long)((n_tgt + kNT * v.tpt - 1) / (kNT * v.tpt)) * 16 < 2 * slots) use = vi >= 12 ? 18 : (vi >= 8 ? 11 : 6);
-    if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 7;
+    int use = vi >= 0 ? vi : (n_tgt >= 500000 ? 1 : 0);
+    // small problems: narrower target blocks so the grid fills the GPU
+    const int tpt = kRhsVariants[use].tpt;
+    if ((long)((n_tgt + kNT * tpt - 1) / (kNT * tpt)) * 16 < 2 * slots && use < 2) use = 2;
+    if ((long)((n_tgt + kNT * 2 - 1) / (kNT * 2)) * 16 < 2 * slots) use = 3;
     const RhsVariant u = kRhsVariants[use];
-    static int occs[kNumRhsVariants] = {
-        occ_rhs_f32<8, 3, true>(), occ_rhs_f32<8, 3, false>(), occ_rhs_f32<8, 4, true>(),
-        occ_rhs_f32<4, 6, true>(), occ_rhs_f32<4, 4, false>(), occ_rhs_f32<6, 4, true>(),
-        occ_rhs_f32<2, 8, true>(), occ_rhs_f32<1, 8, true>(),
-        occ_rhs_f32x2<8, 3>(), occ_rhs_f32x2<8, 4>(), occ_rhs_f32x2<4, 6>(),
-        occ_rhs_f32x2<2, 8>(), occ_rhs_f32x2<8, 3, 4>(), occ_rhs_f32x2<8, 3, 8>(),
-        occ_rhs_f32x2<12, 2, 4>(), occ_rhs_f32x2<12, 2, 8>(), occ_rhs_f32x2<16, 2, 4>(),
-        occ_rhs_f32x2<16, 1, 4>(), occ_rhs_f32x2<2, 8, 8>()};
+    static int occs[kNumRhsVariants] = {occ_rhs_f32x2<8, 3, 8>(), occ_rhs_f32x2<12, 2, 8>(),
+                                        occ_rhs_f32x2<2, 8, 8>(), occ_rhs_f32<1, 8>()};
     const int tp[] = {u.tpt};
     Plan pl = fit(plan(n, n_tgt, kNT, tp, 1, kTile, occs[use], dev.sms), real_tgt);
     if (pl.S > part_cap_chunks) return -1;
@@ -1579,25 +1542,10 @@ int rhs_partials(const Device& dev, int prec, const void* rec, int n, int tgt_be
     float4* o = (float4*)part;
     n_tgt = real_tgt;
     switch (use) {
-      case 0: launch_rhs_f32<8, 3, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 1: launch_rhs_f32<8, 3, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 2: launch_rhs_f32<8, 4, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 3: launch_rhs_f32<4, 6, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 4: launch_rhs_f32<4, 4, false>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 5: launch_rhs_f32<6, 4, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 6: launch_rhs_f32<2, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 8: launch_rhs_f32x2<8, 3>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 9: launch_rhs_f32x2<8, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 10: launch_rhs_f32x2<4, 6>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 11: launch_rhs_f32x2<2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 12: launch_rhs_f32x2<8, 3, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 13: launch_rhs_f32x2<8, 3, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 14: launch_rhs_f32x2<12, 2, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 15: launch_rhs_f32x2<12, 2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 16: launch_rhs_f32x2<16, 2, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 17: launch_rhs_f32x2<16, 1, 4>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      case 18: launch_rhs_f32x2<2, 8, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
-      default: launch_rhs_f32<1, 8, true>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 0: launch_rhs_f32x2<8, 3, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 1: launch_rhs_f32x2<12, 2, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      case 2: launch_rhs_f32x2<2, 8, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
+      default: launch_rhs_f32<1, 8>(pl, st, r, n, tgt_begin, n_tgt, kc, o); break;
     }
     return pl.S;
   }

@@ -38,7 +38,7 @@ if __name__ == "__main__":
     if os.environ.get("GS_SWEEP_CHILD"):
         one(n, 2)
     else:
-        vs = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else range(8)
+        vs = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else range(4)
         for v in vs:
             env = dict(os.environ, GS_RHS_VARIANT=str(v), GS_SWEEP_CHILD="1")
             subprocess.run([sys.executable, __file__, str(n)], env=env, check=False)
