@@ -111,3 +111,34 @@ def test_exact_dhdp_1m_against_reference_velocity(gs, ref):
     rows = np.random.default_rng(8).choice(len(q), 48, replace=False)
     v = ref.exact_velocity(q[rows], q, p, sigma)
     assert rel_l2(dp[rows], 2.0 * v) < 1e-5
+
+
+def test_exact_f64_dhdp_1m_against_reference_velocity(gs, ref):
+    """Config 4 exact RHS at N = 1M in FP64 (the symmetric FP64 kernel, 977
+    tiles, diagonals in 16 groups): dH/dp = 2 v on sampled targets against the
+    reference's exact_velocity over all 1M sources."""
+    q, p, sigma = c4(1_000_000)(F64)
+    assert gs.exact_pairs_plan(len(q), F64) > 0
+    _, dp, _ = gs.hamiltonian_with_gradients(q, p, sigma, precision=F64)
+    rows = np.random.default_rng(9).choice(len(q), 32, replace=False)
+    v = ref.exact_velocity(q[rows], q, p, sigma)
+    assert rel_l2(dp[rows], 2.0 * v) < 1e-12
+
+
+def test_exact_adjoint_c3_symmetric_equals_gather(gs):
+    """Config 3 size (50k tube): the symmetric Hessian-product kernel against
+    the gather kernel (each checked against the reference at small N in
+    test_gpu_exact.py) -- FP32 rounding apart."""
+    q, p, sigma = c3_template(F32)
+    q, p = f32(q), f32(p)
+    n = len(q)
+    a, b = f32(sym_uniform(n, 1.0, 93)), f32(sym_uniform(n, 1.0, 94))
+    assert gs.exact_pairs_plan(n, F32) > 0
+    sym = gs.hessian_products(q, p, a, b, sigma, precision=F32)
+    gs.set_exact_pairs(1)
+    try:
+        gather = gs.hessian_products(q, p, a, b, sigma, precision=F32)
+    finally:
+        gs.set_exact_pairs(-1)
+    for s_, g_ in zip(sym, gather):
+        assert rel_l2(s_, g_) < 2e-6
