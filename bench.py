@@ -279,7 +279,7 @@ def run_ours(args):
     achieved = pairs_per_launch / (k_ms * 1e-3) / 1e9  # Gpair/s
     # the symmetric kernel (unsharded, N >= 200k) evaluates each unordered pair
     # once for both ends: 22 FP32 per unordered pair = 11 per ordered pair
-    tiles = gs.exact_pairs_plan(N, F32) if world == 1 else 0
+    tiles = gs.exact_pairs_plan(N, F32) if (world == 1 or (drv is not None and drv.pairs)) else 0
     fp32_pp = RHS_SYM_FP32_PER_PAIR if tiles else RHS_FP32_PER_PAIR
     peak = mb["ffma"] / fp32_pp / 1e9
     mp = peaks_json()
@@ -315,7 +315,10 @@ def run_ours(args):
         "config": {"workload": f"config4: exact all-pairs RHS, RK4 x {T_STEPS} steps, N={N}, "
                                f"sigma={SIGMA}, unit cube, fp32; 1 step = 4 RHS",
                    "n": N, "sigma": SIGMA, "integrator": "rk4", "timesteps": T_STEPS,
-                   "backend": "exact", "parallelism": f"target-shard x{world}",
+                   "backend": "exact",
+                   "parallelism": (f"pair-rows x{world} (symmetric tile-pair rows, all-to-all of "
+                                   "per-target partials + all-gather of records per stage)")
+                   if drv is not None and drv.pairs else f"target-shard x{world}",
                    "l2": "flushed (256 MB write) before every timed step"},
         "pair_interactions_per_s": pairs_per_s,
         "gpu_launches": launches,

@@ -358,6 +358,21 @@ int64_t gs_flow_record_bytes(const gs_flow* flow);
  * epilogue that rewrites the shard's records); stage = 0..stages-1 of the
  * current step (Euler 1, RK4 4). */
 gs_status gs_flow_stage(gs_flow* flow, int32_t stage);
+/* Multi-GPU symmetric exact stages (exact FP32 flows whose
+ * problem takes the symmetric kernel, gs_exact_pairs_plan): rank `rank` of
+ * `world` evaluates the unordered tile pairs of its rows of the tile-pair
+ * grid -- each pair once, for both ends, as the reference's i < j sweep
+ * (kernel_exact.cpp:29-61) -- instead of the gather form over its target
+ * shard. *enabled = 0 when the flow does not qualify (the caller then uses
+ * gs_flow_stage). A stage is then: gs_flow_stage_pairs (this rank's rows,
+ * folded per target into n x 2 float4 partials {A = sum g p, B = sum c d'} on
+ * the flow's stream; *partials = that device buffer), an exchange by the
+ * caller (every rank sends each shard's slice to its owner), and
+ * gs_flow_stage_apply (the shard's stage epilogue over nparts partials laid
+ * out [part][shard_count] x 2 float4, folded in order). */
+gs_status gs_flow_set_pair_rows(gs_flow* flow, int32_t rank, int32_t world, int32_t* enabled);
+gs_status gs_flow_stage_pairs(gs_flow* flow, int32_t stage, void** partials);
+gs_status gs_flow_stage_apply(gs_flow* flow, int32_t stage, const void* partials, int32_t nparts);
 
 /* ---- registration optimizer ------------------------------
  * optimize(), optimizer.cpp:301-351: L-BFGS + strong-Wolfe line search over p0

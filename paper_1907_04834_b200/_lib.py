@@ -158,6 +158,9 @@ SIGNATURES = [
     ("gs_flow_source_buffer", _vp, [_vp]),
     ("gs_flow_record_bytes", _i64, [_vp]),
     ("gs_flow_stage", _st, [_vp, C.c_int32]),
+    ("gs_flow_set_pair_rows", _st, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+    ("gs_flow_stage_pairs", _st, [_vp, C.c_int32, C.POINTER(_vp)]),
+    ("gs_flow_stage_apply", _st, [_vp, C.c_int32, _vp, C.c_int32]),
     ("gs_microbench", _st, [C.c_int, C.c_int32, _d]),
     ("gs_format_for_path", C.c_int32, [C.c_char_p]),
     ("gs_procrustes_align", _st, [_vp, _i64, _d, _d, _d, _d, _d]),

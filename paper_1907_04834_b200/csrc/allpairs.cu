@@ -259,13 +259,13 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
 template <int TPT, int NT, int MINB, int SB, int SYM_UNR = GS_SYM_UNR>
 __global__ void __launch_bounds__(NT, MINB)
     k_rhs_sym_f32x2(const float4* __restrict__ rec, int n, int T, float kap, float kc0x,
-                    float kc0y, float kc0z, float4* __restrict__ part) {
+                    float kc0y, float kc0z, float4* __restrict__ part, int row0 = 0) {
   constexpr int TP = TPT / 2, TILE = NT * TPT, NW = NT / 32;
   static_assert(TILE % SB == 0 && SB % 32 == 0 && TPT % 2 == 0, "tile shape");
   __shared__ float4 sq[SB];
   __shared__ float4 sp[SB];
   __shared__ float2 sj[NW][3][SB];
-  const int I = blockIdx.x, k = blockIdx.y;
+  const int I = row0 + blockIdx.x, k = blockIdx.y;  // row0: multi-GPU rows (rhs_sym_rows)
   if (2 * k == T && I >= k) return;  // even T: the pair {I, I + T/2} once
   const int J = I + k < T ? I + k : I + k - T;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1616,6 +1616,58 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
 }
 
 size_t sym_part_bytes(int n) { return (size_t)sym_tiles(n) * (size_t)n * 2 * sizeof(float4); }
+
+// Multi-GPU symmetric RHS: rank r of G evaluates the tile-pair
+// rows I in [T r / G, T (r+1) / G) -- every unordered tile pair belongs to
+// exactly one row, and rows are equally loaded (T/2 + 1 pairs each) -- and
+// folds, for EVERY target, the slots its rows wrote (in slot order) into one
+// partial (A, B). The ranks then exchange the partials of each target shard
+// (all-to-all) and the shard's epilogue folds the G partials in rank order.
+// owner(X, Y): the row whose CTA evaluates the pair {X, Y} (k = (Y - X) mod T;
+// k <= T/2 -> X, except the even-T k = T/2 pairs, taken by min(X, Y); else Y).
+__device__ __forceinline__ int pair_owner(int X, int Y, int T) {
+  const int k = Y >= X ? Y - X : Y - X + T;
+  if (2 * k == T) return min(X, Y);
+  return 2 * k < T ? X : Y;
+}
+
+__global__ void k_fold_rows(const float4* __restrict__ part, int n, int T, int tile, int ra,
+                            int rb, float4* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int X = t / tile;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  for (int Y = 0; Y < T; ++Y) {
+    const int o = pair_owner(X, Y, T);
+    if (o < ra || o >= rb) continue;
+    const float4 u = part[2 * ((size_t)Y * n + t)], v = part[2 * ((size_t)Y * n + t) + 1];
+    a.x += u.x; a.y += u.y; a.z += u.z;
+    b.x += v.x; b.y += v.y; b.z += v.z;
+  }
+  out[2 * t] = a;
+  out[2 * t + 1] = b;
+}
+
+int rhs_sym_rows(const void* rec, int n, const KernelConsts& kc, void* part, void* out, int rank,
+                 int world, cudaStream_t st) {
+  const int T = sym_tiles(n);
+  const int v = sym_variant(n);
+  const int tile = kSym[v].tpt * kSym[v].nt;
+  const int ra = (int)((long)T * rank / world), rb = (int)((long)T * (rank + 1) / world);
+  const float kap = (float)kc.kappa, a = (float)(kc.kappa * kc.c0[0]),
+              b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
+  const float4* r = (const float4*)rec;
+  float4* o = (float4*)part;
+  if (rb > ra) {
+    const dim3 grid((unsigned)(rb - ra), (unsigned)(T / 2 + 1), 1);
+    if (v == 0)
+      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o, ra);
+    else
+      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o, ra);
+  }
+  k_fold_rows<<<(n + 255) / 256, 256, 0, st>>>(o, n, T, tile, ra, rb, (float4*)out);
+  return T;
+}
 
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st) {
   const int T = sym_tiles(n);

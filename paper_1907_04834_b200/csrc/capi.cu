@@ -112,6 +112,10 @@ struct gs_flow {
   std::vector<gs_flow*> subs;
   PeerOut peers;     // set by the multi-device driver for the next stage
   int plan_tgt = -1; // exact RHS planned for this many targets (bitwise shards)
+  // multi-GPU symmetric exact stages (gs_flow_set_pair_rows): this rank's
+  // tile-pair rows, and its per-target fold of them (n x 2 float4)
+  int pair_rank = -1, pair_world = 0;
+  DBuf pair_out;
   // CUDA graph of one integrator step (all stages + the step-counter bump),
   // captured after the first eager step and replayed for the following ones
   DBuf stepctr;
@@ -408,12 +412,11 @@ struct TimerInstall {
 // One integrator stage for the shard: RHS (exact or Barnes-Hut) + epilogue.
 // rec_in (default: the flow's records) holds all n source records; the
 // shard's updated records go to rec_out (default: in place).
-int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
-  gs_ctx* c = f->ctx;
-  cudaStream_t st = c->stream;
-  if (!rec_in) rec_in = f->rec.ptr;
+// The stage epilogue's parameters for the flow's shard (flow_stage and the
+// multi-GPU symmetric stage, gs_flow_stage_apply); *first: this stage also
+// forms the energy term (step 0, stage 0).
+int flow_epi(gs_flow* f, int stage, void* rec_in, void* rec_out, FwdEpi& e, bool& first) {
   GS_TRY(f->flags.ensure(64));
-  FwdEpi e;
   e.rec = rec_in;
   e.rec_out = rec_out;
   e.y = f->y.ptr;
@@ -427,13 +430,23 @@ int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
   e.step_dev = f->stepctr.as<int>();
   if (stage == flow_stages(f) - 1) e.step_inc = f->stepctr.as<int>();
   e.peers = f->peers;
-  const bool first = f->want_energy && f->steps_done == 0 && stage == 0;
+  first = f->want_energy && f->steps_done == 0 && stage == 0;
   if (first) {
     GS_TRY(f->epart.ensure(sizeof(double) * (f->shard_count / 128 + 8)));
     GS_TRY(f->dhdp0.ensure(sizeof(double) * 3 * f->shard_count));
     e.energy_part = f->epart.as<double>();
     e.dhdp_out = f->dhdp0.as<double>();
   }
+  return GS_OK;
+}
+
+int flow_stage(gs_flow* f, int stage, void* rec_in, void* rec_out) {
+  gs_ctx* c = f->ctx;
+  cudaStream_t st = c->stream;
+  if (!rec_in) rec_in = f->rec.ptr;
+  FwdEpi e;
+  bool first = false;
+  GS_TRY(flow_epi(f, stage, rec_in, rec_out, e, first));
   int blocks = 0;
   TimerInstall install(f->timer);
   const bool sorted = f->cfg.backend == GS_EXACT && f->prec == kF32 &&
@@ -879,6 +892,62 @@ gs_status gs_flow_set_shard(gs_flow* f, int64_t begin, int64_t count) {
 
 void* gs_flow_source_buffer(gs_flow* f) { return f ? f->rec.ptr : nullptr; }
 int64_t gs_flow_record_bytes(const gs_flow* f) { return f ? 2 * (int64_t)vec_bytes(f->prec) : 0; }
+
+gs_status gs_flow_set_pair_rows(gs_flow* f, int32_t rank, int32_t world, int32_t* enabled) {
+  if (!f || !enabled || world < 1 || rank < 0 || rank >= world) return bad_arg("bad rank / world");
+  if (!f->subs.empty()) return bad_arg("a multi-device flow shards itself");
+  const bool ok = f->cfg.backend == GS_EXACT && f->prec == kF32 &&
+                  !(f->cfg.flags & (GS_FLAG_EXACT_CUTOFF | GS_FLAG_EXACT_MORTON)) &&
+                  use_sym(kF32, (int)f->n, 0, (int)f->n, -1);
+  f->pair_rank = ok ? rank : -1;
+  f->pair_world = ok ? world : 0;
+  *enabled = ok ? 1 : 0;
+  return GS_OK;
+}
+
+gs_status gs_flow_stage_pairs(gs_flow* f, int32_t stage, void** partials) {
+  if (!f || !partials || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");
+  if (f->pair_rank < 0) return bad_arg("gs_flow_set_pair_rows has not enabled pair rows");
+  gs_ctx* c = f->ctx;
+  GS_TRY(f->part.ensure(sym_part_bytes((int)f->n)));
+  GS_TRY(f->pair_out.ensure(2 * sizeof(float4) * (size_t)f->n));
+  f->launches = 0;
+  TimerInstall install(f->timer);
+  kt_mark(0, c->stream);
+  rhs_sym_rows(f->rec.ptr, (int)f->n, f->kc, f->part.ptr, f->pair_out.ptr, f->pair_rank,
+               f->pair_world, c->stream);
+  kt_mark(0, c->stream);
+  GS_CUDA_OK(cudaGetLastError());
+  f->launches += 2;
+  *partials = f->pair_out.ptr;
+  return GS_OK;
+}
+
+gs_status gs_flow_stage_apply(gs_flow* f, int32_t stage, const void* parts, int32_t nparts) {
+  if (!f || !parts || nparts < 1 || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");
+  if (f->pair_rank < 0) return bad_arg("gs_flow_set_pair_rows has not enabled pair rows");
+  gs_ctx* c = f->ctx;
+  FwdEpi e;
+  bool first = false;
+  GS_TRY(flow_epi(f, stage, f->rec.ptr, nullptr, e, first));
+  e.S = nparts;
+  e.part = parts;
+  e.n_tgt = (int)f->shard_count;
+  e.tgt_begin = (int)f->shard_begin;
+  e.cp = 2.0;
+  e.cq = fwd_cq(kF32, f->kc);
+  int blocks = 0;
+  GS_TRY(fwd_epilogue(kF32, e, c->stream, &blocks));
+  f->launches = 1;
+  f->stats.direct_interactions += (uint64_t)f->n * (uint64_t)f->shard_count;
+  f->stats.traversal_queries += (uint64_t)f->shard_count;
+  if (first) {
+    f->have_energy_part = true;
+    f->energy_blocks = blocks;
+  }
+  if (stage == flow_stages(f) - 1) ++f->steps_done;
+  return GS_OK;
+}
 
 gs_status gs_flow_stage(gs_flow* f, int32_t stage) {
   if (!f || stage < 0 || stage >= flow_stages(f)) return bad_arg("bad stage");

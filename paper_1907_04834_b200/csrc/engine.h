@@ -120,6 +120,10 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt);
 int sym_tiles(int n);
 size_t sym_part_bytes(int n);
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st);
+// multi-GPU rows of the symmetric RHS: this rank's tile-pair rows into part
+// (T slots x n), folded per target into out (n x 2 float4); returns T
+int rhs_sym_rows(const void* rec, int n, const KernelConsts& kc, void* part, void* out, int rank,
+                 int world, cudaStream_t st);
 // FP64 symmetric RHS (k_rhs_sym_f64, diagonal groups folded into a running
 // sum): returns S = 1 (part holds the running sum first)
 bool use_sym_f64(int n, int tgt_begin, int n_tgt, int plan_tgt);

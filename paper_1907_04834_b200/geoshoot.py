@@ -680,3 +680,22 @@ class Flow:
 
     def stage(self, s: int):
         self.gs.check(self.gs.lib.gs_flow_stage(self.h, s))
+
+    # ---- multi-GPU symmetric exact stages (gs_flow_set_pair_rows) ------------
+    def set_pair_rows(self, rank: int, world: int) -> bool:
+        """Use this rank's rows of the symmetric tile-pair grid for the exact
+        RHS (False: the flow does not qualify; stage() stays the path)."""
+        en = C.c_int32()
+        self.gs.check(self.gs.lib.gs_flow_set_pair_rows(self.h, rank, world, C.byref(en)))
+        return bool(en.value)
+
+    def stage_pairs(self, s: int) -> int:
+        """This rank's rows for stage s, folded per target: device pointer to
+        n x 8 float32 partials {A.xyz, 0, B.xyz, 0} (valid until the next call)."""
+        ptr = C.c_void_p()
+        self.gs.check(self.gs.lib.gs_flow_stage_pairs(self.h, s, C.byref(ptr)))
+        return ptr.value or 0
+
+    def stage_apply(self, s: int, partials_ptr: int, nparts: int):
+        """The shard's stage epilogue over nparts partials [part][shard] x 8 float32."""
+        self.gs.check(self.gs.lib.gs_flow_stage_apply(self.h, s, C.c_void_p(partials_ptr), nparts))

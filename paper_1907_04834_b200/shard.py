@@ -134,6 +134,41 @@ class ShardedFlow:
         per = self._rec.numel() // flow.n
         self._mine = self._rec[self.begin * per:(self.begin + self.count) * per]
         self.collectives = 0
+        # exact FP32 flows that take the symmetric kernel: each rank evaluates
+        # its rows of the unordered tile-pair grid (both ends of every pair),
+        # folds them per target, and the ranks exchange the shard slices of
+        # those partials (all-to-all) before each shard's epilogue -- one
+        # extra collective per stage, half the pair arithmetic of the gather
+        # form
+        self.pairs = (self.world > 1 and hasattr(flow, "set_pair_rows")
+                      and flow.set_pair_rows(self.rank, self.world))
+        if self.pairs:
+            dev = self._rec.device
+            self._pair_out = torch.empty(self.world * self.count * 8, dtype=self._rec.dtype, device=dev)
+
+    def _pair_stage(self, s: int):
+        """One symmetric stage: this rank's pair rows, the all-to-all of the
+        per-target partials (rank r receives every rank's slice of its shard,
+        in rank order) and the shard's epilogue over the world partials."""
+        n = self.flow.n
+        if hasattr(self.flow, "stage_pairs_tensor"):  # CPU stand-in (tests)
+            inp = self.flow.stage_pairs_tensor(s)
+        else:
+            inp = torch.as_tensor(_CudaBuf(self.flow.stage_pairs(s), n * 32), device="cuda")
+        if hasattr(self.flow, "last_launches"):
+            self.launches += self.flow.last_launches()
+        if self.stream is not None:
+            with torch.cuda.stream(self.stream):
+                dist.all_to_all_single(self._pair_out, inp, group=self.group)
+        else:
+            dist.all_to_all_single(self._pair_out, inp, group=self.group)
+        self.collectives += 1
+        if hasattr(self.flow, "stage_apply_tensor"):
+            self.flow.stage_apply_tensor(s, self._pair_out, self.world)
+        else:
+            self.flow.stage_apply(s, self._pair_out.data_ptr(), self.world)
+            if hasattr(self.flow, "last_launches"):
+                self.launches += self.flow.last_launches()
 
     def _gather(self):
         if self.world == 1:
@@ -148,7 +183,10 @@ class ShardedFlow:
     def step(self, steps: int = 1):
         for _ in range(steps):
             for s in range(self.stages):
-                self.flow.stage(s)
-                if hasattr(self.flow, "last_launches"):
-                    self.launches += self.flow.last_launches()
+                if self.pairs:
+                    self._pair_stage(s)
+                else:
+                    self.flow.stage(s)
+                    if hasattr(self.flow, "last_launches"):
+                        self.launches += self.flow.last_launches()
                 self._gather()

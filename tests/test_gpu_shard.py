@@ -14,7 +14,7 @@ import pytest
 import torch
 
 from paper_1907_04834_b200 import BARNES_HUT, EXACT, F32, RK4, ShootingConfig
-from paper_1907_04834_b200.shard import records_view
+from paper_1907_04834_b200.shard import _CudaBuf, records_view
 from tests.util import rel_l2
 
 pytestmark = pytest.mark.gpu
@@ -76,3 +76,76 @@ def test_two_shards_equal_one_flow(gs, gather, backend):
             assert np.array_equal(gq, wq) and np.array_equal(gp, wp)
         else:  # same interaction sets; the group walk's summation order depends on the warp
             assert rel_l2(gq, wq) < 1e-6 and rel_l2(gp, wp) < 1e-5
+
+
+def _pair_shards(gs, q, p, cfg, world, steps):
+    """Symmetric multi-GPU stages emulated with `world` flows on one GPU: each
+    evaluates its rows of the tile-pair grid, the per-target partials are
+    exchanged as the all-to-all of shard.ShardedFlow would (rank r receives
+    every rank's slice of its shard, in rank order), each shard's epilogue
+    folds them, and the updated records are exchanged."""
+    n = len(q)
+    flows = [gs.flow(cfg, n) for _ in range(world)]
+    cnt = n // world
+    for r, f in enumerate(flows):
+        f.upload(q, p)
+        f.set_shard(r * cnt, cnt)
+        assert f.set_pair_rows(r, world)
+    recs = [records_view(f) for f in flows]
+    per = recs[0].numel() // n
+    outs = [torch.empty(world * cnt * 8, dtype=torch.float32, device="cuda") for _ in range(world)]
+    stages = 4 if cfg.integrator == RK4 else 1
+    for _ in range(steps):
+        for s in range(stages):
+            parts = []
+            for f in flows:
+                ptr = f.stage_pairs(s)
+                torch.cuda.synchronize()
+                parts.append(torch.as_tensor(_CudaBuf(ptr, n * 32), device="cuda").clone())
+            for r, f in enumerate(flows):
+                for w in range(world):
+                    outs[r][w * cnt * 8:(w + 1) * cnt * 8] = parts[w][r * cnt * 8:(r + 1) * cnt * 8]
+                torch.cuda.synchronize()
+                f.stage_apply(s, outs[r].data_ptr(), world)
+            torch.cuda.synchronize()
+            for r in range(world):
+                for w in range(world):
+                    if w != r:
+                        recs[w][r * cnt * per:(r + 1) * cnt * per] = recs[r][r * cnt * per:(r + 1) * cnt * per]
+            torch.cuda.synchronize()
+    for f in flows:
+        f.sync()
+    return [f.download() for f in flows]
+
+
+def test_pair_rows_shards_match_one_flow(gs):
+    """Symmetric multi-GPU stages (gs_flow_set_pair_rows): 1 rank is bitwise
+    the one-GPU symmetric flow (its fold takes every slot in slot order); 2 and
+    3 ranks (3: unequal row counts) equal it to FP32 rounding and are bitwise
+    repeatable."""
+    n = 60_000
+    rng = np.random.default_rng(78)
+    q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+    cfg = ShootingConfig(sigma=0.03, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    assert gs.exact_pairs_plan(n, F32) > 0
+    one = gs.flow(cfg, n)
+    one.upload(q, p)
+    one.advance(2)
+    one.sync()
+    wq, wp = one.download()
+    (aq, ap), = _pair_shards(gs, q, p, cfg, 1, 2)
+    assert np.array_equal(aq, wq) and np.array_equal(ap, wp)
+    for world in (2, 3):
+        got = _pair_shards(gs, q, p, cfg, world, 2)
+        again = _pair_shards(gs, q, p, cfg, world, 2)
+        for (gq, gp), (hq, hp) in zip(got, again):
+            assert np.array_equal(gq, hq) and np.array_equal(gp, hp)
+            assert rel_l2(gq, wq) < 1e-6 and rel_l2(gp, wp) < 1e-5
+
+
+def test_pair_rows_not_for_gather_problems(gs):
+    cfg = ShootingConfig(sigma=0.03, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    f = gs.flow(cfg, 20_000)  # below 40k points: the gather kernel
+    assert not f.set_pair_rows(0, 2)
+    fb = gs.flow(ShootingConfig(sigma=0.03, timesteps=10, backend=BARNES_HUT, precision=F32), 60_000)
+    assert not fb.set_pair_rows(0, 2)

@@ -48,6 +48,57 @@ class CpuFlow:
         return r[:, 0, :3].copy(), r[:, 1, :3].copy()
 
 
+class PairCpuFlow(CpuFlow):
+    """Stand-in for the symmetric multi-GPU stages (gs_flow_set_pair_rows):
+    tiles of 8 points, rank r evaluates the unordered tile pairs of its rows
+    (CTA (I, k), J = (I + k) mod T, k = 0..T/2, the even-T k = T/2 pairs by
+    I < T/2 only -- allpairs.cu k_rhs_sym_f32x2) for BOTH ends, folds them per
+    target, and the shard's epilogue folds the world partials it receives."""
+    TILE = 8
+
+    def set_pair_rows(self, rank, world):
+        self.rank, self.world = rank, world
+        return True
+
+    def stage_pairs_tensor(self, s):
+        r = self.rec.numpy().reshape(self.n, 2, 4)
+        q, p = r[:, 0, :3], r[:, 1, :3]
+        T = (self.n + self.TILE - 1) // self.TILE
+        ra, rb = T * self.rank // self.world, T * (self.rank + 1) // self.world
+        A, B = np.zeros((self.n, 3)), np.zeros((self.n, 3))
+        inv = 1.0 / (2 * self.sigma ** 2)
+
+        def add(ti, tj):  # targets of tile ti from sources of tile tj
+            a, b = slice(ti * self.TILE, (ti + 1) * self.TILE), slice(tj * self.TILE, (tj + 1) * self.TILE)
+            d = q[a][:, None, :] - q[b][None, :, :]
+            g = np.exp(-(d * d).sum(2) * inv)
+            A[a] += g @ p[b]
+            B[a] += ((p[a] @ p[b].T) * g)[:, :, None].__mul__(d).sum(1)
+
+        for I in range(ra, rb):
+            for k in range(T // 2 + 1):
+                if 2 * k == T and I >= k:
+                    continue
+                J = (I + k) % T
+                add(I, J)
+                if k:
+                    add(J, I)
+        out = np.zeros((self.n, 8))
+        out[:, :3], out[:, 4:7] = A, B
+        return torch.from_numpy(out.reshape(-1).copy())
+
+    def stage_apply_tensor(self, s, parts, world):
+        x = parts.numpy().reshape(world, self.count, 8)
+        A, B = x[0, :, :3].copy(), x[0, :, 4:7].copy()
+        for w in range(1, world):
+            A += x[w, :, :3]
+            B += x[w, :, 4:7]
+        r = self.rec.numpy().reshape(self.n, 2, 4)
+        sl = slice(self.begin, self.begin + self.count)
+        r[sl, 0, :3] += self.dt * 2.0 * A            # dH/dp = 2 sum g p
+        r[sl, 1, :3] -= self.dt * (-2.0 / self.sigma ** 2) * B  # dH/dq = -(2/s) sum c d
+
+
 def inputs():
     rng = np.random.default_rng(5)
     return rng.uniform(0, 2, (64, 3)), rng.uniform(-0.3, 0.3, (64, 3))
@@ -140,3 +191,37 @@ def test_two_rank_subjects_match_single_rank(tmp_path):
     assert [r["subject"] for r in want] == list(range(7))
     for r in range(2):
         assert np.array_equal(np.load(tmp_path / f"s{r}.npy"), flat)
+
+
+def pair_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q, p = inputs()
+    f = PairCpuFlow(q, p, 0.7, 0.1)
+    drv = ShardedFlow(f, stages=1)
+    assert drv.pairs
+    drv.step(5)
+    assert drv.collectives == 10  # all-to-all of the partials + all-gather of the records
+    fq, fp = f.state()
+    np.save(os.path.join(out, f"q{rank}.npy"), fq)
+    np.save(os.path.join(out, f"p{rank}.npy"), fp)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_pair_rows_gloo_match_single_rank(tmp_path, world):
+    """The symmetric multi-GPU stage logic (rows of the tile-pair grid, the
+    all-to-all of per-target partials, the shard epilogue) over gloo against
+    the unsharded reference-RHS flow: every unordered pair exactly once
+    (T = 8 tiles: even T, so the k = T/2 rule matters)."""
+    port = 29700 + world * 10 + os.getpid() % 500
+    mp.spawn(pair_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    q, p = inputs()
+    f = CpuFlow(q, p, 0.7, 0.1)
+    for _ in range(5):
+        f.stage(0)
+    wq, wp = f.state()
+    for r in range(world):
+        assert np.allclose(np.load(tmp_path / f"q{r}.npy"), wq, rtol=0, atol=1e-12)
+        assert np.allclose(np.load(tmp_path / f"p{r}.npy"), wp, rtol=0, atol=1e-12)
