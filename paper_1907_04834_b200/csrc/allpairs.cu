@@ -259,15 +259,32 @@ __global__ void __launch_bounds__(NT, MINB) k_rhs_f32x2(const float4* __restrict
 template <int TPT, int NT, int MINB, int SB, int SYM_UNR = GS_SYM_UNR>
 __global__ void __launch_bounds__(NT, MINB)
     k_rhs_sym_f32x2(const float4* __restrict__ rec, int n, int T, float kap, float kc0x,
-                    float kc0y, float kc0z, float4* __restrict__ part, int row0 = 0) {
+                    float kc0y, float kc0z, float4* __restrict__ part, int row0 = 0,
+                    int k0 = -1) {
   constexpr int TP = TPT / 2, TILE = NT * TPT, NW = NT / 32;
   static_assert(TILE % SB == 0 && SB % 32 == 0 && TPT % 2 == 0, "tile shape");
   __shared__ float4 sq[SB];
   __shared__ float4 sp[SB];
   __shared__ float2 sj[NW][3][SB];
-  const int I = row0 + blockIdx.x, k = blockIdx.y;  // row0: multi-GPU rows (rhs_sym_rows)
-  if (2 * k == T && I >= k) return;  // even T: the pair {I, I + T/2} once
+  // row0: multi-GPU rows (rhs_sym_rows). k0 >= 0: diagonal group [k0, k0 +
+  // gridDim.y) of a problem whose T tile slots would not fit (rhs_sym_partials):
+  // the i side goes to slot 2(k - k0), the j side to 2(k - k0) + 1 (the
+  // layout of k_rhs_sym_f64), folded into a running sum by k_fold_group_f32
+  const int I = row0 + blockIdx.x, k = (k0 < 0 ? 0 : k0) + blockIdx.y;
   const int J = I + k < T ? I + k : I + k - T;
+  const size_t slot_i = k0 < 0 ? (size_t)J : (size_t)(2 * (k - k0));
+  const size_t slot_j = k0 < 0 ? (size_t)I : (size_t)(2 * (k - k0) + 1);
+  if (2 * k == T && I >= k) {  // even T: the pair {I, I + T/2} once
+    if (k0 >= 0) {  // grouped: zeros in the two slots this CTA leaves empty
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = threadIdx.x; u < TILE; u += NT) {
+        const int t = I * TILE + u, j = J * TILE + u;
+        if (t < n) part[2 * (slot_i * n + t)] = part[2 * (slot_i * n + t) + 1] = z;
+        if (j < n) part[2 * (slot_j * n + j)] = part[2 * (slot_j * n + j) + 1] = z;
+      }
+    }
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
   f2 ax[TP], ay[TP], az[TP], bx[TP], by[TP], bz[TP];
@@ -407,7 +424,7 @@ __global__ void __launch_bounds__(NT, MINB)
           const float2 t0 = sj[w][0][u], t1 = sj[w][1][u], t2 = sj[w][2][u];
           s0.x += t0.x; s0.y += t0.y; s1.x += t1.x; s1.y += t1.y; s2.x += t2.x; s2.y += t2.y;
         }
-        float4* o = part + 2 * ((size_t)I * n + j);
+        float4* o = part + 2 * (slot_j * n + j);
         o[0] = make_float4(s0.x, s0.y, s1.x, 0.f);
         o[1] = make_float4(-s1.y, -s2.x, -s2.y, 0.f);
       }
@@ -423,12 +440,32 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int h = 0; h < 2; ++h) {
       const int t = tb + (2 * kk + h) * NT;
       if (t < n) {
-        float4* o = part + 2 * ((size_t)J * n + t);
+        float4* o = part + 2 * (slot_i * n + t);
         o[0] = make_float4(a0[h][0], a0[h][1], a0[h][2], 0.f);
         o[1] = make_float4(b0[h][0], b0[h][1], b0[h][2], 0.f);
+        if (k0 >= 0 && k == 0) {  // grouped diagonal: its j slot is zero
+          float4* z = part + 2 * (slot_j * n + t);
+          z[0] = z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
   }
+}
+
+// acc[t] (+)= sum over a diagonal group's S slots of part[s][t], in slot order
+__global__ void k_fold_group_f32(const float4* __restrict__ part, int S, int n, int first,
+                                 float4* __restrict__ acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[2 * t];
+  float4 b = first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[2 * t + 1];
+  for (int s = 0; s < S; ++s) {
+    const float4 x = part[2 * ((size_t)s * n + t)], y = part[2 * ((size_t)s * n + t) + 1];
+    a.x += x.x; a.y += x.y; a.z += x.z;
+    b.x += y.x; b.y += y.y; b.z += y.z;
+  }
+  acc[2 * t] = a;
+  acc[2 * t + 1] = b;
 }
 
 // ---- exact RHS in Morton order with the FP32 underflow cutoff -----------------
@@ -1607,15 +1644,35 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
   if (prec != kF32 || tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
   const int mode = exact_pairs_mode();
   if (mode == 1) return false;
-  const long T = sym_tiles(n);
-  // partial buffer: T slots x n targets x 32 B
-  if ((double)T * n * 32.0 > 24e9) return false;
+  // (problems whose T slots x n x 32 B exceed kSymSlotBudget run in
+  // diagonal groups folded into a running sum: rhs_sym_partials)
   if (mode == 2) return true;
   // by size: enough tile pairs for many waves (T(T+1)/2 CTAs)
   return n >= 40000;
 }
 
-size_t sym_part_bytes(int n) { return (size_t)sym_tiles(n) * (size_t)n * 2 * sizeof(float4); }
+// One slot per tile up to kSymSlotBudget bytes of partials (1M points: 10.4
+// GB); above it (from ~1.5M points) the diagonals run in groups of
+// kSymGroup, each folded into a running sum (2 x kSymGroup slots + the sum).
+constexpr double kSymSlotBudget = 24e9;
+constexpr int kSymGroup = 32;
+
+bool sym_grouped(int n) {
+  static const double budget = [] {  // GS_SYM_SLOT_BUDGET: test hook (bytes)
+    const char* e = std::getenv("GS_SYM_SLOT_BUDGET");
+    return e ? std::atof(e) : kSymSlotBudget;
+  }();
+  return (double)sym_tiles(n) * n * 32.0 > budget;
+}
+
+size_t sym_part_bytes(int n) {
+  const size_t slots = sym_grouped(n) ? 1 + 2 * kSymGroup : sym_tiles(n);
+  return slots * (size_t)n * 2 * sizeof(float4);
+}
+
+int sym_launches(int n) {
+  return sym_grouped(n) ? 2 * ((sym_tiles(n) / 2 + 1 + kSymGroup - 1) / kSymGroup) : 1;
+}
 
 // Multi-GPU symmetric RHS: rank r of G evaluates the tile-pair
 // rows I in [T r / G, T (r+1) / G) -- every unordered tile pair belongs to
@@ -1671,16 +1728,32 @@ int rhs_sym_rows(const void* rec, int n, const KernelConsts& kc, void* part, voi
 
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st) {
   const int T = sym_tiles(n);
-  const dim3 grid((unsigned)T, (unsigned)(T / 2 + 1), 1);
   const float kap = (float)kc.kappa, a = (float)(kc.kappa * kc.c0[0]),
               b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
   const float4* r = (const float4*)rec;
-  float4* o = (float4*)part;
-  if (sym_variant(n) == 0)
-    k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o);
-  else
-    k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o);
-  return T;
+  const bool big = sym_variant(n) == 0;
+  if (!sym_grouped(n)) {
+    const dim3 grid((unsigned)T, (unsigned)(T / 2 + 1), 1);
+    float4* o = (float4*)part;
+    if (big)
+      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o);
+    else
+      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o);
+    return T;
+  }
+  float4* acc = (float4*)part;
+  float4* slots = acc + 2 * (size_t)n;
+  const int kend = T / 2 + 1;
+  for (int k0 = 0; k0 < kend; k0 += kSymGroup) {
+    const int k1 = std::min(kend, k0 + kSymGroup);
+    const dim3 grid((unsigned)T, (unsigned)(k1 - k0), 1);
+    if (big)
+      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, slots, 0, k0);
+    else
+      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, slots, 0, k0);
+    k_fold_group_f32<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);
+  }
+  return 1;  // the epilogue reads the running sum as a single partial
 }
 
 // Symmetric FP64 RHS (k_rhs_sym_f64): 1024-point tiles (4 targets x 256

@@ -380,7 +380,7 @@ int exact_stage(const Device& dev, int prec, const KernelConsts& kc, const void*
   e.cp = 2.0;
   e.cq = fwd_cq(prec, kc);
   GS_TRY(fwd_epilogue(prec, e, st, energy_blocks));
-  if (launches) *launches += sym64 ? 1 + sym_f64_launches((int)n) : 2;
+  if (launches) *launches += sym64 ? 1 + sym_f64_launches((int)n) : sym ? 1 + sym_launches((int)n) : 2;
   return GS_OK;
 }
 
@@ -898,7 +898,7 @@ gs_status gs_flow_set_pair_rows(gs_flow* f, int32_t rank, int32_t world, int32_t
   if (!f->subs.empty()) return bad_arg("a multi-device flow shards itself");
   const bool ok = f->cfg.backend == GS_EXACT && f->prec == kF32 &&
                   !(f->cfg.flags & (GS_FLAG_EXACT_CUTOFF | GS_FLAG_EXACT_MORTON)) &&
-                  use_sym(kF32, (int)f->n, 0, (int)f->n, -1);
+                  use_sym(kF32, (int)f->n, 0, (int)f->n, -1) && !sym_grouped((int)f->n);
   f->pair_rank = ok ? rank : -1;
   f->pair_world = ok ? world : 0;
   *enabled = ok ? 1 : 0;

@@ -119,6 +119,8 @@ void set_exact_pairs(int mode);
 bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt);
 int sym_tiles(int n);
 size_t sym_part_bytes(int n);
+bool sym_grouped(int n);  // diagonal groups + running sum (slots over budget)
+int sym_launches(int n);
 int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part, cudaStream_t st);
 // multi-GPU rows of the symmetric RHS: this rank's tile-pair rows into part
 // (T slots x n), folded per target into out (n x 2 float4); returns T

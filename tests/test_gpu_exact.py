@@ -384,3 +384,46 @@ def test_symmetric_rhs_f64_groups_equal_gather(gs, pairs):
     assert gs.exact_pairs_plan(n, F64) == 0
     _, gp, gq = gs.hamiltonian_with_gradients(q, p, 0.03)
     assert rel_l2(dp, gp) < 1e-13 and rel_l2(dq, gq) < 1e-12
+
+
+_GROUPED = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1907_04834_b200 import F32, Geoshoot
+gs = Geoshoot(0)
+n = 100_000
+rng = np.random.default_rng(100)
+q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+out = []
+for mode in (2, 2, 1):
+    gs.set_exact_pairs(mode)
+    out.append(gs.hamiltonian_with_gradients(q, p, 0.02, precision=F32)[1:])
+np.savez(sys.argv[2], a0=out[0][0], a1=out[0][1], b0=out[1][0], b1=out[1][1], g0=out[2][0], g1=out[2][1])
+"""
+
+
+@pytest.mark.parametrize("budget", ["1e6", ""])
+def test_symmetric_grouped_diagonals(tmp_path, budget):
+    """Problems whose tile slots exceed the partial budget (from ~1.5M points)
+    run the symmetric kernel in diagonal groups of 32 folded into a running
+    sum. GS_SYM_SLOT_BUDGET (read once per process, hence a subprocess) forces
+    it at 100k points: 66 tiles, 34 diagonals in two groups, even T. Against
+    the one-slot-per-tile run and the gather kernel: FP32 rounding; repeatable."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    if budget:
+        env["GS_SYM_SLOT_BUDGET"] = budget
+    f = tmp_path / f"g{budget or 'std'}.npz"
+    subprocess.run([sys.executable, "-c", _GROUPED, root, str(f)], env=env, check=True, timeout=600)
+    d = np.load(f)
+    assert np.array_equal(d["a0"], d["b0"]) and np.array_equal(d["a1"], d["b1"])
+    assert rel_l2(d["a0"], d["g0"]) < 2e-6 and rel_l2(d["a1"], d["g1"]) < 2e-6
+    if budget:
+        std = tmp_path / "std.npz"
+        subprocess.run([sys.executable, "-c", _GROUPED, root, str(std)], check=True, timeout=600)
+        s = np.load(std)
+        assert not np.array_equal(d["a1"], s["a1"])  # a different (grouped) summation really ran
+        assert rel_l2(d["a0"], s["a0"]) < 2e-6 and rel_l2(d["a1"], s["a1"]) < 2e-6
