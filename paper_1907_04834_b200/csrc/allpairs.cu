@@ -452,6 +452,22 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 }
 
+// acc[t] (+)= sum over a diagonal group's S slots of part[s][t] (4 float4 per
+// target: the Hessian products), in slot order
+__global__ void k_fold_group4_f32(const float4* __restrict__ part, int S, int n, int first,
+                                  float4* __restrict__ acc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  for (int c = 0; c < 4; ++c) {
+    float4 a = first ? make_float4(0.f, 0.f, 0.f, 0.f) : acc[4 * t + c];
+    for (int s = 0; s < S; ++s) {
+      const float4 x = part[4 * ((size_t)s * n + t) + c];
+      a.x += x.x; a.y += x.y; a.z += x.z;
+    }
+    acc[4 * t + c] = a;
+  }
+}
+
 // acc[t] (+)= sum over a diagonal group's S slots of part[s][t], in slot order
 __global__ void k_fold_group_f32(const float4* __restrict__ part, int S, int n, int first,
                                  float4* __restrict__ acc) {
@@ -747,14 +763,29 @@ template <int TPT, int NT, int MINB, int SB>
 __global__ void __launch_bounds__(NT, MINB)
     k_hess_sym_f32x2(const float4* __restrict__ rec, const float4* __restrict__ adj, int n,
                      int T, float kap, float kc0x, float kc0y, float kc0z, float c1,
-                     float4* __restrict__ part) {
+                     float4* __restrict__ part, int k0 = -1) {
   constexpr int TP = TPT / 2, TILE = NT * TPT, NW = NT / 32;
   static_assert(TILE % SB == 0 && SB % 32 == 0 && TPT % 2 == 0, "tile shape");
   __shared__ float4 sq[SB], sp[SB], sa[SB], sb[SB];
   __shared__ float4 sj[NW][3][SB];
-  const int I = blockIdx.x, k = blockIdx.y;
-  if (2 * k == T && I >= k) return;  // even T: the pair {I, I + T/2} once
+  // k0 >= 0: diagonal group (slots 2(k - k0) / 2(k - k0) + 1), as k_rhs_sym_f32x2
+  const int I = blockIdx.x, k = (k0 < 0 ? 0 : k0) + blockIdx.y;
   const int J = I + k < T ? I + k : I + k - T;
+  const size_t slot_i = k0 < 0 ? (size_t)J : (size_t)(2 * (k - k0));
+  const size_t slot_j = k0 < 0 ? (size_t)I : (size_t)(2 * (k - k0) + 1);
+  if (2 * k == T && I >= k) {  // even T: the pair {I, I + T/2} once
+    if (k0 >= 0) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = threadIdx.x; u < TILE; u += NT) {
+        const int t = I * TILE + u, j = J * TILE + u;
+        for (int c = 0; c < 4; ++c) {
+          if (t < n) part[4 * (slot_i * n + t) + c] = z;
+          if (j < n) part[4 * (slot_j * n + j) + c] = z;
+        }
+      }
+    }
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   f2 qx[TP], qy[TP], qz[TP], px[TP], py[TP], pz[TP];
   f2 ix[TP], iy[TP], iz[TP], jx[TP], jy[TP], jz[TP];  // alpha_i, beta_i
@@ -876,7 +907,7 @@ __global__ void __launch_bounds__(NT, MINB)
           s2.x += t2.x; s2.y += t2.y; s2.z += t2.z; s2.w += t2.w;
         }
         // (Apq, App, Aqq, Aqp') of j = (-J0..2, J3..5, -J6..8, -J9..11)
-        float4* o = part + 4 * ((size_t)I * n + j);
+        float4* o = part + 4 * (slot_j * n + j);
         o[0] = make_float4(-s0.x, -s0.y, -s0.z, 0.f);
         o[1] = make_float4(s0.w, s1.x, s1.y, 0.f);
         o[2] = make_float4(-s1.z, -s1.w, -s2.x, 0.f);
@@ -894,7 +925,9 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int h = 0; h < 2; ++h) {
       const int t = tb + (2 * kk + h) * NT;
       if (t < n) {
-        float4* o = part + 4 * ((size_t)J * n + t);
+        float4* o = part + 4 * (slot_i * n + t);
+        if (k0 >= 0 && k == 0)  // grouped diagonal: its j slot is zero
+          for (int c = 0; c < 4; ++c) part[4 * (slot_j * n + t) + c] = make_float4(0.f, 0.f, 0.f, 0.f);
         o[0] = make_float4(v[h][0], v[h][1], v[h][2], 0.f);
         o[1] = make_float4(v[h][3], v[h][4], v[h][5], 0.f);
         o[2] = make_float4(v[h][6], v[h][7], v[h][8], 0.f);
@@ -1657,13 +1690,15 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
 constexpr double kSymSlotBudget = 24e9;
 constexpr int kSymGroup = 32;
 
-bool sym_grouped(int n) {
+static double sym_slot_budget() {
   static const double budget = [] {  // GS_SYM_SLOT_BUDGET: test hook (bytes)
     const char* e = std::getenv("GS_SYM_SLOT_BUDGET");
     return e ? std::atof(e) : kSymSlotBudget;
   }();
-  return (double)sym_tiles(n) * n * 32.0 > budget;
+  return budget;
 }
+
+bool sym_grouped(int n) { return (double)sym_tiles(n) * n * 32.0 > sym_slot_budget(); }
 
 size_t sym_part_bytes(int n) {
   const size_t slots = sym_grouped(n) ? 1 + 2 * kSymGroup : sym_tiles(n);
@@ -1799,13 +1834,17 @@ static bool use_sym_hess(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt
   if (prec != kF32 || tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
   const int mode = exact_pairs_mode();
   if (mode == 1) return false;
-  if ((double)hess_sym_tiles(n) * n * 64.0 > 24e9) return false;
   return mode == 2 || n >= 40000;
 }
 
+// slots over the budget: diagonal groups folded into a running sum (as the RHS)
+static bool hess_sym_grouped(int n) { return (double)hess_sym_tiles(n) * n * 64.0 > sym_slot_budget(); }
+constexpr int kHessSymGroup = 16;
+
 size_t hess_part_bytes(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
   if (use_sym_hess(prec, n, tgt_begin, n_tgt, plan_tgt))
-    return (size_t)hess_sym_tiles(n) * (size_t)n * 4 * sizeof(float4);
+    return (size_t)(hess_sym_grouped(n) ? 1 + 2 * kHessSymGroup : hess_sym_tiles(n)) * (size_t)n *
+           4 * sizeof(float4);
   return (size_t)kMaxChunks * 4 * vec_bytes(prec) * (size_t)std::max(n_tgt, 1);
 }
 
@@ -1817,10 +1856,23 @@ int hess_partials(const Device& dev, int prec, const void* rec, const void* adj,
     const int T = hess_sym_tiles(n);
     const float kap = (float)kc.kappa;
     const float c1 = (float)(1.0 / (kc.kappa * kc.kappa * kc.s));
-    k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(T / 2 + 1)), 128, 0, st>>>(
-        (const float4*)rec, (const float4*)adj, n, T, kap, (float)(kc.kappa * kc.c0[0]),
-        (float)(kc.kappa * kc.c0[1]), (float)(kc.kappa * kc.c0[2]), c1, (float4*)part);
-    return T;
+    const float a = (float)(kc.kappa * kc.c0[0]), b = (float)(kc.kappa * kc.c0[1]),
+                c = (float)(kc.kappa * kc.c0[2]);
+    if (!hess_sym_grouped(n)) {
+      k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(T / 2 + 1)), 128, 0, st>>>(
+          (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, (float4*)part);
+      return T;
+    }
+    float4* acc = (float4*)part;
+    float4* slots = acc + 4 * (size_t)n;
+    const int kend = T / 2 + 1;
+    for (int k0 = 0; k0 < kend; k0 += kHessSymGroup) {
+      const int k1 = std::min(kend, k0 + kHessSymGroup);
+      k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 128, 0, st>>>(
+          (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, slots, k0);
+      k_fold_group4_f32<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);
+    }
+    return 1;
   }
   const int real_tgt = n_tgt;
   if (plan_tgt > 0) n_tgt = plan_tgt;

@@ -394,11 +394,14 @@ gs = Geoshoot(0)
 n = 100_000
 rng = np.random.default_rng(100)
 q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
-out = []
+out, hp = [], []
+a, b = rng.normal(0, 1, (n, 3)), rng.normal(0, 1, (n, 3))
 for mode in (2, 2, 1):
     gs.set_exact_pairs(mode)
     out.append(gs.hamiltonian_with_gradients(q, p, 0.02, precision=F32)[1:])
-np.savez(sys.argv[2], a0=out[0][0], a1=out[0][1], b0=out[1][0], b1=out[1][1], g0=out[2][0], g1=out[2][1])
+    hp.append(np.concatenate(gs.hessian_products(q, p, a, b, 0.02, precision=F32)))
+np.savez(sys.argv[2], a0=out[0][0], a1=out[0][1], b0=out[1][0], b1=out[1][1], g0=out[2][0], g1=out[2][1],
+         h0=hp[0], h1=hp[1], hg=hp[2])
 """
 
 
@@ -421,9 +424,14 @@ def test_symmetric_grouped_diagonals(tmp_path, budget):
     d = np.load(f)
     assert np.array_equal(d["a0"], d["b0"]) and np.array_equal(d["a1"], d["b1"])
     assert rel_l2(d["a0"], d["g0"]) < 2e-6 and rel_l2(d["a1"], d["g1"]) < 2e-6
+    # Hessian products (768-point tiles: 131 tiles, 66 diagonals in 5 groups of 16)
+    assert np.array_equal(d["h0"], d["h1"])
+    assert rel_l2(d["h0"], d["hg"]) < 4e-6
     if budget:
         std = tmp_path / "std.npz"
         subprocess.run([sys.executable, "-c", _GROUPED, root, str(std)], check=True, timeout=600)
         s = np.load(std)
         assert not np.array_equal(d["a1"], s["a1"])  # a different (grouped) summation really ran
+        assert not np.array_equal(d["h0"], s["h0"])
+        assert rel_l2(d["h0"], s["h0"]) < 4e-6
         assert rel_l2(d["a0"], s["a0"]) < 2e-6 and rel_l2(d["a1"], s["a1"]) < 2e-6
