@@ -288,7 +288,7 @@ def pairs(gs):
 
 # 1536-point tiles below 150k points: one tile (diagonal only), 4 tiles (even
 # T: the k = T/2 pairs taken once), 5 tiles (odd T), ragged last tiles
-@pytest.mark.parametrize("n", [700, 1536 * 3 + 17, 1536 * 4 + 5])
+@pytest.mark.parametrize("n", [1, 2, 700, 1537, 1536 * 3 + 17, 1536 * 4 + 5])
 def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
     """Every unordered pair evaluated once and fed to both ends, as the
     reference's i < j sweep (kernel_exact.cpp:29-61): FP32 RHS to 1e-5 of the
@@ -327,7 +327,7 @@ def test_exact_pairs_choice_is_validated(gs):
 
 
 # 768-point tiles: one tile, 4 tiles (even T), 5 tiles (odd T), ragged
-@pytest.mark.parametrize("n", [300, 768 * 3 + 11, 768 * 4 + 3])
+@pytest.mark.parametrize("n", [1, 300, 769, 768 * 3 + 11, 768 * 4 + 3])
 def test_symmetric_hessian_products_match_reference(gs, ref, pairs, n):
     """k_hess_sym_f32x2: each unordered pair once, the j terms by symmetry
     (d -> -d, db -> -db), against the reference's hessian_products
@@ -359,7 +359,7 @@ def test_symmetric_evaluate_matches_reference(gs, ref, pairs):
 
 
 # FP64: 1024-point tiles, diagonals in groups of 32 folded into a running sum
-@pytest.mark.parametrize("n", [300, 1024 * 3 + 17, 1024 * 4 + 5])
+@pytest.mark.parametrize("n", [1, 300, 1025, 1024 * 3 + 17, 1024 * 4 + 5])
 def test_symmetric_rhs_f64_matches_reference(gs, ref, pairs, n):
     q, p = uniform(n, 10.0, seed=n + 7), sym_uniform(n, 1.0, seed=n + 8)
     pairs(2)
