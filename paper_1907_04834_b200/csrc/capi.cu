@@ -115,7 +115,7 @@ struct gs_flow {
   // multi-GPU symmetric exact stages (gs_flow_set_pair_rows): this rank's
   // tile-pair rows, and its per-target fold of them (n x 2 float4)
   int pair_rank = -1, pair_world = 0;
-  DBuf pair_out;
+  DBuf pair_out, pair_in;  // (pair_in: a multi-device shard's gathered partials)
   // CUDA graph of one integrator step (all stages + the step-counter bump),
   // captured after the first eager step and replayed for the following ones
   DBuf stepctr;
@@ -2026,16 +2026,83 @@ int multi_flow_upload(gs_flow* f, const double* q0, const double* p0) {
   return GS_OK;
 }
 
+// One symmetric exact stage across the devices (pair rows):
+// every device evaluates its rows of the tile-pair grid and folds them per
+// target; each shard then peer-copies the G partials of its targets (device
+// order) and runs its epilogue over them, storing its records into every
+// peer's next buffer as in the gather path.
+int multi_pair_stage(gs_flow* f, int stage, const std::vector<void*>& next) {
+  gs_ctx* c = f->ctx;
+  const int G = (int)f->subs.size();
+  const int n = (int)f->n;
+  const size_t rb = 2 * vec_bytes(f->prec), pb = 2 * sizeof(float4);
+  GS_TRY(multi_wait_all(c));
+  for (int d = 0; d < G; ++d) {
+    gs_flow* s = f->subs[d];
+    DevGuard g(sub_dev(s));
+    GS_TRY(s->part.ensure(sym_part_bytes(n)));
+    GS_TRY(s->pair_out.ensure(pb * n));
+    GS_TRY(s->pair_in.ensure(pb * G * std::max<int64_t>(s->shard_count, 1)));
+    TimerInstall install(s->timer);
+    kt_mark(0, s->ctx->stream);
+    rhs_sym_rows(s->rec.ptr, n, s->kc, s->part.ptr, s->pair_out.ptr, d, G, s->ctx->stream);
+    kt_mark(0, s->ctx->stream);
+    GS_CUDA_OK(cudaGetLastError());
+    s->launches += 2;
+    GS_TRY(multi_record(c, d));
+  }
+  GS_TRY(multi_wait_all(c));
+  for (int d = 0; d < G; ++d) {
+    gs_flow* s = f->subs[d];
+    DevGuard g(sub_dev(s));
+    cudaStream_t st = s->ctx->stream;
+    for (int o = 0; o < G; ++o)
+      GS_CUDA_OK(cudaMemcpyPeerAsync(s->pair_in.as<char>() + pb * o * s->shard_count, sub_dev(s),
+                                     f->subs[o]->pair_out.as<char>() + pb * s->shard_begin,
+                                     sub_dev(f->subs[o]), pb * s->shard_count, st));
+    FwdEpi e;
+    bool first = false;
+    GS_TRY(flow_epi(s, stage, s->rec.ptr, s->rec_next.ptr, e, first));
+    e.peers = peer_bufs(c, next, d);
+    e.S = G;
+    e.part = s->pair_in.ptr;
+    e.n_tgt = (int)s->shard_count;
+    e.tgt_begin = (int)s->shard_begin;
+    e.cp = 2.0;
+    e.cq = fwd_cq(kF32, s->kc);
+    int blocks = 0;
+    GS_TRY(fwd_epilogue(kF32, e, st, &blocks));
+    s->launches += 1;
+    s->stats.direct_interactions += (uint64_t)n * (uint64_t)s->shard_count;
+    s->stats.traversal_queries += (uint64_t)s->shard_count;
+    if (first) {
+      s->have_energy_part = true;
+      s->energy_blocks = blocks;
+    }
+    GS_TRY(peer_copies(c, next, d, rb * s->shard_begin, rb * s->shard_count));
+    GS_TRY(multi_record(c, d));
+  }
+  return GS_OK;
+}
+
+bool multi_pairs(const gs_flow* f) {
+  return f->subs.size() > 1 && f->cfg.backend == GS_EXACT && f->prec == kF32 &&
+         !(f->cfg.flags & (GS_FLAG_EXACT_CUTOFF | GS_FLAG_EXACT_MORTON)) &&
+         use_sym(kF32, (int)f->n, 0, (int)f->n, -1) && !sym_grouped((int)f->n);
+}
+
 int multi_flow_advance(gs_flow* f, int steps) {
   gs_ctx* c = f->ctx;
   const int G = (int)f->subs.size();
   const size_t rb = 2 * vec_bytes(f->prec);
+  const bool pairs = multi_pairs(f);
   for (int k = 0; k < steps; ++k) {
     for (int stage = 0; stage < flow_stages(f); ++stage) {
       GS_TRY(multi_wait_all(c));  // the previous stage of every shard is in every buffer
       std::vector<void*> next(G);
       for (int d = 0; d < G; ++d) next[d] = f->subs[d]->rec_next.ptr;
-      for (int d = 0; d < G; ++d) {
+      if (pairs) GS_TRY(multi_pair_stage(f, stage, next));
+      for (int d = 0; d < G && !pairs; ++d) {
         gs_flow* s = f->subs[d];
         DevGuard g(sub_dev(s));
         s->peers = peer_bufs(c, next, d);

@@ -46,6 +46,26 @@ def test_multi_context_reports_devices(multi):
     assert multi.peer_stores
 
 
+def test_exact_pair_rows_match_one_device(gs, multi):
+    """From 40k points one device takes the symmetric kernel; a multi-device
+    flow then runs pair rows (each device its rows of the tile-pair grid,
+    partials peer-copied to the shard owners, capi.cu multi_pair_stage): equal
+    to the one-device flow to FP32 rounding, bitwise repeatable."""
+    n = 60_001  # unequal shards
+    q, p = cube(n, 6)
+    p = p * 1e-2  # momenta of config 4's scale: a well-conditioned flow (at 1e-2 and
+    #               sigma 0.03 this one is chaotic: even FP64 vs FP32 differ by 1-10 %)
+    cfg = ShootingConfig(sigma=0.03, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    assert gs.exact_pairs_plan(n, F32) > 0
+    wq, wp, we, wst = gs.shoot_forward(q, p, cfg, keep_trajectory=False)
+    gq, gp, ge, gst = multi.shoot_forward(q, p, cfg, keep_trajectory=False)
+    hq, hp, he, _ = multi.shoot_forward(q, p, cfg, keep_trajectory=False)
+    assert np.array_equal(gq, hq) and np.array_equal(gp, hp) and ge == he
+    assert rel_l2(gq, wq) < 1e-6 and rel_l2(gp, wp) < 1e-5
+    assert ge == pytest.approx(we, rel=1e-6)
+    assert gst["direct_interactions"] == wst["direct_interactions"]
+
+
 @pytest.mark.parametrize("prec,integ", [(F32, RK4), (F64, EULER), (F32, EULER)])
 def test_exact_shoot_forward_bitwise_equals_one_device(gs, multi, prec, integ):
     n = 20_001  # not divisible by the shard count
