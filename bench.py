@@ -306,6 +306,11 @@ def run_ours(args):
                                   f"{pairs_per_launch:.3e} ordered pairs x 16 FP32 + 1 MUFU",
         # the same time against the gather formulation's ceiling (16 FP32 per ordered pair)
         "frac_of_gather_ceiling": achieved / (mb["ffma"] / RHS_FP32_PER_PAIR / 1e9),
+        "traffic_note": ("FMA-pipe bound: the algorithmic bytes are the 32-B records (32 MB at 1M); "
+                         "the rest is the tile-slot partials the symmetric kernel writes by design "
+                         "(T slots x N x 32 B, read once by the stage epilogue) -- "
+                         f"{(traffic or 0) / (k_ms * 1e-3) / 1e9:.0f} GB/s during the kernel")
+                        if tiles else None,
     }
     line = {
         "metric": METRIC, "value": value, "unit": "flow steps/s", "n_gpus": world,
