@@ -1321,6 +1321,79 @@ __global__ void __launch_bounds__(NT) k_hess_f64(const double4* __restrict__ rec
 // (exact_velocity, kernel_exact.cpp:70-82; warp, shooting.cpp:288-294).
 // 9 FP32 + 1 SFU per pair. Eval points: records of (x, unused).
 // ----------------------------------------------------------------------------
+// Packed variant of k_vel_f32 (exact_velocity / the dense warp): TPT
+// evaluation points per thread as TPT/2 register pairs; per two (point,
+// source) pairs 3 FADD2 + FMUL2 + 2 FFMA2 (-r^2) + 2 MUFU + 3 FFMA2 (sum g p)
+// = 9 packed + 2 MUFU issue slots (scalar: 20): FMA-pipe bound at 9 FP32 per
+// pair instead of issue bound at 10 instructions per pair.
+template <int TPT, int NT>
+__global__ void __launch_bounds__(NT) k_vel_f32x2(const float4* __restrict__ rec, int n,
+                                                  const float4* __restrict__ ev, int m, int chunk,
+                                                  float kap, float kc0x, float kc0y, float kc0z,
+                                                  float4* __restrict__ part) {
+  constexpr int TP = TPT / 2;
+  __shared__ float4 sq[kTile], sp[kTile];
+  f2 qx[TP], qy[TP], qz[TP], ax[TP], ay[TP], az[TP];
+  const int tb = blockIdx.x * NT * TPT + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float4 x[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      x[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < m) x[h] = ev[2 * t];
+      x[h] = make_float4(fmaf(kap, x[h].x, -kc0x), fmaf(kap, x[h].y, -kc0y), fmaf(kap, x[h].z, -kc0z), 0.f);
+    }
+    qx[k] = pk2(x[0].x, x[1].x); qy[k] = pk2(x[0].y, x[1].y); qz[k] = pk2(x[0].z, x[1].z);
+    ax[k] = ay[k] = az[k] = pk2(0.f, 0.f);
+  }
+  const int j0 = blockIdx.y * chunk;
+  const int j1 = min(n, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTile) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < kTile; u += NT) {
+      const int j = jt + u;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f), p = q;
+      if (j < j1) {
+        q = rec[2 * j]; p = rec[2 * j + 1];
+        q = make_float4(fmaf(kap, q.x, -kc0x), fmaf(kap, q.y, -kc0y), fmaf(kap, q.z, -kc0z), 0.f);
+      }
+      sq[u] = q; sp[u] = p;  // zero records contribute exactly 0 (p = 0)
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int u = 0; u < kTile; ++u) {
+      const float4 a = sq[u], b = sp[u];
+      const f2 axx = bc2(a.x), ayy = bc2(a.y), azz = bc2(a.z);
+      const f2 bxx = bc2(b.x), byy = bc2(b.y), bzz = bc2(b.z);
+      f2 g[TP];
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        const f2 dx = sub2(qx[k], axx), dy = sub2(qy[k], ayy), dz = sub2(qz[k], azz);
+        f2 r2 = mul2(dx, dx);
+        r2 = fma2(dy, dy, r2);
+        r2 = fma2(dz, dz, r2);
+        g[k] = nex2x2(r2);
+      }
+#pragma unroll
+      for (int k = 0; k < TP; ++k) {
+        ax[k] = fma2(g[k], bxx, ax[k]); ay[k] = fma2(g[k], byy, ay[k]); az[k] = fma2(g[k], bzz, az[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TP; ++k) {
+    float lx[2], ly[2], lz[2];
+    up2(ax[k], lx[0], lx[1]); up2(ay[k], ly[0], ly[1]); up2(az[k], lz[0], lz[1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = tb + (2 * k + h) * NT;
+      if (t < m) part[(size_t)blockIdx.y * m + t] = make_float4(lx[h], ly[h], lz[h], 0.f);
+    }
+  }
+}
+
 template <int TPT, int NT>
 __global__ void __launch_bounds__(NT) k_vel_f32(const float4* __restrict__ rec, int n,
                                                 const float4* __restrict__ ev, int m, int chunk,
@@ -1924,12 +1997,20 @@ int vel_partials(const Device& dev, int prec, const void* rec, int n, const void
                  const KernelConsts& kc, void* part, int part_cap_chunks, cudaStream_t st) {
   if (prec == kF32) {
     static const int tpts[] = {8, 4, 2, 1};
-    static int occ = occupancy(k_vel_f32<8, kNT>, kNT);
+    static int occ = occupancy(k_vel_f32x2<8, kNT>, kNT);
     Plan pl = plan(n, m, kNT, tpts, 4, kTile, occ, dev.sms);
     if (pl.S > part_cap_chunks) return -1;
-    GS_TPT_SWITCH(pl.tpt, k_vel_f32, (const float4*)rec, n, (const float4*)ev, m, pl.chunk,
-                  (float)kc.kappa, (float)(kc.kappa * kc.c0[0]), (float)(kc.kappa * kc.c0[1]),
-                  (float)(kc.kappa * kc.c0[2]), (float4*)part);
+    const float kap = (float)kc.kappa, a = (float)(kc.kappa * kc.c0[0]),
+                b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
+    const float4* r = (const float4*)rec;
+    const float4* e = (const float4*)ev;
+    float4* o = (float4*)part;
+    switch (pl.tpt) {  // packed pairs of evaluation points; TPT 1 stays scalar
+      case 8: k_vel_f32x2<8, kNT><<<pl.grid, kNT, 0, st>>>(r, n, e, m, pl.chunk, kap, a, b, c, o); break;
+      case 4: k_vel_f32x2<4, kNT><<<pl.grid, kNT, 0, st>>>(r, n, e, m, pl.chunk, kap, a, b, c, o); break;
+      case 2: k_vel_f32x2<2, kNT><<<pl.grid, kNT, 0, st>>>(r, n, e, m, pl.chunk, kap, a, b, c, o); break;
+      default: k_vel_f32<1, kNT><<<pl.grid, kNT, 0, st>>>(r, n, e, m, pl.chunk, kap, a, b, c, o); break;
+    }
     return pl.S;
   }
   static const int tpts[] = {4, 2, 1};
