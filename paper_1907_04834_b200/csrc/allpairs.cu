@@ -1720,25 +1720,28 @@ static int exact_pairs_mode() {
   return m;
 }
 
-// Tile shapes: 0 = 12 targets x 256 threads (3072-point tiles, one CTA per
-// SM; the default from 150k points), 1 = 12 x 128 (1536-point tiles, two CTAs
-// per SM: enough tile pairs for smaller problems). Measured alternatives
-// (DESIGN.md §2): 8 x 128 / 8 x 384 / 10 x 256 / 14 x 128 targets, 64- or
-// 256-source sub-tiles, source-step unroll 2 / 4, and the j side accumulated
-// after the whole i side were all equal or slower (1.65-1.79 s per RK4 step
-// at 1M against 1.657 s).
+// Tile shapes, by size (tools/check_sym.py sweeps, profiles/r02_sym/): 0 =
+// 12 targets x 256 threads (3072-point tiles, one CTA per SM) from 150k
+// points; 1 = 12 x 128 (1536, two CTAs per SM) from 75k; 2 = 6 x 128 (768,
+// three per SM) from 35k; 3 = 4 x 128 (512, four per SM) from 8k -- smaller
+// tiles give the small problems enough tile pairs to fill the GPU (20k:
+// 1.24x the gather kernel with 512-point tiles, 0.88x with 1536). Below 8k
+// the gather kernel wins. Measured alternatives at 1M: 8 x
+// 128 / 8 x 256 / 8 x 384 / 10 x 256 / 14 x 128 targets, 64- or 256-source
+// sub-tiles, step unroll 2 / 4 / 16, the j side accumulated after the whole i
+// side: all equal or slower.
 struct SymShape {
   int tpt, nt;
 };
-static const SymShape kSym[] = {{12, 256}, {12, 128}};
+static const SymShape kSym[] = {{12, 256}, {12, 128}, {6, 128}, {4, 128}};
 
 static int sym_variant(int n) {
   static int forced = [] {
     const char* e = std::getenv("GS_SYM_VARIANT");
     return e ? std::atoi(e) : -1;
   }();
-  if (forced == 0 || forced == 1) return forced;
-  return n >= 150000 ? 0 : 1;
+  if (forced >= 0 && forced <= 3) return forced;
+  return n >= 150000 ? 0 : n >= 75000 ? 1 : n >= 35000 ? 2 : 3;
 }
 
 int sym_tiles(int n) {
@@ -1753,8 +1756,8 @@ bool use_sym(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
   // (problems whose T slots x n x 32 B exceed kSymSlotBudget run in
   // diagonal groups folded into a running sum: rhs_sym_partials)
   if (mode == 2) return true;
-  // by size: enough tile pairs for many waves (T(T+1)/2 CTAs)
-  return n >= 40000;
+  // by size: enough tile pairs to fill the GPU (T(T+1)/2 CTAs)
+  return n >= 8000;
 }
 
 // One slot per tile up to kSymSlotBudget bytes of partials (1M points: 10.4
@@ -1780,6 +1783,17 @@ size_t sym_part_bytes(int n) {
 
 int sym_launches(int n) {
   return sym_grouped(n) ? 2 * ((sym_tiles(n) / 2 + 1 + kSymGroup - 1) / kSymGroup) : 1;
+}
+
+// k_rhs_sym_f32x2 in tile shape v (kSym) over grid (rows, diagonals)
+static void launch_sym(int v, dim3 grid, cudaStream_t st, const float4* r, int n, int T,
+                       float kap, float a, float b, float c, float4* o, int row0, int k0) {
+  switch (v) {
+    case 0: k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o, row0, k0); break;
+    case 1: k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o, row0, k0); break;
+    case 2: k_rhs_sym_f32x2<6, 128, 3, 128, 8><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o, row0, k0); break;
+    default: k_rhs_sym_f32x2<4, 128, 4, 128, 8><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o, row0, k0); break;
+  }
 }
 
 // Multi-GPU symmetric RHS: rank r of G evaluates the tile-pair
@@ -1823,13 +1837,7 @@ int rhs_sym_rows(const void* rec, int n, const KernelConsts& kc, void* part, voi
               b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
   const float4* r = (const float4*)rec;
   float4* o = (float4*)part;
-  if (rb > ra) {
-    const dim3 grid((unsigned)(rb - ra), (unsigned)(T / 2 + 1), 1);
-    if (v == 0)
-      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o, ra);
-    else
-      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o, ra);
-  }
+  if (rb > ra) launch_sym(v, dim3((unsigned)(rb - ra), (unsigned)(T / 2 + 1), 1), st, r, n, T, kap, a, b, c, o, ra, -1);
   k_fold_rows<<<(n + 255) / 256, 256, 0, st>>>(o, n, T, tile, ra, rb, (float4*)out);
   return T;
 }
@@ -1839,14 +1847,10 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
   const float kap = (float)kc.kappa, a = (float)(kc.kappa * kc.c0[0]),
               b = (float)(kc.kappa * kc.c0[1]), c = (float)(kc.kappa * kc.c0[2]);
   const float4* r = (const float4*)rec;
-  const bool big = sym_variant(n) == 0;
+  const int v = sym_variant(n);
   if (!sym_grouped(n)) {
-    const dim3 grid((unsigned)T, (unsigned)(T / 2 + 1), 1);
-    float4* o = (float4*)part;
-    if (big)
-      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, o);
-    else
-      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, o);
+    launch_sym(v, dim3((unsigned)T, (unsigned)(T / 2 + 1), 1), st, r, n, T, kap, a, b, c,
+               (float4*)part, 0, -1);
     return T;
   }
   float4* acc = (float4*)part;
@@ -1854,11 +1858,7 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
   const int kend = T / 2 + 1;
   for (int k0 = 0; k0 < kend; k0 += kSymGroup) {
     const int k1 = std::min(kend, k0 + kSymGroup);
-    const dim3 grid((unsigned)T, (unsigned)(k1 - k0), 1);
-    if (big)
-      k_rhs_sym_f32x2<12, 256, 1, 128, 8><<<grid, 256, 0, st>>>(r, n, T, kap, a, b, c, slots, 0, k0);
-    else
-      k_rhs_sym_f32x2<12, 128, 2, 256, 4><<<grid, 128, 0, st>>>(r, n, T, kap, a, b, c, slots, 0, k0);
+    launch_sym(v, dim3((unsigned)T, (unsigned)(k1 - k0), 1), st, r, n, T, kap, a, b, c, slots, 0, k0);
     k_fold_group_f32<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);
   }
   return 1;  // the epilogue reads the running sum as a single partial

@@ -286,9 +286,9 @@ def pairs(gs):
     gs.set_exact_pairs(-1)
 
 
-# 1536-point tiles below 150k points: one tile (diagonal only), 4 tiles (even
-# T: the k = T/2 pairs taken once), 5 tiles (odd T), ragged last tiles
-@pytest.mark.parametrize("n", [1, 2, 700, 1537, 1536 * 3 + 17, 1536 * 4 + 5])
+# 512-point tiles below 35k points: one tile (diagonal only), 2 and 4 tiles
+# (even T: the k = T/2 pairs taken once), 5 tiles (odd T), ragged last tiles
+@pytest.mark.parametrize("n", [1, 2, 300, 513, 512 * 3 + 17, 512 * 4 + 5])
 def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
     """Every unordered pair evaluated once and fed to both ends, as the
     reference's i < j sweep (kernel_exact.cpp:29-61): FP32 RHS to 1e-5 of the
@@ -308,10 +308,23 @@ def test_symmetric_rhs_matches_reference(gs, ref, pairs, n):
     assert rel_l2(dp, gp) < 2e-6 and rel_l2(dq, gq) < 2e-6
 
 
+@pytest.mark.parametrize("n", [9_000, 40_000, 80_000])
+def test_symmetric_tile_shapes_match_gather(gs, pairs, n):
+    """The by-size tile shapes (512-point tiles from 8k, 768 from 35k, 1536 from
+    75k points) against the gather kernel, to FP32 rounding."""
+    rng = np.random.default_rng(n)
+    q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
+    assert gs.exact_pairs_plan(n, F32) > 0
+    _, dp, dq = gs.hamiltonian_with_gradients(q, p, 0.03, precision=F32)
+    pairs(1)
+    _, gp, gq = gs.hamiltonian_with_gradients(q, p, 0.03, precision=F32)
+    assert rel_l2(dp, gp) < 2e-6 and rel_l2(dq, gq) < 2e-6
+
+
 def test_symmetric_flow_matches_reference(gs, port, pairs):
     """RK4 flow through the symmetric kernel against the port's RK4 over the
     reference RHS (FP32 trajectory tolerance)."""
-    n, sigma = 1536 * 2 + 100, 0.05
+    n, sigma = 512 * 2 + 100, 0.05
     q, p = f32(uniform(n, 1.0, 541)), f32(sym_uniform(n, 1e-3, 542))
     pairs(2)
     cfg = ShootingConfig(sigma=sigma, timesteps=4, backend=EXACT, integrator=RK4, precision=F32)

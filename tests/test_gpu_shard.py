@@ -145,7 +145,7 @@ def test_pair_rows_shards_match_one_flow(gs):
 
 def test_pair_rows_not_for_gather_problems(gs):
     cfg = ShootingConfig(sigma=0.03, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
-    f = gs.flow(cfg, 20_000)  # below 40k points: the gather kernel
+    f = gs.flow(cfg, 5_000)  # below 8k points: the gather kernel
     assert not f.set_pair_rows(0, 2)
     fb = gs.flow(ShootingConfig(sigma=0.03, timesteps=10, backend=BARNES_HUT, precision=F32), 60_000)
     assert not fb.set_pair_rows(0, 2)
