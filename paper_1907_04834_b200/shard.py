@@ -8,7 +8,7 @@ gloo in the CPU tests). The all-gather is in place: every rank's record buffer
 is the gather output and its own shard is the input slice. An exact shard
 launches under the full problem's plan (gs_flow_set_shard), so its per-target
 sums -- and the flow -- are bit-identical to one GPU's gather-kernel run
-(below 40k points the one-GPU default; above it one GPU takes the symmetric
+(below 8k points the one-GPU default; above it one GPU takes the symmetric
 kernel, equal to FP32 rounding -- DESIGN.md §2, §7); Barnes-Hut shards have
 the reference's interaction sets, equal to summation-order rounding.
 
