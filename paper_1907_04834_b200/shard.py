@@ -116,7 +116,7 @@ class ShardedFlow:
     the flow launches on; the all-gather is ordered after it.
     """
 
-    def __init__(self, flow, stages: int, group=None, stream=None):
+    def __init__(self, flow, stages: int, group=None, stream=None, pairs=None):
         self.flow = flow
         self.stages = stages
         self.group = group
@@ -140,7 +140,10 @@ class ShardedFlow:
         # those partials (all-to-all) before each shard's epilogue -- one
         # extra collective per stage, half the pair arithmetic of the gather
         # form
-        self.pairs = (self.world > 1 and hasattr(flow, "set_pair_rows")
+        # (pairs=True also takes the path with one rank: tests of the NCCL
+        # exchange on a single GPU)
+        want = (self.world > 1) if pairs is None else bool(pairs)
+        self.pairs = (want and hasattr(flow, "set_pair_rows")
                       and flow.set_pair_rows(self.rank, self.world))
         if self.pairs:
             dev = self._rec.device

@@ -149,3 +149,51 @@ def test_pair_rows_not_for_gather_problems(gs):
     assert not f.set_pair_rows(0, 2)
     fb = gs.flow(ShootingConfig(sigma=0.03, timesteps=10, backend=BARNES_HUT, precision=F32), 60_000)
     assert not fb.set_pair_rows(0, 2)
+
+
+def _nccl_single_rank(out):
+    import os
+    import torch.distributed as dist
+    from paper_1907_04834_b200 import Geoshoot
+    from paper_1907_04834_b200.shard import ShardedFlow
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(29900 + os.getpid() % 90)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    gs = Geoshoot(0)
+    n = 40_000
+    rng = np.random.default_rng(79)
+    q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-4, (n, 3))
+    cfg = ShootingConfig(sigma=0.03, timesteps=10, backend=EXACT, integrator=RK4, precision=F32)
+    f = gs.flow(cfg, n)
+    drv = ShardedFlow(f, 4, pairs=True)
+    assert drv.pairs
+    f.upload(q, p)
+    drv.step(2)
+    f.sync()
+    gq, gp = f.download()
+    one = gs.flow(cfg, n)
+    one.upload(q, p)
+    one.advance(2)
+    one.sync()
+    wq, wp = one.download()
+    np.savez(out, gq=gq, gp=gp, wq=wq, wp=wp, coll=drv.collectives)
+    dist.destroy_process_group()
+
+
+def test_pair_rows_through_nccl_single_rank(tmp_path):
+    """The torchrun path's pair-row stages through a real NCCL process group
+    (one rank on one GPU: the all-to-all is a copy): the ShardedFlow stage
+    sequence -- gs_flow_stage_pairs on the flow's stream, all_to_all_single on
+    that stream, gs_flow_stage_apply, the record all-gather -- bitwise equal to
+    the one-GPU symmetric flow (a one-rank fold takes every slot in order)."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "nccl1.npz")
+    ctx = mp.get_context("spawn")
+    proc = ctx.Process(target=_nccl_single_rank, args=(out,))
+    proc.start()
+    proc.join(600)
+    assert proc.exitcode == 0
+    d = np.load(out)
+    assert int(d["coll"]) == 8  # 2 steps x 4 stages x all-to-all (no all-gather with one rank)
+    assert np.array_equal(d["gq"], d["wq"]) and np.array_equal(d["gp"], d["wp"])
