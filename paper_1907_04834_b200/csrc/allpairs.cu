@@ -1898,16 +1898,33 @@ int rhs_sym_f64_partials(const void* rec, int n, const KernelConsts& kc, void* p
 
 int sym_f64_launches(int n) { return 2 * ((sym_f64_tiles(n) / 2 + 1 + kSymF64Group - 1) / kSymF64Group); }
 
+#ifndef HESS_SYM_MIN_N
+#define HESS_SYM_MIN_N 8000
+#endif
 // Symmetric Hessian products (k_hess_sym_f32x2): 768-point tiles (6 targets
 // x 128 threads, two CTAs per SM), the same choice rules as the RHS.
-constexpr int kHessSymTile = 6 * 128;
-static int hess_sym_tiles(int n) { return (n + kHessSymTile - 1) / kHessSymTile; }
+// (512-point tiles -- 4 targets x 128 threads, three CTAs per SM -- below 40k
+// points, so that small problems still fill the GPU with tile pairs)
+constexpr int kHessSymTile = 6 * 128, kHessSymTileSmall = 4 * 128;
+static int hess_sym_forced() {
+  static const int v = [] {  // GS_HESS_SYM_TILE: 768 / 512 (sweeps)
+    const char* e = std::getenv("GS_HESS_SYM_TILE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+static int hess_sym_tile(int n) {
+  const int f = hess_sym_forced();
+  if (f == kHessSymTile || f == kHessSymTileSmall) return f;
+  return n >= 40000 ? kHessSymTile : kHessSymTileSmall;
+}
+static int hess_sym_tiles(int n) { return (n + hess_sym_tile(n) - 1) / hess_sym_tile(n); }
 
 static bool use_sym_hess(int prec, int n, int tgt_begin, int n_tgt, int plan_tgt) {
   if (prec != kF32 || tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
   const int mode = exact_pairs_mode();
   if (mode == 1) return false;
-  return mode == 2 || n >= 40000;
+  return mode == 2 || n >= HESS_SYM_MIN_N;
 }
 
 // slots over the budget: diagonal groups folded into a running sum (as the RHS)
@@ -1932,8 +1949,13 @@ int hess_partials(const Device& dev, int prec, const void* rec, const void* adj,
     const float a = (float)(kc.kappa * kc.c0[0]), b = (float)(kc.kappa * kc.c0[1]),
                 c = (float)(kc.kappa * kc.c0[2]);
     if (!hess_sym_grouped(n)) {
-      k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(T / 2 + 1)), 128, 0, st>>>(
-          (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, (float4*)part);
+      const dim3 grid((unsigned)T, (unsigned)(T / 2 + 1));
+      if (hess_sym_tile(n) == kHessSymTileSmall)
+        k_hess_sym_f32x2<4, 128, 3, 64><<<grid, 128, 0, st>>>(
+            (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, (float4*)part);
+      else
+        k_hess_sym_f32x2<6, 128, 2, 64><<<grid, 128, 0, st>>>(
+            (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, (float4*)part);
       return T;
     }
     float4* acc = (float4*)part;
@@ -1941,8 +1963,12 @@ int hess_partials(const Device& dev, int prec, const void* rec, const void* adj,
     const int kend = T / 2 + 1;
     for (int k0 = 0; k0 < kend; k0 += kHessSymGroup) {
       const int k1 = std::min(kend, k0 + kHessSymGroup);
-      k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 128, 0, st>>>(
-          (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, slots, k0);
+      if (hess_sym_tile(n) == kHessSymTileSmall)
+        k_hess_sym_f32x2<4, 128, 3, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 128, 0, st>>>(
+            (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, slots, k0);
+      else
+        k_hess_sym_f32x2<6, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 128, 0, st>>>(
+            (const float4*)rec, (const float4*)adj, n, T, kap, a, b, c, c1, slots, k0);
       k_fold_group4_f32<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);
     }
     return 1;

@@ -339,8 +339,9 @@ def test_exact_pairs_choice_is_validated(gs):
         gs.set_exact_pairs(3)
 
 
-# 768-point tiles: one tile, 4 tiles (even T), 5 tiles (odd T), ragged
-@pytest.mark.parametrize("n", [1, 300, 769, 768 * 3 + 11, 768 * 4 + 3])
+# 512-point tiles below 40k points: one tile, 2 and 4 tiles (even T), 5 tiles
+# (odd T), ragged
+@pytest.mark.parametrize("n", [1, 300, 513, 512 * 3 + 11, 512 * 4 + 3])
 def test_symmetric_hessian_products_match_reference(gs, ref, pairs, n):
     """k_hess_sym_f32x2: each unordered pair once, the j terms by symmetry
     (d -> -d, db -> -db), against the reference's hessian_products
