@@ -160,8 +160,7 @@ int gs_abi_version(void);
  * environment's choice. Every choice gives the reference's interaction sets. */
 gs_status gs_set_bh_walk(int32_t kernel, int32_t windows);
 /* Exact FP32 all-pairs formulation, process-wide (GS_EXACT_PAIRS sets the
- * default): 0 = by size (symmetric FP32 RHS and Hessian products from 8k
- * points, FP64 from 40k; unsharded), 1 = gather
+ * default): 0 = by size (the symmetric kernels from 8k points; unsharded), 1 = gather
  * (each ordered pair per target, k_rhs_f32x2), 2 = symmetric whenever it
  * applies (each unordered pair once, fed to both ends, as the reference's
  * i < j sweep, kernel_exact.cpp:29-61); -1 restores the environment's choice. */

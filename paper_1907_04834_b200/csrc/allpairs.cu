@@ -1864,16 +1864,32 @@ int rhs_sym_partials(const void* rec, int n, const KernelConsts& kc, void* part,
   return 1;  // the epilogue reads the running sum as a single partial
 }
 
+#ifndef SYM_F64_BIG_N
+#define SYM_F64_BIG_N 100000
+#endif
+#ifndef SYM_F64_MIN_N
+#define SYM_F64_MIN_N 8000
+#endif
 // Symmetric FP64 RHS (k_rhs_sym_f64): 1024-point tiles (4 targets x 256
 // threads), diagonal groups of kSymF64Group folded into a running sum.
-constexpr int kSymF64Tile = 4 * 256, kSymF64Group = 32;
-int sym_f64_tiles(int n) { return (n + kSymF64Tile - 1) / kSymF64Tile; }
+// (512-point tiles -- 4 targets x 128 threads, two CTAs per SM -- below
+// 100k points: enough tile pairs for the small problems)
+constexpr int kSymF64Tile = 4 * 256, kSymF64TileSmall = 4 * 128, kSymF64Group = 32;
+static int sym_f64_tile(int n) {
+  static const int forced = [] {  // GS_SYM_F64_TILE: 1024 / 512 (sweeps)
+    const char* e = std::getenv("GS_SYM_F64_TILE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == kSymF64Tile || forced == kSymF64TileSmall) return forced;
+  return n >= SYM_F64_BIG_N ? kSymF64Tile : kSymF64TileSmall;
+}
+int sym_f64_tiles(int n) { return (n + sym_f64_tile(n) - 1) / sym_f64_tile(n); }
 
 bool use_sym_f64(int n, int tgt_begin, int n_tgt, int plan_tgt) {
   if (tgt_begin != 0 || n_tgt != n || plan_tgt > 0) return false;
   const int mode = exact_pairs_mode();
   if (mode == 1) return false;
-  return mode == 2 || n >= 40000;
+  return mode == 2 || n >= SYM_F64_MIN_N;
 }
 
 size_t sym_f64_part_bytes(int n) {
@@ -1889,6 +1905,10 @@ int rhs_sym_f64_partials(const void* rec, int n, const KernelConsts& kc, void* p
   const int kend = T / 2 + 1;
   for (int k0 = 0; k0 < kend; k0 += kSymF64Group) {
     const int k1 = std::min(kend, k0 + kSymF64Group);
+    if (sym_f64_tile(n) == kSymF64TileSmall)
+      k_rhs_sym_f64<4, 128, 2, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 128, 0, st>>>(
+          (const double4*)rec, n, T, k0, kc.inv_two_s, slots);
+    else
     k_rhs_sym_f64<4, 256, 1, 64><<<dim3((unsigned)T, (unsigned)(k1 - k0)), 256, 0, st>>>(
         (const double4*)rec, n, T, k0, kc.inv_two_s, slots);
     k_fold_group<<<(n + 255) / 256, 256, 0, st>>>(slots, 2 * (k1 - k0), n, k0 == 0, acc);

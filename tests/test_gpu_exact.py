@@ -372,8 +372,9 @@ def test_symmetric_evaluate_matches_reference(gs, ref, pairs):
     assert rel_l2(ev.gradient, g) <= 1e-3
 
 
-# FP64: 1024-point tiles, diagonals in groups of 32 folded into a running sum
-@pytest.mark.parametrize("n", [1, 300, 1025, 1024 * 3 + 17, 1024 * 4 + 5])
+# FP64: 512-point tiles below 100k points (1024 above), diagonals in groups of
+# 32 folded into a running sum; T = 1, 1, 2, 4 (even), 5 (odd)
+@pytest.mark.parametrize("n", [1, 300, 513, 512 * 3 + 17, 512 * 4 + 5])
 def test_symmetric_rhs_f64_matches_reference(gs, ref, pairs, n):
     q, p = uniform(n, 10.0, seed=n + 7), sym_uniform(n, 1.0, seed=n + 8)
     pairs(2)
@@ -387,12 +388,12 @@ def test_symmetric_rhs_f64_matches_reference(gs, ref, pairs, n):
 
 
 def test_symmetric_rhs_f64_groups_equal_gather(gs, pairs):
-    """70k points: T = 69 tiles, 35 diagonals in two groups (32 + 3): the
+    """70k points: T = 137 tiles of 512, 69 diagonals in three groups (32 + 32 + 5): the
     symmetric FP64 sum against the gather kernel's to FP64 rounding."""
     n = 70_000
     rng = np.random.default_rng(70)
     q, p = rng.uniform(0, 1, (n, 3)), rng.normal(0, 1e-2, (n, 3))
-    assert gs.exact_pairs_plan(n, F64) == 69
+    assert gs.exact_pairs_plan(n, F64) == 137
     _, dp, dq = gs.hamiltonian_with_gradients(q, p, 0.03)
     pairs(1)
     assert gs.exact_pairs_plan(n, F64) == 0
